@@ -1,0 +1,228 @@
+"""Generate golden fixtures under tests/golden/ by running the UNMODIFIED reference.
+
+TEST INFRASTRUCTURE ONLY.  Run in the build container (where /root/reference
+exists):  python -m oracle.make_golden
+Each .npz holds the seeded inputs and the reference's outputs; the CPU tests
+pin `oracle/stage1.py` against them and the GPU tests pin the CUDA path against
+them.  The reference runs with BLAS pinned to one thread.
+"""
+
+from __future__ import annotations
+
+import os
+
+import numpy as np
+from threadpoolctl import threadpool_limits
+
+from oracle import refbridge as rb
+from paper_2403_01444_b200 import scenes
+
+OUT = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests", "golden")
+
+
+def _grid_arr(grid):
+    return dict(grid_levels=grid["levels"], grid_features=grid["features"],
+                grid_log2_table=grid["log2_table"], grid_base=grid["base"],
+                grid_growth=grid["growth"], grid_lo=np.array(grid["lo"]),
+                grid_hi=np.array(grid["hi"]))
+
+
+def _cam_arr(cam, p="cam_"):
+    return {p + "w2c": cam["w2c"], p + "intr": np.array([cam["fx"], cam["fy"], cam["cx"], cam["cy"]]),
+            p + "size": np.array([cam["width"], cam["height"]]), p + "near": cam["near"]}
+
+
+def _cloud_arr(cloud, p="cloud_"):
+    return {p + k: v for k, v in cloud.items()}
+
+
+def _flat_tiles(tiles):
+    """[(y0,y1,x0,x1,members)] -> (rects (T,4) int64, counts (T,), members (D,))."""
+    rects = np.array([[t[0], t[1], t[2], t[3]] for t in tiles], dtype=np.int64).reshape(-1, 4)
+    counts = np.array([len(t[4]) for t in tiles], dtype=np.int64)
+    mem = np.concatenate([t[4] for t in tiles]).astype(np.int64) if tiles else np.zeros(0, np.int64)
+    return rects, counts, mem
+
+
+def gen_encode(R):
+    rng = np.random.default_rng(101)
+    out = {}
+    for tag, grid in (
+        ("small", dict(levels=4, features=2, log2_table=10, base=4, growth=1.5,
+                       lo=(-1.1, -0.9, -1.3), hi=(1.2, 1.0, 0.8))),
+        ("cfg1", dict(levels=16, features=2, log2_table=15, base=16,
+                      growth=scenes.growth_for(16, 2048, 16),
+                      lo=(-3.7, -3.2, -3.9), hi=(3.5, 3.6, 3.1))),
+    ):
+        lo, hi = np.array(grid["lo"]), np.array(grid["hi"])
+        x = scenes.f32(rng.uniform(lo, hi, size=(1500, 3)))
+        x[:5] = lo  # corners / faces of the box
+        x[5:10] = hi
+        cache = rb.ref_cache(R, grid, *_rand_ntc(grid, 64, seed=3))
+        feats, ctx = cache.encode(x)
+        res = np.array([cache.grid.resolution(l) for l in range(grid["levels"])])
+        extra = dict(feats=feats, tables=cache.tables) if tag == "small" else {}
+        np.savez_compressed(os.path.join(OUT, f"encode_{tag}.npz"), x=x,
+                            idx=ctx.corner_idx.astype(np.int32), w=ctx.corner_w, res=res,
+                            **extra, **_grid_arr(grid))
+        out[tag] = len(x)
+    return out
+
+
+def _rand_ntc(grid, hidden, seed):
+    from oracle import stage1 as O
+
+    tables, mlp = O.init_ntc(grid, hidden_dim=hidden, output_init="random", seed=seed)
+    return tables, mlp
+
+
+def gen_ntc(R):
+    rng = np.random.default_rng(202)
+    grid = dict(levels=4, features=2, log2_table=10, base=4, growth=1.5,
+                lo=(-1.0, -1.0, -1.0), hi=(1.0, 1.0, 1.0))
+    tables, mlp = _rand_ntc(grid, 64, seed=5)
+    # non-trivial tables so hidden units leave the ReLU floor
+    tables = scenes.f32(rng.uniform(-0.5, 0.5, size=tables.shape))
+    cache = rb.ref_cache(R, grid, tables, mlp)
+    x = scenes.f32(rng.uniform(-1, 1, size=(500, 3)))
+    d_mu, d_q, ctx = cache.forward(x)
+    g_mu = rng.normal(size=d_mu.shape)
+    g_q = rng.normal(size=d_q.shape)
+    grads, touched = cache.backward(ctx, g_mu, g_q)
+    arrs = dict(x=x, tables=tables, d_mu=d_mu, d_q=d_q, g_mu=g_mu, g_q=g_q,
+                **{f"mlp_w{i}": w for i, w in enumerate(mlp["weights"])},
+                **{f"mlp_b{i}": b for i, b in enumerate(mlp["biases"])},
+                **{f"grad_{k}": v for k, v in grads.items()},
+                **{f"touched_{k}": v for k, v in touched.items()}, **_grid_arr(grid))
+    # two lazy Adam steps on those grads
+    cache.adam_step(grads, 0.002, touched)
+    cache.adam_step(grads, 0.002, touched)
+    arrs.update({f"after2_{k}": v for k, v in cache.get_params().items()})
+    np.savez_compressed(os.path.join(OUT, "ntc.npz"), **arrs)
+
+
+def gen_transform(R):
+    rng = np.random.default_rng(303)
+    sc = scenes.small_scene(seed=7, n=300, sh_degree=1)
+    cloud = sc.cloud
+    grid = dict(sc.grid)
+    # leave a few means outside the box (pass-through rows)
+    cloud["means"][:4] += np.array([10.0, 0.0, 0.0])
+    tables, mlp = _rand_ntc(grid, 64, seed=9)
+    tables = scenes.f32(rng.uniform(-0.3, 0.3, size=tables.shape))
+    cache = rb.ref_cache(R, grid, tables, mlp)
+    rc = rb.ref_cloud(R, cloud)
+    out, tctx = R["transform"].apply_ntc(rc, cache)
+    gm = rng.normal(size=(len(cloud["means"]), 3))
+    gr = rng.normal(size=(len(cloud["means"]), 4))
+    gs = rng.normal(size=(len(cloud["means"]), 4, 3))
+    grads, _ = R["transform"].apply_ntc_backward(tctx, gm, gr, gs)
+    np.savez_compressed(os.path.join(OUT, "transform.npz"), tables=tables,
+                        **{f"mlp_w{i}": w for i, w in enumerate(mlp["weights"])},
+                        **{f"mlp_b{i}": b for i, b in enumerate(mlp["biases"])},
+                        **_grid_arr(grid), **_cloud_arr(cloud), inside=tctx.inside,
+                        out_means=out.means, out_rotations=out.rotations, out_sh=out.sh,
+                        g_means=gm, g_rot=gr, g_sh=gs,
+                        **{f"grad_{k}": v for k, v in grads.items()})
+
+
+def gen_raster(R):
+    rng = np.random.default_rng(404)
+    for tag, sh_deg, bg, settings in (
+        ("default", 1, np.array([0.1, 0.3, 0.2]), dict(tile_size=16, alpha_clamp=0.99,
+                                                       skip_alpha=1 / 255.0,
+                                                       stop_transmittance=1e-4)),
+        ("smooth", 1, np.array([0.3, 0.2, 0.4]), dict(tile_size=16, alpha_clamp=0.99,
+                                                      skip_alpha=0.0,
+                                                      stop_transmittance=0.0)),
+    ):
+        sc = scenes.small_scene(seed=11, n=600, width=70, height=52, sh_degree=sh_deg)
+        cloud = sc.cloud
+        cloud["opacity_logits"][:20] = 6.0  # some clamped splats
+        cam = sc.cameras[0]
+        rc = rb.ref_cloud(R, cloud)
+        out, ctx = R["rasterizer"].rasterize_forward(rc, rb.ref_camera(R, cam), bg,
+                                                      rb.ref_settings(R, settings))
+        d_img = rng.normal(size=out.image.shape)
+        g = R["rasterizer"].rasterize_backward(ctx, d_img)
+        rects, counts, mem = _flat_tiles(ctx.tiles)
+        np.savez_compressed(os.path.join(OUT, f"raster_{tag}.npz"), **_cloud_arr(cloud),
+                            **_cam_arr(cam), bg=bg,
+                            settings=np.array([settings["tile_size"], settings["alpha_clamp"],
+                                               settings["skip_alpha"],
+                                               settings["stop_transmittance"]]),
+                            image=out.image, alpha=out.alpha_map,
+                            touch=out.per_gaussian_touch_count, indices=ctx.indices,
+                            tile_rects=rects, tile_counts=counts, tile_members=mem,
+                            d_image=d_img, d_means=g.d_means, d_rotations=g.d_rotations,
+                            d_log_scales=g.d_log_scales, d_opacity_logits=g.d_opacity_logits,
+                            d_sh=g.d_sh, viewspace=g.viewspace_grad_norm,
+                            contributed=g.contributed)
+
+
+def gen_loss(R):
+    rng = np.random.default_rng(505)
+    x = rng.uniform(0.1, 0.9, size=(40, 37, 3))
+    y = np.clip(x + rng.normal(scale=0.1, size=x.shape), 0, 1)
+    loss, grad = R["losses"].render_loss(x, y)
+    np.savez_compressed(os.path.join(OUT, "loss.npz"), x=x, y=y, loss=loss, grad=grad)
+
+
+def gen_stage1(R):
+    """Two Stage-1 iterations driven through the reference functions in
+    process_frame order (pipeline.py:262-277)."""
+    from oracle import stage1 as O
+
+    sc = scenes.small_scene(seed=21, n=1500, width=64, height=48, sh_degree=1, n_views=2)
+    cloud, grid = sc.cloud, sc.grid
+    tables, mlp = O.init_ntc(grid, hidden_dim=64, output_init="random", seed=4)
+    rng = np.random.default_rng(606)
+    tables = scenes.f32(rng.uniform(-0.05, 0.05, size=tables.shape))
+    cache = rb.ref_cache(R, grid, tables, mlp)
+    targets = []
+    for cam in sc.cameras:
+        moved = scenes.moved_cloud(cloud, np.random.default_rng(99), deg=3.0)
+        img, _ = R["rasterizer"].rasterize_forward(rb.ref_cloud(R, moved), rb.ref_camera(R, cam))
+        targets.append(img.image)
+    rc = rb.ref_cloud(R, cloud)
+    enc = None
+    losses, grads_first = [], None
+    order = [0, 1]
+    for t, v in enumerate(order):
+        tr, tctx = R["transform"].apply_ntc(rc, cache, encode_ctx=enc)
+        enc = tctx.fwd.encode if enc is None else enc
+        out, rctx = R["rasterizer"].rasterize_forward(tr, rb.ref_camera(R, sc.cameras[v]))
+        loss, d_img = R["losses"].render_loss(out.image, targets[v])
+        losses.append(loss)
+        g = R["rasterizer"].rasterize_backward(rctx, d_img)
+        cg, touched = R["transform"].apply_ntc_backward(tctx, g.d_means, g.d_rotations, g.d_sh)
+        if grads_first is None:
+            grads_first = dict(cg)
+            img_first = out.image
+        cache.adam_step(cg, 0.002, touched)
+    np.savez_compressed(os.path.join(OUT, "stage1.npz"), **_cloud_arr(cloud), **_grid_arr(grid),
+                        tables=tables, **{f"mlp_w{i}": w for i, w in enumerate(mlp["weights"])},
+                        **{f"mlp_b{i}": b for i, b in enumerate(mlp["biases"])},
+                        **_cam_arr(sc.cameras[0], "cam0_"), **_cam_arr(sc.cameras[1], "cam1_"),
+                        target0=targets[0], target1=targets[1], losses=np.array(losses),
+                        image_first=img_first,
+                        **{f"grad1_{k}": v for k, v in grads_first.items()},
+                        **{f"after2_{k}": v for k, v in cache.get_params().items()})
+
+
+def main():
+    os.makedirs(OUT, exist_ok=True)
+    R = rb.load()
+    with threadpool_limits(1):
+        gen_encode(R)
+        gen_ntc(R)
+        gen_transform(R)
+        gen_raster(R)
+        gen_loss(R)
+        gen_stage1(R)
+    for f in sorted(os.listdir(OUT)):
+        print(f, os.path.getsize(os.path.join(OUT, f)))
+
+
+if __name__ == "__main__":
+    main()
