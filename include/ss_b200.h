@@ -1,0 +1,281 @@
+/*
+ * ss_b200.h -- C ABI of the B200-native 3DGStream Stage-1 hot path.
+ *
+ * Every entry point replaces one function of the reference package
+ * `splatstream` (paths relative to /root/reference/pkg/src/splatstream/);
+ * the citation is on each declaration.  Conventions:
+ *   - plain pointers and sizes only; all device memory is CALLER-OWNED
+ *     (the library allocates nothing persistent).  Data-dependent scratch is
+ *     sized with the *_bytes queries first (CUB style).
+ *   - every function is stream-ordered on the `stream` argument (a
+ *     cudaStream_t passed as void*), never synchronises the device, and
+ *     returns an ss_status.  Device-detected numerical failures (zero-norm
+ *     quaternion, non-finite loss) are OR-ed into a caller-provided device
+ *     status word and mapped to NumericalError by the host.
+ *   - float32 storage; float64 wherever bit-exactness with the float64
+ *     reference needs it (hash positions, depth keys, tile rectangles).
+ */
+#ifndef SS_B200_H
+#define SS_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SS_MAX_LEVELS 32
+#define SS_MAX_SH 16
+
+/* status codes (errors.py:8-21; CLI exit-code mapping cli.py:40-43) */
+typedef enum {
+  SS_OK = 0,
+  SS_ERR_DATA = 1,      /* DataError: bad shape/argument, point outside the AABB */
+  SS_ERR_NUMERICAL = 2, /* NumericalError: zero-norm quaternion, non-finite loss */
+  SS_ERR_CUDA = 3,      /* CUDA launch / runtime failure */
+  SS_ERR_CAPACITY = 4   /* caller workspace too small: query *_bytes and retry */
+} ss_status;
+
+/* device status-word bits */
+#define SS_FLAG_ZERO_QUAT 1u   /* |d_q| < 1e-12 (gaussians.py:46-47) */
+#define SS_FLAG_NONFINITE 2u   /* check_finite("stage1 loss") (errors.py:24-29) */
+#define SS_FLAG_OUTSIDE 4u     /* encode(): point outside the AABB (ntc.py:166-168) */
+#define SS_FLAG_OVERFLOW 8u    /* tile-pair count exceeded the capacity */
+
+/* HashGridConfig (ntc.py:30-61).  resolution[] = floor(base*growth^l) is
+ * computed on the host in float64 with the reference formula (ntc.py:54-55). */
+typedef struct ss_grid {
+  int32_t n_levels, n_features, log2_table, reserved;
+  int32_t resolution[SS_MAX_LEVELS];
+  double aabb_min[3], aabb_max[3];
+} ss_grid;
+
+/* NeuralTransformationCache decoder (ntc.py:102-128): in -> hidden^n_hidden -> 7,
+ * ReLU hidden layers.  Supported: in_dim <= 64, hidden_dim <= 64, n_hidden 1|2,
+ * out_dim 7. */
+typedef struct ss_mlp {
+  int32_t in_dim, hidden_dim, n_hidden, out_dim;
+} ss_mlp;
+
+/* Device parameter layout: one packed fp32 vector W0 | b0 | [W1 | b1] | W2 | b2,
+ * weights (fan_in, fan_out) row-major as in the reference (ntc.py:111), zero-
+ * padded to in_pad (16|32|64) x 64 hidden x 8 outputs.  Zero padding is exact:
+ * padded units stay 0 and receive exactly zero gradient, so Adam keeps them 0. */
+typedef struct ss_mlp_layout {
+  int32_t in_pad, hidden_pad, out_pad, n_hidden;
+  int64_t w0, b0, w1, b1, w2, b2, total;
+} ss_mlp_layout;
+int ss_mlp_get_layout(const ss_mlp* mlp, ss_mlp_layout* out);
+
+/* Camera (cameras.py:30-80): world_to_camera row-major 4x4. */
+typedef struct ss_camera {
+  double w2c[16];
+  double fx, fy, cx, cy, near_clip;
+  int32_t width, height;
+} ss_camera;
+
+/* RasterSettings (rasterizer.py:33-38) + the background colour argument. */
+typedef struct ss_raster_settings {
+  int32_t tile_size, reserved;
+  double alpha_clamp, skip_alpha, stop_transmittance;
+  double background[3];
+} ss_raster_settings;
+
+/* GaussianCloud, SoA fp32 (gaussians.py:179-216); sh is (n, sh_coeffs, 3). */
+typedef struct ss_cloud {
+  int64_t n;
+  int32_t sh_coeffs, reserved;
+  const float* means;
+  const float* rotations;
+  const float* log_scales;
+  const float* opacity_logits;
+  const float* sh;
+} ss_cloud;
+
+/* GradientBuffer (rasterizer.py:48-68).  Any pointer may be NULL to skip it. */
+typedef struct ss_cloud_grads {
+  float* d_means;          /* (n,3) */
+  float* d_rotations;      /* (n,4) */
+  float* d_log_scales;     /* (n,3) */
+  float* d_opacity_logits; /* (n,)  */
+  float* d_sh;             /* (n,K,3) */
+  float* viewspace;        /* (n,) |dL/d mean2d| */
+  uint8_t* contributed;    /* (n,) */
+} ss_cloud_grads;
+
+/* ------------------------------------------------------------------ */
+/* library                                                             */
+/* ------------------------------------------------------------------ */
+const char* ss_last_error(void);
+int32_t ss_version(void);
+/* number of kernel launches issued by this library since load (telemetry) */
+int64_t ss_launch_count(void);
+
+/* ------------------------------------------------------------------ */
+/* NTC: hash-grid encode / decoder / lazy Adam   (ntc.py, optim.py)    */
+/* ------------------------------------------------------------------ */
+/* NeuralTransformationCache.encode (ntc.py:161-203): corner rows (n,L,8) int32
+ * and trilinear weights (n,L,8) f32; float64 position math. */
+int ss_ntc_encode(const ss_grid* grid, int64_t n, const float* means, int32_t* corner_idx,
+                  float* corner_w, uint32_t* status, void* stream);
+
+/* per-level touched-row mask (the EncodeContext.touched sets, ntc.py:187),
+ * mask is (L, T) bytes, OR-ed (caller zeroes it). */
+int ss_ntc_touched(const ss_grid* grid, int64_t n, const float* means, const int32_t* rows,
+                   uint8_t* mask, void* stream);
+
+/* NeuralTransformationCache.forward (ntc.py:219-248): out7 (n,7) = [d_mu | d_q]. */
+int ss_ntc_forward(const ss_grid* grid, const ss_mlp* mlp, int64_t n, const float* means,
+                   const int32_t* rows, const float* tables, const float* params, float* out7,
+                   void* stream);
+
+/* NeuralTransformationCache.backward (ntc.py:250-288).  Accumulates (+=) into
+ * g_tables (L,T,F) and g_params; caller zeroes them.  `scratch` must hold
+ * ss_ntc_backward_bytes(mlp) bytes. */
+size_t ss_ntc_backward_bytes(const ss_mlp* mlp);
+int ss_ntc_backward(const ss_grid* grid, const ss_mlp* mlp, int64_t n, const float* means,
+                    const int32_t* rows, const float* tables, const float* params,
+                    const float* g_out7, float* g_tables, float* g_params, void* scratch,
+                    void* stream);
+
+/* Adam.step (optim.py:33-66) via cache.adam_step (ntc.py:290-293):
+ * lazy rows for the tables (row_mask (L*T) bytes, row width F), dense for the
+ * MLP.  `step_dev` is a device int32 step counter incremented by this call
+ * (bias correction uses the global step, optim.py:52-54).  Moments are kept in
+ * float64 like the reference (eps = 1e-15 makes tiny gradients matter, D10).
+ * Zeroes the grads
+ * after use when zero_grads != 0. */
+int ss_adam_step(int64_t n_table, float* tables, float* g_tables, double* m_tables,
+                 double* v_tables, const uint8_t* row_mask, int32_t row_width,
+                 int64_t n_params, float* params, float* g_params, double* m_params,
+                 double* v_params, int32_t* step_dev, double lr, double beta1, double beta2,
+                 double eps, int32_t zero_grads, void* stream);
+
+/* ------------------------------------------------------------------ */
+/* NTC transform (transform.py)                                        */
+/* ------------------------------------------------------------------ */
+/* apply_ntc (transform.py:53-96) fused with the NTC forward: for the `n_in`
+ * Gaussians listed in `rows` (the inside-AABB set) writes means/rotations/sh
+ * of `out` (other rows untouched: caller pre-copies the source cloud). */
+int ss_apply_ntc(const ss_grid* grid, const ss_mlp* mlp, const ss_cloud* src, int64_t n_in,
+                 const int32_t* rows, const float* tables, const float* params,
+                 int32_t rotate_sh, float* out_means, float* out_rotations, float* out_sh,
+                 float* out7, uint32_t* status, void* stream);
+
+/* apply_ntc_backward (transform.py:99-135) fused with the NTC backward
+ * (ntc.py:250-288): gradients on the transformed cloud -> += g_tables, g_params. */
+int ss_apply_ntc_backward(const ss_grid* grid, const ss_mlp* mlp, const ss_cloud* src,
+                          int64_t n_in, const int32_t* rows, const float* tables,
+                          const float* params, int32_t rotate_sh, const float* d_means,
+                          const float* d_rotations, const float* d_sh, float* g_tables,
+                          float* g_params, void* scratch, void* stream);
+
+/* ------------------------------------------------------------------ */
+/* rasterizer (rasterizer.py)                                          */
+/* ------------------------------------------------------------------ */
+/* Workspace of a render, in two parts:
+ *   geom: per-Gaussian / per-pixel buffers, ss_raster_geom_bytes(n, cam, settings)
+ *   bins: per tile-pair buffers,            ss_raster_bin_bytes(n_pairs, cam, settings)
+ * The same workspace pointers must be passed to the backward call. */
+size_t ss_raster_geom_bytes(int64_t n, const ss_camera* cam, const ss_raster_settings* s);
+size_t ss_raster_bin_bytes(int64_t n_pairs, int64_t n, const ss_camera* cam,
+                           const ss_raster_settings* s);
+
+/* rasterize_forward phase 1 (rasterizer.py:227-261 up to the tile counts):
+ * projection + SH colour (fp64), stable depth sort, per-splat tile rectangles
+ * and their prefix sum.  Writes [n_survivors, n_pairs] to `counts_host`
+ * (pinned host int64[2]) asynchronously: synchronise `stream` before reading. */
+int ss_raster_forward_begin(const ss_cloud* cloud, const ss_camera* cam,
+                            const ss_raster_settings* s, void* geom, int64_t* counts_host,
+                            void* stream);
+
+/* rasterize_forward phase 2 (tile_bin rasterizer.py:107-175 + blending
+ * :178-211, :264-281): key duplication, stable tile sort, tile ranges, tile
+ * blend.  image (H,W,3) f32, alpha_map (H,W) f32, touch (n,) int32 (nullable). */
+int ss_raster_forward_finish(const ss_cloud* cloud, const ss_camera* cam,
+                             const ss_raster_settings* s, void* geom, void* bins,
+                             int64_t n_pairs, float* image, float* alpha_map, int32_t* touch,
+                             void* stream);
+
+/* rasterize_backward (rasterizer.py:284-402).  Output arrays are written for
+ * survivors only: caller zeroes them.  opacity_and_scales=0 skips
+ * d_opacity_logits / d_log_scales work (Stage 1 consumes neither). */
+int ss_raster_backward(const ss_cloud* cloud, const ss_camera* cam, const ss_raster_settings* s,
+                       void* geom, void* bins, int64_t n_pairs, const float* d_image,
+                       const ss_cloud_grads* grads, void* stream);
+
+/* Tile lists of the last forward (rasterizer.py:107-175 output): per tile
+ * [start,end) into the sorted pair array, and the sorted members (depth ranks,
+ * exactly the reference's `members`) and the survivor order (`indices`). */
+int ss_raster_tile_lists(const ss_camera* cam, const ss_raster_settings* s, const void* geom,
+                         const void* bins, int64_t n_pairs, int64_t n, int32_t* tile_ranges,
+                         int32_t* members, int32_t* indices, void* stream);
+
+/* ------------------------------------------------------------------ */
+/* loss (losses.py)                                                    */
+/* ------------------------------------------------------------------ */
+/* render_loss (losses.py:84-148): (1-lam) L1 + lam (1-SSIM)/2 over valid
+ * 11x11 windows, gradient d_image.  loss_dev: device double[1] (written).
+ * scratch: ss_loss_bytes(h, w) bytes. */
+size_t ss_loss_bytes(int32_t height, int32_t width);
+int ss_render_loss(const float* image, const float* target, int32_t height, int32_t width,
+                   double lam, double c1, double c2, void* scratch, double* loss_dev,
+                   float* d_image, uint32_t* status, void* stream);
+
+/* ------------------------------------------------------------------ */
+/* fused Stage-1 iteration (pipeline.py:262-277)                       */
+/* ------------------------------------------------------------------ */
+typedef struct ss_stage1 {
+  /* configuration */
+  ss_grid grid;
+  ss_mlp mlp;
+  ss_raster_settings settings;
+  double lr, beta1, beta2, eps, lambda_dssim;
+  int32_t rotate_sh, accumulate_stats;
+  /* source (frozen previous-frame) cloud and its inside-AABB rows */
+  ss_cloud src;
+  int64_t n_in;
+  const int32_t* rows;
+  /* NTC parameters, Adam state, gradients (caller-owned) */
+  float *tables, *params, *g_tables, *g_params;
+  double *m_tables, *v_tables, *m_params, *v_params;
+  uint8_t* row_mask;
+  int32_t* step_dev;
+  /* transformed cloud (means/rotations/sh; scales/opacities shared with src) */
+  float *t_means, *t_rotations, *t_sh;
+  /* per-view render buffers */
+  float *image, *alpha_map, *d_image;
+  float *d_means, *d_rotations, *d_sh; /* transformed-cloud grads (n) */
+  float* viewspace;
+  uint8_t* contributed;
+  float* stats_norm;      /* ViewspaceStats.norm_accum (adaptive.py:79-97), (n,) */
+  int32_t* stats_count;   /* ViewspaceStats.view_count, (n,) */
+  double* loss_dev;       /* last loss */
+  double* loss_history;   /* optional (nullable): loss of iteration i at [i] */
+  int32_t iteration;
+  uint32_t* status;
+  void *geom, *bins, *loss_scratch, *ntc_scratch;
+  int64_t bin_capacity; /* n_pairs the `bins` workspace holds */
+} ss_stage1;
+
+/* Start of a frame: touched-row mask, transformed <- source copy, zero Adam
+ * state and gradients, step = 0 (clone_cache + reset_adam, pipeline.py:213-219). */
+int ss_stage1_frame_begin(ss_stage1* st, void* stream);
+/* Iteration part A: apply_ntc + projection/depth sort/tile counts.
+ * counts_host (pinned int64[2]) receives [n_survivors, n_pairs]. */
+int ss_stage1_iter_begin(ss_stage1* st, const ss_camera* cam, int64_t* counts_host, void* stream);
+/* Iteration part B: binning, blend, loss, raster backward, transform+NTC
+ * backward, lazy Adam, view-space stats.  Requires n_pairs <= bin_capacity. */
+int ss_stage1_iter_finish(ss_stage1* st, const ss_camera* cam, const float* target,
+                          int64_t n_pairs, void* stream);
+/* Part B up to (and including) the NTC gradients but without the Adam step
+ * (view-sharded data parallelism all-reduces g_tables/g_params in between). */
+int ss_stage1_iter_grads(ss_stage1* st, const ss_camera* cam, const float* target,
+                         int64_t n_pairs, float grad_scale, void* stream);
+int ss_stage1_apply_adam(ss_stage1* st, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SS_B200_H */

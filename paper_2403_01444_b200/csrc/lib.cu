@@ -1,0 +1,134 @@
+// Library-level state: last-error string, launch telemetry, SH rotation
+// constants, MLP layout.  See include/ss_b200.h for the ABI contract.
+#include <mutex>
+#include <vector>
+
+#include "common.cuh"
+
+namespace ss {
+
+static thread_local std::string t_last_error;
+std::atomic<int64_t> g_launches{0};
+
+void set_error(const std::string& msg) { t_last_error = msg; }
+
+// Band-l basis values at a unit direction (degree-l part of sh_basis).
+static void band_values(int l, const double d[3], double* out) {
+  double b[16];
+  sh_basis<double>(l, d[0], d[1], d[2], b);
+  for (int m = 0; m < 2 * l + 1; ++m) out[m] = b[l * l + m];
+}
+
+// Gauss-Jordan inverse with partial pivoting; returns the inf-norm condition.
+static double invert(int n, std::vector<double> a, std::vector<double>& inv) {
+  double anorm = 0;
+  for (int i = 0; i < n; ++i) {
+    double r = 0;
+    for (int j = 0; j < n; ++j) r += std::fabs(a[i * n + j]);
+    anorm = std::max(anorm, r);
+  }
+  inv.assign(n * n, 0.0);
+  for (int i = 0; i < n; ++i) inv[i * n + i] = 1.0;
+  for (int c = 0; c < n; ++c) {
+    int p = c;
+    for (int r = c + 1; r < n; ++r)
+      if (std::fabs(a[r * n + c]) > std::fabs(a[p * n + c])) p = r;
+    if (std::fabs(a[p * n + c]) < 1e-12) return 1e300;
+    for (int j = 0; j < n; ++j) {
+      std::swap(a[c * n + j], a[p * n + j]);
+      std::swap(inv[c * n + j], inv[p * n + j]);
+    }
+    double d = a[c * n + c];
+    for (int j = 0; j < n; ++j) {
+      a[c * n + j] /= d;
+      inv[c * n + j] /= d;
+    }
+    for (int r = 0; r < n; ++r) {
+      if (r == c) continue;
+      double f = a[r * n + c];
+      for (int j = 0; j < n; ++j) {
+        a[r * n + j] -= f * a[c * n + j];
+        inv[r * n + j] -= f * inv[c * n + j];
+      }
+    }
+  }
+  double inorm = 0;
+  for (int i = 0; i < n; ++i) {
+    double r = 0;
+    for (int j = 0; j < n; ++j) r += std::fabs(inv[i * n + j]);
+    inorm = std::max(inorm, r);
+  }
+  return anorm * inorm;
+}
+
+// Pick 2l+1 sample directions with a well-conditioned S_{km} = Y_m(d_k) and
+// store S^{-1}: the band rotation is M = S^{-1} E, E_{kb} = Y_b(R^T d_k).
+static void build_band(int l, float (*dirs)[3], float* sinv) {
+  const int n = 2 * l + 1;
+  uint64_t state = 0x9E3779B97F4A7C15ull * (l + 1);
+  auto uni = [&]() {
+    state = state * 6364136223846793005ull + 1442695040888963407ull;
+    return ((state >> 11) * (1.0 / 9007199254740992.0)) * 2.0 - 1.0;
+  };
+  double best = 1e300;
+  std::vector<double> best_inv, best_dirs(n * 3);
+  for (int trial = 0; trial < 400; ++trial) {
+    std::vector<double> dd(n * 3), s(n * n), inv;
+    for (int k = 0; k < n; ++k) {
+      double v[3], nrm;
+      do {
+        v[0] = uni(), v[1] = uni(), v[2] = uni();
+        nrm = std::sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]);
+      } while (nrm < 0.2 || nrm > 1.0);
+      for (int j = 0; j < 3; ++j) dd[k * 3 + j] = v[j] / nrm;
+      band_values(l, &dd[k * 3], &s[k * n]);
+    }
+    double cond = invert(n, s, inv);
+    if (cond < best) {
+      best = cond;
+      best_inv = inv;
+      best_dirs = dd;
+    }
+  }
+  for (int k = 0; k < n; ++k)
+    for (int j = 0; j < 3; ++j) dirs[k][j] = (float)best_dirs[k * 3 + j];
+  for (int i = 0; i < n * n; ++i) sinv[i] = (float)best_inv[i];
+}
+
+void build_shrot_host(ShRotConst* h) {
+  build_band(2, h->dirs2, &h->binvT2[0][0]);
+  build_band(3, h->dirs3, &h->binvT3[0][0]);
+}
+
+}  // namespace ss
+
+extern "C" {
+
+const char* ss_last_error(void) { return ss::t_last_error.c_str(); }
+int32_t ss_version(void) { return 1; }
+int64_t ss_launch_count(void) { return ss::g_launches.load(); }
+
+int ss_mlp_get_layout(const ss_mlp* mlp, ss_mlp_layout* out) {
+  if (!mlp || !out) return SS_ERR_DATA;
+  if (mlp->in_dim < 1 || mlp->in_dim > 64 || mlp->hidden_dim < 1 || mlp->hidden_dim > 64 ||
+      mlp->n_hidden < 1 || mlp->n_hidden > 2 || mlp->out_dim != 7) {
+    ss::set_error("unsupported decoder shape (in<=64, hidden<=64, 1-2 hidden layers, 7 outputs)");
+    return SS_ERR_DATA;
+  }
+  ss_mlp_layout L{};
+  L.in_pad = mlp->in_dim <= 16 ? 16 : (mlp->in_dim <= 32 ? 32 : 64);
+  L.hidden_pad = 64;
+  L.out_pad = 8;
+  L.n_hidden = mlp->n_hidden;
+  L.w0 = 0;
+  L.b0 = (int64_t)L.in_pad * 64;
+  L.w1 = L.b0 + 64;
+  L.b1 = L.w1 + (L.n_hidden == 2 ? 64 * 64 : 0);
+  L.w2 = L.b1 + (L.n_hidden == 2 ? 64 : 0);
+  L.b2 = L.w2 + 64 * 8;
+  L.total = L.b2 + 8;
+  *out = L;
+  return SS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,865 @@
+// Tile rasterizer on sm_100a: EWA projection + SH colour (K4a, float64),
+// stable depth order (K4b), tile-rect prefix sum and key duplication (K4c),
+// stable tile sort (K4d), tile blend (K4e), reverse blend (K5a) and the
+// per-Gaussian chain back to raw parameters (K5b).
+//
+// Reference: rasterizer.py:107-402, cameras.py:132-178, sh.py:51-81,
+// gaussians.py:120-154 (/root/reference/pkg/src/splatstream/).
+#include <cub/cub.cuh>
+
+#include "common.cuh"
+
+namespace ss {
+
+// ------------------------------------------------------------------ workspace
+struct Geom {
+  double *key_in, *key_out;
+  int32_t *idx_in, *order;
+  double2* g_mean;   // per gid
+  double4* g_conop;  // per gid (c00, c01+c10, c11, opacity)
+  float4* g_color;   // per gid
+  double2* g_cov;    // per gid (cov2d[0][0], cov2d[1][1]) for the tile rect
+  double2* r_mean;   // per rank
+  float4* r_conop;   // per rank, fp32 copy for the blend
+  double4* r_conop_d;
+  float4* r_color;
+  int4* r_rect;     // per rank (tx0, tx1, ty0, ty1)
+  int64_t* offsets;  // per rank, exclusive prefix of tile counts (n+1)
+  float* acc;        // per rank x 9 (colour 3, opacity, mean2d 2, conic 00/01/11)
+  uint8_t* touched;  // per rank
+  float* t_final;    // per pixel
+  int32_t* n_contrib;
+  int2* ranges;      // per tile
+  int64_t* dev_counts;  // [survivors, pairs]
+  void* cub_sort;
+  size_t cub_sort_bytes;
+  void* cub_scan;
+  size_t cub_scan_bytes;
+  size_t total;
+};
+
+struct Bins {
+  uint32_t *keys_in, *keys_out, *vals_in, *vals_out;
+  void* cub_sort;
+  size_t cub_sort_bytes;
+  size_t total;
+};
+
+static inline int ntiles_x(const ss_camera* c, const ss_raster_settings* s) {
+  return (c->width + s->tile_size - 1) / s->tile_size;
+}
+static inline int ntiles_y(const ss_camera* c, const ss_raster_settings* s) {
+  return (c->height + s->tile_size - 1) / s->tile_size;
+}
+static inline int key_bits(int64_t ntiles) {
+  int b = 1;
+  while ((int64_t(1) << b) < ntiles) ++b;
+  return b;
+}
+
+static Geom plan_geom(void* base, int64_t n, const ss_camera* cam, const ss_raster_settings* s) {
+  Geom g{};
+  Carve c(base);
+  const int64_t P = (int64_t)cam->width * cam->height;
+  const int64_t NT = (int64_t)ntiles_x(cam, s) * ntiles_y(cam, s);
+  const int64_t nn = n > 0 ? n : 1;
+  g.key_in = c.take<double>(nn);
+  g.key_out = c.take<double>(nn);
+  g.idx_in = c.take<int32_t>(nn);
+  g.order = c.take<int32_t>(nn);
+  g.g_mean = c.take<double2>(nn);
+  g.g_conop = c.take<double4>(nn);
+  g.g_color = c.take<float4>(nn);
+  g.g_cov = c.take<double2>(nn);
+  g.r_mean = c.take<double2>(nn);
+  g.r_conop = c.take<float4>(nn);
+  g.r_conop_d = c.take<double4>(nn);
+  g.r_color = c.take<float4>(nn);
+  g.r_rect = c.take<int4>(nn);
+  g.offsets = c.take<int64_t>(nn + 1);
+  g.acc = c.take<float>(nn * 9);
+  g.touched = c.take<uint8_t>(nn);
+  g.t_final = c.take<float>(P);
+  g.n_contrib = c.take<int32_t>(P);
+  g.ranges = c.take<int2>(NT);
+  g.dev_counts = c.take<int64_t>(2);
+  size_t sb = 0, qb = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, sb, (const double*)nullptr, (double*)nullptr,
+                                  (const int32_t*)nullptr, (int32_t*)nullptr, (int)nn);
+  cub::DeviceScan::InclusiveSum(nullptr, qb, (const int64_t*)nullptr, (int64_t*)nullptr,
+                                (int)nn);
+  g.cub_sort_bytes = sb;
+  g.cub_sort = c.take<char>(sb);
+  g.cub_scan_bytes = qb;
+  g.cub_scan = c.take<char>(qb);
+  g.total = c.bytes();
+  return g;
+}
+
+static Bins plan_bins(void* base, int64_t pairs) {
+  Bins b{};
+  Carve c(base);
+  const int64_t pp = pairs > 0 ? pairs : 1;
+  b.keys_in = c.take<uint32_t>(pp);
+  b.keys_out = c.take<uint32_t>(pp);
+  b.vals_in = c.take<uint32_t>(pp);
+  b.vals_out = c.take<uint32_t>(pp);
+  size_t sb = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, sb, (const uint32_t*)nullptr, (uint32_t*)nullptr,
+                                  (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)pp);
+  b.cub_sort_bytes = sb;
+  b.cub_sort = c.take<char>(sb);
+  b.total = c.bytes();
+  return b;
+}
+
+// ------------------------------------------------------------------ projection
+struct CamD {
+  double R[3][3], t[3], pos[3];
+  double fx, fy, cx, cy, near_clip;
+  int W, H;
+};
+
+static CamD make_cam(const ss_camera* c) {
+  CamD d{};
+  for (int i = 0; i < 3; ++i) {
+    for (int j = 0; j < 3; ++j) d.R[i][j] = c->w2c[4 * i + j];
+    d.t[i] = c->w2c[4 * i + 3];
+  }
+  for (int i = 0; i < 3; ++i)  // position = -R^T t (cameras.py:73-76)
+    d.pos[i] = -(d.R[0][i] * d.t[0] + d.R[1][i] * d.t[1] + d.R[2][i] * d.t[2]);
+  d.fx = c->fx, d.fy = c->fy, d.cx = c->cx, d.cy = c->cy, d.near_clip = c->near_clip;
+  d.W = c->width, d.H = c->height;
+  return d;
+}
+
+// world covariance from raw quaternion + log scales (gaussians.py:120-124, :231-235)
+__device__ inline void covariance3d(const float* q, const float* ls, double S[3][3],
+                                    double Rq[3][3], double var[3], double u[4], double& qn) {
+  double w = q[0], x = q[1], y = q[2], z = q[3];
+  qn = sqrt(w * w + x * x + y * y + z * z);
+  double inv = qn > 0 ? 1.0 / qn : 0.0;
+  u[0] = w * inv, u[1] = x * inv, u[2] = y * inv, u[3] = z * inv;
+  quat_to_rot(u[0], u[1], u[2], u[3], Rq);
+  for (int i = 0; i < 3; ++i) var[i] = exp(2.0 * (double)ls[i]);
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j)
+      S[i][j] = Rq[i][0] * var[0] * Rq[j][0] + Rq[i][1] * var[1] * Rq[j][1] +
+                Rq[i][2] * var[2] * Rq[j][2];
+}
+
+struct Projected {
+  double p[3], mean[2], M[2][3], cov2d[2][2], conic[2][2], dir[3], dist, op;
+  double S[3][3], Rq[3][3], var[3], u[4], qn;
+  double raw[3];
+};
+
+__device__ inline void project_one(const CamD& cam, const ss_cloud& cl, int64_t i, Projected& P) {
+  const float* m = cl.means + 3 * i;
+  for (int r = 0; r < 3; ++r)
+    P.p[r] = cam.R[r][0] * (double)m[0] + cam.R[r][1] * (double)m[1] +
+             cam.R[r][2] * (double)m[2] + cam.t[r];
+  const double x = P.p[0], y = P.p[1], z = P.p[2];
+  P.mean[0] = cam.fx * x / z + cam.cx;  // cameras.py:141-145
+  P.mean[1] = cam.fy * y / z + cam.cy;
+  covariance3d(cl.rotations + 4 * i, cl.log_scales + 3 * i, P.S, P.Rq, P.var, P.u, P.qn);
+  // J (cameras.py:148-160), M = J R_w, cov2d = M S M^T + 0.3 I (cameras.py:163-178)
+  const double J[2][3] = {{cam.fx / z, 0.0, -cam.fx * x / (z * z)},
+                          {0.0, cam.fy / z, -cam.fy * y / (z * z)}};
+  for (int a = 0; a < 2; ++a)
+    for (int b = 0; b < 3; ++b)
+      P.M[a][b] = J[a][0] * cam.R[0][b] + J[a][1] * cam.R[1][b] + J[a][2] * cam.R[2][b];
+  for (int a = 0; a < 2; ++a)
+    for (int b = 0; b < 2; ++b) {
+      double s = 0;
+      for (int j = 0; j < 3; ++j)
+        for (int k = 0; k < 3; ++k) s += P.M[a][j] * P.S[j][k] * P.M[b][k];
+      P.cov2d[a][b] = s;
+    }
+  P.cov2d[0][0] += kLowpass;
+  P.cov2d[1][1] += kLowpass;
+  const double A = P.cov2d[0][0], B = P.cov2d[0][1], C = P.cov2d[1][0], D = P.cov2d[1][1];
+  const double det = A * D - B * C;  // rasterizer.py:93-104
+  P.conic[0][0] = D / det;
+  P.conic[0][1] = -B / det;
+  P.conic[1][0] = -C / det;
+  P.conic[1][1] = A / det;
+  double d[3];
+  for (int r = 0; r < 3; ++r) d[r] = (double)m[r] - cam.pos[r];
+  P.dist = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
+  const double dd = fmax(P.dist, 1e-12);
+  for (int r = 0; r < 3; ++r) P.dir[r] = d[r] / dd;
+  const int K = cl.sh_coeffs;
+  double basis[16];
+  sh_basis<double>(sh_degree_of(K), P.dir[0], P.dir[1], P.dir[2], basis);
+  for (int c = 0; c < 3; ++c) {
+    double s = 0.5;
+    for (int k = 0; k < K; ++k) s += basis[k] * (double)cl.sh[(i * K + k) * 3 + c];
+    P.raw[c] = s;
+  }
+  P.op = 1.0 / (1.0 + exp(-(double)cl.opacity_logits[i]));
+}
+
+// K4a: per-Gaussian projection; depth key (+inf when culled)
+__global__ void preprocess_kernel(CamD cam, ss_cloud cl, Geom g) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= cl.n) return;
+  g.idx_in[i] = (int32_t)i;
+  const float* m = cl.means + 3 * i;
+  const double z = cam.R[2][0] * (double)m[0] + cam.R[2][1] * (double)m[1] +
+                   cam.R[2][2] * (double)m[2] + cam.t[2];
+  if (!(z > cam.near_clip)) {  // rasterizer.py:228
+    g.key_in[i] = __longlong_as_double(0x7ff0000000000000ll);  // +inf
+    return;
+  }
+  g.key_in[i] = z;
+  atomicAdd(reinterpret_cast<unsigned long long*>(&g.dev_counts[0]), 1ull);
+  Projected P;
+  project_one(cam, cl, i, P);
+  g.g_mean[i] = make_double2(P.mean[0], P.mean[1]);
+  g.g_conop[i] = make_double4(P.conic[0][0], P.conic[0][1] + P.conic[1][0], P.conic[1][1], P.op);
+  g.g_color[i] = make_float4((float)fmin(fmax(P.raw[0], 0.0), 1.0),
+                             (float)fmin(fmax(P.raw[1], 0.0), 1.0),
+                             (float)fmin(fmax(P.raw[2], 0.0), 1.0), 0.f);
+  g.g_cov[i] = make_double2(P.cov2d[0][0], P.cov2d[1][1]);
+}
+
+// floor(v) // ts with Python floor-division semantics, clipped (rasterizer.py:142-145)
+__device__ inline int tile_of(double v, int ts, int nt) {
+  double f = floor(v);
+  f = fmin(fmax(f, -4.0e18), 4.0e18);
+  long long q = (long long)f;
+  long long t = q >= 0 ? q / ts : -((-q + ts - 1) / ts);
+  t = t < 0 ? 0 : (t > nt - 1 ? nt - 1 : t);
+  return (int)t;
+}
+
+// K4b/K4c: gather per-rank records, tile rectangle and its count
+__global__ void rank_kernel(CamD cam, ss_raster_settings s, int64_t n, Geom g) {
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const int64_t V = g.dev_counts[0];
+  if (r >= V) {
+    g.offsets[r] = 0;
+    return;
+  }
+  const int gid = g.order[r];
+  const double2 m = g.g_mean[gid];
+  const double4 co = g.g_conop[gid];
+  g.r_mean[r] = m;
+  g.r_conop_d[r] = co;
+  g.r_conop[r] = make_float4((float)co.x, (float)co.y, (float)co.z, (float)co.w);
+  g.r_color[r] = g.g_color[gid];
+  const int ts = s.tile_size;
+  const int ntx = (cam.W + ts - 1) / ts, nty = (cam.H + ts - 1) / ts;
+  int4 rect;
+  bool vis;
+  if (s.skip_alpha > 0.0) {  // rasterizer.py:132-148
+    const double ratio = fmax(co.w / s.skip_alpha, 1.0);
+    const double r2 = sqrt(fmax(9.0, 2.0 * log(ratio)));
+    const double2 cv = g.g_cov[gid];
+    const double hx = r2 * sqrt(fmax(cv.x, 0.0));
+    const double hy = r2 * sqrt(fmax(cv.y, 0.0));
+    const double xl = m.x - hx, xh = m.x + hx, yl = m.y - hy, yh = m.y + hy;
+    rect = make_int4(tile_of(xl, ts, ntx), tile_of(xh, ts, ntx), tile_of(yl, ts, nty),
+                     tile_of(yh, ts, nty));
+    vis = !((xh < 0) || (xl > cam.W - 1) || (yh < 0) || (yl > cam.H - 1));
+  } else {  // skip = 0: every tile (rasterizer.py:149-154)
+    rect = make_int4(0, ntx - 1, 0, nty - 1);
+    vis = true;
+  }
+  g.r_rect[r] = rect;
+  g.offsets[r] = vis ? (int64_t)(rect.y - rect.x + 1) * (rect.w - rect.z + 1) : 0;
+}
+
+__global__ void finish_counts_kernel(Geom g, int64_t n) {
+  // inclusive scan was written to offsets[1..n]; offsets[0] = 0; pairs = offsets[n]
+  g.offsets[0] = 0;
+  g.dev_counts[1] = n > 0 ? g.offsets[n] : 0;
+}
+
+// K4c: emit (tile id, rank) in rank order
+__global__ void duplicate_kernel(ss_raster_settings s, int ntx, int64_t n, Geom g, Bins b) {
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= n || r >= g.dev_counts[0]) return;
+  int64_t off = g.offsets[r];
+  const int64_t end = g.offsets[r + 1];
+  if (off == end) return;
+  const int4 rc = g.r_rect[r];
+  for (int ty = rc.z; ty <= rc.w; ++ty)
+    for (int tx = rc.x; tx <= rc.y; ++tx) {
+      b.keys_in[off] = (uint32_t)(ty * ntx + tx);
+      b.vals_in[off] = (uint32_t)r;
+      ++off;
+    }
+}
+
+__global__ void ranges_kernel(int64_t pairs, const uint32_t* __restrict__ keys, int2* ranges) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= pairs) return;
+  const uint32_t k = keys[i];
+  if (i == 0 || keys[i - 1] != k) ranges[k].x = (int)i;
+  if (i == pairs - 1 || keys[i + 1] != k) ranges[k].y = (int)(i + 1);
+}
+
+// ------------------------------------------------------------------ blend
+struct BlendParams {
+  int W, H, ntx;
+  float clamp, skip, stop;
+  double clamp_d, skip_d;
+  float bg[3];
+};
+
+// alpha of one pixel/splat pair (rasterizer.py:187-199).  Pairs whose fp32
+// alpha lies within 1e-4 (relative) of the skip threshold are recomputed in
+// float64 from the float64 records so the include/skip decision matches the
+// float64 reference (SURVEY.md "Hard parts").
+__device__ inline float pair_alpha(const BlendParams& bp, float dx, float dy, float4 co,
+                                   int rank, float px, float py, const double2* __restrict__ mean_d,
+                                   const double4* __restrict__ conop_d, float& G, float& og) {
+  const float maha = co.x * dx * dx + co.y * dx * dy + co.z * dy * dy;
+  G = expf(-0.5f * maha);
+  og = co.w * G;
+  float a = fminf(bp.clamp, og);
+  if (fabsf(a - bp.skip) <= 1e-4f * bp.skip) {
+    const double2 m = mean_d[rank];
+    const double4 c = conop_d[rank];
+    const double ddx = (double)px - m.x, ddy = (double)py - m.y;
+    const double mh = c.x * ddx * ddx + c.y * ddx * ddy + c.z * ddy * ddy;
+    const double ad = fmin(bp.clamp_d, c.w * exp(-0.5 * mh));
+    return ad < bp.skip_d ? 0.f : fmaxf((float)ad, bp.skip);
+  }
+  return a < bp.skip ? 0.f : a;
+}
+
+template <int TS>
+struct BlendShape {
+  static constexpr int NT = TS * TS <= 256 ? TS * TS : 256;
+  static constexpr int PPT = TS * TS / NT;
+};
+
+template <int TS, bool TOUCH>
+__global__ void __launch_bounds__(BlendShape<TS>::NT) blend_fwd_kernel(
+    BlendParams bp, Geom g, const uint32_t* __restrict__ vals, float* __restrict__ image,
+    float* __restrict__ alpha_map, int32_t* __restrict__ touch) {
+  constexpr int NT = BlendShape<TS>::NT, PPT = BlendShape<TS>::PPT;
+  __shared__ float2 s_xy[NT];
+  __shared__ float4 s_co[NT];
+  __shared__ float4 s_col[NT];
+  __shared__ int s_rank[NT];
+  __shared__ int s_touch[TOUCH ? NT : 1];
+  const int tile = blockIdx.x;
+  const int x0 = (tile % bp.ntx) * TS, y0 = (tile / bp.ntx) * TS;
+  const int2 range = g.ranges[tile];
+  float T[PPT], C[PPT][3];
+  int last[PPT];
+  bool done[PPT];
+  float lx[PPT], ly[PPT];
+#pragma unroll
+  for (int p = 0; p < PPT; ++p) {
+    const int li = threadIdx.x + p * NT;
+    lx[p] = (float)(li % TS);
+    ly[p] = (float)(li / TS);
+    T[p] = 1.f;
+    C[p][0] = C[p][1] = C[p][2] = 0.f;
+    last[p] = 0;
+    done[p] = (x0 + li % TS >= bp.W) || (y0 + li / TS >= bp.H);
+  }
+  for (int b = range.x; b < range.y; b += NT) {
+    bool all_done = true;
+#pragma unroll
+    for (int p = 0; p < PPT; ++p) all_done &= done[p];
+    if (__syncthreads_count(all_done) == NT) break;
+    const int j = b + threadIdx.x;
+    if (j < range.y) {
+      const int r = (int)vals[j];
+      const double2 m = g.r_mean[r];
+      s_xy[threadIdx.x] = make_float2((float)(m.x - x0), (float)(m.y - y0));
+      s_co[threadIdx.x] = g.r_conop[r];
+      s_col[threadIdx.x] = g.r_color[r];
+      s_rank[threadIdx.x] = r;
+    }
+    if (TOUCH) s_touch[threadIdx.x] = 0;
+    __syncthreads();
+    const int cnt = min(NT, range.y - b);
+    for (int k = 0; k < cnt; ++k) {
+      const float2 xy = s_xy[k];
+      const float4 co = s_co[k];
+      int contrib = 0;
+#pragma unroll
+      for (int p = 0; p < PPT; ++p) {
+        if (done[p]) continue;
+        const float dx = lx[p] - xy.x, dy = ly[p] - xy.y;
+        float G, og;
+        const float a = pair_alpha(bp, dx, dy, co, s_rank[k], lx[p] + x0, ly[p] + y0, g.r_mean,
+                                   g.r_conop_d, G, og);
+        if (a == 0.f) continue;
+        const float4 col = s_col[k];
+        const float w = a * T[p];
+        C[p][0] = fmaf(w, col.x, C[p][0]);
+        C[p][1] = fmaf(w, col.y, C[p][1]);
+        C[p][2] = fmaf(w, col.z, C[p][2]);
+        T[p] *= 1.f - a;
+        last[p] = b - range.x + k + 1;
+        ++contrib;
+        if (T[p] < bp.stop) done[p] = true;  // later splats fail T_before >= stop
+      }
+      if (TOUCH) {
+        const unsigned bal = __ballot_sync(0xffffffffu, contrib > 0);
+        int tot = contrib;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+        if (bal && (threadIdx.x & 31) == 0) atomicAdd(&s_touch[k], tot);
+      }
+    }
+    if (TOUCH) {
+      __syncthreads();
+      if (threadIdx.x < cnt && s_touch[threadIdx.x] > 0)
+        atomicAdd(&touch[g.order[s_rank[threadIdx.x]]], s_touch[threadIdx.x]);
+    }
+  }
+#pragma unroll
+  for (int p = 0; p < PPT; ++p) {
+    const int li = threadIdx.x + p * NT;
+    const int px = x0 + li % TS, py = y0 + li / TS;
+    if (px >= bp.W || py >= bp.H) continue;
+    const int64_t pix = (int64_t)py * bp.W + px;
+    image[3 * pix + 0] = C[p][0] + T[p] * bp.bg[0];
+    image[3 * pix + 1] = C[p][1] + T[p] * bp.bg[1];
+    image[3 * pix + 2] = C[p][2] + T[p] * bp.bg[2];
+    if (alpha_map) alpha_map[pix] = 1.f - T[p];
+    g.t_final[pix] = T[p];
+    g.n_contrib[pix] = last[p];
+  }
+}
+
+// K5a: reverse blend (rasterizer.py:306-349).  Per pixel, walk the tile list
+// back to front from the last contributor reconstructing T_before by
+// division, keeping the suffix sum incl. the background term; per-splat
+// gradients are warp-reduced and added to the per-rank accumulators.
+template <int TS>
+__global__ void __launch_bounds__(BlendShape<TS>::NT) blend_bwd_kernel(
+    BlendParams bp, Geom g, const uint32_t* __restrict__ vals, const float* __restrict__ d_image) {
+  constexpr int NT = BlendShape<TS>::NT, PPT = BlendShape<TS>::PPT;
+  __shared__ float2 s_xy[NT];
+  __shared__ float4 s_co[NT];
+  __shared__ float4 s_col[NT];
+  __shared__ int s_rank[NT];
+  const int tile = blockIdx.x;
+  const int x0 = (tile % bp.ntx) * TS, y0 = (tile / bp.ntx) * TS;
+  const int2 range = g.ranges[tile];
+  float T[PPT], S[PPT], gp[PPT][3], lx[PPT], ly[PPT];
+  int last[PPT];
+  int max_last = 0;
+#pragma unroll
+  for (int p = 0; p < PPT; ++p) {
+    const int li = threadIdx.x + p * NT;
+    const int px = x0 + li % TS, py = y0 + li / TS;
+    lx[p] = (float)(li % TS);
+    ly[p] = (float)(li / TS);
+    if (px < bp.W && py < bp.H) {
+      const int64_t pix = (int64_t)py * bp.W + px;
+      T[p] = g.t_final[pix];
+      last[p] = g.n_contrib[pix];
+      gp[p][0] = d_image[3 * pix];
+      gp[p][1] = d_image[3 * pix + 1];
+      gp[p][2] = d_image[3 * pix + 2];
+    } else {
+      T[p] = 0.f;
+      last[p] = 0;
+      gp[p][0] = gp[p][1] = gp[p][2] = 0.f;
+    }
+    const float gb = gp[p][0] * bp.bg[0] + gp[p][1] * bp.bg[1] + gp[p][2] * bp.bg[2];
+    S[p] = gb * T[p];
+    max_last = max(max_last, last[p]);
+  }
+  // only positions below the tile-wide max contributor count matter
+  __shared__ int s_last;
+  if (threadIdx.x == 0) s_last = 0;
+  __syncthreads();
+  atomicMax(&s_last, max_last);
+  __syncthreads();
+  const int tile_last = s_last;
+  const int end0 = range.x + tile_last;
+  for (int end = end0; end > range.x; end -= NT) {
+    const int start = max(range.x, end - NT);
+    const int cnt = end - start;
+    __syncthreads();
+    if (threadIdx.x < cnt) {
+      const int pos = end - 1 - threadIdx.x;
+      const int r = (int)vals[pos];
+      const double2 m = g.r_mean[r];
+      s_xy[threadIdx.x] = make_float2((float)(m.x - x0), (float)(m.y - y0));
+      s_co[threadIdx.x] = g.r_conop[r];
+      s_col[threadIdx.x] = g.r_color[r];
+      s_rank[threadIdx.x] = r;
+    }
+    __syncthreads();
+    for (int k = 0; k < cnt; ++k) {
+      const int pos_rel = end - 1 - k - range.x;
+      const float2 xy = s_xy[k];
+      const float4 co = s_co[k];
+      const float4 col = s_col[k];
+      float v[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      bool any = false;
+#pragma unroll
+      for (int p = 0; p < PPT; ++p) {
+        if (pos_rel >= last[p]) continue;
+        const float dx = lx[p] - xy.x, dy = ly[p] - xy.y;
+        float G, og;
+        const float a = pair_alpha(bp, dx, dy, co, s_rank[k], lx[p] + x0, ly[p] + y0, g.r_mean,
+                                   g.r_conop_d, G, og);
+        if (a == 0.f) continue;
+        const float oma = 1.f - a;
+        const float tb = T[p] / oma;  // T_before
+        const float w = a * tb;
+        v[0] = fmaf(w, gp[p][0], v[0]);
+        v[1] = fmaf(w, gp[p][1], v[1]);
+        v[2] = fmaf(w, gp[p][2], v[2]);
+        const float u = gp[p][0] * col.x + gp[p][1] * col.y + gp[p][2] * col.z;
+        float da = u * tb - S[p] / fmaxf(oma, 1e-12f);
+        S[p] = fmaf(u * a, tb, S[p]);
+        T[p] = tb;
+        if (!(og < bp.clamp)) da = 0.f;  // flat above the clamp (rasterizer.py:336-337)
+        const float dm = -0.5f * G * co.w * da;
+        const float c01 = 0.5f * co.y;
+        v[3] = fmaf(da, G, v[3]);
+        v[4] -= 2.f * dm * (co.x * dx + c01 * dy);
+        v[5] -= 2.f * dm * (c01 * dx + co.z * dy);
+        v[6] = fmaf(dm, dx * dx, v[6]);
+        v[7] = fmaf(dm, dx * dy, v[7]);
+        v[8] = fmaf(dm, dy * dy, v[8]);
+        any = true;
+      }
+      if (__any_sync(0xffffffffu, any)) {
+#pragma unroll
+        for (int q = 0; q < 9; ++q) v[q] = warp_sum(v[q]);
+        const unsigned bal = __ballot_sync(0xffffffffu, any);
+        if ((threadIdx.x & 31) == 0) {
+          float* a = g.acc + (int64_t)s_rank[k] * 9;
+#pragma unroll
+          for (int q = 0; q < 9; ++q) atomicAdd(a + q, v[q]);
+          if (bal) g.touched[s_rank[k]] = 1;
+        }
+      }
+    }
+  }
+}
+
+// K5b: per-survivor chain to raw parameters (rasterizer.py:351-402), float64
+__global__ void gaussian_bwd_kernel(CamD cam, ss_cloud cl, Geom g, int64_t n, ss_cloud_grads out,
+                                    int full) {
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const int gid = g.order[r];
+  if (r >= g.dev_counts[0]) {  // culled: zero rows so callers need no memset
+    const int K = cl.sh_coeffs;
+    if (out.viewspace) out.viewspace[gid] = 0.f;
+    if (out.contributed) out.contributed[gid] = 0;
+    if (out.d_means) for (int j = 0; j < 3; ++j) out.d_means[3 * gid + j] = 0.f;
+    if (out.d_rotations) for (int j = 0; j < 4; ++j) out.d_rotations[4 * gid + j] = 0.f;
+    if (out.d_sh) for (int j = 0; j < 3 * K; ++j) out.d_sh[(int64_t)gid * 3 * K + j] = 0.f;
+    if (full && out.d_log_scales) for (int j = 0; j < 3; ++j) out.d_log_scales[3 * gid + j] = 0.f;
+    if (full && out.d_opacity_logits) out.d_opacity_logits[gid] = 0.f;
+    return;
+  }
+  const float* a = g.acc + r * 9;
+  const double acol[3] = {a[0], a[1], a[2]};
+  const double aop = a[3];
+  const double am[2] = {a[4], a[5]};
+  const double A[2][2] = {{a[6], a[7]}, {a[7], a[8]}};
+  if (out.viewspace) out.viewspace[gid] = (float)sqrt(am[0] * am[0] + am[1] * am[1]);
+  if (out.contributed) out.contributed[gid] = g.touched[r];
+  Projected P;
+  project_one(cam, cl, gid, P);
+  const int K = cl.sh_coeffs;
+  const int deg = sh_degree_of(K);
+  // colour -> SH and view direction (sh.py:62-81)
+  double gc[3];
+  for (int c = 0; c < 3; ++c) gc[c] = (P.raw[c] > 0.0 && P.raw[c] < 1.0) ? acol[c] : 0.0;
+  double basis[16], gbasis[16];
+  sh_basis<double>(deg, P.dir[0], P.dir[1], P.dir[2], basis);
+  for (int k = 0; k < K; ++k) {
+    const float* shk = cl.sh + (gid * K + k) * 3;
+    gbasis[k] = shk[0] * gc[0] + shk[1] * gc[1] + shk[2] * gc[2];
+    if (out.d_sh)
+      for (int c = 0; c < 3; ++c) out.d_sh[(gid * K + k) * 3 + c] = (float)(basis[k] * gc[c]);
+  }
+  double gdir[3] = {0.0, 0.0, 0.0};
+  sh_basis_vjp<double>(deg, P.dir[0], P.dir[1], P.dir[2], gbasis, gdir);
+  const double dd = fmax(P.dist, 1e-12);
+  const double dg = P.dir[0] * gdir[0] + P.dir[1] * gdir[1] + P.dir[2] * gdir[2];
+  double gw[3];
+  for (int i = 0; i < 3; ++i) gw[i] = (gdir[i] - P.dir[i] * dg) / dd;
+  // conic -> cov2d: -C A C
+  double CA[2][2], gcov2[2][2];
+  for (int i = 0; i < 2; ++i)
+    for (int j = 0; j < 2; ++j) CA[i][j] = P.conic[i][0] * A[0][j] + P.conic[i][1] * A[1][j];
+  for (int i = 0; i < 2; ++i)
+    for (int j = 0; j < 2; ++j) gcov2[i][j] = -(CA[i][0] * P.conic[0][j] + CA[i][1] * P.conic[1][j]);
+  // cov2d = M S M^T: g_S = M^T G M, g_M = (G + G^T) M S
+  double gS[3][3], GM[2][3], gM[2][3];
+  for (int i = 0; i < 2; ++i)
+    for (int j = 0; j < 3; ++j)
+      GM[i][j] = (gcov2[i][0] + gcov2[0][i]) * P.M[0][j] + (gcov2[i][1] + gcov2[1][i]) * P.M[1][j];
+  for (int i = 0; i < 2; ++i)
+    for (int j = 0; j < 3; ++j)
+      gM[i][j] = GM[i][0] * P.S[0][j] + GM[i][1] * P.S[1][j] + GM[i][2] * P.S[2][j];
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) {
+      double s = 0;
+      for (int p = 0; p < 2; ++p)
+        for (int q = 0; q < 2; ++q) s += P.M[p][i] * gcov2[p][q] * P.M[q][j];
+      gS[i][j] = s;
+    }
+  // g_J = g_M R_w^T
+  double gJ[2][3];
+  for (int i = 0; i < 2; ++i)
+    for (int k = 0; k < 3; ++k)
+      gJ[i][k] = gM[i][0] * cam.R[k][0] + gM[i][1] * cam.R[k][1] + gM[i][2] * cam.R[k][2];
+  const double x = P.p[0], y = P.p[1], z = P.p[2];
+  const double fx = cam.fx, fy = cam.fy;
+  double gp[3];
+  gp[0] = gJ[0][2] * (-fx / (z * z));
+  gp[1] = gJ[1][2] * (-fy / (z * z));
+  gp[2] = gJ[0][0] * (-fx / (z * z)) + gJ[1][1] * (-fy / (z * z)) +
+          gJ[0][2] * (2.0 * fx * x / (z * z * z)) + gJ[1][2] * (2.0 * fy * y / (z * z * z));
+  // + J^T acc_mean2d
+  gp[0] += (fx / z) * am[0];
+  gp[1] += (fy / z) * am[1];
+  gp[2] += (-fx * x / (z * z)) * am[0] + (-fy * y / (z * z)) * am[1];
+  for (int j = 0; j < 3; ++j)
+    gw[j] += gp[0] * cam.R[0][j] + gp[1] * cam.R[1][j] + gp[2] * cam.R[2][j];
+  if (out.d_means)
+    for (int j = 0; j < 3; ++j) out.d_means[3 * gid + j] = (float)gw[j];
+  // covariance -> quaternion / log scales (gaussians.py:127-154)
+  double gsym[3][3], gR[3][3];
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) gsym[i][j] = gS[i][j] + gS[j][i];
+  for (int i = 0; i < 3; ++i)
+    for (int k = 0; k < 3; ++k)
+      gR[i][k] = (gsym[i][0] * P.Rq[0][k] + gsym[i][1] * P.Rq[1][k] + gsym[i][2] * P.Rq[2][k]) *
+                 P.var[k];
+  if (out.d_rotations) {
+    double gu[4];
+    quat_to_rot_vjp(P.u[0], P.u[1], P.u[2], P.u[3], gR, gu);
+    const double dot = P.u[0] * gu[0] + P.u[1] * gu[1] + P.u[2] * gu[2] + P.u[3] * gu[3];
+    for (int k = 0; k < 4; ++k)
+      out.d_rotations[4 * gid + k] = (float)((gu[k] - P.u[k] * dot) / P.qn);
+  }
+  if (full) {
+    if (out.d_log_scales)
+      for (int i = 0; i < 3; ++i) {
+        double s = 0;
+        for (int j = 0; j < 3; ++j)
+          for (int k = 0; k < 3; ++k) s += P.Rq[j][i] * gS[j][k] * P.Rq[k][i];
+        out.d_log_scales[3 * gid + i] = (float)(s * 2.0 * P.var[i]);
+      }
+    if (out.d_opacity_logits) out.d_opacity_logits[gid] = (float)(aop * P.op * (1.0 - P.op));
+  }
+}
+
+// ------------------------------------------------------------------ host glue
+static BlendParams blend_params(const ss_camera* cam, const ss_raster_settings* s) {
+  BlendParams bp{};
+  bp.W = cam->width;
+  bp.H = cam->height;
+  bp.ntx = ntiles_x(cam, s);
+  bp.clamp = (float)s->alpha_clamp;
+  bp.skip = (float)s->skip_alpha;
+  bp.stop = (float)s->stop_transmittance;
+  bp.clamp_d = s->alpha_clamp;
+  bp.skip_d = s->skip_alpha;
+  for (int i = 0; i < 3; ++i) bp.bg[i] = (float)s->background[i];
+  return bp;
+}
+
+static int check_raster(const ss_cloud* cl, const ss_camera* cam, const ss_raster_settings* s) {
+  if (!cam || !s || cam->width <= 0 || cam->height <= 0) {
+    set_error("invalid camera");
+    return SS_ERR_DATA;
+  }
+  if (s->tile_size != 8 && s->tile_size != 16 && s->tile_size != 32 && s->tile_size != 64) {
+    set_error("tile_size must be 8, 16, 32 or 64");
+    return SS_ERR_DATA;
+  }
+  if (cl && (cl->sh_coeffs < 1 || cl->sh_coeffs > 16 ||
+             sh_degree_of(cl->sh_coeffs) != (int)std::sqrt((double)cl->sh_coeffs) - 1)) {
+    set_error("sh_coeffs must be 1, 4, 9 or 16");
+    return SS_ERR_DATA;
+  }
+  return SS_OK;
+}
+
+template <bool TOUCH>
+static int launch_blend_fwd(int ts, int64_t ntiles, cudaStream_t st, const BlendParams& bp,
+                            const Geom& g, const uint32_t* vals, float* image, float* alpha,
+                            int32_t* touch) {
+  const unsigned grid = (unsigned)ntiles;
+  switch (ts) {
+    case 8: blend_fwd_kernel<8, TOUCH><<<grid, BlendShape<8>::NT, 0, st>>>(bp, g, vals, image, alpha, touch); break;
+    case 16: blend_fwd_kernel<16, TOUCH><<<grid, BlendShape<16>::NT, 0, st>>>(bp, g, vals, image, alpha, touch); break;
+    case 32: blend_fwd_kernel<32, TOUCH><<<grid, BlendShape<32>::NT, 0, st>>>(bp, g, vals, image, alpha, touch); break;
+    default: blend_fwd_kernel<64, TOUCH><<<grid, BlendShape<64>::NT, 0, st>>>(bp, g, vals, image, alpha, touch); break;
+  }
+  SS_CHECK_LAUNCH("blend_fwd_kernel");
+  return SS_OK;
+}
+
+static int launch_blend_bwd(int ts, int64_t ntiles, cudaStream_t st, const BlendParams& bp,
+                            const Geom& g, const uint32_t* vals, const float* d_image) {
+  const unsigned grid = (unsigned)ntiles;
+  switch (ts) {
+    case 8: blend_bwd_kernel<8><<<grid, BlendShape<8>::NT, 0, st>>>(bp, g, vals, d_image); break;
+    case 16: blend_bwd_kernel<16><<<grid, BlendShape<16>::NT, 0, st>>>(bp, g, vals, d_image); break;
+    case 32: blend_bwd_kernel<32><<<grid, BlendShape<32>::NT, 0, st>>>(bp, g, vals, d_image); break;
+    default: blend_bwd_kernel<64><<<grid, BlendShape<64>::NT, 0, st>>>(bp, g, vals, d_image); break;
+  }
+  SS_CHECK_LAUNCH("blend_bwd_kernel");
+  return SS_OK;
+}
+
+int raster_begin(const ss_cloud* cl, const ss_camera* cam, const ss_raster_settings* s,
+                 void* geom, int64_t* counts_host, cudaStream_t st) {
+  SS_TRY(check_raster(cl, cam, s));
+  const int64_t n = cl->n;
+  Geom g = plan_geom(geom, n, cam, s);
+  const CamD cd = make_cam(cam);
+  SS_CUDA(cudaMemsetAsync(g.dev_counts, 0, 2 * sizeof(int64_t), st));
+  if (n > 0) {
+    preprocess_kernel<<<(unsigned)cdiv(n, 256), 256, 0, st>>>(cd, *cl, g);
+    SS_CHECK_LAUNCH("preprocess_kernel");
+    size_t sb = g.cub_sort_bytes;
+    SS_CUDA(cub::DeviceRadixSort::SortPairs(g.cub_sort, sb, g.key_in, g.key_out, g.idx_in,
+                                            g.order, (int)n, 0, 64, st));
+    g_launches.fetch_add(4);
+    rank_kernel<<<(unsigned)cdiv(n, 256), 256, 0, st>>>(cd, *s, n, g);
+    SS_CHECK_LAUNCH("rank_kernel");
+    size_t qb = g.cub_scan_bytes;
+    SS_CUDA(cub::DeviceScan::InclusiveSum(g.cub_scan, qb, g.offsets, g.offsets + 1, (int)n, st));
+    g_launches.fetch_add(2);
+  }
+  finish_counts_kernel<<<1, 1, 0, st>>>(g, n);
+  SS_CHECK_LAUNCH("finish_counts_kernel");
+  if (counts_host)
+    SS_CUDA(cudaMemcpyAsync(counts_host, g.dev_counts, 2 * sizeof(int64_t),
+                            cudaMemcpyDeviceToHost, st));
+  return SS_OK;
+}
+
+int raster_finish(const ss_cloud* cl, const ss_camera* cam, const ss_raster_settings* s,
+                  void* geom, void* bins, int64_t pairs, float* image, float* alpha,
+                  int32_t* touch, cudaStream_t st) {
+  SS_TRY(check_raster(cl, cam, s));
+  const int64_t n = cl->n;
+  Geom g = plan_geom(geom, n, cam, s);
+  Bins b = plan_bins(bins, pairs);
+  const int ntx = ntiles_x(cam, s), nty = ntiles_y(cam, s);
+  const int64_t ntiles = (int64_t)ntx * nty;
+  if (pairs > (int64_t)0x7fffffff) {
+    set_error("more than 2^31 tile pairs in one view");
+    return SS_ERR_CAPACITY;
+  }
+  SS_CUDA(cudaMemsetAsync(g.ranges, 0, ntiles * sizeof(int2), st));
+  if (pairs > 0) {
+    duplicate_kernel<<<(unsigned)cdiv(n, 256), 256, 0, st>>>(*s, ntx, n, g, b);
+    SS_CHECK_LAUNCH("duplicate_kernel");
+    size_t sb = b.cub_sort_bytes;
+    SS_CUDA(cub::DeviceRadixSort::SortPairs(b.cub_sort, sb, b.keys_in, b.keys_out, b.vals_in,
+                                            b.vals_out, (int)pairs, 0, key_bits(ntiles), st));
+    g_launches.fetch_add(2 * ((key_bits(ntiles) + 7) / 8));
+    ranges_kernel<<<(unsigned)cdiv(pairs, 256), 256, 0, st>>>(pairs, b.keys_out, g.ranges);
+    SS_CHECK_LAUNCH("ranges_kernel");
+  }
+  const BlendParams bp = blend_params(cam, s);
+  if (touch)
+    return launch_blend_fwd<true>(s->tile_size, ntiles, st, bp, g, b.vals_out, image, alpha, touch);
+  return launch_blend_fwd<false>(s->tile_size, ntiles, st, bp, g, b.vals_out, image, alpha,
+                                 nullptr);
+}
+
+int raster_backward(const ss_cloud* cl, const ss_camera* cam, const ss_raster_settings* s,
+                    void* geom, void* bins, int64_t pairs, const float* d_image,
+                    const ss_cloud_grads* grads, int full, cudaStream_t st) {
+  SS_TRY(check_raster(cl, cam, s));
+  const int64_t n = cl->n;
+  if (n == 0) return SS_OK;
+  Geom g = plan_geom(geom, n, cam, s);
+  Bins b = plan_bins(bins, pairs);
+  const int64_t ntiles = (int64_t)ntiles_x(cam, s) * ntiles_y(cam, s);
+  SS_CUDA(cudaMemsetAsync(g.acc, 0, n * 9 * sizeof(float), st));
+  SS_CUDA(cudaMemsetAsync(g.touched, 0, n, st));
+  const BlendParams bp = blend_params(cam, s);
+  if (pairs > 0) SS_TRY(launch_blend_bwd(s->tile_size, ntiles, st, bp, g, b.vals_out, d_image));
+  gaussian_bwd_kernel<<<(unsigned)cdiv(n, 128), 128, 0, st>>>(make_cam(cam), *cl, g, n, *grads,
+                                                               full);
+  SS_CHECK_LAUNCH("gaussian_bwd_kernel");
+  return SS_OK;
+}
+
+__global__ void tile_lists_kernel(int64_t ntiles, const int2* ranges, int32_t* out) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= ntiles) return;
+  out[2 * t] = ranges[t].x;
+  out[2 * t + 1] = ranges[t].y;
+}
+
+}  // namespace ss
+
+using namespace ss;
+
+extern "C" {
+
+size_t ss_raster_geom_bytes(int64_t n, const ss_camera* cam, const ss_raster_settings* s) {
+  if (check_raster(nullptr, cam, s) != SS_OK) return 0;
+  return plan_geom(nullptr, n, cam, s).total;
+}
+
+size_t ss_raster_bin_bytes(int64_t n_pairs, int64_t n, const ss_camera* cam,
+                           const ss_raster_settings* s) {
+  (void)n, (void)cam, (void)s;
+  return plan_bins(nullptr, n_pairs).total;
+}
+
+int ss_raster_forward_begin(const ss_cloud* cloud, const ss_camera* cam,
+                            const ss_raster_settings* s, void* geom, int64_t* counts_host,
+                            void* stream) {
+  return raster_begin(cloud, cam, s, geom, counts_host, as_stream(stream));
+}
+
+int ss_raster_forward_finish(const ss_cloud* cloud, const ss_camera* cam,
+                             const ss_raster_settings* s, void* geom, void* bins,
+                             int64_t n_pairs, float* image, float* alpha_map, int32_t* touch,
+                             void* stream) {
+  return raster_finish(cloud, cam, s, geom, bins, n_pairs, image, alpha_map, touch,
+                       as_stream(stream));
+}
+
+int ss_raster_backward(const ss_cloud* cloud, const ss_camera* cam, const ss_raster_settings* s,
+                       void* geom, void* bins, int64_t n_pairs, const float* d_image,
+                       const ss_cloud_grads* grads, void* stream) {
+  return raster_backward(cloud, cam, s, geom, bins, n_pairs, d_image, grads, 1,
+                         as_stream(stream));
+}
+
+int ss_raster_tile_lists(const ss_camera* cam, const ss_raster_settings* s, const void* geom,
+                         const void* bins, int64_t n_pairs, int64_t n, int32_t* tile_ranges,
+                         int32_t* members, int32_t* indices, void* stream) {
+  SS_TRY(check_raster(nullptr, cam, s));
+  cudaStream_t st = as_stream(stream);
+  Geom g = plan_geom(const_cast<void*>(geom), n, cam, s);
+  Bins b = plan_bins(const_cast<void*>(bins), n_pairs);
+  const int64_t ntiles = (int64_t)ntiles_x(cam, s) * ntiles_y(cam, s);
+  if (tile_ranges && ntiles > 0) {
+    tile_lists_kernel<<<(unsigned)cdiv(ntiles, 256), 256, 0, st>>>(ntiles, g.ranges, tile_ranges);
+    SS_CHECK_LAUNCH("tile_lists_kernel");
+  }
+  if (members && n_pairs > 0)
+    SS_CUDA(cudaMemcpyAsync(members, b.vals_out, n_pairs * sizeof(uint32_t),
+                            cudaMemcpyDeviceToDevice, st));
+  if (indices && n > 0)
+    SS_CUDA(cudaMemcpyAsync(indices, g.order, n * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+  return SS_OK;
+}
+
+}  // extern "C"

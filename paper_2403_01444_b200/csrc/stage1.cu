@@ -1,0 +1,137 @@
+// Fused Stage-1 iteration (pipeline.py:262-277): one stream-ordered sequence
+// apply_ntc -> rasterize_forward -> render_loss -> rasterize_backward ->
+// apply_ntc_backward -> lazy Adam (+ view-space stats), with no host work in
+// between except the tile-pair count readback that sizes the sort.
+#include "common.cuh"
+
+namespace ss {
+
+static ss_cloud transformed(const ss_stage1* st) {
+  ss_cloud c = st->src;
+  c.means = st->t_means;
+  c.rotations = st->t_rotations;
+  c.sh = st->t_sh;
+  return c;
+}
+
+__global__ void stats_kernel(int64_t n, const float* __restrict__ vs,
+                             const uint8_t* __restrict__ contrib, float* __restrict__ norm,
+                             int32_t* __restrict__ count) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  norm[i] += vs[i];  // ViewspaceStats.add (adaptive.py:92-94)
+  count[i] += contrib[i];
+}
+
+__global__ void scale_kernel(int64_t n, float* __restrict__ v, float s) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) v[i] *= s;
+}
+
+static int64_t n_table(const ss_stage1* st) {
+  return (int64_t)st->grid.n_levels * ((int64_t)1 << st->grid.log2_table) * st->grid.n_features;
+}
+
+static int64_t n_params(const ss_stage1* st) {
+  ss_mlp_layout L{};
+  ss_mlp_get_layout(&st->mlp, &L);
+  return L.total;
+}
+
+}  // namespace ss
+
+using namespace ss;
+
+extern "C" {
+
+int ss_stage1_frame_begin(ss_stage1* st, void* stream) {
+  cudaStream_t s = as_stream(stream);
+  const int64_t n = st->src.n, K = st->src.sh_coeffs;
+  const int64_t T = (int64_t)1 << st->grid.log2_table;
+  SS_CUDA(cudaMemsetAsync(st->row_mask, 0, (size_t)st->grid.n_levels * T, s));
+  SS_TRY(ss_ntc_touched(&st->grid, st->n_in, st->src.means, st->rows, st->row_mask, stream));
+  SS_CUDA(cudaMemcpyAsync(st->t_means, st->src.means, n * 3 * sizeof(float),
+                          cudaMemcpyDeviceToDevice, s));
+  SS_CUDA(cudaMemcpyAsync(st->t_rotations, st->src.rotations, n * 4 * sizeof(float),
+                          cudaMemcpyDeviceToDevice, s));
+  SS_CUDA(cudaMemcpyAsync(st->t_sh, st->src.sh, n * K * 3 * sizeof(float),
+                          cudaMemcpyDeviceToDevice, s));
+  const int64_t nt = n_table(st), np = n_params(st);
+  SS_CUDA(cudaMemsetAsync(st->g_tables, 0, nt * sizeof(float), s));
+  SS_CUDA(cudaMemsetAsync(st->g_params, 0, np * sizeof(float), s));
+  SS_CUDA(cudaMemsetAsync(st->m_tables, 0, nt * sizeof(double), s));
+  SS_CUDA(cudaMemsetAsync(st->v_tables, 0, nt * sizeof(double), s));
+  SS_CUDA(cudaMemsetAsync(st->m_params, 0, np * sizeof(double), s));
+  SS_CUDA(cudaMemsetAsync(st->v_params, 0, np * sizeof(double), s));
+  SS_CUDA(cudaMemsetAsync(st->step_dev, 0, sizeof(int32_t), s));
+  if (st->stats_norm) SS_CUDA(cudaMemsetAsync(st->stats_norm, 0, n * sizeof(float), s));
+  if (st->stats_count) SS_CUDA(cudaMemsetAsync(st->stats_count, 0, n * sizeof(int32_t), s));
+  st->iteration = 0;
+  return SS_OK;
+}
+
+int ss_stage1_iter_begin(ss_stage1* st, const ss_camera* cam, int64_t* counts_host,
+                         void* stream) {
+  SS_TRY(ss_apply_ntc(&st->grid, &st->mlp, &st->src, st->n_in, st->rows, st->tables, st->params,
+                      st->rotate_sh, st->t_means, st->t_rotations, st->t_sh, nullptr, st->status,
+                      stream));
+  const ss_cloud tc = transformed(st);
+  return raster_begin(&tc, cam, &st->settings, st->geom, counts_host, as_stream(stream));
+}
+
+int ss_stage1_iter_grads(ss_stage1* st, const ss_camera* cam, const float* target,
+                         int64_t n_pairs, float grad_scale, void* stream) {
+  cudaStream_t s = as_stream(stream);
+  if (n_pairs > st->bin_capacity) {
+    set_error("tile-pair workspace too small");
+    return SS_ERR_CAPACITY;
+  }
+  const ss_cloud tc = transformed(st);
+  SS_TRY(raster_finish(&tc, cam, &st->settings, st->geom, st->bins, n_pairs, st->image,
+                       st->alpha_map, nullptr, s));
+  SS_TRY(ss_render_loss(st->image, target, cam->height, cam->width, st->lambda_dssim,
+                        0.01 * 0.01, 0.03 * 0.03, st->loss_scratch, st->loss_dev, st->d_image,
+                        st->status, stream));
+  if (st->loss_history)
+    SS_CUDA(cudaMemcpyAsync(st->loss_history + st->iteration, st->loss_dev, sizeof(double),
+                            cudaMemcpyDeviceToDevice, s));
+  if (grad_scale != 1.0f) {
+    const int64_t m = (int64_t)cam->width * cam->height * 3;
+    scale_kernel<<<(unsigned)cdiv(m, 256), 256, 0, s>>>(m, st->d_image, grad_scale);
+    SS_CHECK_LAUNCH("scale_kernel");
+  }
+  ss_cloud_grads gr{};
+  gr.d_means = st->d_means;
+  gr.d_rotations = st->d_rotations;
+  gr.d_sh = st->d_sh;
+  gr.viewspace = st->viewspace;
+  gr.contributed = st->contributed;
+  SS_TRY(raster_backward(&tc, cam, &st->settings, st->geom, st->bins, n_pairs, st->d_image, &gr,
+                         0, s));
+  if (st->accumulate_stats && st->stats_norm && st->stats_count) {
+    const int64_t n = st->src.n;
+    stats_kernel<<<(unsigned)cdiv(n, 256), 256, 0, s>>>(n, st->viewspace, st->contributed,
+                                                         st->stats_norm, st->stats_count);
+    SS_CHECK_LAUNCH("stats_kernel");
+  }
+  SS_TRY(ss_apply_ntc_backward(&st->grid, &st->mlp, &st->src, st->n_in, st->rows, st->tables,
+                               st->params, st->rotate_sh, st->d_means, st->d_rotations,
+                               st->d_sh, st->g_tables, st->g_params, st->ntc_scratch, stream));
+  st->iteration += 1;
+  return SS_OK;
+}
+
+int ss_stage1_apply_adam(ss_stage1* st, void* stream) {
+  return ss_adam_step(n_table(st), st->tables, st->g_tables, st->m_tables, st->v_tables,
+                      st->row_mask, st->grid.n_features, n_params(st), st->params, st->g_params,
+                      st->m_params, st->v_params, st->step_dev, st->lr, st->beta1, st->beta2,
+                      st->eps, 1, stream);
+}
+
+int ss_stage1_iter_finish(ss_stage1* st, const ss_camera* cam, const float* target,
+                          int64_t n_pairs, void* stream) {
+  SS_TRY(ss_stage1_iter_grads(st, cam, target, n_pairs, 1.0f, stream));
+  return ss_stage1_apply_adam(st, stream);
+}
+
+}  // extern "C"
