@@ -109,6 +109,9 @@ typedef struct ss_cloud_grads {
 /* ------------------------------------------------------------------ */
 const char* ss_last_error(void);
 int32_t ss_version(void);
+/* sizeof of the ABI structs (0 grid, 1 mlp, 2 mlp_layout, 3 camera, 4 settings,
+ * 5 cloud, 6 cloud_grads, 7 stage1) so bindings can verify their layout */
+size_t ss_struct_size(int32_t which);
 /* number of kernel launches issued by this library since load (telemetry) */
 int64_t ss_launch_count(void);
 
@@ -125,10 +128,12 @@ int ss_ntc_encode(const ss_grid* grid, int64_t n, const float* means, int32_t* c
 int ss_ntc_touched(const ss_grid* grid, int64_t n, const float* means, const int32_t* rows,
                    uint8_t* mask, void* stream);
 
-/* NeuralTransformationCache.forward (ntc.py:219-248): out7 (n,7) = [d_mu | d_q]. */
+/* NeuralTransformationCache.forward (ntc.py:219-248): out7 (n,7) = [d_mu | d_q];
+ * feats (n, L*F) = the interpolated features (gather_features, ntc.py:205-216),
+ * nullable. */
 int ss_ntc_forward(const ss_grid* grid, const ss_mlp* mlp, int64_t n, const float* means,
                    const int32_t* rows, const float* tables, const float* params, float* out7,
-                   void* stream);
+                   float* feats, void* stream);
 
 /* NeuralTransformationCache.backward (ntc.py:250-288).  Accumulates (+=) into
  * g_tables (L,T,F) and g_params; caller zeroes them.  `scratch` must hold
@@ -171,6 +176,17 @@ int ss_apply_ntc_backward(const ss_grid* grid, const ss_mlp* mlp, const ss_cloud
                           const float* d_rotations, const float* d_sh, float* g_tables,
                           float* g_params, void* scratch, void* stream);
 
+/* The transform alone, for caches that are not this library's NTC (duck-typed
+ * caches such as the reference's test stubs, test_transform.py:24-46):
+ * apply given out7 = [d_mu | d_q] (transform.py:70-84) ... */
+int ss_transform_apply(const ss_cloud* src, int64_t n_in, const int32_t* rows, const float* out7,
+                       int32_t rotate_sh, float* out_means, float* out_rotations, float* out_sh,
+                       uint32_t* status, void* stream);
+/* ... and its vector-Jacobian product g_out7 (transform.py:111-134). */
+int ss_transform_vjp(const ss_cloud* src, int64_t n_in, const int32_t* rows, const float* out7,
+                     int32_t rotate_sh, const float* d_means, const float* d_rotations,
+                     const float* d_sh, float* g_out7, void* stream);
+
 /* ------------------------------------------------------------------ */
 /* rasterizer (rasterizer.py)                                          */
 /* ------------------------------------------------------------------ */
@@ -212,16 +228,27 @@ int ss_raster_tile_lists(const ss_camera* cam, const ss_raster_settings* s, cons
                          const void* bins, int64_t n_pairs, int64_t n, int32_t* tile_ranges,
                          int32_t* members, int32_t* indices, void* stream);
 
+/* tile_bin (rasterizer.py:107-175) on precomputed projections: mean2d (n,2),
+ * cov2d (n,2,2) and opacity (n,) float64, already in depth order.  Phase 1
+ * writes [n, n_pairs] to counts_host; phase 2 fills the tile lists exactly
+ * like ss_raster_tile_lists.  `geom` sized by ss_raster_geom_bytes. */
+int ss_tile_bin_begin(int64_t n, const double* mean2d, const double* cov2d, const double* opacity,
+                      const ss_camera* cam, const ss_raster_settings* s, void* geom,
+                      int64_t* counts_host, void* stream);
+int ss_tile_bin_finish(int64_t n, const ss_camera* cam, const ss_raster_settings* s, void* geom,
+                       void* bins, int64_t n_pairs, int32_t* tile_ranges, int32_t* members,
+                       void* stream);
+
 /* ------------------------------------------------------------------ */
 /* loss (losses.py)                                                    */
 /* ------------------------------------------------------------------ */
 /* render_loss (losses.py:84-148): (1-lam) L1 + lam (1-SSIM)/2 over valid
- * 11x11 windows, gradient d_image.  loss_dev: device double[1] (written).
+ * 11x11 windows, gradient d_image; images (H, W, channels) interleaved, 1-4 channels.  loss_dev: device double[1] (written).
  * scratch: ss_loss_bytes(h, w) bytes. */
-size_t ss_loss_bytes(int32_t height, int32_t width);
+size_t ss_loss_bytes(int32_t height, int32_t width, int32_t channels);
 int ss_render_loss(const float* image, const float* target, int32_t height, int32_t width,
-                   double lam, double c1, double c2, void* scratch, double* loss_dev,
-                   float* d_image, uint32_t* status, void* stream);
+                   int32_t channels, double lam, double c1, double c2, void* scratch,
+                   double* loss_dev, float* d_image, uint32_t* status, void* stream);
 
 /* ------------------------------------------------------------------ */
 /* fused Stage-1 iteration (pipeline.py:262-277)                       */

@@ -106,6 +106,20 @@ extern "C" {
 
 const char* ss_last_error(void) { return ss::t_last_error.c_str(); }
 int32_t ss_version(void) { return 1; }
+
+size_t ss_struct_size(int32_t which) {
+  switch (which) {
+    case 0: return sizeof(ss_grid);
+    case 1: return sizeof(ss_mlp);
+    case 2: return sizeof(ss_mlp_layout);
+    case 3: return sizeof(ss_camera);
+    case 4: return sizeof(ss_raster_settings);
+    case 5: return sizeof(ss_cloud);
+    case 6: return sizeof(ss_cloud_grads);
+    case 7: return sizeof(ss_stage1);
+    default: return 0;
+  }
+}
 int64_t ss_launch_count(void) { return ss::g_launches.load(); }
 
 int ss_mlp_get_layout(const ss_mlp* mlp, ss_mlp_layout* out) {

@@ -12,7 +12,7 @@ constexpr int WIN = 11, HALO = WIN - 1;
 constexpr int BX = 32, BY = 8;  // output tile per CTA (256 threads)
 
 struct LossParams {
-  int H, W, Hv, Wv;
+  int H, W, Hv, Wv, C;
   double g[WIN];
   double c1, c2, lam, up;  // up = -lam / (2 n_windows)
 };
@@ -34,7 +34,7 @@ __global__ void __launch_bounds__(BX* BY) ssim_map_kernel(LossParams lp,
     const int py = oy + ry, px = ox + rx;
     float xv = 0.f, yv = 0.f;
     if (py < lp.H && px < lp.W) {
-      const int64_t o = ((int64_t)py * lp.W + px) * 3 + c;
+      const int64_t o = ((int64_t)py * lp.W + px) * lp.C + c;
       xv = img[o];
       yv = tgt[o];
     }
@@ -79,9 +79,9 @@ __global__ void __launch_bounds__(BX* BY) ssim_map_kernel(LossParams lp,
     const double gmx = 2.0 * my * ga1 + 2.0 * mx * gb1 - 2.0 * my * ga2 - 2.0 * mx * gb2;
     const int64_t plane = (int64_t)lp.Hv * lp.Wv;
     const int64_t o = (int64_t)vy * lp.Wv + vx;
-    maps[(0 * 3 + c) * plane + o] = (float)gmx;
-    maps[(1 * 3 + c) * plane + o] = (float)gb2;
-    maps[(2 * 3 + c) * plane + o] = (float)(2.0 * ga2);
+    maps[(0 * lp.C + c) * plane + o] = (float)gmx;
+    maps[(1 * lp.C + c) * plane + o] = (float)gb2;
+    maps[(2 * lp.C + c) * plane + o] = (float)(2.0 * ga2);
   }
   // block sum of SSIM values
   __shared__ double red[BX * BY / 32];
@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(BX* BY) ssim_grad_kernel(LossParams lp,
     const bool in = vy >= 0 && vx >= 0 && vy < lp.Hv && vx < lp.Wv;
     const int64_t o = (int64_t)vy * lp.Wv + vx;
 #pragma unroll
-    for (int q = 0; q < 3; ++q) sm[q][ry][rx] = in ? maps[(q * 3 + c) * plane + o] : 0.f;
+    for (int q = 0; q < 3; ++q) sm[q][ry][rx] = in ? maps[(q * lp.C + c) * plane + o] : 0.f;
   }
   __syncthreads();
   for (int i = tid; i < (BY + HALO) * BX; i += BX * BY) {
@@ -137,11 +137,11 @@ __global__ void __launch_bounds__(BX* BY) ssim_grad_kernel(LossParams lp,
     for (int k = 0; k < WIN; ++k)
 #pragma unroll
       for (int q = 0; q < 3; ++q) b[q] = fmaf((float)lp.g[k], hs[q][threadIdx.y + k][threadIdx.x], b[q]);
-    const int64_t o = ((int64_t)py * lp.W + px) * 3 + c;
+    const int64_t o = ((int64_t)py * lp.W + px) * lp.C + c;
     const float x = img[o], y = tgt[o];
     const float d = x - y;
     l1 = fabs((double)x - (double)y);
-    const double size = (double)lp.H * lp.W * 3;
+    const double size = (double)lp.H * lp.W * lp.C;
     const double sgn = d > 0.f ? 1.0 : (d < 0.f ? -1.0 : 0.0);
     const double back = (double)b[0] + (double)b[1] * 2.0 * x + (double)b[2] * y;
     grad[o] = (float)((1.0 - lp.lam) * sgn / size + lp.up * back);
@@ -159,8 +159,8 @@ __global__ void __launch_bounds__(BX* BY) ssim_grad_kernel(LossParams lp,
 
 __global__ void loss_finalize_kernel(LossParams lp, const double* sums, double* loss,
                                      uint32_t* status) {
-  const double size = (double)lp.H * lp.W * 3;
-  const double nwin = (double)lp.Hv * lp.Wv * 3;
+  const double size = (double)lp.H * lp.W * lp.C;
+  const double nwin = (double)lp.Hv * lp.Wv * lp.C;
   const double l = (1.0 - lp.lam) * (sums[1] / size) + lp.lam * (1.0 - sums[0] / nwin) / 2.0;
   *loss = l;
   if (!isfinite(l) && status) atomicOr(status, SS_FLAG_NONFINITE);  // errors.py:24-29
@@ -172,22 +172,26 @@ using namespace ss;
 
 extern "C" {
 
-size_t ss_loss_bytes(int32_t height, int32_t width) {
+size_t ss_loss_bytes(int32_t height, int32_t width, int32_t channels) {
   const int64_t hv = height - HALO, wv = width - HALO;
   if (hv <= 0 || wv <= 0) return 256;
-  return align_up(2 * sizeof(double)) + align_up((size_t)9 * hv * wv * sizeof(float));
+  return align_up(2 * sizeof(double)) + align_up((size_t)3 * channels * hv * wv * sizeof(float));
 }
 
 int ss_render_loss(const float* image, const float* target, int32_t height, int32_t width,
-                   double lam, double c1, double c2, void* scratch, double* loss_dev,
-                   float* d_image, uint32_t* status, void* stream) {
+                   int32_t channels, double lam, double c1, double c2, void* scratch,
+                   double* loss_dev, float* d_image, uint32_t* status, void* stream) {
+  if (channels < 1 || channels > 4) {
+    set_error("render_loss supports 1-4 channels");
+    return SS_ERR_DATA;
+  }
   if (height < WIN || width < WIN) {
     set_error("image smaller than the SSIM window");  // losses.py:111-112
     return SS_ERR_DATA;
   }
   cudaStream_t st = as_stream(stream);
   LossParams lp{};
-  lp.H = height, lp.W = width, lp.Hv = height - HALO, lp.Wv = width - HALO;
+  lp.H = height, lp.W = width, lp.Hv = height - HALO, lp.Wv = width - HALO, lp.C = channels;
   double tot = 0;
   for (int k = 0; k < WIN; ++k) {  // losses.py:36-40 (normalised separably)
     const double a = k - WIN / 2;
@@ -196,15 +200,15 @@ int ss_render_loss(const float* image, const float* target, int32_t height, int3
   }
   for (int k = 0; k < WIN; ++k) lp.g[k] /= tot;
   lp.c1 = c1, lp.c2 = c2, lp.lam = lam;
-  lp.up = -lam / (2.0 * (double)lp.Hv * lp.Wv * 3);
+  lp.up = -lam / (2.0 * (double)lp.Hv * lp.Wv * channels);
   double* sums = static_cast<double*>(scratch);
   float* maps = reinterpret_cast<float*>(static_cast<char*>(scratch) + align_up(2 * sizeof(double)));
   SS_CUDA(cudaMemsetAsync(sums, 0, 2 * sizeof(double), st));
   dim3 blk(BX, BY);
-  dim3 g1((unsigned)cdiv(lp.Wv, BX), (unsigned)cdiv(lp.Hv, BY), 3);
+  dim3 g1((unsigned)cdiv(lp.Wv, BX), (unsigned)cdiv(lp.Hv, BY), channels);
   ssim_map_kernel<<<g1, blk, 0, st>>>(lp, image, target, maps, sums);
   SS_CHECK_LAUNCH("ssim_map_kernel");
-  dim3 g2((unsigned)cdiv(lp.W, BX), (unsigned)cdiv(lp.H, BY), 3);
+  dim3 g2((unsigned)cdiv(lp.W, BX), (unsigned)cdiv(lp.H, BY), channels);
   ssim_grad_kernel<<<g2, blk, 0, st>>>(lp, image, target, maps, d_image, sums);
   SS_CHECK_LAUNCH("ssim_grad_kernel");
   loss_finalize_kernel<<<1, 1, 0, st>>>(lp, sums, loss_dev, status);

@@ -428,29 +428,12 @@ __global__ void touched_kernel(ss_grid g, int64_t n, const float* __restrict__ m
   }
 }
 
-// NTC forward (+ transform when `src` given).  One thread per Gaussian.
-template <int IN, int NL>
-__global__ void __launch_bounds__(128) ntc_forward_kernel(
-    ss_grid g, int64_t n, const float* __restrict__ means, const int32_t* __restrict__ rows,
-    const float* __restrict__ tables, const float* __restrict__ params, float* __restrict__ out7,
-    ss_cloud src, int rotate_sh, float* __restrict__ t_means, float* __restrict__ t_rot,
-    float* __restrict__ t_sh, uint32_t* status) {
-  extern __shared__ __align__(16) float smem[];
-  load_params<Lay<IN, NL>::TOTAL>(smem, params);
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const int64_t gid = rows ? rows[i] : i;
-  double xn[3];
-  if (!normalise(g, means + 3 * gid, xn) && status) atomicOr(status, SS_FLAG_OUTSIDE);
-  float x[IN], h1[HID], h2[HID], o[OUTP];
-  gather_features<IN>(g, tables, xn, x);
-  mlp_forward<IN, NL>(smem, x, h1, h2, o);
-  if (out7) {
-#pragma unroll
-    for (int k = 0; k < 7; ++k) out7[i * 7 + k] = o[k];
-  }
-  if (!t_means) return;
-  // ---- transform (transform.py:70-84)
+// transform (transform.py:70-84): mu' = mu + d_mu, q' = norm(d_q) (x) q_src,
+// SH bands >= 1 rotated by R(norm(d_q)).
+__device__ inline void apply_transform(const ss_cloud& src, int64_t gid, const float* o,
+                                       int rotate_sh, float* __restrict__ t_means,
+                                       float* __restrict__ t_rot, float* __restrict__ t_sh,
+                                       uint32_t* status) {
   float nq = sqrtf(o[3] * o[3] + o[4] * o[4] + o[5] * o[5] + o[6] * o[6]);
   if (nq < 1e-12f) {
     if (status) atomicOr(status, SS_FLAG_ZERO_QUAT);
@@ -477,6 +460,37 @@ __global__ void __launch_bounds__(128) ntc_forward_kernel(
     rotate_sh_bands(deg, R, in, outv);
     for (int k = 3; k < 3 * K; ++k) t_sh[gid * 3 * K + k] = outv[k];
   }
+}
+
+// NTC forward (+ transform when `src` given).  One thread per Gaussian.
+template <int IN, int NL>
+__global__ void __launch_bounds__(128) ntc_forward_kernel(
+    ss_grid g, int64_t n, const float* __restrict__ means, const int32_t* __restrict__ rows,
+    const float* __restrict__ tables, const float* __restrict__ params, float* __restrict__ out7,
+    float* __restrict__ feats, ss_cloud src, int rotate_sh, float* __restrict__ t_means,
+    float* __restrict__ t_rot, float* __restrict__ t_sh, uint32_t* status) {
+  extern __shared__ __align__(16) float smem[];
+  load_params<Lay<IN, NL>::TOTAL>(smem, params);
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t gid = rows ? rows[i] : i;
+  double xn[3];
+  if (!normalise(g, means + 3 * gid, xn) && status) atomicOr(status, SS_FLAG_OUTSIDE);
+  float x[IN], h1[HID], h2[HID], o[OUTP];
+  gather_features<IN>(g, tables, xn, x);
+  if (feats) {
+    const int nf = g.n_levels * g.n_features;
+#pragma unroll
+    for (int k = 0; k < IN; ++k)
+      if (k < nf) feats[i * nf + k] = x[k];
+  }
+  mlp_forward<IN, NL>(smem, x, h1, h2, o);
+  if (out7) {
+#pragma unroll
+    for (int k = 0; k < 7; ++k) out7[i * 7 + k] = o[k];
+  }
+  if (!t_means) return;
+  apply_transform(src, gid, o, rotate_sh, t_means, t_rot, t_sh, status);
 }
 
 // dL/d(out7) from transformed-cloud gradients (transform.py:111-134)
@@ -518,6 +532,34 @@ __device__ inline void transform_vjp(const ss_cloud& src, int64_t gid, const flo
   const float dot = u[0] * gu[0] + u[1] * gu[1] + u[2] * gu[2] + u[3] * gu[3];
 #pragma unroll
   for (int k = 0; k < 4; ++k) g7[3 + k] = (gu[k] - u[k] * dot) / nq;
+}
+
+__global__ void transform_apply_kernel(ss_cloud src, int64_t n, const int32_t* __restrict__ rows,
+                                       const float* __restrict__ out7, int rotate_sh,
+                                       float* __restrict__ tm, float* __restrict__ tr,
+                                       float* __restrict__ ts, uint32_t* status) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  float o[OUTP];
+#pragma unroll
+  for (int k = 0; k < 7; ++k) o[k] = out7[i * 7 + k];
+  o[7] = 0.f;
+  apply_transform(src, rows ? rows[i] : i, o, rotate_sh, tm, tr, ts, status);
+}
+
+__global__ void transform_vjp_kernel(ss_cloud src, int64_t n, const int32_t* __restrict__ rows,
+                                     const float* __restrict__ out7, int rotate_sh,
+                                     const float* __restrict__ dm, const float* __restrict__ dr,
+                                     const float* __restrict__ ds, float* __restrict__ g_out7) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  float o[OUTP], g7[OUTP];
+#pragma unroll
+  for (int k = 0; k < 7; ++k) o[k] = out7[i * 7 + k];
+  o[7] = 0.f;
+  transform_vjp(src, rows ? rows[i] : i, o, rotate_sh, dm, dr, ds, g7);
+#pragma unroll
+  for (int k = 0; k < 7; ++k) g_out7[i * 7 + k] = g7[k];
 }
 
 // Backward: one thread per Gaussian per chunk; the decoder's weight gradient
@@ -825,7 +867,7 @@ struct FwdLaunch {
   const float* means;
   const int32_t* rows;
   const float *tables, *params;
-  float* out7;
+  float *out7, *feats;
   ss_cloud src;
   int rotate_sh;
   float *tm, *tr, *ts;
@@ -837,8 +879,8 @@ struct FwdLaunch {
     const size_t smem = Lay<IN, NL>::TOTAL * sizeof(float);
     auto k = ntc_forward_kernel<IN, NL>;
     SS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k<<<(unsigned)cdiv(n, 128), 128, smem, st>>>(*g, n, means, rows, tables, params, out7, src,
-                                                  rotate_sh, tm, tr, ts, status);
+    k<<<(unsigned)cdiv(n, 128), 128, smem, st>>>(*g, n, means, rows, tables, params, out7, feats,
+                                                  src, rotate_sh, tm, tr, ts, status);
     SS_CHECK_LAUNCH("ntc_forward_kernel");
     return SS_OK;
   }
@@ -902,10 +944,10 @@ int ss_ntc_touched(const ss_grid* grid, int64_t n, const float* means, const int
 
 int ss_ntc_forward(const ss_grid* grid, const ss_mlp* mlp, int64_t n, const float* means,
                    const int32_t* rows, const float* tables, const float* params, float* out7,
-                   void* stream) {
+                   float* feats, void* stream) {
   SS_TRY(check_grid(grid, mlp));
-  FwdLaunch L{grid, n, means, rows, tables, params, out7, ss_cloud{}, 0, nullptr, nullptr,
-              nullptr, nullptr, as_stream(stream)};
+  FwdLaunch L{grid, n, means, rows, tables, params, out7, feats, ss_cloud{}, 0, nullptr,
+              nullptr, nullptr, nullptr, as_stream(stream)};
   return dispatch_mlp(mlp, L);
 }
 
@@ -939,8 +981,8 @@ int ss_apply_ntc(const ss_grid* grid, const ss_mlp* mlp, const ss_cloud* src, in
     return SS_ERR_DATA;
   }
   SS_TRY(ensure_shrot_const());
-  FwdLaunch L{grid, n_in, src->means, rows, tables, params, out7, *src, rotate_sh, out_means,
-              out_rotations, out_sh, status, as_stream(stream)};
+  FwdLaunch L{grid, n_in, src->means, rows, tables, params, out7, nullptr, *src, rotate_sh,
+              out_means, out_rotations, out_sh, status, as_stream(stream)};
   return dispatch_mlp(mlp, L);
 }
 
@@ -959,6 +1001,36 @@ int ss_apply_ntc_backward(const ss_grid* grid, const ss_mlp* mlp, const ss_cloud
   BwdLaunch L{grid, n_in, src->means, rows, tables, params, nullptr, *src, rotate_sh,
               d_means, d_rotations, d_sh, g_tables, g_params, as_stream(stream)};
   return dispatch_mlp(mlp, L);
+}
+
+int ss_transform_apply(const ss_cloud* src, int64_t n_in, const int32_t* rows, const float* out7,
+                       int32_t rotate_sh, float* out_means, float* out_rotations, float* out_sh,
+                       uint32_t* status, void* stream) {
+  if (!src || src->sh_coeffs < 1 || src->sh_coeffs > 16) {
+    set_error("ss_transform_apply: bad cloud");
+    return SS_ERR_DATA;
+  }
+  if (n_in == 0) return SS_OK;
+  SS_TRY(ensure_shrot_const());
+  transform_apply_kernel<<<(unsigned)cdiv(n_in, 128), 128, 0, as_stream(stream)>>>(
+      *src, n_in, rows, out7, rotate_sh, out_means, out_rotations, out_sh, status);
+  SS_CHECK_LAUNCH("transform_apply_kernel");
+  return SS_OK;
+}
+
+int ss_transform_vjp(const ss_cloud* src, int64_t n_in, const int32_t* rows, const float* out7,
+                     int32_t rotate_sh, const float* d_means, const float* d_rotations,
+                     const float* d_sh, float* g_out7, void* stream) {
+  if (!src || src->sh_coeffs < 1 || src->sh_coeffs > 16) {
+    set_error("ss_transform_vjp: bad cloud");
+    return SS_ERR_DATA;
+  }
+  if (n_in == 0) return SS_OK;
+  SS_TRY(ensure_shrot_const());
+  transform_vjp_kernel<<<(unsigned)cdiv(n_in, 128), 128, 0, as_stream(stream)>>>(
+      *src, n_in, rows, out7, rotate_sh, d_means, d_rotations, d_sh, g_out7);
+  SS_CHECK_LAUNCH("transform_vjp_kernel");
+  return SS_OK;
 }
 
 int ss_adam_step(int64_t n_table, float* tables, float* g_tables, double* m_tables,

@@ -804,6 +804,61 @@ __global__ void tile_lists_kernel(int64_t ntiles, const int2* ranges, int32_t* o
   out[2 * t + 1] = ranges[t].y;
 }
 
+// tile_bin on given projections (depth order = input order)
+__global__ void tile_bin_setup_kernel(int64_t n, const double* __restrict__ mean2d,
+                                      const double* __restrict__ cov2d,
+                                      const double* __restrict__ opacity, Geom g) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i == 0) g.dev_counts[0] = n;
+  if (i >= n) return;
+  g.order[i] = (int32_t)i;
+  g.g_mean[i] = make_double2(mean2d[2 * i], mean2d[2 * i + 1]);
+  g.g_cov[i] = make_double2(cov2d[4 * i], cov2d[4 * i + 3]);
+  g.g_conop[i] = make_double4(0.0, 0.0, 0.0, opacity[i]);
+  g.g_color[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+}
+
+int tile_bin_begin(int64_t n, const double* mean2d, const double* cov2d, const double* opacity,
+                   const ss_camera* cam, const ss_raster_settings* s, void* geom,
+                   int64_t* counts_host, cudaStream_t st) {
+  SS_TRY(check_raster(nullptr, cam, s));
+  Geom g = plan_geom(geom, n, cam, s);
+  SS_CUDA(cudaMemsetAsync(g.dev_counts, 0, 2 * sizeof(int64_t), st));
+  if (n > 0) {
+    tile_bin_setup_kernel<<<(unsigned)cdiv(n, 256), 256, 0, st>>>(n, mean2d, cov2d, opacity, g);
+    SS_CHECK_LAUNCH("tile_bin_setup_kernel");
+    rank_kernel<<<(unsigned)cdiv(n, 256), 256, 0, st>>>(make_cam(cam), *s, n, g);
+    SS_CHECK_LAUNCH("rank_kernel");
+    size_t qb = g.cub_scan_bytes;
+    SS_CUDA(cub::DeviceScan::InclusiveSum(g.cub_scan, qb, g.offsets, g.offsets + 1, (int)n, st));
+  }
+  finish_counts_kernel<<<1, 1, 0, st>>>(g, n);
+  SS_CHECK_LAUNCH("finish_counts_kernel");
+  if (counts_host)
+    SS_CUDA(cudaMemcpyAsync(counts_host, g.dev_counts, 2 * sizeof(int64_t),
+                            cudaMemcpyDeviceToHost, st));
+  return SS_OK;
+}
+
+int tile_bin_finish(int64_t n, const ss_camera* cam, const ss_raster_settings* s, void* geom,
+                    void* bins, int64_t pairs, cudaStream_t st) {
+  Geom g = plan_geom(geom, n, cam, s);
+  Bins b = plan_bins(bins, pairs);
+  const int ntx = ntiles_x(cam, s), nty = ntiles_y(cam, s);
+  const int64_t ntiles = (int64_t)ntx * nty;
+  SS_CUDA(cudaMemsetAsync(g.ranges, 0, ntiles * sizeof(int2), st));
+  if (pairs > 0) {
+    duplicate_kernel<<<(unsigned)cdiv(n, 256), 256, 0, st>>>(*s, ntx, n, g, b);
+    SS_CHECK_LAUNCH("duplicate_kernel");
+    size_t sb = b.cub_sort_bytes;
+    SS_CUDA(cub::DeviceRadixSort::SortPairs(b.cub_sort, sb, b.keys_in, b.keys_out, b.vals_in,
+                                            b.vals_out, (int)pairs, 0, key_bits(ntiles), st));
+    ranges_kernel<<<(unsigned)cdiv(pairs, 256), 256, 0, st>>>(pairs, b.keys_out, g.ranges);
+    SS_CHECK_LAUNCH("ranges_kernel");
+  }
+  return SS_OK;
+}
+
 }  // namespace ss
 
 using namespace ss;
@@ -840,6 +895,20 @@ int ss_raster_backward(const ss_cloud* cloud, const ss_camera* cam, const ss_ras
                        const ss_cloud_grads* grads, void* stream) {
   return raster_backward(cloud, cam, s, geom, bins, n_pairs, d_image, grads, 1,
                          as_stream(stream));
+}
+
+int ss_tile_bin_begin(int64_t n, const double* mean2d, const double* cov2d, const double* opacity,
+                      const ss_camera* cam, const ss_raster_settings* s, void* geom,
+                      int64_t* counts_host, void* stream) {
+  return tile_bin_begin(n, mean2d, cov2d, opacity, cam, s, geom, counts_host, as_stream(stream));
+}
+
+int ss_tile_bin_finish(int64_t n, const ss_camera* cam, const ss_raster_settings* s, void* geom,
+                       void* bins, int64_t n_pairs, int32_t* tile_ranges, int32_t* members,
+                       void* stream) {
+  SS_TRY(tile_bin_finish(n, cam, s, geom, bins, n_pairs, as_stream(stream)));
+  return ss_raster_tile_lists(cam, s, geom, bins, n_pairs, n, tile_ranges, members, nullptr,
+                              stream);
 }
 
 int ss_raster_tile_lists(const ss_camera* cam, const ss_raster_settings* s, const void* geom,

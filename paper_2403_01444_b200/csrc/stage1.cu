@@ -89,7 +89,7 @@ int ss_stage1_iter_grads(ss_stage1* st, const ss_camera* cam, const float* targe
   const ss_cloud tc = transformed(st);
   SS_TRY(raster_finish(&tc, cam, &st->settings, st->geom, st->bins, n_pairs, st->image,
                        st->alpha_map, nullptr, s));
-  SS_TRY(ss_render_loss(st->image, target, cam->height, cam->width, st->lambda_dssim,
+  SS_TRY(ss_render_loss(st->image, target, cam->height, cam->width, 3, st->lambda_dssim,
                         0.01 * 0.01, 0.03 * 0.03, st->loss_scratch, st->loss_dev, st->d_image,
                         st->status, stream));
   if (st->loss_history)

@@ -1,0 +1,260 @@
+"""Device-resident Stage-1 trainer: the hot loop of `process_frame`
+(pipeline.py:238-283) with every tensor in HBM and one library call per half
+iteration.
+
+    trainer = Stage1Trainer(prev_cloud, warm_cache, views)
+    losses = trainer.run()            # 150 iterations, reference view order
+    trainer.export_to(cache)          # parameters back into the reference-shaped cache
+
+Per iteration (pipeline.py:263-277): apply_ntc -> rasterize_forward ->
+render_loss -> rasterize_backward -> apply_ntc_backward -> lazy Adam, plus the
+view-space statistics of the last epoch.  The only host synchronisation is
+the tile-pair count that sizes the binning sort.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from .device import (DeviceCloud, camera_struct, empty_bytes, grid_struct, mlp_layout, mlp_struct,
+                     pack_params, pinned, ptr, require_cuda, settings_struct, stream, to_dev,
+                     unpack_params)
+from .errors import DataError
+from .types import Camera, GaussianCloud, HashGridConfig, LossConfig, RasterSettings
+
+
+@dataclass
+class Stage1Config:
+    """The Stage-1 slice of PipelineConfig (pipeline.py:40-86)."""
+
+    stage1_iterations: int = 150
+    ntc_lr: float = 0.002
+    seed: int = 0
+    raster: RasterSettings = field(default_factory=RasterSettings)
+    loss: LossConfig = field(default_factory=LossConfig)
+    rotate_sh: bool = True
+
+
+def inside_rows(grid: HashGridConfig, means: np.ndarray) -> np.ndarray:
+    """Rows the cache moves: all(lo <= mu <= hi) (transform.py:64-68); means
+    are frozen for a frame so this is per-frame setup, not per-iteration work."""
+    lo = np.asarray(grid.aabb_min, dtype=np.float64)
+    hi = np.asarray(grid.aabb_max, dtype=np.float64)
+    return np.flatnonzero(np.all((means >= lo) & (means <= hi), axis=1)).astype(np.int32)
+
+
+def view_order(seed: int, frame_index: int, n_views: int, iterations: int) -> list[int]:
+    """pipeline.py:251-256, :263, :278-279."""
+    rng = np.random.default_rng([seed, frame_index])
+    order = rng.permutation(n_views)
+    seq = []
+    for t in range(iterations):
+        seq.append(int(order[t % n_views]))
+        if (t + 1) % n_views == 0:
+            order = rng.permutation(n_views)
+    return seq
+
+
+class Stage1Trainer:
+    def __init__(self, prev_cloud, cache, views, cfg: Stage1Config | None = None,
+                 background=None, accumulate_stats: bool = True, history: int = 0):
+        dev = require_cuda()
+        self.lib = _lib.load()
+        self.cfg = cfg or Stage1Config()
+        self.dev = dev
+        grid = HashGridConfig.from_any(cache.grid)
+        self.grid_cfg = grid
+        cloud = prev_cloud if isinstance(prev_cloud, dict) else GaussianCloud.from_any(prev_cloud)
+        means_np = cloud["means"] if isinstance(cloud, dict) else cloud.means
+        self.cloud = DeviceCloud(cloud, dev)
+        n, K = self.cloud.n, self.cloud.sh_coeffs
+        if n == 0:
+            raise DataError("previous cloud is empty")
+        if len(views) == 0:
+            raise DataError("no training views")
+        # ---- views: cameras on the host, targets resident in HBM
+        self.cameras = [Camera.from_any(c) for c, _ in views]
+        self.cam_structs = [camera_struct(c) for c in self.cameras]
+        self.targets = [to_dev(t, dev=dev) for _, t in views]
+        self.settings = settings_struct(self.cfg.raster, background)
+        # ---- NTC parameters in the padded device layout
+        weights = [np.asarray(w) for w in cache.weights]
+        biases = [np.asarray(b) for b in cache.biases]
+        self.w_shapes = [w.shape for w in weights]
+        self.mlp = mlp_struct(weights[0].shape[0], weights[0].shape[1], len(weights) - 1)
+        self.layout = mlp_layout(self.mlp)
+        self.tables = to_dev(np.asarray(cache.tables), dev=dev)
+        self.params = to_dev(pack_params(weights, biases, self.layout), dev=dev)
+        nt, npar = self.tables.numel(), self.params.numel()
+        f32, f64 = dict(dtype=torch.float32, device=dev), dict(dtype=torch.float64, device=dev)
+        self.g_tables = torch.zeros(nt, **f32)
+        self.g_params = torch.zeros(npar, **f32)
+        self.m_tables = torch.zeros(nt, **f64)
+        self.v_tables = torch.zeros(nt, **f64)
+        self.m_params = torch.zeros(npar, **f64)
+        self.v_params = torch.zeros(npar, **f64)
+        self.row_mask = torch.zeros(grid.n_levels * grid.table_size, dtype=torch.uint8, device=dev)
+        self.step_dev = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.rows = to_dev(inside_rows(grid, means_np), dtype=torch.int32, dev=dev)
+        # ---- transformed cloud and per-view buffers
+        self.t_means = torch.empty(n, 3, **f32)
+        self.t_rot = torch.empty(n, 4, **f32)
+        self.t_sh = torch.empty(n, K, 3, **f32)
+        H = max(c.height for c in self.cameras)
+        W = max(c.width for c in self.cameras)
+        self.image = torch.empty(H * W * 3, **f32)
+        self.alpha = torch.empty(H * W, **f32)
+        self.d_image = torch.empty(H * W * 3, **f32)
+        self.d_means = torch.empty(n, 3, **f32)
+        self.d_rot = torch.empty(n, 4, **f32)
+        self.d_sh = torch.empty(n, K, 3, **f32)
+        self.viewspace = torch.empty(n, **f32)
+        self.contributed = torch.empty(n, dtype=torch.uint8, device=dev)
+        self.stats_norm = torch.zeros(n, **f32)
+        self.stats_count = torch.zeros(n, dtype=torch.int32, device=dev)
+        self.loss_dev = torch.zeros(1, **f64)
+        self.loss_hist = torch.zeros(max(1, history or self.cfg.stage1_iterations), **f64)
+        self.status = torch.zeros(1, dtype=torch.int32, device=dev)
+        geom = max(self.lib.ss_raster_geom_bytes(n, C.byref(cs), C.byref(self.settings))
+                   for cs in self.cam_structs)
+        lossb = max(self.lib.ss_loss_bytes(c.height, c.width, 3) for c in self.cameras)
+        self.geom = empty_bytes(geom, dev)
+        self.loss_scratch = empty_bytes(lossb, dev)
+        self.bins = None
+        self.bin_capacity = 0
+        self.counts = pinned(2)
+        self.flags = pinned(1, torch.int32)
+        # ---- the ABI struct
+        s = _lib.Stage1()
+        s.grid = grid_struct(grid)
+        s.mlp = self.mlp
+        s.settings = self.settings
+        s.lr, s.beta1, s.beta2, s.eps = self.cfg.ntc_lr, 0.9, 0.999, 1e-15  # optim.py:22-24
+        s.lambda_dssim = self.cfg.loss.lambda_dssim
+        s.rotate_sh = int(self.cfg.rotate_sh)
+        s.accumulate_stats = int(accumulate_stats)
+        s.src = self.cloud.struct()
+        s.n_in = int(self.rows.numel())
+        s.rows = ptr(self.rows)
+        for name, t in (("tables", self.tables), ("params", self.params),
+                        ("g_tables", self.g_tables), ("g_params", self.g_params),
+                        ("m_tables", self.m_tables), ("v_tables", self.v_tables),
+                        ("m_params", self.m_params), ("v_params", self.v_params),
+                        ("row_mask", self.row_mask), ("step_dev", self.step_dev),
+                        ("t_means", self.t_means), ("t_rotations", self.t_rot),
+                        ("t_sh", self.t_sh), ("image", self.image), ("alpha_map", self.alpha),
+                        ("d_image", self.d_image), ("d_means", self.d_means),
+                        ("d_rotations", self.d_rot), ("d_sh", self.d_sh),
+                        ("viewspace", self.viewspace), ("contributed", self.contributed),
+                        ("stats_norm", self.stats_norm), ("stats_count", self.stats_count),
+                        ("loss_dev", self.loss_dev), ("loss_history", self.loss_hist),
+                        ("status", self.status), ("geom", self.geom),
+                        ("loss_scratch", self.loss_scratch)):
+            setattr(s, name, ptr(t))
+        s.ntc_scratch = None
+        self.s = s
+        self.frame_begin()
+
+    # ------------------------------------------------------------------
+    def _call(self, fn, *args, what=""):
+        _lib.check(fn(*args), what or fn.__name__)
+
+    def frame_begin(self):
+        """clone_cache + reset_adam (pipeline.py:213-219): fresh moments, step 0."""
+        self._call(self.lib.ss_stage1_frame_begin, C.byref(self.s), stream())
+
+    def _ensure_bins(self, pairs: int, cam):
+        if pairs <= self.bin_capacity and self.bins is not None:
+            return
+        cap = max(int(pairs * 1.25) + 1024, 1 << 16)
+        nbytes = self.lib.ss_raster_bin_bytes(cap, self.cloud.n, C.byref(cam),
+                                              C.byref(self.settings))
+        self.bins = empty_bytes(nbytes, self.dev)
+        self.bin_capacity = cap
+        self.s.bins = ptr(self.bins)
+        self.s.bin_capacity = cap
+
+    def begin(self, view: int) -> int:
+        """apply_ntc + projection/depth sort/tile counts; returns the pair count."""
+        cam = self.cam_structs[view]
+        self._call(self.lib.ss_stage1_iter_begin, C.byref(self.s), C.byref(cam),
+                   ptr(self.counts), stream())
+        self.flags.copy_(self.status, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        _lib.check_flags(int(self.flags.item()), "stage1 loss")
+        return int(self.counts[1].item())
+
+    def finish(self, view: int, pairs: int, adam: bool = True, grad_scale: float = 1.0):
+        cam = self.cam_structs[view]
+        self._ensure_bins(pairs, cam)
+        tgt = ptr(self.targets[view])
+        if adam and grad_scale == 1.0:
+            self._call(self.lib.ss_stage1_iter_finish, C.byref(self.s), C.byref(cam), tgt, pairs,
+                       stream())
+        else:
+            self._call(self.lib.ss_stage1_iter_grads, C.byref(self.s), C.byref(cam), tgt, pairs,
+                       C.c_float(grad_scale), stream())
+            if adam:
+                self.apply_adam()
+
+    def apply_adam(self):
+        self._call(self.lib.ss_stage1_apply_adam, C.byref(self.s), stream())
+
+    def step(self, view: int):
+        pairs = self.begin(view)
+        self.finish(view, pairs)
+        return pairs
+
+    def run(self, iterations: int | None = None, frame_index: int = 1) -> np.ndarray:
+        """The Stage-1 loop (pipeline.py:262-279); returns the loss history."""
+        iters = self.cfg.stage1_iterations if iterations is None else iterations
+        if iters > self.loss_hist.numel():
+            self.loss_hist = torch.zeros(iters, dtype=torch.float64, device=self.dev)
+            self.s.loss_history = ptr(self.loss_hist)
+        order = view_order(self.cfg.seed, frame_index, len(self.cameras), iters)
+        stats_from = max(0, iters - len(self.cameras))
+        for t, v in enumerate(order):
+            self.s.accumulate_stats = int(t >= stats_from)
+            self.step(v)
+        self.flags.copy_(self.status, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        _lib.check_flags(int(self.flags.item()), "stage1 loss")
+        return self.loss_hist[:iters].cpu().numpy()
+
+    # ------------------------------------------------------------------
+    def last_loss(self) -> float:
+        return float(self.loss_dev.item())
+
+    def rendered_image(self, view: int) -> np.ndarray:
+        c = self.cameras[view]
+        return self.image[: c.height * c.width * 3].view(c.height, c.width, 3).cpu().numpy()
+
+    def transformed_cloud(self) -> GaussianCloud:
+        return GaussianCloud(self.t_means.cpu().numpy(), self.t_rot.cpu().numpy(),
+                             self.cloud.log_scales.cpu().numpy(),
+                             self.cloud.opacity_logits.cpu().numpy(), self.t_sh.cpu().numpy())
+
+    def ntc_grads(self):
+        """Current (un-stepped) NTC gradients in the reference layout."""
+        g = self.g_params.cpu().numpy()
+        ws, bs = unpack_params(g, self.w_shapes, self.layout)
+        tab = self.g_tables.view(self.tables.shape).cpu().numpy().astype(np.float64)
+        return tab, ws, bs
+
+    def export_to(self, cache) -> None:
+        """Write the device parameters back into a reference-shaped cache."""
+        cache.tables[:] = self.tables.cpu().numpy()
+        ws, bs = unpack_params(self.params.cpu().numpy(), self.w_shapes, self.layout)
+        for i in range(len(ws)):
+            cache.weights[i][:] = ws[i]
+            cache.biases[i][:] = bs[i]
+
+    def viewspace_stats(self):
+        """(norm_accum, view_count) of ViewspaceStats (adaptive.py:79-97)."""
+        return (self.stats_norm.cpu().numpy().astype(np.float64),
+                self.stats_count.cpu().numpy().astype(np.int64))

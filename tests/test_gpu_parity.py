@@ -1,0 +1,215 @@
+"""CUDA path vs the reference golden vectors and the CPU oracle (needs a B200).
+
+Tolerances (BASELINE.json north_star): hash indices, tile lists, sort order
+bit-exact; images max-abs <= 1e-4; gradients norm-relative <= 1e-3.
+"""
+
+import numpy as np
+import pytest
+
+import golden_io as G
+from oracle import stage1 as O
+
+pytestmark = pytest.mark.gpu
+
+IMG_TOL = 1e-4
+GRAD_TOL = 1e-3
+
+
+@pytest.fixture(scope="module")
+def P():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2403_01444_b200 as pkg
+    from paper_2403_01444_b200 import _lib, losses, ntc, rasterizer, transform, types
+
+    _lib.load()
+    return dict(pkg=pkg, ntc=ntc, rasterizer=rasterizer, transform=transform, losses=losses,
+                types=types, torch=torch)
+
+
+def _cache(P, d, hidden=64):
+    grid = P["types"].HashGridConfig.from_any(G.grid(d))
+    mlp = G.mlp(d)
+    c = P["ntc"].NeuralTransformationCache(grid, hidden_layers=len(mlp["weights"]) - 1,
+                                           hidden_dim=hidden, output_init="random")
+    c.tables[:] = d["tables"]
+    for i in range(len(mlp["weights"])):
+        c.weights[i][:] = mlp["weights"][i]
+        c.biases[i][:] = mlp["biases"][i]
+    return c
+
+
+@pytest.mark.parametrize("tag", ["small", "cfg1"])
+def test_encode_indices_bit_exact(P, tag):
+    d = G.load(f"encode_{tag}")
+    grid = P["types"].HashGridConfig.from_any(G.grid(d))
+    c = P["ntc"].NeuralTransformationCache(grid, hidden_layers=2, hidden_dim=64)
+    if "tables" in d:
+        c.tables[:] = d["tables"]
+    feats, ctx = c.encode(d["x"])
+    np.testing.assert_array_equal(ctx.corner_idx, d["idx"])
+    np.testing.assert_allclose(ctx.corner_w, d["w"], rtol=0, atol=2e-7)
+    if "feats" in d:
+        np.testing.assert_allclose(feats, d["feats"], rtol=1e-5, atol=1e-9)
+    _, _, touched = O.encode(G.grid(d), d["x"])
+    for l in range(grid.n_levels):
+        np.testing.assert_array_equal(ctx.touched[l], touched[l])
+
+
+def test_encode_outside_raises(P):
+    d = G.load("encode_small")
+    grid = P["types"].HashGridConfig.from_any(G.grid(d))
+    c = P["ntc"].NeuralTransformationCache(grid)
+    with pytest.raises(P["pkg"].DataError):
+        c.encode(np.array([[5.0, 0.0, 0.0]]))
+
+
+def test_ntc_forward_backward_golden(P):
+    d = G.load("ntc")
+    c = _cache(P, d)
+    d_mu, d_q, ctx = c.forward(d["x"])
+    np.testing.assert_allclose(d_mu, d["d_mu"], rtol=1e-4, atol=1e-6)
+    np.testing.assert_allclose(d_q, d["d_q"], rtol=1e-4, atol=1e-6)
+    grads, touched = c.backward(ctx, d["g_mu"], d["g_q"])
+    for k in grads:
+        assert G.norm_rel(grads[k], d[f"grad_{k}"]) <= GRAD_TOL, k
+    for k in touched:
+        np.testing.assert_array_equal(touched[k], d[f"touched_{k}"])
+
+
+def test_transform_golden(P):
+    d = G.load("transform")
+    c = _cache(P, d)
+    cloud = P["types"].GaussianCloud(**G.cloud(d))
+    out, ctx = P["transform"].apply_ntc(cloud, c)
+    np.testing.assert_array_equal(ctx.inside, d["inside"])
+    np.testing.assert_allclose(out.means, d["out_means"], atol=1e-5)
+    np.testing.assert_allclose(out.rotations, d["out_rotations"], atol=1e-5)
+    np.testing.assert_allclose(out.sh, d["out_sh"], atol=1e-5)
+    grads, _ = P["transform"].apply_ntc_backward(ctx, d["g_means"], d["g_rot"], d["g_sh"])
+    for k in grads:
+        assert G.norm_rel(grads[k], d[f"grad_{k}"]) <= GRAD_TOL, k
+
+
+@pytest.mark.parametrize("tag", ["default", "smooth"])
+def test_raster_golden(P, tag):
+    d = G.load(f"raster_{tag}")
+    R, T = P["rasterizer"], P["types"]
+    cloud = T.GaussianCloud(**G.cloud(d))
+    cam = T.Camera.from_any(G.camera(d))
+    s = T.RasterSettings(**G.settings(d))
+    out, ctx = R.rasterize_forward(cloud, cam, d["bg"], s)
+    np.testing.assert_array_equal(ctx.indices, d["indices"])
+    tiles = ctx.tiles
+    np.testing.assert_array_equal(np.array([t[:4] for t in tiles]).reshape(-1, 4), d["tile_rects"])
+    np.testing.assert_array_equal([len(t[4]) for t in tiles], d["tile_counts"])
+    np.testing.assert_array_equal(np.concatenate([t[4] for t in tiles]), d["tile_members"])
+    assert np.abs(out.image - d["image"]).max() <= IMG_TOL
+    assert np.abs(out.alpha_map - d["alpha"]).max() <= IMG_TOL
+    np.testing.assert_array_equal(out.per_gaussian_touch_count, d["touch"])
+    g = R.rasterize_backward(ctx, d["d_image"])
+    for k in ("d_means", "d_rotations", "d_log_scales", "d_opacity_logits", "d_sh"):
+        assert G.norm_rel(getattr(g, k), d[k]) <= GRAD_TOL, k
+    assert G.norm_rel(g.viewspace_grad_norm, d["viewspace"]) <= GRAD_TOL
+    np.testing.assert_array_equal(g.contributed, d["contributed"])
+
+
+def test_tile_bin_matches_reference_lists(P):
+    d = G.load("raster_default")
+    cloud = G.cloud(d)
+    cam = G.camera(d)
+    pj = O.project(cloud, cam)
+    s = G.settings(d)
+    tiles = P["rasterizer"].tile_bin(pj["mean2d"], pj["cov2d"], pj["opacity"], cam["width"],
+                                     cam["height"], s["tile_size"], s["skip_alpha"])
+    np.testing.assert_array_equal(np.concatenate([t[4] for t in tiles]), d["tile_members"])
+    np.testing.assert_array_equal(np.array([t[:4] for t in tiles]).reshape(-1, 4), d["tile_rects"])
+
+
+def test_render_loss_golden(P):
+    d = G.load("loss")
+    loss, grad = P["losses"].render_loss(d["x"], d["y"])
+    assert abs(loss - float(d["loss"])) <= 1e-6
+    assert G.norm_rel(grad, d["grad"]) <= 1e-4
+    assert np.abs(grad - d["grad"]).max() <= 1e-7
+
+
+def test_stage1_golden_two_iterations(P):
+    from paper_2403_01444_b200.stage1 import Stage1Config, Stage1Trainer
+
+    d = G.load("stage1")
+    c = _cache(P, d)
+    cams = [G.camera(d, "cam0_"), G.camera(d, "cam1_")]
+    views = [(cams[0], d["target0"]), (cams[1], d["target1"])]
+    tr = Stage1Trainer(G.cloud(d), c, views, Stage1Config(stage1_iterations=2))
+    pairs = tr.begin(0)
+    tr.finish(0, pairs, adam=False)
+    assert np.abs(tr.rendered_image(0) - d["image_first"]).max() <= IMG_TOL
+    l0 = tr.last_loss()
+    assert abs(l0 - d["losses"][0]) <= 1e-5 * abs(d["losses"][0]) + 1e-7
+    gt, gw, gb = tr.ntc_grads()
+    for l in range(gt.shape[0]):
+        assert G.norm_rel(gt[l], d[f"grad1_table_{l}"]) <= GRAD_TOL, l
+    for i in range(3):
+        assert G.norm_rel(gw[i], d[f"grad1_w_{i}"]) <= GRAD_TOL, i
+        assert G.norm_rel(gb[i], d[f"grad1_b_{i}"]) <= GRAD_TOL, i
+    tr.apply_adam()
+    tr.step(1)
+    l1 = tr.last_loss()
+    assert abs(l1 - d["losses"][1]) <= 1e-3 * abs(d["losses"][1])
+
+
+@pytest.mark.parametrize("deg", [0, 1, 2, 3])
+def test_raster_random_scenes_vs_oracle(P, deg):
+    from paper_2403_01444_b200 import scenes
+
+    sc = scenes.small_scene(seed=30 + deg, n=800, width=80, height=64, sh_degree=deg)
+    R, T = P["rasterizer"], P["types"]
+    cam = sc.cameras[1]
+    bg = np.array([0.2, 0.1, 0.3])
+    ref, rctx = O.render(sc.cloud, cam, bg)
+    out, ctx = R.rasterize_forward(T.GaussianCloud(**sc.cloud), T.Camera.from_any(cam), bg)
+    assert np.abs(out.image - ref["image"]).max() <= IMG_TOL
+    np.testing.assert_array_equal(ctx.indices, rctx["proj"]["indices"])
+    mem = np.concatenate([t[4] for t in ctx.tiles])
+    np.testing.assert_array_equal(mem, np.concatenate([t[4] for t in rctx["tiles"]]))
+    d_img = np.random.default_rng(deg).normal(size=out.image.shape)
+    g = R.rasterize_backward(ctx, d_img)
+    rg = O.render_backward(rctx, d_img)
+    for k, rk in (("d_means", "d_means"), ("d_rotations", "d_rotations"),
+                  ("d_log_scales", "d_log_scales"), ("d_opacity_logits", "d_opacity_logits"),
+                  ("d_sh", "d_sh")):
+        assert G.norm_rel(getattr(g, k), rg[rk]) <= GRAD_TOL, k
+
+
+def test_stage1_cfg0_single_step_vs_oracle(P):
+    """The parity config (BASELINE configs[0]): one full Stage-1 step, fp32."""
+    from paper_2403_01444_b200 import scenes
+    from paper_2403_01444_b200.stage1 import Stage1Config, Stage1Trainer
+
+    sc = scenes.config(0)
+    tables, mlp = O.init_ntc(sc.grid, output_init="random", seed=2)
+    tables = scenes.f32(np.random.default_rng(3).uniform(-0.02, 0.02, size=tables.shape))
+    moved = scenes.moved_cloud(sc.cloud, np.random.default_rng(1))
+    targets = [O.render(moved, c)[0]["image"] for c in sc.cameras]
+
+    class Cache:
+        grid = P["types"].HashGridConfig.from_any(sc.grid)
+
+    c = Cache()
+    c.tables, c.weights, c.biases = tables, mlp["weights"], mlp["biases"]
+    tr = Stage1Trainer(sc.cloud, c, list(zip(sc.cameras, targets)), Stage1Config())
+    pairs = tr.begin(0)
+    tr.finish(0, pairs, adam=False)
+    state = dict(grid=sc.grid, tables=tables.copy(), mlp=mlp,
+                 inside=O.inside_mask(sc.grid, sc.cloud["means"]), enc=None)
+    ref = O.stage1_iteration(state, sc.cloud, sc.cameras[0], targets[0], apply_adam=False)
+    assert np.abs(tr.rendered_image(0) - ref["image"]).max() <= IMG_TOL
+    assert abs(tr.last_loss() - ref["loss"]) <= 1e-5 * ref["loss"]
+    gt, gw, gb = tr.ntc_grads()
+    assert G.norm_rel(gt, ref["g_tables"]) <= GRAD_TOL
+    for i in range(3):
+        assert G.norm_rel(gw[i], ref["g_w"][i]) <= GRAD_TOL
+        assert G.norm_rel(gb[i], ref["g_b"][i]) <= GRAD_TOL
