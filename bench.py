@@ -1,7 +1,13 @@
 """Stage-1 benchmark (BASELINE.json metric): NTC train iterations/s at 1352x1014
-with 250k SH-3 Gaussians (config 1), plus render FPS (config 2) and roofline.
+with 250k SH-3 Gaussians (config 1), render FPS (config 2), roofline and the
+CPU baseline, as one JSON line.
 
-python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+    python bench.py [--gpus N --steps K --warmup W]           # B200 path
+    python bench.py --impl reference [--steps K --warmup W]   # CPU oracle port
+
+A "step" is one Stage-1 iteration (pipeline.py:263-277) over one view.  With N
+GPUs (torchrun) each iteration trains N views, one per rank, and all-reduces
+the NTC gradients over NCCL (view-sharded data parallelism, weak scaling).
 """
 
 from __future__ import annotations
@@ -10,7 +16,6 @@ import argparse
 import json
 import math
 import os
-import subprocess
 import sys
 import threading
 import time
@@ -20,31 +25,89 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+METRIC = "stage1_ntc_train_iters_per_s"
+UNIT = "iter/s"
+L2_FLUSH_BYTES = 256 << 20  # > 126 MB L2
+
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--quick", action="store_true")
+    ap.add_argument("--no-render", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
 
 
-def make_cache(scene, output_init="identity", seed=0):
-    from oracle import stage1 as O  # noqa: F401  (never used on the product path)
-    return None
+# ---------------------------------------------------------------- helpers
+class Clocks:
+    """Samples SM clocks and throttle reasons (NVML) while the timed region runs."""
+
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x2: "applications_clocks_setting", 0x1: "gpu_idle"}
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.stop = [], set(), threading.Event()
+        self.max_mhz = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # pragma: no cover - NVML missing
+            self.nv = None
+
+    def _run(self):
+        while not self.stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.05)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self.stop.set()
+        if self.nv is not None:
+            self.t.join()
+
+    def summary(self):
+        s = sorted(self.samples)
+        return {"sm_mhz": float(np.median(s)) if s else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(s)}
 
 
-def build_problem(cfg_idx):
-    """Scene, an identity-initialised NTC (ntc.py:100-128 init) and targets rendered
-    on the device from the seeded motion field."""
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d["hbm_gbs"], d.get("bf16_tflops_sustained", d["bf16_tflops"]), "measured"
+    return 6650.0, 1590.0, "fallback"
+
+
+def build_problem(cfg_idx, targets_on_device=True):
+    """Scene, an identity-initialised NTC (ntc.py:100-128) and targets rendered on
+    the device from the seeded rigid + sinusoidal motion field (synthetic data)."""
     from paper_2403_01444_b200 import scenes
+    from paper_2403_01444_b200.device import DeviceCloud
     from paper_2403_01444_b200.ntc import NeuralTransformationCache
     from paper_2403_01444_b200.rasterizer import render_device
-    from paper_2403_01444_b200.device import DeviceCloud
     from paper_2403_01444_b200.types import HashGridConfig
 
     sc = scenes.config(cfg_idx)
@@ -52,52 +115,271 @@ def build_problem(cfg_idx):
     moved = scenes.moved_cloud(sc.cloud, np.random.default_rng(7), axis=(0.3, 1.0, 0.2),
                                deg=1.5, shift=(0.01, -0.005, 0.008))
     dm = DeviceCloud(moved)
-    targets = []
-    for cam in sc.cameras:
-        img = render_device(dm, cam, None, want_touch=False)[0]
-        targets.append(img)
+    targets = [render_device(dm, cam, None, want_touch=False)[0] for cam in sc.cameras]
     return sc, cache, targets
 
 
+# algorithmic bytes per phase: units x bytes/unit
+def phase_bytes(phase, n, n_in, K, pairs, P, ltf):
+    return {
+        "ntc_forward_transform": n_in * (12 + 16 + 12 * K + 12 + 16 + 12 * (K - 1)) + 4 * ltf,
+        "project": n * (12 + 16 + 12 + 4 + 12 * K) + n * 80,
+        "blend_forward": P * 24 + pairs * 52,
+        "loss": P * 12 * 3 + P * 12,
+        "blend_backward": P * 20 + pairs * 52 + n * 36,
+        "gaussian_backward": n * (12 + 16 + 12 + 4 + 12 * K + 36) + n * (12 + 16 + 12 * K + 5),
+        "ntc_backward": n_in * (12 + 16 + 12 * K + 12 + 16 + 12 * K) + 3 * 4 * ltf,
+        "tile_sort": pairs * 16 * 2,
+        "adam": ltf * (4 * 3 + 16 * 2 + 1 / 2),
+    }.get(phase)
+
+
+def cpu_baseline_sample(sc, cache, target, rows=(32, 64)):
+    """The float64 oracle port timed on this host: one Stage-1 iteration of the
+    same workload restricted to two horizontal image bands (full per-Gaussian
+    work, all tiles of the band), extrapolated linearly to the full height."""
+    from threadpoolctl import threadpool_limits
+
+    from oracle import stage1 as O
+
+    grid = dict(levels=cache.grid.n_levels, features=cache.grid.n_features,
+                log2_table=cache.grid.table_size_log2, base=cache.grid.base_resolution,
+                growth=cache.grid.growth_factor, lo=cache.grid.aabb_min, hi=cache.grid.aabb_max)
+    cam = dict(sc.cameras[0])
+    tgt = target.cpu().numpy().astype(np.float64)
+    H = cam["height"]
+    times = []
+    with threadpool_limits(1):
+        for r in rows:
+            y0 = H // 2 - r // 2
+            c = dict(cam, height=r, cy=cam["cy"] - y0)
+            mlp = dict(weights=[w.copy() for w in cache.weights],
+                       biases=[b.copy() for b in cache.biases])
+            state = dict(grid=grid, tables=cache.tables.copy(), mlp=mlp,
+                         inside=O.inside_mask(grid, sc.cloud["means"]), enc=None)
+            O.encode  # the encode context is cached per frame (pipeline.py:264-266)
+            state["enc"] = O.encode(grid, sc.cloud["means"][state["inside"]])
+            t0 = time.perf_counter()
+            O.stage1_iteration(state, sc.cloud, c, tgt[y0:y0 + r])
+            times.append(time.perf_counter() - t0)
+    slope = (times[1] - times[0]) / (rows[1] - rows[0])
+    full = times[0] + slope * (H - rows[0])
+    return {"value": 1.0 / full, "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"oracle/stage1.py float64 port, 1 thread: one Stage-1 iteration of "
+                      f"{sc.name} view 0 on {rows[0]}- and {rows[1]}-row bands "
+                      f"({times[0]:.1f} s, {times[1]:.1f} s), linear extrapolation to {H} rows "
+                      f"= {full:.1f} s/iter"}
+
+
+# ---------------------------------------------------------------- reference arm
+def run_reference(a):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import torch  # noqa: F401  (only for the device-free scene generator types)
+    from threadpoolctl import threadpool_limits
+
+    from oracle import stage1 as O
+    from paper_2403_01444_b200 import scenes
+
+    sc = scenes.config(a.config)
+    grid = sc.grid
+    tables, mlp = O.init_ntc(grid, output_init="identity", seed=0)
+    cam = dict(sc.cameras[0])
+    H = cam["height"]
+    rows = 32
+    cores = os.cpu_count() or 1
+    y0 = H // 2 - rows // 2
+    c = dict(cam, height=rows, cy=cam["cy"] - y0)
+    rng = np.random.default_rng(0)
+    tgt = rng.uniform(size=(rows, cam["width"], 3))
+    state = dict(grid=grid, tables=tables, mlp=mlp,
+                 inside=O.inside_mask(grid, sc.cloud["means"]), enc=None)
+    state["enc"] = O.encode(grid, sc.cloud["means"][state["inside"]])
+    # per-row cost measured once on a second band (not part of each step)
+    with threadpool_limits(cores):
+        t0 = time.perf_counter()
+        O.stage1_iteration(state, sc.cloud, dict(cam, height=2 * rows, cy=cam["cy"] - y0),
+                           rng.uniform(size=(2 * rows, cam["width"], 3)))
+        t_2r = time.perf_counter() - t0
+        step_times = []
+        for k in range(a.warmup + a.steps):
+            t0 = time.perf_counter()
+            O.stage1_iteration(state, sc.cloud, c, tgt)
+            if k >= a.warmup:
+                step_times.append(time.perf_counter() - t0)
+    t_r = float(np.mean(step_times))
+    slope = (t_2r - t_r) / rows
+    full = t_r + slope * (H - rows)
+    v = 1.0 / full
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": a.gpus,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1000.0 * full,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": sc.name, "gaussians": int(len(sc.cloud["means"])),
+                       "resolution": [cam["width"], H], "sh_degree": sc.sh_degree},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
+                             "sample": f"each step = one Stage-1 iteration of {sc.name} view 0 "
+                                       f"on a {rows}-row band ({t_r:.1f} s); per-row cost from "
+                                       f"a {2 * rows}-row band; linear extrapolation to {H} "
+                                       f"rows"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- B200 arm
 def main():
     a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+        return
     import torch
+    import torch.distributed as dist
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    if a.impl == "reference":
-        if rank == 0:
-            print(json.dumps({"impl": "reference", "unavailable": "not yet wired"}))
-        return
-    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2403_01444_b200 import _lib
-    from paper_2403_01444_b200.stage1 import Stage1Config, Stage1Trainer
+    from paper_2403_01444_b200.dist import ViewShardedStage1
+    from paper_2403_01444_b200.stage1 import Stage1Config
 
     lib = _lib.load()
     sc, cache, targets = build_problem(a.config)
     views = list(zip(sc.cameras, targets))
-    tr = Stage1Trainer(sc.cloud, cache, views, Stage1Config())
-    order = [k % len(views) for k in range(a.warmup + a.steps)]
+    n_views = len(views)
+    tr = ViewShardedStage1(sc.cloud, cache, views, Stage1Config(), rank=rank, world=world)
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device="cuda")
+
+    def batch(k):  # views of iteration k: world consecutive views of a fixed cycle
+        return [(k * world + r) % n_views for r in range(world)]
+
     for k in range(a.warmup):
-        tr.step(order[k])
+        tr.step(batch(k))
     torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    lib.ss_profile_enable(1)
+    names = [lib.ss_profile_name(i).decode() for i in range(13)]
+    phase_ms = {n: [] for n in names}
+    buf = (np.ctypeslib.ctypes.c_double * 13)()
+    step_ms, pairs = [], []
     l0 = lib.ss_launch_count()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    pairs = []
-    ev0.record()
-    for k in range(a.steps):
-        pairs.append(tr.step(order[a.warmup + k]))
-    ev1.record()
-    torch.cuda.synchronize()
-    ms = ev0.elapsed_time(ev1) / a.steps
+    with Clocks(local) as clk:
+        for k in range(a.steps):
+            flush.fill_(k & 0xFF)  # L2 flush between timed steps (outside the events)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            pairs.append(tr.step(batch(a.warmup + k)))
+            e1.record()
+            e1.synchronize()
+            step_ms.append(e0.elapsed_time(e1))
+            lib.ss_profile_read(buf, 13)
+            for i, n in enumerate(names):
+                if buf[i] >= 0:
+                    phase_ms[n].append(buf[i])
     launches = lib.ss_launch_count() - l0
-    line = {"metric": "stage1_iters_per_s", "value": 1000.0 / ms, "unit": "iter/s",
-            "n_gpus": world, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms,
-            "higher_is_better": True, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": sc.name, "gaussians": len(sc.cloud["means"]),
-                       "resolution": [1352, 1014], "mean_pairs": float(np.mean(pairs))},
-            "gpu_launches": launches, "loss": tr.last_loss()}
-    print(json.dumps(line))
+    lib.ss_profile_enable(0)
+    ms = float(np.mean(step_ms))
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = world * 1000.0 / ms  # view-iterations per second over the whole job
+    hbm, tc, peak_kind = peaks()
+    n = len(sc.cloud["means"])
+    K = sc.cloud["sh"].shape[1]
+    P = sc.cameras[0]["width"] * sc.cameras[0]["height"]
+    ltf = cache.tables.size
+    mean_pairs = float(np.mean(pairs))
+    n_in = int(tr.trainer.rows.numel())
+    phases = {}
+    for nm, v in phase_ms.items():
+        if v:
+            b = phase_bytes(nm, n, n_in, K, mean_pairs, P, ltf)
+            m = float(np.mean(v))
+            phases[nm] = {"ms": m, "share": m / ms,
+                          "gbs": (b / (m * 1e-3) / 1e9) if b else None}
+    dom = max(phases, key=lambda k: phases[k]["ms"])
+    dom_bytes = phase_bytes(dom, n, n_in, K, mean_pairs, P, ltf)
+    achieved = dom_bytes / (phases[dom]["ms"] * 1e-3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get(dom)
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": sc.name, "gaussians": n, "sh_degree": sc.sh_degree,
+                       "resolution": [sc.cameras[0]["width"], sc.cameras[0]["height"]],
+                       "views": n_views, "views_per_iteration": world,
+                       "parallelism": f"view-sharded dp{world}" if world > 1 else "single",
+                       "mean_tile_pairs": mean_pairs,
+                       "l2": "flushed between timed steps (256 MB write)",
+                       "ntc": "16 levels x 2 features, 2^15 rows, MLP 32-64-64-7 fp32"},
+            "gpu_launches": int(launches),
+            "loss_last": tr.trainer.last_loss(),
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm,
+                         "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic,
+                         "peak_source": f"{peak_kind} hbm_gbs (MEASURED_PEAKS.json)"},
+            "phases": phases}
+    # ---- end to end through the public API with host buffers
+    if not a.no_e2e:
+        host_t = [t.cpu().pin_memory() for t in targets]
+        for k in range(2):
+            tr.step_from_host(batch(k), host_t)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for k in range(a.steps):
+            tr.step_from_host(batch(k), host_t)
+        e2e_s = (time.perf_counter() - t0) / a.steps
+        if world > 1:
+            t = torch.tensor([e2e_s], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_s = float(t.item())
+        line["e2e"] = {"value": world / e2e_s, "unit": UNIT,
+                       "h2d_bytes_per_step": int(targets[0].numel() * 4),
+                       "d2h_bytes_per_step": 8 + 16 + 4,
+                       "path": "ViewShardedStage1.step_from_host: pinned target H2D + "
+                               "iteration + loss D2H"}
+    line["clocks"] = clk.summary()
+    # ---- render-only throughput (config 2) and the CPU baseline: rank 0, N = 1
+    if rank == 0 and world == 1 and not a.no_render:
+        line["render"] = render_fps(a)
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline_sample(sc, cache, targets[0])
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def render_fps(a):
+    """Config 2: NTC transform + rasterize_forward of 300k SH-3 Gaussians per view."""
+    import torch
+
+    from paper_2403_01444_b200.stage1 import Stage1Config, Stage1Trainer
+
+    sc, cache, targets = build_problem(2)
+    tr = Stage1Trainer(sc.cloud, cache, list(zip(sc.cameras, targets)), Stage1Config())
+    for v in range(3):
+        tr.render(v)
+    torch.cuda.synchronize()
+    times = []
+    for r in range(2):
+        for v in range(len(sc.cameras)):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            tr.render(v)
+            e1.record()
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1))
+    ms = float(np.mean(times))
+    return {"metric": "render_fps", "value": 1000.0 / ms, "unit": "frames/s", "ms_per_frame": ms,
+            "workload": "cfg2: 300k SH-3 Gaussians, 1352x1014, NTC transform + forward, "
+                        "20 views x 2, L2 not flushed"}
 
 
 if __name__ == "__main__":

@@ -114,6 +114,12 @@ int32_t ss_version(void);
 size_t ss_struct_size(int32_t which);
 /* number of kernel launches issued by this library since load (telemetry) */
 int64_t ss_launch_count(void);
+/* Phase timing: when enabled, CUDA events are recorded on the launching
+ * stream around each hot-path phase; ss_profile_read returns the ms of the
+ * last instance of each phase (-1 when not run since the previous read). */
+int ss_profile_enable(int32_t on);
+const char* ss_profile_name(int32_t phase);
+int ss_profile_read(double* ms, int32_t n);
 
 /* ------------------------------------------------------------------ */
 /* NTC: hash-grid encode / decoder / lazy Adam   (ntc.py, optim.py)    */

@@ -48,11 +48,12 @@ def gen_encode(R):
     rng = np.random.default_rng(101)
     out = {}
     for tag, grid in (
+        # box corners exactly representable in float32 so the face points stay inside
         ("small", dict(levels=4, features=2, log2_table=10, base=4, growth=1.5,
-                       lo=(-1.1, -0.9, -1.3), hi=(1.2, 1.0, 0.8))),
+                       lo=(-1.125, -0.875, -1.25), hi=(1.25, 1.0, 0.75))),
         ("cfg1", dict(levels=16, features=2, log2_table=15, base=16,
                       growth=scenes.growth_for(16, 2048, 16),
-                      lo=(-3.7, -3.2, -3.9), hi=(3.5, 3.6, 3.1))),
+                      lo=(-3.75, -3.25, -3.875), hi=(3.5, 3.625, 3.125))),
     ):
         lo, hi = np.array(grid["lo"]), np.array(grid["hi"])
         x = scenes.f32(rng.uniform(lo, hi, size=(1500, 3)))

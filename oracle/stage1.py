@@ -314,16 +314,18 @@ def sh_basis_jac(d, deg):
 
 _PERM = np.array([[0.0, 1.0, 0.0], [0.0, 0.0, 1.0], [1.0, 0.0, 0.0]])  # sh.py:30-32
 
-# least-squares sample set for band rotations of degree 2-3 (oracle-only)
-_LS_DIRS = None
+# sample directions for band rotations of degree 2-3 (oracle-only; independent
+# of the CUDA library's own set -- M does not depend on the choice)
+_LS_DIRS = {}
 
 
-def _ls_dirs():
-    global _LS_DIRS
-    if _LS_DIRS is None:
-        r = np.random.default_rng(20240302).normal(size=(64, 3))
-        _LS_DIRS = r / np.linalg.norm(r, axis=1, keepdims=True)
-    return _LS_DIRS
+def _ls_dirs(l):
+    if l not in _LS_DIRS:
+        r = np.random.default_rng(20240302 + l).normal(size=(2 * l + 1, 3))
+        d = r / np.linalg.norm(r, axis=1, keepdims=True)
+        assert np.linalg.cond(sh_basis(d, l)[:, _band(l)]) < 1e3
+        _LS_DIRS[l] = d
+    return _LS_DIRS[l]
 
 
 def _band(l):
@@ -334,11 +336,11 @@ def sh_band_rotation(rot, l):
     """(..., 2l+1, 2l+1) M with f'(d) = f(R^T d) coefficient-wise.
 
     l = 1 is the reference's P R P^T (sh.py:84-109).  l = 2, 3 solve the same
-    identity in least squares over a fixed direction set (extension).
+    identity exactly on 2l+1 fixed directions (extension).
     """
     if l == 1:
         return _PERM @ rot @ _PERM.T
-    s = _ls_dirs()
+    s = _ls_dirs(l)
     ys = sh_basis(s, l)[:, _band(l)]  # (n, 2l+1)
     pinv = np.linalg.pinv(ys)
     e = np.einsum("...ji,kj->...ki", rot, s)  # R^T s_k
@@ -350,7 +352,7 @@ def sh_band_rotation_vjp(rot, l, g_m):
     """dL/dR from dL/dM for sh_band_rotation; sh.py:103-109 for l = 1."""
     if l == 1:
         return _PERM.T @ g_m @ _PERM
-    s = _ls_dirs()
+    s = _ls_dirs(l)
     pinv = np.linalg.pinv(sh_basis(s, l)[:, _band(l)])
     e = np.einsum("...ji,kj->...ki", rot, s)
     jac = sh_basis_jac(e, l)[..., _band(l), :]  # (..., n, 2l+1, 3)
@@ -534,17 +536,16 @@ def tile_lists(mean2d, cov2d, opacity, width, height, ts, skip):
     in depth-rank order; rasterizer.py:107-175 (vectorised binning)."""
     rect, vis = tile_rects(mean2d, cov2d, opacity, width, height, ts, skip)
     ntx = (width + ts - 1) // ts
-    ranks, tids = [], []
-    for i in np.flatnonzero(vis):
-        x0, x1, y0, y1 = rect[i]
-        ty, tx = np.mgrid[y0:y1 + 1, x0:x1 + 1]
-        t = (ty * ntx + tx).ravel()
-        tids.append(t)
-        ranks.append(np.full(len(t), i, dtype=np.int64))
-    if not tids:
+    idx = np.flatnonzero(vis)
+    if len(idx) == 0:
         return []
-    tids = np.concatenate(tids)
-    ranks = np.concatenate(ranks)
+    x0, x1, y0, y1 = rect[idx].T
+    wx = x1 - x0 + 1
+    cnt = wx * (y1 - y0 + 1)
+    ranks = np.repeat(idx, cnt)  # emitted in rank order, tiles row-major per splat
+    local = np.arange(cnt.sum()) - np.repeat(np.cumsum(cnt) - cnt, cnt)
+    wxr = np.repeat(wx, cnt)
+    tids = (np.repeat(y0, cnt) + local // wxr) * ntx + np.repeat(x0, cnt) + local % wxr
     order = np.lexsort((ranks, tids))
     tids, ranks = tids[order], ranks[order]
     starts = np.flatnonzero(np.r_[True, tids[1:] != tids[:-1]])

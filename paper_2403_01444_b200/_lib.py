@@ -90,6 +90,9 @@ SIGNATURES = [
     ("ss_version", I32, []),
     ("ss_struct_size", SZ, [I32]),
     ("ss_launch_count", I64, []),
+    ("ss_profile_enable", I32, [I32]),
+    ("ss_profile_name", C.c_char_p, [I32]),
+    ("ss_profile_read", I32, [C.POINTER(D), I32]),
     ("ss_mlp_get_layout", I32, [PMlp, C.POINTER(MlpLayout)]),
     ("ss_ntc_encode", I32, [PGrid, I64, P, P, P, P, P]),
     ("ss_ntc_touched", I32, [PGrid, I64, P, P, P, P]),

@@ -211,3 +211,15 @@ int raster_backward(const ss_cloud* cl, const ss_camera* cam, const ss_raster_se
                     void* geom, void* bins, int64_t pairs, const float* d_image,
                     const ss_cloud_grads* grads, int full, cudaStream_t st);
 }  // namespace ss
+
+// ---------------------------------------------------------------- phase timing
+// CUDA events recorded on the launching stream around each hot-path phase when
+// enabled with ss_profile_enable(1); read back with ss_profile_read().
+namespace ss {
+enum Phase {
+  PH_NTC_FWD = 0, PH_PROJECT, PH_DEPTH_SORT, PH_RANK_SCAN, PH_DUPLICATE, PH_TILE_SORT,
+  PH_RANGES, PH_BLEND_FWD, PH_LOSS, PH_BLEND_BWD, PH_GAUSS_BWD, PH_NTC_BWD, PH_ADAM, PH_COUNT
+};
+void prof_begin(int phase, cudaStream_t s);
+void prof_end(int phase, cudaStream_t s);
+}  // namespace ss

@@ -146,3 +146,53 @@ int ss_mlp_get_layout(const ss_mlp* mlp, ss_mlp_layout* out) {
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------- phase timing
+namespace ss {
+static bool g_prof = false;
+static cudaEvent_t g_ev[2 * PH_COUNT];
+static bool g_ev_ready = false, g_used[PH_COUNT];
+static const char* kPhaseNames[PH_COUNT] = {
+    "ntc_forward_transform", "project", "depth_sort", "rank_scan", "duplicate", "tile_sort",
+    "ranges", "blend_forward", "loss", "blend_backward", "gaussian_backward",
+    "ntc_backward", "adam"};
+
+void prof_begin(int phase, cudaStream_t s) {
+  if (!g_prof) return;
+  if (!g_ev_ready) {
+    for (auto& e : g_ev) cudaEventCreate(&e);
+    g_ev_ready = true;
+  }
+  cudaEventRecord(g_ev[2 * phase], s);
+}
+void prof_end(int phase, cudaStream_t s) {
+  if (!g_prof || !g_ev_ready) return;
+  cudaEventRecord(g_ev[2 * phase + 1], s);
+  g_used[phase] = true;
+}
+}  // namespace ss
+
+extern "C" {
+int ss_profile_enable(int32_t on) {
+  ss::g_prof = on != 0;
+  for (bool& u : ss::g_used) u = false;
+  return SS_OK;
+}
+const char* ss_profile_name(int32_t phase) {
+  return phase >= 0 && phase < ss::PH_COUNT ? ss::kPhaseNames[phase] : "";
+}
+/* ms of the last recorded instance of each phase (-1 if not recorded since the
+ * previous read); synchronises on the recorded events. */
+int ss_profile_read(double* ms, int32_t n) {
+  for (int p = 0; p < n && p < ss::PH_COUNT; ++p) {
+    ms[p] = -1.0;
+    if (!ss::g_used[p]) continue;
+    float t = 0.f;
+    SS_CUDA(cudaEventSynchronize(ss::g_ev[2 * p + 1]));
+    SS_CUDA(cudaEventElapsedTime(&t, ss::g_ev[2 * p], ss::g_ev[2 * p + 1]));
+    ms[p] = t;
+    ss::g_used[p] = false;
+  }
+  return SS_OK;
+}
+}

@@ -203,6 +203,7 @@ int ss_render_loss(const float* image, const float* target, int32_t height, int3
   lp.up = -lam / (2.0 * (double)lp.Hv * lp.Wv * channels);
   double* sums = static_cast<double*>(scratch);
   float* maps = reinterpret_cast<float*>(static_cast<char*>(scratch) + align_up(2 * sizeof(double)));
+  prof_begin(PH_LOSS, st);
   SS_CUDA(cudaMemsetAsync(sums, 0, 2 * sizeof(double), st));
   dim3 blk(BX, BY);
   dim3 g1((unsigned)cdiv(lp.Wv, BX), (unsigned)cdiv(lp.Hv, BY), channels);
@@ -213,6 +214,7 @@ int ss_render_loss(const float* image, const float* target, int32_t height, int3
   SS_CHECK_LAUNCH("ssim_grad_kernel");
   loss_finalize_kernel<<<1, 1, 0, st>>>(lp, sums, loss_dev, status);
   SS_CHECK_LAUNCH("loss_finalize_kernel");
+  prof_end(PH_LOSS, st);
   return SS_OK;
 }
 

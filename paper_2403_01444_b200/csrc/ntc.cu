@@ -879,9 +879,11 @@ struct FwdLaunch {
     const size_t smem = Lay<IN, NL>::TOTAL * sizeof(float);
     auto k = ntc_forward_kernel<IN, NL>;
     SS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    prof_begin(PH_NTC_FWD, st);
     k<<<(unsigned)cdiv(n, 128), 128, smem, st>>>(*g, n, means, rows, tables, params, out7, feats,
                                                   src, rotate_sh, tm, tr, ts, status);
     SS_CHECK_LAUNCH("ntc_forward_kernel");
+    prof_end(PH_NTC_FWD, st);
     return SS_OK;
   }
 };
@@ -908,9 +910,11 @@ struct BwdLaunch {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int64_t chunks = cdiv(n, kChunk);
     const unsigned grid = (unsigned)std::min<int64_t>(chunks, sms);
+    prof_begin(PH_NTC_BWD, st);
     k<<<grid, kChunk, smem, st>>>(*g, n, means, rows, tables, params, g_out7, src, rotate_sh, dm,
                                   dr, ds, g_tables, g_params);
     SS_CHECK_LAUNCH("ntc_backward_kernel");
+    prof_end(PH_NTC_BWD, st);
     return SS_OK;
   }
 };
@@ -1046,10 +1050,12 @@ int ss_adam_step(int64_t n_table, float* tables, float* g_tables, double* m_tabl
   const int64_t total = n_table + n_params;
   if (total > 0) {
     const unsigned blocks = (unsigned)std::min<int64_t>(cdiv(total, 256), 148 * 8);
+    prof_begin(PH_ADAM, st);
     adam_kernel<<<blocks, 256, 0, st>>>(n_table, tables, g_tables, m_tables, v_tables, row_mask,
                                         row_width, n_params, params, g_params, m_params,
                                         v_params, step_dev, lr, beta1, beta2, eps, zero_grads);
     SS_CHECK_LAUNCH("adam_kernel");
+    prof_end(PH_ADAM, st);
   }
   increment_kernel<<<1, 1, 0, st>>>(step_dev);
   SS_CHECK_LAUNCH("increment_kernel");

@@ -352,6 +352,7 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_fwd_kernel(
   const int x0 = (tile % bp.ntx) * TS, y0 = (tile / bp.ntx) * TS;
   const int2 range = g.ranges[tile];
   float T[PPT], C[PPT][3];
+  double logT[PPT];  // float64 log-transmittance, touch counting with skip_alpha = 0 only
   int last[PPT];
   bool done[PPT];
   float lx[PPT], ly[PPT];
@@ -361,6 +362,7 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_fwd_kernel(
     lx[p] = (float)(li % TS);
     ly[p] = (float)(li / TS);
     T[p] = 1.f;
+    logT[p] = 0.0;
     C[p][0] = C[p][1] = C[p][2] = 0.f;
     last[p] = 0;
     done[p] = (x0 + li % TS >= bp.W) || (y0 + li / TS >= bp.H);
@@ -393,7 +395,24 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_fwd_kernel(
         float G, og;
         const float a = pair_alpha(bp, dx, dy, co, s_rank[k], lx[p] + x0, ly[p] + y0, g.r_mean,
                                    g.r_conop_d, G, og);
-        if (a == 0.f) continue;
+        // Touch counts (rasterizer.py:279) count weight = alpha T_before > 0 in
+        // float64.  With skip_alpha = 0 that includes alphas and transmittances far
+        // below the float32 range (glibc keeps denormals down to 2^-1075), so that
+        // mode tracks log(alpha) + log(T) in float64; the colour is unaffected.
+        const bool exact_touch = TOUCH && bp.skip_d == 0.0;
+        const double lim = -745.1332191019412;  // ln(2^-1075)
+        if (a == 0.f) {
+          if (exact_touch) {
+            const double mh = (double)co.x * dx * dx + (double)co.y * dx * dy + (double)co.z * dy * dy;
+            const double la = -0.5 * mh + log((double)co.w);
+            if (-0.5 * mh > lim && la > lim && la + logT[p] > lim) ++contrib;
+          }
+          continue;
+        }
+        if (exact_touch) {
+          if (log((double)a) + logT[p] > lim) ++contrib;
+          logT[p] += log1p(-(double)a);
+        }
         const float4 col = s_col[k];
         const float w = a * T[p];
         C[p][0] = fmaf(w, col.x, C[p][0]);
@@ -401,7 +420,7 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_fwd_kernel(
         C[p][2] = fmaf(w, col.z, C[p][2]);
         T[p] *= 1.f - a;
         last[p] = b - range.x + k + 1;
-        ++contrib;
+        if (!exact_touch) ++contrib;
         if (T[p] < bp.stop) done[p] = true;  // later splats fail T_before >= stop
       }
       if (TOUCH) {
@@ -727,12 +746,17 @@ int raster_begin(const ss_cloud* cl, const ss_camera* cam, const ss_raster_setti
   const CamD cd = make_cam(cam);
   SS_CUDA(cudaMemsetAsync(g.dev_counts, 0, 2 * sizeof(int64_t), st));
   if (n > 0) {
+    prof_begin(PH_PROJECT, st);
     preprocess_kernel<<<(unsigned)cdiv(n, 256), 256, 0, st>>>(cd, *cl, g);
     SS_CHECK_LAUNCH("preprocess_kernel");
+    prof_end(PH_PROJECT, st);
+    prof_begin(PH_DEPTH_SORT, st);
     size_t sb = g.cub_sort_bytes;
     SS_CUDA(cub::DeviceRadixSort::SortPairs(g.cub_sort, sb, g.key_in, g.key_out, g.idx_in,
                                             g.order, (int)n, 0, 64, st));
     g_launches.fetch_add(4);
+    prof_end(PH_DEPTH_SORT, st);
+    prof_begin(PH_RANK_SCAN, st);
     rank_kernel<<<(unsigned)cdiv(n, 256), 256, 0, st>>>(cd, *s, n, g);
     SS_CHECK_LAUNCH("rank_kernel");
     size_t qb = g.cub_scan_bytes;
@@ -741,6 +765,7 @@ int raster_begin(const ss_cloud* cl, const ss_camera* cam, const ss_raster_setti
   }
   finish_counts_kernel<<<1, 1, 0, st>>>(g, n);
   SS_CHECK_LAUNCH("finish_counts_kernel");
+  if (n > 0) prof_end(PH_RANK_SCAN, st);
   if (counts_host)
     SS_CUDA(cudaMemcpyAsync(counts_host, g.dev_counts, 2 * sizeof(int64_t),
                             cudaMemcpyDeviceToHost, st));
@@ -762,20 +787,29 @@ int raster_finish(const ss_cloud* cl, const ss_camera* cam, const ss_raster_sett
   }
   SS_CUDA(cudaMemsetAsync(g.ranges, 0, ntiles * sizeof(int2), st));
   if (pairs > 0) {
+    prof_begin(PH_DUPLICATE, st);
     duplicate_kernel<<<(unsigned)cdiv(n, 256), 256, 0, st>>>(*s, ntx, n, g, b);
     SS_CHECK_LAUNCH("duplicate_kernel");
+    prof_end(PH_DUPLICATE, st);
+    prof_begin(PH_TILE_SORT, st);
     size_t sb = b.cub_sort_bytes;
     SS_CUDA(cub::DeviceRadixSort::SortPairs(b.cub_sort, sb, b.keys_in, b.keys_out, b.vals_in,
                                             b.vals_out, (int)pairs, 0, key_bits(ntiles), st));
     g_launches.fetch_add(2 * ((key_bits(ntiles) + 7) / 8));
+    prof_end(PH_TILE_SORT, st);
+    prof_begin(PH_RANGES, st);
     ranges_kernel<<<(unsigned)cdiv(pairs, 256), 256, 0, st>>>(pairs, b.keys_out, g.ranges);
     SS_CHECK_LAUNCH("ranges_kernel");
+    prof_end(PH_RANGES, st);
   }
   const BlendParams bp = blend_params(cam, s);
-  if (touch)
-    return launch_blend_fwd<true>(s->tile_size, ntiles, st, bp, g, b.vals_out, image, alpha, touch);
-  return launch_blend_fwd<false>(s->tile_size, ntiles, st, bp, g, b.vals_out, image, alpha,
-                                 nullptr);
+  prof_begin(PH_BLEND_FWD, st);
+  const int rc = touch ? launch_blend_fwd<true>(s->tile_size, ntiles, st, bp, g, b.vals_out, image,
+                                                alpha, touch)
+                       : launch_blend_fwd<false>(s->tile_size, ntiles, st, bp, g, b.vals_out,
+                                                 image, alpha, nullptr);
+  prof_end(PH_BLEND_FWD, st);
+  return rc;
 }
 
 int raster_backward(const ss_cloud* cl, const ss_camera* cam, const ss_raster_settings* s,
@@ -787,13 +821,17 @@ int raster_backward(const ss_cloud* cl, const ss_camera* cam, const ss_raster_se
   Geom g = plan_geom(geom, n, cam, s);
   Bins b = plan_bins(bins, pairs);
   const int64_t ntiles = (int64_t)ntiles_x(cam, s) * ntiles_y(cam, s);
+  prof_begin(PH_BLEND_BWD, st);
   SS_CUDA(cudaMemsetAsync(g.acc, 0, n * 9 * sizeof(float), st));
   SS_CUDA(cudaMemsetAsync(g.touched, 0, n, st));
   const BlendParams bp = blend_params(cam, s);
   if (pairs > 0) SS_TRY(launch_blend_bwd(s->tile_size, ntiles, st, bp, g, b.vals_out, d_image));
+  prof_end(PH_BLEND_BWD, st);
+  prof_begin(PH_GAUSS_BWD, st);
   gaussian_bwd_kernel<<<(unsigned)cdiv(n, 128), 128, 0, st>>>(make_cam(cam), *cl, g, n, *grads,
                                                                full);
   SS_CHECK_LAUNCH("gaussian_bwd_kernel");
+  prof_end(PH_GAUSS_BWD, st);
   return SS_OK;
 }
 

@@ -22,6 +22,8 @@ def require_cuda() -> torch.device:
 
 
 def ptr(t) -> C.c_void_p | None:
+    """Raw device address.  The caller must keep `t` referenced until the
+    launch is enqueued (a freed temporary can be reused by the next allocation)."""
     if t is None:
         return None
     return C.c_void_p(t.data_ptr())

@@ -147,7 +147,8 @@ class NeuralTransformationCache:
         nf = self.grid.n_levels * self.grid.n_features
         out7 = torch.zeros(max(n, 1), 7, dtype=torch.float32, device=dev)
         feats = torch.zeros(max(n, 1), nf, dtype=torch.float32, device=dev)
-        _lib.check(lib.ss_ntc_forward(C.byref(gs), C.byref(m), n, ptr(to_dev(x, dev=dev)), None,
+        xd = to_dev(x, dev=dev)  # keep alive until the launch is enqueued
+        _lib.check(lib.ss_ntc_forward(C.byref(gs), C.byref(m), n, ptr(xd), None,
                                       ptr(tab), ptr(par), ptr(out7), ptr(feats), stream()),
                    "forward")
         return (out7[:n].cpu().numpy().astype(np.float64),
@@ -185,8 +186,9 @@ class NeuralTransformationCache:
         g_tab = torch.zeros_like(tab)
         g_par = torch.zeros_like(par)
         if n:
-            _lib.check(lib.ss_ntc_backward(C.byref(gs), C.byref(m), n, ptr(to_dev(x, dev=dev)),
-                                           None, ptr(tab), ptr(par), ptr(to_dev(g7, dev=dev)),
+            xd, g7d = to_dev(x, dev=dev), to_dev(g7, dev=dev)  # alive across the launch
+            _lib.check(lib.ss_ntc_backward(C.byref(gs), C.byref(m), n, ptr(xd),
+                                           None, ptr(tab), ptr(par), ptr(g7d),
                                            ptr(g_tab), ptr(g_par), None, stream()), "backward")
         gt = g_tab.cpu().numpy().astype(np.float64)
         ws, bs = unpack_params(g_par.cpu().numpy(), [w.shape for w in self.weights], lay)

@@ -92,8 +92,11 @@ class Stage1Trainer:
         self.params = to_dev(pack_params(weights, biases, self.layout), dev=dev)
         nt, npar = self.tables.numel(), self.params.numel()
         f32, f64 = dict(dtype=torch.float32, device=dev), dict(dtype=torch.float64, device=dev)
-        self.g_tables = torch.zeros(nt, **f32)
-        self.g_params = torch.zeros(npar, **f32)
+        # one packed gradient buffer [tables | MLP] so data parallelism needs a
+        # single all-reduce (nt is a multiple of 4: the MLP part stays 16B-aligned)
+        self.g_flat = torch.zeros(nt + npar, **f32)
+        self.g_tables = self.g_flat[:nt]
+        self.g_params = self.g_flat[nt:]
         self.m_tables = torch.zeros(nt, **f64)
         self.v_tables = torch.zeros(nt, **f64)
         self.m_params = torch.zeros(npar, **f64)
@@ -189,10 +192,18 @@ class Stage1Trainer:
         _lib.check_flags(int(self.flags.item()), "stage1 loss")
         return int(self.counts[1].item())
 
-    def finish(self, view: int, pairs: int, adam: bool = True, grad_scale: float = 1.0):
+    def stage_target(self, view: int, target_host: torch.Tensor):
+        """Asynchronous H2D copy of a view's target from pinned host memory."""
+        if getattr(self, "_staging", None) is None:
+            self._staging = torch.empty_like(self.targets[0])
+        self._staging.view(-1)[: target_host.numel()].copy_(target_host.view(-1),
+                                                            non_blocking=True)
+
+    def finish(self, view: int, pairs: int, adam: bool = True, grad_scale: float = 1.0,
+               staged: bool = False):
         cam = self.cam_structs[view]
         self._ensure_bins(pairs, cam)
-        tgt = ptr(self.targets[view])
+        tgt = ptr(self._staging if staged else self.targets[view])
         if adam and grad_scale == 1.0:
             self._call(self.lib.ss_stage1_iter_finish, C.byref(self.s), C.byref(cam), tgt, pairs,
                        stream())
@@ -204,6 +215,26 @@ class Stage1Trainer:
 
     def apply_adam(self):
         self._call(self.lib.ss_stage1_apply_adam, C.byref(self.s), stream())
+
+    def render(self, view: int) -> int:
+        """Forward only (render-only config 2 / playback, pipeline.py:471-480):
+        NTC transform + rasterize_forward of the current cache into self.image."""
+        pairs = self.begin(view)
+        cam = self.cam_structs[view]
+        self._ensure_bins(pairs, cam)
+        tc = self.cloud.struct(self.t_means, self.t_rot, self.t_sh)
+        self._call(self.lib.ss_raster_forward_finish, C.byref(tc), C.byref(cam),
+                   C.byref(self.settings), ptr(self.geom), ptr(self.bins), pairs, ptr(self.image),
+                   ptr(self.alpha), None, stream())
+        return pairs
+
+    def step_from_host(self, view: int, target_host: torch.Tensor) -> float:
+        """End-to-end step through host buffers: H2D copy of the view's target
+        from pinned memory, the iteration, D2H read of the loss."""
+        self.stage_target(view, target_host)
+        pairs = self.begin(view)
+        self.finish(view, pairs, staged=True)
+        return float(self.loss_dev.item())
 
     def step(self, view: int):
         pairs = self.begin(view)

@@ -127,8 +127,9 @@ def apply_ntc_backward(ctx: TransformContext, d_means_t, d_rotations_t, d_sh_t):
         return grads, touched
     g7 = torch.zeros(max(n_in, 1), 7, dtype=torch.float32, device=dev)
     if n_in:
+        o7 = to_dev(ctx.out7, dev=dev)  # alive across the launch
         _lib.check(lib.ss_transform_vjp(C.byref(dc.struct()), n_in, ptr(rows),
-                                        ptr(to_dev(ctx.out7, dev=dev)), int(ctx.rotate_sh),
+                                        ptr(o7), int(ctx.rotate_sh),
                                         ptr(dm), ptr(dr), ptr(ds), ptr(g7), stream()),
                    "apply_ntc_backward")
     g = g7[:n_in].cpu().numpy().astype(np.float64)
