@@ -131,7 +131,11 @@ def phase_bytes(phase, n, n_in, K, pairs, P, ltf):
         "ntc_backward": n_in * (12 + 16 + 12 * K + 12 + 16 + 12 * K) + 3 * 4 * ltf,
         "tile_sort": pairs * 16 * 2,
         "adam": ltf * (4 * 3 + 16 * 2 + 1 / 2),
-    }.get(phase)
+        "depth_sort": n * 12 * 2 * 2,
+        "rank_scan": n * (4 + 16 + 32 + 16 + 16 + 16 + 64 + 8 * 2),
+        "duplicate": pairs * 8 + n * 24,
+        "ranges": pairs * 4 + 8 * (P // 256),
+    }.get(phase, 0)
 
 
 def cpu_baseline_sample(sc, cache, target, rows=(32, 64)):

@@ -174,8 +174,18 @@ int ss_apply_ntc(const ss_grid* grid, const ss_mlp* mlp, const ss_cloud* src, in
                  int32_t rotate_sh, float* out_means, float* out_rotations, float* out_sh,
                  float* out7, uint32_t* status, void* stream);
 
-/* apply_ntc_backward (transform.py:99-135) fused with the NTC backward
- * (ntc.py:250-288): gradients on the transformed cloud -> += g_tables, g_params. */
+/* apply_ntc_backward (transform.py:99-135) chained with the NTC backward
+ * (ntc.py:250-288): gradients on the transformed cloud -> += g_tables, g_params.
+ * scratch: ss_apply_ntc_backward_bytes(n_in) bytes (the decoder output is
+ * recomputed there).  The _stored variant takes the forward's out7 instead
+ * and a caller buffer g_out7 (n_in, 7). */
+size_t ss_apply_ntc_backward_bytes(int64_t n_in);
+int ss_apply_ntc_backward_stored(const ss_grid* grid, const ss_mlp* mlp, const ss_cloud* src,
+                                 int64_t n_in, const int32_t* rows, const float* tables,
+                                 const float* params, int32_t rotate_sh, const float* out7,
+                                 const float* d_means, const float* d_rotations,
+                                 const float* d_sh, float* g_out7, float* g_tables,
+                                 float* g_params, void* stream);
 int ss_apply_ntc_backward(const ss_grid* grid, const ss_mlp* mlp, const ss_cloud* src,
                           int64_t n_in, const int32_t* rows, const float* tables,
                           const float* params, int32_t rotate_sh, const float* d_means,

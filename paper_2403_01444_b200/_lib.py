@@ -103,6 +103,9 @@ SIGNATURES = [
     ("ss_apply_ntc", I32, [PGrid, PMlp, PCloud, I64, P, P, P, I32, P, P, P, P, P, P]),
     ("ss_apply_ntc_backward", I32, [PGrid, PMlp, PCloud, I64, P, P, P, I32, P, P, P, P, P, P,
                                     P]),
+    ("ss_apply_ntc_backward_bytes", SZ, [I64]),
+    ("ss_apply_ntc_backward_stored", I32, [PGrid, PMlp, PCloud, I64, P, P, P, I32, P, P, P, P,
+                                           P, P, P, P]),
     ("ss_transform_apply", I32, [PCloud, I64, P, P, I32, P, P, P, P, P]),
     ("ss_transform_vjp", I32, [PCloud, I64, P, P, I32, P, P, P, P, P]),
     ("ss_raster_geom_bytes", SZ, [I64, PCam, PSet]),

@@ -170,6 +170,82 @@ __device__ inline void scatter_features(const ss_grid& g, float* __restrict__ g_
   }
 }
 
+// Features of one point written into a shared-memory row (zero-padded to
+// `width`); the level loop is deliberately not unrolled.
+__device__ inline void gather_to_row(const ss_grid& g, const float* __restrict__ tables,
+                                     const double xn[3], float* row, int width) {
+  const int F = g.n_features;
+  const size_t T = (size_t)1 << g.log2_table;
+#pragma unroll 1
+  for (int l = 0; l < g.n_levels; ++l) {
+    uint32_t idx[8];
+    float w[8];
+    level_corners(g, l, xn, idx, w);
+    const float* tl = tables + (size_t)l * T * F;
+    if (F == 2) {
+      float a0 = 0.f, a1 = 0.f;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const float2 v = __ldg(reinterpret_cast<const float2*>(tl) + idx[k]);
+        a0 = fmaf(w[k], v.x, a0);
+        a1 = fmaf(w[k], v.y, a1);
+      }
+      row[2 * l] = a0;
+      row[2 * l + 1] = a1;
+    } else {
+      for (int f = 0; f < F; ++f) {
+        float a = 0.f;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) a = fmaf(w[k], __ldg(tl + (size_t)idx[k] * F + f), a);
+        row[l * F + f] = a;
+      }
+    }
+  }
+  for (int k = g.n_levels * F; k < width; ++k) row[k] = 0.f;
+}
+
+// dx_j = W0[j,:] . d1 for the features of each level, scattered with vector
+// reductions into the table gradient (level loop not unrolled).
+template <int IN>
+__device__ inline void scatter_rows(const ss_grid& g, const float* __restrict__ w0,
+                                    const float (&d1)[HID], const double xn[3],
+                                    float* __restrict__ g_tables) {
+  const int F = g.n_features;
+  const size_t T = (size_t)1 << g.log2_table;
+#pragma unroll 1
+  for (int l = 0; l < g.n_levels; ++l) {
+    uint32_t idx[8];
+    float w[8];
+    level_corners(g, l, xn, idx, w);
+    float* gl = g_tables + (size_t)l * T * F;
+    for (int f0 = 0; f0 < F; f0 += 2) {
+      float dv[2] = {0.f, 0.f};
+      for (int u = 0; u < 2 && f0 + u < F; ++u) {
+        const float4* w4 = reinterpret_cast<const float4*>(w0 + (l * F + f0 + u) * HID);
+        float s = 0.f;
+#pragma unroll
+        for (int q = 0; q < HID / 4; ++q) {
+          const float4 ww = w4[q];
+          s = fmaf(ww.x, d1[4 * q], s);
+          s = fmaf(ww.y, d1[4 * q + 1], s);
+          s = fmaf(ww.z, d1[4 * q + 2], s);
+          s = fmaf(ww.w, d1[4 * q + 3], s);
+        }
+        dv[u] = s;
+      }
+      if (F - f0 >= 2 && (F % 2) == 0) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          red_add_v2(gl + (size_t)idx[k] * F + f0, w[k] * dv[0], w[k] * dv[1]);
+      } else {
+        for (int u = 0; u < 2 && f0 + u < F; ++u)
+#pragma unroll
+          for (int k = 0; k < 8; ++k) atomicAdd(gl + (size_t)idx[k] * F + f0 + u, w[k] * dv[u]);
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------------ decoder
 template <int IN, int NL>
 __device__ inline void mlp_forward(const float* __restrict__ sp, const float (&x)[IN],
@@ -631,9 +707,7 @@ template <int IN, int NL>
 __global__ void __launch_bounds__(kChunk, 1) ntc_backward_kernel(
     ss_grid g, int64_t n, const float* __restrict__ means, const int32_t* __restrict__ rows,
     const float* __restrict__ tables, const float* __restrict__ params,
-    const float* __restrict__ g_out7,  // API path: (n,7) upstream
-    ss_cloud src, int rotate_sh, const float* __restrict__ d_means,
-    const float* __restrict__ d_rot, const float* __restrict__ d_sh,  // transform path
+    const float* __restrict__ g_out7,  // (n,7) upstream dL/d[d_mu | d_q]
     float* __restrict__ g_tables, float* __restrict__ g_params) {
   using S = BwdSmem<IN, NL>;
   using L = Lay<IN, NL>;
@@ -653,95 +727,106 @@ __global__ void __launch_bounds__(kChunk, 1) ntc_backward_kernel(
       const int64_t gid = rows ? rows[i] : i;
       double xn[3];
       normalise(g, means + 3 * gid, xn);
+      // recompute the hidden activations, staging each layer through this
+      // thread's shared-memory rows so at most two 64-vectors live in registers
       uint64_t mask1 = 0, mask2 = 0;
-      float o[OUTP];
+      gather_to_row(g, tables, xn, sX, IN);  // level loop not unrolled (register budget)
       {
-        float x[IN], h1[HID], h2[HID];
-        gather_features<IN>(g, tables, xn, x);
-        mlp_forward<IN, NL>(smem, x, h1, h2, o);
+        float h[HID];
 #pragma unroll
-        for (int k = 0; k < IN; k += 4)
-          *reinterpret_cast<float4*>(sX + k) = make_float4(x[k], x[k + 1], x[k + 2], x[k + 3]);
+        for (int j = 0; j < HID; ++j) h[j] = smem[L::B0 + j];
+#pragma unroll 4
+        for (int i2 = 0; i2 < IN; ++i2) {
+          const float xi = sX[i2];
+          const float4* w4 = reinterpret_cast<const float4*>(smem + L::W0 + i2 * HID);
 #pragma unroll
-        for (int k = 0; k < HID; k += 4) {
-          *reinterpret_cast<float4*>(sH1 + k) =
-              make_float4(h1[k], h1[k + 1], h1[k + 2], h1[k + 3]);
-          if (NL == 2)
-            *reinterpret_cast<float4*>(sH2 + k) =
-                make_float4(h2[k], h2[k + 1], h2[k + 2], h2[k + 3]);
+          for (int q = 0; q < HID / 4; ++q) {
+            const float4 w = w4[q];
+            h[4 * q] = fmaf(xi, w.x, h[4 * q]);
+            h[4 * q + 1] = fmaf(xi, w.y, h[4 * q + 1]);
+            h[4 * q + 2] = fmaf(xi, w.z, h[4 * q + 2]);
+            h[4 * q + 3] = fmaf(xi, w.w, h[4 * q + 3]);
+          }
         }
 #pragma unroll
         for (int k = 0; k < HID; ++k) {
-          mask1 |= (uint64_t)(h1[k] > 0.f) << k;
-          mask2 |= (uint64_t)(h2[k] > 0.f) << k;
+          h[k] = fmaxf(h[k], 0.f);
+          mask1 |= (uint64_t)(h[k] > 0.f) << k;
         }
+#pragma unroll
+        for (int k = 0; k < HID; k += 4)
+          *reinterpret_cast<float4*>(sH1 + k) = make_float4(h[k], h[k + 1], h[k + 2], h[k + 3]);
+      }
+      if (NL == 2) {
+        float h[HID];
+#pragma unroll
+        for (int j = 0; j < HID; ++j) h[j] = smem[L::B1 + j];
+#pragma unroll 4
+        for (int i2 = 0; i2 < HID; ++i2) {
+          const float hi = sH1[i2];
+          const float4* w4 = reinterpret_cast<const float4*>(smem + L::W1 + i2 * HID);
+#pragma unroll
+          for (int q = 0; q < HID / 4; ++q) {
+            const float4 w = w4[q];
+            h[4 * q] = fmaf(hi, w.x, h[4 * q]);
+            h[4 * q + 1] = fmaf(hi, w.y, h[4 * q + 1]);
+            h[4 * q + 2] = fmaf(hi, w.z, h[4 * q + 2]);
+            h[4 * q + 3] = fmaf(hi, w.w, h[4 * q + 3]);
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < HID; ++k) {
+          h[k] = fmaxf(h[k], 0.f);
+          mask2 |= (uint64_t)(h[k] > 0.f) << k;
+        }
+#pragma unroll
+        for (int k = 0; k < HID; k += 4)
+          *reinterpret_cast<float4*>(sH2 + k) = make_float4(h[k], h[k + 1], h[k + 2], h[k + 3]);
+      } else {
+        mask2 = mask1;
       }
       float g7[OUTP];
-      if (g_out7) {
 #pragma unroll
-        for (int k = 0; k < 7; ++k) g7[k] = g_out7[i * 7 + k];
-        g7[7] = 0.f;
-      } else {
-        transform_vjp(src, gid, o, rotate_sh, d_means, d_rot, d_sh, g7);
-      }
+      for (int k = 0; k < 7; ++k) g7[k] = g_out7[i * 7 + k];
+      g7[7] = 0.f;
       *reinterpret_cast<float4*>(sG) = make_float4(g7[0], g7[1], g7[2], g7[3]);
       *reinterpret_cast<float4*>(sG + 4) = make_float4(g7[4], g7[5], g7[6], g7[7]);
       // delta through the output layer: dl = (W2 g7) * (h_last > 0)
       float d1[HID];
       {
-        float dl[HID];
+        float* sDl = NL == 2 ? sD2 : sD1;
 #pragma unroll
         for (int j = 0; j < HID; ++j) {
           const float4* w4 = reinterpret_cast<const float4*>(smem + L::W2 + j * OUTP);
-          float4 a = w4[0], b = w4[1];
-          float s = a.x * g7[0] + a.y * g7[1] + a.z * g7[2] + a.w * g7[3] + b.x * g7[4] +
-                    b.y * g7[5] + b.z * g7[6];
-          dl[j] = ((mask2 >> j) & 1) ? s : 0.f;
+          const float4 a = w4[0], b = w4[1];
+          const float sv = a.x * g7[0] + a.y * g7[1] + a.z * g7[2] + a.w * g7[3] + b.x * g7[4] +
+                           b.y * g7[5] + b.z * g7[6];
+          d1[j] = ((mask2 >> j) & 1) ? sv : 0.f;
         }
+#pragma unroll
+        for (int k = 0; k < HID; k += 4)
+          *reinterpret_cast<float4*>(sDl + k) = make_float4(d1[k], d1[k + 1], d1[k + 2], d1[k + 3]);
         if (NL == 2) {
+          // d1 = (W1 dl) * (h1 > 0), dl read back from its shared row
+#pragma unroll
+          for (int k = 0; k < HID; ++k) d1[k] = 0.f;
+#pragma unroll 4
+          for (int q = 0; q < HID; ++q) {
+            const float dq = sD2[q];
+#pragma unroll
+            for (int r = 0; r < HID; ++r) d1[r] = fmaf(smem[L::W1 + r * HID + q], dq, d1[r]);
+          }
+#pragma unroll
+          for (int k = 0; k < HID; ++k) d1[k] = ((mask1 >> k) & 1) ? d1[k] : 0.f;
 #pragma unroll
           for (int k = 0; k < HID; k += 4)
-            *reinterpret_cast<float4*>(sD2 + k) =
-                make_float4(dl[k], dl[k + 1], dl[k + 2], dl[k + 3]);
-#pragma unroll
-          for (int r = 0; r < HID; ++r) {
-            const float4* w4 = reinterpret_cast<const float4*>(smem + L::W1 + r * HID);
-            float s = 0.f;
-#pragma unroll
-            for (int q = 0; q < HID / 4; ++q) {
-              float4 w = w4[q];
-              s = fmaf(w.x, dl[4 * q], s);
-              s = fmaf(w.y, dl[4 * q + 1], s);
-              s = fmaf(w.z, dl[4 * q + 2], s);
-              s = fmaf(w.w, dl[4 * q + 3], s);
-            }
-            d1[r] = ((mask1 >> r) & 1) ? s : 0.f;
-          }
-        } else {
-#pragma unroll
-          for (int k = 0; k < HID; ++k) d1[k] = dl[k];
+            *reinterpret_cast<float4*>(sD1 + k) =
+                make_float4(d1[k], d1[k + 1], d1[k + 2], d1[k + 3]);
         }
       }
-#pragma unroll
-      for (int k = 0; k < HID; k += 4)
-        *reinterpret_cast<float4*>(sD1 + k) = make_float4(d1[k], d1[k + 1], d1[k + 2], d1[k + 3]);
-      // feature gradient dx = W0 d1, scattered into the tables
-      float dx[IN];
-#pragma unroll
-      for (int r = 0; r < IN; ++r) {
-        const float4* w4 = reinterpret_cast<const float4*>(smem + L::W0 + r * HID);
-        float s = 0.f;
-#pragma unroll
-        for (int q = 0; q < HID / 4; ++q) {
-          float4 w = w4[q];
-          s = fmaf(w.x, d1[4 * q], s);
-          s = fmaf(w.y, d1[4 * q + 1], s);
-          s = fmaf(w.z, d1[4 * q + 2], s);
-          s = fmaf(w.w, d1[4 * q + 3], s);
-        }
-        dx[r] = s;
-      }
-      scatter_features<IN>(g, g_tables, xn, dx);
+      // feature gradient dx = W0 d1, computed per level and scattered into the
+      // tables (ntc.py:278-288)
+      scatter_rows<IN>(g, smem + L::W0, d1, xn, g_tables);
     } else {
       for (int k = 0; k < S::SX; ++k) sX[k] = 0.f;
       for (int k = 0; k < S::SH; ++k) {
@@ -894,9 +979,6 @@ struct BwdLaunch {
   const float* means;
   const int32_t* rows;
   const float *tables, *params, *g_out7;
-  ss_cloud src;
-  int rotate_sh;
-  const float *dm, *dr, *ds;
   float *g_tables, *g_params;
   cudaStream_t st;
   template <int IN, int NL>
@@ -911,8 +993,8 @@ struct BwdLaunch {
     const int64_t chunks = cdiv(n, kChunk);
     const unsigned grid = (unsigned)std::min<int64_t>(chunks, sms);
     prof_begin(PH_NTC_BWD, st);
-    k<<<grid, kChunk, smem, st>>>(*g, n, means, rows, tables, params, g_out7, src, rotate_sh, dm,
-                                  dr, ds, g_tables, g_params);
+    k<<<grid, kChunk, smem, st>>>(*g, n, means, rows, tables, params, g_out7, g_tables,
+                                  g_params);
     SS_CHECK_LAUNCH("ntc_backward_kernel");
     prof_end(PH_NTC_BWD, st);
     return SS_OK;
@@ -966,8 +1048,12 @@ int ss_ntc_backward(const ss_grid* grid, const ss_mlp* mlp, int64_t n, const flo
                     void* stream) {
   (void)scratch;
   SS_TRY(check_grid(grid, mlp));
-  BwdLaunch L{grid, n, means, rows, tables, params, g_out7, ss_cloud{}, 0, nullptr, nullptr,
-              nullptr, g_tables, g_params, as_stream(stream)};
+  if (!g_out7) {
+    set_error("ss_ntc_backward: g_out7 required");
+    return SS_ERR_DATA;
+  }
+  BwdLaunch L{grid, n, means, rows, tables, params, g_out7, g_tables, g_params,
+              as_stream(stream)};
   return dispatch_mlp(mlp, L);
 }
 
@@ -990,21 +1076,44 @@ int ss_apply_ntc(const ss_grid* grid, const ss_mlp* mlp, const ss_cloud* src, in
   return dispatch_mlp(mlp, L);
 }
 
+size_t ss_apply_ntc_backward_bytes(int64_t n_in) {
+  return align_up((size_t)(n_in > 0 ? n_in : 1) * 7 * sizeof(float)) * 2;
+}
+
 int ss_apply_ntc_backward(const ss_grid* grid, const ss_mlp* mlp, const ss_cloud* src,
                           int64_t n_in, const int32_t* rows, const float* tables,
                           const float* params, int32_t rotate_sh, const float* d_means,
                           const float* d_rotations, const float* d_sh, float* g_tables,
                           float* g_params, void* scratch, void* stream) {
-  (void)scratch;
   SS_TRY(check_grid(grid, mlp));
-  if (!src || !d_means || !d_rotations || (rotate_sh && src->sh_coeffs > 1 && !d_sh)) {
-    set_error("ss_apply_ntc_backward: missing gradient buffers");
+  if (!src || !d_means || !d_rotations || (rotate_sh && src->sh_coeffs > 1 && !d_sh) ||
+      !scratch) {
+    set_error("ss_apply_ntc_backward: missing gradient or scratch buffers");
     return SS_ERR_DATA;
   }
-  SS_TRY(ensure_shrot_const());
-  BwdLaunch L{grid, n_in, src->means, rows, tables, params, nullptr, *src, rotate_sh,
-              d_means, d_rotations, d_sh, g_tables, g_params, as_stream(stream)};
-  return dispatch_mlp(mlp, L);
+  if (n_in == 0) return SS_OK;
+  // the decoder output is recomputed (K2f), then the transform VJP (K3b) and the
+  // decoder/table backward (K2b/K1b) run as separate kernels
+  float* out7 = static_cast<float*>(scratch);
+  float* g7 = reinterpret_cast<float*>(static_cast<char*>(scratch) +
+                                       ss_apply_ntc_backward_bytes(n_in) / 2);
+  SS_TRY(ss_ntc_forward(grid, mlp, n_in, src->means, rows, tables, params, out7, nullptr,
+                        stream));
+  return ss_apply_ntc_backward_stored(grid, mlp, src, n_in, rows, tables, params, rotate_sh,
+                                      out7, d_means, d_rotations, d_sh, g7, g_tables, g_params,
+                                      stream);
+}
+
+int ss_apply_ntc_backward_stored(const ss_grid* grid, const ss_mlp* mlp, const ss_cloud* src,
+                                 int64_t n_in, const int32_t* rows, const float* tables,
+                                 const float* params, int32_t rotate_sh, const float* out7,
+                                 const float* d_means, const float* d_rotations,
+                                 const float* d_sh, float* g_out7, float* g_tables,
+                                 float* g_params, void* stream) {
+  SS_TRY(ss_transform_vjp(src, n_in, rows, out7, rotate_sh, d_means, d_rotations, d_sh, g_out7,
+                          stream));
+  return ss_ntc_backward(grid, mlp, n_in, src->means, rows, tables, params, g_out7, g_tables,
+                         g_params, nullptr, stream);
 }
 
 int ss_transform_apply(const ss_cloud* src, int64_t n_in, const int32_t* rows, const float* out7,

@@ -12,6 +12,8 @@
 namespace ss {
 
 // ------------------------------------------------------------------ workspace
+constexpr int kAccStride = 12;  // 48 B per rank: two aligned v4 reductions
+
 struct Geom {
   double *key_in, *key_out;
   int32_t *idx_in, *order;
@@ -25,7 +27,7 @@ struct Geom {
   float4* r_color;
   int4* r_rect;     // per rank (tx0, tx1, ty0, ty1)
   int64_t* offsets;  // per rank, exclusive prefix of tile counts (n+1)
-  float* acc;        // per rank x 9 (colour 3, opacity, mean2d 2, conic 00/01/11)
+  float* acc;        // per rank x kAccStride: colour 3, mean2d 2, conic 00/01/11, opacity
   uint8_t* touched;  // per rank
   float* t_final;    // per pixel
   int32_t* n_contrib;
@@ -77,7 +79,7 @@ static Geom plan_geom(void* base, int64_t n, const ss_camera* cam, const ss_rast
   g.r_color = c.take<float4>(nn);
   g.r_rect = c.take<int4>(nn);
   g.offsets = c.take<int64_t>(nn + 1);
-  g.acc = c.take<float>(nn * 9);
+  g.acc = c.take<float>(nn * kAccStride);
   g.touched = c.take<uint8_t>(nn);
   g.t_final = c.take<float>(P);
   g.n_contrib = c.take<int32_t>(P);
@@ -279,19 +281,23 @@ __global__ void finish_counts_kernel(Geom g, int64_t n) {
 }
 
 // K4c: emit (tile id, rank) in rank order
-__global__ void duplicate_kernel(ss_raster_settings s, int ntx, int64_t n, Geom g, Bins b) {
-  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (r >= n || r >= g.dev_counts[0]) return;
-  int64_t off = g.offsets[r];
-  const int64_t end = g.offsets[r + 1];
-  if (off == end) return;
-  const int4 rc = g.r_rect[r];
-  for (int ty = rc.z; ty <= rc.w; ++ty)
-    for (int tx = rc.x; tx <= rc.y; ++tx) {
-      b.keys_in[off] = (uint32_t)(ty * ntx + tx);
-      b.vals_in[off] = (uint32_t)r;
-      ++off;
-    }
+// K4c: emit (tile id, rank) in rank order, one thread per pair (load-balanced:
+// near-camera splats can cover thousands of tiles).  The owning rank is the last
+// r with offsets[r] <= j (zero-count ranks are skipped by construction).
+__global__ void duplicate_kernel(int ntx, int64_t n, int64_t pairs, Geom g, Bins b) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= pairs) return;
+  int64_t lo = 0, hi = n;  // offsets[lo] <= j < offsets[hi]
+  while (hi - lo > 1) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (g.offsets[mid] <= j) lo = mid; else hi = mid;
+  }
+  const int4 rc = g.r_rect[lo];
+  const int wx = rc.y - rc.x + 1;
+  const int local = (int)(j - g.offsets[lo]);
+  const int ty = rc.z + local / wx, tx = rc.x + local % wx;
+  b.keys_in[j] = (uint32_t)(ty * ntx + tx);
+  b.vals_in[j] = (uint32_t)lo;
 }
 
 __global__ void ranges_kernel(int64_t pairs, const uint32_t* __restrict__ keys, int2* ranges) {
@@ -454,16 +460,24 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_fwd_kernel(
 
 // K5a: reverse blend (rasterizer.py:306-349).  Per pixel, walk the tile list
 // back to front from the last contributor reconstructing T_before by
-// division, keeping the suffix sum incl. the background term; per-splat
-// gradients are warp-reduced and added to the per-rank accumulators.
-template <int TS>
+// division, keeping the suffix sum incl. the background term.  Per splat, the
+// 8 pixel-gradient terms are reduced across the warp with a reduce-scatter
+// butterfly (9 shuffles instead of 8x5) so lane 4i ends up holding term i;
+// those lanes add into shared-memory per-splat accumulators (8 warps -> one
+// row), which are flushed to the per-rank global accumulators once per batch.
+template <int TS, bool FULL>
 __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_bwd_kernel(
     BlendParams bp, Geom g, const uint32_t* __restrict__ vals, const float* __restrict__ d_image) {
   constexpr int NT = BlendShape<TS>::NT, PPT = BlendShape<TS>::PPT;
+  constexpr int NA = 9;  // colour 3, mean2d 2, conic 3, opacity
   __shared__ float2 s_xy[NT];
   __shared__ float4 s_co[NT];
   __shared__ float4 s_col[NT];
   __shared__ int s_rank[NT];
+  __shared__ float s_acc[NT * NA];
+  __shared__ int s_any[NT];
+  __shared__ int s_last;
+  const int lane = threadIdx.x & 31;
   const int tile = blockIdx.x;
   const int x0 = (tile % bp.ntx) * TS, y0 = (tile / bp.ntx) * TS;
   const int2 range = g.ranges[tile];
@@ -492,18 +506,16 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_bwd_kernel(
     S[p] = gb * T[p];
     max_last = max(max_last, last[p]);
   }
-  // only positions below the tile-wide max contributor count matter
-  __shared__ int s_last;
   if (threadIdx.x == 0) s_last = 0;
+  for (int i = threadIdx.x; i < NT * NA; i += NT) s_acc[i] = 0.f;
+  s_any[threadIdx.x] = 0;
   __syncthreads();
   atomicMax(&s_last, max_last);
   __syncthreads();
-  const int tile_last = s_last;
-  const int end0 = range.x + tile_last;
+  const int end0 = range.x + s_last;  // positions past every pixel's last contributor are dead
   for (int end = end0; end > range.x; end -= NT) {
     const int start = max(range.x, end - NT);
     const int cnt = end - start;
-    __syncthreads();
     if (threadIdx.x < cnt) {
       const int pos = end - 1 - threadIdx.x;
       const int r = (int)vals[pos];
@@ -518,8 +530,7 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_bwd_kernel(
       const int pos_rel = end - 1 - k - range.x;
       const float2 xy = s_xy[k];
       const float4 co = s_co[k];
-      const float4 col = s_col[k];
-      float v[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      float v[NA] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
       bool any = false;
 #pragma unroll
       for (int p = 0; p < PPT; ++p) {
@@ -529,6 +540,7 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_bwd_kernel(
         const float a = pair_alpha(bp, dx, dy, co, s_rank[k], lx[p] + x0, ly[p] + y0, g.r_mean,
                                    g.r_conop_d, G, og);
         if (a == 0.f) continue;
+        const float4 col = s_col[k];
         const float oma = 1.f - a;
         const float tb = T[p] / oma;  // T_before
         const float w = a * tb;
@@ -542,26 +554,58 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_bwd_kernel(
         if (!(og < bp.clamp)) da = 0.f;  // flat above the clamp (rasterizer.py:336-337)
         const float dm = -0.5f * G * co.w * da;
         const float c01 = 0.5f * co.y;
-        v[3] = fmaf(da, G, v[3]);
-        v[4] -= 2.f * dm * (co.x * dx + c01 * dy);
-        v[5] -= 2.f * dm * (c01 * dx + co.z * dy);
-        v[6] = fmaf(dm, dx * dx, v[6]);
-        v[7] = fmaf(dm, dx * dy, v[7]);
-        v[8] = fmaf(dm, dy * dy, v[8]);
+        v[3] -= 2.f * dm * (co.x * dx + c01 * dy);
+        v[4] -= 2.f * dm * (c01 * dx + co.z * dy);
+        v[5] = fmaf(dm, dx * dx, v[5]);
+        v[6] = fmaf(dm, dx * dy, v[6]);
+        v[7] = fmaf(dm, dy * dy, v[7]);
+        if (FULL) v[8] = fmaf(da, G, v[8]);
         any = true;
       }
-      if (__any_sync(0xffffffffu, any)) {
+      const unsigned bal = __ballot_sync(0xffffffffu, any);
+      if (bal) {
+        // reduce-scatter butterfly over terms 0..7: after it lane L holds the
+        // warp total of term (L >> 2) (valid in lanes with L & 3 == 0)
+        const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+        float h4[4], h2[2], h1;
 #pragma unroll
-        for (int q = 0; q < 9; ++q) v[q] = warp_sum(v[q]);
-        const unsigned bal = __ballot_sync(0xffffffffu, any);
-        if ((threadIdx.x & 31) == 0) {
-          float* a = g.acc + (int64_t)s_rank[k] * 9;
-#pragma unroll
-          for (int q = 0; q < 9; ++q) atomicAdd(a + q, v[q]);
-          if (bal) g.touched[s_rank[k]] = 1;
+        for (int i = 0; i < 4; ++i) {
+          const float send = b4 ? v[i] : v[4 + i];
+          h4[i] = (b4 ? v[4 + i] : v[i]) + __shfl_xor_sync(0xffffffffu, send, 16);
         }
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const float send = b3 ? h4[i] : h4[2 + i];
+          h2[i] = (b3 ? h4[2 + i] : h4[i]) + __shfl_xor_sync(0xffffffffu, send, 8);
+        }
+        {
+          const float send = b2 ? h2[0] : h2[1];
+          h1 = (b2 ? h2[1] : h2[0]) + __shfl_xor_sync(0xffffffffu, send, 4);
+        }
+        h1 += __shfl_xor_sync(0xffffffffu, h1, 2);
+        h1 += __shfl_xor_sync(0xffffffffu, h1, 1);
+        if ((lane & 3) == 0) atomicAdd(&s_acc[k * NA + (lane >> 2)], h1);
+        if (FULL) {
+          const float o = warp_sum(v[8]);
+          if (lane == 0) atomicAdd(&s_acc[k * NA + 8], o);
+        }
+        if (lane == 0) s_any[k] = 1;
       }
     }
+    __syncthreads();
+    // flush this batch's per-splat sums (one row per splat) and reset them
+    if (threadIdx.x < cnt && s_any[threadIdx.x]) {
+      float* a = g.acc + (int64_t)s_rank[threadIdx.x] * kAccStride;
+      float* sa = s_acc + threadIdx.x * NA;
+      red_add_v4(a, sa[0], sa[1], sa[2], sa[3]);
+      red_add_v4(a + 4, sa[4], sa[5], sa[6], sa[7]);
+      if (FULL) atomicAdd(a + 8, sa[8]);
+      g.touched[s_rank[threadIdx.x]] = 1;
+#pragma unroll
+      for (int q = 0; q < NA; ++q) sa[q] = 0.f;
+      s_any[threadIdx.x] = 0;
+    }
+    __syncthreads();
   }
 }
 
@@ -582,11 +626,11 @@ __global__ void gaussian_bwd_kernel(CamD cam, ss_cloud cl, Geom g, int64_t n, ss
     if (full && out.d_opacity_logits) out.d_opacity_logits[gid] = 0.f;
     return;
   }
-  const float* a = g.acc + r * 9;
+  const float* a = g.acc + r * kAccStride;
   const double acol[3] = {a[0], a[1], a[2]};
-  const double aop = a[3];
-  const double am[2] = {a[4], a[5]};
-  const double A[2][2] = {{a[6], a[7]}, {a[7], a[8]}};
+  const double am[2] = {a[3], a[4]};
+  const double A[2][2] = {{a[5], a[6]}, {a[6], a[7]}};
+  const double aop = a[8];
   if (out.viewspace) out.viewspace[gid] = (float)sqrt(am[0] * am[0] + am[1] * am[1]);
   if (out.contributed) out.contributed[gid] = g.touched[r];
   Projected P;
@@ -725,14 +769,15 @@ static int launch_blend_fwd(int ts, int64_t ntiles, cudaStream_t st, const Blend
   return SS_OK;
 }
 
+template <bool FULL>
 static int launch_blend_bwd(int ts, int64_t ntiles, cudaStream_t st, const BlendParams& bp,
                             const Geom& g, const uint32_t* vals, const float* d_image) {
   const unsigned grid = (unsigned)ntiles;
   switch (ts) {
-    case 8: blend_bwd_kernel<8><<<grid, BlendShape<8>::NT, 0, st>>>(bp, g, vals, d_image); break;
-    case 16: blend_bwd_kernel<16><<<grid, BlendShape<16>::NT, 0, st>>>(bp, g, vals, d_image); break;
-    case 32: blend_bwd_kernel<32><<<grid, BlendShape<32>::NT, 0, st>>>(bp, g, vals, d_image); break;
-    default: blend_bwd_kernel<64><<<grid, BlendShape<64>::NT, 0, st>>>(bp, g, vals, d_image); break;
+    case 8: blend_bwd_kernel<8, FULL><<<grid, BlendShape<8>::NT, 0, st>>>(bp, g, vals, d_image); break;
+    case 16: blend_bwd_kernel<16, FULL><<<grid, BlendShape<16>::NT, 0, st>>>(bp, g, vals, d_image); break;
+    case 32: blend_bwd_kernel<32, FULL><<<grid, BlendShape<32>::NT, 0, st>>>(bp, g, vals, d_image); break;
+    default: blend_bwd_kernel<64, FULL><<<grid, BlendShape<64>::NT, 0, st>>>(bp, g, vals, d_image); break;
   }
   SS_CHECK_LAUNCH("blend_bwd_kernel");
   return SS_OK;
@@ -788,7 +833,7 @@ int raster_finish(const ss_cloud* cl, const ss_camera* cam, const ss_raster_sett
   SS_CUDA(cudaMemsetAsync(g.ranges, 0, ntiles * sizeof(int2), st));
   if (pairs > 0) {
     prof_begin(PH_DUPLICATE, st);
-    duplicate_kernel<<<(unsigned)cdiv(n, 256), 256, 0, st>>>(*s, ntx, n, g, b);
+    duplicate_kernel<<<(unsigned)cdiv(pairs, 256), 256, 0, st>>>(ntx, n, pairs, g, b);
     SS_CHECK_LAUNCH("duplicate_kernel");
     prof_end(PH_DUPLICATE, st);
     prof_begin(PH_TILE_SORT, st);
@@ -822,10 +867,13 @@ int raster_backward(const ss_cloud* cl, const ss_camera* cam, const ss_raster_se
   Bins b = plan_bins(bins, pairs);
   const int64_t ntiles = (int64_t)ntiles_x(cam, s) * ntiles_y(cam, s);
   prof_begin(PH_BLEND_BWD, st);
-  SS_CUDA(cudaMemsetAsync(g.acc, 0, n * 9 * sizeof(float), st));
+  SS_CUDA(cudaMemsetAsync(g.acc, 0, n * kAccStride * sizeof(float), st));
   SS_CUDA(cudaMemsetAsync(g.touched, 0, n, st));
   const BlendParams bp = blend_params(cam, s);
-  if (pairs > 0) SS_TRY(launch_blend_bwd(s->tile_size, ntiles, st, bp, g, b.vals_out, d_image));
+  if (pairs > 0) {
+    if (full) SS_TRY(launch_blend_bwd<true>(s->tile_size, ntiles, st, bp, g, b.vals_out, d_image));
+    else SS_TRY(launch_blend_bwd<false>(s->tile_size, ntiles, st, bp, g, b.vals_out, d_image));
+  }
   prof_end(PH_BLEND_BWD, st);
   prof_begin(PH_GAUSS_BWD, st);
   gaussian_bwd_kernel<<<(unsigned)cdiv(n, 128), 128, 0, st>>>(make_cam(cam), *cl, g, n, *grads,
@@ -886,7 +934,7 @@ int tile_bin_finish(int64_t n, const ss_camera* cam, const ss_raster_settings* s
   const int64_t ntiles = (int64_t)ntx * nty;
   SS_CUDA(cudaMemsetAsync(g.ranges, 0, ntiles * sizeof(int2), st));
   if (pairs > 0) {
-    duplicate_kernel<<<(unsigned)cdiv(n, 256), 256, 0, st>>>(*s, ntx, n, g, b);
+    duplicate_kernel<<<(unsigned)cdiv(pairs, 256), 256, 0, st>>>(ntx, n, pairs, g, b);
     SS_CHECK_LAUNCH("duplicate_kernel");
     size_t sb = b.cub_sort_bytes;
     SS_CUDA(cub::DeviceRadixSort::SortPairs(b.cub_sort, sb, b.keys_in, b.keys_out, b.vals_in,

@@ -159,7 +159,8 @@ class Stage1Trainer:
                         ("status", self.status), ("geom", self.geom),
                         ("loss_scratch", self.loss_scratch)):
             setattr(s, name, ptr(t))
-        s.ntc_scratch = None
+        self.ntc_scratch = empty_bytes(self.lib.ss_apply_ntc_backward_bytes(s.n_in), dev)
+        s.ntc_scratch = ptr(self.ntc_scratch)
         self.s = s
         self.frame_begin()
 

@@ -107,11 +107,13 @@ def apply_ntc_backward(ctx: TransformContext, d_means_t, d_rotations_t, d_sh_t):
         _, gs, m, lay, tab, par = cache._dev()
         g_tab = torch.zeros_like(tab)
         g_par = torch.zeros_like(par)
+        scratch = torch.empty(max(lib.ss_apply_ntc_backward_bytes(n_in), 256), dtype=torch.uint8,
+                              device=dev)
         if n_in:
             _lib.check(lib.ss_apply_ntc_backward(C.byref(gs), C.byref(m), C.byref(dc.struct()),
                                                  n_in, ptr(rows), ptr(tab), ptr(par),
                                                  int(ctx.rotate_sh), ptr(dm), ptr(dr), ptr(ds),
-                                                 ptr(g_tab), ptr(g_par), None, stream()),
+                                                 ptr(g_tab), ptr(g_par), ptr(scratch), stream()),
                        "apply_ntc_backward")
         from .device import unpack_params
 
