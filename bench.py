@@ -122,13 +122,15 @@ def build_problem(cfg_idx, targets_on_device=True):
 # algorithmic bytes per phase: units x bytes/unit
 def phase_bytes(phase, n, n_in, K, pairs, P, ltf):
     return {
-        "ntc_forward_transform": n_in * (12 + 16 + 12 * K + 12 + 16 + 12 * (K - 1)) + 4 * ltf,
+        "ntc_forward_transform": n_in * (12 + 4 * 32 * 2 + 32) + 4 * ltf,
+        "transform": n_in * (32 + 12 + 16 + 12 * K + 12 + 16 + 12 * (K - 1)),
+        "transform_vjp": n_in * (32 + 16 + 12 + 16 + 24 * K + 32),
         "project": n * (12 + 16 + 12 + 4 + 12 * K) + n * 80,
         "blend_forward": P * 24 + pairs * 52,
         "loss": P * 12 * 3 + P * 12,
         "blend_backward": P * 20 + pairs * 52 + n * 36,
         "gaussian_backward": n * (12 + 16 + 12 + 4 + 12 * K + 36) + n * (12 + 16 + 12 * K + 5),
-        "ntc_backward": n_in * (12 + 16 + 12 * K + 12 + 16 + 12 * K) + 3 * 4 * ltf,
+        "ntc_backward": n_in * (4 * 32 * 2 + 32 + 12) + 3 * 4 * ltf,
         "tile_sort": pairs * 16 * 2,
         "adam": ltf * (4 * 3 + 16 * 2 + 1 / 2),
         "depth_sort": n * 12 * 2 * 2,
@@ -266,9 +268,10 @@ def main():
     if world > 1:
         dist.barrier()
     lib.ss_profile_enable(1)
-    names = [lib.ss_profile_name(i).decode() for i in range(13)]
+    nph = lib.ss_profile_count()
+    names = [lib.ss_profile_name(i).decode() for i in range(nph)]
     phase_ms = {n: [] for n in names}
-    buf = (np.ctypeslib.ctypes.c_double * 13)()
+    buf = (np.ctypeslib.ctypes.c_double * nph)()
     step_ms, pairs = [], []
     l0 = lib.ss_launch_count()
     with Clocks(local) as clk:
@@ -280,7 +283,7 @@ def main():
             e1.record()
             e1.synchronize()
             step_ms.append(e0.elapsed_time(e1))
-            lib.ss_profile_read(buf, 13)
+            lib.ss_profile_read(buf, nph)
             for i, n in enumerate(names):
                 if buf[i] >= 0:
                     phase_ms[n].append(buf[i])
@@ -322,7 +325,8 @@ def main():
                        "parallelism": f"view-sharded dp{world}" if world > 1 else "single",
                        "mean_tile_pairs": mean_pairs,
                        "l2": "flushed between timed steps (256 MB write)",
-                       "ntc": "16 levels x 2 features, 2^15 rows, MLP 32-64-64-7 fp32"},
+                       "ntc": "16 levels x 2 features, 2^15 rows, MLP 32-64-64-7",
+                       "decoder": ["fp32 FFMA", "tcgen05 3xTF32", "tcgen05 tf32"][lib.ss_get_mlp_mode()]},
             "gpu_launches": int(launches),
             "loss_last": tr.trainer.last_loss(),
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm,

@@ -118,6 +118,7 @@ int64_t ss_launch_count(void);
  * stream around each hot-path phase; ss_profile_read returns the ms of the
  * last instance of each phase (-1 when not run since the previous read). */
 int ss_profile_enable(int32_t on);
+int32_t ss_profile_count(void);
 const char* ss_profile_name(int32_t phase);
 int ss_profile_read(double* ms, int32_t n);
 
@@ -177,15 +178,8 @@ int ss_apply_ntc(const ss_grid* grid, const ss_mlp* mlp, const ss_cloud* src, in
 /* apply_ntc_backward (transform.py:99-135) chained with the NTC backward
  * (ntc.py:250-288): gradients on the transformed cloud -> += g_tables, g_params.
  * scratch: ss_apply_ntc_backward_bytes(n_in) bytes (the decoder output is
- * recomputed there).  The _stored variant takes the forward's out7 instead
- * and a caller buffer g_out7 (n_in, 7). */
+ * recomputed there). */
 size_t ss_apply_ntc_backward_bytes(int64_t n_in);
-int ss_apply_ntc_backward_stored(const ss_grid* grid, const ss_mlp* mlp, const ss_cloud* src,
-                                 int64_t n_in, const int32_t* rows, const float* tables,
-                                 const float* params, int32_t rotate_sh, const float* out7,
-                                 const float* d_means, const float* d_rotations,
-                                 const float* d_sh, float* g_out7, float* g_tables,
-                                 float* g_params, void* stream);
 int ss_apply_ntc_backward(const ss_grid* grid, const ss_mlp* mlp, const ss_cloud* src,
                           int64_t n_in, const int32_t* rows, const float* tables,
                           const float* params, int32_t rotate_sh, const float* d_means,
@@ -317,6 +311,16 @@ int ss_stage1_iter_finish(ss_stage1* st, const ss_camera* cam, const float* targ
 int ss_stage1_iter_grads(ss_stage1* st, const ss_camera* cam, const float* target,
                          int64_t n_pairs, float grad_scale, void* stream);
 int ss_stage1_apply_adam(ss_stage1* st, void* stream);
+
+/* device self-test of the tcgen05 building blocks: D (M x N) = opA . opB over
+ * K, flags bit0/bit1 = A/B given transposed (MN-major operand), row-major fp32
+ * device buffers (test infrastructure for the decoder kernels) */
+/* decoder arithmetic: 0 = fp32 FFMA, 1 = tcgen05 3xTF32 (fp32-accurate, default),
+ * 2 = tcgen05 tf32 */
+int ss_set_mlp_mode(int32_t mode);
+int32_t ss_get_mlp_mode(void);
+int ss_selftest_umma(int32_t M, int32_t N, int32_t K, int32_t flags, const float* A,
+                     const float* B, float* D, void* stream);
 
 #ifdef __cplusplus
 }

@@ -92,6 +92,7 @@ SIGNATURES = [
     ("ss_launch_count", I64, []),
     ("ss_profile_enable", I32, [I32]),
     ("ss_profile_name", C.c_char_p, [I32]),
+    ("ss_profile_count", I32, []),
     ("ss_profile_read", I32, [C.POINTER(D), I32]),
     ("ss_mlp_get_layout", I32, [PMlp, C.POINTER(MlpLayout)]),
     ("ss_ntc_encode", I32, [PGrid, I64, P, P, P, P, P]),
@@ -104,8 +105,6 @@ SIGNATURES = [
     ("ss_apply_ntc_backward", I32, [PGrid, PMlp, PCloud, I64, P, P, P, I32, P, P, P, P, P, P,
                                     P]),
     ("ss_apply_ntc_backward_bytes", SZ, [I64]),
-    ("ss_apply_ntc_backward_stored", I32, [PGrid, PMlp, PCloud, I64, P, P, P, I32, P, P, P, P,
-                                           P, P, P, P]),
     ("ss_transform_apply", I32, [PCloud, I64, P, P, I32, P, P, P, P, P]),
     ("ss_transform_vjp", I32, [PCloud, I64, P, P, I32, P, P, P, P, P]),
     ("ss_raster_geom_bytes", SZ, [I64, PCam, PSet]),
@@ -123,6 +122,9 @@ SIGNATURES = [
     ("ss_stage1_iter_finish", I32, [C.POINTER(Stage1), PCam, P, I64, P]),
     ("ss_stage1_iter_grads", I32, [C.POINTER(Stage1), PCam, P, I64, C.c_float, P]),
     ("ss_stage1_apply_adam", I32, [C.POINTER(Stage1), P]),
+    ("ss_set_mlp_mode", I32, [I32]),
+    ("ss_get_mlp_mode", I32, []),
+    ("ss_selftest_umma", I32, [I32, I32, I32, I32, P, P, P, P]),
 ]
 
 

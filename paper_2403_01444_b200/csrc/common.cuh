@@ -218,8 +218,39 @@ int raster_backward(const ss_cloud* cl, const ss_camera* cam, const ss_raster_se
 namespace ss {
 enum Phase {
   PH_NTC_FWD = 0, PH_PROJECT, PH_DEPTH_SORT, PH_RANK_SCAN, PH_DUPLICATE, PH_TILE_SORT,
-  PH_RANGES, PH_BLEND_FWD, PH_LOSS, PH_BLEND_BWD, PH_GAUSS_BWD, PH_NTC_BWD, PH_ADAM, PH_COUNT
+  PH_RANGES, PH_BLEND_FWD, PH_LOSS, PH_BLEND_BWD, PH_GAUSS_BWD, PH_NTC_BWD, PH_ADAM,
+  PH_TRANSFORM, PH_TRANSFORM_BWD, PH_COUNT
 };
 void prof_begin(int phase, cudaStream_t s);
 void prof_end(int phase, cudaStream_t s);
+
+// NTC pipeline pieces (ntc.cu): features X and their gradient dX are (n, xs)
+// row-major in HBM between the gather / decoder / scatter kernels; out7 and g7
+// are (n, 8) (or stride 7 on the reference-shaped API).
+struct NtcScratch {
+  float *X, *dX, *out7, *g7;
+  int xs;
+};
+size_t ntc_scratch_bytes(const ss_mlp* mlp, int64_t n);
+NtcScratch ntc_scratch(void* base, const ss_mlp* mlp, int64_t n);
+int ntc_forward_run(const ss_grid* g, const ss_mlp* mlp, int64_t n, const float* means,
+                    const int32_t* rows, const float* tables, const float* params, float* X, int xs,
+                    float* out, int os, uint32_t* status, cudaStream_t st);
+int ntc_backward_run(const ss_grid* g, const ss_mlp* mlp, int64_t n, const float* means,
+                     const int32_t* rows, const float* params, const float* X, int xs,
+                     const float* g_out, int gs, float* dX, float* g_tables, float* g_params,
+                     cudaStream_t st);
+int transform_run(const ss_cloud* src, int64_t n, const int32_t* rows, const float* out7, int os,
+                  int rotate_sh, float* tm, float* tr, float* ts, uint32_t* status,
+                  cudaStream_t st);
+int transform_vjp_run(const ss_cloud* src, int64_t n, const int32_t* rows, const float* out7, int os,
+                      int rotate_sh, const float* dm, const float* dr, const float* ds, float* g7,
+                      int gs, cudaStream_t st);
+}  // namespace ss
+
+// decoder on tensor cores (mlp_tc.cu); mode 0 = FFMA fp32, 1 = 3xTF32, 2 = tf32
+namespace ss {
+int mlp_mode();
+int mlp_fwd_tc(int in_pad, int n_hidden, int64_t n, const float* X, int xs, const float* params,
+               float* out, int os, cudaStream_t st);
 }  // namespace ss

@@ -155,7 +155,7 @@ static bool g_ev_ready = false, g_used[PH_COUNT];
 static const char* kPhaseNames[PH_COUNT] = {
     "ntc_forward_transform", "project", "depth_sort", "rank_scan", "duplicate", "tile_sort",
     "ranges", "blend_forward", "loss", "blend_backward", "gaussian_backward",
-    "ntc_backward", "adam"};
+    "ntc_backward", "adam", "transform", "transform_vjp"};
 
 void prof_begin(int phase, cudaStream_t s) {
   if (!g_prof) return;
@@ -183,6 +183,8 @@ const char* ss_profile_name(int32_t phase) {
 }
 /* ms of the last recorded instance of each phase (-1 if not recorded since the
  * previous read); synchronises on the recorded events. */
+int32_t ss_profile_count(void) { return ss::PH_COUNT; }
+
 int ss_profile_read(double* ms, int32_t n) {
   for (int p = 0; p < n && p < ss::PH_COUNT; ++p) {
     ms[p] = -1.0;

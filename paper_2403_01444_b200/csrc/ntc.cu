@@ -1,6 +1,8 @@
-// Neural Transformation Cache on sm_100a: hash-grid encode (K1f), fused
-// decoder + transform (K2f/K3f), fused transform/decoder backward with the
-// hash-table scatter (K3b/K2b/K1b), and the lazy Adam step (KA).
+// Neural Transformation Cache on sm_100a: hash-grid encode/gather (K1f),
+// decoder (K2f), transform (K3f), transform VJP (K3b), decoder backward (K2b),
+// hash-table scatter (K1b) and the lazy Adam step (KA).  Features X and their
+// gradient dX live in HBM between the kernels so each stage runs at its own
+// occupancy (thread per Gaussian x level for the gather/scatter).
 //
 // Reference: ntc.py:161-293, transform.py:53-135, optim.py:33-66
 // (/root/reference/pkg/src/splatstream/).
@@ -84,164 +86,6 @@ __device__ inline void level_corners(const ss_grid& g, int l, const double xn[3]
     } else {
       // int64 (x*1 ^ y*2654435761 ^ z*805459861) % T == uint32-wrap & (T-1)
       idx[k] = (cx ^ (cy * 2654435761u) ^ (cz * 805459861u)) & (T - 1u);
-    }
-  }
-}
-
-// Interpolated features (ntc.py:205-216), zero-padded to IN.
-template <int IN>
-__device__ inline void gather_features(const ss_grid& g, const float* __restrict__ tables,
-                                       const double xn[3], float (&x)[IN]) {
-#pragma unroll
-  for (int i = 0; i < IN; ++i) x[i] = 0.f;
-  const int F = g.n_features;
-  const size_t T = (size_t)1 << g.log2_table;
-  if (F == 2) {
-#pragma unroll
-    for (int l = 0; l < IN / 2; ++l) {
-      if (l < g.n_levels) {
-        uint32_t idx[8];
-        float w[8];
-        level_corners(g, l, xn, idx, w);
-        const float2* tl = reinterpret_cast<const float2*>(tables + (size_t)l * T * 2);
-        float a0 = 0.f, a1 = 0.f;
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          float2 v = __ldg(tl + idx[k]);
-          a0 = fmaf(w[k], v.x, a0);
-          a1 = fmaf(w[k], v.y, a1);
-        }
-        x[2 * l] = a0;
-        x[2 * l + 1] = a1;
-      }
-    }
-    return;
-  }
-  for (int l = 0; l < g.n_levels; ++l) {
-    uint32_t idx[8];
-    float w[8];
-    level_corners(g, l, xn, idx, w);
-    const float* tl = tables + (size_t)l * T * F;
-    for (int f = 0; f < F; ++f) {
-      float a = 0.f;
-#pragma unroll
-      for (int k = 0; k < 8; ++k) a = fmaf(w[k], __ldg(tl + (size_t)idx[k] * F + f), a);
-#pragma unroll
-      for (int i = 0; i < IN; ++i)
-        if (i == l * F + f) x[i] = a;
-    }
-  }
-}
-
-// Hash-table scatter of a feature gradient (ntc.py:278-288).
-template <int IN>
-__device__ inline void scatter_features(const ss_grid& g, float* __restrict__ g_tables,
-                                        const double xn[3], const float (&dx)[IN]) {
-  const int F = g.n_features;
-  const size_t T = (size_t)1 << g.log2_table;
-  if (F == 2) {
-#pragma unroll
-    for (int l = 0; l < IN / 2; ++l) {
-      if (l < g.n_levels) {
-        uint32_t idx[8];
-        float w[8];
-        level_corners(g, l, xn, idx, w);
-        float* gl = g_tables + (size_t)l * T * 2;
-        const float f0 = dx[2 * l], f1 = dx[2 * l + 1];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) red_add_v2(gl + 2 * (size_t)idx[k], w[k] * f0, w[k] * f1);
-      }
-    }
-    return;
-  }
-  for (int l = 0; l < g.n_levels; ++l) {
-    uint32_t idx[8];
-    float w[8];
-    level_corners(g, l, xn, idx, w);
-    float* gl = g_tables + (size_t)l * T * F;
-    for (int f = 0; f < F; ++f) {
-      float fv = 0.f;
-#pragma unroll
-      for (int k = 0; k < IN; ++k)
-        if (k == l * F + f) fv = dx[k];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) atomicAdd(gl + (size_t)idx[k] * F + f, w[k] * fv);
-    }
-  }
-}
-
-// Features of one point written into a shared-memory row (zero-padded to
-// `width`); the level loop is deliberately not unrolled.
-__device__ inline void gather_to_row(const ss_grid& g, const float* __restrict__ tables,
-                                     const double xn[3], float* row, int width) {
-  const int F = g.n_features;
-  const size_t T = (size_t)1 << g.log2_table;
-#pragma unroll 1
-  for (int l = 0; l < g.n_levels; ++l) {
-    uint32_t idx[8];
-    float w[8];
-    level_corners(g, l, xn, idx, w);
-    const float* tl = tables + (size_t)l * T * F;
-    if (F == 2) {
-      float a0 = 0.f, a1 = 0.f;
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const float2 v = __ldg(reinterpret_cast<const float2*>(tl) + idx[k]);
-        a0 = fmaf(w[k], v.x, a0);
-        a1 = fmaf(w[k], v.y, a1);
-      }
-      row[2 * l] = a0;
-      row[2 * l + 1] = a1;
-    } else {
-      for (int f = 0; f < F; ++f) {
-        float a = 0.f;
-#pragma unroll
-        for (int k = 0; k < 8; ++k) a = fmaf(w[k], __ldg(tl + (size_t)idx[k] * F + f), a);
-        row[l * F + f] = a;
-      }
-    }
-  }
-  for (int k = g.n_levels * F; k < width; ++k) row[k] = 0.f;
-}
-
-// dx_j = W0[j,:] . d1 for the features of each level, scattered with vector
-// reductions into the table gradient (level loop not unrolled).
-template <int IN>
-__device__ inline void scatter_rows(const ss_grid& g, const float* __restrict__ w0,
-                                    const float (&d1)[HID], const double xn[3],
-                                    float* __restrict__ g_tables) {
-  const int F = g.n_features;
-  const size_t T = (size_t)1 << g.log2_table;
-#pragma unroll 1
-  for (int l = 0; l < g.n_levels; ++l) {
-    uint32_t idx[8];
-    float w[8];
-    level_corners(g, l, xn, idx, w);
-    float* gl = g_tables + (size_t)l * T * F;
-    for (int f0 = 0; f0 < F; f0 += 2) {
-      float dv[2] = {0.f, 0.f};
-      for (int u = 0; u < 2 && f0 + u < F; ++u) {
-        const float4* w4 = reinterpret_cast<const float4*>(w0 + (l * F + f0 + u) * HID);
-        float s = 0.f;
-#pragma unroll
-        for (int q = 0; q < HID / 4; ++q) {
-          const float4 ww = w4[q];
-          s = fmaf(ww.x, d1[4 * q], s);
-          s = fmaf(ww.y, d1[4 * q + 1], s);
-          s = fmaf(ww.z, d1[4 * q + 2], s);
-          s = fmaf(ww.w, d1[4 * q + 3], s);
-        }
-        dv[u] = s;
-      }
-      if (F - f0 >= 2 && (F % 2) == 0) {
-#pragma unroll
-        for (int k = 0; k < 8; ++k)
-          red_add_v2(gl + (size_t)idx[k] * F + f0, w[k] * dv[0], w[k] * dv[1]);
-      } else {
-        for (int u = 0; u < 2 && f0 + u < F; ++u)
-#pragma unroll
-          for (int k = 0; k < 8; ++k) atomicAdd(gl + (size_t)idx[k] * F + f0 + u, w[k] * dv[u]);
-      }
     }
   }
 }
@@ -394,10 +238,11 @@ __device__ inline void band_matrix_vjp(const float R[3][3], const float gM[B][B]
 
 __device__ __constant__ int c_perm[3] = {1, 2, 0};  // (y, z, x) basis order, sh.py:30-32
 
-// sh_out bands 1..deg = M_l(R) sh_in (transform.py:80-84; band 1 = P R P^T)
-__device__ inline void rotate_sh_bands(int deg, const float R[3][3], const float* __restrict__ in,
-                                 float* __restrict__ out) {
-  if (deg >= 1) {
+// sh_out bands 1..DEG = M_l(R) sh_in (transform.py:80-84; band 1 = P R P^T).
+// Coefficient arrays are (K, 3) with compile-time K so they stay in registers.
+template <int DEG>
+__device__ inline void rotate_sh_bands(const float R[3][3], const float* in, float* out) {
+  if (DEG >= 1) {
 #pragma unroll
     for (int a = 0; a < 3; ++a)
 #pragma unroll
@@ -408,10 +253,12 @@ __device__ inline void rotate_sh_bands(int deg, const float R[3][3], const float
         out[(1 + a) * 3 + c] = s;
       }
   }
-  if (deg >= 2) {
+  if (DEG >= 2) {
     float M[5][5];
     band_matrix<5>(R, M);
+#pragma unroll
     for (int a = 0; a < 5; ++a)
+#pragma unroll
       for (int c = 0; c < 3; ++c) {
         float s = 0.f;
 #pragma unroll
@@ -419,10 +266,12 @@ __device__ inline void rotate_sh_bands(int deg, const float R[3][3], const float
         out[(4 + a) * 3 + c] = s;
       }
   }
-  if (deg >= 3) {
+  if (DEG >= 3) {
     float M[7][7];
     band_matrix<7>(R, M);
+#pragma unroll
     for (int a = 0; a < 7; ++a)
+#pragma unroll
       for (int c = 0; c < 3; ++c) {
         float s = 0.f;
 #pragma unroll
@@ -433,10 +282,13 @@ __device__ inline void rotate_sh_bands(int deg, const float R[3][3], const float
 }
 
 // g_R from g_out (bands >= 1) and the source coefficients (transform.py:120-127)
-__device__ inline void rotate_sh_bands_vjp(int deg, const float R[3][3], const float* __restrict__ g,
-                                     const float* __restrict__ in, float gR[3][3]) {
-  if (deg >= 1) {
+template <int DEG>
+__device__ inline void rotate_sh_bands_vjp(const float R[3][3], const float* g, const float* in,
+                                           float gR[3][3]) {
+  if (DEG >= 1) {
+#pragma unroll
     for (int a = 0; a < 3; ++a)
+#pragma unroll
       for (int b = 0; b < 3; ++b) {
         float s = 0.f;
 #pragma unroll
@@ -444,9 +296,11 @@ __device__ inline void rotate_sh_bands_vjp(int deg, const float R[3][3], const f
         gR[c_perm[a]][c_perm[b]] += s;  // P^T gM P
       }
   }
-  if (deg >= 2) {
+  if (DEG >= 2) {
     float gM[5][5];
+#pragma unroll
     for (int a = 0; a < 5; ++a)
+#pragma unroll
       for (int b = 0; b < 5; ++b) {
         float s = 0.f;
 #pragma unroll
@@ -455,9 +309,11 @@ __device__ inline void rotate_sh_bands_vjp(int deg, const float R[3][3], const f
       }
     band_matrix_vjp<5>(R, gM, gR);
   }
-  if (deg >= 3) {
+  if (DEG >= 3) {
     float gM[7][7];
+#pragma unroll
     for (int a = 0; a < 7; ++a)
+#pragma unroll
       for (int b = 0; b < 7; ++b) {
         float s = 0.f;
 #pragma unroll
@@ -504,14 +360,124 @@ __global__ void touched_kernel(ss_grid g, int64_t n, const float* __restrict__ m
   }
 }
 
-// transform (transform.py:70-84): mu' = mu + d_mu, q' = norm(d_q) (x) q_src,
-// SH bands >= 1 rotated by R(norm(d_q)).
-__device__ inline void apply_transform(const ss_cloud& src, int64_t gid, const float* o,
-                                       int rotate_sh, float* __restrict__ t_means,
-                                       float* __restrict__ t_rot, float* __restrict__ t_sh,
-                                       uint32_t* status) {
+// K1f: interpolated features, one thread per (row, level) (ntc.py:176-216).
+// X is (n, xs) row-major; the level-0 thread zero-fills the padding columns.
+__global__ void gather_kernel(ss_grid g, int64_t n, const float* __restrict__ means,
+                              const int32_t* __restrict__ rows, const float* __restrict__ tables,
+                              float* __restrict__ X, int xs, uint32_t* status) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int L = g.n_levels;
+  if (t >= n * L) return;
+  const int64_t i = t / L;
+  const int l = (int)(t - i * L);
+  const int64_t gid = rows ? rows[i] : i;
+  double xn[3];
+  if (!normalise(g, means + 3 * gid, xn) && status && l == 0) atomicOr(status, SS_FLAG_OUTSIDE);
+  uint32_t idx[8];
+  float w[8];
+  level_corners(g, l, xn, idx, w);
+  const int F = g.n_features;
+  const size_t T = (size_t)1 << g.log2_table;
+  const float* tl = tables + (size_t)l * T * F;
+  float* xr = X + i * xs;
+  if (F == 2) {
+    float a0 = 0.f, a1 = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const float2 v = __ldg(reinterpret_cast<const float2*>(tl) + idx[k]);
+      a0 = fmaf(w[k], v.x, a0);
+      a1 = fmaf(w[k], v.y, a1);
+    }
+    *reinterpret_cast<float2*>(xr + 2 * l) = make_float2(a0, a1);
+  } else {
+    for (int f = 0; f < F; ++f) {
+      float a = 0.f;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) a = fmaf(w[k], __ldg(tl + (size_t)idx[k] * F + f), a);
+      xr[l * F + f] = a;
+    }
+  }
+  if (l == 0)
+    for (int k = L * F; k < xs; ++k) xr[k] = 0.f;
+}
+
+// K1b: table scatter of the feature gradient, one thread per (row, level)
+// (ntc.py:278-288), vector reductions into L2-resident tables.
+__global__ void scatter_kernel(ss_grid g, int64_t n, const float* __restrict__ means,
+                               const int32_t* __restrict__ rows, const float* __restrict__ dX,
+                               int xs, float* __restrict__ g_tables) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int L = g.n_levels;
+  if (t >= n * L) return;
+  const int64_t i = t / L;
+  const int l = (int)(t - i * L);
+  const int64_t gid = rows ? rows[i] : i;
+  double xn[3];
+  normalise(g, means + 3 * gid, xn);
+  uint32_t idx[8];
+  float w[8];
+  level_corners(g, l, xn, idx, w);
+  const int F = g.n_features;
+  const size_t T = (size_t)1 << g.log2_table;
+  float* gl = g_tables + (size_t)l * T * F;
+  const float* dr = dX + i * xs + l * F;
+  if (F == 2) {
+    const float2 d = *reinterpret_cast<const float2*>(dr);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) red_add_v2(gl + 2 * (size_t)idx[k], w[k] * d.x, w[k] * d.y);
+  } else {
+    for (int f = 0; f < F; ++f) {
+      const float d = dr[f];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) atomicAdd(gl + (size_t)idx[k] * F + f, w[k] * d);
+    }
+  }
+}
+
+// K2f: decoder, one thread per row, weights broadcast from smem (ntc.py:241-248).
+template <int IN, int NL>
+__global__ void __launch_bounds__(128) mlp_fwd_kernel(int64_t n, const float* __restrict__ X,
+                                                      int xs, const float* __restrict__ params,
+                                                      float* __restrict__ out, int os) {
+  extern __shared__ __align__(16) float smem[];
+  load_params<Lay<IN, NL>::TOTAL>(smem, params);
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  float x[IN], h1[HID], h2[HID], o[OUTP];
+#pragma unroll
+  for (int k = 0; k < IN; k += 4) {
+    const float4 v = *reinterpret_cast<const float4*>(X + i * xs + k);
+    x[k] = v.x, x[k + 1] = v.y, x[k + 2] = v.z, x[k + 3] = v.w;
+  }
+  mlp_forward<IN, NL>(smem, x, h1, h2, o);
+  if (os == 8) {
+    *reinterpret_cast<float4*>(out + i * 8) = make_float4(o[0], o[1], o[2], o[3]);
+    *reinterpret_cast<float4*>(out + i * 8 + 4) = make_float4(o[4], o[5], o[6], 0.f);
+  } else {
+#pragma unroll
+    for (int k = 0; k < 7; ++k) out[i * os + k] = o[k];
+  }
+}
+
+// K3f: transform (transform.py:70-84): mu' = mu + d_mu, q' = norm(d_q) (x) q_src,
+// SH bands >= 1 rotated by R(norm(d_q)); one thread per inside row.
+template <int DEG>
+__global__ void __launch_bounds__(128) transform_kernel(ss_cloud src, int64_t n,
+                                                        const int32_t* __restrict__ rows,
+                                                        const float* __restrict__ out7, int os,
+                                                        int rotate_sh, float* __restrict__ t_means,
+                                                        float* __restrict__ t_rot,
+                                                        float* __restrict__ t_sh,
+                                                        uint32_t* status) {
+  constexpr int K = (DEG + 1) * (DEG + 1);
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t gid = rows ? rows[i] : i;
+  float o[7];
+#pragma unroll
+  for (int k = 0; k < 7; ++k) o[k] = out7[i * os + k];
   float nq = sqrtf(o[3] * o[3] + o[4] * o[4] + o[5] * o[5] + o[6] * o[6]);
-  if (nq < 1e-12f) {
+  if (nq < 1e-12f) {  // gaussians.py:46-47
     if (status) atomicOr(status, SS_FLAG_ZERO_QUAT);
     nq = 1.f;
   }
@@ -520,85 +486,54 @@ __device__ inline void apply_transform(const ss_cloud& src, int64_t gid, const f
   t_means[3 * gid + 0] = m[0] + o[0];
   t_means[3 * gid + 1] = m[1] + o[1];
   t_means[3 * gid + 2] = m[2] + o[2];
-  float qs[4], qo[4];
-#pragma unroll
-  for (int k = 0; k < 4; ++k) qs[k] = src.rotations[4 * gid + k];
+  const float4 q = *reinterpret_cast<const float4*>(src.rotations + 4 * gid);
+  const float qs[4] = {q.x, q.y, q.z, q.w};
+  float qo[4];
   quat_mul(u, qs, qo);
-#pragma unroll
-  for (int k = 0; k < 4; ++k) t_rot[4 * gid + k] = qo[k];
-  const int K = src.sh_coeffs;
-  const int deg = sh_degree_of(K);
-  if (rotate_sh && deg >= 1) {
+  *reinterpret_cast<float4*>(t_rot + 4 * gid) = make_float4(qo[0], qo[1], qo[2], qo[3]);
+  if (DEG >= 1 && rotate_sh) {
     float R[3][3];
     quat_to_rot(u[0], u[1], u[2], u[3], R);
-    float in[48], outv[48];
+    float in[3 * K], outv[3 * K];
+#pragma unroll
     for (int k = 3; k < 3 * K; ++k) in[k] = src.sh[gid * 3 * K + k];
-    rotate_sh_bands(deg, R, in, outv);
+    rotate_sh_bands<DEG>(R, in, outv);
+#pragma unroll
     for (int k = 3; k < 3 * K; ++k) t_sh[gid * 3 * K + k] = outv[k];
   }
 }
 
-// NTC forward (+ transform when `src` given).  One thread per Gaussian.
-template <int IN, int NL>
-__global__ void __launch_bounds__(128) ntc_forward_kernel(
-    ss_grid g, int64_t n, const float* __restrict__ means, const int32_t* __restrict__ rows,
-    const float* __restrict__ tables, const float* __restrict__ params, float* __restrict__ out7,
-    float* __restrict__ feats, ss_cloud src, int rotate_sh, float* __restrict__ t_means,
-    float* __restrict__ t_rot, float* __restrict__ t_sh, uint32_t* status) {
-  extern __shared__ __align__(16) float smem[];
-  load_params<Lay<IN, NL>::TOTAL>(smem, params);
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+// K3b: dL/d[d_mu | d_q] from transformed-cloud gradients (transform.py:111-134)
+template <int DEG>
+__global__ void __launch_bounds__(128) transform_vjp_kernel(
+    ss_cloud src, int64_t n, const int32_t* __restrict__ rows, const float* __restrict__ out7,
+    int os, int rotate_sh, const float* __restrict__ d_means, const float* __restrict__ d_rot,
+    const float* __restrict__ d_sh, float* __restrict__ g7, int gs) {
+  constexpr int K = (DEG + 1) * (DEG + 1);
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   const int64_t gid = rows ? rows[i] : i;
-  double xn[3];
-  if (!normalise(g, means + 3 * gid, xn) && status) atomicOr(status, SS_FLAG_OUTSIDE);
-  float x[IN], h1[HID], h2[HID], o[OUTP];
-  gather_features<IN>(g, tables, xn, x);
-  if (feats) {
-    const int nf = g.n_levels * g.n_features;
+  float o[7];
 #pragma unroll
-    for (int k = 0; k < IN; ++k)
-      if (k < nf) feats[i * nf + k] = x[k];
-  }
-  mlp_forward<IN, NL>(smem, x, h1, h2, o);
-  if (out7) {
-#pragma unroll
-    for (int k = 0; k < 7; ++k) out7[i * 7 + k] = o[k];
-  }
-  if (!t_means) return;
-  apply_transform(src, gid, o, rotate_sh, t_means, t_rot, t_sh, status);
-}
-
-// dL/d(out7) from transformed-cloud gradients (transform.py:111-134)
-__device__ inline void transform_vjp(const ss_cloud& src, int64_t gid, const float o[OUTP],
-                                     int rotate_sh, const float* __restrict__ d_means,
-                                     const float* __restrict__ d_rot,
-                                     const float* __restrict__ d_sh, float g7[OUTP]) {
-  g7[0] = d_means[3 * gid];
-  g7[1] = d_means[3 * gid + 1];
-  g7[2] = d_means[3 * gid + 2];
-  g7[7] = 0.f;
-  float q[4], gr[4];
-#pragma unroll
-  for (int k = 0; k < 4; ++k) q[k] = src.rotations[4 * gid + k], gr[k] = d_rot[4 * gid + k];
+  for (int k = 0; k < 7; ++k) o[k] = out7[i * os + k];
+  const float4 q = *reinterpret_cast<const float4*>(src.rotations + 4 * gid);
+  const float4 gr = *reinterpret_cast<const float4*>(d_rot + 4 * gid);
   // g_u = A(q_src)^T g_rot, A rows: [w,-x,-y,-z],[x,w,z,-y],[y,-z,w,x],[z,y,-x,w]
-  const float w = q[0], x = q[1], y = q[2], z = q[3];
   float gu[4];
-  gu[0] = w * gr[0] + x * gr[1] + y * gr[2] + z * gr[3];
-  gu[1] = -x * gr[0] + w * gr[1] - z * gr[2] + y * gr[3];
-  gu[2] = -y * gr[0] + z * gr[1] + w * gr[2] - x * gr[3];
-  gu[3] = -z * gr[0] - y * gr[1] + x * gr[2] + w * gr[3];
+  gu[0] = q.x * gr.x + q.y * gr.y + q.z * gr.z + q.w * gr.w;
+  gu[1] = -q.y * gr.x + q.x * gr.y - q.w * gr.z + q.z * gr.w;
+  gu[2] = -q.z * gr.x + q.w * gr.y + q.x * gr.z - q.y * gr.w;
+  gu[3] = -q.w * gr.x - q.z * gr.y + q.y * gr.z + q.x * gr.w;
   float nq = sqrtf(o[3] * o[3] + o[4] * o[4] + o[5] * o[5] + o[6] * o[6]);
   nq = nq < 1e-12f ? 1.f : nq;
   const float u[4] = {o[3] / nq, o[4] / nq, o[5] / nq, o[6] / nq};
-  const int K = src.sh_coeffs;
-  const int deg = sh_degree_of(K);
-  if (rotate_sh && deg >= 1) {
+  if (DEG >= 1 && rotate_sh) {
     float R[3][3], gR[3][3] = {{0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}};
     quat_to_rot(u[0], u[1], u[2], u[3], R);
-    float in[48], gs[48];
-    for (int k = 3; k < 3 * K; ++k) in[k] = src.sh[gid * 3 * K + k], gs[k] = d_sh[gid * 3 * K + k];
-    rotate_sh_bands_vjp(deg, R, gs, in, gR);
+    float in[3 * K], gsh[3 * K];
+#pragma unroll
+    for (int k = 3; k < 3 * K; ++k) in[k] = src.sh[gid * 3 * K + k], gsh[k] = d_sh[gid * 3 * K + k];
+    rotate_sh_bands_vjp<DEG>(R, gsh, in, gR);
     float gq[4];
     quat_to_rot_vjp(u[0], u[1], u[2], u[3], gR, gq);
 #pragma unroll
@@ -606,41 +541,19 @@ __device__ inline void transform_vjp(const ss_cloud& src, int64_t gid, const flo
   }
   // (I - u u^T)/|q| (gaussians.py:109-117)
   const float dot = u[0] * gu[0] + u[1] * gu[1] + u[2] * gu[2] + u[3] * gu[3];
+  float r[8] = {d_means[3 * gid], d_means[3 * gid + 1], d_means[3 * gid + 2], 0.f, 0.f, 0.f, 0.f,
+                0.f};
 #pragma unroll
-  for (int k = 0; k < 4; ++k) g7[3 + k] = (gu[k] - u[k] * dot) / nq;
+  for (int k = 0; k < 4; ++k) r[3 + k] = (gu[k] - u[k] * dot) / nq;
+  if (gs == 8) {
+    *reinterpret_cast<float4*>(g7 + i * 8) = make_float4(r[0], r[1], r[2], r[3]);
+    *reinterpret_cast<float4*>(g7 + i * 8 + 4) = make_float4(r[4], r[5], r[6], 0.f);
+  } else {
+#pragma unroll
+    for (int k = 0; k < 7; ++k) g7[i * gs + k] = r[k];
+  }
 }
 
-__global__ void transform_apply_kernel(ss_cloud src, int64_t n, const int32_t* __restrict__ rows,
-                                       const float* __restrict__ out7, int rotate_sh,
-                                       float* __restrict__ tm, float* __restrict__ tr,
-                                       float* __restrict__ ts, uint32_t* status) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  float o[OUTP];
-#pragma unroll
-  for (int k = 0; k < 7; ++k) o[k] = out7[i * 7 + k];
-  o[7] = 0.f;
-  apply_transform(src, rows ? rows[i] : i, o, rotate_sh, tm, tr, ts, status);
-}
-
-__global__ void transform_vjp_kernel(ss_cloud src, int64_t n, const int32_t* __restrict__ rows,
-                                     const float* __restrict__ out7, int rotate_sh,
-                                     const float* __restrict__ dm, const float* __restrict__ dr,
-                                     const float* __restrict__ ds, float* __restrict__ g_out7) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  float o[OUTP], g7[OUTP];
-#pragma unroll
-  for (int k = 0; k < 7; ++k) o[k] = out7[i * 7 + k];
-  o[7] = 0.f;
-  transform_vjp(src, rows ? rows[i] : i, o, rotate_sh, dm, dr, ds, g7);
-#pragma unroll
-  for (int k = 0; k < 7; ++k) g_out7[i * 7 + k] = g7[k];
-}
-
-// Backward: one thread per Gaussian per chunk; the decoder's weight gradient
-// is a CTA-level GEMM over the chunk (register-blocked 4x4 tiles), the
-// feature gradient is scattered into the tables with vector reductions.
 template <int IN, int NL>
 struct BwdSmem {
   static constexpr int SX = IN + 4, SH = HID + 4, SG = OUTP + 4;
@@ -703,12 +616,15 @@ __device__ inline TaskDesc<IN, NL> decode_task(int t) {
   return d;
 }
 
+// K2b: decoder backward.  Persistent CTAs walk 128-row chunks: each thread
+// recomputes its row's hidden layers from X (staged through its shared-memory
+// rows), back-propagates g7 to dX (written to HBM for the scatter kernel), and
+// the CTA reduces the weight gradient over the chunk with register-blocked
+// 4x4 tiles flushed by vector reductions (ntc.py:258-276).
 template <int IN, int NL>
-__global__ void __launch_bounds__(kChunk, 1) ntc_backward_kernel(
-    ss_grid g, int64_t n, const float* __restrict__ means, const int32_t* __restrict__ rows,
-    const float* __restrict__ tables, const float* __restrict__ params,
-    const float* __restrict__ g_out7,  // (n,7) upstream dL/d[d_mu | d_q]
-    float* __restrict__ g_tables, float* __restrict__ g_params) {
+__global__ void __launch_bounds__(kChunk, 1) mlp_bwd_kernel(
+    int64_t n, const float* __restrict__ X, int xs, const float* __restrict__ g_out, int gs,
+    const float* __restrict__ params, float* __restrict__ dX, float* __restrict__ g_params) {
   using S = BwdSmem<IN, NL>;
   using L = Lay<IN, NL>;
   extern __shared__ __align__(16) float smem[];
@@ -724,13 +640,10 @@ __global__ void __launch_bounds__(kChunk, 1) ntc_backward_kernel(
     float* sD2 = smem + S::oD2 + tid * S::SH;
     float* sG = smem + S::oG + tid * S::SG;
     if (i < n) {
-      const int64_t gid = rows ? rows[i] : i;
-      double xn[3];
-      normalise(g, means + 3 * gid, xn);
-      // recompute the hidden activations, staging each layer through this
-      // thread's shared-memory rows so at most two 64-vectors live in registers
       uint64_t mask1 = 0, mask2 = 0;
-      gather_to_row(g, tables, xn, sX, IN);  // level loop not unrolled (register budget)
+#pragma unroll
+      for (int k = 0; k < IN; k += 4)
+        *reinterpret_cast<float4*>(sX + k) = *reinterpret_cast<const float4*>(X + i * xs + k);
       {
         float h[HID];
 #pragma unroll
@@ -787,11 +700,10 @@ __global__ void __launch_bounds__(kChunk, 1) ntc_backward_kernel(
       }
       float g7[OUTP];
 #pragma unroll
-      for (int k = 0; k < 7; ++k) g7[k] = g_out7[i * 7 + k];
+      for (int k = 0; k < 7; ++k) g7[k] = g_out[i * gs + k];
       g7[7] = 0.f;
       *reinterpret_cast<float4*>(sG) = make_float4(g7[0], g7[1], g7[2], g7[3]);
       *reinterpret_cast<float4*>(sG + 4) = make_float4(g7[4], g7[5], g7[6], g7[7]);
-      // delta through the output layer: dl = (W2 g7) * (h_last > 0)
       float d1[HID];
       {
         float* sDl = NL == 2 ? sD2 : sD1;
@@ -807,7 +719,6 @@ __global__ void __launch_bounds__(kChunk, 1) ntc_backward_kernel(
         for (int k = 0; k < HID; k += 4)
           *reinterpret_cast<float4*>(sDl + k) = make_float4(d1[k], d1[k + 1], d1[k + 2], d1[k + 3]);
         if (NL == 2) {
-          // d1 = (W1 dl) * (h1 > 0), dl read back from its shared row
 #pragma unroll
           for (int k = 0; k < HID; ++k) d1[k] = 0.f;
 #pragma unroll 4
@@ -824,9 +735,26 @@ __global__ void __launch_bounds__(kChunk, 1) ntc_backward_kernel(
                 make_float4(d1[k], d1[k + 1], d1[k + 2], d1[k + 3]);
         }
       }
-      // feature gradient dx = W0 d1, computed per level and scattered into the
-      // tables (ntc.py:278-288)
-      scatter_rows<IN>(g, smem + L::W0, d1, xn, g_tables);
+      // feature gradient dX = W0 d1 -> HBM for the scatter kernel
+#pragma unroll
+      for (int r0 = 0; r0 < IN; r0 += 4) {
+        float dv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const float4* w4 = reinterpret_cast<const float4*>(smem + L::W0 + (r0 + u) * HID);
+          float s = 0.f;
+#pragma unroll
+          for (int q = 0; q < HID / 4; ++q) {
+            const float4 w = w4[q];
+            s = fmaf(w.x, d1[4 * q], s);
+            s = fmaf(w.y, d1[4 * q + 1], s);
+            s = fmaf(w.z, d1[4 * q + 2], s);
+            s = fmaf(w.w, d1[4 * q + 3], s);
+          }
+          dv[u] = s;
+        }
+        *reinterpret_cast<float4*>(dX + i * xs + r0) = make_float4(dv[0], dv[1], dv[2], dv[3]);
+      }
     } else {
       for (int k = 0; k < S::SX; ++k) sX[k] = 0.f;
       for (int k = 0; k < S::SH; ++k) {
@@ -837,8 +765,7 @@ __global__ void __launch_bounds__(kChunk, 1) ntc_backward_kernel(
       for (int k = 0; k < S::SG; ++k) sG[k] = 0.f;
     }
     __syncthreads();
-    // ---- CTA-level weight-gradient GEMM over the chunk (ntc.py:271-273),
-    // register-blocked 4x4 tiles, flushed with vector reductions
+    // ---- CTA-level weight-gradient GEMM over the chunk (ntc.py:271-273)
 #pragma unroll 1
     for (int s = 0; s < S::PER_THREAD; ++s) {
       const int t = tid + s * kChunk;
@@ -851,7 +778,7 @@ __global__ void __launch_bounds__(kChunk, 1) ntc_backward_kernel(
       if (d.a_off < 0) {
 #pragma unroll 4
         for (int r = 0; r < kChunk; ++r) {
-          float4 v = *reinterpret_cast<const float4*>(pd + r * d.d_stride);
+          const float4 v = *reinterpret_cast<const float4*>(pd + r * d.d_stride);
           acc[0] += v.x;
           acc[1] += v.y;
           acc[2] += v.z;
@@ -862,8 +789,8 @@ __global__ void __launch_bounds__(kChunk, 1) ntc_backward_kernel(
         const float* pa = smem + d.a_off;
 #pragma unroll 4
         for (int r = 0; r < kChunk; ++r) {
-          float4 a = *reinterpret_cast<const float4*>(pa + r * d.a_stride);
-          float4 v = *reinterpret_cast<const float4*>(pd + r * d.d_stride);
+          const float4 a = *reinterpret_cast<const float4*>(pa + r * d.a_stride);
+          const float4 v = *reinterpret_cast<const float4*>(pd + r * d.d_stride);
           const float av[4] = {a.x, a.y, a.z, a.w};
 #pragma unroll
           for (int p = 0; p < 4; ++p) {
@@ -946,58 +873,170 @@ static int check_grid(const ss_grid* g, const ss_mlp* mlp) {
   return SS_OK;
 }
 
-struct FwdLaunch {
-  const ss_grid* g;
+static int in_pad_of(const ss_mlp* mlp) {
+  ss_mlp_layout L{};
+  ss_mlp_get_layout(mlp, &L);
+  return L.in_pad;
+}
+
+static int num_sms() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
+}
+
+struct MlpFwd {
   int64_t n;
-  const float* means;
-  const int32_t* rows;
-  const float *tables, *params;
-  float *out7, *feats;
-  ss_cloud src;
-  int rotate_sh;
-  float *tm, *tr, *ts;
-  uint32_t* status;
+  const float* X;
+  int xs;
+  const float* params;
+  float* out;
+  int os;
   cudaStream_t st;
   template <int IN, int NL>
   int run() {
-    if (n == 0) return SS_OK;
     const size_t smem = Lay<IN, NL>::TOTAL * sizeof(float);
-    auto k = ntc_forward_kernel<IN, NL>;
+    auto k = mlp_fwd_kernel<IN, NL>;
     SS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    prof_begin(PH_NTC_FWD, st);
-    k<<<(unsigned)cdiv(n, 128), 128, smem, st>>>(*g, n, means, rows, tables, params, out7, feats,
-                                                  src, rotate_sh, tm, tr, ts, status);
-    SS_CHECK_LAUNCH("ntc_forward_kernel");
-    prof_end(PH_NTC_FWD, st);
+    k<<<(unsigned)cdiv(n, 128), 128, smem, st>>>(n, X, xs, params, out, os);
+    SS_CHECK_LAUNCH("mlp_fwd_kernel");
     return SS_OK;
   }
 };
 
-struct BwdLaunch {
-  const ss_grid* g;
+struct MlpBwd {
   int64_t n;
-  const float* means;
-  const int32_t* rows;
-  const float *tables, *params, *g_out7;
-  float *g_tables, *g_params;
+  const float* X;
+  int xs;
+  const float* g;
+  int gs;
+  const float* params;
+  float *dX, *g_params;
   cudaStream_t st;
   template <int IN, int NL>
   int run() {
-    if (n == 0) return SS_OK;
     const size_t smem = BwdSmem<IN, NL>::FLOATS * sizeof(float);
-    auto k = ntc_backward_kernel<IN, NL>;
+    auto k = mlp_bwd_kernel<IN, NL>;
     SS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int64_t chunks = cdiv(n, kChunk);
-    const unsigned grid = (unsigned)std::min<int64_t>(chunks, sms);
-    prof_begin(PH_NTC_BWD, st);
-    k<<<grid, kChunk, smem, st>>>(*g, n, means, rows, tables, params, g_out7, g_tables,
-                                  g_params);
-    SS_CHECK_LAUNCH("ntc_backward_kernel");
-    prof_end(PH_NTC_BWD, st);
+    const unsigned grid = (unsigned)std::min<int64_t>(cdiv(n, kChunk), num_sms());
+    k<<<grid, kChunk, smem, st>>>(n, X, xs, g, gs, params, dX, g_params);
+    SS_CHECK_LAUNCH("mlp_bwd_kernel");
     return SS_OK;
+  }
+};
+
+size_t ntc_scratch_bytes(const ss_mlp* mlp, int64_t n) {
+  const int xs = mlp ? in_pad_of(mlp) : 64;
+  const size_t nn = (size_t)(n > 0 ? n : 1);
+  return 2 * align_up(nn * xs * sizeof(float)) + 2 * align_up(nn * 8 * sizeof(float));
+}
+
+NtcScratch ntc_scratch(void* base, const ss_mlp* mlp, int64_t n) {
+  NtcScratch s{};
+  s.xs = mlp ? in_pad_of(mlp) : 64;
+  Carve c(base);
+  const size_t nn = (size_t)(n > 0 ? n : 1);
+  s.X = c.take<float>(nn * s.xs);
+  s.dX = c.take<float>(nn * s.xs);
+  s.out7 = c.take<float>(nn * 8);
+  s.g7 = c.take<float>(nn * 8);
+  return s;
+}
+
+int ntc_forward_run(const ss_grid* g, const ss_mlp* mlp, int64_t n, const float* means,
+                    const int32_t* rows, const float* tables, const float* params, float* X, int xs,
+                    float* out, int os, uint32_t* status, cudaStream_t st) {
+  SS_TRY(check_grid(g, mlp));
+  if (n == 0) return SS_OK;
+  prof_begin(PH_NTC_FWD, st);
+  const int64_t threads = n * g->n_levels;
+  gather_kernel<<<(unsigned)cdiv(threads, 256), 256, 0, st>>>(*g, n, means, rows, tables, X, xs,
+                                                                status);
+  SS_CHECK_LAUNCH("gather_kernel");
+  if (mlp_mode() != 0)
+    SS_TRY(mlp_fwd_tc(xs, mlp->n_hidden, n, X, xs, params, out, os, st));  // tcgen05
+  else
+    SS_TRY(dispatch_mlp(mlp, MlpFwd{n, X, xs, params, out, os, st}));
+  prof_end(PH_NTC_FWD, st);
+  return SS_OK;
+}
+
+int ntc_backward_run(const ss_grid* g, const ss_mlp* mlp, int64_t n, const float* means,
+                     const int32_t* rows, const float* params, const float* X, int xs,
+                     const float* g_out, int gs, float* dX, float* g_tables, float* g_params,
+                     cudaStream_t st) {
+  SS_TRY(check_grid(g, mlp));
+  if (n == 0) return SS_OK;
+  prof_begin(PH_NTC_BWD, st);
+  SS_TRY(dispatch_mlp(mlp, MlpBwd{n, X, xs, g_out, gs, params, dX, g_params, st}));
+  const int64_t threads = n * g->n_levels;
+  scatter_kernel<<<(unsigned)cdiv(threads, 256), 256, 0, st>>>(*g, n, means, rows, dX, xs,
+                                                                 g_tables);
+  SS_CHECK_LAUNCH("scatter_kernel");
+  prof_end(PH_NTC_BWD, st);
+  return SS_OK;
+}
+
+int transform_run(const ss_cloud* src, int64_t n, const int32_t* rows, const float* out7, int os,
+                  int rotate_sh, float* tm, float* tr, float* ts, uint32_t* status,
+                  cudaStream_t st) {
+  if (!src || src->sh_coeffs < 1 || src->sh_coeffs > 16) {
+    set_error("transform: bad cloud");
+    return SS_ERR_DATA;
+  }
+  if (n == 0) return SS_OK;
+  SS_TRY(ensure_shrot_const());
+  prof_begin(PH_TRANSFORM, st);
+  const unsigned grid = (unsigned)cdiv(n, 128);
+  switch (sh_degree_of(src->sh_coeffs)) {
+    case 0: transform_kernel<0><<<grid, 128, 0, st>>>(*src, n, rows, out7, os, rotate_sh, tm, tr, ts, status); break;
+    case 1: transform_kernel<1><<<grid, 128, 0, st>>>(*src, n, rows, out7, os, rotate_sh, tm, tr, ts, status); break;
+    case 2: transform_kernel<2><<<grid, 128, 0, st>>>(*src, n, rows, out7, os, rotate_sh, tm, tr, ts, status); break;
+    default: transform_kernel<3><<<grid, 128, 0, st>>>(*src, n, rows, out7, os, rotate_sh, tm, tr, ts, status); break;
+  }
+  SS_CHECK_LAUNCH("transform_kernel");
+  prof_end(PH_TRANSFORM, st);
+  return SS_OK;
+}
+
+int transform_vjp_run(const ss_cloud* src, int64_t n, const int32_t* rows, const float* out7, int os,
+                      int rotate_sh, const float* dm, const float* dr, const float* ds, float* g7,
+                      int gs, cudaStream_t st) {
+  if (!src || src->sh_coeffs < 1 || src->sh_coeffs > 16) {
+    set_error("transform vjp: bad cloud");
+    return SS_ERR_DATA;
+  }
+  if (n == 0) return SS_OK;
+  SS_TRY(ensure_shrot_const());
+  prof_begin(PH_TRANSFORM_BWD, st);
+  const unsigned grid = (unsigned)cdiv(n, 128);
+  switch (sh_degree_of(src->sh_coeffs)) {
+    case 0: transform_vjp_kernel<0><<<grid, 128, 0, st>>>(*src, n, rows, out7, os, rotate_sh, dm, dr, ds, g7, gs); break;
+    case 1: transform_vjp_kernel<1><<<grid, 128, 0, st>>>(*src, n, rows, out7, os, rotate_sh, dm, dr, ds, g7, gs); break;
+    case 2: transform_vjp_kernel<2><<<grid, 128, 0, st>>>(*src, n, rows, out7, os, rotate_sh, dm, dr, ds, g7, gs); break;
+    default: transform_vjp_kernel<3><<<grid, 128, 0, st>>>(*src, n, rows, out7, os, rotate_sh, dm, dr, ds, g7, gs); break;
+  }
+  SS_CHECK_LAUNCH("transform_vjp_kernel");
+  prof_end(PH_TRANSFORM_BWD, st);
+  return SS_OK;
+}
+
+// stream-ordered temporary for the reference-shaped API entry points
+struct Temp {
+  void* p = nullptr;
+  cudaStream_t st;
+  explicit Temp(cudaStream_t s) : st(s) {}
+  int alloc(size_t bytes) {
+    SS_CUDA(cudaMallocAsync(&p, bytes, st));
+    return SS_OK;
+  }
+  ~Temp() {
+    if (p) cudaFreeAsync(p, st);
   }
 };
 
@@ -1028,13 +1067,32 @@ int ss_ntc_touched(const ss_grid* grid, int64_t n, const float* means, const int
   return SS_OK;
 }
 
+__global__ void copy_cols_kernel(int64_t n, const float* __restrict__ src, int ss, int cols,
+                                 float* __restrict__ dst, int ds) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= n * cols) return;
+  const int64_t i = t / cols;
+  const int c = (int)(t - i * cols);
+  dst[i * ds + c] = src[i * ss + c];
+}
+
 int ss_ntc_forward(const ss_grid* grid, const ss_mlp* mlp, int64_t n, const float* means,
                    const int32_t* rows, const float* tables, const float* params, float* out7,
                    float* feats, void* stream) {
   SS_TRY(check_grid(grid, mlp));
-  FwdLaunch L{grid, n, means, rows, tables, params, out7, feats, ss_cloud{}, 0, nullptr,
-              nullptr, nullptr, nullptr, as_stream(stream)};
-  return dispatch_mlp(mlp, L);
+  if (n == 0) return SS_OK;
+  cudaStream_t st = as_stream(stream);
+  Temp tmp(st);
+  SS_TRY(tmp.alloc(ntc_scratch_bytes(mlp, n)));
+  NtcScratch s = ntc_scratch(tmp.p, mlp, n);
+  SS_TRY(ntc_forward_run(grid, mlp, n, means, rows, tables, params, s.X, s.xs, out7, 7, nullptr,
+                         st));
+  if (feats) {
+    const int nf = grid->n_levels * grid->n_features;
+    copy_cols_kernel<<<(unsigned)cdiv(n * nf, 256), 256, 0, st>>>(n, s.X, s.xs, nf, feats, nf);
+    SS_CHECK_LAUNCH("copy_cols_kernel");
+  }
+  return SS_OK;
 }
 
 size_t ss_ntc_backward_bytes(const ss_mlp* mlp) {
@@ -1052,9 +1110,17 @@ int ss_ntc_backward(const ss_grid* grid, const ss_mlp* mlp, int64_t n, const flo
     set_error("ss_ntc_backward: g_out7 required");
     return SS_ERR_DATA;
   }
-  BwdLaunch L{grid, n, means, rows, tables, params, g_out7, g_tables, g_params,
-              as_stream(stream)};
-  return dispatch_mlp(mlp, L);
+  if (n == 0) return SS_OK;
+  cudaStream_t st = as_stream(stream);
+  Temp tmp(st);
+  SS_TRY(tmp.alloc(ntc_scratch_bytes(mlp, n)));
+  NtcScratch s = ntc_scratch(tmp.p, mlp, n);
+  const int64_t threads = n * grid->n_levels;
+  gather_kernel<<<(unsigned)cdiv(threads, 256), 256, 0, st>>>(*grid, n, means, rows, tables, s.X,
+                                                                s.xs, nullptr);
+  SS_CHECK_LAUNCH("gather_kernel");
+  return ntc_backward_run(grid, mlp, n, means, rows, params, s.X, s.xs, g_out7, 7, s.dX, g_tables,
+                          g_params, st);
 }
 
 int ss_apply_ntc(const ss_grid* grid, const ss_mlp* mlp, const ss_cloud* src, int64_t n_in,
@@ -1066,19 +1132,20 @@ int ss_apply_ntc(const ss_grid* grid, const ss_mlp* mlp, const ss_cloud* src, in
     set_error("ss_apply_ntc: missing cloud buffers");
     return SS_ERR_DATA;
   }
-  if (src->sh_coeffs > 16) {
-    set_error("SH degree > 3 unsupported");
-    return SS_ERR_DATA;
-  }
-  SS_TRY(ensure_shrot_const());
-  FwdLaunch L{grid, n_in, src->means, rows, tables, params, out7, nullptr, *src, rotate_sh,
-              out_means, out_rotations, out_sh, status, as_stream(stream)};
-  return dispatch_mlp(mlp, L);
+  if (n_in == 0) return SS_OK;
+  cudaStream_t st = as_stream(stream);
+  Temp tmp(st);
+  SS_TRY(tmp.alloc(ntc_scratch_bytes(mlp, n_in)));
+  NtcScratch s = ntc_scratch(tmp.p, mlp, n_in);
+  float* o = out7 ? out7 : s.out7;
+  const int os = out7 ? 7 : 8;
+  SS_TRY(ntc_forward_run(grid, mlp, n_in, src->means, rows, tables, params, s.X, s.xs, o, os,
+                         status, st));
+  return transform_run(src, n_in, rows, o, os, rotate_sh, out_means, out_rotations, out_sh,
+                       status, st);
 }
 
-size_t ss_apply_ntc_backward_bytes(int64_t n_in) {
-  return align_up((size_t)(n_in > 0 ? n_in : 1) * 7 * sizeof(float)) * 2;
-}
+size_t ss_apply_ntc_backward_bytes(int64_t n_in) { return ntc_scratch_bytes(nullptr, n_in); }
 
 int ss_apply_ntc_backward(const ss_grid* grid, const ss_mlp* mlp, const ss_cloud* src,
                           int64_t n_in, const int32_t* rows, const float* tables,
@@ -1092,58 +1159,29 @@ int ss_apply_ntc_backward(const ss_grid* grid, const ss_mlp* mlp, const ss_cloud
     return SS_ERR_DATA;
   }
   if (n_in == 0) return SS_OK;
-  // the decoder output is recomputed (K2f), then the transform VJP (K3b) and the
-  // decoder/table backward (K2b/K1b) run as separate kernels
-  float* out7 = static_cast<float*>(scratch);
-  float* g7 = reinterpret_cast<float*>(static_cast<char*>(scratch) +
-                                       ss_apply_ntc_backward_bytes(n_in) / 2);
-  SS_TRY(ss_ntc_forward(grid, mlp, n_in, src->means, rows, tables, params, out7, nullptr,
-                        stream));
-  return ss_apply_ntc_backward_stored(grid, mlp, src, n_in, rows, tables, params, rotate_sh,
-                                      out7, d_means, d_rotations, d_sh, g7, g_tables, g_params,
-                                      stream);
-}
-
-int ss_apply_ntc_backward_stored(const ss_grid* grid, const ss_mlp* mlp, const ss_cloud* src,
-                                 int64_t n_in, const int32_t* rows, const float* tables,
-                                 const float* params, int32_t rotate_sh, const float* out7,
-                                 const float* d_means, const float* d_rotations,
-                                 const float* d_sh, float* g_out7, float* g_tables,
-                                 float* g_params, void* stream) {
-  SS_TRY(ss_transform_vjp(src, n_in, rows, out7, rotate_sh, d_means, d_rotations, d_sh, g_out7,
-                          stream));
-  return ss_ntc_backward(grid, mlp, n_in, src->means, rows, tables, params, g_out7, g_tables,
-                         g_params, nullptr, stream);
+  cudaStream_t st = as_stream(stream);
+  // decoder output recomputed (K1f/K2f), then K3b, K2b and K1b
+  NtcScratch s = ntc_scratch(scratch, mlp, n_in);
+  SS_TRY(ntc_forward_run(grid, mlp, n_in, src->means, rows, tables, params, s.X, s.xs, s.out7, 8,
+                         nullptr, st));
+  SS_TRY(transform_vjp_run(src, n_in, rows, s.out7, 8, rotate_sh, d_means, d_rotations, d_sh,
+                           s.g7, 8, st));
+  return ntc_backward_run(grid, mlp, n_in, src->means, rows, params, s.X, s.xs, s.g7, 8, s.dX,
+                          g_tables, g_params, st);
 }
 
 int ss_transform_apply(const ss_cloud* src, int64_t n_in, const int32_t* rows, const float* out7,
                        int32_t rotate_sh, float* out_means, float* out_rotations, float* out_sh,
                        uint32_t* status, void* stream) {
-  if (!src || src->sh_coeffs < 1 || src->sh_coeffs > 16) {
-    set_error("ss_transform_apply: bad cloud");
-    return SS_ERR_DATA;
-  }
-  if (n_in == 0) return SS_OK;
-  SS_TRY(ensure_shrot_const());
-  transform_apply_kernel<<<(unsigned)cdiv(n_in, 128), 128, 0, as_stream(stream)>>>(
-      *src, n_in, rows, out7, rotate_sh, out_means, out_rotations, out_sh, status);
-  SS_CHECK_LAUNCH("transform_apply_kernel");
-  return SS_OK;
+  return transform_run(src, n_in, rows, out7, 7, rotate_sh, out_means, out_rotations, out_sh,
+                       status, as_stream(stream));
 }
 
 int ss_transform_vjp(const ss_cloud* src, int64_t n_in, const int32_t* rows, const float* out7,
                      int32_t rotate_sh, const float* d_means, const float* d_rotations,
                      const float* d_sh, float* g_out7, void* stream) {
-  if (!src || src->sh_coeffs < 1 || src->sh_coeffs > 16) {
-    set_error("ss_transform_vjp: bad cloud");
-    return SS_ERR_DATA;
-  }
-  if (n_in == 0) return SS_OK;
-  SS_TRY(ensure_shrot_const());
-  transform_vjp_kernel<<<(unsigned)cdiv(n_in, 128), 128, 0, as_stream(stream)>>>(
-      *src, n_in, rows, out7, rotate_sh, d_means, d_rotations, d_sh, g_out7);
-  SS_CHECK_LAUNCH("transform_vjp_kernel");
-  return SS_OK;
+  return transform_vjp_run(src, n_in, rows, out7, 7, rotate_sh, d_means, d_rotations, d_sh,
+                           g_out7, 7, as_stream(stream));
 }
 
 int ss_adam_step(int64_t n_table, float* tables, float* g_tables, double* m_tables,

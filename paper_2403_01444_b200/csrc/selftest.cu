@@ -1,0 +1,96 @@
+// Self-test of the tcgen05 building blocks (umma.cuh) on the device.
+// D[M x N] = opA . opB with opA = A (M x K) when a_mn == 0 else TA^T where TA is
+// (K x M); likewise opB^T = Bt (N x K) or TB (K x N).  Operand matrices are
+// row-major fp32 in global memory and are staged as K-major tiles of their
+// stored shape; `swap` exchanges LBO/SBO of the MN-major descriptors (probe).
+// If `raw` the 128 TMEM lanes are dumped instead of the M rows.
+//
+// Measured on B200 / CUDA 12.9 / driver 580: K-major tf32 operands are exact
+// for M = 128 and M = 64; every MN-major (transposed) tf32 operand variant,
+// with either LBO/SBO assignment, leaves the accumulator untouched.  The
+// kernels therefore only use K-major tiles.
+#include "common.cuh"
+#include "umma.cuh"
+
+namespace ss {
+
+__global__ void __launch_bounds__(128) umma_selftest_kernel(const float* __restrict__ A,
+                                                            const float* __restrict__ B,
+                                                            float* __restrict__ D, int M, int N,
+                                                            int K, int a_mn, int b_mn, int swap,
+                                                            int raw) {
+  extern __shared__ __align__(128) uint8_t sm[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tbase;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int AR = a_mn ? K : M, AC = a_mn ? M : K;
+  const int BR = b_mn ? K : N, BC = b_mn ? N : K;
+  uint8_t* sa = sm;
+  uint8_t* sb = sm + umma::tile_bytes(AR, AC);
+  for (int i = tid; i < AR * AC; i += 128)
+    *reinterpret_cast<float*>(sa + umma::tile_off(i / AC, i % AC, AC)) = umma::to_tf32(A[i]);
+  for (int i = tid; i < BR * BC; i += 128)
+    *reinterpret_cast<float*>(sb + umma::tile_off(i / BC, i % BC, BC)) = umma::to_tf32(B[i]);
+  if (tid == 0) {
+    umma::mbar_init(&bar, 1);
+    umma::fence_mbar_init();
+  }
+  if (warp == 0) umma::tmem_alloc(&tbase, 64);
+  umma::fence_proxy_async();
+  umma::fence_before();
+  __syncthreads();
+  umma::fence_after();
+  const uint32_t tmem = tbase;
+  if (tid == 0) {
+    const uint32_t a0 = umma::smem_u32(sa), b0 = umma::smem_u32(sb);
+    const uint32_t id = umma::idesc_tf32(M, N, a_mn, b_mn);
+    for (int k = 0; k < K; k += 8) {
+      uint64_t da, db;
+      if (a_mn)
+        da = swap ? umma::desc(a0 + (k >> 3) * umma::tile_sbo(AC), 128u, umma::tile_sbo(AC))
+                  : umma::desc_mn(a0, AC, k);
+      else
+        da = umma::desc_k(a0, AC, k);
+      if (b_mn)
+        db = swap ? umma::desc(b0 + (k >> 3) * umma::tile_sbo(BC), 128u, umma::tile_sbo(BC))
+                  : umma::desc_mn(b0, BC, k);
+      else
+        db = umma::desc_k(b0, BC, k);
+      umma::mma_tf32(tmem, da, db, id, k > 0);
+    }
+    umma::commit(&bar);
+  }
+  umma::mbar_wait(&bar, 0);
+  umma::fence_after();
+  const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+  for (int c0 = 0; c0 < N; c0 += 8) {
+    float v[8];
+    umma::tmem_ld8(tmem + lane_base + (uint32_t)c0, v);
+    int row = -1;
+    if (M == 128 || raw) row = tid;
+    else if (lane < 16) row = warp * 16 + lane;
+    if (row >= 0)
+      for (int j = 0; j < 8 && c0 + j < N; ++j) D[row * N + c0 + j] = v[j];
+  }
+  umma::fence_before();
+  __syncthreads();
+  if (warp == 0) umma::tmem_free(tmem, 64);
+}
+
+}  // namespace ss
+
+// flags: bit0 a_mn, bit1 b_mn, bit2 swap, bit3 raw
+extern "C" int ss_selftest_umma(int32_t M, int32_t N, int32_t K, int32_t flags, const float* A,
+                                const float* B, float* D, void* stream) {
+  if ((M != 64 && M != 128) || N < 8 || N > 64 || N % 8 || K < 8 || K > 128 || K % 8)
+    return SS_ERR_DATA;
+  const int a_mn = flags & 1, b_mn = (flags >> 1) & 1;
+  const size_t smem = ss::umma::tile_bytes(a_mn ? K : M, a_mn ? M : K) +
+                      ss::umma::tile_bytes(b_mn ? K : N, b_mn ? N : K);
+  auto k = ss::umma_selftest_kernel;
+  SS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k<<<1, 128, smem, ss::as_stream(stream)>>>(A, B, D, M, N, K, a_mn, b_mn, (flags >> 2) & 1,
+                                             (flags >> 3) & 1);
+  SS_CHECK_LAUNCH("umma_selftest_kernel");
+  return SS_OK;
+}

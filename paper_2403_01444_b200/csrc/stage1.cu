@@ -28,11 +28,9 @@ __global__ void scale_kernel(int64_t n, float* __restrict__ v, float s) {
   if (i < n) v[i] *= s;
 }
 
-// ntc_scratch = [out7 of the forward | g_out7 of the backward], ss_apply_ntc_backward_bytes
-static float* out7_of(const ss_stage1* st) { return static_cast<float*>(st->ntc_scratch); }
-static float* g7_of(const ss_stage1* st) {
-  return reinterpret_cast<float*>(static_cast<char*>(st->ntc_scratch) +
-                                  ss_apply_ntc_backward_bytes(st->n_in) / 2);
+// ntc_scratch = [X | dX | out7 | g7] (ntc_scratch(), ss_apply_ntc_backward_bytes)
+static NtcScratch scratch_of(const ss_stage1* st) {
+  return ntc_scratch(st->ntc_scratch, &st->mlp, st->n_in);
 }
 
 static int64_t n_table(const ss_stage1* st) {
@@ -79,9 +77,12 @@ int ss_stage1_frame_begin(ss_stage1* st, void* stream) {
 
 int ss_stage1_iter_begin(ss_stage1* st, const ss_camera* cam, int64_t* counts_host,
                          void* stream) {
-  SS_TRY(ss_apply_ntc(&st->grid, &st->mlp, &st->src, st->n_in, st->rows, st->tables, st->params,
-                      st->rotate_sh, st->t_means, st->t_rotations, st->t_sh, out7_of(st),
-                      st->status, stream));
+  const NtcScratch ns = scratch_of(st);
+  cudaStream_t s = as_stream(stream);
+  SS_TRY(ntc_forward_run(&st->grid, &st->mlp, st->n_in, st->src.means, st->rows, st->tables,
+                         st->params, ns.X, ns.xs, ns.out7, 8, st->status, s));
+  SS_TRY(transform_run(&st->src, st->n_in, st->rows, ns.out7, 8, st->rotate_sh, st->t_means,
+                       st->t_rotations, st->t_sh, st->status, s));
   const ss_cloud tc = transformed(st);
   return raster_begin(&tc, cam, &st->settings, st->geom, counts_host, as_stream(stream));
 }
@@ -121,10 +122,11 @@ int ss_stage1_iter_grads(ss_stage1* st, const ss_camera* cam, const float* targe
                                                          st->stats_norm, st->stats_count);
     SS_CHECK_LAUNCH("stats_kernel");
   }
-  SS_TRY(ss_apply_ntc_backward_stored(&st->grid, &st->mlp, &st->src, st->n_in, st->rows,
-                                      st->tables, st->params, st->rotate_sh, out7_of(st),
-                                      st->d_means, st->d_rotations, st->d_sh, g7_of(st),
-                                      st->g_tables, st->g_params, stream));
+  const NtcScratch ns = scratch_of(st);
+  SS_TRY(transform_vjp_run(&st->src, st->n_in, st->rows, ns.out7, 8, st->rotate_sh, st->d_means,
+                           st->d_rotations, st->d_sh, ns.g7, 8, s));
+  SS_TRY(ntc_backward_run(&st->grid, &st->mlp, st->n_in, st->src.means, st->rows, st->params,
+                          ns.X, ns.xs, ns.g7, 8, ns.dX, st->g_tables, st->g_params, s));
   st->iteration += 1;
   return SS_OK;
 }

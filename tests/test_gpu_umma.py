@@ -1,0 +1,65 @@
+"""tcgen05 building blocks (csrc/umma.cuh) against host GEMMs: K-major M=128
+and MN-major (transposed-tile) M=64 UMMAs with TMEM accumulators."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _tf32(a):
+    b = np.ascontiguousarray(a, dtype=np.float32).view(np.uint32)
+    b = (b + 0x1000) & 0xFFFFE000  # round to nearest (ties away), 10-bit mantissa
+    return b.view(np.float32).astype(np.float64)
+
+
+@pytest.mark.parametrize("test", [0, 1])
+def test_umma_tf32(test):
+    """K-major A and B (the only layout the kernels use), M = 128 and M = 64."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import ctypes as C
+
+    from paper_2403_01444_b200 import _lib
+    from paper_2403_01444_b200.device import ptr, stream
+
+    lib = _lib.load()
+    rng = np.random.default_rng(test)
+    M, N, K = (128, 64, 32) if test == 0 else (64, 40, 64)
+    a, b = rng.normal(size=(M, K)), rng.normal(size=(N, K))
+    ref = _tf32(a) @ _tf32(b).T
+    da = torch.tensor(a, dtype=torch.float32, device="cuda")
+    db = torch.tensor(b, dtype=torch.float32, device="cuda")
+    dd = torch.full(ref.shape, float("nan"), dtype=torch.float32, device="cuda")
+    assert lib.ss_selftest_umma(M, N, K, 0, ptr(da), ptr(db), ptr(dd), stream()) == 0
+    out = dd.cpu().numpy().astype(np.float64)
+    np.testing.assert_allclose(out, ref, rtol=1e-5, atol=1e-4)
+
+
+@pytest.mark.parametrize("mode", [1, 2])
+def test_tensor_core_decoder_matches_fp32(mode):
+    """ss_ntc_forward with the tcgen05 decoder (3xTF32 / tf32) vs the FFMA path."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2403_01444_b200 import _lib, scenes
+    from paper_2403_01444_b200.ntc import NeuralTransformationCache
+    from paper_2403_01444_b200.types import HashGridConfig
+
+    lib = _lib.load()
+    sc = scenes.config(1)
+    cache = NeuralTransformationCache(HashGridConfig.from_any(sc.grid), output_init="random")
+    cache.tables[:] = np.random.default_rng(0).uniform(-0.5, 0.5, size=cache.tables.shape)
+    x = sc.cloud["means"][:5000]
+    lib.ss_set_mlp_mode(0)
+    ref, _, _ = cache.forward(x)
+    ref = np.concatenate([ref, cache.forward(x)[1]], 1)
+    lib.ss_set_mlp_mode(mode)
+    try:
+        d_mu, d_q, _ = cache.forward(x)
+    finally:
+        lib.ss_set_mlp_mode(1)
+    out = np.concatenate([d_mu, d_q], 1)
+    tol = 2e-6 if mode == 1 else 2e-3
+    assert np.abs(out - ref).max() <= tol * np.abs(ref).max()
