@@ -229,17 +229,18 @@ void prof_end(int phase, cudaStream_t s);
 // are (n, 8) (or stride 7 on the reference-shaped API).
 struct NtcScratch {
   float *X, *dX, *out7, *g7;
+  uint64_t* relu;  // (n, 2) ReLU masks of the decoder forward, reused by its backward
   int xs;
 };
 size_t ntc_scratch_bytes(const ss_mlp* mlp, int64_t n);
 NtcScratch ntc_scratch(void* base, const ss_mlp* mlp, int64_t n);
 int ntc_forward_run(const ss_grid* g, const ss_mlp* mlp, int64_t n, const float* means,
                     const int32_t* rows, const float* tables, const float* params, float* X, int xs,
-                    float* out, int os, uint32_t* status, cudaStream_t st);
+                    float* out, int os, uint64_t* relu, uint32_t* status, cudaStream_t st);
 int ntc_backward_run(const ss_grid* g, const ss_mlp* mlp, int64_t n, const float* means,
                      const int32_t* rows, const float* params, const float* X, int xs,
-                     const float* g_out, int gs, float* dX, float* g_tables, float* g_params,
-                     cudaStream_t st);
+                     const float* g_out, int gs, const uint64_t* relu, float* dX,
+                     float* g_tables, float* g_params, cudaStream_t st);
 int transform_run(const ss_cloud* src, int64_t n, const int32_t* rows, const float* out7, int os,
                   int rotate_sh, float* tm, float* tr, float* ts, uint32_t* status,
                   cudaStream_t st);
@@ -252,5 +253,8 @@ int transform_vjp_run(const ss_cloud* src, int64_t n, const int32_t* rows, const
 namespace ss {
 int mlp_mode();
 int mlp_fwd_tc(int in_pad, int n_hidden, int64_t n, const float* X, int xs, const float* params,
-               float* out, int os, cudaStream_t st);
+               float* out, int os, uint64_t* relu_masks, cudaStream_t st);
+int mlp_bwd_tc(int in_pad, int n_hidden, int64_t n, const float* X, int xs, const float* g,
+               int gs, const uint64_t* relu_masks, const float* params, float* dX,
+               float* g_params, cudaStream_t st);
 }  // namespace ss

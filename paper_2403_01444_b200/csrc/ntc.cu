@@ -933,7 +933,8 @@ struct MlpBwd {
 size_t ntc_scratch_bytes(const ss_mlp* mlp, int64_t n) {
   const int xs = mlp ? in_pad_of(mlp) : 64;
   const size_t nn = (size_t)(n > 0 ? n : 1);
-  return 2 * align_up(nn * xs * sizeof(float)) + 2 * align_up(nn * 8 * sizeof(float));
+  return 2 * align_up(nn * xs * sizeof(float)) + 2 * align_up(nn * 8 * sizeof(float)) +
+         align_up(nn * 2 * sizeof(uint64_t));
 }
 
 NtcScratch ntc_scratch(void* base, const ss_mlp* mlp, int64_t n) {
@@ -945,12 +946,13 @@ NtcScratch ntc_scratch(void* base, const ss_mlp* mlp, int64_t n) {
   s.dX = c.take<float>(nn * s.xs);
   s.out7 = c.take<float>(nn * 8);
   s.g7 = c.take<float>(nn * 8);
+  s.relu = c.take<uint64_t>(nn * 2);
   return s;
 }
 
 int ntc_forward_run(const ss_grid* g, const ss_mlp* mlp, int64_t n, const float* means,
                     const int32_t* rows, const float* tables, const float* params, float* X, int xs,
-                    float* out, int os, uint32_t* status, cudaStream_t st) {
+                    float* out, int os, uint64_t* relu, uint32_t* status, cudaStream_t st) {
   SS_TRY(check_grid(g, mlp));
   if (n == 0) return SS_OK;
   prof_begin(PH_NTC_FWD, st);
@@ -959,7 +961,7 @@ int ntc_forward_run(const ss_grid* g, const ss_mlp* mlp, int64_t n, const float*
                                                                 status);
   SS_CHECK_LAUNCH("gather_kernel");
   if (mlp_mode() != 0)
-    SS_TRY(mlp_fwd_tc(xs, mlp->n_hidden, n, X, xs, params, out, os, st));  // tcgen05
+    SS_TRY(mlp_fwd_tc(xs, mlp->n_hidden, n, X, xs, params, out, os, relu, st));  // tcgen05
   else
     SS_TRY(dispatch_mlp(mlp, MlpFwd{n, X, xs, params, out, os, st}));
   prof_end(PH_NTC_FWD, st);
@@ -968,12 +970,15 @@ int ntc_forward_run(const ss_grid* g, const ss_mlp* mlp, int64_t n, const float*
 
 int ntc_backward_run(const ss_grid* g, const ss_mlp* mlp, int64_t n, const float* means,
                      const int32_t* rows, const float* params, const float* X, int xs,
-                     const float* g_out, int gs, float* dX, float* g_tables, float* g_params,
-                     cudaStream_t st) {
+                     const float* g_out, int gs, const uint64_t* relu, float* dX,
+                     float* g_tables, float* g_params, cudaStream_t st) {
   SS_TRY(check_grid(g, mlp));
   if (n == 0) return SS_OK;
   prof_begin(PH_NTC_BWD, st);
-  SS_TRY(dispatch_mlp(mlp, MlpBwd{n, X, xs, g_out, gs, params, dX, g_params, st}));
+  if (mlp_mode() != 0)
+    SS_TRY(mlp_bwd_tc(xs, mlp->n_hidden, n, X, xs, g_out, gs, relu, params, dX, g_params, st));
+  else
+    SS_TRY(dispatch_mlp(mlp, MlpBwd{n, X, xs, g_out, gs, params, dX, g_params, st}));
   const int64_t threads = n * g->n_levels;
   scatter_kernel<<<(unsigned)cdiv(threads, 256), 256, 0, st>>>(*g, n, means, rows, dX, xs,
                                                                  g_tables);
@@ -1085,8 +1090,8 @@ int ss_ntc_forward(const ss_grid* grid, const ss_mlp* mlp, int64_t n, const floa
   Temp tmp(st);
   SS_TRY(tmp.alloc(ntc_scratch_bytes(mlp, n)));
   NtcScratch s = ntc_scratch(tmp.p, mlp, n);
-  SS_TRY(ntc_forward_run(grid, mlp, n, means, rows, tables, params, s.X, s.xs, out7, 7, nullptr,
-                         st));
+  SS_TRY(ntc_forward_run(grid, mlp, n, means, rows, tables, params, s.X, s.xs, out7, 7, s.relu,
+                         nullptr, st));
   if (feats) {
     const int nf = grid->n_levels * grid->n_features;
     copy_cols_kernel<<<(unsigned)cdiv(n * nf, 256), 256, 0, st>>>(n, s.X, s.xs, nf, feats, nf);
@@ -1115,12 +1120,11 @@ int ss_ntc_backward(const ss_grid* grid, const ss_mlp* mlp, int64_t n, const flo
   Temp tmp(st);
   SS_TRY(tmp.alloc(ntc_scratch_bytes(mlp, n)));
   NtcScratch s = ntc_scratch(tmp.p, mlp, n);
-  const int64_t threads = n * grid->n_levels;
-  gather_kernel<<<(unsigned)cdiv(threads, 256), 256, 0, st>>>(*grid, n, means, rows, tables, s.X,
-                                                                s.xs, nullptr);
-  SS_CHECK_LAUNCH("gather_kernel");
-  return ntc_backward_run(grid, mlp, n, means, rows, params, s.X, s.xs, g_out7, 7, s.dX, g_tables,
-                          g_params, st);
+  // decoder forward recomputed: features and the ReLU masks the backward reuses
+  SS_TRY(ntc_forward_run(grid, mlp, n, means, rows, tables, params, s.X, s.xs, s.out7, 8, s.relu,
+                         nullptr, st));
+  return ntc_backward_run(grid, mlp, n, means, rows, params, s.X, s.xs, g_out7, 7, s.relu, s.dX,
+                          g_tables, g_params, st);
 }
 
 int ss_apply_ntc(const ss_grid* grid, const ss_mlp* mlp, const ss_cloud* src, int64_t n_in,
@@ -1140,7 +1144,7 @@ int ss_apply_ntc(const ss_grid* grid, const ss_mlp* mlp, const ss_cloud* src, in
   float* o = out7 ? out7 : s.out7;
   const int os = out7 ? 7 : 8;
   SS_TRY(ntc_forward_run(grid, mlp, n_in, src->means, rows, tables, params, s.X, s.xs, o, os,
-                         status, st));
+                         s.relu, status, st));
   return transform_run(src, n_in, rows, o, os, rotate_sh, out_means, out_rotations, out_sh,
                        status, st);
 }
@@ -1163,10 +1167,11 @@ int ss_apply_ntc_backward(const ss_grid* grid, const ss_mlp* mlp, const ss_cloud
   // decoder output recomputed (K1f/K2f), then K3b, K2b and K1b
   NtcScratch s = ntc_scratch(scratch, mlp, n_in);
   SS_TRY(ntc_forward_run(grid, mlp, n_in, src->means, rows, tables, params, s.X, s.xs, s.out7, 8,
-                         nullptr, st));
+                         s.relu, nullptr, st));
   SS_TRY(transform_vjp_run(src, n_in, rows, s.out7, 8, rotate_sh, d_means, d_rotations, d_sh,
                            s.g7, 8, st));
-  return ntc_backward_run(grid, mlp, n_in, src->means, rows, params, s.X, s.xs, s.g7, 8, s.dX,
+  return ntc_backward_run(grid, mlp, n_in, src->means, rows, params, s.X, s.xs, s.g7, 8, s.relu,
+                          s.dX,
                           g_tables, g_params, st);
 }
 

@@ -77,14 +77,84 @@ __global__ void __launch_bounds__(128) umma_selftest_kernel(const float* __restr
   if (warp == 0) umma::tmem_free(tmem, 64);
 }
 
+// kind::f16 (bf16) variant: operands rounded to bf16, K steps of 16,
+// MN-major operands read from the stored (K x MN) tile via desc16_mn.
+__global__ void __launch_bounds__(128) umma_selftest16_kernel(const float* __restrict__ A,
+                                                              const float* __restrict__ B,
+                                                              float* __restrict__ D, int M, int N,
+                                                              int K, int a_mn, int b_mn, int swap,
+                                                              int raw) {
+  extern __shared__ __align__(128) uint8_t sm[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tbase;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int AR = a_mn ? K : M, AC = a_mn ? M : K;
+  const int BR = b_mn ? K : N, BC = b_mn ? N : K;
+  uint8_t* sa = sm;
+  uint8_t* sb = sm + umma::tile16_bytes(AR, AC);
+  for (int i = tid; i < AR * AC; i += 128)
+    *reinterpret_cast<__nv_bfloat16*>(sa + umma::tile16_off(i / AC, i % AC, AC)) =
+        __float2bfloat16_rn(A[i]);
+  for (int i = tid; i < BR * BC; i += 128)
+    *reinterpret_cast<__nv_bfloat16*>(sb + umma::tile16_off(i / BC, i % BC, BC)) =
+        __float2bfloat16_rn(B[i]);
+  if (tid == 0) {
+    umma::mbar_init(&bar, 1);
+    umma::fence_mbar_init();
+  }
+  if (warp == 0) umma::tmem_alloc(&tbase, 128);
+  umma::fence_proxy_async();
+  umma::fence_before();
+  __syncthreads();
+  umma::fence_after();
+  const uint32_t tmem = tbase;
+  if (tid == 0) {
+    const uint32_t a0 = umma::smem_u32(sa), b0 = umma::smem_u32(sb);
+    const uint32_t id = umma::idesc_bf16(M, N, a_mn, b_mn);
+    for (int k = 0; k < K; k += 16) {
+      const uint64_t da = a_mn ? umma::desc16_mn(a0, AC, k, 0, swap) : umma::desc16_k(a0, AC, k);
+      const uint64_t db = b_mn ? umma::desc16_mn(b0, BC, k, 0, swap) : umma::desc16_k(b0, BC, k);
+      umma::mma_bf16(tmem, da, db, id, k > 0);
+    }
+    umma::commit(&bar);
+  }
+  umma::mbar_wait(&bar, 0);
+  umma::fence_after();
+  const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+  for (int c0 = 0; c0 < N; c0 += 8) {
+    float v[8];
+    umma::tmem_ld8(tmem + lane_base + (uint32_t)c0, v);
+    int row = -1;
+    if (M == 128 || raw) row = tid;
+    else if (lane < 16) row = warp * 16 + lane;
+    if (row >= 0)
+      for (int j = 0; j < 8 && c0 + j < N; ++j) D[row * N + c0 + j] = v[j];
+  }
+  umma::fence_before();
+  __syncthreads();
+  if (warp == 0) umma::tmem_free(tmem, 128);
+}
+
 }  // namespace ss
 
-// flags: bit0 a_mn, bit1 b_mn, bit2 swap, bit3 raw
+// flags: bit0 a_mn, bit1 b_mn, bit2 swap, bit3 raw, bit4 bf16 (kind::f16)
 extern "C" int ss_selftest_umma(int32_t M, int32_t N, int32_t K, int32_t flags, const float* A,
                                 const float* B, float* D, void* stream) {
-  if ((M != 64 && M != 128) || N < 8 || N > 64 || N % 8 || K < 8 || K > 128 || K % 8)
+  const int bf16 = (flags >> 4) & 1;
+  if ((M != 64 && M != 128) || N < 8 || N > 128 || N % 8 || K < 8 || K > 128 ||
+      K % (bf16 ? 16 : 8) || (!bf16 && N > 64))
     return SS_ERR_DATA;
   const int a_mn = flags & 1, b_mn = (flags >> 1) & 1;
+  if (bf16) {
+    const size_t smem = ss::umma::tile16_bytes(a_mn ? K : M, a_mn ? M : K) +
+                        ss::umma::tile16_bytes(b_mn ? K : N, b_mn ? N : K);
+    auto k = ss::umma_selftest16_kernel;
+    SS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k<<<1, 128, smem, ss::as_stream(stream)>>>(A, B, D, M, N, K, a_mn, b_mn, (flags >> 2) & 1,
+                                               (flags >> 3) & 1);
+    SS_CHECK_LAUNCH("umma_selftest16_kernel");
+    return SS_OK;
+  }
   const size_t smem = ss::umma::tile_bytes(a_mn ? K : M, a_mn ? M : K) +
                       ss::umma::tile_bytes(b_mn ? K : N, b_mn ? N : K);
   auto k = ss::umma_selftest_kernel;

@@ -28,7 +28,7 @@ __global__ void scale_kernel(int64_t n, float* __restrict__ v, float s) {
   if (i < n) v[i] *= s;
 }
 
-// ntc_scratch = [X | dX | out7 | g7] (ntc_scratch(), ss_apply_ntc_backward_bytes)
+// ntc_scratch = [X | dX | out7 | g7 | relu] (ntc_scratch(), ss_apply_ntc_backward_bytes)
 static NtcScratch scratch_of(const ss_stage1* st) {
   return ntc_scratch(st->ntc_scratch, &st->mlp, st->n_in);
 }
@@ -80,7 +80,7 @@ int ss_stage1_iter_begin(ss_stage1* st, const ss_camera* cam, int64_t* counts_ho
   const NtcScratch ns = scratch_of(st);
   cudaStream_t s = as_stream(stream);
   SS_TRY(ntc_forward_run(&st->grid, &st->mlp, st->n_in, st->src.means, st->rows, st->tables,
-                         st->params, ns.X, ns.xs, ns.out7, 8, st->status, s));
+                         st->params, ns.X, ns.xs, ns.out7, 8, ns.relu, st->status, s));
   SS_TRY(transform_run(&st->src, st->n_in, st->rows, ns.out7, 8, st->rotate_sh, st->t_means,
                        st->t_rotations, st->t_sh, st->status, s));
   const ss_cloud tc = transformed(st);
@@ -126,7 +126,7 @@ int ss_stage1_iter_grads(ss_stage1* st, const ss_camera* cam, const float* targe
   SS_TRY(transform_vjp_run(&st->src, st->n_in, st->rows, ns.out7, 8, st->rotate_sh, st->d_means,
                            st->d_rotations, st->d_sh, ns.g7, 8, s));
   SS_TRY(ntc_backward_run(&st->grid, &st->mlp, st->n_in, st->src.means, st->rows, st->params,
-                          ns.X, ns.xs, ns.g7, 8, ns.dX, st->g_tables, st->g_params, s));
+                          ns.X, ns.xs, ns.g7, 8, ns.relu, ns.dX, st->g_tables, st->g_params, s));
   st->iteration += 1;
   return SS_OK;
 }

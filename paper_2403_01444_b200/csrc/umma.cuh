@@ -12,6 +12,7 @@
 //   in lanes 32w..32w+15 (w = 0..3), column n at base column + n.
 #pragma once
 
+#include <cuda_bf16.h>
 #include <stdint.h>
 
 namespace ss {
@@ -141,6 +142,58 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
   for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// ---- 16-bit operands (kind::f16 with bf16 inputs, fp32 accumulate)
+//
+// A 16-bit tile is stored with 8x8-element core matrices (8 rows x 16 bytes,
+// 128 contiguous bytes): element (r, c) at
+//   (r / 8) * SBO16 + (c / 8) * 128 + (r % 8) * 16 + (c % 8) * 2,  SBO16 = 16 * cols.
+// K-major read (K along the columns): LBO = 128 (next core along K), SBO = SBO16.
+// MN-major read of the same bytes (the transposed matrix, MN along the
+// columns, K along the rows): SBO = 128 (next core along MN), LBO = SBO16
+// (next 8 K-rows), cute/atom/mma_traits_sm100.hpp canonical INTERLEAVE forms.
+__host__ __device__ constexpr uint32_t sbo16(int cols) { return 16u * (uint32_t)cols; }
+__host__ __device__ constexpr uint32_t tile16_bytes(int rows, int cols) {
+  return (uint32_t)(rows / 8) * sbo16(cols);
+}
+__device__ __forceinline__ uint32_t tile16_off(int r, int c, int cols) {
+  return (uint32_t)(r >> 3) * sbo16(cols) + (uint32_t)(c >> 3) * 128u + (uint32_t)(r & 7) * 16u +
+         (uint32_t)(c & 7) * 2u;
+}
+// K-major operand from column k0 (multiple of 16), rows from row0 (multiple of 8)
+__device__ __forceinline__ uint64_t desc16_k(uint32_t tile, int cols, int k0, int row0 = 0) {
+  return desc(tile + (uint32_t)(k0 >> 3) * 128u + (uint32_t)(row0 >> 3) * sbo16(cols), 128u,
+              sbo16(cols));
+}
+// MN-major operand (transpose of the stored tile): K from row k0 (multiple of
+// 16), MN from column mn0 (multiple of 8).  `swap` exchanges LBO/SBO (probe).
+__device__ __forceinline__ uint64_t desc16_mn(uint32_t tile, int cols, int k0, int mn0 = 0,
+                                              int swap = 0) {
+  const uint32_t a = tile + (uint32_t)(k0 >> 3) * sbo16(cols) + (uint32_t)(mn0 >> 3) * 128u;
+  return swap ? desc(a, 128u, sbo16(cols)) : desc(a, sbo16(cols), 128u);
+}
+// instruction descriptor: kind::f16 with bf16 A/B, fp32 accumulate
+__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, int a_mn_major, int b_mn_major) {
+  return (1u << 4)                          // D format f32
+         | (1u << 7) | (1u << 10)           // A, B format bf16
+         | ((uint32_t)a_mn_major << 15) | ((uint32_t)b_mn_major << 16)
+         | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+// x = hi + lo with hi = bf16(x) (round to nearest even), lo = bf16(x - hi):
+// the 3-product split A_hi.B_hi + A_hi.B_lo + A_lo.B_hi keeps ~16 mantissa bits.
+__device__ __forceinline__ void split_bf16(float x, uint16_t& hi, uint16_t& lo) {
+  const __nv_bfloat16 h = __float2bfloat16_rn(x);
+  const __nv_bfloat16 l = __float2bfloat16_rn(x - __bfloat162float(h));
+  hi = __bfloat16_as_ushort(h);
+  lo = __bfloat16_as_ushort(l);
 }
 
 // fp32 -> tf32 with round-to-nearest (kept in a 32-bit container)
