@@ -290,10 +290,13 @@ typedef struct ss_stage1 {
   int32_t* stats_count;   /* ViewspaceStats.view_count, (n,) */
   double* loss_dev;       /* last loss */
   double* loss_history;   /* optional (nullable): loss of iteration i at [i] */
+  int64_t* pair_history;  /* optional (nullable): tile pairs of iteration i at [i] */
+  int64_t history_len;    /* entries of the histories (iteration i -> [i % history_len]) */
   int32_t iteration;
   uint32_t* status;
   void *geom, *bins, *loss_scratch, *ntc_scratch;
-  int64_t bin_capacity; /* n_pairs the `bins` workspace holds */
+  int64_t bin_capacity; /* n_pairs the `bins` workspace holds; more raises
+                           SS_FLAG_OVERFLOW in *status (the pairs beyond are dropped) */
 } ss_stage1;
 
 /* Start of a frame: touched-row mask, transformed <- source copy, zero Adam
@@ -303,7 +306,8 @@ int ss_stage1_frame_begin(ss_stage1* st, void* stream);
  * counts_host (pinned int64[2]) receives [n_survivors, n_pairs]. */
 int ss_stage1_iter_begin(ss_stage1* st, const ss_camera* cam, int64_t* counts_host, void* stream);
 /* Iteration part B: binning, blend, loss, raster backward, transform+NTC
- * backward, lazy Adam, view-space stats.  Requires n_pairs <= bin_capacity. */
+ * backward, lazy Adam, view-space stats.  The binning reads the pair count
+ * from the device; n_pairs (>= 0) only asserts n_pairs <= bin_capacity. */
 int ss_stage1_iter_finish(ss_stage1* st, const ss_camera* cam, const float* target,
                           int64_t n_pairs, void* stream);
 /* Part B up to (and including) the NTC gradients but without the Adam step
@@ -311,6 +315,15 @@ int ss_stage1_iter_finish(ss_stage1* st, const ss_camera* cam, const float* targ
 int ss_stage1_iter_grads(ss_stage1* st, const ss_camera* cam, const float* target,
                          int64_t n_pairs, float grad_scale, void* stream);
 int ss_stage1_apply_adam(ss_stage1* st, void* stream);
+/* One whole iteration (parts A and B, plus Adam when apply_adam != 0) with no
+ * host synchronisation: the pair count stays on the device and the binning
+ * is bounded by bin_capacity (overflow -> SS_FLAG_OVERFLOW).  Stream-ordered,
+ * so consecutive iterations queue back to back (and can be graph-captured). */
+int ss_stage1_iter(ss_stage1* st, const ss_camera* cam, const float* target, float grad_scale,
+                   int32_t apply_adam, void* stream);
+/* Forward only (render-only throughput, playback): apply_ntc + rasterize_forward
+ * into st->image / st->alpha_map, with no host synchronisation. */
+int ss_stage1_render(ss_stage1* st, const ss_camera* cam, void* stream);
 
 /* device self-test of the tcgen05 building blocks: D (M x N) = opA . opB over
  * K, flags bit0/bit1 = A/B given transposed (MN-major operand), row-major fp32
@@ -319,6 +332,10 @@ int ss_stage1_apply_adam(ss_stage1* st, void* stream);
  * 2 = tcgen05 tf32 */
 int ss_set_mlp_mode(int32_t mode);
 int32_t ss_get_mlp_mode(void);
+// Debug: clock64 stamps of CTA 0 / thread 0 at the decoder kernels' stage
+// boundaries (out: 2 x 64 uint64, forward then backward).
+int ss_debug_mlp_trace(uint64_t* out);
+
 int ss_selftest_umma(int32_t M, int32_t N, int32_t K, int32_t flags, const float* A,
                      const float* B, float* D, void* stream);
 

@@ -75,7 +75,8 @@ class Stage1(C.Structure):
                 ("image", P), ("alpha_map", P), ("d_image", P),
                 ("d_means", P), ("d_rotations", P), ("d_sh", P),
                 ("viewspace", P), ("contributed", P), ("stats_norm", P), ("stats_count", P),
-                ("loss_dev", P), ("loss_history", P), ("iteration", C.c_int32),
+                ("loss_dev", P), ("loss_history", P), ("pair_history", P),
+                ("history_len", C.c_int64), ("iteration", C.c_int32),
                 ("status", P), ("geom", P), ("bins", P), ("loss_scratch", P),
                 ("ntc_scratch", P), ("bin_capacity", C.c_int64)]
 
@@ -122,9 +123,12 @@ SIGNATURES = [
     ("ss_stage1_iter_finish", I32, [C.POINTER(Stage1), PCam, P, I64, P]),
     ("ss_stage1_iter_grads", I32, [C.POINTER(Stage1), PCam, P, I64, C.c_float, P]),
     ("ss_stage1_apply_adam", I32, [C.POINTER(Stage1), P]),
+    ("ss_stage1_iter", I32, [C.POINTER(Stage1), PCam, P, C.c_float, I32, P]),
+    ("ss_stage1_render", I32, [C.POINTER(Stage1), PCam, P]),
     ("ss_set_mlp_mode", I32, [I32]),
     ("ss_get_mlp_mode", I32, []),
     ("ss_selftest_umma", I32, [I32, I32, I32, I32, P, P, P, P]),
+    ("ss_debug_mlp_trace", I32, [P]),
 ]
 
 

@@ -1,0 +1,231 @@
+// K4d: stable LSD radix sort of (tile key, depth rank) pairs whose count lives
+// in device memory (rasterizer.py:155-175: per-tile member lists in depth
+// order).  Because the pair count never has to reach the host, a whole
+// Stage-1 iteration is stream-ordered without a synchronisation and can be
+// captured in a CUDA graph; buffers are sized by a capacity bound and an
+// overflow raises SS_FLAG_OVERFLOW on the device.
+//
+// Per 8-bit digit pass ("onesweep"): a CTA of 256 threads takes a logical
+// tile id from an atomic ticket (so every predecessor is already running),
+// ranks its 4096 keys stably with warp match + per-warp digit counters (warp
+// w owns items [512 w, 512 w + 512) of the tile, in index order), publishes
+// its per-digit counts and resolves its global offsets by decoupled look-back
+// over the predecessors, stages the tile in shared memory in sorted order and
+// writes it out in coalesced runs.  One histogram kernel serves all passes.
+// Input order is the rank order the duplicate kernel emits, so LSD stability
+// gives exactly the reference's (tile, rank) order.
+#include "common.cuh"
+
+namespace ss {
+
+namespace {
+constexpr int kBsThreads = 256;
+constexpr int kBsWarps = kBsThreads / 32;
+constexpr int kBsSteps = 16;  // items per lane
+constexpr int kBsTile = kBsThreads * kBsSteps;
+constexpr uint32_t kFlagAgg = 1u << 30, kFlagInc = 2u << 30, kCntMask = (1u << 30) - 1;
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+__device__ __forceinline__ uint32_t ld_volatile(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.volatile.global.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+}  // namespace
+
+BinSortWS binsort_plan(Carve& c, int64_t capacity) {
+  BinSortWS w{};
+  w.max_blocks = (capacity + kBsTile - 1) / kBsTile;
+  if (w.max_blocks < 1) w.max_blocks = 1;
+  w.hist = c.take<uint32_t>(2 * 256 + 64);  // [pass][digit], then tickets
+  w.status = c.take<uint32_t>((size_t)2 * w.max_blocks * 256);
+  return w;
+}
+
+size_t binsort_clear_bytes(const BinSortWS& w) {
+  return (2 * 256 + 64) * sizeof(uint32_t);
+}
+
+// one histogram kernel for both passes
+__global__ void __launch_bounds__(256) bs_hist_kernel(const uint32_t* __restrict__ keys,
+                                                      const int64_t* __restrict__ d_n,
+                                                      int64_t cap, int bits0, int bits1,
+                                                      uint32_t* __restrict__ hist) {
+  __shared__ uint32_t sh[2][256];
+  for (int i = threadIdx.x; i < 512; i += blockDim.x) (&sh[0][0])[i] = 0;
+  __syncthreads();
+  const int64_t n = min(*d_n, cap);
+  const uint32_t m0 = (1u << bits0) - 1, m1 = (1u << bits1) - 1;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t k = keys[i];
+    atomicAdd(&sh[0][k & m0], 1u);
+    if (bits1 > 0) atomicAdd(&sh[1][(k >> bits0) & m1], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 512; i += blockDim.x) {
+    const uint32_t v = (&sh[0][0])[i];
+    if (v) atomicAdd(hist + i, v);
+  }
+}
+
+// pass over digit bits [shift, shift + bits)
+__global__ void __launch_bounds__(kBsThreads) bs_pass_kernel(
+    const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin, uint32_t* __restrict__ kout,
+    uint32_t* __restrict__ vout, const int64_t* __restrict__ d_n, int64_t cap, int shift, int bits,
+    const uint32_t* __restrict__ hist, uint32_t* __restrict__ ticket, uint32_t* __restrict__ status) {
+  __shared__ uint32_t s_bid;
+  __shared__ uint32_t wh[kBsWarps][256];  // per-warp digit counts -> exclusive prefix over warps
+  __shared__ uint32_t s_gbase[256];       // global position of this tile's first item of digit d
+  __shared__ uint32_t s_lstart[256];      // tile-local start of digit d
+  __shared__ uint32_t s_scan[256];
+  __shared__ uint32_t s_keys[kBsTile], s_vals[kBsTile];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) s_bid = atomicAdd(ticket, 1u);
+  for (int i = tid; i < kBsWarps * 256; i += kBsThreads) (&wh[0][0])[i] = 0;
+  __syncthreads();
+  const int64_t n = min(*d_n, cap);
+  const uint32_t bid = s_bid;
+  const int64_t base = (int64_t)bid * kBsTile;
+  if (base >= n) return;  // block-uniform
+  const uint32_t dmask = (1u << bits) - 1;
+  // ---- load and rank (warp-contiguous segments, lane order within a step)
+  uint32_t k[kBsSteps], v[kBsSteps], rk[kBsSteps];
+  const int64_t wbase = base + warp * (kBsSteps * 32);
+#pragma unroll
+  for (int s = 0; s < kBsSteps; ++s) {
+    const int64_t i = wbase + s * 32 + lane;
+    const bool ok = i < n;
+    k[s] = ok ? kin[i] : 0u;
+    v[s] = ok ? vin[i] : 0u;
+    const uint32_t d = ok ? ((k[s] >> shift) & dmask) : 256u;  // 256 = past the end
+    const uint32_t peers = __match_any_sync(0xffffffffu, d);
+    const int leader = __ffs(peers) - 1;
+    uint32_t old = 0;
+    if (ok && lane == leader) {
+      old = wh[warp][d];
+      wh[warp][d] = old + __popc(peers);
+    }
+    old = __shfl_sync(0xffffffffu, old, leader);
+    rk[s] = old + __popc(peers & lanemask_lt());
+    __syncwarp();
+  }
+  __syncthreads();
+  // ---- per digit (thread = digit): counts -> exclusive prefix over warps
+  const int d = tid;
+  uint32_t cnt = 0;
+#pragma unroll
+  for (int w = 0; w < kBsWarps; ++w) {
+    const uint32_t t = wh[w][d];
+    wh[w][d] = cnt;
+    cnt += t;
+  }
+  // ---- decoupled look-back over the predecessors' per-digit counts
+  uint32_t* my = status + (size_t)bid * 256 + d;
+  uint32_t excl = 0;
+  if (bid == 0) {
+    atomicExch(my, kFlagInc | cnt);
+  } else {
+    atomicExch(my, kFlagAgg | cnt);
+    for (int64_t p = (int64_t)bid - 1; p >= 0; --p) {
+      uint32_t st;
+      do {
+        st = ld_volatile(status + (size_t)p * 256 + d);
+      } while ((st & ~kCntMask) == 0);
+      excl += st & kCntMask;
+      if (st & kFlagInc) break;
+    }
+    atomicExch(my, kFlagInc | (excl + cnt));
+  }
+  // ---- exclusive scans over digits: global digit offsets and tile-local starts
+  const uint32_t h = hist[d];
+  s_scan[d] = h;
+  s_lstart[d] = cnt;
+  __syncthreads();
+  for (int off = 1; off < 256; off <<= 1) {
+    const uint32_t a = d >= off ? s_scan[d - off] : 0u;
+    const uint32_t b = d >= off ? s_lstart[d - off] : 0u;
+    __syncthreads();
+    s_scan[d] += a;
+    s_lstart[d] += b;
+    __syncthreads();
+  }
+  const uint32_t g_excl = s_scan[d] - h;
+  const uint32_t l_excl = s_lstart[d] - cnt;
+  __syncthreads();
+  s_lstart[d] = l_excl;
+  s_gbase[d] = g_excl + excl;
+  __syncthreads();
+  // ---- stage in sorted order, then coalesced write-out
+#pragma unroll
+  for (int s = 0; s < kBsSteps; ++s) {
+    const int64_t i = wbase + s * 32 + lane;
+    if (i < n) {
+      const uint32_t dd = (k[s] >> shift) & dmask;
+      const uint32_t p = s_lstart[dd] + wh[warp][dd] + rk[s];
+      s_keys[p] = k[s];
+      s_vals[p] = v[s];
+    }
+  }
+  __syncthreads();
+  const int cnt_tile = (int)min((int64_t)kBsTile, n - base);
+  for (int i = tid; i < cnt_tile; i += kBsThreads) {
+    const uint32_t key = s_keys[i];
+    const uint32_t dd = (key >> shift) & dmask;
+    const uint32_t gp = s_gbase[dd] + (uint32_t)i - s_lstart[dd];
+    kout[gp] = key;
+    vout[gp] = s_vals[i];
+  }
+}
+
+int binsort_passes(int key_bits) { return key_bits > 8 ? 2 : 1; }
+
+// Sorts the (count *d_n, at most cap) pairs by the low `key_bits` bits into
+// keys_out/vals_out.  The input must be in keys_out/vals_out for two passes
+// (out -> tmp -> out) and in keys_tmp/vals_tmp for one (tmp -> out): see
+// binsort_passes().
+int binsort_run(const BinSortWS& w, uint32_t* keys_tmp, uint32_t* vals_tmp, uint32_t* keys_out,
+                uint32_t* vals_out, const int64_t* d_n, int64_t cap, int key_bits,
+                cudaStream_t st) {
+  if (key_bits > 16) {
+    set_error("binsort: more than 2^16 tiles");
+    return SS_ERR_DATA;
+  }
+  const int b0 = key_bits < 8 ? key_bits : 8, b1 = key_bits - b0;
+  SS_CUDA(cudaMemsetAsync(w.hist, 0, binsort_clear_bytes(w), st));
+  SS_CUDA(cudaMemsetAsync(w.status, 0, (size_t)(b1 > 0 ? 2 : 1) * w.max_blocks * 256 *
+                                           sizeof(uint32_t), st));
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  uint32_t* src_k = b1 > 0 ? keys_out : keys_tmp;
+  const unsigned hgrid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(cap, 256), 4 * sms));
+  bs_hist_kernel<<<hgrid, 256, 0, st>>>(src_k, d_n, cap, b0, b1, w.hist);
+  SS_CHECK_LAUNCH("bs_hist_kernel");
+  uint32_t* tickets = w.hist + 512;
+  const unsigned grid = (unsigned)w.max_blocks;
+  if (b1 == 0) {
+    bs_pass_kernel<<<grid, kBsThreads, 0, st>>>(keys_tmp, vals_tmp, keys_out, vals_out, d_n, cap,
+                                                0, b0, w.hist, tickets, w.status);
+    SS_CHECK_LAUNCH("bs_pass_kernel");
+    return SS_OK;
+  }
+  bs_pass_kernel<<<grid, kBsThreads, 0, st>>>(keys_out, vals_out, keys_tmp, vals_tmp, d_n, cap, 0,
+                                              b0, w.hist, tickets, w.status);
+  SS_CHECK_LAUNCH("bs_pass_kernel");
+  bs_pass_kernel<<<grid, kBsThreads, 0, st>>>(keys_tmp, vals_tmp, keys_out, vals_out, d_n, cap, b0,
+                                              b1, w.hist + 256, tickets + 1,
+                                              w.status + (size_t)w.max_blocks * 256);
+  SS_CHECK_LAUNCH("bs_pass_kernel");
+  return SS_OK;
+}
+
+}  // namespace ss

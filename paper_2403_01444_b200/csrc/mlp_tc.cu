@@ -1,22 +1,37 @@
-// NTC decoder forward on the 5th-generation tensor cores (K2f, ntc.py:241-248).
+// NTC decoder on the 5th-generation tensor cores: forward (K2f, ntc.py:241-248)
+// and backward (K2b, ntc.py:258-276).
 //
-// Persistent CTAs of 128 threads walk 128-row tiles of the feature matrix X.
-// Per tile, three chained tcgen05.mma.kind::tf32 GEMMs (M = 128 rows,
-// N = 64 / 64 / 16, K = in / 64 / 64) accumulate in TMEM; between them each
-// thread owns one TMEM lane (= one row): tcgen05.ld, bias + ReLU, and the next
-// layer's A tile is written back to shared memory.  Weights are staged once
-// per CTA as K-major B tiles.
+// Both kernels are persistent: one CTA of 512 threads per SM walks 128-row
+// tiles of the feature matrix X.  Row r of a tile lives in TMEM lane r; the
+// four warps that share a TMEM lane quarter (warps w, w+4, w+8, w+12) split the
+// accumulator columns, so every epilogue (tcgen05.ld, bias, ReLU, operand
+// split, st.shared) runs on 16 warps instead of 4.  One elected thread issues
+// the MMAs and commits them to an mbarrier.  The next tile's rows are
+// prefetched into registers while the current tile's MMAs run.
 //
-// Precision: P = 3 splits every operand into tf32 hi + lo parts and issues
-// A_hi.B_hi + A_hi.B_lo + A_lo.B_hi (3xTF32), which restores fp32-level
-// accuracy (the parity tests' 1e-3 gradient bar); P = 1 is plain tf32.
+// Precision:
+//  * forward: kind::tf32 with every operand split into tf32 hi + lo and three
+//    products per K step (3xTF32), i.e. fp32-level accuracy; mode 2 = tf32.
+//  * backward: kind::f16 with bf16 hi + lo operands and three products per K
+//    step (~16 mantissa bits, fp32 accumulation), because its transposed
+//    operands need MN-major descriptors (16-bit types).  The ReLU decisions are
+//    the forward's (relu_masks), so the gradient is that of the function the
+//    forward evaluated.
 #include "common.cuh"
 #include "umma.cuh"
 
 namespace ss {
 
+// per-stage clock64 stamps of CTA 0, thread 0, first tiles (ss_debug_mlp_trace)
+__device__ unsigned long long g_mlp_trace[2][64];
+#define SS_STAMP(k, i)                                                           \
+  do {                                                                           \
+    if (blockIdx.x == 0 && threadIdx.x == 0 && (i) < 64) g_mlp_trace[k][i] = clock64(); \
+  } while (0)
+
 namespace {
 constexpr int HIDT = 64;
+constexpr int NT = 512;  // threads per CTA: 4 per row, each a 16-column slice
 
 template <int IN, int NL>
 struct TcLay {  // same packed layout as ntc.cu's Lay<IN, NL>
@@ -26,6 +41,19 @@ struct TcLay {  // same packed layout as ntc.cu's Lay<IN, NL>
   static constexpr int B2 = W2 + HIDT * 8;
 };
 
+__device__ __forceinline__ void to_async() {
+  umma::fence_proxy_async();
+  umma::fence_before();
+  __syncthreads();
+}
+
+__device__ __forceinline__ void sync_mma(uint64_t* bar, uint32_t& phase) {
+  umma::mbar_wait(bar, phase);
+  phase ^= 1;
+  umma::fence_after();
+}
+
+// ---------------------------------------------------------------- tf32 pieces
 template <int IN, int NL, int P>
 struct TcFwdSmem {
   static constexpr uint32_t W0 = umma::tile_bytes(64, IN);
@@ -48,230 +76,69 @@ __device__ __forceinline__ void put(uint8_t* hi, uint32_t lo_off, uint32_t off, 
   if (P == 3) *reinterpret_cast<float*>(hi + lo_off + off) = umma::to_tf32(x - h);
 }
 
-// one layer: acc[M=128, N] (+)= A[128, K] . B[N, K]^T over K in steps of 8
+// 4 consecutive columns (one 16-byte core row) as a tf32 hi/lo pair
 template <int P>
-__device__ __forceinline__ void mma_layer(uint32_t acc, uint32_t a, uint32_t a_lo_off, int acols,
-                                          uint32_t b, uint32_t b_lo_off, int bcols, int K,
+__device__ __forceinline__ void put4(uint8_t* hi, uint32_t lo_off, uint32_t off, const float* v) {
+  float4 h, l;
+  h.x = umma::to_tf32(v[0]), h.y = umma::to_tf32(v[1]);
+  h.z = umma::to_tf32(v[2]), h.w = umma::to_tf32(v[3]);
+  *reinterpret_cast<float4*>(hi + off) = h;
+  if (P == 3) {
+    l.x = umma::to_tf32(v[0] - h.x), l.y = umma::to_tf32(v[1] - h.y);
+    l.z = umma::to_tf32(v[2] - h.z), l.w = umma::to_tf32(v[3] - h.w);
+    *reinterpret_cast<float4*>(hi + lo_off + off) = l;
+  }
+}
+
+// K-major tf32 operand: descriptors of the hi and lo planes at k = 0; one
+// 8-wide K step advances the start address by 256 bytes (16 in descriptor units).
+struct Op32 {
+  uint64_t hi, lo;
+};
+__device__ __forceinline__ Op32 op32(uint32_t addr, uint32_t lo_off, int cols) {
+  return {umma::desc_k(addr, cols, 0), umma::desc_k(addr + lo_off, cols, 0)};
+}
+
+// one layer: acc[M=128, N] (+)= A[128, K] . B[N, K]^T over K = 8 * NK
+template <int P, int NK>
+__device__ __forceinline__ void mma_layer(uint32_t acc, const Op32& A, const Op32& B,
                                           uint32_t idesc) {
-  for (int k = 0; k < K; k += 8) {
-    umma::mma_tf32(acc, umma::desc_k(a, acols, k), umma::desc_k(b, bcols, k), idesc, k > 0);
+#pragma unroll
+  for (int s = 0; s < NK; ++s) {
+    const uint64_t d = 16ull * s;
+    umma::mma_tf32(acc, A.hi + d, B.hi + d, idesc, s > 0);
     if (P == 3) {
-      umma::mma_tf32(acc, umma::desc_k(a, acols, k), umma::desc_k(b + b_lo_off, bcols, k), idesc,
-                     1);
-      umma::mma_tf32(acc, umma::desc_k(a + a_lo_off, acols, k), umma::desc_k(b, bcols, k), idesc,
-                     1);
+      umma::mma_tf32(acc, A.hi + d, B.lo + d, idesc, 1);
+      umma::mma_tf32(acc, A.lo + d, B.hi + d, idesc, 1);
     }
   }
 }
-}  // namespace
 
-template <int IN, int NL, int P>
-__global__ void __launch_bounds__(128, 1) mlp_fwd_tc_kernel(int64_t n, const float* __restrict__ X,
-                                                            int xs, const float* __restrict__ params,
-                                                            float* __restrict__ out, int os,
-                                                            uint64_t* __restrict__ relu_masks) {
-  using L = TcLay<IN, NL>;
-  using S = TcFwdSmem<IN, NL, P>;
-  extern __shared__ __align__(1024) uint8_t sm[];
-  __shared__ uint64_t bar;
-  __shared__ uint32_t tbase;
-  __shared__ float sbias[64 + 64 + 8];
-  const int tid = threadIdx.x, warp = tid >> 5;
-  // ---- stage the weights as K-major B tiles (rows = output unit, cols = input)
-  for (int i = tid; i < 64 * IN; i += 128) {
-    const int nn = i / IN, k = i % IN;
-    put<P>(sm + S::oW0, S::W0, umma::tile_off(nn, k, IN), params[L::W0 + k * 64 + nn]);
-  }
-  if (NL == 2)
-    for (int i = tid; i < 64 * 64; i += 128) {
-      const int nn = i / 64, k = i % 64;
-      put<P>(sm + S::oW1, S::W1, umma::tile_off(nn, k, 64), params[L::W1 + k * 64 + nn]);
-    }
-  for (int i = tid; i < 16 * 64; i += 128) {
-    const int nn = i / 64, k = i % 64;
-    put<P>(sm + S::oW2, S::W2, umma::tile_off(nn, k, 64), nn < 8 ? params[L::W2 + k * 8 + nn] : 0.f);
-  }
-  for (int i = tid; i < 64; i += 128) {
-    sbias[i] = params[L::B0 + i];
-    sbias[64 + i] = NL == 2 ? params[L::B1 + i] : 0.f;
-  }
-  if (tid < 8) sbias[128 + tid] = params[L::B2 + tid];
-  if (tid == 0) {
-    umma::mbar_init(&bar, 1);
-    umma::fence_mbar_init();
-  }
-  if (warp == 0) umma::tmem_alloc(&tbase, 256);
-  umma::fence_proxy_async();
-  umma::fence_before();
-  __syncthreads();
-  umma::fence_after();
-  const uint32_t tmem = tbase;
-  const uint32_t acc1 = tmem, acc2 = tmem + 64, acc3 = tmem + 128;
-  const uint32_t lane = (uint32_t)(warp * 32) << 16;
-  const uint32_t sW0 = umma::smem_u32(sm + S::oW0), sW1 = umma::smem_u32(sm + S::oW1);
-  const uint32_t sW2 = umma::smem_u32(sm + S::oW2);
-  const uint32_t sA0 = umma::smem_u32(sm + S::oA0), sA1 = umma::smem_u32(sm + S::oA1);
-  constexpr uint32_t id64 = umma::idesc_tf32(128, 64, 0, 0);
-  constexpr uint32_t id16 = umma::idesc_tf32(128, 16, 0, 0);
-  uint32_t phase = 0;
-  const int64_t ntiles = (n + 127) / 128;
-  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    const int64_t row = t * 128 + tid;
-    // ---- X row -> A0 (IN columns)
-#pragma unroll
-    for (int k = 0; k < IN; k += 4) {
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (row < n) v = *reinterpret_cast<const float4*>(X + row * xs + k);
-      put<P>(sm + S::oA0, S::A, umma::tile_off(tid, k, IN), v.x);
-      put<P>(sm + S::oA0, S::A, umma::tile_off(tid, k + 1, IN), v.y);
-      put<P>(sm + S::oA0, S::A, umma::tile_off(tid, k + 2, IN), v.z);
-      put<P>(sm + S::oA0, S::A, umma::tile_off(tid, k + 3, IN), v.w);
-    }
-    umma::fence_proxy_async();
-    umma::fence_before();
-    __syncthreads();
-    if (tid == 0) {
-      umma::fence_after();
-      mma_layer<P>(acc1, sA0, S::A, IN, sW0, S::W0, IN, IN, id64);
-      umma::commit(&bar);
-    }
-    umma::mbar_wait(&bar, phase);
-    phase ^= 1;
-    umma::fence_after();
-    // ---- h1 = relu(acc1 + b0) -> A1 (64 columns)
-    uint64_t m1 = 0, m2 = 0;
-#pragma unroll
-    for (int c0 = 0; c0 < 64; c0 += 16) {
-      float v[16];
-      umma::tmem_ld16(acc1 + lane + c0, v);
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const float h = fmaxf(v[j] + sbias[c0 + j], 0.f);
-        m1 |= (uint64_t)(h > 0.f) << (c0 + j);
-        put<P>(sm + S::oA1, S::A, umma::tile_off(tid, c0 + j, 64), h);
-      }
-    }
-    uint32_t last = sA1;
-    uint32_t last_lo = S::A;
-    if (NL == 2) {
-      umma::fence_proxy_async();
-      umma::fence_before();
-      __syncthreads();
-      if (tid == 0) {
-        umma::fence_after();
-        mma_layer<P>(acc2, sA1, S::A, 64, sW1, S::W1, 64, 64, id64);
-        umma::commit(&bar);
-      }
-      umma::mbar_wait(&bar, phase);
-      phase ^= 1;
-      umma::fence_after();
-#pragma unroll
-      for (int c0 = 0; c0 < 64; c0 += 16) {
-        float v[16];
-        umma::tmem_ld16(acc2 + lane + c0, v);
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const float h = fmaxf(v[j] + sbias[64 + c0 + j], 0.f);
-          m2 |= (uint64_t)(h > 0.f) << (c0 + j);
-          put<P>(sm + S::oA0, S::A, umma::tile_off(tid, c0 + j, 64), h);
-        }
-      }
-      last = sA0;
-    } else {
-      m2 = m1;
-    }
-    // the backward reuses the forward's ReLU decisions (self-consistent gradient)
-    if (relu_masks && row < n)
-      *reinterpret_cast<ulonglong2*>(relu_masks + 2 * row) = make_ulonglong2(m1, m2);
-    umma::fence_proxy_async();
-    umma::fence_before();
-    __syncthreads();
-    if (tid == 0) {
-      umma::fence_after();
-      mma_layer<P>(acc3, last, last_lo, 64, sW2, S::W2, 64, 64, id16);
-      umma::commit(&bar);
-    }
-    umma::mbar_wait(&bar, phase);
-    phase ^= 1;
-    umma::fence_after();
-    float o[8];
-    umma::tmem_ld8(acc3 + lane, o);
-    if (row < n) {
-      if (os == 8) {
-        *reinterpret_cast<float4*>(out + row * 8) =
-            make_float4(o[0] + sbias[128], o[1] + sbias[129], o[2] + sbias[130], o[3] + sbias[131]);
-        *reinterpret_cast<float4*>(out + row * 8 + 4) =
-            make_float4(o[4] + sbias[132], o[5] + sbias[133], o[6] + sbias[134], 0.f);
-      } else {
-#pragma unroll
-        for (int k = 0; k < 7; ++k) out[row * os + k] = o[k] + sbias[128 + k];
-      }
-    }
-    umma::fence_before();
-    __syncthreads();  // TMEM and the A tiles are reused by the next tile
-  }
-  if (warp == 0) {
-    umma::fence_after();
-    umma::tmem_free(tmem, 256);
-  }
-}
-
-// ------------------------------------------------------------------ backward
-// K2b on the tensor cores (ntc.py:258-276).  Persistent CTAs of 128 threads
-// walk 128-row tiles; per tile, with every operand split into bf16 hi + lo
-// parts (kind::f16, three products per K step, fp32 accumulation in TMEM):
-//
-//   recompute  H1 = relu(X W0 + b0), H2 = relu(H1 W1 + b1)      (M = 128)
-//   deltas     DL = (G W2^T) * [H_last > 0]
-//              D1 = (D2 W1^T) * [H1 > 0]                         (NL = 2)
-//              dX = D1 W0^T  -> HBM for the table scatter
-//   weights    dW2   += H_last^T G                                (M = 64, N = 8)
-//              dW1^T += D2^T [H1 | 1]   (column 64 = db1)         (M = 64, N = 72)
-//              dW0^T += D1^T [X | 1]    (column IN = db0)         (M = 64, N = IN + 8)
-//
-// The weight-gradient accumulators stay in TMEM across all tiles of the CTA
-// and are flushed once with reductions into g_params.  Transposed operands are
-// the same shared-memory tiles read through MN-major descriptors, so each
-// activation is staged exactly once.  db2 is summed in registers.
-namespace {
-template <int IN, int NL>
-struct TcBwdSmem {
-  static constexpr int XC = IN + 8, HC = 72;
-  static constexpr uint32_t W0 = umma::tile16_bytes(64, IN);
-  static constexpr uint32_t W1 = NL == 2 ? umma::tile16_bytes(64, 64) : 0;
-  static constexpr uint32_t W2 = umma::tile16_bytes(16, 64);
-  static constexpr uint32_t X = umma::tile16_bytes(128, XC);
-  static constexpr uint32_t H1 = umma::tile16_bytes(128, HC);
-  static constexpr uint32_t H2 = umma::tile16_bytes(128, 64);  // H2, then D1
-  static constexpr uint32_t G = umma::tile16_bytes(128, 16);
-  static constexpr uint32_t D2 = NL == 2 ? umma::tile16_bytes(128, 64) : 0;
-  // every tile is followed by its lo plane (same size)
-  static constexpr uint32_t oW0 = 0, oW1 = oW0 + 2 * W0, oW2 = oW1 + 2 * W1;
-  static constexpr uint32_t oX = oW2 + 2 * W2, oH1 = oX + 2 * X, oH2 = oH1 + 2 * H1;
-  static constexpr uint32_t oG = oH2 + 2 * H2, oD2 = oG + 2 * G;
-  static constexpr uint32_t BYTES = oD2 + 2 * D2;
-  // TMEM columns
-  static constexpr uint32_t cH1 = 0, cH2 = 64, cDL = 128, cD1 = 192, cDX = 256;
-  static constexpr uint32_t cW2 = 320, cW1 = 328, cW0 = 400;
-};
-
+// ---------------------------------------------------------------- bf16 pieces
+// 16-bit operand: descriptors of the hi and lo planes at k = 0 and the
+// descriptor increment of one 16-wide K step (2 core matrices along K)
 struct Op16 {
-  uint32_t addr, lo;  // hi plane address, byte distance to the lo plane
-  int cols, mn;       // stored tile columns, MN-major read
+  uint64_t hi, lo;
+  uint32_t kstep;
 };
-
-__device__ __forceinline__ uint64_t op_desc(const Op16& o, int k, int lo) {
-  const uint32_t a = o.addr + (lo ? o.lo : 0u);
-  return o.mn ? umma::desc16_mn(a, o.cols, k) : umma::desc16_k(a, o.cols, k);
+__device__ __forceinline__ Op16 op16(uint32_t addr, uint32_t lo_off, int cols, int mn) {
+  Op16 o;
+  o.hi = mn ? umma::desc16_mn(addr, cols, 0) : umma::desc16_k(addr, cols, 0);
+  o.lo = mn ? umma::desc16_mn(addr + lo_off, cols, 0) : umma::desc16_k(addr + lo_off, cols, 0);
+  o.kstep = (mn ? 2u * umma::sbo16(cols) : 256u) >> 4;
+  return o;
 }
 
-// acc (+)= A . B over K (multiple of 16) with the 3-product bf16 split
-__device__ __forceinline__ void gemm3(uint32_t acc, const Op16& A, const Op16& B, int K,
-                                      uint32_t idesc, uint32_t accumulate) {
-  for (int k = 0; k < K; k += 16) {
-    umma::mma_bf16(acc, op_desc(A, k, 0), op_desc(B, k, 0), idesc, accumulate | (k > 0));
-    umma::mma_bf16(acc, op_desc(A, k, 0), op_desc(B, k, 1), idesc, 1);
-    umma::mma_bf16(acc, op_desc(A, k, 1), op_desc(B, k, 0), idesc, 1);
+// acc (+)= A . B over K = 16 * NK with the 3-product bf16 split
+template <int NK>
+__device__ __forceinline__ void gemm3(uint32_t acc, const Op16& A, const Op16& B, uint32_t idesc,
+                                      uint32_t accumulate) {
+#pragma unroll
+  for (int s = 0; s < NK; ++s) {
+    const uint64_t da = (uint64_t)A.kstep * s, db = (uint64_t)B.kstep * s;
+    umma::mma_bf16(acc, A.hi + da, B.hi + db, idesc, accumulate | (s > 0));
+    umma::mma_bf16(acc, A.hi + da, B.lo + db, idesc, 1);
+    umma::mma_bf16(acc, A.lo + da, B.hi + db, idesc, 1);
   }
 }
 
@@ -301,32 +168,244 @@ __device__ __forceinline__ void put_scalar(uint8_t* tile, uint32_t lo_off, int r
   *reinterpret_cast<uint16_t*>(tile + lo_off + off) = l;
 }
 
-__device__ __forceinline__ void sync_mma(uint64_t* bar, uint32_t& phase) {
-  umma::mbar_wait(bar, phase);
-  phase ^= 1;
-  umma::fence_after();
-}
+// X row slices: thread quarter q owns column blocks 8q + 32b < IN
+template <int IN>
+struct XSlice {
+  static constexpr int NB = (IN + 31) / 32;
+  float v[NB][8];
+  __device__ __forceinline__ void load(const float* __restrict__ X, int64_t row, int xs, int q,
+                                       bool ok) {
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      const int c = 8 * q + 32 * b;
+      float4 a = make_float4(0.f, 0.f, 0.f, 0.f), d = a;
+      if (ok && c < IN) {
+        a = __ldg(reinterpret_cast<const float4*>(X + row * xs + c));
+        d = __ldg(reinterpret_cast<const float4*>(X + row * xs + c + 4));
+      }
+      v[b][0] = a.x, v[b][1] = a.y, v[b][2] = a.z, v[b][3] = a.w;
+      v[b][4] = d.x, v[b][5] = d.y, v[b][6] = d.z, v[b][7] = d.w;
+    }
+  }
+};
+}  // namespace
 
-__device__ __forceinline__ void to_async() {
-  umma::fence_proxy_async();
+// ================================================================= forward
+template <int IN, int NL, int P>
+__global__ void __launch_bounds__(NT, 1) mlp_fwd_tc_kernel(int64_t n, const float* __restrict__ X,
+                                                           int xs, const float* __restrict__ params,
+                                                           float* __restrict__ out, int os,
+                                                           uint64_t* __restrict__ relu_masks) {
+  using L = TcLay<IN, NL>;
+  using S = TcFwdSmem<IN, NL, P>;
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tbase;
+  __shared__ float sbias[64 + 64 + 8];
+  __shared__ uint16_t smask[2][4][128];
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int r = tid & 127, q = tid >> 7;
+  // ---- stage the weights as K-major B tiles (rows = output unit, cols = input)
+  for (int i = tid; i < 64 * IN; i += NT) {
+    const int nn = i / IN, k = i % IN;
+    put<P>(sm + S::oW0, S::W0, umma::tile_off(nn, k, IN), params[L::W0 + k * 64 + nn]);
+  }
+  if (NL == 2)
+    for (int i = tid; i < 64 * 64; i += NT) {
+      const int nn = i / 64, k = i % 64;
+      put<P>(sm + S::oW1, S::W1, umma::tile_off(nn, k, 64), params[L::W1 + k * 64 + nn]);
+    }
+  for (int i = tid; i < 16 * 64; i += NT) {
+    const int nn = i / 64, k = i % 64;
+    put<P>(sm + S::oW2, S::W2, umma::tile_off(nn, k, 64), nn < 8 ? params[L::W2 + k * 8 + nn] : 0.f);
+  }
+  if (tid < 64) {
+    sbias[tid] = params[L::B0 + tid];
+    sbias[64 + tid] = NL == 2 ? params[L::B1 + tid] : 0.f;
+  }
+  if (tid < 8) sbias[128 + tid] = params[L::B2 + tid];
+  if (tid == 0) {
+    umma::mbar_init(&bar, 1);
+    umma::fence_mbar_init();
+  }
+  if (warp == 0) umma::tmem_alloc(&tbase, 256);
+  to_async();
+  umma::fence_after();
+  const uint32_t tmem = tbase;
+  const uint32_t acc1 = tmem, acc2 = tmem + 64, acc3 = tmem + 128;
+  const uint32_t lane = (uint32_t)((warp & 3) * 32) << 16;
+  const Op32 dW0 = op32(umma::smem_u32(sm + S::oW0), S::W0, IN);
+  const Op32 dW1 = op32(umma::smem_u32(sm + S::oW1), S::W1, 64);
+  const Op32 dW2 = op32(umma::smem_u32(sm + S::oW2), S::W2, 64);
+  const Op32 dX0 = op32(umma::smem_u32(sm + S::oA0), S::A, IN);
+  const Op32 dA0 = op32(umma::smem_u32(sm + S::oA0), S::A, 64);
+  const Op32 dA1 = op32(umma::smem_u32(sm + S::oA1), S::A, 64);
+  constexpr uint32_t id64 = umma::idesc_tf32(128, 64, 0, 0);
+  constexpr uint32_t id16 = umma::idesc_tf32(128, 16, 0, 0);
+  const int c0 = 16 * q;  // this thread's accumulator columns
+  uint32_t phase = 0;
+  const int64_t ntiles = (n + 127) / 128;
+  XSlice<IN> xr;
+  // X slice of the prefetched tile -> A0 and the first layer's MMAs
+  auto issue_l1 = [&]() {
+#pragma unroll
+    for (int b = 0; b < XSlice<IN>::NB; ++b) {
+      const int c = 8 * q + 32 * b;
+      if (c < IN) {
+        put4<P>(sm + S::oA0, S::A, umma::tile_off(r, c, IN), xr.v[b]);
+        put4<P>(sm + S::oA0, S::A, umma::tile_off(r, c + 4, IN), xr.v[b] + 4);
+      }
+    }
+    to_async();
+    if (tid == 0) {
+      umma::fence_after();
+      mma_layer<P, IN / 8>(acc1, dX0, dW0, id64);
+      umma::commit(&bar);
+    }
+  };
+  if (blockIdx.x < ntiles) {
+    xr.load(X, (int64_t)blockIdx.x * 128 + r, xs, q, (int64_t)blockIdx.x * 128 + r < n);
+    issue_l1();
+  }
+  int it = 0;
+  SS_STAMP(0, 0);
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+    const int64_t row = t * 128 + r;
+    SS_STAMP(0, 1 + 8 * it);
+    {
+      const int64_t nrow = (t + gridDim.x) * 128 + r;
+      xr.load(X, nrow, xs, q, t + gridDim.x < ntiles && nrow < n);
+    }
+    sync_mma(&bar, phase);
+    SS_STAMP(0, 2 + 8 * it);
+    // ---- h1 = relu(acc1 + b0) -> A1 (64 columns), this thread's 16
+    uint32_t m1 = 0, m2 = 0;
+    {
+      float v[16];
+      umma::tmem_ld16(acc1 + lane + c0, v);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        v[j] = fmaxf(v[j] + sbias[c0 + j], 0.f);
+        m1 |= (uint32_t)(v[j] > 0.f) << j;
+      }
+#pragma unroll
+      for (int j = 0; j < 16; j += 4) put4<P>(sm + S::oA1, S::A, umma::tile_off(r, c0 + j, 64), v + j);
+    }
+    if (NL == 2) {
+      SS_STAMP(0, 3 + 8 * it);
+      to_async();
+      if (tid == 0) {
+        umma::fence_after();
+        mma_layer<P, 8>(acc2, dA1, dW1, id64);
+        umma::commit(&bar);
+      }
+      sync_mma(&bar, phase);
+      SS_STAMP(0, 4 + 8 * it);
+      float v[16];
+      umma::tmem_ld16(acc2 + lane + c0, v);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        v[j] = fmaxf(v[j] + sbias[64 + c0 + j], 0.f);
+        m2 |= (uint32_t)(v[j] > 0.f) << j;
+      }
+#pragma unroll
+      for (int j = 0; j < 16; j += 4) put4<P>(sm + S::oA0, S::A, umma::tile_off(r, c0 + j, 64), v + j);
+    } else {
+      m2 = m1;
+    }
+    smask[0][q][r] = (uint16_t)m1;
+    smask[1][q][r] = (uint16_t)m2;
+    SS_STAMP(0, 5 + 8 * it);
+    to_async();
+    if (tid == 0) {
+      umma::fence_after();
+      mma_layer<P, 8>(acc3, NL == 2 ? dA0 : dA1, dW2, id16);
+      umma::commit(&bar);
+    }
+    // the backward reuses the forward's ReLU decisions (self-consistent gradient)
+    if (q == 1 && relu_masks && row < n) {
+      uint64_t a = 0, b = 0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        a |= (uint64_t)smask[0][k][r] << (16 * k);
+        b |= (uint64_t)smask[1][k][r] << (16 * k);
+      }
+      *reinterpret_cast<ulonglong2*>(relu_masks + 2 * row) = make_ulonglong2(a, b);
+    }
+    sync_mma(&bar, phase);
+    SS_STAMP(0, 6 + 8 * it);
+    // ---- the next tile's first layer runs under this tile's output epilogue
+    if (t + gridDim.x < ntiles) issue_l1();
+    SS_STAMP(0, 7 + 8 * it);
+    if (q == 0) {
+      float o[8];
+      umma::tmem_ld8(acc3 + lane, o);
+      if (row < n) {
+        if (os == 8) {
+          *reinterpret_cast<float4*>(out + row * 8) = make_float4(
+              o[0] + sbias[128], o[1] + sbias[129], o[2] + sbias[130], o[3] + sbias[131]);
+          *reinterpret_cast<float4*>(out + row * 8 + 4) =
+              make_float4(o[4] + sbias[132], o[5] + sbias[133], o[6] + sbias[134], 0.f);
+        } else {
+#pragma unroll
+          for (int k = 0; k < 7; ++k) out[row * os + k] = o[k] + sbias[128 + k];
+        }
+      }
+    }
+  }
   umma::fence_before();
   __syncthreads();
-}
-
-// TMEM row (64 columns from col) -> f(row values, column block) in blocks of 16
-template <class Fn>
-__device__ __forceinline__ void tmem_row64(uint32_t taddr, Fn&& fn) {
-#pragma unroll
-  for (int c0 = 0; c0 < 64; c0 += 16) {
-    float v[16];
-    umma::tmem_ld16(taddr + c0, v);
-    fn(v, c0);
+  if (warp == 0) {
+    umma::fence_after();
+    umma::tmem_free(tmem, 256);
   }
 }
+
+// ================================================================= backward
+// Per 128-row tile, every operand split into bf16 hi + lo.  With the forward's
+// ReLU masks given, the delta chain does not depend on the recomputed
+// activations, so the two chains run side by side in three MMA stages:
+//
+//   stage 1   H1 = X W0 (+ b0)                 DL = G W2^T
+//             -> H1 = relu * m1                -> D_last = DL * m_last
+//   stage 2   H2 = H1 W1 (+ b1)                D1 = D2 W1^T          (NL = 2)
+//             dW1^T += D2^T [H1 | 1]  (col 64 = db1)
+//             -> H2 = relu * m2                -> D1 *= m1
+//   stage 3   dX = D1 W0^T -> HBM (table scatter)
+//             dW0^T += D1^T [X | 1]   (col IN = db0)
+//             dW2   += H_last^T G
+//
+// Stage 1 of the next tile is issued before stage 3's epilogue (dX) runs.  The
+// weight-gradient accumulators (M = 64) stay in TMEM across the CTA's tiles and
+// are flushed once with reductions into g_params.  Transposed operands are the
+// same shared-memory tiles read through MN-major descriptors.  db2 is summed in
+// registers.
+namespace {
+template <int IN, int NL>
+struct TcBwdSmem {
+  static constexpr int XC = IN + 8, HC = 72;
+  static constexpr uint32_t W0 = umma::tile16_bytes(64, IN);
+  static constexpr uint32_t W1 = NL == 2 ? umma::tile16_bytes(64, 64) : 0;
+  static constexpr uint32_t W2 = umma::tile16_bytes(16, 64);
+  static constexpr uint32_t X = umma::tile16_bytes(128, XC);
+  static constexpr uint32_t H1 = umma::tile16_bytes(128, HC);
+  static constexpr uint32_t H2 = NL == 2 ? umma::tile16_bytes(128, 64) : 0;
+  static constexpr uint32_t G = umma::tile16_bytes(128, 16);
+  static constexpr uint32_t D2 = NL == 2 ? umma::tile16_bytes(128, 64) : 0;
+  static constexpr uint32_t D1 = umma::tile16_bytes(128, 64);
+  // every tile is followed by its lo plane (same size)
+  static constexpr uint32_t oW0 = 0, oW1 = oW0 + 2 * W0, oW2 = oW1 + 2 * W1;
+  static constexpr uint32_t oX = oW2 + 2 * W2, oH1 = oX + 2 * X, oH2 = oH1 + 2 * H1;
+  static constexpr uint32_t oG = oH2 + 2 * H2, oD2 = oG + 2 * G, oD1 = oD2 + 2 * D2;
+  static constexpr uint32_t BYTES = oD1 + 2 * D1;
+  // TMEM columns
+  static constexpr uint32_t cH1 = 0, cDL = 64, cH2 = 128, cD1 = 192, cDX = 256;
+  static constexpr uint32_t cW2 = 320, cW1 = 328, cW0 = 400;
+};
 }  // namespace
 
 template <int IN, int NL>
-__global__ void __launch_bounds__(128, 1) mlp_bwd_tc_kernel(
+__global__ void __launch_bounds__(NT, 1) mlp_bwd_tc_kernel(
     int64_t n, const float* __restrict__ X, int xs, const float* __restrict__ g_out, int gs,
     const uint64_t* __restrict__ relu_masks, const float* __restrict__ params,
     float* __restrict__ dX, float* __restrict__ g_params) {
@@ -337,19 +416,22 @@ __global__ void __launch_bounds__(128, 1) mlp_bwd_tc_kernel(
   __shared__ uint64_t bar;
   __shared__ uint32_t tbase;
   __shared__ float sbias[128];
+  __shared__ float sdb2[4][8];
   const int tid = threadIdx.x, warp = tid >> 5, lane_id = tid & 31;
+  const int r = tid & 127, q = tid >> 7;
+  const int c0 = 16 * q;  // this thread's 16 columns of every 64-wide accumulator
   // ---- weights as bf16 hi/lo tiles: W0t (j, f) = W0[f][j]; W1t (j, i) = W1[i][j];
   //      W2t (o, j) = W2[j][o] (rows 7..15 zero)
-  for (int i = tid; i < 64 * IN; i += 128) {
+  for (int i = tid; i < 64 * IN; i += NT) {
     const int j = i / IN, f = i % IN;
     put_scalar(sm + S::oW0, S::W0, j, f, IN, params[L::W0 + f * 64 + j]);
   }
   if (NL == 2)
-    for (int i = tid; i < 64 * 64; i += 128) {
+    for (int i = tid; i < 64 * 64; i += NT) {
       const int j = i / 64, k = i % 64;
       put_scalar(sm + S::oW1, S::W1, j, k, 64, params[L::W1 + k * 64 + j]);
     }
-  for (int i = tid; i < 16 * 64; i += 128) {
+  for (int i = tid; i < 16 * 64; i += NT) {
     const int o = i / 64, j = i % 64;
     put_scalar(sm + S::oW2, S::W2, o, j, 64, o < 7 ? params[L::W2 + j * 8 + o] : 0.f);
   }
@@ -357,13 +439,13 @@ __global__ void __launch_bounds__(128, 1) mlp_bwd_tc_kernel(
     sbias[tid] = params[L::B0 + tid];
     sbias[64 + tid] = NL == 2 ? params[L::B1 + tid] : 0.f;
   }
-  // constant columns: X col IN = 1 (db0), H1 col 64 = 1 (db1), the rest of the pads 0
+  // constant columns: X col IN = 1 (db0), H1 col 64 = 1 (db1), G cols 8..15 = 0
   {
-    float pad[8] = {1.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    put8(sm + S::oX, S::X, tid, IN, XC, pad);
-    put8(sm + S::oH1, S::H1, tid, 64, HC, pad);
-    float z[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    put8(sm + S::oG, S::G, tid, 8, 16, z);
+    const float pad[8] = {1.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    const float z[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    if (q == 0) put8(sm + S::oX, S::X, r, IN, XC, pad);
+    if (q == 1) put8(sm + S::oH1, S::H1, r, 64, HC, pad);
+    if (q == 2) put8(sm + S::oG, S::G, r, 8, 16, z);
   }
   if (tid == 0) {
     umma::mbar_init(&bar, 1);
@@ -373,22 +455,21 @@ __global__ void __launch_bounds__(128, 1) mlp_bwd_tc_kernel(
   to_async();
   umma::fence_after();
   const uint32_t tmem = tbase;
-  const uint32_t lane = (uint32_t)(warp * 32) << 16;
-  const Op16 oX_k{umma::smem_u32(sm + S::oX), S::X, XC, 0};
-  const Op16 oX_mn{oX_k.addr, S::X, XC, 1};
-  const Op16 oW0_k{umma::smem_u32(sm + S::oW0), S::W0, IN, 0};
-  const Op16 oW0_mn{oW0_k.addr, S::W0, IN, 1};
-  const Op16 oW1_k{umma::smem_u32(sm + S::oW1), S::W1, 64, 0};
-  const Op16 oW1_mn{oW1_k.addr, S::W1, 64, 1};
-  const Op16 oW2_mn{umma::smem_u32(sm + S::oW2), S::W2, 64, 1};
-  const Op16 oH1_k{umma::smem_u32(sm + S::oH1), S::H1, HC, 0};
-  const Op16 oH1_mn{oH1_k.addr, S::H1, HC, 1};
-  const Op16 oH2_k{umma::smem_u32(sm + S::oH2), S::H2, 64, 0};  // also D1
-  const Op16 oH2_mn{oH2_k.addr, S::H2, 64, 1};
-  const Op16 oG_k{umma::smem_u32(sm + S::oG), S::G, 16, 0};
-  const Op16 oG_mn{oG_k.addr, S::G, 16, 1};
-  const Op16 oD2_k{umma::smem_u32(sm + S::oD2), S::D2, 64, 0};
-  const Op16 oD2_mn{oD2_k.addr, S::D2, 64, 1};
+  const uint32_t lane = (uint32_t)((warp & 3) * 32) << 16;
+  const uint32_t aX = umma::smem_u32(sm + S::oX), aW0 = umma::smem_u32(sm + S::oW0);
+  const uint32_t aW1 = umma::smem_u32(sm + S::oW1), aW2 = umma::smem_u32(sm + S::oW2);
+  const uint32_t aH1 = umma::smem_u32(sm + S::oH1), aH2 = umma::smem_u32(sm + S::oH2);
+  const uint32_t aG = umma::smem_u32(sm + S::oG), aD2 = umma::smem_u32(sm + S::oD2);
+  const uint32_t aD1 = umma::smem_u32(sm + S::oD1);
+  const Op16 oX_k = op16(aX, S::X, XC, 0), oX_mn = op16(aX, S::X, XC, 1);
+  const Op16 oW0_k = op16(aW0, S::W0, IN, 0), oW0_mn = op16(aW0, S::W0, IN, 1);
+  const Op16 oW1_k = op16(aW1, S::W1, 64, 0), oW1_mn = op16(aW1, S::W1, 64, 1);
+  const Op16 oW2_mn = op16(aW2, S::W2, 64, 1);
+  const Op16 oH1_k = op16(aH1, S::H1, HC, 0), oH1_mn = op16(aH1, S::H1, HC, 1);
+  const Op16 oH2_mn = op16(aH2, S::H2, 64, 1);
+  const Op16 oG_k = op16(aG, S::G, 16, 0), oG_mn = op16(aG, S::G, 16, 1);
+  const Op16 oD2_k = op16(aD2, S::D2, 64, 0), oD2_mn = op16(aD2, S::D2, 64, 1);
+  const Op16 oD1_k = op16(aD1, S::D1, 64, 0), oD1_mn = op16(aD1, S::D1, 64, 1);
   const Op16 oHl_mn = NL == 2 ? oH2_mn : oH1_mn;
   constexpr uint32_t idF = umma::idesc_bf16(128, 64, 0, 0);
   constexpr uint32_t idB64 = umma::idesc_bf16(128, 64, 0, 1);
@@ -399,131 +480,142 @@ __global__ void __launch_bounds__(128, 1) mlp_bwd_tc_kernel(
   uint32_t phase = 0, acc_w = 0;
   float db2[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   const int64_t ntiles = (n + 127) / 128;
-  // register prefetch of this thread's X and g rows for the first tile
-  float xr[IN], gr[8];
-  ulonglong2 mr;
+  // register prefetch of this thread's slices of the X, g and mask rows
+  XSlice<IN> xr;
+  float gr[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  ulonglong2 mr = make_ulonglong2(0, 0);
   auto fetch = [&](int64_t t) {
-    const int64_t row = t * 128 + tid;
+    const int64_t row = t * 128 + r;
     const bool ok = t < ntiles && row < n;
-    mr = ok ? __ldg(reinterpret_cast<const ulonglong2*>(relu_masks) + row) : make_ulonglong2(0, 0);
+    xr.load(X, row, xs, q, ok);
+    if (q == 0) {
 #pragma unroll
-    for (int k = 0; k < IN; k += 4) {
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (ok) v = __ldg(reinterpret_cast<const float4*>(X + row * xs + k));
-      xr[k] = v.x, xr[k + 1] = v.y, xr[k + 2] = v.z, xr[k + 3] = v.w;
+      for (int k = 0; k < 8; ++k) gr[k] = (ok && k < 7) ? __ldg(g_out + row * gs + k) : 0.f;
     }
-#pragma unroll
-    for (int k = 0; k < 8; ++k) gr[k] = (ok && k < 7) ? __ldg(g_out + row * gs + k) : 0.f;
+    mr = ok ? __ldg(reinterpret_cast<const ulonglong2*>(relu_masks) + row) : make_ulonglong2(0, 0);
   };
-  fetch(blockIdx.x);
-  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    const int64_t row = t * 128 + tid;
-    // ---- stage A: X -> smem, H1 = X W0 (+ b0)
+  // X and G of the prefetched tile -> smem (their previous readers have completed)
+  auto stage_in = [&]() {
 #pragma unroll
-    for (int k = 0; k < IN; k += 8) put8(sm + S::oX, S::X, tid, k, XC, xr + k);
+    for (int b = 0; b < XSlice<IN>::NB; ++b) {
+      const int c = 8 * q + 32 * b;
+      if (c < IN) put8(sm + S::oX, S::X, r, c, XC, xr.v[b]);
+    }
+    if (q == 0) {
 #pragma unroll
-    for (int k = 0; k < 8; ++k) db2[k] += gr[k];
-    put8(sm + S::oG, S::G, tid, 0, 16, gr);
+      for (int k = 0; k < 8; ++k) db2[k] += gr[k];
+      put8(sm + S::oG, S::G, r, 0, 16, gr);
+    }
+  };
+  auto issue_stage1 = [&]() {
     to_async();
     if (tid == 0) {
       umma::fence_after();
-      gemm3(tmem + S::cH1, oX_k, oW0_k, IN, idF, 0);
+      gemm3<IN / 16>(tmem + S::cH1, oX_k, oW0_k, idF, 0);
+      gemm3<1>(tmem + S::cDL, oG_k, oW2_mn, idB64, 0);
       umma::commit(&bar);
     }
-    const uint64_t mask1 = mr.x, mask2 = mr.y;  // the forward's ReLU decisions
+  };
+  if (blockIdx.x < ntiles) {
+    fetch(blockIdx.x);
+    stage_in();
+    issue_stage1();
+  }
+  int it = 0;
+  SS_STAMP(1, 0);
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+    const int64_t row = t * 128 + r;
+    SS_STAMP(1, 1 + 8 * it);
+    const uint32_t mask1 = (uint32_t)(mr.x >> c0) & 0xFFFFu;  // the forward's ReLU decisions
+    const uint32_t mask2 = (uint32_t)(mr.y >> c0) & 0xFFFFu;
     fetch(t + gridDim.x);  // next tile's rows, overlapped with this tile
     sync_mma(&bar, phase);
-    tmem_row64(tmem + S::cH1 + lane, [&](float (&v)[16], int c0) {
+    SS_STAMP(1, 2 + 8 * it);
+    // ---- epilogue 1: H1, D_last
+    {
+      float v[16];
+      umma::tmem_ld16(tmem + S::cH1 + lane + c0, v);
 #pragma unroll
       for (int j = 0; j < 16; ++j)
-        v[j] = ((mask1 >> (c0 + j)) & 1) ? fmaxf(v[j] + sbias[c0 + j], 0.f) : 0.f;
-      put8(sm + S::oH1, S::H1, tid, c0, HC, v);
-      put8(sm + S::oH1, S::H1, tid, c0 + 8, HC, v + 8);
-    });
+        v[j] = ((mask1 >> j) & 1) ? fmaxf(v[j] + sbias[c0 + j], 0.f) : 0.f;
+      put8(sm + S::oH1, S::H1, r, c0, HC, v);
+      put8(sm + S::oH1, S::H1, r, c0 + 8, HC, v + 8);
+      umma::tmem_ld16(tmem + S::cDL + lane + c0, v);
+      const uint32_t ml = NL == 2 ? mask2 : mask1;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) v[j] = ((ml >> j) & 1) ? v[j] : 0.f;
+      uint8_t* dst = sm + (NL == 2 ? S::oD2 : S::oD1);
+      const uint32_t dlo = NL == 2 ? S::D2 : S::D1;
+      put8(dst, dlo, r, c0, 64, v);
+      put8(dst, dlo, r, c0 + 8, 64, v + 8);
+    }
     if (NL == 2) {
-      // ---- stage B: H2 = H1 W1 (+ b1)
+      // ---- stage 2: H2 = H1 W1;  D1 = D2 W1^T;  dW1^T += D2^T [H1 | 1]
+      SS_STAMP(1, 3 + 8 * it);
       to_async();
       if (tid == 0) {
         umma::fence_after();
-        gemm3(tmem + S::cH2, oH1_k, oW1_k, 64, idF, 0);
+        gemm3<4>(tmem + S::cH2, oH1_k, oW1_k, idF, 0);
+        gemm3<4>(tmem + S::cD1, oD2_k, oW1_mn, idB64, 0);
+        gemm3<8>(tmem + S::cW1, oD2_mn, oH1_mn, idW1, acc_w);
         umma::commit(&bar);
       }
       sync_mma(&bar, phase);
-      tmem_row64(tmem + S::cH2 + lane, [&](float (&v)[16], int c0) {
-#pragma unroll
-        for (int j = 0; j < 16; ++j)
-          v[j] = ((mask2 >> (c0 + j)) & 1) ? fmaxf(v[j] + sbias[64 + c0 + j], 0.f) : 0.f;
-        put8(sm + S::oH2, S::H2, tid, c0, 64, v);
-        put8(sm + S::oH2, S::H2, tid, c0 + 8, 64, v + 8);
-      });
-    }
-    // ---- stage C: DL = G W2^T;  dW2 += H_last^T G
-    to_async();
-    if (tid == 0) {
-      umma::fence_after();
-      gemm3(tmem + S::cDL, oG_k, oW2_mn, 16, idB64, 0);
-      gemm3(tmem + S::cW2, oHl_mn, oG_mn, 128, idW2, acc_w);
-      umma::commit(&bar);
-    }
-    sync_mma(&bar, phase);
-    {
-      // NL = 2: DL = D2 (own tile); NL = 1: DL = D1 (the H2 tile)
-      uint8_t* dst = sm + (NL == 2 ? S::oD2 : S::oH2);
-      const uint32_t dlo = NL == 2 ? S::D2 : S::H2;
-      tmem_row64(tmem + S::cDL + lane, [&](float (&v)[16], int c0) {
-#pragma unroll
-        for (int j = 0; j < 16; ++j) v[j] = ((mask2 >> (c0 + j)) & 1) ? v[j] : 0.f;
-        put8(dst, dlo, tid, c0, 64, v);
-        put8(dst, dlo, tid, c0 + 8, 64, v + 8);
-      });
-    }
-    if (NL == 2) {
-      // ---- stage D: D1 = D2 W1^T * mask1;  dW1^T += D2^T [H1 | 1]
-      to_async();
-      if (tid == 0) {
-        umma::fence_after();
-        gemm3(tmem + S::cD1, oD2_k, oW1_mn, 64, idB64, 0);
-        gemm3(tmem + S::cW1, oD2_mn, oH1_mn, 128, idW1, acc_w);
-        umma::commit(&bar);
-      }
-      sync_mma(&bar, phase);
-      tmem_row64(tmem + S::cD1 + lane, [&](float (&v)[16], int c0) {
-#pragma unroll
-        for (int j = 0; j < 16; ++j) v[j] = ((mask1 >> (c0 + j)) & 1) ? v[j] : 0.f;
-        put8(sm + S::oH2, S::H2, tid, c0, 64, v);
-        put8(sm + S::oH2, S::H2, tid, c0 + 8, 64, v + 8);
-      });
-    }
-    // ---- stage E: dX = D1 W0^T;  dW0^T += D1^T [X | 1]
-    to_async();
-    if (tid == 0) {
-      umma::fence_after();
-      gemm3(tmem + S::cDX, oH2_k, oW0_mn, 64, idBX, 0);
-      gemm3(tmem + S::cW0, oH2_mn, oX_mn, 128, idW0, acc_w);
-      umma::commit(&bar);
-    }
-    sync_mma(&bar, phase);
-    acc_w = 1;
-#pragma unroll
-    for (int c0 = 0; c0 < IN; c0 += 16) {
+      SS_STAMP(1, 4 + 8 * it);
       float v[16];
-      umma::tmem_ld16(tmem + S::cDX + lane + c0, v);
-      if (row < n) {
+      umma::tmem_ld16(tmem + S::cH2 + lane + c0, v);
 #pragma unroll
-        for (int j = 0; j < 16; j += 4)
-          *reinterpret_cast<float4*>(dX + row * xs + c0 + j) =
-              make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+      for (int j = 0; j < 16; ++j)
+        v[j] = ((mask2 >> j) & 1) ? fmaxf(v[j] + sbias[64 + c0 + j], 0.f) : 0.f;
+      put8(sm + S::oH2, S::H2, r, c0, 64, v);
+      put8(sm + S::oH2, S::H2, r, c0 + 8, 64, v + 8);
+      umma::tmem_ld16(tmem + S::cD1 + lane + c0, v);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) v[j] = ((mask1 >> j) & 1) ? v[j] : 0.f;
+      put8(sm + S::oD1, S::D1, r, c0, 64, v);
+      put8(sm + S::oD1, S::D1, r, c0 + 8, 64, v + 8);
+    }
+    // ---- stage 3: dX = D1 W0^T;  dW0^T += D1^T [X | 1];  dW2 += H_last^T G
+    SS_STAMP(1, 5 + 8 * it);
+    to_async();
+    if (tid == 0) {
+      umma::fence_after();
+      gemm3<4>(tmem + S::cDX, oD1_k, oW0_mn, idBX, 0);
+      gemm3<8>(tmem + S::cW0, oD1_mn, oX_mn, idW0, acc_w);
+      gemm3<8>(tmem + S::cW2, oHl_mn, oG_mn, idW2, acc_w);
+      umma::commit(&bar);
+    }
+    sync_mma(&bar, phase);
+    SS_STAMP(1, 6 + 8 * it);
+    acc_w = 1;
+    // ---- next tile's stage 1 runs under this tile's dX epilogue
+    if (t + gridDim.x < ntiles) {
+      stage_in();
+      issue_stage1();
+    }
+    SS_STAMP(1, 7 + 8 * it);
+#pragma unroll
+    for (int b = 0; b < XSlice<IN>::NB; ++b) {
+      const int c = 8 * q + 32 * b;
+      if (c < IN) {  // warp-uniform
+        float v[8];
+        umma::tmem_ld8(tmem + S::cDX + lane + c, v);
+        if (row < n) {
+          *reinterpret_cast<float4*>(dX + row * xs + c) = make_float4(v[0], v[1], v[2], v[3]);
+          *reinterpret_cast<float4*>(dX + row * xs + c + 4) = make_float4(v[4], v[5], v[6], v[7]);
+        }
       }
     }
-    umma::fence_before();
-    __syncthreads();  // the tiles of this iteration are rewritten by the next
   }
-  // ---- flush the weight gradients: M = 64 accumulators, row j = 16 w + lane (lane < 16)
+  // ---- flush the weight gradients: M = 64 accumulators, row j = 16 (w & 3) + lane
+  //      (lanes < 16); the four warps of a lane quarter take 8-column blocks 8q + 32b
+  umma::fence_before();
+  __syncthreads();
   umma::fence_after();
   if (acc_w) {
-    const int j = warp * 16 + lane_id;
+    const int j = (warp & 3) * 16 + lane_id;
     const bool own = lane_id < 16;
-    {
+    if (q == 0) {
       float v[8];
       umma::tmem_ld8(tmem + S::cW2 + lane, v);
       if (own) {
@@ -532,80 +624,66 @@ __global__ void __launch_bounds__(128, 1) mlp_bwd_tc_kernel(
       }
     }
     if (NL == 2) {
-      tmem_row64(tmem + S::cW1 + lane, [&](float (&v)[16], int c0) {
+      for (int c = 8 * q; c < HC; c += 32) {
+        float v[8];
+        umma::tmem_ld8(tmem + S::cW1 + lane + c, v);
         if (own) {
 #pragma unroll
-          for (int q = 0; q < 16; ++q) atomicAdd(g_params + L::W1 + (c0 + q) * 64 + j, v[q]);
+          for (int k = 0; k < 8; ++k) {
+            if (c + k < 64) atomicAdd(g_params + L::W1 + (c + k) * 64 + j, v[k]);
+            else if (c + k == 64) atomicAdd(g_params + L::B1 + j, v[k]);
+          }
         }
-      });
-      float v[8];
-      umma::tmem_ld8(tmem + S::cW1 + 64 + lane, v);
-      if (own) atomicAdd(g_params + L::B1 + j, v[0]);
-    }
-#pragma unroll
-    for (int c0 = 0; c0 < IN; c0 += 16) {
-      float v[16];
-      umma::tmem_ld16(tmem + S::cW0 + lane + c0, v);
-      if (own) {
-#pragma unroll
-        for (int q = 0; q < 16; ++q) atomicAdd(g_params + L::W0 + (c0 + q) * 64 + j, v[q]);
       }
     }
-    {
+    for (int c = 8 * q; c < XC; c += 32) {
       float v[8];
-      umma::tmem_ld8(tmem + S::cW0 + IN + lane, v);
-      if (own) atomicAdd(g_params + L::B0 + j, v[0]);
+      umma::tmem_ld8(tmem + S::cW0 + lane + c, v);
+      if (own) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          if (c + k < IN) atomicAdd(g_params + L::W0 + (c + k) * 64 + j, v[k]);
+          else if (c + k == IN) atomicAdd(g_params + L::B0 + j, v[k]);
+        }
+      }
     }
   }
+  if (q == 0) {
 #pragma unroll
-  for (int k = 0; k < 7; ++k) {
-    const float s = warp_sum(db2[k]);
-    if (lane_id == 0) atomicAdd(g_params + L::B2 + k, s);
+    for (int k = 0; k < 8; ++k) {
+      const float s = warp_sum(db2[k]);
+      if (lane_id == 0) sdb2[warp][k] = s;
+    }
   }
   umma::fence_before();
   __syncthreads();
+  if (tid < 7) {
+    float s = 0.f;
+#pragma unroll
+    for (int w = 0; w < 4; ++w) s += sdb2[w][tid];
+    atomicAdd(g_params + L::B2 + tid, s);
+  }
   if (warp == 0) {
     umma::fence_after();
     umma::tmem_free(tmem, 512);
   }
 }
 
-template <int IN, int NL>
-static int launch_bwd_tc(int64_t n, const float* X, int xs, const float* g, int gs,
-                         const uint64_t* masks, const float* params, float* dX, float* g_params,
-                         cudaStream_t st) {
-  constexpr uint32_t smem = TcBwdSmem<IN, NL>::BYTES;
-  static_assert(smem <= 220 * 1024, "backward tiles exceed shared memory");
-  auto k = mlp_bwd_tc_kernel<IN, NL>;
-  SS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const unsigned grid = (unsigned)std::min<int64_t>((n + 127) / 128, (int64_t)sms);
-  k<<<grid, 128, smem, st>>>(n, X, xs, g, gs, masks, params, dX, g_params);
-  SS_CHECK_LAUNCH("mlp_bwd_tc_kernel");
-  return SS_OK;
-}
-
-int mlp_bwd_tc(int in_pad, int n_hidden, int64_t n, const float* X, int xs, const float* g,
-               int gs, const uint64_t* masks, const float* params, float* dX, float* g_params,
-               cudaStream_t st) {
-  if (!masks) {
-    set_error("mlp_bwd_tc: the forward's ReLU masks are required");
-    return SS_ERR_DATA;
-  }
-#define SS_TCB(IN, NL)                   \
-  if (in_pad == IN && n_hidden == NL) \
-    return launch_bwd_tc<IN, NL>(n, X, xs, g, gs, masks, params, dX, g_params, st);
-  SS_TCB(16, 1) SS_TCB(16, 2) SS_TCB(32, 1) SS_TCB(32, 2) SS_TCB(64, 1) SS_TCB(64, 2)
-#undef SS_TCB
-  set_error("mlp_bwd_tc: unsupported decoder shape");
-  return SS_ERR_DATA;
-}
-
-static int g_mlp_mode = 1;  // 0 FFMA fp32, 1 tensor cores 3xTF32, 2 tensor cores tf32
+// ================================================================= launch
+static int g_mlp_mode = 1;  // 0 FFMA fp32, 1 tensor cores 3xTF32 / bf16x3, 2 tensor cores tf32
 
 int mlp_mode() { return g_mlp_mode; }
+
+static int num_sms_tc() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
+}
 
 template <int IN, int NL, int P>
 static int launch_tc(int64_t n, const float* X, int xs, const float* params, float* out, int os,
@@ -613,12 +691,8 @@ static int launch_tc(int64_t n, const float* X, int xs, const float* params, flo
   constexpr uint32_t smem = TcFwdSmem<IN, NL, P>::BYTES;
   auto k = mlp_fwd_tc_kernel<IN, NL, P>;
   SS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int per_sm = smem <= 100 * 1024 ? 2 : 1;
-  const unsigned grid = (unsigned)std::min<int64_t>((n + 127) / 128, (int64_t)sms * per_sm);
-  k<<<grid, 128, smem, st>>>(n, X, xs, params, out, os, masks);
+  const unsigned grid = (unsigned)std::min<int64_t>((n + 127) / 128, (int64_t)num_sms_tc());
+  k<<<grid, NT, smem, st>>>(n, X, xs, params, out, os, masks);
   SS_CHECK_LAUNCH("mlp_fwd_tc_kernel");
   return SS_OK;
 }
@@ -636,6 +710,36 @@ int mlp_fwd_tc(int in_pad, int n_hidden, int64_t n, const float* X, int xs, cons
   return SS_ERR_DATA;
 }
 
+template <int IN, int NL>
+static int launch_bwd_tc(int64_t n, const float* X, int xs, const float* g, int gs,
+                         const uint64_t* masks, const float* params, float* dX, float* g_params,
+                         cudaStream_t st) {
+  constexpr uint32_t smem = TcBwdSmem<IN, NL>::BYTES;
+  static_assert(smem <= 220 * 1024, "backward tiles exceed shared memory");
+  auto k = mlp_bwd_tc_kernel<IN, NL>;
+  SS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const unsigned grid = (unsigned)std::min<int64_t>((n + 127) / 128, (int64_t)num_sms_tc());
+  k<<<grid, NT, smem, st>>>(n, X, xs, g, gs, masks, params, dX, g_params);
+  SS_CHECK_LAUNCH("mlp_bwd_tc_kernel");
+  return SS_OK;
+}
+
+int mlp_bwd_tc(int in_pad, int n_hidden, int64_t n, const float* X, int xs, const float* g,
+               int gs, const uint64_t* masks, const float* params, float* dX, float* g_params,
+               cudaStream_t st) {
+  if (!masks) {
+    set_error("mlp_bwd_tc: the forward's ReLU masks are required");
+    return SS_ERR_DATA;
+  }
+#define SS_TCB(IN, NL)                \
+  if (in_pad == IN && n_hidden == NL) \
+    return launch_bwd_tc<IN, NL>(n, X, xs, g, gs, masks, params, dX, g_params, st);
+  SS_TCB(16, 1) SS_TCB(16, 2) SS_TCB(32, 1) SS_TCB(32, 2) SS_TCB(64, 1) SS_TCB(64, 2)
+#undef SS_TCB
+  set_error("mlp_bwd_tc: unsupported decoder shape");
+  return SS_ERR_DATA;
+}
+
 }  // namespace ss
 
 extern "C" int ss_set_mlp_mode(int32_t mode) {
@@ -644,3 +748,9 @@ extern "C" int ss_set_mlp_mode(int32_t mode) {
   return SS_OK;
 }
 extern "C" int32_t ss_get_mlp_mode(void) { return ss::g_mlp_mode; }
+
+// debug: clock64 stamps of CTA 0 (kernel 0 = forward, 1 = backward), 64 each
+extern "C" int ss_debug_mlp_trace(uint64_t* out) {
+  SS_CUDA(cudaMemcpyFromSymbol(out, ss::g_mlp_trace, sizeof(ss::g_mlp_trace)));
+  return SS_OK;
+}

@@ -42,8 +42,8 @@ struct Geom {
 
 struct Bins {
   uint32_t *keys_in, *keys_out, *vals_in, *vals_out;
-  void* cub_sort;
-  size_t cub_sort_bytes;
+  int64_t capacity;  // pairs the buffers hold; the count itself stays on the device
+  BinSortWS sort;
   size_t total;
 };
 
@@ -98,21 +98,22 @@ static Geom plan_geom(void* base, int64_t n, const ss_camera* cam, const ss_rast
   return g;
 }
 
-static Bins plan_bins(void* base, int64_t pairs) {
+static Bins plan_bins(void* base, int64_t capacity) {
   Bins b{};
   Carve c(base);
-  const int64_t pp = pairs > 0 ? pairs : 1;
+  const int64_t pp = capacity > 0 ? capacity : 1;
+  b.capacity = pp;
   b.keys_in = c.take<uint32_t>(pp);
   b.keys_out = c.take<uint32_t>(pp);
   b.vals_in = c.take<uint32_t>(pp);
   b.vals_out = c.take<uint32_t>(pp);
-  size_t sb = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, sb, (const uint32_t*)nullptr, (uint32_t*)nullptr,
-                                  (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)pp);
-  b.cub_sort_bytes = sb;
-  b.cub_sort = c.take<char>(sb);
+  b.sort = binsort_plan(c, pp);
   b.total = c.bytes();
   return b;
+}
+
+static unsigned stride_grid(int64_t items) {
+  return (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(items, 256), 148 * 16));
 }
 
 // ------------------------------------------------------------------ projection
@@ -284,28 +285,63 @@ __global__ void finish_counts_kernel(Geom g, int64_t n) {
 // K4c: emit (tile id, rank) in rank order, one thread per pair (load-balanced:
 // near-camera splats can cover thousands of tiles).  The owning rank is the last
 // r with offsets[r] <= j (zero-count ranks are skipped by construction).
-__global__ void duplicate_kernel(int ntx, int64_t n, int64_t pairs, Geom g, Bins b) {
-  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (j >= pairs) return;
-  int64_t lo = 0, hi = n;  // offsets[lo] <= j < offsets[hi]
-  while (hi - lo > 1) {
-    const int64_t mid = (lo + hi) >> 1;
-    if (g.offsets[mid] <= j) lo = mid; else hi = mid;
+__global__ void duplicate_kernel(int ntx, int64_t n, Geom g, Bins b, uint32_t* kdst,
+                                 uint32_t* vdst, uint32_t* status) {
+  const int64_t count = g.dev_counts[1];
+  if (count > b.capacity && blockIdx.x == 0 && threadIdx.x == 0 && status)
+    atomicOr(status, SS_FLAG_OVERFLOW);
+  const int64_t pairs = min(count, b.capacity);
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < pairs;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    int64_t lo = 0, hi = n;  // offsets[lo] <= j < offsets[hi]
+    while (hi - lo > 1) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (g.offsets[mid] <= j) lo = mid; else hi = mid;
+    }
+    const int4 rc = g.r_rect[lo];
+    const int wx = rc.y - rc.x + 1;
+    const int local = (int)(j - g.offsets[lo]);
+    const int ty = rc.z + local / wx, tx = rc.x + local % wx;
+    kdst[j] = (uint32_t)(ty * ntx + tx);
+    vdst[j] = (uint32_t)lo;
   }
-  const int4 rc = g.r_rect[lo];
-  const int wx = rc.y - rc.x + 1;
-  const int local = (int)(j - g.offsets[lo]);
-  const int ty = rc.z + local / wx, tx = rc.x + local % wx;
-  b.keys_in[j] = (uint32_t)(ty * ntx + tx);
-  b.vals_in[j] = (uint32_t)lo;
 }
 
-__global__ void ranges_kernel(int64_t pairs, const uint32_t* __restrict__ keys, int2* ranges) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= pairs) return;
-  const uint32_t k = keys[i];
-  if (i == 0 || keys[i - 1] != k) ranges[k].x = (int)i;
-  if (i == pairs - 1 || keys[i + 1] != k) ranges[k].y = (int)(i + 1);
+__global__ void ranges_kernel(const int64_t* __restrict__ d_pairs, int64_t cap,
+                              const uint32_t* __restrict__ keys, int2* ranges) {
+  const int64_t pairs = min(*d_pairs, cap);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < pairs;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t k = keys[i];
+    if (i == 0 || keys[i - 1] != k) ranges[k].x = (int)i;
+    if (i == pairs - 1 || keys[i + 1] != k) ranges[k].y = (int)(i + 1);
+  }
+}
+
+// duplicate -> stable tile sort -> per-tile ranges, all driven by the device count
+static int bin_pairs(const ss_camera* cam, const ss_raster_settings* s, int64_t n, Geom& g,
+                     Bins& b, uint32_t* status, cudaStream_t st) {
+  const int ntx = ntiles_x(cam, s), nty = ntiles_y(cam, s);
+  const int64_t ntiles = (int64_t)ntx * nty;
+  const int kb = key_bits(ntiles);
+  const bool two = binsort_passes(kb) == 2;
+  SS_CUDA(cudaMemsetAsync(g.ranges, 0, ntiles * sizeof(int2), st));
+  prof_begin(PH_DUPLICATE, st);
+  duplicate_kernel<<<stride_grid(b.capacity), 256, 0, st>>>(
+      ntx, n, g, b, two ? b.keys_out : b.keys_in, two ? b.vals_out : b.vals_in, status);
+  SS_CHECK_LAUNCH("duplicate_kernel");
+  prof_end(PH_DUPLICATE, st);
+  prof_begin(PH_TILE_SORT, st);
+  SS_TRY(binsort_run(b.sort, b.keys_in, b.vals_in, b.keys_out, b.vals_out, g.dev_counts + 1,
+                     b.capacity, kb, st));
+  g_launches.fetch_add(two ? 3 : 2);
+  prof_end(PH_TILE_SORT, st);
+  prof_begin(PH_RANGES, st);
+  ranges_kernel<<<stride_grid(b.capacity), 256, 0, st>>>(g.dev_counts + 1, b.capacity, b.keys_out,
+                                                         g.ranges);
+  SS_CHECK_LAUNCH("ranges_kernel");
+  prof_end(PH_RANGES, st);
+  return SS_OK;
 }
 
 // ------------------------------------------------------------------ blend
@@ -819,7 +855,7 @@ int raster_begin(const ss_cloud* cl, const ss_camera* cam, const ss_raster_setti
 
 int raster_finish(const ss_cloud* cl, const ss_camera* cam, const ss_raster_settings* s,
                   void* geom, void* bins, int64_t pairs, float* image, float* alpha,
-                  int32_t* touch, cudaStream_t st) {
+                  int32_t* touch, uint32_t* status, cudaStream_t st) {
   SS_TRY(check_raster(cl, cam, s));
   const int64_t n = cl->n;
   Geom g = plan_geom(geom, n, cam, s);
@@ -830,23 +866,7 @@ int raster_finish(const ss_cloud* cl, const ss_camera* cam, const ss_raster_sett
     set_error("more than 2^31 tile pairs in one view");
     return SS_ERR_CAPACITY;
   }
-  SS_CUDA(cudaMemsetAsync(g.ranges, 0, ntiles * sizeof(int2), st));
-  if (pairs > 0) {
-    prof_begin(PH_DUPLICATE, st);
-    duplicate_kernel<<<(unsigned)cdiv(pairs, 256), 256, 0, st>>>(ntx, n, pairs, g, b);
-    SS_CHECK_LAUNCH("duplicate_kernel");
-    prof_end(PH_DUPLICATE, st);
-    prof_begin(PH_TILE_SORT, st);
-    size_t sb = b.cub_sort_bytes;
-    SS_CUDA(cub::DeviceRadixSort::SortPairs(b.cub_sort, sb, b.keys_in, b.keys_out, b.vals_in,
-                                            b.vals_out, (int)pairs, 0, key_bits(ntiles), st));
-    g_launches.fetch_add(2 * ((key_bits(ntiles) + 7) / 8));
-    prof_end(PH_TILE_SORT, st);
-    prof_begin(PH_RANGES, st);
-    ranges_kernel<<<(unsigned)cdiv(pairs, 256), 256, 0, st>>>(pairs, b.keys_out, g.ranges);
-    SS_CHECK_LAUNCH("ranges_kernel");
-    prof_end(PH_RANGES, st);
-  }
+  SS_TRY(bin_pairs(cam, s, n, g, b, status, st));
   const BlendParams bp = blend_params(cam, s);
   prof_begin(PH_BLEND_FWD, st);
   const int rc = touch ? launch_blend_fwd<true>(s->tile_size, ntiles, st, bp, g, b.vals_out, image,
@@ -855,6 +875,11 @@ int raster_finish(const ss_cloud* cl, const ss_camera* cam, const ss_raster_sett
                                                  image, alpha, nullptr);
   prof_end(PH_BLEND_FWD, st);
   return rc;
+}
+
+const int64_t* raster_counts(void* geom, int64_t n, const ss_camera* cam,
+                             const ss_raster_settings* s) {
+  return plan_geom(geom, n, cam, s).dev_counts;
 }
 
 int raster_backward(const ss_cloud* cl, const ss_camera* cam, const ss_raster_settings* s,
@@ -870,10 +895,8 @@ int raster_backward(const ss_cloud* cl, const ss_camera* cam, const ss_raster_se
   SS_CUDA(cudaMemsetAsync(g.acc, 0, n * kAccStride * sizeof(float), st));
   SS_CUDA(cudaMemsetAsync(g.touched, 0, n, st));
   const BlendParams bp = blend_params(cam, s);
-  if (pairs > 0) {
-    if (full) SS_TRY(launch_blend_bwd<true>(s->tile_size, ntiles, st, bp, g, b.vals_out, d_image));
-    else SS_TRY(launch_blend_bwd<false>(s->tile_size, ntiles, st, bp, g, b.vals_out, d_image));
-  }
+  if (full) SS_TRY(launch_blend_bwd<true>(s->tile_size, ntiles, st, bp, g, b.vals_out, d_image));
+  else SS_TRY(launch_blend_bwd<false>(s->tile_size, ntiles, st, bp, g, b.vals_out, d_image));
   prof_end(PH_BLEND_BWD, st);
   prof_begin(PH_GAUSS_BWD, st);
   gaussian_bwd_kernel<<<(unsigned)cdiv(n, 128), 128, 0, st>>>(make_cam(cam), *cl, g, n, *grads,
@@ -932,17 +955,8 @@ int tile_bin_finish(int64_t n, const ss_camera* cam, const ss_raster_settings* s
   Bins b = plan_bins(bins, pairs);
   const int ntx = ntiles_x(cam, s), nty = ntiles_y(cam, s);
   const int64_t ntiles = (int64_t)ntx * nty;
-  SS_CUDA(cudaMemsetAsync(g.ranges, 0, ntiles * sizeof(int2), st));
-  if (pairs > 0) {
-    duplicate_kernel<<<(unsigned)cdiv(pairs, 256), 256, 0, st>>>(ntx, n, pairs, g, b);
-    SS_CHECK_LAUNCH("duplicate_kernel");
-    size_t sb = b.cub_sort_bytes;
-    SS_CUDA(cub::DeviceRadixSort::SortPairs(b.cub_sort, sb, b.keys_in, b.keys_out, b.vals_in,
-                                            b.vals_out, (int)pairs, 0, key_bits(ntiles), st));
-    ranges_kernel<<<(unsigned)cdiv(pairs, 256), 256, 0, st>>>(pairs, b.keys_out, g.ranges);
-    SS_CHECK_LAUNCH("ranges_kernel");
-  }
-  return SS_OK;
+  (void)ntiles;
+  return bin_pairs(cam, s, n, g, b, nullptr, st);
 }
 
 }  // namespace ss
@@ -972,7 +986,7 @@ int ss_raster_forward_finish(const ss_cloud* cloud, const ss_camera* cam,
                              const ss_raster_settings* s, void* geom, void* bins,
                              int64_t n_pairs, float* image, float* alpha_map, int32_t* touch,
                              void* stream) {
-  return raster_finish(cloud, cam, s, geom, bins, n_pairs, image, alpha_map, touch,
+  return raster_finish(cloud, cam, s, geom, bins, n_pairs, image, alpha_map, touch, nullptr,
                        as_stream(stream));
 }
 

@@ -94,14 +94,20 @@ int ss_stage1_iter_grads(ss_stage1* st, const ss_camera* cam, const float* targe
     set_error("tile-pair workspace too small");
     return SS_ERR_CAPACITY;
   }
+  const int64_t cap = st->bin_capacity;
   const ss_cloud tc = transformed(st);
-  SS_TRY(raster_finish(&tc, cam, &st->settings, st->geom, st->bins, n_pairs, st->image,
-                       st->alpha_map, nullptr, s));
+  SS_TRY(raster_finish(&tc, cam, &st->settings, st->geom, st->bins, cap, st->image,
+                       st->alpha_map, nullptr, st->status, s));
+  const int64_t slot = st->history_len > 0 ? st->iteration % st->history_len : 0;
+  if (st->pair_history && st->history_len > 0)
+    SS_CUDA(cudaMemcpyAsync(st->pair_history + slot,
+                            raster_counts(st->geom, tc.n, cam, &st->settings) + 1, sizeof(int64_t),
+                            cudaMemcpyDeviceToDevice, s));
   SS_TRY(ss_render_loss(st->image, target, cam->height, cam->width, 3, st->lambda_dssim,
                         0.01 * 0.01, 0.03 * 0.03, st->loss_scratch, st->loss_dev, st->d_image,
                         st->status, stream));
-  if (st->loss_history)
-    SS_CUDA(cudaMemcpyAsync(st->loss_history + st->iteration, st->loss_dev, sizeof(double),
+  if (st->loss_history && st->history_len > 0)
+    SS_CUDA(cudaMemcpyAsync(st->loss_history + slot, st->loss_dev, sizeof(double),
                             cudaMemcpyDeviceToDevice, s));
   if (grad_scale != 1.0f) {
     const int64_t m = (int64_t)cam->width * cam->height * 3;
@@ -114,8 +120,8 @@ int ss_stage1_iter_grads(ss_stage1* st, const ss_camera* cam, const float* targe
   gr.d_sh = st->d_sh;
   gr.viewspace = st->viewspace;
   gr.contributed = st->contributed;
-  SS_TRY(raster_backward(&tc, cam, &st->settings, st->geom, st->bins, n_pairs, st->d_image, &gr,
-                         0, s));
+  SS_TRY(raster_backward(&tc, cam, &st->settings, st->geom, st->bins, cap, st->d_image, &gr, 0,
+                         s));
   if (st->accumulate_stats && st->stats_norm && st->stats_count) {
     const int64_t n = st->src.n;
     stats_kernel<<<(unsigned)cdiv(n, 256), 256, 0, s>>>(n, st->viewspace, st->contributed,
@@ -142,6 +148,20 @@ int ss_stage1_iter_finish(ss_stage1* st, const ss_camera* cam, const float* targ
                           int64_t n_pairs, void* stream) {
   SS_TRY(ss_stage1_iter_grads(st, cam, target, n_pairs, 1.0f, stream));
   return ss_stage1_apply_adam(st, stream);
+}
+
+int ss_stage1_render(ss_stage1* st, const ss_camera* cam, void* stream) {
+  SS_TRY(ss_stage1_iter_begin(st, cam, nullptr, stream));
+  const ss_cloud tc = transformed(st);
+  return raster_finish(&tc, cam, &st->settings, st->geom, st->bins, st->bin_capacity, st->image,
+                       st->alpha_map, nullptr, st->status, as_stream(stream));
+}
+
+int ss_stage1_iter(ss_stage1* st, const ss_camera* cam, const float* target, float grad_scale,
+                   int32_t apply_adam, void* stream) {
+  SS_TRY(ss_stage1_iter_begin(st, cam, nullptr, stream));
+  SS_TRY(ss_stage1_iter_grads(st, cam, target, 0, grad_scale, stream));
+  return apply_adam ? ss_stage1_apply_adam(st, stream) : SS_OK;
 }
 
 }  // extern "C"

@@ -42,25 +42,22 @@ class ViewShardedStage1:
         self.trainer = Stage1Trainer(prev_cloud, cache, views, cfg)
         self.views_per_iteration = views_per_iteration
 
-    def _grads_for(self, views: list[int], total: int):
+    def _grads_for(self, views: list[int], total: int) -> None:
         tr = self.trainer
-        pairs = 0
         for v in views:
-            p = tr.begin(v)
-            tr.finish(v, p, adam=False, grad_scale=1.0 / total)
-            pairs += p
-        return pairs
+            tr.iterate(v, grad_scale=1.0 / total, adam=False)
 
-    def step(self, batch: list[int]) -> int:
-        """One iteration over `batch` (global view ids); returns this rank's tile pairs."""
+    def step(self, batch: list[int]) -> None:
+        """One iteration over `batch` (global view ids), stream-ordered with no
+        host synchronisation (the all-reduce is an NCCL kernel on the stream)."""
         tr = self.trainer
         if self.world == 1 and len(batch) == 1:
-            return tr.step(batch[0])
+            tr.iterate(batch[0])
+            return
         mine = shard_views(batch, self.rank, self.world)
-        pairs = self._grads_for(mine, len(batch))
+        self._grads_for(mine, len(batch))
         allreduce_sum_(tr.g_flat, self.world, self.group)
         tr.apply_adam()
-        return pairs
 
     def step_from_host(self, batch: list[int], host_targets) -> float:
         """End-to-end iteration through host buffers (pinned target H2D, loss D2H)."""
@@ -71,8 +68,7 @@ class ViewShardedStage1:
         loss = 0.0
         for v in mine:
             tr.stage_target(v, host_targets[v])
-            p = tr.begin(v)
-            tr.finish(v, p, adam=False, grad_scale=1.0 / len(batch), staged=True)
+            tr.iterate(v, grad_scale=1.0 / len(batch), adam=False, staged=True)
             loss += tr.last_loss()
         allreduce_sum_(tr.g_flat, self.world, self.group)
         tr.apply_adam()

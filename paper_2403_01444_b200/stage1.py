@@ -121,7 +121,9 @@ class Stage1Trainer:
         self.stats_norm = torch.zeros(n, **f32)
         self.stats_count = torch.zeros(n, dtype=torch.int32, device=dev)
         self.loss_dev = torch.zeros(1, **f64)
-        self.loss_hist = torch.zeros(max(1, history or self.cfg.stage1_iterations), **f64)
+        hist = max(1, history or self.cfg.stage1_iterations)
+        self.loss_hist = torch.zeros(hist, **f64)
+        self.pair_hist = torch.zeros(hist, dtype=torch.int64, device=dev)
         self.status = torch.zeros(1, dtype=torch.int32, device=dev)
         geom = max(self.lib.ss_raster_geom_bytes(n, C.byref(cs), C.byref(self.settings))
                    for cs in self.cam_structs)
@@ -156,12 +158,15 @@ class Stage1Trainer:
                         ("viewspace", self.viewspace), ("contributed", self.contributed),
                         ("stats_norm", self.stats_norm), ("stats_count", self.stats_count),
                         ("loss_dev", self.loss_dev), ("loss_history", self.loss_hist),
+                        ("pair_history", self.pair_hist),
                         ("status", self.status), ("geom", self.geom),
                         ("loss_scratch", self.loss_scratch)):
             setattr(s, name, ptr(t))
+        s.history_len = hist
         self.ntc_scratch = empty_bytes(self.lib.ss_apply_ntc_backward_bytes(s.n_in), dev)
         s.ntc_scratch = ptr(self.ntc_scratch)
         self.s = s
+        self.capacity_margin = 1.3
         self.frame_begin()
 
     # ------------------------------------------------------------------
@@ -172,10 +177,10 @@ class Stage1Trainer:
         """clone_cache + reset_adam (pipeline.py:213-219): fresh moments, step 0."""
         self._call(self.lib.ss_stage1_frame_begin, C.byref(self.s), stream())
 
-    def _ensure_bins(self, pairs: int, cam):
+    def _ensure_bins(self, pairs: int, cam, exact: bool = False):
         if pairs <= self.bin_capacity and self.bins is not None:
             return
-        cap = max(int(pairs * 1.25) + 1024, 1 << 16)
+        cap = max(pairs if exact else int(pairs * 1.25) + 1024, 1 << 16)
         nbytes = self.lib.ss_raster_bin_bytes(cap, self.cloud.n, C.byref(cam),
                                               C.byref(self.settings))
         self.bins = empty_bytes(nbytes, self.dev)
@@ -217,6 +222,13 @@ class Stage1Trainer:
     def apply_adam(self):
         self._call(self.lib.ss_stage1_apply_adam, C.byref(self.s), stream())
 
+    def render_async(self, view: int) -> None:
+        """Forward only with no host synchronisation (ss_stage1_render)."""
+        if self.bins is None:
+            self.plan_capacity()
+        self._call(self.lib.ss_stage1_render, C.byref(self.s), C.byref(self.cam_structs[view]),
+                   stream())
+
     def render(self, view: int) -> int:
         """Forward only (render-only config 2 / playback, pipeline.py:471-480):
         NTC transform + rasterize_forward of the current cache into self.image."""
@@ -229,33 +241,82 @@ class Stage1Trainer:
                    ptr(self.alpha), None, stream())
         return pairs
 
+    def plan_capacity(self, margin: float | None = None) -> int:
+        """Size the tile-pair workspace for the no-sync iteration: the pair
+        count of every view under the current parameters (one host read per
+        view, once), times a margin for the motion Stage 1 applies."""
+        m = self.capacity_margin if margin is None else margin
+        peak = max(self.begin(v) for v in range(len(self.cameras)))
+        cap = int(peak * m) + 65536
+        if cap > self.bin_capacity:
+            self._ensure_bins(cap, self.cam_structs[0], exact=True)
+        return self.bin_capacity
+
     def step_from_host(self, view: int, target_host: torch.Tensor) -> float:
         """End-to-end step through host buffers: H2D copy of the view's target
         from pinned memory, the iteration, D2H read of the loss."""
         self.stage_target(view, target_host)
-        pairs = self.begin(view)
-        self.finish(view, pairs, staged=True)
+        self.iterate(view, staged=True)
         return float(self.loss_dev.item())
 
-    def step(self, view: int):
-        pairs = self.begin(view)
-        self.finish(view, pairs)
-        return pairs
+    def iterate(self, view: int, grad_scale: float = 1.0, adam: bool = True,
+                staged: bool = False) -> None:
+        """One Stage-1 iteration with no host synchronisation (ss_stage1_iter):
+        the pair count stays on the device, bounded by the planned capacity."""
+        if self.bins is None:
+            self.plan_capacity()
+        cam = self.cam_structs[view]
+        tgt = ptr(self._staging if staged else self.targets[view])
+        self._call(self.lib.ss_stage1_iter, C.byref(self.s), C.byref(cam), tgt,
+                   C.c_float(grad_scale), int(adam), stream())
+
+    def step(self, view: int) -> None:
+        self.iterate(view)
+
+    def pairs_of_last(self, k: int) -> np.ndarray:
+        """Tile-pair counts of the last k iterations (device history; syncs)."""
+        h, it = self.pair_hist.numel(), int(self.s.iteration)
+        idx = [(it - k + j) % h for j in range(k)]
+        return self.pair_hist.cpu().numpy()[idx]
+
+    def check_status(self, what: str = "stage1 loss") -> int:
+        self.flags.copy_(self.status, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return int(self.flags.item())
 
     def run(self, iterations: int | None = None, frame_index: int = 1) -> np.ndarray:
-        """The Stage-1 loop (pipeline.py:262-279); returns the loss history."""
+        """The Stage-1 loop (pipeline.py:262-279); returns the loss history.
+        Iterations queue back to back without host synchronisation; if the
+        pair capacity overflowed, the frame is replayed from its starting
+        parameters with a larger workspace."""
         iters = self.cfg.stage1_iterations if iterations is None else iterations
         if iters > self.loss_hist.numel():
             self.loss_hist = torch.zeros(iters, dtype=torch.float64, device=self.dev)
+            self.pair_hist = torch.zeros(iters, dtype=torch.int64, device=self.dev)
             self.s.loss_history = ptr(self.loss_hist)
+            self.s.pair_history = ptr(self.pair_hist)
+            self.s.history_len = iters
         order = view_order(self.cfg.seed, frame_index, len(self.cameras), iters)
         stats_from = max(0, iters - len(self.cameras))
-        for t, v in enumerate(order):
-            self.s.accumulate_stats = int(t >= stats_from)
-            self.step(v)
-        self.flags.copy_(self.status, non_blocking=True)
-        torch.cuda.current_stream().synchronize()
-        _lib.check_flags(int(self.flags.item()), "stage1 loss")
+        if self.bins is None:
+            self.plan_capacity()
+        start = (self.tables.clone(), self.params.clone())
+        for attempt in range(4):
+            for t, v in enumerate(order):
+                self.s.accumulate_stats = int(t >= stats_from)
+                self.iterate(v)
+            flags = self.check_status()
+            if not flags & _lib.FLAG_OVERFLOW:
+                break
+            # replay the frame from its start with a larger pair workspace
+            peak = int(self.pair_hist[:iters].max().item())
+            self.tables.copy_(start[0])
+            self.params.copy_(start[1])
+            self.status.zero_()
+            self._ensure_bins(int(max(peak, self.bin_capacity) * 1.5), self.cam_structs[0],
+                              exact=True)
+            self.frame_begin()
+        _lib.check_flags(flags, "stage1 loss")
         return self.loss_hist[:iters].cpu().numpy()
 
     # ------------------------------------------------------------------

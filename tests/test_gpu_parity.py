@@ -218,3 +218,66 @@ def test_stage1_cfg0_single_step_vs_oracle(P):
     for i in range(3):
         assert G.norm_rel(gw[i], ref["g_w"][i]) <= GRAD_TOL
         assert G.norm_rel(gb[i], ref["g_b"][i]) <= GRAD_TOL
+
+
+def test_stage1_no_sync_matches_synchronised_path(P):
+    """ss_stage1_iter (device-side pair count, capacity-bounded binning, no
+    host synchronisation) reproduces the begin/finish path: the first
+    iteration bit for bit, later ones up to the float-atomic accumulation
+    order of the gradients; and run()'s replay after a capacity overflow
+    restores the same trajectory."""
+    import torch
+
+    from paper_2403_01444_b200 import scenes
+    from paper_2403_01444_b200.stage1 import Stage1Config, Stage1Trainer
+    from oracle import stage1 as O
+
+    sc = scenes.small_scene(seed=11, n=3000, width=96, height=72, sh_degree=1, n_views=3)
+    tables, mlp = O.init_ntc(sc.grid, output_init="random", seed=2)
+    tables = scenes.f32(np.random.default_rng(4).uniform(-0.05, 0.05, size=tables.shape))
+    targets = [O.render(scenes.moved_cloud(sc.cloud, np.random.default_rng(9)), c)[0]["image"]
+               for c in sc.cameras]
+
+    class Cache:
+        grid = P["types"].HashGridConfig.from_any(sc.grid)
+
+    def trainer():
+        c = Cache()
+        c.tables, c.weights, c.biases = tables.copy(), mlp["weights"], mlp["biases"]
+        return Stage1Trainer(sc.cloud, c, list(zip(sc.cameras, targets)),
+                             Stage1Config(stage1_iterations=6))
+
+    def close(x, y):
+        return torch.allclose(x, y, rtol=1e-4, atol=1e-7)
+
+    views = [0, 1, 2, 1, 0, 2]
+    a, b = trainer(), trainer()
+    p0 = a.begin(0)
+    a.finish(0, p0, adam=False)
+    b.iterate(0, adam=False)
+    torch.cuda.synchronize()
+    assert torch.equal(a.image, b.image)
+    assert a.last_loss() == b.last_loss()
+    assert int(b.pairs_of_last(1)[0]) == p0
+    a.apply_adam()
+    b.apply_adam()
+    ref_losses, ref_pairs = [], []
+    for v in views[1:]:
+        p = a.begin(v)
+        a.finish(v, p)
+        ref_losses.append(a.last_loss())
+        ref_pairs.append(p)
+    for v in views[1:]:
+        b.iterate(v)
+    torch.cuda.synchronize()
+    assert b.check_status() == 0
+    np.testing.assert_allclose(b.pairs_of_last(5), ref_pairs, rtol=1e-3)
+    np.testing.assert_allclose(b.loss_hist[1:6].cpu().numpy(), ref_losses, rtol=1e-6)
+    assert close(a.tables, b.tables) and close(a.params, b.params)
+    # run() with a deliberately tiny workspace: overflow -> replay with a larger one
+    c, d = trainer(), trainer()
+    la = c.run(6)
+    d.plan_capacity(margin=0.2)
+    lb = d.run(6)
+    np.testing.assert_allclose(la, lb, rtol=1e-6)
+    assert close(c.tables, d.tables) and close(c.params, d.params)
