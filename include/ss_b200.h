@@ -273,7 +273,9 @@ typedef struct ss_stage1 {
   /* source (frozen previous-frame) cloud and its inside-AABB rows */
   ss_cloud src;
   int64_t n_in;
-  const int32_t* rows;
+  const int32_t* rows;       /* inside rows in the order the NTC kernels use (e.g. Morton) */
+  const int32_t* rows_index; /* optional: the inside rows in index order ... */
+  const int32_t* rows_pos;   /* ... and the position of each in `rows` (coalesced transform) */
   /* NTC parameters, Adam state, gradients (caller-owned) */
   float *tables, *params, *g_tables, *g_params;
   double *m_tables, *v_tables, *m_params, *v_params;

@@ -67,7 +67,8 @@ class Stage1(C.Structure):
                 ("lr", C.c_double), ("beta1", C.c_double), ("beta2", C.c_double),
                 ("eps", C.c_double), ("lambda_dssim", C.c_double),
                 ("rotate_sh", C.c_int32), ("accumulate_stats", C.c_int32),
-                ("src", Cloud), ("n_in", C.c_int64), ("rows", P),
+                ("src", Cloud), ("n_in", C.c_int64), ("rows", P), ("rows_index", P),
+                ("rows_pos", P),
                 ("tables", P), ("params", P), ("g_tables", P), ("g_params", P),
                 ("m_tables", P), ("v_tables", P), ("m_params", P), ("v_params", P),
                 ("row_mask", P), ("step_dev", P),

@@ -256,12 +256,13 @@ int ntc_backward_run(const ss_grid* g, const ss_mlp* mlp, int64_t n, const float
                      const int32_t* rows, const float* params, const float* X, int xs,
                      const float* g_out, int gs, const uint64_t* relu, float* dX,
                      float* g_tables, float* g_params, cudaStream_t st);
-int transform_run(const ss_cloud* src, int64_t n, const int32_t* rows, const float* out7, int os,
-                  int rotate_sh, float* tm, float* tr, float* ts, uint32_t* status,
-                  cudaStream_t st);
-int transform_vjp_run(const ss_cloud* src, int64_t n, const int32_t* rows, const float* out7, int os,
-                      int rotate_sh, const float* dm, const float* dr, const float* ds, float* g7,
-                      int gs, cudaStream_t st);
+// rows: cloud row of thread j; pos (nullable = identity): its slot in out7 / g7
+int transform_run(const ss_cloud* src, int64_t n, const int32_t* rows, const int32_t* pos,
+                  const float* out7, int os, int rotate_sh, float* tm, float* tr, float* ts,
+                  uint32_t* status, cudaStream_t st);
+int transform_vjp_run(const ss_cloud* src, int64_t n, const int32_t* rows, const int32_t* pos,
+                      const float* out7, int os, int rotate_sh, const float* dm, const float* dr,
+                      const float* ds, float* g7, int gs, cudaStream_t st);
 }  // namespace ss
 
 // decoder on tensor cores (mlp_tc.cu); mode 0 = FFMA fp32, 1 = 3xTF32, 2 = tf32

@@ -3,13 +3,14 @@
 //   L = (1-lam) mean|x-y| + lam (1 - mean_valid SSIM) / 2,
 // 11x11 Gaussian window (sigma 1.5), VALID windows only, mean over windows x
 // channels; the SSIM adjoint is a FULL convolution of three per-window maps.
-// Separable 11-tap passes staged in shared memory; window statistics in fp64.
+// Separable 11-tap strip walks (below); window statistics in fp64.
 #include "common.cuh"
 
 namespace ss {
 
 constexpr int WIN = 11, HALO = WIN - 1;
-constexpr int BX = 32, BY = 8;  // output tile per CTA (256 threads)
+constexpr int SW = 32;   // strip width: one warp per channel, a lane per column
+constexpr int RCH = 72;  // rows per chunk: 42 x 14 CTAs of 3 warps at 1352x1014 = one wave at 4 CTAs/SM
 
 struct LossParams {
   int H, W, Hv, Wv, C;
@@ -17,144 +18,218 @@ struct LossParams {
   double c1, c2, lam, up;  // up = -lam / (2 n_windows)
 };
 
-// pass 1: per valid window -> SSIM value (summed) and the three adjoint maps
-// (losses.py:121-137): A = dL/dmu_x part, B = dL/dconv_xx, C = dL/dconv_xy
-__global__ void __launch_bounds__(BX* BY) ssim_map_kernel(LossParams lp,
+// The separable 11-tap passes walk a 32-column strip down a chunk of rows.
+// Each input row's horizontal sums are scattered into 11 rotating vertical
+// accumulators (slot = output row mod 11, kept in registers), so every input
+// row is filtered horizontally once and an output row completes every step.
+// CTA = 3 warps (one per channel) sharing the row loads through shared memory.
+
+// pass 1: valid windows -> SSIM (summed) and the three adjoint maps
+// (losses.py:121-137): dL/dmu_x part, dL/dsigma_xx, dL/dsigma_xy (all / lam-scale)
+__global__ void __launch_bounds__(SW * 3, 4) ssim_map_kernel(LossParams lp,
                                                           const float* __restrict__ img,
                                                           const float* __restrict__ tgt,
                                                           float* __restrict__ maps,
                                                           double* __restrict__ sums) {
-  __shared__ float sx[BY + HALO][BX + HALO + 1], sy[BY + HALO][BX + HALO + 1];
-  __shared__ double hs[5][BY + HALO][BX];
-  const int c = blockIdx.z;
-  const int ox = blockIdx.x * BX, oy = blockIdx.y * BY;
-  const int tid = threadIdx.y * BX + threadIdx.x;
-  for (int i = tid; i < (BY + HALO) * (BX + HALO); i += BX * BY) {
-    const int ry = i / (BX + HALO), rx = i % (BX + HALO);
-    const int py = oy + ry, px = ox + rx;
-    float xv = 0.f, yv = 0.f;
-    if (py < lp.H && px < lp.W) {
-      const int64_t o = ((int64_t)py * lp.W + px) * lp.C + c;
-      xv = img[o];
-      yv = tgt[o];
+  constexpr int RW = SW + HALO;  // input columns of a strip
+  __shared__ float sx[3][RW], sy[3][RW];
+  const int lane = threadIdx.x, c = threadIdx.y, tid = c * SW + lane;
+  const int C = lp.C;
+  const int x0 = blockIdx.x * SW, oy0 = blockIdx.y * RCH;
+  const int oy1 = min(oy0 + RCH, lp.Hv), iy1 = oy1 + HALO;
+  const int xcol = x0 + lane;
+  const bool col_ok = xcol < lp.Wv && c < C;
+  // register prefetch of one interleaved input row segment (RW pixels x C)
+  constexpr int SEG = RW * 3, PER = (SEG + SW * 3 - 1) / (SW * 3);
+  float px[PER], py[PER], qx[PER], qy[PER];  // rows yi + 1 and yi + 2 in flight
+  auto fetch = [&](int y, float (&fx)[PER], float (&fy)[PER]) {
+#pragma unroll
+    for (int m = 0; m < PER; ++m) {
+      const int e = tid + m * SW * 3;
+      const int col = x0 + e / C;
+      const bool ok = e < RW * C && y < lp.H && col < lp.W;
+      const int64_t o = ((int64_t)y * lp.W + x0) * C + e;
+      fx[m] = ok ? __ldg(img + o) : 0.f;
+      fy[m] = ok ? __ldg(tgt + o) : 0.f;
     }
-    sx[ry][rx] = xv;
-    sy[ry][rx] = yv;
-  }
-  __syncthreads();
-  for (int i = tid; i < (BY + HALO) * BX; i += BX * BY) {
-    const int ry = i / BX, rx = i % BX;
-    double a = 0, b = 0, xx = 0, yy = 0, xy = 0;
+  };
+  double ax[WIN], ay[WIN], axx[WIN], ayy[WIN], axy[WIN];
 #pragma unroll
-    for (int k = 0; k < WIN; ++k) {
-      const double xv = sx[ry][rx + k], yv = sy[ry][rx + k], w = lp.g[k];
-      a += w * xv;
-      b += w * yv;
-      xx += w * xv * xv;
-      yy += w * yv * yv;
-      xy += w * xv * yv;
+  for (int j = 0; j < WIN; ++j) ax[j] = ay[j] = axx[j] = ayy[j] = axy[j] = 0.0;
+  double ssum = 0.0;
+  const int64_t plane = (int64_t)lp.Hv * lp.Wv;
+  fetch(oy0, px, py);
+  fetch(oy0 + 1, qx, qy);
+  for (int yb = oy0; yb < iy1; yb += WIN) {
+#pragma unroll
+    for (int u = 0; u < WIN; ++u) {
+      const int yi = yb + u;
+      if (yi < iy1) {  // block-uniform
+        __syncthreads();
+#pragma unroll
+        for (int m = 0; m < PER; ++m) {
+          const int e = tid + m * SW * 3;
+          if (e < RW * C) {
+            sx[e % C][e / C] = px[m];
+            sy[e % C][e / C] = py[m];
+          }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int m = 0; m < PER; ++m) px[m] = qx[m], py[m] = qy[m];
+        fetch(yi + 2, qx, qy);
+        // horizontal sums of this input row at column xcol
+        double hx = 0, hy = 0, hxx = 0, hyy = 0, hxy = 0;
+#pragma unroll
+        for (int k = 0; k < WIN; ++k) {
+          const double xv = sx[c < C ? c : 0][lane + k], yv = sy[c < C ? c : 0][lane + k];
+          const double gx = lp.g[k] * xv, gy = lp.g[k] * yv;
+          hx += gx;
+          hy += gy;
+          hxx = fma(gx, xv, hxx);
+          hxy = fma(gx, yv, hxy);
+          hyy = fma(gy, yv, hyy);
+        }
+        // scatter into the 11 rotating vertical accumulators (tap t -> output row yi - t)
+#pragma unroll
+        for (int t = 0; t < WIN; ++t) {
+          const int sl = (u - t + WIN) % WIN;
+          const double w = lp.g[t];
+          ax[sl] = fma(w, hx, ax[sl]);
+          ay[sl] = fma(w, hy, ay[sl]);
+          axx[sl] = fma(w, hxx, axx[sl]);
+          ayy[sl] = fma(w, hyy, ayy[sl]);
+          axy[sl] = fma(w, hxy, axy[sl]);
+        }
+        // output row yi - 10 is complete in slot (u + 1) % 11
+        const int sl = (u + 1) % WIN;
+        const int o = yi - HALO;
+        if (o >= oy0 && col_ok) {
+          const double mx = ax[sl], my = ay[sl];
+          const double vxx = axx[sl] - mx * mx, vyy = ayy[sl] - my * my, cxy = axy[sl] - mx * my;
+          const double a1 = 2.0 * mx * my + lp.c1, a2 = 2.0 * cxy + lp.c2;
+          const double b1 = mx * mx + my * my + lp.c1, b2 = vxx + vyy + lp.c2;
+          const double inv = 1.0 / (b1 * b2);
+          const double sv = a1 * a2 * inv;
+          ssum += sv;
+          const double ga1 = a2 * inv, ga2 = a1 * inv, gb1 = -sv / b1, gb2 = -sv / b2;
+          const double gmx = 2.0 * my * ga1 + 2.0 * mx * gb1 - 2.0 * my * ga2 - 2.0 * mx * gb2;
+          const int64_t oo = (int64_t)o * lp.Wv + xcol;
+          maps[(0 * C + c) * plane + oo] = (float)gmx;
+          maps[(1 * C + c) * plane + oo] = (float)gb2;
+          maps[(2 * C + c) * plane + oo] = (float)(2.0 * ga2);
+        }
+        ax[sl] = ay[sl] = axx[sl] = ayy[sl] = axy[sl] = 0.0;
+      }
     }
-    hs[0][ry][rx] = a;
-    hs[1][ry][rx] = b;
-    hs[2][ry][rx] = xx;
-    hs[3][ry][rx] = yy;
-    hs[4][ry][rx] = xy;
   }
-  __syncthreads();
-  const int vx = ox + threadIdx.x, vy = oy + threadIdx.y;
-  double s = 0.0;
-  if (vx < lp.Wv && vy < lp.Hv) {
-    double v[5] = {0, 0, 0, 0, 0};
-#pragma unroll
-    for (int k = 0; k < WIN; ++k)
-#pragma unroll
-      for (int q = 0; q < 5; ++q) v[q] += lp.g[k] * hs[q][threadIdx.y + k][threadIdx.x];
-    const double mx = v[0], my = v[1];
-    const double vxx = v[2] - mx * mx, vyy = v[3] - my * my, cxy = v[4] - mx * my;
-    const double a1 = 2.0 * mx * my + lp.c1, a2 = 2.0 * cxy + lp.c2;
-    const double b1 = mx * mx + my * my + lp.c1, b2 = vxx + vyy + lp.c2;
-    s = (a1 * a2) / (b1 * b2);
-    const double inv = 1.0 / (b1 * b2);
-    const double ga1 = a2 * inv, ga2 = a1 * inv, gb1 = -s / b1, gb2 = -s / b2;
-    const double gmx = 2.0 * my * ga1 + 2.0 * mx * gb1 - 2.0 * my * ga2 - 2.0 * mx * gb2;
-    const int64_t plane = (int64_t)lp.Hv * lp.Wv;
-    const int64_t o = (int64_t)vy * lp.Wv + vx;
-    maps[(0 * lp.C + c) * plane + o] = (float)gmx;
-    maps[(1 * lp.C + c) * plane + o] = (float)gb2;
-    maps[(2 * lp.C + c) * plane + o] = (float)(2.0 * ga2);
-  }
-  // block sum of SSIM values
-  __shared__ double red[BX * BY / 32];
-  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  if ((tid & 31) == 0) red[tid >> 5] = s;
-  __syncthreads();
-  if (tid == 0) {
-    double t = 0;
-    for (int i = 0; i < BX * BY / 32; ++i) t += red[i];
-    atomicAdd(&sums[0], t);
-  }
+  for (int o = 16; o > 0; o >>= 1) ssum += __shfl_xor_sync(0xffffffffu, ssum, o);
+  if (lane == 0 && ssum != 0.0) atomicAdd(&sums[0], ssum);
 }
 
 // pass 2: full convolution of the maps + L1 term -> dL/dimage; sum |x - y|
-__global__ void __launch_bounds__(BX* BY) ssim_grad_kernel(LossParams lp,
+// (losses.py:106-108, :138-145).  Same strip walk in fp32: map rows
+// [oy0 - 10, oy1) feed output rows [oy0, oy1), map columns [x0 - 10, x0 + 32).
+__global__ void __launch_bounds__(SW * 3, 5) ssim_grad_kernel(LossParams lp,
                                                            const float* __restrict__ img,
                                                            const float* __restrict__ tgt,
                                                            const float* __restrict__ maps,
                                                            float* __restrict__ grad,
                                                            double* __restrict__ sums) {
-  __shared__ float sm[3][BY + HALO][BX + HALO + 1];
-  __shared__ float hs[3][BY + HALO][BX];
-  const int c = blockIdx.z;
-  const int ox = blockIdx.x * BX, oy = blockIdx.y * BY;
-  const int tid = threadIdx.y * BX + threadIdx.x;
+  constexpr int RW = SW + HALO;
+  __shared__ float sm[3][3][RW + 1];  // [channel][map][column]
+  const int lane = threadIdx.x, c = threadIdx.y, tid = c * SW + lane;
+  const int C = lp.C;
+  const int x0 = blockIdx.x * SW, oy0 = blockIdx.y * RCH;
+  const int oy1 = min(oy0 + RCH, lp.H);
+  const int ry0 = max(oy0 - HALO, 0), ry1 = min(oy1, lp.Hv);  // map rows that contribute
   const int64_t plane = (int64_t)lp.Hv * lp.Wv;
-  // map rows/cols [o - HALO, o + B) (zero outside the valid range)
-  for (int i = tid; i < (BY + HALO) * (BX + HALO); i += BX * BY) {
-    const int ry = i / (BX + HALO), rx = i % (BX + HALO);
-    const int vy = oy - HALO + ry, vx = ox - HALO + rx;
-    const bool in = vy >= 0 && vx >= 0 && vy < lp.Hv && vx < lp.Wv;
-    const int64_t o = (int64_t)vy * lp.Wv + vx;
+  float g[WIN];
 #pragma unroll
-    for (int q = 0; q < 3; ++q) sm[q][ry][rx] = in ? maps[(q * lp.C + c) * plane + o] : 0.f;
-  }
-  __syncthreads();
-  for (int i = tid; i < (BY + HALO) * BX; i += BX * BY) {
-    const int ry = i / BX, rx = i % BX;
+  for (int k = 0; k < WIN; ++k) g[k] = (float)lp.g[k];
+  // prefetch: thread (c, lane) loads map q of channel c at columns x0 - 10 + lane (+32)
+  constexpr int PER = 2;
+  float pm[3][PER], qm[3][PER];  // map rows r + 1 and r + 2 in flight
+  float pi0, pt0, pi1, pt1;      // image / target at (r + 1, px_) and (r + 2, px_)
+  const int px_ = x0 + lane;
+  const bool col_ok = px_ < lp.W && c < C;
+  auto fetch = [&](int r, float (&fm)[3][PER], float& fi, float& ft) {
 #pragma unroll
-    for (int q = 0; q < 3; ++q) {
-      float a = 0.f;
+    for (int q = 0; q < 3; ++q)
 #pragma unroll
-      for (int k = 0; k < WIN; ++k) a = fmaf((float)lp.g[k], sm[q][ry][rx + k], a);
-      hs[q][ry][rx] = a;
+      for (int m = 0; m < PER; ++m) {
+        const int e = lane + m * SW, vx = x0 - HALO + e;
+        const bool ok = c < C && e < RW && r < ry1 && vx >= 0 && vx < lp.Wv;
+        fm[q][m] = ok ? __ldg(maps + (q * C + c) * plane + (int64_t)r * lp.Wv + vx) : 0.f;
+      }
+    const bool ok = col_ok && r >= oy0 && r < oy1;
+    const int64_t o = ((int64_t)r * lp.W + px_) * C + c;
+    fi = ok ? __ldg(img + o) : 0.f;
+    ft = ok ? __ldg(tgt + o) : 0.f;
+  };
+  float a0[WIN], a1[WIN], a2[WIN];
+#pragma unroll
+  for (int j = 0; j < WIN; ++j) a0[j] = a1[j] = a2[j] = 0.f;
+  const double size = (double)lp.H * lp.W * C;
+  double l1 = 0.0;
+  // walk map rows r = ry0 .. oy1 - 1 (rows >= Hv contribute zero); output row
+  // y = r completes after map row r (tap 0): accumulator slot y mod 11
+  auto emit = [&](int y, float b0, float b1, float b2, float x, float t) {
+    if (y >= oy0 && y < oy1 && col_ok) {
+      const int64_t o = ((int64_t)y * lp.W + px_) * C + c;
+      const float d = x - t;
+      l1 += fabs((double)x - (double)t);
+      const double sgn = d > 0.f ? 1.0 : (d < 0.f ? -1.0 : 0.0);
+      const double back = (double)b0 + (double)b1 * 2.0 * x + (double)b2 * t;
+      grad[o] = (float)((1.0 - lp.lam) * sgn / size + lp.up * back);
+    }
+  };
+  fetch(ry0, pm, pi0, pt0);
+  fetch(ry0 + 1, qm, pi1, pt1);
+  for (int rb = ry0; rb < oy1; rb += WIN) {
+#pragma unroll
+    for (int u = 0; u < WIN; ++u) {
+      const int r = rb + u;
+      if (r < oy1) {  // block-uniform
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < 3; ++q)
+#pragma unroll
+          for (int m = 0; m < PER; ++m)
+            if (lane + m * SW < RW) sm[c][q][lane + m * SW] = pm[q][m];
+        __syncthreads();
+        const float xi = pi0, ti = pt0;  // image / target of output row r
+#pragma unroll
+        for (int q = 0; q < 3; ++q)
+#pragma unroll
+          for (int m = 0; m < PER; ++m) pm[q][m] = qm[q][m];
+        pi0 = pi1, pt0 = pt1;
+        fetch(r + 2, qm, pi1, pt1);
+        // horizontal full convolution at output column px_: map cols px_ - j
+        float h0 = 0.f, h1 = 0.f, h2 = 0.f;
+#pragma unroll
+        for (int j = 0; j < WIN; ++j) {
+          const int e = lane + HALO - j;
+          h0 = fmaf(g[j], sm[c][0][e], h0);
+          h1 = fmaf(g[j], sm[c][1][e], h1);
+          h2 = fmaf(g[j], sm[c][2][e], h2);
+        }
+        // map row r feeds output rows r + i (i = 0..10): slot (u + i) % 11
+#pragma unroll
+        for (int i = 0; i < WIN; ++i) {
+          const int sl = (u + i) % WIN;
+          a0[sl] = fmaf(g[i], h0, a0[sl]);
+          a1[sl] = fmaf(g[i], h1, a1[sl]);
+          a2[sl] = fmaf(g[i], h2, a2[sl]);
+        }
+        // output row r is complete (its last map row is r itself): slot u
+        emit(r, a0[u], a1[u], a2[u], xi, ti);
+        a0[u] = a1[u] = a2[u] = 0.f;
+      }
     }
   }
-  __syncthreads();
-  const int px = ox + threadIdx.x, py = oy + threadIdx.y;
-  double l1 = 0.0;
-  if (px < lp.W && py < lp.H) {
-    float b[3] = {0.f, 0.f, 0.f};
-#pragma unroll
-    for (int k = 0; k < WIN; ++k)
-#pragma unroll
-      for (int q = 0; q < 3; ++q) b[q] = fmaf((float)lp.g[k], hs[q][threadIdx.y + k][threadIdx.x], b[q]);
-    const int64_t o = ((int64_t)py * lp.W + px) * lp.C + c;
-    const float x = img[o], y = tgt[o];
-    const float d = x - y;
-    l1 = fabs((double)x - (double)y);
-    const double size = (double)lp.H * lp.W * lp.C;
-    const double sgn = d > 0.f ? 1.0 : (d < 0.f ? -1.0 : 0.0);
-    const double back = (double)b[0] + (double)b[1] * 2.0 * x + (double)b[2] * y;
-    grad[o] = (float)((1.0 - lp.lam) * sgn / size + lp.up * back);
-  }
-  __shared__ double red[BX * BY / 32];
   for (int o = 16; o > 0; o >>= 1) l1 += __shfl_xor_sync(0xffffffffu, l1, o);
-  if ((tid & 31) == 0) red[tid >> 5] = l1;
-  __syncthreads();
-  if (tid == 0) {
-    double t = 0;
-    for (int i = 0; i < BX * BY / 32; ++i) t += red[i];
-    atomicAdd(&sums[1], t);
-  }
+  if (lane == 0 && l1 != 0.0) atomicAdd(&sums[1], l1);
 }
 
 __global__ void loss_finalize_kernel(LossParams lp, const double* sums, double* loss,
@@ -181,8 +256,8 @@ size_t ss_loss_bytes(int32_t height, int32_t width, int32_t channels) {
 int ss_render_loss(const float* image, const float* target, int32_t height, int32_t width,
                    int32_t channels, double lam, double c1, double c2, void* scratch,
                    double* loss_dev, float* d_image, uint32_t* status, void* stream) {
-  if (channels < 1 || channels > 4) {
-    set_error("render_loss supports 1-4 channels");
+  if (channels < 1 || channels > 3) {
+    set_error("render_loss supports 1-3 channels");
     return SS_ERR_DATA;
   }
   if (height < WIN || width < WIN) {
@@ -205,11 +280,11 @@ int ss_render_loss(const float* image, const float* target, int32_t height, int3
   float* maps = reinterpret_cast<float*>(static_cast<char*>(scratch) + align_up(2 * sizeof(double)));
   prof_begin(PH_LOSS, st);
   SS_CUDA(cudaMemsetAsync(sums, 0, 2 * sizeof(double), st));
-  dim3 blk(BX, BY);
-  dim3 g1((unsigned)cdiv(lp.Wv, BX), (unsigned)cdiv(lp.Hv, BY), channels);
+  dim3 blk(SW, 3);
+  dim3 g1((unsigned)cdiv(lp.Wv, SW), (unsigned)cdiv(lp.Hv, RCH));
   ssim_map_kernel<<<g1, blk, 0, st>>>(lp, image, target, maps, sums);
   SS_CHECK_LAUNCH("ssim_map_kernel");
-  dim3 g2((unsigned)cdiv(lp.W, BX), (unsigned)cdiv(lp.H, BY), channels);
+  dim3 g2((unsigned)cdiv(lp.W, SW), (unsigned)cdiv(lp.H, RCH));
   ssim_grad_kernel<<<g2, blk, 0, st>>>(lp, image, target, maps, d_image, sums);
   SS_CHECK_LAUNCH("ssim_grad_kernel");
   loss_finalize_kernel<<<1, 1, 0, st>>>(lp, sums, loss_dev, status);

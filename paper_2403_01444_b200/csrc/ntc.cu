@@ -360,76 +360,112 @@ __global__ void touched_kernel(ss_grid g, int64_t n, const float* __restrict__ m
   }
 }
 
-// K1f: interpolated features, one thread per (row, level) (ntc.py:176-216).
-// X is (n, xs) row-major; the level-0 thread zero-fills the padding columns.
-__global__ void gather_kernel(ss_grid g, int64_t n, const float* __restrict__ means,
-                              const int32_t* __restrict__ rows, const float* __restrict__ tables,
-                              float* __restrict__ X, int xs, uint32_t* status) {
-  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int L = g.n_levels;
-  if (t >= n * L) return;
-  const int64_t i = t / L;
-  const int l = (int)(t - i * L);
+// K1f: interpolated features (ntc.py:176-216), one thread per inside row:
+// the fp64 normalisation is done once and the L levels are walked in turn
+// (8 float2 gathers each from the L2-resident tables).  Stage 1 orders the
+// inside rows along a Morton curve, so neighbouring threads gather
+// neighbouring cells.  X is (n, xs) row-major, padding columns zeroed.
+__global__ void __launch_bounds__(256) gather_kernel(ss_grid g, int64_t n,
+                                                     const float* __restrict__ means,
+                                                     const int32_t* __restrict__ rows,
+                                                     const float* __restrict__ tables,
+                                                     float* __restrict__ X, int xs,
+                                                     uint32_t* status) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int L = g.n_levels, F = g.n_features;
   const int64_t gid = rows ? rows[i] : i;
   double xn[3];
-  if (!normalise(g, means + 3 * gid, xn) && status && l == 0) atomicOr(status, SS_FLAG_OUTSIDE);
-  uint32_t idx[8];
-  float w[8];
-  level_corners(g, l, xn, idx, w);
-  const int F = g.n_features;
+  if (!normalise(g, means + 3 * gid, xn) && status) atomicOr(status, SS_FLAG_OUTSIDE);
   const size_t T = (size_t)1 << g.log2_table;
-  const float* tl = tables + (size_t)l * T * F;
   float* xr = X + i * xs;
-  if (F == 2) {
-    float a0 = 0.f, a1 = 0.f;
+  for (int l = 0; l < L; ++l) {
+    uint32_t idx[8];
+    float w[8];
+    level_corners(g, l, xn, idx, w);
+    const float* tl = tables + (size_t)l * T * F;
+    if (F == 2) {
+      float2 v[8];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const float2 v = __ldg(reinterpret_cast<const float2*>(tl) + idx[k]);
-      a0 = fmaf(w[k], v.x, a0);
-      a1 = fmaf(w[k], v.y, a1);
-    }
-    *reinterpret_cast<float2*>(xr + 2 * l) = make_float2(a0, a1);
-  } else {
-    for (int f = 0; f < F; ++f) {
-      float a = 0.f;
+      for (int k = 0; k < 8; ++k) v[k] = __ldg(reinterpret_cast<const float2*>(tl) + idx[k]);
+      float a0 = 0.f, a1 = 0.f;
 #pragma unroll
-      for (int k = 0; k < 8; ++k) a = fmaf(w[k], __ldg(tl + (size_t)idx[k] * F + f), a);
-      xr[l * F + f] = a;
+      for (int k = 0; k < 8; ++k) {
+        a0 = fmaf(w[k], v[k].x, a0);
+        a1 = fmaf(w[k], v[k].y, a1);
+      }
+      *reinterpret_cast<float2*>(xr + 2 * l) = make_float2(a0, a1);
+    } else {
+      for (int f = 0; f < F; ++f) {
+        float a = 0.f;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) a = fmaf(w[k], __ldg(tl + (size_t)idx[k] * F + f), a);
+        xr[l * F + f] = a;
+      }
     }
   }
-  if (l == 0)
-    for (int k = L * F; k < xs; ++k) xr[k] = 0.f;
+  for (int k = L * F; k < xs; ++k) xr[k] = 0.f;
 }
 
-// K1b: table scatter of the feature gradient, one thread per (row, level)
-// (ntc.py:278-288), vector reductions into L2-resident tables.
-__global__ void scatter_kernel(ss_grid g, int64_t n, const float* __restrict__ means,
-                               const int32_t* __restrict__ rows, const float* __restrict__ dX,
-                               int xs, float* __restrict__ g_tables) {
-  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int L = g.n_levels;
-  if (t >= n * L) return;
-  const int64_t i = t / L;
-  const int l = (int)(t - i * L);
-  const int64_t gid = rows ? rows[i] : i;
+// Warp-aggregated reduction of (vx, vy) into g[key]: lanes whose key equals
+// their left neighbour's form a run (the rows are Morton-ordered, so equal
+// corners are adjacent at the coarse levels); a segmented suffix sum gives
+// each run head the run total and only heads issue the vector reduction.
+// Non-adjacent duplicates are separate runs (still correct).  Lanes with
+// key == 0xffffffff are inactive.
+__device__ __forceinline__ void red_add_v2_agg(float* gl, uint32_t key, float vx, float vy) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t prev = __shfl_up_sync(0xffffffffu, key, 1);
+  const bool head = lane == 0 || prev != key;
+  const uint32_t heads = __ballot_sync(0xffffffffu, head);
+  if (heads == 0xffffffffu) {  // no two adjacent lanes share a corner
+    if (key != 0xffffffffu) red_add_v2(gl + 2 * (size_t)key, vx, vy);
+    return;
+  }
+  const uint32_t after = heads & ~(0xffffffffu >> (31 - lane));  // heads strictly above lane
+  const int seg_end = after ? __ffs(after) - 1 : 32;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const float ox = __shfl_down_sync(0xffffffffu, vx, off);
+    const float oy = __shfl_down_sync(0xffffffffu, vy, off);
+    if (lane + off < seg_end) vx += ox, vy += oy;
+  }
+  if (head && key != 0xffffffffu) red_add_v2(gl + 2 * (size_t)key, vx, vy);
+}
+
+// K1b: table scatter of the feature gradient (ntc.py:278-288), one thread per
+// inside row walking the levels, warp-aggregated vector reductions into the
+// L2-resident gradient tables.
+__global__ void __launch_bounds__(256) scatter_kernel(ss_grid g, int64_t n,
+                                                      const float* __restrict__ means,
+                                                      const int32_t* __restrict__ rows,
+                                                      const float* __restrict__ dX, int xs,
+                                                      float* __restrict__ g_tables) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const bool ok = i < n;
+  if (__all_sync(0xffffffffu, !ok)) return;  // warp-uniform exit keeps the shuffles full
+  const int L = g.n_levels, F = g.n_features;
+  const int64_t gid = ok ? (rows ? rows[i] : i) : 0;
   double xn[3];
   normalise(g, means + 3 * gid, xn);
-  uint32_t idx[8];
-  float w[8];
-  level_corners(g, l, xn, idx, w);
-  const int F = g.n_features;
   const size_t T = (size_t)1 << g.log2_table;
-  float* gl = g_tables + (size_t)l * T * F;
-  const float* dr = dX + i * xs + l * F;
-  if (F == 2) {
-    const float2 d = *reinterpret_cast<const float2*>(dr);
+  const float* dr = dX + (ok ? i : 0) * xs;
+  for (int l = 0; l < L; ++l) {
+    uint32_t idx[8];
+    float w[8];
+    level_corners(g, l, xn, idx, w);
+    float* gl = g_tables + (size_t)l * T * F;
+    if (F == 2) {
+      const float2 d = ok ? *reinterpret_cast<const float2*>(dr + 2 * l) : make_float2(0.f, 0.f);
 #pragma unroll
-    for (int k = 0; k < 8; ++k) red_add_v2(gl + 2 * (size_t)idx[k], w[k] * d.x, w[k] * d.y);
-  } else {
-    for (int f = 0; f < F; ++f) {
-      const float d = dr[f];
+      for (int k = 0; k < 8; ++k)
+        red_add_v2_agg(gl, ok ? idx[k] : 0xffffffffu, w[k] * d.x, w[k] * d.y);
+    } else if (ok) {
+      for (int f = 0; f < F; ++f) {
+        const float d = dr[l * F + f];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) atomicAdd(gl + (size_t)idx[k] * F + f, w[k] * d);
+        for (int k = 0; k < 8; ++k) atomicAdd(gl + (size_t)idx[k] * F + f, w[k] * d);
+      }
     }
   }
 }
@@ -464,15 +500,18 @@ __global__ void __launch_bounds__(128) mlp_fwd_kernel(int64_t n, const float* __
 template <int DEG>
 __global__ void __launch_bounds__(128) transform_kernel(ss_cloud src, int64_t n,
                                                         const int32_t* __restrict__ rows,
+                                                        const int32_t* __restrict__ pos,
                                                         const float* __restrict__ out7, int os,
                                                         int rotate_sh, float* __restrict__ t_means,
                                                         float* __restrict__ t_rot,
                                                         float* __restrict__ t_sh,
                                                         uint32_t* status) {
   constexpr int K = (DEG + 1) * (DEG + 1);
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const int64_t gid = rows ? rows[i] : i;
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  // rows in index order (coalesced cloud rows); pos = the row's slot in out7
+  const int64_t gid = rows ? rows[j] : j;
+  const int64_t i = pos ? pos[j] : j;
   float o[7];
 #pragma unroll
   for (int k = 0; k < 7; ++k) o[k] = out7[i * os + k];
@@ -506,13 +545,16 @@ __global__ void __launch_bounds__(128) transform_kernel(ss_cloud src, int64_t n,
 // K3b: dL/d[d_mu | d_q] from transformed-cloud gradients (transform.py:111-134)
 template <int DEG>
 __global__ void __launch_bounds__(128) transform_vjp_kernel(
-    ss_cloud src, int64_t n, const int32_t* __restrict__ rows, const float* __restrict__ out7,
-    int os, int rotate_sh, const float* __restrict__ d_means, const float* __restrict__ d_rot,
-    const float* __restrict__ d_sh, float* __restrict__ g7, int gs) {
+    ss_cloud src, int64_t n, const int32_t* __restrict__ rows, const int32_t* __restrict__ pos,
+    const float* __restrict__ out7, int os, int rotate_sh, const float* __restrict__ d_means,
+    const float* __restrict__ d_rot, const float* __restrict__ d_sh, float* __restrict__ g7,
+    int gs) {
   constexpr int K = (DEG + 1) * (DEG + 1);
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const int64_t gid = rows ? rows[i] : i;
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  // rows in index order (coalesced cloud rows); pos = the row's slot in out7
+  const int64_t gid = rows ? rows[j] : j;
+  const int64_t i = pos ? pos[j] : j;
   float o[7];
 #pragma unroll
   for (int k = 0; k < 7; ++k) o[k] = out7[i * os + k];
@@ -956,9 +998,7 @@ int ntc_forward_run(const ss_grid* g, const ss_mlp* mlp, int64_t n, const float*
   SS_TRY(check_grid(g, mlp));
   if (n == 0) return SS_OK;
   prof_begin(PH_NTC_FWD, st);
-  const int64_t threads = n * g->n_levels;
-  gather_kernel<<<(unsigned)cdiv(threads, 256), 256, 0, st>>>(*g, n, means, rows, tables, X, xs,
-                                                                status);
+  gather_kernel<<<(unsigned)cdiv(n, 256), 256, 0, st>>>(*g, n, means, rows, tables, X, xs, status);
   SS_CHECK_LAUNCH("gather_kernel");
   if (mlp_mode() != 0)
     SS_TRY(mlp_fwd_tc(xs, mlp->n_hidden, n, X, xs, params, out, os, relu, st));  // tcgen05
@@ -979,17 +1019,15 @@ int ntc_backward_run(const ss_grid* g, const ss_mlp* mlp, int64_t n, const float
     SS_TRY(mlp_bwd_tc(xs, mlp->n_hidden, n, X, xs, g_out, gs, relu, params, dX, g_params, st));
   else
     SS_TRY(dispatch_mlp(mlp, MlpBwd{n, X, xs, g_out, gs, params, dX, g_params, st}));
-  const int64_t threads = n * g->n_levels;
-  scatter_kernel<<<(unsigned)cdiv(threads, 256), 256, 0, st>>>(*g, n, means, rows, dX, xs,
-                                                                 g_tables);
+  scatter_kernel<<<(unsigned)cdiv(n, 256), 256, 0, st>>>(*g, n, means, rows, dX, xs, g_tables);
   SS_CHECK_LAUNCH("scatter_kernel");
   prof_end(PH_NTC_BWD, st);
   return SS_OK;
 }
 
-int transform_run(const ss_cloud* src, int64_t n, const int32_t* rows, const float* out7, int os,
-                  int rotate_sh, float* tm, float* tr, float* ts, uint32_t* status,
-                  cudaStream_t st) {
+int transform_run(const ss_cloud* src, int64_t n, const int32_t* rows, const int32_t* pos,
+                  const float* out7, int os, int rotate_sh, float* tm, float* tr, float* ts,
+                  uint32_t* status, cudaStream_t st) {
   if (!src || src->sh_coeffs < 1 || src->sh_coeffs > 16) {
     set_error("transform: bad cloud");
     return SS_ERR_DATA;
@@ -999,19 +1037,19 @@ int transform_run(const ss_cloud* src, int64_t n, const int32_t* rows, const flo
   prof_begin(PH_TRANSFORM, st);
   const unsigned grid = (unsigned)cdiv(n, 128);
   switch (sh_degree_of(src->sh_coeffs)) {
-    case 0: transform_kernel<0><<<grid, 128, 0, st>>>(*src, n, rows, out7, os, rotate_sh, tm, tr, ts, status); break;
-    case 1: transform_kernel<1><<<grid, 128, 0, st>>>(*src, n, rows, out7, os, rotate_sh, tm, tr, ts, status); break;
-    case 2: transform_kernel<2><<<grid, 128, 0, st>>>(*src, n, rows, out7, os, rotate_sh, tm, tr, ts, status); break;
-    default: transform_kernel<3><<<grid, 128, 0, st>>>(*src, n, rows, out7, os, rotate_sh, tm, tr, ts, status); break;
+    case 0: transform_kernel<0><<<grid, 128, 0, st>>>(*src, n, rows, pos, out7, os, rotate_sh, tm, tr, ts, status); break;
+    case 1: transform_kernel<1><<<grid, 128, 0, st>>>(*src, n, rows, pos, out7, os, rotate_sh, tm, tr, ts, status); break;
+    case 2: transform_kernel<2><<<grid, 128, 0, st>>>(*src, n, rows, pos, out7, os, rotate_sh, tm, tr, ts, status); break;
+    default: transform_kernel<3><<<grid, 128, 0, st>>>(*src, n, rows, pos, out7, os, rotate_sh, tm, tr, ts, status); break;
   }
   SS_CHECK_LAUNCH("transform_kernel");
   prof_end(PH_TRANSFORM, st);
   return SS_OK;
 }
 
-int transform_vjp_run(const ss_cloud* src, int64_t n, const int32_t* rows, const float* out7, int os,
-                      int rotate_sh, const float* dm, const float* dr, const float* ds, float* g7,
-                      int gs, cudaStream_t st) {
+int transform_vjp_run(const ss_cloud* src, int64_t n, const int32_t* rows, const int32_t* pos,
+                      const float* out7, int os, int rotate_sh, const float* dm, const float* dr,
+                      const float* ds, float* g7, int gs, cudaStream_t st) {
   if (!src || src->sh_coeffs < 1 || src->sh_coeffs > 16) {
     set_error("transform vjp: bad cloud");
     return SS_ERR_DATA;
@@ -1021,10 +1059,10 @@ int transform_vjp_run(const ss_cloud* src, int64_t n, const int32_t* rows, const
   prof_begin(PH_TRANSFORM_BWD, st);
   const unsigned grid = (unsigned)cdiv(n, 128);
   switch (sh_degree_of(src->sh_coeffs)) {
-    case 0: transform_vjp_kernel<0><<<grid, 128, 0, st>>>(*src, n, rows, out7, os, rotate_sh, dm, dr, ds, g7, gs); break;
-    case 1: transform_vjp_kernel<1><<<grid, 128, 0, st>>>(*src, n, rows, out7, os, rotate_sh, dm, dr, ds, g7, gs); break;
-    case 2: transform_vjp_kernel<2><<<grid, 128, 0, st>>>(*src, n, rows, out7, os, rotate_sh, dm, dr, ds, g7, gs); break;
-    default: transform_vjp_kernel<3><<<grid, 128, 0, st>>>(*src, n, rows, out7, os, rotate_sh, dm, dr, ds, g7, gs); break;
+    case 0: transform_vjp_kernel<0><<<grid, 128, 0, st>>>(*src, n, rows, pos, out7, os, rotate_sh, dm, dr, ds, g7, gs); break;
+    case 1: transform_vjp_kernel<1><<<grid, 128, 0, st>>>(*src, n, rows, pos, out7, os, rotate_sh, dm, dr, ds, g7, gs); break;
+    case 2: transform_vjp_kernel<2><<<grid, 128, 0, st>>>(*src, n, rows, pos, out7, os, rotate_sh, dm, dr, ds, g7, gs); break;
+    default: transform_vjp_kernel<3><<<grid, 128, 0, st>>>(*src, n, rows, pos, out7, os, rotate_sh, dm, dr, ds, g7, gs); break;
   }
   SS_CHECK_LAUNCH("transform_vjp_kernel");
   prof_end(PH_TRANSFORM_BWD, st);
@@ -1145,8 +1183,8 @@ int ss_apply_ntc(const ss_grid* grid, const ss_mlp* mlp, const ss_cloud* src, in
   const int os = out7 ? 7 : 8;
   SS_TRY(ntc_forward_run(grid, mlp, n_in, src->means, rows, tables, params, s.X, s.xs, o, os,
                          s.relu, status, st));
-  return transform_run(src, n_in, rows, o, os, rotate_sh, out_means, out_rotations, out_sh,
-                       status, st);
+  return transform_run(src, n_in, rows, nullptr, o, os, rotate_sh, out_means, out_rotations,
+                       out_sh, status, st);
 }
 
 size_t ss_apply_ntc_backward_bytes(int64_t n_in) { return ntc_scratch_bytes(nullptr, n_in); }
@@ -1168,8 +1206,8 @@ int ss_apply_ntc_backward(const ss_grid* grid, const ss_mlp* mlp, const ss_cloud
   NtcScratch s = ntc_scratch(scratch, mlp, n_in);
   SS_TRY(ntc_forward_run(grid, mlp, n_in, src->means, rows, tables, params, s.X, s.xs, s.out7, 8,
                          s.relu, nullptr, st));
-  SS_TRY(transform_vjp_run(src, n_in, rows, s.out7, 8, rotate_sh, d_means, d_rotations, d_sh,
-                           s.g7, 8, st));
+  SS_TRY(transform_vjp_run(src, n_in, rows, nullptr, s.out7, 8, rotate_sh, d_means, d_rotations,
+                           d_sh, s.g7, 8, st));
   return ntc_backward_run(grid, mlp, n_in, src->means, rows, params, s.X, s.xs, s.g7, 8, s.relu,
                           s.dX,
                           g_tables, g_params, st);
@@ -1178,15 +1216,15 @@ int ss_apply_ntc_backward(const ss_grid* grid, const ss_mlp* mlp, const ss_cloud
 int ss_transform_apply(const ss_cloud* src, int64_t n_in, const int32_t* rows, const float* out7,
                        int32_t rotate_sh, float* out_means, float* out_rotations, float* out_sh,
                        uint32_t* status, void* stream) {
-  return transform_run(src, n_in, rows, out7, 7, rotate_sh, out_means, out_rotations, out_sh,
-                       status, as_stream(stream));
+  return transform_run(src, n_in, rows, nullptr, out7, 7, rotate_sh, out_means, out_rotations,
+                       out_sh, status, as_stream(stream));
 }
 
 int ss_transform_vjp(const ss_cloud* src, int64_t n_in, const int32_t* rows, const float* out7,
                      int32_t rotate_sh, const float* d_means, const float* d_rotations,
                      const float* d_sh, float* g_out7, void* stream) {
-  return transform_vjp_run(src, n_in, rows, out7, 7, rotate_sh, d_means, d_rotations, d_sh,
-                           g_out7, 7, as_stream(stream));
+  return transform_vjp_run(src, n_in, rows, nullptr, out7, 7, rotate_sh, d_means, d_rotations,
+                           d_sh, g_out7, 7, as_stream(stream));
 }
 
 int ss_adam_step(int64_t n_table, float* tables, float* g_tables, double* m_tables,

@@ -81,7 +81,9 @@ int ss_stage1_iter_begin(ss_stage1* st, const ss_camera* cam, int64_t* counts_ho
   cudaStream_t s = as_stream(stream);
   SS_TRY(ntc_forward_run(&st->grid, &st->mlp, st->n_in, st->src.means, st->rows, st->tables,
                          st->params, ns.X, ns.xs, ns.out7, 8, ns.relu, st->status, s));
-  SS_TRY(transform_run(&st->src, st->n_in, st->rows, ns.out7, 8, st->rotate_sh, st->t_means,
+  const bool perm = st->rows_index && st->rows_pos;
+  SS_TRY(transform_run(&st->src, st->n_in, perm ? st->rows_index : st->rows,
+                       perm ? st->rows_pos : nullptr, ns.out7, 8, st->rotate_sh, st->t_means,
                        st->t_rotations, st->t_sh, st->status, s));
   const ss_cloud tc = transformed(st);
   return raster_begin(&tc, cam, &st->settings, st->geom, counts_host, as_stream(stream));
@@ -129,7 +131,9 @@ int ss_stage1_iter_grads(ss_stage1* st, const ss_camera* cam, const float* targe
     SS_CHECK_LAUNCH("stats_kernel");
   }
   const NtcScratch ns = scratch_of(st);
-  SS_TRY(transform_vjp_run(&st->src, st->n_in, st->rows, ns.out7, 8, st->rotate_sh, st->d_means,
+  const bool perm = st->rows_index && st->rows_pos;
+  SS_TRY(transform_vjp_run(&st->src, st->n_in, perm ? st->rows_index : st->rows,
+                           perm ? st->rows_pos : nullptr, ns.out7, 8, st->rotate_sh, st->d_means,
                            st->d_rotations, st->d_sh, ns.g7, 8, s));
   SS_TRY(ntc_backward_run(&st->grid, &st->mlp, st->n_in, st->src.means, st->rows, st->params,
                           ns.X, ns.xs, ns.g7, 8, ns.relu, ns.dX, st->g_tables, st->g_params, s));

@@ -48,6 +48,31 @@ def inside_rows(grid: HashGridConfig, means: np.ndarray) -> np.ndarray:
     return np.flatnonzero(np.all((means >= lo) & (means <= hi), axis=1)).astype(np.int32)
 
 
+def _spread10(v: np.ndarray) -> np.ndarray:
+    v = v.astype(np.uint64) & np.uint64(0x3FF)
+    v = (v | (v << np.uint64(16))) & np.uint64(0x030000FF)
+    v = (v | (v << np.uint64(8))) & np.uint64(0x0300F00F)
+    v = (v | (v << np.uint64(4))) & np.uint64(0x030C30C3)
+    v = (v | (v << np.uint64(2))) & np.uint64(0x09249249)
+    return v
+
+
+def morton_rows(grid: HashGridConfig, means: np.ndarray, rows: np.ndarray) -> np.ndarray:
+    """Inside rows ordered along a 30-bit Morton curve of their AABB-normalised
+    position (stable for ties).  The NTC kernels run a thread per row, so this
+    puts rows that share hash-grid cells in the same warp: coalesced gathers
+    and warp-aggregated table scatters.  Frame setup; the order of the rows
+    does not change any result."""
+    if len(rows) == 0:
+        return rows
+    lo = np.asarray(grid.aabb_min, dtype=np.float64)
+    hi = np.asarray(grid.aabb_max, dtype=np.float64)
+    q = np.clip((means[rows].astype(np.float64) - lo) / (hi - lo), 0.0, 1.0)
+    c = np.minimum((q * 1024.0).astype(np.int64), 1023)
+    code = _spread10(c[:, 0]) | (_spread10(c[:, 1]) << np.uint64(1)) | (_spread10(c[:, 2]) << np.uint64(2))
+    return rows[np.argsort(code, kind="stable")].astype(np.int32)
+
+
 def view_order(seed: int, frame_index: int, n_views: int, iterations: int) -> list[int]:
     """pipeline.py:251-256, :263, :278-279."""
     rng = np.random.default_rng([seed, frame_index])
@@ -103,7 +128,13 @@ class Stage1Trainer:
         self.v_params = torch.zeros(npar, **f64)
         self.row_mask = torch.zeros(grid.n_levels * grid.table_size, dtype=torch.uint8, device=dev)
         self.step_dev = torch.zeros(1, dtype=torch.int32, device=dev)
-        self.rows = to_dev(inside_rows(grid, means_np), dtype=torch.int32, dev=dev)
+        rows_idx = inside_rows(grid, means_np)
+        rows_sorted = morton_rows(grid, means_np, rows_idx)
+        pos = np.empty(len(rows_idx), dtype=np.int32)  # slot of rows_idx[j] in rows_sorted
+        pos[np.searchsorted(rows_idx, rows_sorted)] = np.arange(len(rows_idx), dtype=np.int32)
+        self.rows = to_dev(rows_sorted, dtype=torch.int32, dev=dev)
+        self.rows_index = to_dev(rows_idx, dtype=torch.int32, dev=dev)
+        self.rows_pos = to_dev(pos, dtype=torch.int32, dev=dev)
         # ---- transformed cloud and per-view buffers
         self.t_means = torch.empty(n, 3, **f32)
         self.t_rot = torch.empty(n, 4, **f32)
@@ -146,6 +177,8 @@ class Stage1Trainer:
         s.src = self.cloud.struct()
         s.n_in = int(self.rows.numel())
         s.rows = ptr(self.rows)
+        s.rows_index = ptr(self.rows_index)
+        s.rows_pos = ptr(self.rows_pos)
         for name, t in (("tables", self.tables), ("params", self.params),
                         ("g_tables", self.g_tables), ("g_params", self.g_params),
                         ("m_tables", self.m_tables), ("v_tables", self.v_tables),
