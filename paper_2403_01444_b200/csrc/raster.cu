@@ -17,6 +17,7 @@ constexpr int kAccStride = 12;  // 48 B per rank: two aligned v4 reductions
 struct Geom {
   double *key_in, *key_out;
   int32_t *idx_in, *order;
+  int32_t* rank_of;  // per gid: its position in `order` (>= survivors when culled)
   double2* g_mean;   // per gid
   double4* g_conop;  // per gid (c00, c01+c10, c11, opacity)
   float4* g_color;   // per gid
@@ -69,6 +70,7 @@ static Geom plan_geom(void* base, int64_t n, const ss_camera* cam, const ss_rast
   g.key_out = c.take<double>(nn);
   g.idx_in = c.take<int32_t>(nn);
   g.order = c.take<int32_t>(nn);
+  g.rank_of = c.take<int32_t>(nn);
   g.g_mean = c.take<double2>(nn);
   g.g_conop = c.take<double4>(nn);
   g.g_color = c.take<float4>(nn);
@@ -157,7 +159,9 @@ struct Projected {
   double raw[3];
 };
 
-__device__ inline void project_one(const CamD& cam, const ss_cloud& cl, int64_t i, Projected& P) {
+// geometry only (no SH colour): camera-space point, EWA covariance chain,
+// conic, view direction, opacity
+__device__ inline void project_geom(const CamD& cam, const ss_cloud& cl, int64_t i, Projected& P) {
   const float* m = cl.means + 3 * i;
   for (int r = 0; r < 3; ++r)
     P.p[r] = cam.R[r][0] * (double)m[0] + cam.R[r][1] * (double)m[1] +
@@ -192,6 +196,11 @@ __device__ inline void project_one(const CamD& cam, const ss_cloud& cl, int64_t 
   P.dist = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
   const double dd = fmax(P.dist, 1e-12);
   for (int r = 0; r < 3; ++r) P.dir[r] = d[r] / dd;
+  P.op = 1.0 / (1.0 + exp(-(double)cl.opacity_logits[i]));
+}
+
+__device__ inline void project_one(const CamD& cam, const ss_cloud& cl, int64_t i, Projected& P) {
+  project_geom(cam, cl, i, P);
   const int K = cl.sh_coeffs;
   double basis[16];
   sh_basis<double>(sh_degree_of(K), P.dir[0], P.dir[1], P.dir[2], basis);
@@ -200,7 +209,6 @@ __device__ inline void project_one(const CamD& cam, const ss_cloud& cl, int64_t 
     for (int k = 0; k < K; ++k) s += basis[k] * (double)cl.sh[(i * K + k) * 3 + c];
     P.raw[c] = s;
   }
-  P.op = 1.0 / (1.0 + exp(-(double)cl.opacity_logits[i]));
 }
 
 // K4a: per-Gaussian projection; depth key (+inf when culled)
@@ -221,9 +229,12 @@ __global__ void preprocess_kernel(CamD cam, ss_cloud cl, Geom g) {
   project_one(cam, cl, i, P);
   g.g_mean[i] = make_double2(P.mean[0], P.mean[1]);
   g.g_conop[i] = make_double4(P.conic[0][0], P.conic[0][1] + P.conic[1][0], P.conic[1][1], P.op);
+  // w: the unclipped-channel mask of clip(0.5 + SH, 0, 1) (sh.py:51-59) for the backward
+  const int clip_mask = (P.raw[0] > 0.0 && P.raw[0] < 1.0) | (P.raw[1] > 0.0 && P.raw[1] < 1.0) << 1 |
+                        (P.raw[2] > 0.0 && P.raw[2] < 1.0) << 2;
   g.g_color[i] = make_float4((float)fmin(fmax(P.raw[0], 0.0), 1.0),
                              (float)fmin(fmax(P.raw[1], 0.0), 1.0),
-                             (float)fmin(fmax(P.raw[2], 0.0), 1.0), 0.f);
+                             (float)fmin(fmax(P.raw[2], 0.0), 1.0), (float)clip_mask);
   g.g_cov[i] = make_double2(P.cov2d[0][0], P.cov2d[1][1]);
 }
 
@@ -242,6 +253,7 @@ __global__ void rank_kernel(CamD cam, ss_raster_settings s, int64_t n, Geom g) {
   const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (r >= n) return;
   const int64_t V = g.dev_counts[0];
+  g.rank_of[g.order[r]] = (int32_t)r;
   if (r >= V) {
     g.offsets[r] = 0;
     return;
@@ -646,46 +658,59 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_bwd_kernel(
 }
 
 // K5b: per-survivor chain to raw parameters (rasterizer.py:351-402), float64
-__global__ void gaussian_bwd_kernel(CamD cam, ss_cloud cl, Geom g, int64_t n, ss_cloud_grads out,
-                                    int full) {
-  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (r >= n) return;
-  const int gid = g.order[r];
+// K5b: per-Gaussian chain from the rank accumulators back to the raw parameters
+// (rasterizer.py:351-402).  One thread per Gaussian in index order (coalesced
+// parameter reads and gradient writes; the rank accumulators are gathered).
+// The EWA / covariance / projection chain runs in fp64; the SH part (d_sh,
+// the view-direction gradient) in fp32 with the forward's clip mask.
+__global__ void __launch_bounds__(128, 4) gaussian_bwd_kernel(CamD cam, ss_cloud cl, Geom g,
+                                                              int64_t n, ss_cloud_grads out,
+                                                              int full) {
+  const int64_t gid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (gid >= n) return;
+  const int K = cl.sh_coeffs;
+  const int r = g.rank_of[gid];
   if (r >= g.dev_counts[0]) {  // culled: zero rows so callers need no memset
-    const int K = cl.sh_coeffs;
     if (out.viewspace) out.viewspace[gid] = 0.f;
     if (out.contributed) out.contributed[gid] = 0;
     if (out.d_means) for (int j = 0; j < 3; ++j) out.d_means[3 * gid + j] = 0.f;
-    if (out.d_rotations) for (int j = 0; j < 4; ++j) out.d_rotations[4 * gid + j] = 0.f;
-    if (out.d_sh) for (int j = 0; j < 3 * K; ++j) out.d_sh[(int64_t)gid * 3 * K + j] = 0.f;
+    if (out.d_rotations)
+      *reinterpret_cast<float4*>(out.d_rotations + 4 * gid) = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (out.d_sh) for (int j = 0; j < 3 * K; ++j) out.d_sh[gid * 3 * K + j] = 0.f;
     if (full && out.d_log_scales) for (int j = 0; j < 3; ++j) out.d_log_scales[3 * gid + j] = 0.f;
     if (full && out.d_opacity_logits) out.d_opacity_logits[gid] = 0.f;
     return;
   }
-  const float* a = g.acc + r * kAccStride;
-  const double acol[3] = {a[0], a[1], a[2]};
-  const double am[2] = {a[3], a[4]};
-  const double A[2][2] = {{a[5], a[6]}, {a[6], a[7]}};
-  const double aop = a[8];
+  const float4 a0 = *reinterpret_cast<const float4*>(g.acc + (int64_t)r * kAccStride);
+  const float4 a1 = *reinterpret_cast<const float4*>(g.acc + (int64_t)r * kAccStride + 4);
+  const float a8 = g.acc[(int64_t)r * kAccStride + 8];
+  const double am[2] = {a0.w, a1.x};
+  const double A[2][2] = {{a1.y, a1.z}, {a1.z, a1.w}};
+  const double aop = a8;
   if (out.viewspace) out.viewspace[gid] = (float)sqrt(am[0] * am[0] + am[1] * am[1]);
   if (out.contributed) out.contributed[gid] = g.touched[r];
   Projected P;
-  project_one(cam, cl, gid, P);
-  const int K = cl.sh_coeffs;
+  project_geom(cam, cl, gid, P);
   const int deg = sh_degree_of(K);
-  // colour -> SH and view direction (sh.py:62-81)
-  double gc[3];
-  for (int c = 0; c < 3; ++c) gc[c] = (P.raw[c] > 0.0 && P.raw[c] < 1.0) ? acol[c] : 0.0;
-  double basis[16], gbasis[16];
-  sh_basis<double>(deg, P.dir[0], P.dir[1], P.dir[2], basis);
+  // colour -> SH and view direction (sh.py:62-81), fp32, forward clip mask
+  const int cm = (int)g.g_color[gid].w;
+  const float gc[3] = {(cm & 1) ? a0.x : 0.f, (cm & 2) ? a0.y : 0.f, (cm & 4) ? a0.z : 0.f};
+  const float fdir[3] = {(float)P.dir[0], (float)P.dir[1], (float)P.dir[2]};
+  float basis[16], gbasis[16];
+  sh_basis<float>(deg, fdir[0], fdir[1], fdir[2], basis);
+  const float* sh = cl.sh + gid * 3 * K;
+  float* dsh = out.d_sh ? out.d_sh + gid * 3 * K : nullptr;
   for (int k = 0; k < K; ++k) {
-    const float* shk = cl.sh + (gid * K + k) * 3;
-    gbasis[k] = shk[0] * gc[0] + shk[1] * gc[1] + shk[2] * gc[2];
-    if (out.d_sh)
-      for (int c = 0; c < 3; ++c) out.d_sh[(gid * K + k) * 3 + c] = (float)(basis[k] * gc[c]);
+    gbasis[k] = sh[3 * k] * gc[0] + sh[3 * k + 1] * gc[1] + sh[3 * k + 2] * gc[2];
+    if (dsh) {
+      dsh[3 * k] = basis[k] * gc[0];
+      dsh[3 * k + 1] = basis[k] * gc[1];
+      dsh[3 * k + 2] = basis[k] * gc[2];
+    }
   }
-  double gdir[3] = {0.0, 0.0, 0.0};
-  sh_basis_vjp<double>(deg, P.dir[0], P.dir[1], P.dir[2], gbasis, gdir);
+  float gdirf[3] = {0.f, 0.f, 0.f};
+  sh_basis_vjp<float>(deg, fdir[0], fdir[1], fdir[2], gbasis, gdirf);
+  const double gdir[3] = {gdirf[0], gdirf[1], gdirf[2]};
   const double dd = fmax(P.dist, 1e-12);
   const double dg = P.dir[0] * gdir[0] + P.dir[1] * gdir[1] + P.dir[2] * gdir[2];
   double gw[3];
@@ -704,13 +729,11 @@ __global__ void gaussian_bwd_kernel(CamD cam, ss_cloud cl, Geom g, int64_t n, ss
   for (int i = 0; i < 2; ++i)
     for (int j = 0; j < 3; ++j)
       gM[i][j] = GM[i][0] * P.S[0][j] + GM[i][1] * P.S[1][j] + GM[i][2] * P.S[2][j];
+  double GMt[2][3];  // gcov2 M, rows p
+  for (int p = 0; p < 2; ++p)
+    for (int j = 0; j < 3; ++j) GMt[p][j] = gcov2[p][0] * P.M[0][j] + gcov2[p][1] * P.M[1][j];
   for (int i = 0; i < 3; ++i)
-    for (int j = 0; j < 3; ++j) {
-      double s = 0;
-      for (int p = 0; p < 2; ++p)
-        for (int q = 0; q < 2; ++q) s += P.M[p][i] * gcov2[p][q] * P.M[q][j];
-      gS[i][j] = s;
-    }
+    for (int j = 0; j < 3; ++j) gS[i][j] = P.M[0][i] * GMt[0][j] + P.M[1][i] * GMt[1][j];
   // g_J = g_M R_w^T
   double gJ[2][3];
   for (int i = 0; i < 2; ++i)
@@ -718,15 +741,16 @@ __global__ void gaussian_bwd_kernel(CamD cam, ss_cloud cl, Geom g, int64_t n, ss
       gJ[i][k] = gM[i][0] * cam.R[k][0] + gM[i][1] * cam.R[k][1] + gM[i][2] * cam.R[k][2];
   const double x = P.p[0], y = P.p[1], z = P.p[2];
   const double fx = cam.fx, fy = cam.fy;
+  const double iz = 1.0 / z, iz2 = iz * iz;
   double gp[3];
-  gp[0] = gJ[0][2] * (-fx / (z * z));
-  gp[1] = gJ[1][2] * (-fy / (z * z));
-  gp[2] = gJ[0][0] * (-fx / (z * z)) + gJ[1][1] * (-fy / (z * z)) +
-          gJ[0][2] * (2.0 * fx * x / (z * z * z)) + gJ[1][2] * (2.0 * fy * y / (z * z * z));
+  gp[0] = gJ[0][2] * (-fx * iz2);
+  gp[1] = gJ[1][2] * (-fy * iz2);
+  gp[2] = gJ[0][0] * (-fx * iz2) + gJ[1][1] * (-fy * iz2) + gJ[0][2] * (2.0 * fx * x * iz2 * iz) +
+          gJ[1][2] * (2.0 * fy * y * iz2 * iz);
   // + J^T acc_mean2d
-  gp[0] += (fx / z) * am[0];
-  gp[1] += (fy / z) * am[1];
-  gp[2] += (-fx * x / (z * z)) * am[0] + (-fy * y / (z * z)) * am[1];
+  gp[0] += (fx * iz) * am[0];
+  gp[1] += (fy * iz) * am[1];
+  gp[2] += (-fx * x * iz2) * am[0] + (-fy * y * iz2) * am[1];
   for (int j = 0; j < 3; ++j)
     gw[j] += gp[0] * cam.R[0][j] + gp[1] * cam.R[1][j] + gp[2] * cam.R[2][j];
   if (out.d_means)
@@ -743,8 +767,9 @@ __global__ void gaussian_bwd_kernel(CamD cam, ss_cloud cl, Geom g, int64_t n, ss
     double gu[4];
     quat_to_rot_vjp(P.u[0], P.u[1], P.u[2], P.u[3], gR, gu);
     const double dot = P.u[0] * gu[0] + P.u[1] * gu[1] + P.u[2] * gu[2] + P.u[3] * gu[3];
-    for (int k = 0; k < 4; ++k)
-      out.d_rotations[4 * gid + k] = (float)((gu[k] - P.u[k] * dot) / P.qn);
+    *reinterpret_cast<float4*>(out.d_rotations + 4 * gid) =
+        make_float4((float)((gu[0] - P.u[0] * dot) / P.qn), (float)((gu[1] - P.u[1] * dot) / P.qn),
+                    (float)((gu[2] - P.u[2] * dot) / P.qn), (float)((gu[3] - P.u[3] * dot) / P.qn));
   }
   if (full) {
     if (out.d_log_scales)
