@@ -21,9 +21,10 @@ namespace ss {
 namespace {
 constexpr int kBsThreads = 256;
 constexpr int kBsWarps = kBsThreads / 32;
-constexpr int kBsSteps = 16;  // items per lane
-constexpr int kBsTile = kBsThreads * kBsSteps;
+constexpr int kBsStepsBig = 16;   // items per lane (4096-item tiles)
+constexpr int kBsStepsSmall = 4;  // 1024-item tiles for small sorts (more CTAs)
 constexpr uint32_t kFlagAgg = 1u << 30, kFlagInc = 2u << 30, kCntMask = (1u << 30) - 1;
+constexpr int kMaxPasses = 4;
 
 __device__ __forceinline__ uint32_t lanemask_lt() {
   uint32_t m;
@@ -37,43 +38,49 @@ __device__ __forceinline__ uint32_t ld_volatile(const uint32_t* p) {
 }
 }  // namespace
 
-BinSortWS binsort_plan(Carve& c, int64_t capacity) {
+BinSortWS binsort_plan(Carve& c, int64_t capacity, int max_passes) {
   BinSortWS w{};
-  w.max_blocks = (capacity + kBsTile - 1) / kBsTile;
+  w.steps = capacity <= (int64_t)1 << 20 ? kBsStepsSmall : kBsStepsBig;
+  const int64_t tile = (int64_t)kBsThreads * w.steps;
+  w.max_blocks = (capacity + tile - 1) / tile;
   if (w.max_blocks < 1) w.max_blocks = 1;
-  w.hist = c.take<uint32_t>(2 * 256 + 64);  // [pass][digit], then tickets
-  w.status = c.take<uint32_t>((size_t)2 * w.max_blocks * 256);
+  w.max_passes = max_passes;
+  w.hist = c.take<uint32_t>(kMaxPasses * 256 + 64);  // [pass][digit], then tickets
+  w.status = c.take<uint32_t>((size_t)max_passes * w.max_blocks * 256);
   return w;
 }
 
-size_t binsort_clear_bytes(const BinSortWS& w) {
-  return (2 * 256 + 64) * sizeof(uint32_t);
+static size_t binsort_clear_bytes(const BinSortWS&) {
+  return (kMaxPasses * 256 + 64) * sizeof(uint32_t);
 }
 
-// one histogram kernel for both passes
+// one histogram kernel for all passes (8-bit digits; the last may be narrower)
 __global__ void __launch_bounds__(256) bs_hist_kernel(const uint32_t* __restrict__ keys,
                                                       const int64_t* __restrict__ d_n,
-                                                      int64_t cap, int bits0, int bits1,
+                                                      int64_t cap, int key_bits,
                                                       uint32_t* __restrict__ hist) {
-  __shared__ uint32_t sh[2][256];
-  for (int i = threadIdx.x; i < 512; i += blockDim.x) (&sh[0][0])[i] = 0;
+  __shared__ uint32_t sh[kMaxPasses][256];
+  for (int i = threadIdx.x; i < kMaxPasses * 256; i += blockDim.x) (&sh[0][0])[i] = 0;
   __syncthreads();
   const int64_t n = min(*d_n, cap);
-  const uint32_t m0 = (1u << bits0) - 1, m1 = (1u << bits1) - 1;
+  const int passes = (key_bits + 7) / 8;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t k = keys[i];
-    atomicAdd(&sh[0][k & m0], 1u);
-    if (bits1 > 0) atomicAdd(&sh[1][(k >> bits0) & m1], 1u);
+    for (int p = 0; p < passes; ++p) {
+      const int bits = min(8, key_bits - 8 * p);
+      atomicAdd(&sh[p][(k >> (8 * p)) & ((1u << bits) - 1)], 1u);
+    }
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < 512; i += blockDim.x) {
+  for (int i = threadIdx.x; i < passes * 256; i += blockDim.x) {
     const uint32_t v = (&sh[0][0])[i];
     if (v) atomicAdd(hist + i, v);
   }
 }
 
-// pass over digit bits [shift, shift + bits)
+// pass over digit bits [shift, shift + bits); tiles of kBsThreads * STEPS items
+template <int STEPS>
 __global__ void __launch_bounds__(kBsThreads) bs_pass_kernel(
     const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin, uint32_t* __restrict__ kout,
     uint32_t* __restrict__ vout, const int64_t* __restrict__ d_n, int64_t cap, int shift, int bits,
@@ -83,6 +90,7 @@ __global__ void __launch_bounds__(kBsThreads) bs_pass_kernel(
   __shared__ uint32_t s_gbase[256];       // global position of this tile's first item of digit d
   __shared__ uint32_t s_lstart[256];      // tile-local start of digit d
   __shared__ uint32_t s_scan[256];
+  constexpr int kBsSteps = STEPS, kBsTile = kBsThreads * STEPS;
   __shared__ uint32_t s_keys[kBsTile], s_vals[kBsTile];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) s_bid = atomicAdd(ticket, 1u);
@@ -182,23 +190,23 @@ __global__ void __launch_bounds__(kBsThreads) bs_pass_kernel(
   }
 }
 
-int binsort_passes(int key_bits) { return key_bits > 8 ? 2 : 1; }
+int binsort_passes(int key_bits) { return (key_bits + 7) / 8; }
 
-// Sorts the (count *d_n, at most cap) pairs by the low `key_bits` bits into
-// keys_out/vals_out.  The input must be in keys_out/vals_out for two passes
-// (out -> tmp -> out) and in keys_tmp/vals_tmp for one (tmp -> out): see
-// binsort_passes().
+// Sorts the (count *d_n, at most cap) pairs by the low `key_bits` (<= 32) bits
+// into keys_out/vals_out, in ceil(key_bits / 8) passes ping-ponging with the
+// tmp buffers.  The input must be in keys_out/vals_out for an even number of
+// passes and in keys_tmp/vals_tmp for an odd one: see binsort_passes().
 int binsort_run(const BinSortWS& w, uint32_t* keys_tmp, uint32_t* vals_tmp, uint32_t* keys_out,
                 uint32_t* vals_out, const int64_t* d_n, int64_t cap, int key_bits,
                 cudaStream_t st) {
-  if (key_bits > 16) {
-    set_error("binsort: more than 2^16 tiles");
+  const int passes = binsort_passes(key_bits);
+  if (key_bits < 1 || passes > w.max_passes) {
+    set_error("binsort: key wider than the planned passes");
     return SS_ERR_DATA;
   }
-  const int b0 = key_bits < 8 ? key_bits : 8, b1 = key_bits - b0;
   SS_CUDA(cudaMemsetAsync(w.hist, 0, binsort_clear_bytes(w), st));
-  SS_CUDA(cudaMemsetAsync(w.status, 0, (size_t)(b1 > 0 ? 2 : 1) * w.max_blocks * 256 *
-                                           sizeof(uint32_t), st));
+  SS_CUDA(cudaMemsetAsync(w.status, 0, (size_t)passes * w.max_blocks * 256 * sizeof(uint32_t),
+                          st));
   static int sms = 0;
   if (!sms) {
     int dev = 0;
@@ -206,25 +214,22 @@ int binsort_run(const BinSortWS& w, uint32_t* keys_tmp, uint32_t* vals_tmp, uint
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (sms <= 0) sms = 148;
   }
-  uint32_t* src_k = b1 > 0 ? keys_out : keys_tmp;
+  uint32_t *ka = (passes & 1) ? keys_tmp : keys_out, *va = (passes & 1) ? vals_tmp : vals_out;
+  uint32_t *kb = (passes & 1) ? keys_out : keys_tmp, *vb = (passes & 1) ? vals_out : vals_tmp;
   const unsigned hgrid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(cap, 256), 4 * sms));
-  bs_hist_kernel<<<hgrid, 256, 0, st>>>(src_k, d_n, cap, b0, b1, w.hist);
+  bs_hist_kernel<<<hgrid, 256, 0, st>>>(ka, d_n, cap, key_bits, w.hist);
   SS_CHECK_LAUNCH("bs_hist_kernel");
-  uint32_t* tickets = w.hist + 512;
+  uint32_t* tickets = w.hist + kMaxPasses * 256;
   const unsigned grid = (unsigned)w.max_blocks;
-  if (b1 == 0) {
-    bs_pass_kernel<<<grid, kBsThreads, 0, st>>>(keys_tmp, vals_tmp, keys_out, vals_out, d_n, cap,
-                                                0, b0, w.hist, tickets, w.status);
+  for (int p = 0; p < passes; ++p) {
+    const int bits = std::min(8, key_bits - 8 * p);
+    auto k = w.steps == kBsStepsSmall ? bs_pass_kernel<kBsStepsSmall> : bs_pass_kernel<kBsStepsBig>;
+    k<<<grid, kBsThreads, 0, st>>>(ka, va, kb, vb, d_n, cap, 8 * p, bits, w.hist + 256 * p,
+                                   tickets + p, w.status + (size_t)p * w.max_blocks * 256);
     SS_CHECK_LAUNCH("bs_pass_kernel");
-    return SS_OK;
+    std::swap(ka, kb);
+    std::swap(va, vb);
   }
-  bs_pass_kernel<<<grid, kBsThreads, 0, st>>>(keys_out, vals_out, keys_tmp, vals_tmp, d_n, cap, 0,
-                                              b0, w.hist, tickets, w.status);
-  SS_CHECK_LAUNCH("bs_pass_kernel");
-  bs_pass_kernel<<<grid, kBsThreads, 0, st>>>(keys_tmp, vals_tmp, keys_out, vals_out, d_n, cap, b0,
-                                              b1, w.hist + 256, tickets + 1,
-                                              w.status + (size_t)w.max_blocks * 256);
-  SS_CHECK_LAUNCH("bs_pass_kernel");
   return SS_OK;
 }
 

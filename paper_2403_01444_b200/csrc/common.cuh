@@ -206,7 +206,7 @@ int raster_begin(const ss_cloud* cl, const ss_camera* cam, const ss_raster_setti
                  void* geom, int64_t* counts_host, cudaStream_t st);
 int raster_finish(const ss_cloud* cl, const ss_camera* cam, const ss_raster_settings* s,
                   void* geom, void* bins, int64_t pairs, float* image, float* alpha,
-                  int32_t* touch, uint32_t* status, cudaStream_t st);
+                  int32_t* touch, uint32_t* status, int cull, cudaStream_t st);
 // device pointer to [survivors, pairs] of the last raster_begin on `geom`
 const int64_t* raster_counts(void* geom, int64_t n, const ss_camera* cam,
                              const ss_raster_settings* s);
@@ -229,11 +229,13 @@ void prof_end(int phase, cudaStream_t s);
 
 // Device-count stable radix sort of (tile key, rank) pairs (binsort.cu)
 struct BinSortWS {
-  uint32_t* hist;    // [2][256] digit histograms, then the two pass tickets
-  uint32_t* status;  // [2][max_blocks][256] look-back words
+  uint32_t* hist;    // [4][256] digit histograms, then the pass tickets
+  uint32_t* status;  // [passes][max_blocks][256] look-back words
   int64_t max_blocks;
+  int max_passes;
+  int steps;  // items per thread of a pass tile
 };
-BinSortWS binsort_plan(Carve& c, int64_t capacity);
+BinSortWS binsort_plan(Carve& c, int64_t capacity, int max_passes);
 int binsort_passes(int key_bits);
 int binsort_run(const BinSortWS& w, uint32_t* keys_tmp, uint32_t* vals_tmp, uint32_t* keys_out,
                 uint32_t* vals_out, const int64_t* d_n, int64_t cap, int key_bits,

@@ -15,7 +15,8 @@ namespace ss {
 constexpr int kAccStride = 12;  // 48 B per rank: two aligned v4 reductions
 
 struct Geom {
-  double *key_in, *key_out;
+  double* key_in;              // per gid: fp64 depth (+inf when culled), tie-break of the sort
+  uint32_t *key32, *key32_tmp;  // per gid / rank: fp32 depth bits (the radix-sort key)
   int32_t *idx_in, *order;
   int32_t* rank_of;  // per gid: its position in `order` (>= survivors when culled)
   double2* g_mean;   // per gid
@@ -27,15 +28,15 @@ struct Geom {
   double4* r_conop_d;
   float4* r_color;
   int4* r_rect;     // per rank (tx0, tx1, ty0, ty1)
+  double* r_thr;    // per rank: 2 ln(opacity / skip_alpha), the tile-cull threshold
   int64_t* offsets;  // per rank, exclusive prefix of tile counts (n+1)
   float* acc;        // per rank x kAccStride: colour 3, mean2d 2, conic 00/01/11, opacity
   uint8_t* touched;  // per rank
   float* t_final;    // per pixel
   int32_t* n_contrib;
   int2* ranges;      // per tile
-  int64_t* dev_counts;  // [survivors, pairs]
-  void* cub_sort;
-  size_t cub_sort_bytes;
+  int64_t* dev_counts;  // [survivors, pairs, n]
+  BinSortWS dsort;      // depth sort workspace
   void* cub_scan;
   size_t cub_scan_bytes;
   size_t total;
@@ -67,7 +68,8 @@ static Geom plan_geom(void* base, int64_t n, const ss_camera* cam, const ss_rast
   const int64_t NT = (int64_t)ntiles_x(cam, s) * ntiles_y(cam, s);
   const int64_t nn = n > 0 ? n : 1;
   g.key_in = c.take<double>(nn);
-  g.key_out = c.take<double>(nn);
+  g.key32 = c.take<uint32_t>(nn);
+  g.key32_tmp = c.take<uint32_t>(nn);
   g.idx_in = c.take<int32_t>(nn);
   g.order = c.take<int32_t>(nn);
   g.rank_of = c.take<int32_t>(nn);
@@ -80,20 +82,18 @@ static Geom plan_geom(void* base, int64_t n, const ss_camera* cam, const ss_rast
   g.r_conop_d = c.take<double4>(nn);
   g.r_color = c.take<float4>(nn);
   g.r_rect = c.take<int4>(nn);
+  g.r_thr = c.take<double>(nn);
   g.offsets = c.take<int64_t>(nn + 1);
   g.acc = c.take<float>(nn * kAccStride);
   g.touched = c.take<uint8_t>(nn);
   g.t_final = c.take<float>(P);
   g.n_contrib = c.take<int32_t>(P);
   g.ranges = c.take<int2>(NT);
-  g.dev_counts = c.take<int64_t>(2);
-  size_t sb = 0, qb = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, sb, (const double*)nullptr, (double*)nullptr,
-                                  (const int32_t*)nullptr, (int32_t*)nullptr, (int)nn);
+  g.dev_counts = c.take<int64_t>(3);
+  g.dsort = binsort_plan(c, nn, 4);
+  size_t qb = 0;
   cub::DeviceScan::InclusiveSum(nullptr, qb, (const int64_t*)nullptr, (int64_t*)nullptr,
                                 (int)nn);
-  g.cub_sort_bytes = sb;
-  g.cub_sort = c.take<char>(sb);
   g.cub_scan_bytes = qb;
   g.cub_scan = c.take<char>(qb);
   g.total = c.bytes();
@@ -109,7 +109,7 @@ static Bins plan_bins(void* base, int64_t capacity) {
   b.keys_out = c.take<uint32_t>(pp);
   b.vals_in = c.take<uint32_t>(pp);
   b.vals_out = c.take<uint32_t>(pp);
-  b.sort = binsort_plan(c, pp);
+  b.sort = binsort_plan(c, pp, 2);
   b.total = c.bytes();
   return b;
 }
@@ -215,15 +215,20 @@ __device__ inline void project_one(const CamD& cam, const ss_cloud& cl, int64_t 
 __global__ void preprocess_kernel(CamD cam, ss_cloud cl, Geom g) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= cl.n) return;
-  g.idx_in[i] = (int32_t)i;
+  if (i == 0) g.dev_counts[2] = cl.n;
+  g.order[i] = (int32_t)i;  // sort input (4 passes: the input sits in the output buffers)
   const float* m = cl.means + 3 * i;
   const double z = cam.R[2][0] * (double)m[0] + cam.R[2][1] * (double)m[1] +
                    cam.R[2][2] * (double)m[2] + cam.t[2];
   if (!(z > cam.near_clip)) {  // rasterizer.py:228
     g.key_in[i] = __longlong_as_double(0x7ff0000000000000ll);  // +inf
+    g.key32[i] = 0x7f800000u;
     return;
   }
   g.key_in[i] = z;
+  // fp32 rounding is monotone, so sorting by the fp32 bits orders the fp64
+  // depths up to ties, which depth_tie_kernel resolves
+  g.key32[i] = __float_as_uint((float)z);
   atomicAdd(reinterpret_cast<unsigned long long*>(&g.dev_counts[0]), 1ull);
   Projected P;
   project_one(cam, cl, i, P);
@@ -246,6 +251,33 @@ __device__ inline int tile_of(double v, int ts, int nt) {
   long long t = q >= 0 ? q / ts : -((-q + ts - 1) / ts);
   t = t < 0 ? 0 : (t > nt - 1 ? nt - 1 : t);
   return (int)t;
+}
+
+// K4b tie-break: survivors are sorted by their fp32 depth bits (stable, so
+// index order within equal keys); runs of equal fp32 keys are re-sorted by
+// (fp64 depth, index) so the order equals the stable fp64 sort
+// (rasterizer.py:228-230).  Runs are rare and short.
+__global__ void depth_tie_kernel(Geom g) {
+  const int64_t V = g.dev_counts[0];
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= V) return;
+  const uint32_t k = g.key32[r];
+  if ((r > 0 && g.key32[r - 1] == k) || r + 1 >= V || g.key32[r + 1] != k) return;
+  int64_t e = r + 1;
+  while (e < V && g.key32[e] == k) ++e;
+  for (int64_t a = r + 1; a < e; ++a) {  // insertion sort by (fp64 depth, index)
+    const int32_t v = g.order[a];
+    const double dv = g.key_in[v];
+    int64_t b = a - 1;
+    while (b >= r) {
+      const int32_t u = g.order[b];
+      const double du = g.key_in[u];
+      if (du < dv || (du == dv && u < v)) break;
+      g.order[b + 1] = u;
+      --b;
+    }
+    g.order[b + 1] = v;
+  }
 }
 
 // K4b/K4c: gather per-rank records, tile rectangle and its count
@@ -279,6 +311,7 @@ __global__ void rank_kernel(CamD cam, ss_raster_settings s, int64_t n, Geom g) {
     rect = make_int4(tile_of(xl, ts, ntx), tile_of(xh, ts, ntx), tile_of(yl, ts, nty),
                      tile_of(yh, ts, nty));
     vis = !((xh < 0) || (xl > cam.W - 1) || (yh < 0) || (yl > cam.H - 1));
+    g.r_thr[r] = 2.0 * log(co.w / s.skip_alpha);
   } else {  // skip = 0: every tile (rasterizer.py:149-154)
     rect = make_int4(0, ntx - 1, 0, nty - 1);
     vis = true;
@@ -297,34 +330,85 @@ __global__ void finish_counts_kernel(Geom g, int64_t n) {
 // K4c: emit (tile id, rank) in rank order, one thread per pair (load-balanced:
 // near-camera splats can cover thousands of tiles).  The owning rank is the last
 // r with offsets[r] <= j (zero-count ranks are skipped by construction).
-__global__ void duplicate_kernel(int ntx, int64_t n, Geom g, Bins b, uint32_t* kdst,
-                                 uint32_t* vdst, uint32_t* status) {
+// Tile-level cull (render path only): a (splat, tile) pair whose alpha stays
+// below skip_alpha at every pixel centre of the tile contributes nothing to
+// the image, the loss or any gradient (rasterizer.py:198-199), so its key is
+// replaced by the sentinel ntiles and it sorts past every tile list.  The test
+// bounds alpha by the minimum of the fp64 Mahalanobis form over the tile's
+// pixel-centre rectangle (a relaxation of the discrete minimum: conservative).
+__device__ inline bool splat_misses_tile(const double2 m, const double4 co, double thr, double xa,
+                                         double xb, double ya, double yb) {
+  const double lx = xa - m.x, hx = xb - m.x, ly = ya - m.y, hy = yb - m.y;
+  if (lx <= 0.0 && hx >= 0.0 && ly <= 0.0 && hy >= 0.0) return thr < -2e-6;
+  auto q = [&](double dx, double dy) { return co.x * dx * dx + co.y * dx * dy + co.z * dy * dy; };
+  auto clampd = [](double v, double a, double b) { return fmin(fmax(v, a), b); };
+  double qmin = 1e300;
+  // edges x = const: minimise over dy
+  qmin = fmin(qmin, q(lx, clampd(-co.y * lx / (2.0 * co.z), ly, hy)));
+  qmin = fmin(qmin, q(hx, clampd(-co.y * hx / (2.0 * co.z), ly, hy)));
+  // edges y = const: minimise over dx
+  qmin = fmin(qmin, q(clampd(-co.y * ly / (2.0 * co.x), lx, hx), ly));
+  qmin = fmin(qmin, q(clampd(-co.y * hy / (2.0 * co.x), lx, hx), hy));
+  // op exp(-qmin / 2) < skip (1 - 1e-6)  <=>  qmin > 2 ln(op / skip) + 2e-6
+  return qmin > thr + 2e-6;
+}
+
+// K4c: emit (tile id, rank) in rank order, one thread per pair (load-balanced:
+// near-camera splats can cover thousands of tiles).  The owning rank is the last
+// r with offsets[r] <= j; a CTA narrows the search range once per 1024 pairs.
+__device__ inline int64_t owner_rank(const int64_t* __restrict__ off, int64_t lo, int64_t hi,
+                                     int64_t j) {  // offsets[lo] <= j < offsets[hi]
+  while (hi - lo > 1) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (off[mid] <= j) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void __launch_bounds__(256) duplicate_kernel(int ntx, int64_t n, Geom g, Bins b,
+                                                        uint32_t* kdst, uint32_t* vdst,
+                                                        uint32_t* status, int cull, int ts, int W,
+                                                        int H, uint32_t sentinel) {
+  constexpr int CH = 1024;
+  __shared__ int64_t s_lo, s_hi;
   const int64_t count = g.dev_counts[1];
   if (count > b.capacity && blockIdx.x == 0 && threadIdx.x == 0 && status)
     atomicOr(status, SS_FLAG_OVERFLOW);
   const int64_t pairs = min(count, b.capacity);
-  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < pairs;
-       j += (int64_t)gridDim.x * blockDim.x) {
-    int64_t lo = 0, hi = n;  // offsets[lo] <= j < offsets[hi]
-    while (hi - lo > 1) {
-      const int64_t mid = (lo + hi) >> 1;
-      if (g.offsets[mid] <= j) lo = mid; else hi = mid;
+  for (int64_t j0 = (int64_t)blockIdx.x * CH; j0 < pairs; j0 += (int64_t)gridDim.x * CH) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      s_lo = owner_rank(g.offsets, 0, n, j0);
+      s_hi = owner_rank(g.offsets, s_lo, n, min(j0 + CH, pairs) - 1) + 1;
     }
-    const int4 rc = g.r_rect[lo];
-    const int wx = rc.y - rc.x + 1;
-    const int local = (int)(j - g.offsets[lo]);
-    const int ty = rc.z + local / wx, tx = rc.x + local % wx;
-    kdst[j] = (uint32_t)(ty * ntx + tx);
-    vdst[j] = (uint32_t)lo;
+    __syncthreads();
+    const int64_t rlo = s_lo, rhi = s_hi;
+    for (int64_t j = j0 + threadIdx.x; j < min(j0 + CH, pairs); j += blockDim.x) {
+      const int64_t lo = owner_rank(g.offsets, rlo, rhi, j);
+      const int4 rc = g.r_rect[lo];
+      const int wx = rc.y - rc.x + 1;
+      const int local = (int)(j - g.offsets[lo]);
+      const int ty = rc.z + local / wx, tx = rc.x + local % wx;
+      uint32_t key = (uint32_t)(ty * ntx + tx);
+      if (cull) {
+        const double xa = tx * ts, xb = min(tx * ts + ts, W) - 1, ya = ty * ts,
+                     yb = min(ty * ts + ts, H) - 1;
+        if (splat_misses_tile(g.r_mean[lo], g.r_conop_d[lo], g.r_thr[lo], xa, xb, ya, yb))
+          key = sentinel;
+      }
+      kdst[j] = key;
+      vdst[j] = (uint32_t)lo;
+    }
   }
 }
 
 __global__ void ranges_kernel(const int64_t* __restrict__ d_pairs, int64_t cap,
-                              const uint32_t* __restrict__ keys, int2* ranges) {
+                              const uint32_t* __restrict__ keys, int2* ranges, uint32_t ntiles) {
   const int64_t pairs = min(*d_pairs, cap);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < pairs;
        i += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t k = keys[i];
+    if (k >= ntiles) continue;  // culled pairs (sentinel key) sort past the last tile
     if (i == 0 || keys[i - 1] != k) ranges[k].x = (int)i;
     if (i == pairs - 1 || keys[i + 1] != k) ranges[k].y = (int)(i + 1);
   }
@@ -332,15 +416,19 @@ __global__ void ranges_kernel(const int64_t* __restrict__ d_pairs, int64_t cap,
 
 // duplicate -> stable tile sort -> per-tile ranges, all driven by the device count
 static int bin_pairs(const ss_camera* cam, const ss_raster_settings* s, int64_t n, Geom& g,
-                     Bins& b, uint32_t* status, cudaStream_t st) {
+                     Bins& b, uint32_t* status, int cull, cudaStream_t st) {
   const int ntx = ntiles_x(cam, s), nty = ntiles_y(cam, s);
   const int64_t ntiles = (int64_t)ntx * nty;
-  const int kb = key_bits(ntiles);
+  cull = cull && s->skip_alpha > 0.0;
+  const int kb = key_bits(cull ? ntiles + 1 : ntiles);
   const bool two = binsort_passes(kb) == 2;
   SS_CUDA(cudaMemsetAsync(g.ranges, 0, ntiles * sizeof(int2), st));
   prof_begin(PH_DUPLICATE, st);
-  duplicate_kernel<<<stride_grid(b.capacity), 256, 0, st>>>(
-      ntx, n, g, b, two ? b.keys_out : b.keys_in, two ? b.vals_out : b.vals_in, status);
+  const unsigned dgrid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(b.capacity, 1024),
+                                                                         148 * 8));
+  duplicate_kernel<<<dgrid, 256, 0, st>>>(ntx, n, g, b, two ? b.keys_out : b.keys_in,
+                                          two ? b.vals_out : b.vals_in, status, cull, s->tile_size,
+                                          cam->width, cam->height, (uint32_t)ntiles);
   SS_CHECK_LAUNCH("duplicate_kernel");
   prof_end(PH_DUPLICATE, st);
   prof_begin(PH_TILE_SORT, st);
@@ -350,7 +438,7 @@ static int bin_pairs(const ss_camera* cam, const ss_raster_settings* s, int64_t 
   prof_end(PH_TILE_SORT, st);
   prof_begin(PH_RANGES, st);
   ranges_kernel<<<stride_grid(b.capacity), 256, 0, st>>>(g.dev_counts + 1, b.capacity, b.keys_out,
-                                                         g.ranges);
+                                                         g.ranges, (uint32_t)ntiles);
   SS_CHECK_LAUNCH("ranges_kernel");
   prof_end(PH_RANGES, st);
   return SS_OK;
@@ -850,17 +938,18 @@ int raster_begin(const ss_cloud* cl, const ss_camera* cam, const ss_raster_setti
   const int64_t n = cl->n;
   Geom g = plan_geom(geom, n, cam, s);
   const CamD cd = make_cam(cam);
-  SS_CUDA(cudaMemsetAsync(g.dev_counts, 0, 2 * sizeof(int64_t), st));
+  SS_CUDA(cudaMemsetAsync(g.dev_counts, 0, 3 * sizeof(int64_t), st));
   if (n > 0) {
     prof_begin(PH_PROJECT, st);
     preprocess_kernel<<<(unsigned)cdiv(n, 256), 256, 0, st>>>(cd, *cl, g);
     SS_CHECK_LAUNCH("preprocess_kernel");
     prof_end(PH_PROJECT, st);
     prof_begin(PH_DEPTH_SORT, st);
-    size_t sb = g.cub_sort_bytes;
-    SS_CUDA(cub::DeviceRadixSort::SortPairs(g.cub_sort, sb, g.key_in, g.key_out, g.idx_in,
-                                            g.order, (int)n, 0, 64, st));
-    g_launches.fetch_add(4);
+    SS_TRY(binsort_run(g.dsort, g.key32_tmp, reinterpret_cast<uint32_t*>(g.idx_in), g.key32,
+                       reinterpret_cast<uint32_t*>(g.order), g.dev_counts + 2, n, 32, st));
+    g_launches.fetch_add(5);
+    depth_tie_kernel<<<(unsigned)cdiv(n, 256), 256, 0, st>>>(g);
+    SS_CHECK_LAUNCH("depth_tie_kernel");
     prof_end(PH_DEPTH_SORT, st);
     prof_begin(PH_RANK_SCAN, st);
     rank_kernel<<<(unsigned)cdiv(n, 256), 256, 0, st>>>(cd, *s, n, g);
@@ -880,7 +969,7 @@ int raster_begin(const ss_cloud* cl, const ss_camera* cam, const ss_raster_setti
 
 int raster_finish(const ss_cloud* cl, const ss_camera* cam, const ss_raster_settings* s,
                   void* geom, void* bins, int64_t pairs, float* image, float* alpha,
-                  int32_t* touch, uint32_t* status, cudaStream_t st) {
+                  int32_t* touch, uint32_t* status, int cull, cudaStream_t st) {
   SS_TRY(check_raster(cl, cam, s));
   const int64_t n = cl->n;
   Geom g = plan_geom(geom, n, cam, s);
@@ -891,7 +980,7 @@ int raster_finish(const ss_cloud* cl, const ss_camera* cam, const ss_raster_sett
     set_error("more than 2^31 tile pairs in one view");
     return SS_ERR_CAPACITY;
   }
-  SS_TRY(bin_pairs(cam, s, n, g, b, status, st));
+  SS_TRY(bin_pairs(cam, s, n, g, b, status, cull, st));
   const BlendParams bp = blend_params(cam, s);
   prof_begin(PH_BLEND_FWD, st);
   const int rc = touch ? launch_blend_fwd<true>(s->tile_size, ntiles, st, bp, g, b.vals_out, image,
@@ -957,7 +1046,7 @@ int tile_bin_begin(int64_t n, const double* mean2d, const double* cov2d, const d
                    int64_t* counts_host, cudaStream_t st) {
   SS_TRY(check_raster(nullptr, cam, s));
   Geom g = plan_geom(geom, n, cam, s);
-  SS_CUDA(cudaMemsetAsync(g.dev_counts, 0, 2 * sizeof(int64_t), st));
+  SS_CUDA(cudaMemsetAsync(g.dev_counts, 0, 3 * sizeof(int64_t), st));
   if (n > 0) {
     tile_bin_setup_kernel<<<(unsigned)cdiv(n, 256), 256, 0, st>>>(n, mean2d, cov2d, opacity, g);
     SS_CHECK_LAUNCH("tile_bin_setup_kernel");
@@ -981,7 +1070,7 @@ int tile_bin_finish(int64_t n, const ss_camera* cam, const ss_raster_settings* s
   const int ntx = ntiles_x(cam, s), nty = ntiles_y(cam, s);
   const int64_t ntiles = (int64_t)ntx * nty;
   (void)ntiles;
-  return bin_pairs(cam, s, n, g, b, nullptr, st);
+  return bin_pairs(cam, s, n, g, b, nullptr, 0, st);
 }
 
 }  // namespace ss
@@ -1011,7 +1100,7 @@ int ss_raster_forward_finish(const ss_cloud* cloud, const ss_camera* cam,
                              const ss_raster_settings* s, void* geom, void* bins,
                              int64_t n_pairs, float* image, float* alpha_map, int32_t* touch,
                              void* stream) {
-  return raster_finish(cloud, cam, s, geom, bins, n_pairs, image, alpha_map, touch, nullptr,
+  return raster_finish(cloud, cam, s, geom, bins, n_pairs, image, alpha_map, touch, nullptr, 0,
                        as_stream(stream));
 }
 

@@ -99,7 +99,7 @@ int ss_stage1_iter_grads(ss_stage1* st, const ss_camera* cam, const float* targe
   const int64_t cap = st->bin_capacity;
   const ss_cloud tc = transformed(st);
   SS_TRY(raster_finish(&tc, cam, &st->settings, st->geom, st->bins, cap, st->image,
-                       st->alpha_map, nullptr, st->status, s));
+                       st->alpha_map, nullptr, st->status, 1, s));
   const int64_t slot = st->history_len > 0 ? st->iteration % st->history_len : 0;
   if (st->pair_history && st->history_len > 0)
     SS_CUDA(cudaMemcpyAsync(st->pair_history + slot,
@@ -158,7 +158,7 @@ int ss_stage1_render(ss_stage1* st, const ss_camera* cam, void* stream) {
   SS_TRY(ss_stage1_iter_begin(st, cam, nullptr, stream));
   const ss_cloud tc = transformed(st);
   return raster_finish(&tc, cam, &st->settings, st->geom, st->bins, st->bin_capacity, st->image,
-                       st->alpha_map, nullptr, st->status, as_stream(stream));
+                       st->alpha_map, nullptr, st->status, 1, as_stream(stream));
 }
 
 int ss_stage1_iter(ss_stage1* st, const ss_camera* cam, const float* target, float grad_scale,

@@ -281,3 +281,33 @@ def test_stage1_no_sync_matches_synchronised_path(P):
     lb = d.run(6)
     np.testing.assert_allclose(la, lb, rtol=1e-6)
     assert close(c.tables, d.tables) and close(c.params, d.params)
+
+
+@pytest.mark.parametrize("deg", [1, 3])
+def test_tile_cull_render_identical(P, deg):
+    """The Stage-1 render path drops (splat, tile) pairs whose fp64 alpha bound
+    stays below skip_alpha over the whole tile; the image must be bit-identical
+    to the full reference tile lists (public rasterize_forward path)."""
+    import torch
+
+    from paper_2403_01444_b200 import scenes
+    from paper_2403_01444_b200.stage1 import Stage1Config, Stage1Trainer
+    from oracle import stage1 as O
+
+    sc = scenes.small_scene(seed=40 + deg, n=4000, width=160, height=120, sh_degree=deg,
+                            n_views=2)
+    tables, mlp = O.init_ntc(sc.grid, output_init="random", seed=3)
+
+    class Cache:
+        grid = P["types"].HashGridConfig.from_any(sc.grid)
+
+    c = Cache()
+    c.tables, c.weights, c.biases = tables, mlp["weights"], mlp["biases"]
+    views = [(cam, np.zeros((cam["height"], cam["width"], 3))) for cam in sc.cameras]
+    tr = Stage1Trainer(sc.cloud, c, views, Stage1Config())
+    for v in range(2):
+        tr.render(v)  # full lists
+        full = tr.image.clone()
+        tr.render_async(v)  # culled lists
+        torch.cuda.synchronize()
+        assert torch.equal(full, tr.image)
