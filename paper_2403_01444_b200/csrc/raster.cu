@@ -25,6 +25,7 @@ struct Geom {
   double2* g_cov;    // per gid (cov2d[0][0], cov2d[1][1]) for the tile rect
   double2* r_mean;   // per rank
   float4* r_conop;   // per rank, fp32 copy for the blend
+  float4* r_q;       // per rank: log2 Gaussian form (A, B, C) and the reject bound log2(skip/op)
   double4* r_conop_d;
   float4* r_color;
   int4* r_rect;     // per rank (tx0, tx1, ty0, ty1)
@@ -79,6 +80,7 @@ static Geom plan_geom(void* base, int64_t n, const ss_camera* cam, const ss_rast
   g.g_cov = c.take<double2>(nn);
   g.r_mean = c.take<double2>(nn);
   g.r_conop = c.take<float4>(nn);
+  g.r_q = c.take<float4>(nn);
   g.r_conop_d = c.take<double4>(nn);
   g.r_color = c.take<float4>(nn);
   g.r_rect = c.take<int4>(nn);
@@ -296,7 +298,13 @@ __global__ void rank_kernel(CamD cam, ss_raster_settings s, int64_t n, Geom g) {
   g.r_mean[r] = m;
   g.r_conop_d[r] = co;
   g.r_conop[r] = make_float4((float)co.x, (float)co.y, (float)co.z, (float)co.w);
-  g.r_color[r] = g.g_color[gid];
+  // log2 G = A dx^2 + B dx dy + C dy^2; a pixel with log2 G below log2(skip (1 - 2e-4) / op)
+  // has alpha < skip_alpha beyond any fp32 rounding (blend fast reject)
+  constexpr double kq = -0.72134752044448170368;  // -0.5 log2(e)
+  const double qthr = s.skip_alpha > 0.0 ? log2(s.skip_alpha * (1.0 - 2e-4) / co.w) : -1e30;
+  g.r_q[r] = make_float4((float)(kq * co.x), (float)(kq * co.y), (float)(kq * co.z), (float)qthr);
+  const float4 gc = g.g_color[gid];
+  g.r_color[r] = make_float4(gc.x, gc.y, gc.z, (float)co.w);  // w: opacity
   const int ts = s.tile_size;
   const int ntx = (cam.W + ts - 1) / ts, nty = (cam.H + ts - 1) / ts;
   int4 rect;
@@ -474,6 +482,36 @@ __device__ inline float pair_alpha(const BlendParams& bp, float dx, float dy, fl
   return a < bp.skip ? 0.f : a;
 }
 
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// log2 of the Gaussian at (dx, dy) from the per-rank form
+__device__ __forceinline__ float log2_gauss(float4 q, float dx, float dy) {
+  return fmaf(fmaf(q.x, dx, q.y * dy), dx, q.z * dy * dy);
+}
+
+// alpha from the log2 form (caller has already rejected lg < qthr); near the
+// skip threshold it is recomputed in float64 exactly as pair_alpha does
+__device__ inline float alpha_from_log2(const BlendParams& bp, float lg, float op, int rank,
+                                        float px, float py, const double2* __restrict__ mean_d,
+                                        const double4* __restrict__ conop_d, float& G, float& og) {
+  G = ex2_approx(lg);
+  og = op * G;
+  const float a = fminf(bp.clamp, og);
+  if (fabsf(a - bp.skip) <= 1e-4f * bp.skip) {
+    const double2 m = mean_d[rank];
+    const double4 c = conop_d[rank];
+    const double ddx = (double)px - m.x, ddy = (double)py - m.y;
+    const double mh = c.x * ddx * ddx + c.y * ddx * ddy + c.z * ddy * ddy;
+    const double ad = fmin(bp.clamp_d, c.w * exp(-0.5 * mh));
+    return ad < bp.skip_d ? 0.f : fmaxf((float)ad, bp.skip);
+  }
+  return a < bp.skip ? 0.f : a;
+}
+
 template <int TS>
 struct BlendShape {
   static constexpr int NT = TS * TS <= 256 ? TS * TS : 256;
@@ -487,6 +525,7 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_fwd_kernel(
   constexpr int NT = BlendShape<TS>::NT, PPT = BlendShape<TS>::PPT;
   __shared__ float2 s_xy[NT];
   __shared__ float4 s_co[NT];
+  __shared__ float4 s_q[NT];
   __shared__ float4 s_col[NT];
   __shared__ int s_rank[NT];
   __shared__ int s_touch[TOUCH ? NT : 1];
@@ -520,6 +559,7 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_fwd_kernel(
       const double2 m = g.r_mean[r];
       s_xy[threadIdx.x] = make_float2((float)(m.x - x0), (float)(m.y - y0));
       s_co[threadIdx.x] = g.r_conop[r];
+      s_q[threadIdx.x] = g.r_q[r];
       s_col[threadIdx.x] = g.r_color[r];
       s_rank[threadIdx.x] = r;
     }
@@ -528,8 +568,31 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_fwd_kernel(
     const int cnt = min(NT, range.y - b);
     for (int k = 0; k < cnt; ++k) {
       const float2 xy = s_xy[k];
-      const float4 co = s_co[k];
       int contrib = 0;
+      if (!TOUCH) {  // fast path: reject on the log2 form before the exponential
+        const float4 q = s_q[k];
+#pragma unroll
+        for (int p = 0; p < PPT; ++p) {
+          if (done[p]) continue;
+          const float dx = lx[p] - xy.x, dy = ly[p] - xy.y;
+          const float lg = log2_gauss(q, dx, dy);
+          if (lg < q.w) continue;
+          const float4 col = s_col[k];
+          float G, og;
+          const float a = alpha_from_log2(bp, lg, col.w, s_rank[k], lx[p] + x0, ly[p] + y0,
+                                          g.r_mean, g.r_conop_d, G, og);
+          if (a == 0.f) continue;
+          const float w = a * T[p];
+          C[p][0] = fmaf(w, col.x, C[p][0]);
+          C[p][1] = fmaf(w, col.y, C[p][1]);
+          C[p][2] = fmaf(w, col.z, C[p][2]);
+          T[p] *= 1.f - a;
+          last[p] = b - range.x + k + 1;
+          if (T[p] < bp.stop) done[p] = true;  // later splats fail T_before >= stop
+        }
+        continue;
+      }
+      const float4 co = s_co[k];
 #pragma unroll
       for (int p = 0; p < PPT; ++p) {
         if (done[p]) continue;
@@ -608,6 +671,7 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_bwd_kernel(
   constexpr int NA = 9;  // colour 3, mean2d 2, conic 3, opacity
   __shared__ float2 s_xy[NT];
   __shared__ float4 s_co[NT];
+  __shared__ float4 s_q[NT];
   __shared__ float4 s_col[NT];
   __shared__ int s_rank[NT];
   __shared__ float s_acc[NT * NA];
@@ -658,6 +722,7 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_bwd_kernel(
       const double2 m = g.r_mean[r];
       s_xy[threadIdx.x] = make_float2((float)(m.x - x0), (float)(m.y - y0));
       s_co[threadIdx.x] = g.r_conop[r];
+      s_q[threadIdx.x] = g.r_q[r];
       s_col[threadIdx.x] = g.r_color[r];
       s_rank[threadIdx.x] = r;
     }
@@ -672,11 +737,14 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_bwd_kernel(
       for (int p = 0; p < PPT; ++p) {
         if (pos_rel >= last[p]) continue;
         const float dx = lx[p] - xy.x, dy = ly[p] - xy.y;
-        float G, og;
-        const float a = pair_alpha(bp, dx, dy, co, s_rank[k], lx[p] + x0, ly[p] + y0, g.r_mean,
-                                   g.r_conop_d, G, og);
-        if (a == 0.f) continue;
+        const float4 q = s_q[k];
+        const float lg = log2_gauss(q, dx, dy);  // same decisions as the forward
+        if (lg < q.w) continue;
         const float4 col = s_col[k];
+        float G, og;
+        const float a = alpha_from_log2(bp, lg, col.w, s_rank[k], lx[p] + x0, ly[p] + y0,
+                                        g.r_mean, g.r_conop_d, G, og);
+        if (a == 0.f) continue;
         const float oma = 1.f - a;
         const float tb = T[p] / oma;  // T_before
         const float w = a * tb;
