@@ -293,18 +293,59 @@ class Stage1Trainer:
         return float(self.loss_dev.item())
 
     def iterate(self, view: int, grad_scale: float = 1.0, adam: bool = True,
-                staged: bool = False) -> None:
+                staged: bool = False, target: torch.Tensor | None = None) -> None:
         """One Stage-1 iteration with no host synchronisation (ss_stage1_iter):
-        the pair count stays on the device, bounded by the planned capacity."""
+        the pair count stays on the device, bounded by the planned capacity.
+        `target` overrides the view's resident target (a device buffer)."""
         if self.bins is None:
             self.plan_capacity()
         cam = self.cam_structs[view]
-        tgt = ptr(self._staging if staged else self.targets[view])
+        if target is not None:
+            tgt = ptr(target)
+        else:
+            tgt = ptr(self._staging if staged else self.targets[view])
         self._call(self.lib.ss_stage1_iter, C.byref(self.s), C.byref(cam), tgt,
                    C.c_float(grad_scale), int(adam), stream())
 
     def step(self, view: int) -> None:
         self.iterate(view)
+
+    def run_from_host(self, order: list[int], host_targets) -> np.ndarray:
+        """Stage-1 iterations whose targets live in pinned HOST memory: each
+        iteration's target is copied host->device on a copy stream while the
+        previous iteration computes (two staging buffers, event-ordered), and
+        each iteration's loss is read device->host into pinned memory.  One
+        synchronisation at the end; returns the per-iteration losses."""
+        dev = self.dev
+        main = torch.cuda.current_stream(dev)
+        copy = getattr(self, "_copy_stream", None) or torch.cuda.Stream(dev)
+        self._copy_stream = copy
+        if getattr(self, "_stage2", None) is None:
+            self._stage2 = [torch.empty_like(self.targets[0]) for _ in range(2)]
+        ready = [torch.cuda.Event() for _ in range(2)]
+        free = [torch.cuda.Event() for _ in range(2)]
+        losses = torch.empty(len(order), dtype=torch.float64, pin_memory=True)
+
+        def h2d(k):
+            b = k & 1
+            with torch.cuda.stream(copy):
+                if k >= 2:
+                    copy.wait_event(free[b])
+                t = host_targets[order[k]]
+                self._stage2[b].view(-1)[: t.numel()].copy_(t.view(-1), non_blocking=True)
+                ready[b].record(copy)
+
+        if order:
+            h2d(0)
+        for k, v in enumerate(order):
+            if k + 1 < len(order):
+                h2d(k + 1)
+            main.wait_event(ready[k & 1])
+            self.iterate(v, target=self._stage2[k & 1])
+            free[k & 1].record(main)
+            losses[k:k + 1].copy_(self.loss_dev, non_blocking=True)
+        main.synchronize()
+        return losses.numpy().copy()
 
     def pairs_of_last(self, k: int) -> np.ndarray:
         """Tile-pair counts of the last k iterations (device history; syncs)."""

@@ -311,3 +311,37 @@ def test_tile_cull_render_identical(P, deg):
         tr.render_async(v)  # culled lists
         torch.cuda.synchronize()
         assert torch.equal(full, tr.image)
+
+
+def test_run_from_host_matches_resident_targets(P):
+    """run_from_host (pinned host targets, copy-stream H2D overlapped with the
+    previous iteration, async loss D2H) == iterating on resident targets."""
+    import torch
+
+    from paper_2403_01444_b200 import scenes
+    from paper_2403_01444_b200.stage1 import Stage1Config, Stage1Trainer
+    from oracle import stage1 as O
+
+    sc = scenes.small_scene(seed=12, n=2500, width=96, height=72, sh_degree=1, n_views=3)
+    tables, mlp = O.init_ntc(sc.grid, output_init="random", seed=5)
+    targets = [O.render(scenes.moved_cloud(sc.cloud, np.random.default_rng(3)), c)[0]["image"]
+               for c in sc.cameras]
+
+    class Cache:
+        grid = P["types"].HashGridConfig.from_any(sc.grid)
+
+    def trainer():
+        c = Cache()
+        c.tables, c.weights, c.biases = tables.copy(), mlp["weights"], mlp["biases"]
+        return Stage1Trainer(sc.cloud, c, list(zip(sc.cameras, targets)),
+                             Stage1Config(stage1_iterations=8))
+
+    order = [0, 2, 1, 1, 0, 2, 2, 0]
+    a, b = trainer(), trainer()
+    ref = []
+    for v in order:
+        a.iterate(v)
+        ref.append(a.last_loss())
+    host = [torch.tensor(t, dtype=torch.float32).pin_memory() for t in targets]
+    got = b.run_from_host(order, host)
+    np.testing.assert_allclose(got, ref, rtol=1e-6)
