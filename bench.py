@@ -33,8 +33,8 @@ L2_FLUSH_BYTES = 256 << 20  # > 126 MB L2
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=100)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=150)
+    ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -264,6 +264,9 @@ def main():
 
     for k in range(a.warmup):
         tr.step(batch(k))
+    # the timed steps are iterations 0..K-1 of a Stage-1 frame (the per-iteration
+    # cost follows the NTC's motion over the frame): back to the frame start
+    tr.trainer.reset_frame()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -273,19 +276,22 @@ def main():
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(a.steps)]
     l0 = lib.ss_launch_count()
+    g0 = tr.trainer.graph_launches
     with Clocks(local) as clk:
         for k in range(a.steps):
             flush.fill_(k & 0xFF)  # L2 flush between timed steps (outside the events)
             ev[k][0].record()
-            tr.step(batch(a.warmup + k))
+            tr.step(batch(k))
             ev[k][1].record()
         torch.cuda.synchronize()
-    launches = lib.ss_launch_count() - l0
+    launches = lib.ss_launch_count() - l0 + tr.trainer.graph_launches - g0
     step_ms = [e0.elapsed_time(e1) for e0, e1 in ev]
     pairs = [int(p) for p in tr.trainer.pairs_of_last(a.steps)]
     if int(tr.trainer.check_status()) & _lib.FLAG_OVERFLOW:
         raise RuntimeError("tile-pair capacity overflow in the timed region")
     # ---- per-phase breakdown: a separate synchronised pass with phase events
+    tr.trainer.use_graphs = False  # phase events need the eager launches
+    tr.trainer.reset_frame()
     lib.ss_profile_enable(1)
     nph = lib.ss_profile_count()
     names = [lib.ss_profile_name(i).decode() for i in range(nph)]
@@ -293,13 +299,14 @@ def main():
     buf = (np.ctypeslib.ctypes.c_double * nph)()
     for k in range(min(a.steps, 10)):
         flush.fill_(k & 0xFF)
-        tr.step(batch(a.warmup + a.steps + k))
+        tr.step(batch(k))
         torch.cuda.synchronize()
         lib.ss_profile_read(buf, nph)
         for i, n in enumerate(names):
             if buf[i] >= 0:
                 phase_ms[n].append(buf[i])
     lib.ss_profile_enable(0)
+    tr.trainer.use_graphs = True
     ms = float(np.mean(step_ms))
     if world > 1:
         t = torch.tensor([ms], device="cuda")
@@ -336,6 +343,8 @@ def main():
                        "parallelism": f"view-sharded dp{world}" if world > 1 else "single",
                        "mean_tile_pairs": mean_pairs,
                        "l2": "flushed between timed steps (256 MB write)",
+                       "timed_iterations": f"0..{a.steps - 1} of a Stage-1 frame (state reset to "
+                                           f"the frame start after {a.warmup} warm-up steps)",
                        "ntc": "16 levels x 2 features, 2^15 rows, MLP 32-64-64-7",
                        "decoder": ["fp32 FFMA", "tcgen05 3xTF32", "tcgen05 tf32"][lib.ss_get_mlp_mode()]},
             "gpu_launches": int(launches),
@@ -351,7 +360,8 @@ def main():
             # Stage1Trainer.run_from_host: per step, pinned target H2D on a copy
             # stream (overlapping the previous step) + iteration + loss D2H
             order = [batch(k)[0] for k in range(a.steps)]
-            tr.trainer.run_from_host(order[:2], host_t)
+            tr.trainer.run_from_host([batch(k)[0] for k in range(2 * n_views)], host_t)
+            tr.trainer.reset_frame()
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             tr.trainer.run_from_host(order, host_t)
@@ -361,6 +371,7 @@ def main():
         else:
             for k in range(2):
                 tr.step_from_host(batch(k), host_t)
+            tr.trainer.reset_frame()
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             for k in range(a.steps):
@@ -394,7 +405,7 @@ def render_fps(a):
 
     sc, cache, targets = build_problem(2)
     tr = Stage1Trainer(sc.cloud, cache, list(zip(sc.cameras, targets)), Stage1Config())
-    for v in range(3):
+    for v in range(len(sc.cameras)):  # one warm-up frame per view (graph capture)
         tr.render_async(v)
     torch.cuda.synchronize()
     nv = len(sc.cameras)

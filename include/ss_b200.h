@@ -294,7 +294,9 @@ typedef struct ss_stage1 {
   double* loss_history;   /* optional (nullable): loss of iteration i at [i] */
   int64_t* pair_history;  /* optional (nullable): tile pairs of iteration i at [i] */
   int64_t history_len;    /* entries of the histories (iteration i -> [i % history_len]) */
-  int32_t iteration;
+  int32_t iteration;      /* host-side count of enqueued iterations */
+  int32_t* iter_dev;      /* device-side iteration count: indexes the histories, so a
+                             captured CUDA graph of an iteration stays correct on replay */
   uint32_t* status;
   void *geom, *bins, *loss_scratch, *ntc_scratch;
   int64_t bin_capacity; /* n_pairs the `bins` workspace holds; more raises

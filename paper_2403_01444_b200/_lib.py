@@ -77,7 +77,7 @@ class Stage1(C.Structure):
                 ("d_means", P), ("d_rotations", P), ("d_sh", P),
                 ("viewspace", P), ("contributed", P), ("stats_norm", P), ("stats_count", P),
                 ("loss_dev", P), ("loss_history", P), ("pair_history", P),
-                ("history_len", C.c_int64), ("iteration", C.c_int32),
+                ("history_len", C.c_int64), ("iteration", C.c_int32), ("iter_dev", P),
                 ("status", P), ("geom", P), ("bins", P), ("loss_scratch", P),
                 ("ntc_scratch", P), ("bin_capacity", C.c_int64)]
 

@@ -200,6 +200,16 @@ __device__ inline void red_add_v4(float* addr, float a, float b, float c, float 
 
 }  // namespace ss
 
+// Opt a kernel into `bytes` of dynamic shared memory once per (kernel, device):
+// the attribute persists, and re-setting it on every launch costs host time.
+namespace ss {
+cudaError_t smem_attr_once(const void* kernel, int bytes);
+template <class K>
+inline cudaError_t smem_attr_once(K* kernel, int bytes) {
+  return smem_attr_once(reinterpret_cast<const void*>(kernel), bytes);
+}
+}  // namespace ss
+
 // ---------------------------------------------------------------- internal API
 namespace ss {
 int raster_begin(const ss_cloud* cl, const ss_camera* cam, const ss_raster_settings* s,

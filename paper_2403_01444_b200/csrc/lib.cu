@@ -12,6 +12,20 @@ std::atomic<int64_t> g_launches{0};
 
 void set_error(const std::string& msg) { t_last_error = msg; }
 
+cudaError_t smem_attr_once(const void* kernel, int bytes) {
+  static std::mutex mu;
+  static std::vector<std::pair<const void*, int>> done;  // (kernel, device)
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  for (const auto& d : done)
+    if (d.first == kernel && d.second == dev) return cudaSuccess;
+  const cudaError_t e =
+      cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.emplace_back(kernel, dev);
+  return e;
+}
+
 // Band-l basis values at a unit direction (degree-l part of sh_basis).
 static void band_values(int l, const double d[3], double* out) {
   double b[16];

@@ -690,7 +690,7 @@ static int launch_tc(int64_t n, const float* X, int xs, const float* params, flo
                      uint64_t* masks, cudaStream_t st) {
   constexpr uint32_t smem = TcFwdSmem<IN, NL, P>::BYTES;
   auto k = mlp_fwd_tc_kernel<IN, NL, P>;
-  SS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  SS_CUDA(smem_attr_once(k, (int)smem));
   const unsigned grid = (unsigned)std::min<int64_t>((n + 127) / 128, (int64_t)num_sms_tc());
   k<<<grid, NT, smem, st>>>(n, X, xs, params, out, os, masks);
   SS_CHECK_LAUNCH("mlp_fwd_tc_kernel");
@@ -717,7 +717,7 @@ static int launch_bwd_tc(int64_t n, const float* X, int xs, const float* g, int 
   constexpr uint32_t smem = TcBwdSmem<IN, NL>::BYTES;
   static_assert(smem <= 220 * 1024, "backward tiles exceed shared memory");
   auto k = mlp_bwd_tc_kernel<IN, NL>;
-  SS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  SS_CUDA(smem_attr_once(k, (int)smem));
   const unsigned grid = (unsigned)std::min<int64_t>((n + 127) / 128, (int64_t)num_sms_tc());
   k<<<grid, NT, smem, st>>>(n, X, xs, g, gs, masks, params, dX, g_params);
   SS_CHECK_LAUNCH("mlp_bwd_tc_kernel");

@@ -944,7 +944,7 @@ struct MlpFwd {
   int run() {
     const size_t smem = Lay<IN, NL>::TOTAL * sizeof(float);
     auto k = mlp_fwd_kernel<IN, NL>;
-    SS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    SS_CUDA(smem_attr_once(k, (int)smem));
     k<<<(unsigned)cdiv(n, 128), 128, smem, st>>>(n, X, xs, params, out, os);
     SS_CHECK_LAUNCH("mlp_fwd_kernel");
     return SS_OK;
@@ -964,7 +964,7 @@ struct MlpBwd {
   int run() {
     const size_t smem = BwdSmem<IN, NL>::FLOATS * sizeof(float);
     auto k = mlp_bwd_kernel<IN, NL>;
-    SS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    SS_CUDA(smem_attr_once(k, (int)smem));
     const unsigned grid = (unsigned)std::min<int64_t>(cdiv(n, kChunk), num_sms());
     k<<<grid, kChunk, smem, st>>>(n, X, xs, g, gs, params, dX, g_params);
     SS_CHECK_LAUNCH("mlp_bwd_kernel");

@@ -23,6 +23,16 @@ __global__ void stats_kernel(int64_t n, const float* __restrict__ vs,
   count[i] += contrib[i];
 }
 
+// loss / pair-count histories at the device-side iteration index
+__global__ void history_kernel(const double* __restrict__ loss, const int64_t* __restrict__ pairs,
+                               double* loss_hist, int64_t* pair_hist, int64_t len,
+                               int32_t* __restrict__ iter_dev) {
+  const int64_t slot = len > 0 ? *iter_dev % len : 0;
+  if (loss_hist) loss_hist[slot] = *loss;
+  if (pair_hist) pair_hist[slot] = *pairs;
+  *iter_dev += 1;
+}
+
 __global__ void scale_kernel(int64_t n, float* __restrict__ v, float s) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < n) v[i] *= s;
@@ -72,6 +82,7 @@ int ss_stage1_frame_begin(ss_stage1* st, void* stream) {
   if (st->stats_norm) SS_CUDA(cudaMemsetAsync(st->stats_norm, 0, n * sizeof(float), s));
   if (st->stats_count) SS_CUDA(cudaMemsetAsync(st->stats_count, 0, n * sizeof(int32_t), s));
   st->iteration = 0;
+  if (st->iter_dev) SS_CUDA(cudaMemsetAsync(st->iter_dev, 0, sizeof(int32_t), s));
   return SS_OK;
 }
 
@@ -100,17 +111,15 @@ int ss_stage1_iter_grads(ss_stage1* st, const ss_camera* cam, const float* targe
   const ss_cloud tc = transformed(st);
   SS_TRY(raster_finish(&tc, cam, &st->settings, st->geom, st->bins, cap, st->image,
                        st->alpha_map, nullptr, st->status, 1, s));
-  const int64_t slot = st->history_len > 0 ? st->iteration % st->history_len : 0;
-  if (st->pair_history && st->history_len > 0)
-    SS_CUDA(cudaMemcpyAsync(st->pair_history + slot,
-                            raster_counts(st->geom, tc.n, cam, &st->settings) + 1, sizeof(int64_t),
-                            cudaMemcpyDeviceToDevice, s));
   SS_TRY(ss_render_loss(st->image, target, cam->height, cam->width, 3, st->lambda_dssim,
                         0.01 * 0.01, 0.03 * 0.03, st->loss_scratch, st->loss_dev, st->d_image,
                         st->status, stream));
-  if (st->loss_history && st->history_len > 0)
-    SS_CUDA(cudaMemcpyAsync(st->loss_history + slot, st->loss_dev, sizeof(double),
-                            cudaMemcpyDeviceToDevice, s));
+  if (st->iter_dev && st->history_len > 0) {
+    history_kernel<<<1, 1, 0, s>>>(st->loss_dev, raster_counts(st->geom, tc.n, cam, &st->settings) + 1,
+                                   st->loss_history, st->pair_history, st->history_len,
+                                   st->iter_dev);
+    SS_CHECK_LAUNCH("history_kernel");
+  }
   if (grad_scale != 1.0f) {
     const int64_t m = (int64_t)cam->width * cam->height * 3;
     scale_kernel<<<(unsigned)cdiv(m, 256), 256, 0, s>>>(m, st->d_image, grad_scale);

@@ -156,6 +156,7 @@ class Stage1Trainer:
         self.loss_hist = torch.zeros(hist, **f64)
         self.pair_hist = torch.zeros(hist, dtype=torch.int64, device=dev)
         self.status = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.iter_dev = torch.zeros(1, dtype=torch.int32, device=dev)
         geom = max(self.lib.ss_raster_geom_bytes(n, C.byref(cs), C.byref(self.settings))
                    for cs in self.cam_structs)
         lossb = max(self.lib.ss_loss_bytes(c.height, c.width, 3) for c in self.cameras)
@@ -191,7 +192,7 @@ class Stage1Trainer:
                         ("viewspace", self.viewspace), ("contributed", self.contributed),
                         ("stats_norm", self.stats_norm), ("stats_count", self.stats_count),
                         ("loss_dev", self.loss_dev), ("loss_history", self.loss_hist),
-                        ("pair_history", self.pair_hist),
+                        ("pair_history", self.pair_hist), ("iter_dev", self.iter_dev),
                         ("status", self.status), ("geom", self.geom),
                         ("loss_scratch", self.loss_scratch)):
             setattr(s, name, ptr(t))
@@ -200,11 +201,23 @@ class Stage1Trainer:
         s.ntc_scratch = ptr(self.ntc_scratch)
         self.s = s
         self.capacity_margin = 1.3
+        self.use_graphs = True
+        self._graphs = {}
+        self._frame_start = (self.tables.clone(), self.params.clone())
+        self.graph_launches = 0  # kernel launches issued through graph replays
         self.frame_begin()
 
     # ------------------------------------------------------------------
     def _call(self, fn, *args, what=""):
         _lib.check(fn(*args), what or fn.__name__)
+
+    def reset_frame(self):
+        """Back to the start of the frame: the parameters the trainer was built
+        with, fresh Adam state and statistics (captured graphs stay valid)."""
+        self.tables.copy_(self._frame_start[0])
+        self.params.copy_(self._frame_start[1])
+        self.status.zero_()
+        self.frame_begin()
 
     def frame_begin(self):
         """clone_cache + reset_adam (pipeline.py:213-219): fresh moments, step 0."""
@@ -214,6 +227,7 @@ class Stage1Trainer:
         if pairs <= self.bin_capacity and self.bins is not None:
             return
         cap = max(pairs if exact else int(pairs * 1.25) + 1024, 1 << 16)
+        self._graphs = {}  # captured iterations point at the old workspace
         nbytes = self.lib.ss_raster_bin_bytes(cap, self.cloud.n, C.byref(cam),
                                               C.byref(self.settings))
         self.bins = empty_bytes(nbytes, self.dev)
@@ -256,11 +270,19 @@ class Stage1Trainer:
         self._call(self.lib.ss_stage1_apply_adam, C.byref(self.s), stream())
 
     def render_async(self, view: int) -> None:
-        """Forward only with no host synchronisation (ss_stage1_render)."""
+        """Forward only with no host synchronisation (ss_stage1_render), one
+        CUDA-graph replay per call when graphs are on."""
         if self.bins is None:
             self.plan_capacity()
-        self._call(self.lib.ss_stage1_render, C.byref(self.s), C.byref(self.cam_structs[view]),
-                   stream())
+
+        def launch():
+            self._call(self.lib.ss_stage1_render, C.byref(self.s),
+                       C.byref(self.cam_structs[view]), stream())
+
+        if not self.use_graphs:
+            launch()
+            return
+        self._replay(("render", view), launch)
 
     def render(self, view: int) -> int:
         """Forward only (render-only config 2 / playback, pipeline.py:471-480):
@@ -293,12 +315,44 @@ class Stage1Trainer:
         return float(self.loss_dev.item())
 
     def iterate(self, view: int, grad_scale: float = 1.0, adam: bool = True,
-                staged: bool = False, target: torch.Tensor | None = None) -> None:
+                staged: bool = False, target: torch.Tensor | None = None,
+                graph: bool | None = None) -> None:
         """One Stage-1 iteration with no host synchronisation (ss_stage1_iter):
         the pair count stays on the device, bounded by the planned capacity.
-        `target` overrides the view's resident target (a device buffer)."""
+        `target` overrides the view's resident target (a device buffer).
+
+        With graphs on (default), the iteration's ~40 launches are captured
+        once per (view, target buffer, flags) into a CUDA graph and replayed
+        as one launch; everything an iteration reads from the host (camera,
+        buffers, flags) is fixed per key and the iteration index lives on the
+        device, so replays are exact."""
         if self.bins is None:
             self.plan_capacity()
+        use = self.use_graphs if graph is None else graph
+        if not use:
+            self._iterate_eager(view, grad_scale, adam, staged, target)
+            return
+        buf = target if target is not None else (self._staging if staged else None)
+        key = (view, None if buf is None else buf.data_ptr(), int(self.s.accumulate_stats),
+               bool(adam), float(grad_scale))
+        self._replay(key, lambda: self._iterate_eager(view, grad_scale, adam, staged, target))
+
+    def _replay(self, key, launch) -> None:
+        """Capture `launch` into a CUDA graph on first use of `key`, then replay.
+        Kernel nodes per graph are counted (graph_launches) for telemetry."""
+        ent = self._graphs.get(key)
+        if ent is None:
+            g = torch.cuda.CUDAGraph()
+            torch.cuda.synchronize()
+            l0 = self.lib.ss_launch_count()
+            with torch.cuda.graph(g):
+                launch()
+            ent = (g, self.lib.ss_launch_count() - l0)
+            self._graphs[key] = ent
+        ent[0].replay()
+        self.graph_launches += ent[1]
+
+    def _iterate_eager(self, view, grad_scale, adam, staged, target):
         cam = self.cam_structs[view]
         if target is not None:
             tgt = ptr(target)
@@ -349,7 +403,7 @@ class Stage1Trainer:
 
     def pairs_of_last(self, k: int) -> np.ndarray:
         """Tile-pair counts of the last k iterations (device history; syncs)."""
-        h, it = self.pair_hist.numel(), int(self.s.iteration)
+        h, it = self.pair_hist.numel(), int(self.iter_dev.item())
         idx = [(it - k + j) % h for j in range(k)]
         return self.pair_hist.cpu().numpy()[idx]
 
@@ -370,6 +424,7 @@ class Stage1Trainer:
             self.s.loss_history = ptr(self.loss_hist)
             self.s.pair_history = ptr(self.pair_hist)
             self.s.history_len = iters
+            self._graphs = {}
         order = view_order(self.cfg.seed, frame_index, len(self.cameras), iters)
         stats_from = max(0, iters - len(self.cameras))
         if self.bins is None:

@@ -345,3 +345,41 @@ def test_run_from_host_matches_resident_targets(P):
     host = [torch.tensor(t, dtype=torch.float32).pin_memory() for t in targets]
     got = b.run_from_host(order, host)
     np.testing.assert_allclose(got, ref, rtol=1e-6)
+
+
+def test_stage1_trajectory_vs_oracle(P):
+    """Ten Stage-1 iterations with Adam (identity-initialised NTC, as bench.py
+    trains) follow the float64 oracle's loss trajectory and parameters."""
+    import torch
+
+    from paper_2403_01444_b200 import scenes
+    from paper_2403_01444_b200.stage1 import Stage1Config, Stage1Trainer
+    from oracle import stage1 as O
+
+    sc = scenes.small_scene(seed=21, n=1500, width=80, height=64, sh_degree=1, n_views=2)
+    tables, mlp = O.init_ntc(sc.grid, output_init="identity", seed=0)
+    moved = scenes.moved_cloud(sc.cloud, np.random.default_rng(7))
+    targets = [O.render(moved, c)[0]["image"] for c in sc.cameras]
+
+    class Cache:
+        grid = P["types"].HashGridConfig.from_any(sc.grid)
+
+    c = Cache()
+    c.tables = tables.copy()
+    c.weights = [w.copy() for w in mlp["weights"]]
+    c.biases = [b.copy() for b in mlp["biases"]]
+    tr = Stage1Trainer(sc.cloud, c, list(zip(sc.cameras, targets)),
+                       Stage1Config(stage1_iterations=10))
+    state = dict(grid=sc.grid, tables=tables.copy(),
+                 mlp=dict(weights=[w.copy() for w in mlp["weights"]],
+                          biases=[b.copy() for b in mlp["biases"]]),
+                 inside=O.inside_mask(sc.grid, sc.cloud["means"]), enc=None)
+    order = [0, 1, 1, 0, 1, 0, 0, 1, 1, 0]
+    ref = [O.stage1_iteration(state, sc.cloud, sc.cameras[v], targets[v])["loss"] for v in order]
+    for v in order:
+        tr.iterate(v)
+    torch.cuda.synchronize()
+    got = tr.loss_hist[:10].cpu().numpy()
+    np.testing.assert_allclose(got, ref, rtol=1e-3)
+    tab = tr.tables.view(state["tables"].shape).cpu().numpy()
+    assert G.norm_rel(tab, state["tables"]) <= 1e-3
