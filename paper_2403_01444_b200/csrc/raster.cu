@@ -488,6 +488,12 @@ __device__ __forceinline__ float ex2_approx(float x) {
   return y;
 }
 
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 // log2 of the Gaussian at (dx, dy) from the per-rank form
 __device__ __forceinline__ float log2_gauss(float4 q, float dx, float dy) {
   return fmaf(fmaf(q.x, dx, q.y * dy), dx, q.z * dy * dy);
@@ -514,9 +520,19 @@ __device__ inline float alpha_from_log2(const BlendParams& bp, float lg, float o
 
 template <int TS>
 struct BlendShape {
-  static constexpr int NT = TS * TS <= 256 ? TS * TS : 256;
+  // 16x16 tiles: 128 threads with two pixels each (rows r and r + 8), which halves
+  // the per-splat shared-memory loads, loop overhead and (backward) warp
+  // reductions per pixel
+  static constexpr int NT = TS == 16 ? 128 : (TS * TS <= 256 ? TS * TS : 256);
   static constexpr int PPT = TS * TS / NT;
 };
+
+// Pixel p of thread t: each warp owns a contiguous run of 32 * PPT pixels of
+// the tile (whole rows).
+template <int TS>
+__device__ __forceinline__ int tile_pixel(int t, int p) {
+  return (t >> 5) * (32 * BlendShape<TS>::PPT) + p * 32 + (t & 31);
+}
 
 template <int TS, bool TOUCH>
 __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_fwd_kernel(
@@ -539,7 +555,7 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_fwd_kernel(
   float lx[PPT], ly[PPT];
 #pragma unroll
   for (int p = 0; p < PPT; ++p) {
-    const int li = threadIdx.x + p * NT;
+    const int li = tile_pixel<TS>(threadIdx.x, p);
     lx[p] = (float)(li % TS);
     ly[p] = (float)(li / TS);
     T[p] = 1.f;
@@ -644,7 +660,7 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_fwd_kernel(
   }
 #pragma unroll
   for (int p = 0; p < PPT; ++p) {
-    const int li = threadIdx.x + p * NT;
+    const int li = tile_pixel<TS>(threadIdx.x, p);
     const int px = x0 + li % TS, py = y0 + li / TS;
     if (px >= bp.W || py >= bp.H) continue;
     const int64_t pix = (int64_t)py * bp.W + px;
@@ -686,7 +702,7 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_bwd_kernel(
   int max_last = 0;
 #pragma unroll
   for (int p = 0; p < PPT; ++p) {
-    const int li = threadIdx.x + p * NT;
+    const int li = tile_pixel<TS>(threadIdx.x, p);
     const int px = x0 + li % TS, py = y0 + li / TS;
     lx[p] = (float)(li % TS);
     ly[p] = (float)(li / TS);
@@ -745,14 +761,16 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_bwd_kernel(
         const float a = alpha_from_log2(bp, lg, col.w, s_rank[k], lx[p] + x0, ly[p] + y0,
                                         g.r_mean, g.r_conop_d, G, og);
         if (a == 0.f) continue;
-        const float oma = 1.f - a;
-        const float tb = T[p] / oma;  // T_before
+        // one approximate reciprocal serves both
+        // T_before = T / (1 - a) and S / (1 - a)
+        const float ioma = rcp_approx(fmaxf(1.f - a, 1e-12f));
+        const float tb = T[p] * ioma;  // T_before
         const float w = a * tb;
         v[0] = fmaf(w, gp[p][0], v[0]);
         v[1] = fmaf(w, gp[p][1], v[1]);
         v[2] = fmaf(w, gp[p][2], v[2]);
         const float u = gp[p][0] * col.x + gp[p][1] * col.y + gp[p][2] * col.z;
-        float da = u * tb - S[p] / fmaxf(oma, 1e-12f);
+        float da = u * tb - S[p] * ioma;
         S[p] = fmaf(u * a, tb, S[p]);
         T[p] = tb;
         if (!(og < bp.clamp)) da = 0.f;  // flat above the clamp (rasterizer.py:336-337)
