@@ -297,7 +297,7 @@ def main():
     names = [lib.ss_profile_name(i).decode() for i in range(nph)]
     phase_ms = {n: [] for n in names}
     buf = (np.ctypeslib.ctypes.c_double * nph)()
-    for k in range(min(a.steps, 10)):
+    for k in range(a.steps):  # the whole frame window, like the timed steps
         flush.fill_(k & 0xFF)
         tr.step(batch(k))
         torch.cuda.synchronize()
