@@ -389,12 +389,33 @@ def main():
     # ---- render-only throughput (config 2) and the CPU baseline: rank 0, N = 1
     if rank == 0 and world == 1 and not a.no_render:
         line["render"] = render_fps(a)
+        line["warmup"] = warmup_rate(sc, cache)
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline_sample(sc, cache, targets[0])
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def warmup_rate(sc, cache):
+    """NTC warm-up iterations/s (ntc.py:296-333) on the cfg1
+    initial means, 65536-point batches, host sampling included."""
+    import copy
+
+    from paper_2403_01444_b200.warmup import warmup_train
+
+    means = sc.cloud["means"]
+    warmup_train(copy.deepcopy(cache), means, 0.05, 3)
+    t0 = time.perf_counter()
+    n = 20
+    _, hist = warmup_train(copy.deepcopy(cache), means, 0.05, n)
+    dt = time.perf_counter() - t0
+    return {"metric": "ntc_warmup_iters_per_s", "value": n / dt, "unit": "iter/s",
+            "batch": 65536, "loss_first_last": [hist[0], hist[-1]],
+            "workload": "warmup_train on the 250k cfg1 means, noise 0.05, wall clock incl. "
+                        "numpy batch sampling (Generator.choice without replacement), H2D, "
+                        "device step and the final D2H"}
 
 
 def render_fps(a):

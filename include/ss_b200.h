@@ -260,6 +260,19 @@ int ss_render_loss(const float* image, const float* target, int32_t height, int3
                    int32_t channels, double lam, double c1, double c2, void* scratch,
                    double* loss_dev, float* d_image, uint32_t* status, void* stream);
 
+/* NTC warm-up (ntc.py:296-333, losses.py:151-180): one Adam
+ * step of warmup_train on a device batch of n points (n, 3) fp32: touched rows
+ * of the batch, decoder forward, identity-pull loss (the batch SUM of the
+ * per-row terms lands in *loss_sum; the reference's loss is *loss_sum / n),
+ * decoder backward + table scatter, lazy Adam (beta 0.9/0.999, eps 1e-15).
+ * scratch: ss_ntc_warmup_bytes(n) bytes. */
+size_t ss_ntc_warmup_bytes(int64_t n);
+int ss_ntc_warmup_step(const ss_grid* grid, const ss_mlp* mlp, int64_t n, const float* batch,
+                       float* tables, float* params, float* g_tables, float* g_params,
+                       double* m_tables, double* v_tables, double* m_params, double* v_params,
+                       uint8_t* row_mask, int32_t* step_dev, double lr, void* scratch,
+                       double* loss_sum, uint32_t* status, void* stream);
+
 /* ------------------------------------------------------------------ */
 /* fused Stage-1 iteration (pipeline.py:262-277)                       */
 /* ------------------------------------------------------------------ */

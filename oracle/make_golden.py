@@ -211,16 +211,62 @@ def gen_stage1(R):
                         **{f"after2_{k}": v for k, v in cache.get_params().items()})
 
 
+def gen_ntc_blob(R):
+    """streamio.serialize_ntc bytes of a seeded cache."""
+    import sys
+
+    sys.path.insert(0, rb.REF_SRC)
+    from splatstream import streamio
+
+    rng = np.random.default_rng(303)
+    grid = dict(levels=4, features=2, log2_table=9, base=4, growth=1.5,
+                lo=(-1.5, -1.0, -0.75), hi=(1.25, 1.0, 2.0))
+    tables, mlp = _rand_ntc(grid, 64, seed=9)
+    tables = scenes.f32(rng.uniform(-0.5, 0.5, size=tables.shape))
+    cache = rb.ref_cache(R, grid, tables, mlp)
+    blob = streamio.serialize_ntc(cache)
+    np.savez_compressed(os.path.join(OUT, "ntc_blob.npz"), blob=np.frombuffer(blob, np.uint8),
+                        tables=tables, **_grid_arr(grid),
+                        **{f"mlp_w{i}": w for i, w in enumerate(mlp["weights"])},
+                        **{f"mlp_b{i}": b for i, b in enumerate(mlp["biases"])})
+
+
+def gen_warmup(R):
+    """losses.warmup_loss on random outputs and ntc.warmup_train on a small
+    cache."""
+    rng = np.random.default_rng(404)
+    d_mu = rng.normal(scale=0.05, size=(300, 3))
+    d_q = rng.normal(size=(300, 4))
+    loss, g_mu, g_q = R["losses"].warmup_loss(d_mu, d_q)
+    grid = dict(levels=4, features=2, log2_table=10, base=4, growth=1.5,
+                lo=(-1.0, -1.0, -1.0), hi=(1.0, 1.0, 1.0))
+    tables, mlp = _rand_ntc(grid, 64, seed=11)
+    tables = scenes.f32(rng.uniform(-0.2, 0.2, size=tables.shape))
+    cache = rb.ref_cache(R, grid, tables, mlp)
+    means = scenes.f32(rng.uniform(-0.8, 0.8, size=(400, 3)))
+    params, hist = R["ntc"].warmup_train(cache, means, noise_sigma=0.05, iterations=5,
+                                         lr=0.002, batch_size=256, seed=7)
+    np.savez_compressed(os.path.join(OUT, "warmup.npz"), d_mu=d_mu, d_q=d_q, loss=loss,
+                        g_mu=g_mu, g_q=g_q, tables=tables, means=means, history=np.array(hist),
+                        **_grid_arr(grid),
+                        **{f"mlp_w{i}": w for i, w in enumerate(mlp["weights"])},
+                        **{f"mlp_b{i}": b for i, b in enumerate(mlp["biases"])},
+                        **{f"after_{k}": v for k, v in params.items()})
+
+
+GENERATORS = dict(encode=gen_encode, ntc=gen_ntc, transform=gen_transform, raster=gen_raster,
+                  loss=gen_loss, stage1=gen_stage1, ntc_blob=gen_ntc_blob, warmup=gen_warmup)
+
+
 def main():
+    import sys
+
     os.makedirs(OUT, exist_ok=True)
     R = rb.load()
+    which = sys.argv[1:] or list(GENERATORS)
     with threadpool_limits(1):
-        gen_encode(R)
-        gen_ntc(R)
-        gen_transform(R)
-        gen_raster(R)
-        gen_loss(R)
-        gen_stage1(R)
+        for name in which:
+            GENERATORS[name](R)
     for f in sorted(os.listdir(OUT)):
         print(f, os.path.getsize(os.path.join(OUT, f)))
 

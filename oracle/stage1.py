@@ -832,3 +832,50 @@ def stage1_view_order(seed, frame_index, n_views, iterations):
         if (t + 1) % n_views == 0:
             order = rng.permutation(n_views)
     return seq
+
+
+# ---------------------------------------------------------------- NTC warm-up (F2)
+def warmup_loss(d_mu, d_q):
+    """Identity-pull loss, mean over the batch; losses.py:151-180.
+    Per row |d_mu|_1 - cos^2(angle(norm(d_q), identity)); returns (loss, g_mu, g_q)."""
+    d_mu = np.asarray(d_mu, dtype=np.float64)
+    d_q = np.asarray(d_q, dtype=np.float64)
+    b = d_mu.shape[0]
+    n2 = np.sum(d_q * d_q, axis=1)
+    if np.any(n2 < 1e-24):
+        raise OracleNumericalError("zero-norm d_q in warmup_loss")
+    w = d_q[:, 0]
+    loss = float(np.mean(np.sum(np.abs(d_mu), axis=1) - w * w / n2))
+    g_mu = np.sign(d_mu) / b
+    g_q = (-2.0 * (w * w)[:, None] * d_q) / (n2 ** 2)[:, None]
+    g_q[:, 0] = 2.0 * w * (n2 - w * w) / n2 ** 2
+    return loss, g_mu, -g_q / b
+
+
+def warmup_train(grid, tables, mlp, initial_means, noise_sigma, iterations, lr=0.002,
+                 batch_size=65536, seed=0):
+    """ntc.py:296-333: Adam on batches of the initial means plus Gaussian jitter
+    (clamped to the AABB), touched rows = the batch's corners; returns the
+    float32-quantised (tables, mlp) and the loss history."""
+    means = np.asarray(initial_means, dtype=np.float64).reshape(-1, 3)
+    rng = np.random.default_rng(seed)
+    lo, hi = np.asarray(grid["lo"]), np.asarray(grid["hi"])
+    state = dict(grid=grid, tables=np.array(tables, dtype=np.float64),
+                 mlp=dict(weights=[np.array(w, dtype=np.float64) for w in mlp["weights"]],
+                          biases=[np.array(b, dtype=np.float64) for b in mlp["biases"]]))
+    hist = []
+    for _ in range(iterations):
+        take = min(batch_size, len(means))
+        sel = rng.choice(len(means), size=take, replace=False)
+        batch = np.clip(means[sel] + rng.normal(scale=noise_sigma, size=(take, 3)), lo, hi)
+        idx, w, touched = encode(grid, batch)
+        feats = gather(state["tables"], idx, w)
+        out7, hidden = mlp_forward(state["mlp"], feats)
+        loss, g_mu, g_q = warmup_loss(out7[:, :3], out7[:, 3:])
+        hist.append(loss)
+        gw, gb, gf = mlp_backward(state["mlp"], feats, hidden, np.concatenate([g_mu, g_q], 1))
+        state["enc"] = (idx, w, touched)
+        adam_apply(state, table_scatter(state["tables"].shape, idx, w, gf), gw, gb, lr)
+    q = lambda a: a.astype(np.float32).astype(np.float64)  # noqa: E731
+    return (q(state["tables"]), dict(weights=[q(a) for a in state["mlp"]["weights"]],
+                                     biases=[q(a) for a in state["mlp"]["biases"]]), hist)

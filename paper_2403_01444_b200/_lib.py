@@ -119,6 +119,9 @@ SIGNATURES = [
     ("ss_tile_bin_finish", I32, [I64, PCam, PSet, P, P, I64, P, P, P]),
     ("ss_loss_bytes", SZ, [I32, I32, I32]),
     ("ss_render_loss", I32, [P, P, I32, I32, I32, D, D, D, P, P, P, P, P]),
+    ("ss_ntc_warmup_bytes", SZ, [I64]),
+    ("ss_ntc_warmup_step", I32, [PGrid, PMlp, I64, P, P, P, P, P, P, P, P, P, P, P, D, P, P, P,
+                                 P]),
     ("ss_stage1_frame_begin", I32, [C.POINTER(Stage1), P]),
     ("ss_stage1_iter_begin", I32, [C.POINTER(Stage1), PCam, P, P]),
     ("ss_stage1_iter_finish", I32, [C.POINTER(Stage1), PCam, P, I64, P]),

@@ -1069,6 +1069,46 @@ int transform_vjp_run(const ss_cloud* src, int64_t n, const int32_t* rows, const
   return SS_OK;
 }
 
+// F2 warm-up loss (losses.py:151-180): per row |d_mu|_1 - w^2 / |d_q|^2, summed
+// in fp64; gradients of the batch mean written to g7 (n, 8)
+__global__ void __launch_bounds__(256) warmup_loss_kernel(int64_t n, const float* __restrict__ out7,
+                                                          float* __restrict__ g7,
+                                                          double* __restrict__ loss_sum,
+                                                          uint32_t* status) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  double term = 0.0;
+  if (i < n) {
+    const float4 a = *reinterpret_cast<const float4*>(out7 + 8 * i);
+    const float4 b = *reinterpret_cast<const float4*>(out7 + 8 * i + 4);
+    const double mu[3] = {a.x, a.y, a.z}, q[4] = {a.w, b.x, b.y, b.z};
+    const double n2 = q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3];
+    if (n2 < 1e-24 && status) atomicOr(status, SS_FLAG_ZERO_QUAT);
+    const double w = q[0], inv_b = 1.0 / (double)n, in4 = 1.0 / (n2 * n2);
+    term = fabs(mu[0]) + fabs(mu[1]) + fabs(mu[2]) - w * w / n2;
+    auto sgn = [](double v) { return (double)((v > 0.0) - (v < 0.0)); };
+    float4 ga, gb;
+    ga.x = (float)(sgn(mu[0]) * inv_b);
+    ga.y = (float)(sgn(mu[1]) * inv_b);
+    ga.z = (float)(sgn(mu[2]) * inv_b);
+    ga.w = (float)(-2.0 * w * (n2 - w * w) * in4 * inv_b);
+    gb.x = (float)(2.0 * w * w * q[1] * in4 * inv_b);
+    gb.y = (float)(2.0 * w * w * q[2] * in4 * inv_b);
+    gb.z = (float)(2.0 * w * w * q[3] * in4 * inv_b);
+    gb.w = 0.f;
+    *reinterpret_cast<float4*>(g7 + 8 * i) = ga;
+    *reinterpret_cast<float4*>(g7 + 8 * i + 4) = gb;
+  }
+  __shared__ double red[8];
+  for (int o = 16; o > 0; o >>= 1) term += __shfl_xor_sync(0xffffffffu, term, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = term;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) t += red[k];
+    atomicAdd(loss_sum, t);
+  }
+}
+
 // stream-ordered temporary for the reference-shaped API entry points
 struct Temp {
   void* p = nullptr;
@@ -1250,6 +1290,38 @@ int ss_adam_step(int64_t n_table, float* tables, float* g_tables, double* m_tabl
   increment_kernel<<<1, 1, 0, st>>>(step_dev);
   SS_CHECK_LAUNCH("increment_kernel");
   return SS_OK;
+}
+
+size_t ss_ntc_warmup_bytes(int64_t n) { return ntc_scratch_bytes(nullptr, n); }
+
+int ss_ntc_warmup_step(const ss_grid* grid, const ss_mlp* mlp, int64_t n, const float* batch,
+                       float* tables, float* params, float* g_tables, float* g_params,
+                       double* m_tables, double* v_tables, double* m_params, double* v_params,
+                       uint8_t* row_mask, int32_t* step_dev, double lr, void* scratch,
+                       double* loss_sum, uint32_t* status, void* stream) {
+  SS_TRY(check_grid(grid, mlp));
+  if (n <= 0 || !batch || !scratch || !loss_sum || !row_mask || !step_dev) {
+    set_error("ss_ntc_warmup_step: empty batch or missing buffers");  // losses.py:167-168
+    return SS_ERR_DATA;
+  }
+  cudaStream_t st = as_stream(stream);
+  const int64_t T = (int64_t)1 << grid->log2_table;
+  // touched rows = the batch's corners (ntc.py:187, :330)
+  SS_CUDA(cudaMemsetAsync(row_mask, 0, (size_t)grid->n_levels * T, st));
+  SS_TRY(ss_ntc_touched(grid, n, batch, nullptr, row_mask, stream));
+  NtcScratch s = ntc_scratch(scratch, mlp, n);
+  SS_TRY(ntc_forward_run(grid, mlp, n, batch, nullptr, tables, params, s.X, s.xs, s.out7, 8,
+                         s.relu, status, st));
+  SS_CUDA(cudaMemsetAsync(loss_sum, 0, sizeof(double), st));
+  warmup_loss_kernel<<<(unsigned)cdiv(n, 256), 256, 0, st>>>(n, s.out7, s.g7, loss_sum, status);
+  SS_CHECK_LAUNCH("warmup_loss_kernel");
+  SS_TRY(ntc_backward_run(grid, mlp, n, batch, nullptr, params, s.X, s.xs, s.g7, 8, s.relu, s.dX,
+                          g_tables, g_params, st));
+  ss_mlp_layout L{};
+  SS_TRY(ss_mlp_get_layout(mlp, &L));
+  return ss_adam_step((int64_t)grid->n_levels * T * grid->n_features, tables, g_tables, m_tables,
+                      v_tables, row_mask, grid->n_features, L.total, params, g_params, m_params,
+                      v_params, step_dev, lr, 0.9, 0.999, 1e-15, 1, stream);
 }
 
 }  // extern "C"

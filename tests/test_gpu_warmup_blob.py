@@ -1,0 +1,78 @@
+"""GPU tests of the §8(f) rows F2 (device NTC warm-up) and F4 (blob straight
+from device parameters) against the reference's golden runs."""
+
+import numpy as np
+import pytest
+
+import golden_io as G
+
+pytestmark = pytest.mark.gpu
+
+
+def _cache_from(d):
+    from paper_2403_01444_b200.ntc import NeuralTransformationCache
+    from paper_2403_01444_b200.types import HashGridConfig
+
+    g = G.grid(d)
+    grid = HashGridConfig(n_levels=g["levels"], n_features=g["features"],
+                          table_size_log2=g["log2_table"], base_resolution=g["base"],
+                          growth_factor=g["growth"], aabb_min=g["lo"], aabb_max=g["hi"])
+    cache = NeuralTransformationCache(grid, output_init="random")
+    m = G.mlp(d)
+    cache.tables[:] = d["tables"]
+    for i in range(len(m["weights"])):
+        cache.weights[i][:] = m["weights"][i]
+        cache.biases[i][:] = m["biases"][i]
+    return cache
+
+
+def test_device_warmup_matches_reference():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2403_01444_b200.warmup import warmup_train
+
+    d = G.load("warmup")
+    cache = _cache_from(d)
+    before = cache.get_params()
+    params, hist = warmup_train(cache, d["means"], noise_sigma=0.05, iterations=5, lr=0.002,
+                                batch_size=256, seed=7)
+    np.testing.assert_allclose(hist, d["history"], rtol=1e-5)
+    for k, v in params.items():
+        ref = d[f"after_{k}"]
+        delta_ref = ref - before[k]
+        if np.linalg.norm(delta_ref) > 0:
+            assert G.norm_rel(v - before[k], delta_ref) <= 5e-3, k
+    # the cache holds the float32 snapshot
+    np.testing.assert_array_equal(cache.tables[0], params["table_0"])
+    np.testing.assert_array_equal(cache.tables, cache.tables.astype(np.float32))
+
+
+def test_device_warmup_rejects_empty():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2403_01444_b200.errors import DataError
+    from paper_2403_01444_b200.warmup import warmup_train
+
+    d = G.load("warmup")
+    with pytest.raises(DataError):
+        warmup_train(_cache_from(d), np.zeros((0, 3)), 0.05, 1)
+
+
+def test_blob_from_device_params_matches_reference():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2403_01444_b200 import scenes, streamio
+    from paper_2403_01444_b200.stage1 import Stage1Config, Stage1Trainer
+
+    d = G.load("ntc_blob")
+    cache = _cache_from(d)
+    sc = scenes.small_scene(seed=5, n=300, width=48, height=40, sh_degree=0, n_views=1)
+    lo, hi = np.array(cache.grid.aabb_min), np.array(cache.grid.aabb_max)
+    cloud = dict(sc.cloud)
+    cloud["means"] = scenes.f32(np.clip(cloud["means"] * 0.2, lo + 0.01, hi - 0.01))
+    views = [(sc.cameras[0], np.zeros((40, 48, 3)))]
+    tr = Stage1Trainer(cloud, cache, views, Stage1Config())
+    assert streamio.serialize_ntc_device(tr) == d["blob"].tobytes()
