@@ -254,8 +254,45 @@ def gen_warmup(R):
                         **{f"after_{k}": v for k, v in params.items()})
 
 
+def gen_playback(R):
+    """pipeline.materialize_frame / playback_render on a constructed stream
+    (SURVEY.md §8 F3): an initial cloud, three frame records (NTC blob + added
+    Gaussians), frames 0..3 rendered from one camera."""
+    import sys
+
+    sys.path.insert(0, rb.REF_SRC)
+    from splatstream import pipeline, streamio
+
+    rng = np.random.default_rng(505)
+    sc = scenes.small_scene(seed=55, n=600, width=72, height=56, sh_degree=1, n_views=1)
+    grid = sc.grid
+    records, arrs = [], {}
+    for f in range(3):
+        tables, mlp = _rand_ntc(grid, 64, seed=20 + f)
+        tables = scenes.f32(rng.uniform(-0.02, 0.02, size=tables.shape))
+        mlp["weights"][-1] = scenes.f32(mlp["weights"][-1] * 0.05)
+        b = np.zeros(7)
+        b[:3] = rng.normal(scale=0.02, size=3)
+        b[3:] = [1.0, 0.0, 0.0, 0.0]
+        b[3:] += rng.normal(scale=0.05, size=4)
+        mlp["biases"][-1] = scenes.f32(b)
+        blob = streamio.serialize_ntc(rb.ref_cache(R, grid, tables, mlp))
+        add = scenes.small_scene(seed=60 + f, n=40, width=8, height=8, sh_degree=1,
+                                 n_views=1).cloud
+        records.append(streamio.FrameRecord(f + 1, blob, rb.ref_cloud(R, add)))
+        arrs[f"blob{f}"] = np.frombuffer(blob, np.uint8)
+        arrs.update({f"add{f}_{k}": v for k, v in add.items()})
+    bg = [0.1, 0.2, 0.3]
+    stream = streamio.StreamData({"background": bg}, rb.ref_cloud(R, sc.cloud), b"", records)
+    cam = rb.ref_camera(R, sc.cameras[0])
+    for i in range(4):
+        arrs[f"image{i}"] = pipeline.playback_render(stream, i, cam)
+    np.savez_compressed(os.path.join(OUT, "playback.npz"), **_cloud_arr(sc.cloud),
+                        **_cam_arr(sc.cameras[0]), background=np.array(bg), **arrs)
+
+
 GENERATORS = dict(encode=gen_encode, ntc=gen_ntc, transform=gen_transform, raster=gen_raster,
-                  loss=gen_loss, stage1=gen_stage1, ntc_blob=gen_ntc_blob, warmup=gen_warmup)
+                  loss=gen_loss, stage1=gen_stage1, ntc_blob=gen_ntc_blob, warmup=gen_warmup, playback=gen_playback)
 
 
 def main():

@@ -76,3 +76,43 @@ def test_blob_from_device_params_matches_reference():
     views = [(sc.cameras[0], np.zeros((40, 48, 3)))]
     tr = Stage1Trainer(cloud, cache, views, Stage1Config())
     assert streamio.serialize_ntc_device(tr) == d["blob"].tobytes()
+
+
+class _Rec:
+    def __init__(self, blob, add):
+        self.ntc_blob, self.additional = blob, add
+
+
+class _Stream:
+    def __init__(self, d):
+        self.header = {"background": list(d["background"])}
+        self.initial_cloud = G.cloud(d)
+        self.records = [_Rec(d[f"blob{f}"].tobytes(), G.cloud(d, f"add{f}_")) for f in range(3)]
+
+    @property
+    def n_frames(self):
+        return len(self.records) + 1
+
+
+def test_device_playback_matches_reference():
+    """materialize_frame + playback_render of a 3-record stream
+    (NTC folding, added Gaussians, background) against the reference's renders."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2403_01444_b200 import playback
+    from paper_2403_01444_b200.errors import DataError
+
+    d = G.load("playback")
+    st = _Stream(d)
+    cam = G.camera(d)
+    for i in range(4):
+        img = playback.playback_render(st, i, cam)
+        assert np.abs(img - d[f"image{i}"]).max() <= 1e-4, i
+    player = playback.DevicePlayer(st)
+    for i in [0, 1, 2, 3, 1]:  # sequential folding, then a seek backwards
+        img = player.render(i, cam).cpu().numpy()
+        assert np.abs(img - d[f"image{i}"]).max() <= 1e-4, i
+    assert playback.materialize_frame(st, 2).means.shape[0] == len(d["cloud_means"]) + 40
+    with pytest.raises(DataError):
+        playback.playback_render(st, 4, cam)
