@@ -587,24 +587,38 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_fwd_kernel(
       int contrib = 0;
       if (!TOUCH) {  // fast path: reject on the log2 form before the exponential
         const float4 q = s_q[k];
+        float lgs[PPT];
+        bool live[PPT], any_live = false;
 #pragma unroll
         for (int p = 0; p < PPT; ++p) {
-          if (done[p]) continue;
-          const float dx = lx[p] - xy.x, dy = ly[p] - xy.y;
-          const float lg = log2_gauss(q, dx, dy);
-          if (lg < q.w) continue;
-          const float4 col = s_col[k];
-          float G, og;
-          const float a = alpha_from_log2(bp, lg, col.w, s_rank[k], lx[p] + x0, ly[p] + y0,
-                                          g.r_mean, g.r_conop_d, G, og);
-          if (a == 0.f) continue;
-          const float w = a * T[p];
-          C[p][0] = fmaf(w, col.x, C[p][0]);
-          C[p][1] = fmaf(w, col.y, C[p][1]);
-          C[p][2] = fmaf(w, col.z, C[p][2]);
+          lgs[p] = log2_gauss(q, lx[p] - xy.x, ly[p] - xy.y);
+          live[p] = !done[p] && !(lgs[p] < q.w);
+          any_live |= live[p];
+        }
+        if (!__any_sync(0xffffffffu, any_live)) continue;  // warp-uniform skip
+        const float4 col = s_col[k];
+#pragma unroll
+        for (int p = 0; p < PPT; ++p) {  // predicated: a = 0 leaves the pixel unchanged
+          const float G = ex2_approx(lgs[p]);
+          float a = fminf(bp.clamp, col.w * G);
+          if (fabsf(a - bp.skip) <= 1e-4f * bp.skip) {  // rare: decide in float64
+            const double2 m = g.r_mean[s_rank[k]];
+            const double4 c = g.r_conop_d[s_rank[k]];
+            const double ddx = (double)(lx[p] + x0) - m.x, ddy = (double)(ly[p] + y0) - m.y;
+            const double mh = c.x * ddx * ddx + c.y * ddx * ddy + c.z * ddy * ddy;
+            const double ad = fmin(bp.clamp_d, c.w * exp(-0.5 * mh));
+            a = ad < bp.skip_d ? 0.f : fmaxf((float)ad, bp.skip);
+          } else {
+            a = a < bp.skip ? 0.f : a;
+          }
+          a = live[p] ? a : 0.f;
+          const float wgt = a * T[p];
+          C[p][0] = fmaf(wgt, col.x, C[p][0]);
+          C[p][1] = fmaf(wgt, col.y, C[p][1]);
+          C[p][2] = fmaf(wgt, col.z, C[p][2]);
           T[p] *= 1.f - a;
-          last[p] = b - range.x + k + 1;
-          if (T[p] < bp.stop) done[p] = true;  // later splats fail T_before >= stop
+          last[p] = a > 0.f ? b - range.x + k + 1 : last[p];
+          done[p] = done[p] || T[p] < bp.stop;  // later splats fail T_before >= stop
         }
         continue;
       }
@@ -746,25 +760,45 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_bwd_kernel(
     for (int k = 0; k < cnt; ++k) {
       const int pos_rel = end - 1 - k - range.x;
       const float2 xy = s_xy[k];
+      const float4 q = s_q[k];
+      // cheap part for every pixel, then a warp-uniform skip; the rest is
+      // predicated (a = 0 makes every update a no-op) instead of branching
+      float dxs[PPT], dys[PPT], lgs[PPT];
+      bool live[PPT], any_live = false;
+#pragma unroll
+      for (int p = 0; p < PPT; ++p) {
+        dxs[p] = lx[p] - xy.x;
+        dys[p] = ly[p] - xy.y;
+        lgs[p] = log2_gauss(q, dxs[p], dys[p]);  // same decisions as the forward
+        live[p] = pos_rel < last[p] && !(lgs[p] < q.w);
+        any_live |= live[p];
+      }
+      if (!__any_sync(0xffffffffu, any_live)) continue;
+      const float4 col = s_col[k];
       const float4 co = s_co[k];
+      // d(maha)/d(mean2d) and conic coefficients: mean grads += (-2C d) dm
+      const float k1 = -2.f * co.x, k2 = -co.y, k3 = -2.f * co.z;
       float v[NA] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
       bool any = false;
 #pragma unroll
       for (int p = 0; p < PPT; ++p) {
-        if (pos_rel >= last[p]) continue;
-        const float dx = lx[p] - xy.x, dy = ly[p] - xy.y;
-        const float4 q = s_q[k];
-        const float lg = log2_gauss(q, dx, dy);  // same decisions as the forward
-        if (lg < q.w) continue;
-        const float4 col = s_col[k];
-        float G, og;
-        const float a = alpha_from_log2(bp, lg, col.w, s_rank[k], lx[p] + x0, ly[p] + y0,
-                                        g.r_mean, g.r_conop_d, G, og);
-        if (a == 0.f) continue;
-        // one approximate reciprocal serves both
-        // T_before = T / (1 - a) and S / (1 - a)
+        const float G = ex2_approx(lgs[p]);
+        const float og = col.w * G;
+        float a = fminf(bp.clamp, og);
+        if (fabsf(a - bp.skip) <= 1e-4f * bp.skip) {  // rare: decide in float64
+          const double2 m = g.r_mean[s_rank[k]];
+          const double4 c = g.r_conop_d[s_rank[k]];
+          const double ddx = (double)(lx[p] + x0) - m.x, ddy = (double)(ly[p] + y0) - m.y;
+          const double mh = c.x * ddx * ddx + c.y * ddx * ddy + c.z * ddy * ddy;
+          const double ad = fmin(bp.clamp_d, c.w * exp(-0.5 * mh));
+          a = ad < bp.skip_d ? 0.f : fmaxf((float)ad, bp.skip);
+        } else {
+          a = a < bp.skip ? 0.f : a;
+        }
+        a = live[p] ? a : 0.f;
+        // one approximate reciprocal serves T_before = T / (1 - a) and S / (1 - a)
         const float ioma = rcp_approx(fmaxf(1.f - a, 1e-12f));
-        const float tb = T[p] * ioma;  // T_before
+        const float tb = T[p] * ioma;
         const float w = a * tb;
         v[0] = fmaf(w, gp[p][0], v[0]);
         v[1] = fmaf(w, gp[p][1], v[1]);
@@ -773,16 +807,17 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_bwd_kernel(
         float da = u * tb - S[p] * ioma;
         S[p] = fmaf(u * a, tb, S[p]);
         T[p] = tb;
-        if (!(og < bp.clamp)) da = 0.f;  // flat above the clamp (rasterizer.py:336-337)
-        const float dm = -0.5f * G * co.w * da;
-        const float c01 = 0.5f * co.y;
-        v[3] -= 2.f * dm * (co.x * dx + c01 * dy);
-        v[4] -= 2.f * dm * (c01 * dx + co.z * dy);
-        v[5] = fmaf(dm, dx * dx, v[5]);
-        v[6] = fmaf(dm, dx * dy, v[6]);
-        v[7] = fmaf(dm, dy * dy, v[7]);
+        // no contribution, or flat above the clamp (rasterizer.py:336-337)
+        da = (a > 0.f && og < bp.clamp) ? da : 0.f;
+        const float dm = -0.5f * og * da;
+        const float e = dm * dxs[p], f = dm * dys[p];
+        v[3] = fmaf(k1, e, fmaf(k2, f, v[3]));
+        v[4] = fmaf(k2, e, fmaf(k3, f, v[4]));
+        v[5] = fmaf(e, dxs[p], v[5]);
+        v[6] = fmaf(e, dys[p], v[6]);
+        v[7] = fmaf(f, dys[p], v[7]);
         if (FULL) v[8] = fmaf(da, G, v[8]);
-        any = true;
+        any |= a > 0.f;
       }
       const unsigned bal = __ballot_sync(0xffffffffu, any);
       if (bal) {

@@ -257,7 +257,8 @@ def test_stage1_no_sync_matches_synchronised_path(P):
     b.iterate(0, adam=False)
     torch.cuda.synchronize()
     assert torch.equal(a.image, b.image)
-    assert a.last_loss() == b.last_loss()
+    # the loss sums are fp64 atomics: equal up to their accumulation order
+    assert abs(a.last_loss() - b.last_loss()) <= 1e-12 * abs(a.last_loss())
     assert int(b.pairs_of_last(1)[0]) == p0
     a.apply_adam()
     b.apply_adam()
