@@ -181,146 +181,62 @@ __device__ inline void band_vjp(float x, float y, float z, const float* gv, floa
   sh_basis_vjp<float>(B == 5 ? 2 : 3, x, y, z, gb, g);
 }
 
-// M = S^{-1} E with E[k][b] = Y_b(R^T d_k); sample dirs / S^{-1} in c_shrot.
-template <int B>
-__device__ inline void band_matrix(const float R[3][3], float M[B][B]) {
-  const float(*dirs)[3] = B == 5 ? c_shrot.dirs2 : c_shrot.dirs3;
-  const float* sinv = B == 5 ? &c_shrot.binvT2[0][0] : &c_shrot.binvT3[0][0];
-  float E[B][B];
-#pragma unroll
-  for (int k = 0; k < B; ++k) {
-    float e[3];
-#pragma unroll
-    for (int i = 0; i < 3; ++i)
-      e[i] = R[0][i] * dirs[k][0] + R[1][i] * dirs[k][1] + R[2][i] * dirs[k][2];
-    band_vals<B>(e[0], e[1], e[2], E[k]);
-  }
-#pragma unroll
-  for (int a = 0; a < B; ++a)
-#pragma unroll
-    for (int b = 0; b < B; ++b) {
-      float s = 0.f;
-#pragma unroll
-      for (int k = 0; k < B; ++k) s = fmaf(sinv[a * B + k], E[k][b], s);
-      M[a][b] = s;
-    }
-}
-
-// g_R += d(sum g_M . M)/dR for M = S^{-1} E(R)
-template <int B>
-__device__ inline void band_matrix_vjp(const float R[3][3], const float gM[B][B],
-                                       float gR[3][3]) {
-  const float(*dirs)[3] = B == 5 ? c_shrot.dirs2 : c_shrot.dirs3;
-  const float* sinv = B == 5 ? &c_shrot.binvT2[0][0] : &c_shrot.binvT3[0][0];
-#pragma unroll
-  for (int k = 0; k < B; ++k) {
-    float e[3];
-#pragma unroll
-    for (int i = 0; i < 3; ++i)
-      e[i] = R[0][i] * dirs[k][0] + R[1][i] * dirs[k][1] + R[2][i] * dirs[k][2];
-    float gE[B];
-#pragma unroll
-    for (int b = 0; b < B; ++b) {
-      float s = 0.f;
-#pragma unroll
-      for (int a = 0; a < B; ++a) s = fmaf(sinv[a * B + k], gM[a][b], s);
-      gE[b] = s;
-    }
-    float ge[3] = {0.f, 0.f, 0.f};
-    band_vjp<B>(e[0], e[1], e[2], gE, ge);
-    // e_i = sum_j R_ji d_j  ->  dL/dR_ji += d_j ge_i
-#pragma unroll
-    for (int j = 0; j < 3; ++j)
-#pragma unroll
-      for (int i = 0; i < 3; ++i) gR[j][i] = fmaf(dirs[k][j], ge[i], gR[j][i]);
-  }
-}
-
 __device__ __constant__ int c_perm[3] = {1, 2, 0};  // (y, z, x) basis order, sh.py:30-32
 
-// sh_out bands 1..DEG = M_l(R) sh_in (transform.py:80-84; band 1 = P R P^T).
-// Coefficient arrays are (K, 3) with compile-time K so they stay in registers.
-template <int DEG>
-__device__ inline void rotate_sh_bands(const float R[3][3], const float* in, float* out) {
-  if (DEG >= 1) {
+// One colour channel of bands l >= 2 (4 lanes per Gaussian, see
+// transform_kernel): out = S^{-1} y with y_k = f(R^T d_k), f the band-l SH
+// function whose coefficients are `in` -- the same M = S^{-1} E(R) as
+// band_matrix without forming M.
+template <int B>
+__device__ inline void rotate_band_channel(const float R[3][3], const float* in, float* out) {
+  const float(*dirs)[3] = B == 5 ? c_shrot.dirs2 : c_shrot.dirs3;
+  const float* sinv = B == 5 ? &c_shrot.binvT2[0][0] : &c_shrot.binvT3[0][0];
+  float y[B];
 #pragma unroll
-    for (int a = 0; a < 3; ++a)
+  for (int k = 0; k < B; ++k) {
+    float e[3], v[B];
 #pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        float s = 0.f;
+    for (int i = 0; i < 3; ++i)
+      e[i] = R[0][i] * dirs[k][0] + R[1][i] * dirs[k][1] + R[2][i] * dirs[k][2];
+    band_vals<B>(e[0], e[1], e[2], v);
+    float sum = 0.f;
 #pragma unroll
-        for (int b = 0; b < 3; ++b) s = fmaf(R[c_perm[a]][c_perm[b]], in[(1 + b) * 3 + c], s);
-        out[(1 + a) * 3 + c] = s;
-      }
+    for (int b = 0; b < B; ++b) sum = fmaf(v[b], in[b], sum);
+    y[k] = sum;
   }
-  if (DEG >= 2) {
-    float M[5][5];
-    band_matrix<5>(R, M);
 #pragma unroll
-    for (int a = 0; a < 5; ++a)
+  for (int a = 0; a < B; ++a) {
+    float sum = 0.f;
 #pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        float s = 0.f;
-#pragma unroll
-        for (int b = 0; b < 5; ++b) s = fmaf(M[a][b], in[(4 + b) * 3 + c], s);
-        out[(4 + a) * 3 + c] = s;
-      }
-  }
-  if (DEG >= 3) {
-    float M[7][7];
-    band_matrix<7>(R, M);
-#pragma unroll
-    for (int a = 0; a < 7; ++a)
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        float s = 0.f;
-#pragma unroll
-        for (int b = 0; b < 7; ++b) s = fmaf(M[a][b], in[(9 + b) * 3 + c], s);
-        out[(9 + a) * 3 + c] = s;
-      }
+    for (int k = 0; k < B; ++k) sum = fmaf(sinv[a * B + k], y[k], sum);
+    out[a] = sum;
   }
 }
 
-// g_R from g_out (bands >= 1) and the source coefficients (transform.py:120-127)
-template <int DEG>
-__device__ inline void rotate_sh_bands_vjp(const float R[3][3], const float* g, const float* in,
-                                           float gR[3][3]) {
-  if (DEG >= 1) {
+// This channel's share of g_R for band l >= 2 (band_matrix_vjp is linear in
+// g_M = sum_c g_c in_c^T, so the channels' shares add up to it)
+template <int B>
+__device__ inline void band_channel_vjp(const float R[3][3], const float* g, const float* in,
+                                        float gR[3][3]) {
+  const float(*dirs)[3] = B == 5 ? c_shrot.dirs2 : c_shrot.dirs3;
+  const float* sinv = B == 5 ? &c_shrot.binvT2[0][0] : &c_shrot.binvT3[0][0];
 #pragma unroll
-    for (int a = 0; a < 3; ++a)
+  for (int k = 0; k < B; ++k) {
+    float h = 0.f;
 #pragma unroll
-      for (int b = 0; b < 3; ++b) {
-        float s = 0.f;
+    for (int a = 0; a < B; ++a) h = fmaf(sinv[a * B + k], g[a], h);
+    float e[3], gE[B];
 #pragma unroll
-        for (int c = 0; c < 3; ++c) s = fmaf(g[(1 + a) * 3 + c], in[(1 + b) * 3 + c], s);
-        gR[c_perm[a]][c_perm[b]] += s;  // P^T gM P
-      }
-  }
-  if (DEG >= 2) {
-    float gM[5][5];
+    for (int i = 0; i < 3; ++i)
+      e[i] = R[0][i] * dirs[k][0] + R[1][i] * dirs[k][1] + R[2][i] * dirs[k][2];
 #pragma unroll
-    for (int a = 0; a < 5; ++a)
+    for (int b = 0; b < B; ++b) gE[b] = h * in[b];
+    float ge[3] = {0.f, 0.f, 0.f};
+    band_vjp<B>(e[0], e[1], e[2], gE, ge);
 #pragma unroll
-      for (int b = 0; b < 5; ++b) {
-        float s = 0.f;
+    for (int jj = 0; jj < 3; ++jj)
 #pragma unroll
-        for (int c = 0; c < 3; ++c) s = fmaf(g[(4 + a) * 3 + c], in[(4 + b) * 3 + c], s);
-        gM[a][b] = s;
-      }
-    band_matrix_vjp<5>(R, gM, gR);
-  }
-  if (DEG >= 3) {
-    float gM[7][7];
-#pragma unroll
-    for (int a = 0; a < 7; ++a)
-#pragma unroll
-      for (int b = 0; b < 7; ++b) {
-        float s = 0.f;
-#pragma unroll
-        for (int c = 0; c < 3; ++c) s = fmaf(g[(9 + a) * 3 + c], in[(9 + b) * 3 + c], s);
-        gM[a][b] = s;
-      }
-    band_matrix_vjp<7>(R, gM, gR);
+      for (int ii = 0; ii < 3; ++ii) gR[jj][ii] = fmaf(dirs[k][jj], ge[ii], gR[jj][ii]);
   }
 }
 
@@ -496,7 +412,9 @@ __global__ void __launch_bounds__(128) mlp_fwd_kernel(int64_t n, const float* __
 }
 
 // K3f: transform (transform.py:70-84): mu' = mu + d_mu, q' = norm(d_q) (x) q_src,
-// SH bands >= 1 rotated by R(norm(d_q)); one thread per inside row.
+// SH bands >= 1 rotated by R(norm(d_q)).  Four lanes per inside row (rows in
+// index order, so the 4-lane groups of a warp read 8 consecutive cloud rows):
+// lanes 0-2 rotate one colour channel each, lane 3 writes mean and rotation.
 template <int DEG>
 __global__ void __launch_bounds__(128) transform_kernel(ss_cloud src, int64_t n,
                                                         const int32_t* __restrict__ rows,
@@ -507,7 +425,9 @@ __global__ void __launch_bounds__(128) transform_kernel(ss_cloud src, int64_t n,
                                                         float* __restrict__ t_sh,
                                                         uint32_t* status) {
   constexpr int K = (DEG + 1) * (DEG + 1);
-  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t j = t >> 2;
+  const int c = (int)(t & 3);
   if (j >= n) return;
   // rows in index order (coalesced cloud rows); pos = the row's slot in out7
   const int64_t gid = rows ? rows[j] : j;
@@ -517,32 +437,61 @@ __global__ void __launch_bounds__(128) transform_kernel(ss_cloud src, int64_t n,
   for (int k = 0; k < 7; ++k) o[k] = out7[i * os + k];
   float nq = sqrtf(o[3] * o[3] + o[4] * o[4] + o[5] * o[5] + o[6] * o[6]);
   if (nq < 1e-12f) {  // gaussians.py:46-47
-    if (status) atomicOr(status, SS_FLAG_ZERO_QUAT);
+    if (status && c == 3) atomicOr(status, SS_FLAG_ZERO_QUAT);
     nq = 1.f;
   }
   const float u[4] = {o[3] / nq, o[4] / nq, o[5] / nq, o[6] / nq};
-  const float* m = src.means + 3 * gid;
-  t_means[3 * gid + 0] = m[0] + o[0];
-  t_means[3 * gid + 1] = m[1] + o[1];
-  t_means[3 * gid + 2] = m[2] + o[2];
-  const float4 q = *reinterpret_cast<const float4*>(src.rotations + 4 * gid);
-  const float qs[4] = {q.x, q.y, q.z, q.w};
-  float qo[4];
-  quat_mul(u, qs, qo);
-  *reinterpret_cast<float4*>(t_rot + 4 * gid) = make_float4(qo[0], qo[1], qo[2], qo[3]);
-  if (DEG >= 1 && rotate_sh) {
-    float R[3][3];
-    quat_to_rot(u[0], u[1], u[2], u[3], R);
-    float in[3 * K], outv[3 * K];
+  if (c == 3) {
+    const float* m = src.means + 3 * gid;
+    t_means[3 * gid + 0] = m[0] + o[0];
+    t_means[3 * gid + 1] = m[1] + o[1];
+    t_means[3 * gid + 2] = m[2] + o[2];
+    const float4 q = *reinterpret_cast<const float4*>(src.rotations + 4 * gid);
+    const float qs[4] = {q.x, q.y, q.z, q.w};
+    float qo[4];
+    quat_mul(u, qs, qo);
+    *reinterpret_cast<float4*>(t_rot + 4 * gid) = make_float4(qo[0], qo[1], qo[2], qo[3]);
+    return;
+  }
+  if (DEG < 1 || !rotate_sh) return;
+  float R[3][3];
+  quat_to_rot(u[0], u[1], u[2], u[3], R);
+  const float* sh = src.sh + gid * 3 * K + c;
+  float* tsh = t_sh + gid * 3 * K + c;
+  {  // band 1: P R P^T
+    float in[3];
 #pragma unroll
-    for (int k = 3; k < 3 * K; ++k) in[k] = src.sh[gid * 3 * K + k];
-    rotate_sh_bands<DEG>(R, in, outv);
+    for (int b = 0; b < 3; ++b) in[b] = sh[(1 + b) * 3];
 #pragma unroll
-    for (int k = 3; k < 3 * K; ++k) t_sh[gid * 3 * K + k] = outv[k];
+    for (int a = 0; a < 3; ++a) {
+      float sum = 0.f;
+#pragma unroll
+      for (int b = 0; b < 3; ++b) sum = fmaf(R[c_perm[a]][c_perm[b]], in[b], sum);
+      tsh[(1 + a) * 3] = sum;
+    }
+  }
+  if (DEG >= 2) {
+    float in[5], out[5];
+#pragma unroll
+    for (int b = 0; b < 5; ++b) in[b] = sh[(4 + b) * 3];
+    rotate_band_channel<5>(R, in, out);
+#pragma unroll
+    for (int a = 0; a < 5; ++a) tsh[(4 + a) * 3] = out[a];
+  }
+  if (DEG >= 3) {
+    float in[7], out[7];
+#pragma unroll
+    for (int b = 0; b < 7; ++b) in[b] = sh[(9 + b) * 3];
+    rotate_band_channel<7>(R, in, out);
+#pragma unroll
+    for (int a = 0; a < 7; ++a) tsh[(9 + a) * 3] = out[a];
   }
 }
 
-// K3b: dL/d[d_mu | d_q] from transformed-cloud gradients (transform.py:111-134)
+// K3b: dL/d[d_mu | d_q] from transformed-cloud gradients (transform.py:111-134).
+// Four lanes per inside row: lanes 0-2 form one colour channel's share of g_R,
+// the shares are summed with shuffles, lane 3 finishes (A(q_src)^T g_rot, the
+// rotation and normalisation Jacobians) and writes g7.
 template <int DEG>
 __global__ void __launch_bounds__(128) transform_vjp_kernel(
     ss_cloud src, int64_t n, const int32_t* __restrict__ rows, const int32_t* __restrict__ pos,
@@ -550,14 +499,59 @@ __global__ void __launch_bounds__(128) transform_vjp_kernel(
     const float* __restrict__ d_rot, const float* __restrict__ d_sh, float* __restrict__ g7,
     int gs) {
   constexpr int K = (DEG + 1) * (DEG + 1);
-  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (j >= n) return;
-  // rows in index order (coalesced cloud rows); pos = the row's slot in out7
-  const int64_t gid = rows ? rows[j] : j;
-  const int64_t i = pos ? pos[j] : j;
-  float o[7];
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t j = t >> 2;
+  const int c = (int)(t & 3);
+  const bool ok = j < n;  // no early exit: the 4-lane reduction below is warp-wide
+  const int64_t gid = ok ? (rows ? rows[j] : j) : 0;
+  const int64_t i = ok ? (pos ? pos[j] : j) : 0;
+  float o[7] = {0.f, 0.f, 0.f, 1.f, 0.f, 0.f, 0.f};
+  if (ok) {
 #pragma unroll
-  for (int k = 0; k < 7; ++k) o[k] = out7[i * os + k];
+    for (int k = 0; k < 7; ++k) o[k] = out7[i * os + k];
+  }
+  float nq = sqrtf(o[3] * o[3] + o[4] * o[4] + o[5] * o[5] + o[6] * o[6]);
+  nq = nq < 1e-12f ? 1.f : nq;
+  const float u[4] = {o[3] / nq, o[4] / nq, o[5] / nq, o[6] / nq};
+  float gR[3][3] = {{0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}};
+  const bool rot = DEG >= 1 && rotate_sh;
+  if (rot && ok && c < 3) {
+    float R[3][3];
+    quat_to_rot(u[0], u[1], u[2], u[3], R);
+    const float* sh = src.sh + gid * 3 * K + c;
+    const float* gsh = d_sh + gid * 3 * K + c;
+    {  // band 1: g_R += P^T (g in^T) P
+      float in[3], g[3];
+#pragma unroll
+      for (int b = 0; b < 3; ++b) in[b] = sh[(1 + b) * 3], g[b] = gsh[(1 + b) * 3];
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b) gR[c_perm[a]][c_perm[b]] = fmaf(g[a], in[b], gR[c_perm[a]][c_perm[b]]);
+    }
+    if (DEG >= 2) {
+      float in[5], g[5];
+#pragma unroll
+      for (int b = 0; b < 5; ++b) in[b] = sh[(4 + b) * 3], g[b] = gsh[(4 + b) * 3];
+      band_channel_vjp<5>(R, g, in, gR);
+    }
+    if (DEG >= 3) {
+      float in[7], g[7];
+#pragma unroll
+      for (int b = 0; b < 7; ++b) in[b] = sh[(9 + b) * 3], g[b] = gsh[(9 + b) * 3];
+      band_channel_vjp<7>(R, g, in, gR);
+    }
+  }
+  if (rot) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b) {
+        gR[a][b] += __shfl_xor_sync(0xffffffffu, gR[a][b], 1);
+        gR[a][b] += __shfl_xor_sync(0xffffffffu, gR[a][b], 2);
+      }
+  }
+  if (!ok || c != 3) return;
   const float4 q = *reinterpret_cast<const float4*>(src.rotations + 4 * gid);
   const float4 gr = *reinterpret_cast<const float4*>(d_rot + 4 * gid);
   // g_u = A(q_src)^T g_rot, A rows: [w,-x,-y,-z],[x,w,z,-y],[y,-z,w,x],[z,y,-x,w]
@@ -566,16 +560,7 @@ __global__ void __launch_bounds__(128) transform_vjp_kernel(
   gu[1] = -q.y * gr.x + q.x * gr.y - q.w * gr.z + q.z * gr.w;
   gu[2] = -q.z * gr.x + q.w * gr.y + q.x * gr.z - q.y * gr.w;
   gu[3] = -q.w * gr.x - q.z * gr.y + q.y * gr.z + q.x * gr.w;
-  float nq = sqrtf(o[3] * o[3] + o[4] * o[4] + o[5] * o[5] + o[6] * o[6]);
-  nq = nq < 1e-12f ? 1.f : nq;
-  const float u[4] = {o[3] / nq, o[4] / nq, o[5] / nq, o[6] / nq};
-  if (DEG >= 1 && rotate_sh) {
-    float R[3][3], gR[3][3] = {{0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}};
-    quat_to_rot(u[0], u[1], u[2], u[3], R);
-    float in[3 * K], gsh[3 * K];
-#pragma unroll
-    for (int k = 3; k < 3 * K; ++k) in[k] = src.sh[gid * 3 * K + k], gsh[k] = d_sh[gid * 3 * K + k];
-    rotate_sh_bands_vjp<DEG>(R, gsh, in, gR);
+  if (rot) {
     float gq[4];
     quat_to_rot_vjp(u[0], u[1], u[2], u[3], gR, gq);
 #pragma unroll
@@ -1035,7 +1020,7 @@ int transform_run(const ss_cloud* src, int64_t n, const int32_t* rows, const int
   if (n == 0) return SS_OK;
   SS_TRY(ensure_shrot_const());
   prof_begin(PH_TRANSFORM, st);
-  const unsigned grid = (unsigned)cdiv(n, 128);
+  const unsigned grid = (unsigned)cdiv(4 * n, 128);  // 4 lanes per row
   switch (sh_degree_of(src->sh_coeffs)) {
     case 0: transform_kernel<0><<<grid, 128, 0, st>>>(*src, n, rows, pos, out7, os, rotate_sh, tm, tr, ts, status); break;
     case 1: transform_kernel<1><<<grid, 128, 0, st>>>(*src, n, rows, pos, out7, os, rotate_sh, tm, tr, ts, status); break;
@@ -1057,7 +1042,7 @@ int transform_vjp_run(const ss_cloud* src, int64_t n, const int32_t* rows, const
   if (n == 0) return SS_OK;
   SS_TRY(ensure_shrot_const());
   prof_begin(PH_TRANSFORM_BWD, st);
-  const unsigned grid = (unsigned)cdiv(n, 128);
+  const unsigned grid = (unsigned)cdiv(4 * n, 128);  // 4 lanes per row
   switch (sh_degree_of(src->sh_coeffs)) {
     case 0: transform_vjp_kernel<0><<<grid, 128, 0, st>>>(*src, n, rows, pos, out7, os, rotate_sh, dm, dr, ds, g7, gs); break;
     case 1: transform_vjp_kernel<1><<<grid, 128, 0, st>>>(*src, n, rows, pos, out7, os, rotate_sh, dm, dr, ds, g7, gs); break;
