@@ -272,9 +272,12 @@ int ntc_backward_run(const ss_grid* g, const ss_mlp* mlp, int64_t n, const float
 int transform_run(const ss_cloud* src, int64_t n, const int32_t* rows, const int32_t* pos,
                   const float* out7, int os, int rotate_sh, float* tm, float* tr, float* ts,
                   uint32_t* status, cudaStream_t st);
+// live (nullable): per-Gaussian flag of the raster backward's `contributed`;
+// rows without it get a zero g7 row without reading their gradients
 int transform_vjp_run(const ss_cloud* src, int64_t n, const int32_t* rows, const int32_t* pos,
                       const float* out7, int os, int rotate_sh, const float* dm, const float* dr,
-                      const float* ds, float* g7, int gs, cudaStream_t st);
+                      const float* ds, float* g7, int gs, cudaStream_t st,
+                      const uint8_t* live = nullptr);
 }  // namespace ss
 
 // decoder on tensor cores (mlp_tc.cu); mode 0 = FFMA fp32, 1 = 3xTF32, 2 = tf32

@@ -516,15 +516,39 @@ __global__ void __launch_bounds__(NT, 1) mlp_bwd_tc_kernel(
       umma::commit(&bar);
     }
   };
-  if (blockIdx.x < ntiles) {
-    fetch(blockIdx.x);
-    stage_in();
-    issue_stage1();
-  }
+  // a tile whose output gradients are all zero (Gaussians no pixel of the view
+  // used) contributes nothing: its dX rows are zeroed and its MMAs skipped
+  auto tile_zero = [&]() {
+    bool z = true;
+    if (q == 0) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) z &= gr[k] == 0.f;
+    }
+    return __syncthreads_and(z) != 0;
+  };
+  bool issued = false;  // stage 1 of the current tile already in flight
+  if (blockIdx.x < ntiles) fetch(blockIdx.x);
   int it = 0;
   SS_STAMP(1, 0);
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
     const int64_t row = t * 128 + r;
+    if (!issued) {
+      if (tile_zero()) {
+#pragma unroll
+        for (int b = 0; b < XSlice<IN>::NB; ++b) {
+          const int c = 8 * q + 32 * b;
+          if (c < IN && row < n) {
+            *reinterpret_cast<float4*>(dX + row * xs + c) = make_float4(0.f, 0.f, 0.f, 0.f);
+            *reinterpret_cast<float4*>(dX + row * xs + c + 4) = make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+        }
+        fetch(t + gridDim.x);
+        continue;
+      }
+      stage_in();
+      issue_stage1();
+    }
+    issued = false;
     SS_STAMP(1, 1 + 8 * it);
     const uint32_t mask1 = (uint32_t)(mr.x >> c0) & 0xFFFFu;  // the forward's ReLU decisions
     const uint32_t mask2 = (uint32_t)(mr.y >> c0) & 0xFFFFu;
@@ -589,9 +613,10 @@ __global__ void __launch_bounds__(NT, 1) mlp_bwd_tc_kernel(
     SS_STAMP(1, 6 + 8 * it);
     acc_w = 1;
     // ---- next tile's stage 1 runs under this tile's dX epilogue
-    if (t + gridDim.x < ntiles) {
+    if (t + gridDim.x < ntiles && !tile_zero()) {
       stage_in();
       issue_stage1();
+      issued = true;
     }
     SS_STAMP(1, 7 + 8 * it);
 #pragma unroll

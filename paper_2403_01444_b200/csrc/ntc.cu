@@ -358,14 +358,24 @@ __global__ void __launch_bounds__(256) scatter_kernel(ss_grid g, int64_t n,
                                                       const float* __restrict__ dX, int xs,
                                                       float* __restrict__ g_tables) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const bool ok = i < n;
-  if (__all_sync(0xffffffffu, !ok)) return;  // warp-uniform exit keeps the shuffles full
   const int L = g.n_levels, F = g.n_features;
+  const float* dr = dX + (i < n ? i : 0) * xs;
+  // rows with an all-zero feature gradient (Gaussians no pixel saw in this
+  // view) add nothing (np.add.at of zeros): skip them, whole warps at a time
+  bool ok = i < n;
+  if (ok) {
+    bool nz = false;
+    for (int k = 0; k < L * F; k += 4) {
+      const float4 v = *reinterpret_cast<const float4*>(dr + k);
+      nz |= (v.x != 0.f) | (v.y != 0.f) | (v.z != 0.f) | (v.w != 0.f);
+    }
+    ok = nz;
+  }
+  if (__all_sync(0xffffffffu, !ok)) return;  // warp-uniform exit keeps the shuffles full
   const int64_t gid = ok ? (rows ? rows[i] : i) : 0;
   double xn[3];
   normalise(g, means + 3 * gid, xn);
   const size_t T = (size_t)1 << g.log2_table;
-  const float* dr = dX + (ok ? i : 0) * xs;
   for (int l = 0; l < L; ++l) {
     uint32_t idx[8];
     float w[8];
@@ -373,9 +383,10 @@ __global__ void __launch_bounds__(256) scatter_kernel(ss_grid g, int64_t n,
     float* gl = g_tables + (size_t)l * T * F;
     if (F == 2) {
       const float2 d = ok ? *reinterpret_cast<const float2*>(dr + 2 * l) : make_float2(0.f, 0.f);
+      const bool live = ok && (d.x != 0.f || d.y != 0.f);
 #pragma unroll
       for (int k = 0; k < 8; ++k)
-        red_add_v2_agg(gl, ok ? idx[k] : 0xffffffffu, w[k] * d.x, w[k] * d.y);
+        red_add_v2_agg(gl, live ? idx[k] : 0xffffffffu, w[k] * d.x, w[k] * d.y);
     } else if (ok) {
       for (int f = 0; f < F; ++f) {
         const float d = dr[l * F + f];
@@ -497,13 +508,19 @@ __global__ void __launch_bounds__(128) transform_vjp_kernel(
     ss_cloud src, int64_t n, const int32_t* __restrict__ rows, const int32_t* __restrict__ pos,
     const float* __restrict__ out7, int os, int rotate_sh, const float* __restrict__ d_means,
     const float* __restrict__ d_rot, const float* __restrict__ d_sh, float* __restrict__ g7,
-    int gs) {
+    int gs, const uint8_t* __restrict__ live) {
   constexpr int K = (DEG + 1) * (DEG + 1);
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t j = t >> 2;
   const int c = (int)(t & 3);
-  const bool ok = j < n;  // no early exit: the 4-lane reduction below is warp-wide
-  const int64_t gid = ok ? (rows ? rows[j] : j) : 0;
+  const bool in_range = j < n;  // no early exit: the 4-lane reduction below is warp-wide
+  const int64_t gid = in_range ? (rows ? rows[j] : j) : 0;
+  // a Gaussian no pixel of this view used has all-zero gradients: g7 row = 0
+  const bool ok = in_range && (!live || live[gid]);
+  if (in_range && !ok && c == 3) {
+    const int64_t i0 = pos ? pos[j] : j;
+    for (int k = 0; k < gs; ++k) g7[i0 * gs + k] = 0.f;
+  }
   const int64_t i = ok ? (pos ? pos[j] : j) : 0;
   float o[7] = {0.f, 0.f, 0.f, 1.f, 0.f, 0.f, 0.f};
   if (ok) {
@@ -1034,7 +1051,7 @@ int transform_run(const ss_cloud* src, int64_t n, const int32_t* rows, const int
 
 int transform_vjp_run(const ss_cloud* src, int64_t n, const int32_t* rows, const int32_t* pos,
                       const float* out7, int os, int rotate_sh, const float* dm, const float* dr,
-                      const float* ds, float* g7, int gs, cudaStream_t st) {
+                      const float* ds, float* g7, int gs, cudaStream_t st, const uint8_t* live) {
   if (!src || src->sh_coeffs < 1 || src->sh_coeffs > 16) {
     set_error("transform vjp: bad cloud");
     return SS_ERR_DATA;
@@ -1044,10 +1061,10 @@ int transform_vjp_run(const ss_cloud* src, int64_t n, const int32_t* rows, const
   prof_begin(PH_TRANSFORM_BWD, st);
   const unsigned grid = (unsigned)cdiv(4 * n, 128);  // 4 lanes per row
   switch (sh_degree_of(src->sh_coeffs)) {
-    case 0: transform_vjp_kernel<0><<<grid, 128, 0, st>>>(*src, n, rows, pos, out7, os, rotate_sh, dm, dr, ds, g7, gs); break;
-    case 1: transform_vjp_kernel<1><<<grid, 128, 0, st>>>(*src, n, rows, pos, out7, os, rotate_sh, dm, dr, ds, g7, gs); break;
-    case 2: transform_vjp_kernel<2><<<grid, 128, 0, st>>>(*src, n, rows, pos, out7, os, rotate_sh, dm, dr, ds, g7, gs); break;
-    default: transform_vjp_kernel<3><<<grid, 128, 0, st>>>(*src, n, rows, pos, out7, os, rotate_sh, dm, dr, ds, g7, gs); break;
+    case 0: transform_vjp_kernel<0><<<grid, 128, 0, st>>>(*src, n, rows, pos, out7, os, rotate_sh, dm, dr, ds, g7, gs, live); break;
+    case 1: transform_vjp_kernel<1><<<grid, 128, 0, st>>>(*src, n, rows, pos, out7, os, rotate_sh, dm, dr, ds, g7, gs, live); break;
+    case 2: transform_vjp_kernel<2><<<grid, 128, 0, st>>>(*src, n, rows, pos, out7, os, rotate_sh, dm, dr, ds, g7, gs, live); break;
+    default: transform_vjp_kernel<3><<<grid, 128, 0, st>>>(*src, n, rows, pos, out7, os, rotate_sh, dm, dr, ds, g7, gs, live); break;
   }
   SS_CHECK_LAUNCH("transform_vjp_kernel");
   prof_end(PH_TRANSFORM_BWD, st);

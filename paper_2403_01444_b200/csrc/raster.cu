@@ -879,7 +879,9 @@ __global__ void __launch_bounds__(128, 4) gaussian_bwd_kernel(CamD cam, ss_cloud
   if (gid >= n) return;
   const int K = cl.sh_coeffs;
   const int r = g.rank_of[gid];
-  if (r >= g.dev_counts[0]) {  // culled: zero rows so callers need no memset
+  // culled, or no pixel of this view took a weight from it (all accumulators
+  // are exactly 0, so every gradient is): zero rows so callers need no memset
+  if (r >= g.dev_counts[0] || !g.touched[r]) {
     if (out.viewspace) out.viewspace[gid] = 0.f;
     if (out.contributed) out.contributed[gid] = 0;
     if (out.d_means) for (int j = 0; j < 3; ++j) out.d_means[3 * gid + j] = 0.f;

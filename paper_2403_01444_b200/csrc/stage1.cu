@@ -143,7 +143,7 @@ int ss_stage1_iter_grads(ss_stage1* st, const ss_camera* cam, const float* targe
   const bool perm = st->rows_index && st->rows_pos;
   SS_TRY(transform_vjp_run(&st->src, st->n_in, perm ? st->rows_index : st->rows,
                            perm ? st->rows_pos : nullptr, ns.out7, 8, st->rotate_sh, st->d_means,
-                           st->d_rotations, st->d_sh, ns.g7, 8, s));
+                           st->d_rotations, st->d_sh, ns.g7, 8, s, st->contributed));
   SS_TRY(ntc_backward_run(&st->grid, &st->mlp, st->n_in, st->src.means, st->rows, st->params,
                           ns.X, ns.xs, ns.g7, 8, ns.relu, ns.dX, st->g_tables, st->g_params, s));
   st->iteration += 1;
