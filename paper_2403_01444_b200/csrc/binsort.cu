@@ -196,29 +196,38 @@ int binsort_passes(int key_bits) { return (key_bits + 7) / 8; }
 // into keys_out/vals_out, in ceil(key_bits / 8) passes ping-ponging with the
 // tmp buffers.  The input must be in keys_out/vals_out for an even number of
 // passes and in keys_tmp/vals_tmp for an odd one: see binsort_passes().
+int binsort_clear(const BinSortWS& w, int key_bits, cudaStream_t st) {
+  const int passes = binsort_passes(key_bits);
+  SS_CUDA(cudaMemsetAsync(w.hist, 0, binsort_clear_bytes(w), st));
+  SS_CUDA(cudaMemsetAsync(w.status, 0, (size_t)passes * w.max_blocks * 256 * sizeof(uint32_t),
+                          st));
+  return SS_OK;
+}
+
 int binsort_run(const BinSortWS& w, uint32_t* keys_tmp, uint32_t* vals_tmp, uint32_t* keys_out,
                 uint32_t* vals_out, const int64_t* d_n, int64_t cap, int key_bits,
-                cudaStream_t st) {
+                cudaStream_t st, bool hist_ready) {
   const int passes = binsort_passes(key_bits);
   if (key_bits < 1 || passes > w.max_passes) {
     set_error("binsort: key wider than the planned passes");
     return SS_ERR_DATA;
   }
-  SS_CUDA(cudaMemsetAsync(w.hist, 0, binsort_clear_bytes(w), st));
-  SS_CUDA(cudaMemsetAsync(w.status, 0, (size_t)passes * w.max_blocks * 256 * sizeof(uint32_t),
-                          st));
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (sms <= 0) sms = 148;
-  }
   uint32_t *ka = (passes & 1) ? keys_tmp : keys_out, *va = (passes & 1) ? vals_tmp : vals_out;
   uint32_t *kb = (passes & 1) ? keys_out : keys_tmp, *vb = (passes & 1) ? vals_out : vals_tmp;
-  const unsigned hgrid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(cap, 256), 4 * sms));
-  bs_hist_kernel<<<hgrid, 256, 0, st>>>(ka, d_n, cap, key_bits, w.hist);
-  SS_CHECK_LAUNCH("bs_hist_kernel");
+  if (!hist_ready) {  // otherwise the producer cleared and filled w.hist (bs_hist_add)
+    SS_TRY(binsort_clear(w, key_bits, st));
+    static int sms = 0;
+    if (!sms) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      if (sms <= 0) sms = 148;
+    }
+    const unsigned hgrid =
+        (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(cap, 256), 4 * sms));
+    bs_hist_kernel<<<hgrid, 256, 0, st>>>(ka, d_n, cap, key_bits, w.hist);
+    SS_CHECK_LAUNCH("bs_hist_kernel");
+  }
   uint32_t* tickets = w.hist + kMaxPasses * 256;
   const unsigned grid = (unsigned)w.max_blocks;
   for (int p = 0; p < passes; ++p) {

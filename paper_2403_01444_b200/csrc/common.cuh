@@ -247,9 +247,30 @@ struct BinSortWS {
 };
 BinSortWS binsort_plan(Carve& c, int64_t capacity, int max_passes);
 int binsort_passes(int key_bits);
+// zero the histograms, tickets and look-back words (before a producer that
+// accumulates the histograms itself with bs_hist_add, then hist_ready = true)
+int binsort_clear(const BinSortWS& w, int key_bits, cudaStream_t st);
 int binsort_run(const BinSortWS& w, uint32_t* keys_tmp, uint32_t* vals_tmp, uint32_t* keys_out,
                 uint32_t* vals_out, const int64_t* d_n, int64_t cap, int key_bits,
-                cudaStream_t st);
+                cudaStream_t st, bool hist_ready = false);
+
+// Producer-side histogram for binsort (8-bit digits, up to 4 passes): add a
+// key into the block's shared histogram sh[pass][digit]; bs_hist_flush adds
+// the block's counts to the global ones after a __syncthreads().
+__device__ __forceinline__ void bs_hist_add(uint32_t (*sh)[256], uint32_t key, int key_bits) {
+  for (int p = 0; 8 * p < key_bits; ++p) {
+    const int bits = key_bits - 8 * p < 8 ? key_bits - 8 * p : 8;
+    atomicAdd(&sh[p][(key >> (8 * p)) & ((1u << bits) - 1)], 1u);
+  }
+}
+__device__ __forceinline__ void bs_hist_flush(const uint32_t (*sh)[256], uint32_t* hist,
+                                              int key_bits) {
+  const int passes = (key_bits + 7) / 8;
+  for (int i = threadIdx.x; i < passes * 256; i += blockDim.x) {
+    const uint32_t v = sh[i >> 8][i & 255];
+    if (v) atomicAdd(hist + i, v);
+  }
+}
 
 // NTC pipeline pieces (ntc.cu): features X and their gradient dX are (n, xs)
 // row-major in HBM between the gather / decoder / scatter kernels; out7 and g7

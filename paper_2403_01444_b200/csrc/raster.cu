@@ -29,7 +29,7 @@ struct Geom {
   double4* r_conop_d;
   float4* r_color;
   int4* r_rect;     // per rank (tx0, tx1, ty0, ty1)
-  double* r_thr;    // per rank: 2 ln(opacity / skip_alpha), the tile-cull threshold
+  double4* r_cull;  // per rank: 2 ln(opacity / skip_alpha) (tile-cull threshold), -c01/c11, -c01/c00
   int64_t* offsets;  // per rank, exclusive prefix of tile counts (n+1)
   float* acc;        // per rank x kAccStride: colour 3, mean2d 2, conic 00/01/11, opacity
   uint8_t* touched;  // per rank
@@ -84,7 +84,7 @@ static Geom plan_geom(void* base, int64_t n, const ss_camera* cam, const ss_rast
   g.r_conop_d = c.take<double4>(nn);
   g.r_color = c.take<float4>(nn);
   g.r_rect = c.take<int4>(nn);
-  g.r_thr = c.take<double>(nn);
+  g.r_cull = c.take<double4>(nn);
   g.offsets = c.take<int64_t>(nn + 1);
   g.acc = c.take<float>(nn * kAccStride);
   g.touched = c.take<uint8_t>(nn);
@@ -214,35 +214,45 @@ __device__ inline void project_one(const CamD& cam, const ss_cloud& cl, int64_t 
 }
 
 // K4a: per-Gaussian projection; depth key (+inf when culled)
-__global__ void preprocess_kernel(CamD cam, ss_cloud cl, Geom g) {
+__global__ void __launch_bounds__(256) preprocess_kernel(CamD cam, ss_cloud cl, Geom g) {
+  __shared__ uint32_t s_hist[4][256];  // the depth sort's digit histograms
+  for (int k = threadIdx.x; k < 1024; k += blockDim.x) (&s_hist[0][0])[k] = 0;
+  __syncthreads();
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= cl.n) return;
-  if (i == 0) g.dev_counts[2] = cl.n;
-  g.order[i] = (int32_t)i;  // sort input (4 passes: the input sits in the output buffers)
-  const float* m = cl.means + 3 * i;
-  const double z = cam.R[2][0] * (double)m[0] + cam.R[2][1] * (double)m[1] +
-                   cam.R[2][2] * (double)m[2] + cam.t[2];
-  if (!(z > cam.near_clip)) {  // rasterizer.py:228
-    g.key_in[i] = __longlong_as_double(0x7ff0000000000000ll);  // +inf
-    g.key32[i] = 0x7f800000u;
-    return;
+  if (i < cl.n) {
+    if (i == 0) g.dev_counts[2] = cl.n;
+    g.order[i] = (int32_t)i;  // sort input (4 passes: the input sits in the output buffers)
+    const float* m = cl.means + 3 * i;
+    const double z = cam.R[2][0] * (double)m[0] + cam.R[2][1] * (double)m[1] +
+                     cam.R[2][2] * (double)m[2] + cam.t[2];
+    uint32_t key = 0x7f800000u;  // +inf: culled (rasterizer.py:228)
+    if (!(z > cam.near_clip)) {
+      g.key_in[i] = __longlong_as_double(0x7ff0000000000000ll);
+    } else {
+      g.key_in[i] = z;
+      // fp32 rounding is monotone, so sorting by the fp32 bits orders the fp64
+      // depths up to ties, which depth_tie_kernel resolves
+      key = __float_as_uint((float)z);
+      atomicAdd(reinterpret_cast<unsigned long long*>(&g.dev_counts[0]), 1ull);
+      Projected P;
+      project_one(cam, cl, i, P);
+      g.g_mean[i] = make_double2(P.mean[0], P.mean[1]);
+      g.g_conop[i] =
+          make_double4(P.conic[0][0], P.conic[0][1] + P.conic[1][0], P.conic[1][1], P.op);
+      // w: the unclipped-channel mask of clip(0.5 + SH, 0, 1) (sh.py:51-59) for the backward
+      const int clip_mask = (P.raw[0] > 0.0 && P.raw[0] < 1.0) |
+                            (P.raw[1] > 0.0 && P.raw[1] < 1.0) << 1 |
+                            (P.raw[2] > 0.0 && P.raw[2] < 1.0) << 2;
+      g.g_color[i] = make_float4((float)fmin(fmax(P.raw[0], 0.0), 1.0),
+                                 (float)fmin(fmax(P.raw[1], 0.0), 1.0),
+                                 (float)fmin(fmax(P.raw[2], 0.0), 1.0), (float)clip_mask);
+      g.g_cov[i] = make_double2(P.cov2d[0][0], P.cov2d[1][1]);
+    }
+    g.key32[i] = key;
+    bs_hist_add(s_hist, key, 32);
   }
-  g.key_in[i] = z;
-  // fp32 rounding is monotone, so sorting by the fp32 bits orders the fp64
-  // depths up to ties, which depth_tie_kernel resolves
-  g.key32[i] = __float_as_uint((float)z);
-  atomicAdd(reinterpret_cast<unsigned long long*>(&g.dev_counts[0]), 1ull);
-  Projected P;
-  project_one(cam, cl, i, P);
-  g.g_mean[i] = make_double2(P.mean[0], P.mean[1]);
-  g.g_conop[i] = make_double4(P.conic[0][0], P.conic[0][1] + P.conic[1][0], P.conic[1][1], P.op);
-  // w: the unclipped-channel mask of clip(0.5 + SH, 0, 1) (sh.py:51-59) for the backward
-  const int clip_mask = (P.raw[0] > 0.0 && P.raw[0] < 1.0) | (P.raw[1] > 0.0 && P.raw[1] < 1.0) << 1 |
-                        (P.raw[2] > 0.0 && P.raw[2] < 1.0) << 2;
-  g.g_color[i] = make_float4((float)fmin(fmax(P.raw[0], 0.0), 1.0),
-                             (float)fmin(fmax(P.raw[1], 0.0), 1.0),
-                             (float)fmin(fmax(P.raw[2], 0.0), 1.0), (float)clip_mask);
-  g.g_cov[i] = make_double2(P.cov2d[0][0], P.cov2d[1][1]);
+  __syncthreads();
+  bs_hist_flush(s_hist, g.dsort.hist, 32);
 }
 
 // floor(v) // ts with Python floor-division semantics, clipped (rasterizer.py:142-145)
@@ -319,7 +329,9 @@ __global__ void rank_kernel(CamD cam, ss_raster_settings s, int64_t n, Geom g) {
     rect = make_int4(tile_of(xl, ts, ntx), tile_of(xh, ts, ntx), tile_of(yl, ts, nty),
                      tile_of(yh, ts, nty));
     vis = !((xh < 0) || (xl > cam.W - 1) || (yh < 0) || (yl > cam.H - 1));
-    g.r_thr[r] = 2.0 * log(co.w / s.skip_alpha);
+    // co.y = c01 + c10: the minimiser of the form along x = const is dy = -co.y dx / (2 c11)
+    g.r_cull[r] = make_double4(2.0 * log(co.w / s.skip_alpha), -co.y / (2.0 * co.z),
+                               -co.y / (2.0 * co.x), 0.0);
   } else {  // skip = 0: every tile (rasterizer.py:149-154)
     rect = make_int4(0, ntx - 1, 0, nty - 1);
     vis = true;
@@ -334,8 +346,7 @@ __global__ void finish_counts_kernel(Geom g, int64_t n) {
   g.dev_counts[1] = n > 0 ? g.offsets[n] : 0;
 }
 
-// K4c: emit (tile id, rank) in rank order
-// K4c: emit (tile id, rank) in rank order, one thread per pair (load-balanced:
+// K4c (render path) tile cull:
 // near-camera splats can cover thousands of tiles).  The owning rank is the last
 // r with offsets[r] <= j (zero-count ranks are skipped by construction).
 // Tile-level cull (render path only): a (splat, tile) pair whose alpha stays
@@ -344,21 +355,20 @@ __global__ void finish_counts_kernel(Geom g, int64_t n) {
 // replaced by the sentinel ntiles and it sorts past every tile list.  The test
 // bounds alpha by the minimum of the fp64 Mahalanobis form over the tile's
 // pixel-centre rectangle (a relaxation of the discrete minimum: conservative).
-__device__ inline bool splat_misses_tile(const double2 m, const double4 co, double thr, double xa,
-                                         double xb, double ya, double yb) {
+__device__ inline bool splat_misses_tile(const double2 m, const double4 co, const double4 cl,
+                                         double xa, double xb, double ya, double yb) {
   const double lx = xa - m.x, hx = xb - m.x, ly = ya - m.y, hy = yb - m.y;
-  if (lx <= 0.0 && hx >= 0.0 && ly <= 0.0 && hy >= 0.0) return thr < -2e-6;
+  if (lx <= 0.0 && hx >= 0.0 && ly <= 0.0 && hy >= 0.0) return cl.x < -2e-6;
   auto q = [&](double dx, double dy) { return co.x * dx * dx + co.y * dx * dy + co.z * dy * dy; };
   auto clampd = [](double v, double a, double b) { return fmin(fmax(v, a), b); };
   double qmin = 1e300;
-  // edges x = const: minimise over dy
-  qmin = fmin(qmin, q(lx, clampd(-co.y * lx / (2.0 * co.z), ly, hy)));
-  qmin = fmin(qmin, q(hx, clampd(-co.y * hx / (2.0 * co.z), ly, hy)));
-  // edges y = const: minimise over dx
-  qmin = fmin(qmin, q(clampd(-co.y * ly / (2.0 * co.x), lx, hx), ly));
-  qmin = fmin(qmin, q(clampd(-co.y * hy / (2.0 * co.x), lx, hx), hy));
+  // edges x = const: minimise over dy (dy* = cl.y dx); edges y = const: dx* = cl.z dy
+  qmin = fmin(qmin, q(lx, clampd(cl.y * lx, ly, hy)));
+  qmin = fmin(qmin, q(hx, clampd(cl.y * hx, ly, hy)));
+  qmin = fmin(qmin, q(clampd(cl.z * ly, lx, hx), ly));
+  qmin = fmin(qmin, q(clampd(cl.z * hy, lx, hx), hy));
   // op exp(-qmin / 2) < skip (1 - 1e-6)  <=>  qmin > 2 ln(op / skip) + 2e-6
-  return qmin > thr + 2e-6;
+  return qmin > cl.x + 2e-6;
 }
 
 // K4c: emit (tile id, rank) in rank order, one thread per pair (load-balanced:
@@ -376,9 +386,12 @@ __device__ inline int64_t owner_rank(const int64_t* __restrict__ off, int64_t lo
 __global__ void __launch_bounds__(256) duplicate_kernel(int ntx, int64_t n, Geom g, Bins b,
                                                         uint32_t* kdst, uint32_t* vdst,
                                                         uint32_t* status, int cull, int ts, int W,
-                                                        int H, uint32_t sentinel) {
-  constexpr int CH = 1024;
+                                                        int H, uint32_t sentinel, int key_bits) {
+  constexpr int CH = 1024, SOFF = 2048;
   __shared__ int64_t s_lo, s_hi;
+  __shared__ int64_t s_off[SOFF];
+  __shared__ uint32_t s_hist[2][256];  // binsort digit histograms of the emitted keys
+  for (int i = threadIdx.x; i < 512; i += blockDim.x) (&s_hist[0][0])[i] = 0;
   const int64_t count = g.dev_counts[1];
   if (count > b.capacity && blockIdx.x == 0 && threadIdx.x == 0 && status)
     atomicOr(status, SS_FLAG_OVERFLOW);
@@ -391,23 +404,41 @@ __global__ void __launch_bounds__(256) duplicate_kernel(int ntx, int64_t n, Geom
     }
     __syncthreads();
     const int64_t rlo = s_lo, rhi = s_hi;
+    // the chunk's owning ranks' offsets staged in shared memory when they fit
+    const bool staged = rhi - rlo + 1 <= SOFF;
+    if (staged)
+      for (int64_t r = rlo + threadIdx.x; r <= rhi; r += blockDim.x) s_off[r - rlo] = g.offsets[r];
+    __syncthreads();
     for (int64_t j = j0 + threadIdx.x; j < min(j0 + CH, pairs); j += blockDim.x) {
-      const int64_t lo = owner_rank(g.offsets, rlo, rhi, j);
+      int64_t lo;
+      if (staged) {
+        int64_t a = 0, c = rhi - rlo;  // s_off[a] <= j < s_off[c]
+        while (c - a > 1) {
+          const int64_t mid = (a + c) >> 1;
+          if (s_off[mid] <= j) a = mid; else c = mid;
+        }
+        lo = rlo + a;
+      } else {
+        lo = owner_rank(g.offsets, rlo, rhi, j);
+      }
       const int4 rc = g.r_rect[lo];
       const int wx = rc.y - rc.x + 1;
-      const int local = (int)(j - g.offsets[lo]);
+      const int local = (int)(j - (staged ? s_off[lo - rlo] : g.offsets[lo]));
       const int ty = rc.z + local / wx, tx = rc.x + local % wx;
       uint32_t key = (uint32_t)(ty * ntx + tx);
       if (cull) {
         const double xa = tx * ts, xb = min(tx * ts + ts, W) - 1, ya = ty * ts,
                      yb = min(ty * ts + ts, H) - 1;
-        if (splat_misses_tile(g.r_mean[lo], g.r_conop_d[lo], g.r_thr[lo], xa, xb, ya, yb))
+        if (splat_misses_tile(g.r_mean[lo], g.r_conop_d[lo], g.r_cull[lo], xa, xb, ya, yb))
           key = sentinel;
       }
       kdst[j] = key;
       vdst[j] = (uint32_t)lo;
+      bs_hist_add(s_hist, key, key_bits);
     }
   }
+  __syncthreads();
+  bs_hist_flush(s_hist, b.sort.hist, key_bits);
 }
 
 __global__ void ranges_kernel(const int64_t* __restrict__ d_pairs, int64_t cap,
@@ -431,18 +462,19 @@ static int bin_pairs(const ss_camera* cam, const ss_raster_settings* s, int64_t 
   const int kb = key_bits(cull ? ntiles + 1 : ntiles);
   const bool two = binsort_passes(kb) == 2;
   SS_CUDA(cudaMemsetAsync(g.ranges, 0, ntiles * sizeof(int2), st));
+  SS_TRY(binsort_clear(b.sort, kb, st));  // duplicate_kernel builds the sort's histograms
   prof_begin(PH_DUPLICATE, st);
   const unsigned dgrid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(b.capacity, 1024),
                                                                          148 * 8));
   duplicate_kernel<<<dgrid, 256, 0, st>>>(ntx, n, g, b, two ? b.keys_out : b.keys_in,
                                           two ? b.vals_out : b.vals_in, status, cull, s->tile_size,
-                                          cam->width, cam->height, (uint32_t)ntiles);
+                                          cam->width, cam->height, (uint32_t)ntiles, kb);
   SS_CHECK_LAUNCH("duplicate_kernel");
   prof_end(PH_DUPLICATE, st);
   prof_begin(PH_TILE_SORT, st);
   SS_TRY(binsort_run(b.sort, b.keys_in, b.vals_in, b.keys_out, b.vals_out, g.dev_counts + 1,
-                     b.capacity, kb, st));
-  g_launches.fetch_add(two ? 3 : 2);
+                     b.capacity, kb, st, /*hist_ready=*/true));
+  g_launches.fetch_add(two ? 2 : 1);
   prof_end(PH_TILE_SORT, st);
   prof_begin(PH_RANGES, st);
   ranges_kernel<<<stride_grid(b.capacity), 256, 0, st>>>(g.dev_counts + 1, b.capacity, b.keys_out,
@@ -1063,14 +1095,16 @@ int raster_begin(const ss_cloud* cl, const ss_camera* cam, const ss_raster_setti
   const CamD cd = make_cam(cam);
   SS_CUDA(cudaMemsetAsync(g.dev_counts, 0, 3 * sizeof(int64_t), st));
   if (n > 0) {
+    SS_TRY(binsort_clear(g.dsort, 32, st));  // preprocess_kernel builds the histograms
     prof_begin(PH_PROJECT, st);
     preprocess_kernel<<<(unsigned)cdiv(n, 256), 256, 0, st>>>(cd, *cl, g);
     SS_CHECK_LAUNCH("preprocess_kernel");
     prof_end(PH_PROJECT, st);
     prof_begin(PH_DEPTH_SORT, st);
     SS_TRY(binsort_run(g.dsort, g.key32_tmp, reinterpret_cast<uint32_t*>(g.idx_in), g.key32,
-                       reinterpret_cast<uint32_t*>(g.order), g.dev_counts + 2, n, 32, st));
-    g_launches.fetch_add(5);
+                       reinterpret_cast<uint32_t*>(g.order), g.dev_counts + 2, n, 32, st,
+                       /*hist_ready=*/true));
+    g_launches.fetch_add(4);
     depth_tie_kernel<<<(unsigned)cdiv(n, 256), 256, 0, st>>>(g);
     SS_CHECK_LAUNCH("depth_tie_kernel");
     prof_end(PH_DEPTH_SORT, st);
