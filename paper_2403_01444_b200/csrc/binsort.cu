@@ -21,7 +21,7 @@ namespace ss {
 namespace {
 constexpr int kBsThreads = 256;
 constexpr int kBsWarps = kBsThreads / 32;
-constexpr int kBsStepsBig = 16;   // items per lane (4096-item tiles)
+constexpr int kBsStepsBig = 8;    // items per lane (2048-item tiles)
 constexpr int kBsStepsSmall = 4;  // 1024-item tiles for small sorts (more CTAs)
 constexpr uint32_t kFlagAgg = 1u << 30, kFlagInc = 2u << 30, kCntMask = (1u << 30) - 1;
 constexpr int kMaxPasses = 4;
@@ -105,11 +105,15 @@ __global__ void __launch_bounds__(kBsThreads) bs_pass_kernel(
   uint32_t k[kBsSteps], v[kBsSteps], rk[kBsSteps];
   const int64_t wbase = base + warp * (kBsSteps * 32);
 #pragma unroll
+  for (int s = 0; s < kBsSteps; ++s) {  // all loads in flight before the ranking
+    const int64_t i = wbase + s * 32 + lane;
+    k[s] = i < n ? kin[i] : 0u;
+    v[s] = i < n ? vin[i] : 0u;
+  }
+#pragma unroll
   for (int s = 0; s < kBsSteps; ++s) {
     const int64_t i = wbase + s * 32 + lane;
     const bool ok = i < n;
-    k[s] = ok ? kin[i] : 0u;
-    v[s] = ok ? vin[i] : 0u;
     const uint32_t d = ok ? ((k[s] >> shift) & dmask) : 256u;  // 256 = past the end
     const uint32_t peers = __match_any_sync(0xffffffffu, d);
     const int leader = __ffs(peers) - 1;
