@@ -807,16 +807,21 @@ __global__ void __launch_bounds__(kChunk, 1) mlp_bwd_kernel(
 }
 
 // lazy Adam over tables (row mask) + dense MLP (optim.py:33-66)
-__global__ void adam_kernel(int64_t n_table, float* __restrict__ tables,
-                            float* __restrict__ g_tables, double* __restrict__ m_t,
-                            double* __restrict__ v_t, const uint8_t* __restrict__ row_mask,
-                            int row_width, int64_t n_params, float* __restrict__ params,
-                            float* __restrict__ g_params, double* __restrict__ m_p,
-                            double* __restrict__ v_p, const int32_t* __restrict__ step_dev,
-                            double lr, double b1, double b2, double eps, int zero_grads) {
-  const int step = *step_dev + 1;
-  const double bc1 = 1.0 - pow(b1, (double)step);
-  const double bc2 = 1.0 - pow(b2, (double)step);
+__global__ void __launch_bounds__(256) adam_kernel(
+    int64_t n_table, float* __restrict__ tables, float* __restrict__ g_tables,
+    double* __restrict__ m_t, double* __restrict__ v_t, const uint8_t* __restrict__ row_mask,
+    int row_width, int64_t n_params, float* __restrict__ params, float* __restrict__ g_params,
+    double* __restrict__ m_p, double* __restrict__ v_p, const int32_t* __restrict__ step_dev,
+    double lr, double b1, double b2, double eps, int zero_grads) {
+  __shared__ double s_bc[2];
+  if (threadIdx.x == 0) {  // bias corrections once per block (optim.py:52-53)
+    const int step = *step_dev + 1;
+    s_bc[0] = 1.0 - pow(b1, (double)step);
+    s_bc[1] = 1.0 - pow(b2, (double)step);
+  }
+  __syncthreads();
+  const double bc1 = s_bc[0], bc2 = s_bc[1];
+  const int shift = (row_width & (row_width - 1)) == 0 ? __ffs(row_width) - 1 : -1;
   const int64_t total = n_table + n_params;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -826,10 +831,8 @@ __global__ void adam_kernel(int64_t n_table, float* __restrict__ tables,
     if (i < n_table) {
       j = i;
       p = tables, gp = g_tables, m = m_t, v = v_t;
-      if (row_mask && !row_mask[j / row_width]) {
-        if (zero_grads) gp[j] = 0.f;
-        continue;
-      }
+      // untouched rows: no Adam update, and their gradient is never written
+      if (row_mask && !row_mask[shift >= 0 ? (j >> shift) : (j / row_width)]) continue;
     } else {
       j = i - n_table;
       p = params, gp = g_params, m = m_p, v = v_p;
