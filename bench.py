@@ -390,6 +390,7 @@ def main():
     if rank == 0 and world == 1 and not a.no_render:
         line["render"] = render_fps(a)
         line["warmup"] = warmup_rate(sc, cache)
+        line["stage2"] = stage2_rate(sc, targets)
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline_sample(sc, cache, targets[0])
     if rank == 0:
@@ -416,6 +417,29 @@ def warmup_rate(sc, cache):
             "workload": "warmup_train on the 250k cfg1 means, noise 0.05, wall clock incl. "
                         "numpy batch sampling (Generator.choice without replacement), H2D, "
                         "device step and the final D2H"}
+
+
+def stage2_rate(sc, targets):
+    """Stage-2 iterations/s (adaptive.py:218-288) at cfg1 scale:
+    the 250k cloud frozen, 5000 spawned additional Gaussians, one view per
+    iteration over the 20 views (one epoch, then quantity control)."""
+    from paper_2403_01444_b200.stage2 import AdditionConfig, spawn_gaussians, stage2_optimize
+
+    rng = np.random.default_rng(0)
+    cfg = AdditionConfig()
+    sel = np.sort(rng.choice(len(sc.cloud["means"]), 5000, replace=False))
+    add = spawn_gaussians(sc.cloud, sel, cfg, rng)
+    views = [(c, t.cpu().numpy()) for c, t in zip(sc.cameras, targets)]
+    stage2_optimize(sc.cloud, add, views[:2], cfg, 2, np.random.default_rng(1))
+    n = 20
+    t0 = time.perf_counter()
+    out, losses = stage2_optimize(sc.cloud, add, views, cfg, n, np.random.default_rng(1))
+    dt = time.perf_counter() - t0
+    return {"metric": "stage2_iters_per_s", "value": n / dt, "unit": "iter/s",
+            "additional": [5000, len(out.means)], "loss_first_last": [losses[0], losses[-1]],
+            "workload": "stage2_optimize: 250k frozen + 5000 spawned Gaussians at 1352x1014, "
+                        "20 iterations (one epoch + quantity control), wall clock incl. the "
+                        "per-iteration pair-count read and the host split/prune"}
 
 
 def render_fps(a):

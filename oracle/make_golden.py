@@ -291,8 +291,44 @@ def gen_playback(R):
                         **_cam_arr(sc.cameras[0]), background=np.array(bg), **arrs)
 
 
+def gen_stage2(R):
+    """adaptive.stage2_optimize: a small frozen cloud, 60
+    spawned additional Gaussians, 2 views, 6 iterations (3 epochs of quantity
+    control: a split in epoch 2, prunes in epochs 2 and 3).  Decision margins
+    (measured): view-space gradients >= 24 % from tau_grad, opacities >= 2.4 %
+    from tau_alpha."""
+    import sys
+
+    sys.path.insert(0, rb.REF_SRC)
+    from splatstream import adaptive, rasterizer
+
+    sc = scenes.small_scene(seed=77, n=500, width=64, height=48, sh_degree=1, n_views=2)
+    cloud = rb.ref_cloud(R, sc.cloud)
+    rng = np.random.default_rng(3)
+    cfg = adaptive.AdditionConfig(tau_grad=2e-4, max_additional=100)
+    sel = np.sort(rng.choice(len(sc.cloud["means"]), 60, replace=False))
+    add = adaptive.spawn_gaussians(cloud, sel, cfg, rng)
+    moved = rb.ref_cloud(R, scenes.moved_cloud(sc.cloud, np.random.default_rng(9)))
+    views, arrs = [], {}
+    for v, c in enumerate(sc.cameras):
+        cam = rb.ref_camera(R, c)
+        out, _ = rasterizer.rasterize_forward(moved, cam)
+        views.append((cam, out.image))
+        arrs.update(_cam_arr(c, f"cam{v}_"))
+        arrs[f"target{v}"] = out.image
+    add_in = {k: getattr(add, k).copy() for k in ("means", "rotations", "log_scales",
+                                                   "opacity_logits", "sh")}
+    final, losses = adaptive.stage2_optimize(cloud, add, views, cfg, 6, np.random.default_rng(11))
+    np.savez_compressed(os.path.join(OUT, "stage2.npz"), **_cloud_arr(sc.cloud),
+                        **_cloud_arr(add_in, "add_"), **arrs,
+                        **{f"final_{k}": getattr(final, k) for k in add_in},
+                        losses=np.array(losses), tau_grad=2e-4, max_additional=100, iterations=6,
+                        rng_seed=11)
+
+
 GENERATORS = dict(encode=gen_encode, ntc=gen_ntc, transform=gen_transform, raster=gen_raster,
-                  loss=gen_loss, stage1=gen_stage1, ntc_blob=gen_ntc_blob, warmup=gen_warmup, playback=gen_playback)
+                  loss=gen_loss, stage1=gen_stage1, ntc_blob=gen_ntc_blob, warmup=gen_warmup, playback=gen_playback,
+                  stage2=gen_stage2)
 
 
 def main():

@@ -116,3 +116,25 @@ def test_device_playback_matches_reference():
     assert playback.materialize_frame(st, 2).means.shape[0] == len(d["cloud_means"]) + 40
     with pytest.raises(DataError):
         playback.playback_render(st, 4, cam)
+
+
+def test_device_stage2_matches_reference():
+    """stage2_optimize (joint render, full-parameter backward,
+    per-parameter Adam, epoch-boundary split/prune with the reference's
+    generator sequence) against the reference's run: same losses, same
+    surviving rows, parameters within tolerance."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2403_01444_b200.stage2 import AdditionConfig, stage2_optimize
+
+    d = G.load("stage2")
+    cfg = AdditionConfig(tau_grad=float(d["tau_grad"]), max_additional=int(d["max_additional"]))
+    views = [(G.camera(d, f"cam{v}_"), d[f"target{v}"]) for v in range(2)]
+    out, losses = stage2_optimize(G.cloud(d), G.cloud(d, "add_"), views, cfg,
+                                  int(d["iterations"]), np.random.default_rng(int(d["rng_seed"])))
+    np.testing.assert_allclose(losses, d["losses"], rtol=1e-4)
+    assert out.means.shape == d["final_means"].shape
+    for k in ("means", "rotations", "log_scales", "opacity_logits", "sh"):
+        ref = d[f"final_{k}"]
+        assert G.norm_rel(getattr(out, k), ref) <= 1e-3, k
