@@ -195,7 +195,8 @@ def stage2_optimize(transformed, additional, views, cfg: AdditionConfig, iterati
     frozen = _as_dict(transformed)
     cams = [Camera.from_any(c) for c, _ in views]
     cstructs = [camera_struct(c) for c in cams]
-    targets = [to_dev(np.asarray(t, dtype=np.float64), dev=dev) for _, t in views]
+    targets = [t.to(dev, torch.float32).contiguous() if isinstance(t, torch.Tensor)
+               else to_dev(np.asarray(t, dtype=np.float64), dev=dev) for _, t in views]
     sset = settings_struct(settings, background)
     lr = cfg.lr_by_param()
     f64 = dict(dtype=torch.float64, device=dev)
