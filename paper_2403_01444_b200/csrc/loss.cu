@@ -16,6 +16,7 @@ struct LossParams {
   int H, W, Hv, Wv, C;
   double g[WIN];
   double c1, c2, lam, up;  // up = -lam / (2 n_windows)
+  double l1w;              // (1 - lam) / (H W C)
 };
 
 // The separable 11-tap passes walk a 32-column strip down a chunk of rows.
@@ -32,7 +33,9 @@ __global__ void __launch_bounds__(SW * 3, 4) ssim_map_kernel(LossParams lp,
                                                           float* __restrict__ maps,
                                                           double* __restrict__ sums) {
   constexpr int RW = SW + HALO;  // input columns of a strip
-  __shared__ float sx[3][RW], sy[3][RW];
+  // per input column of the current row: x, y, x^2, y^2, xy in fp64, formed
+  // once per element instead of once per tap
+  __shared__ double sv[3][5][RW];
   const int lane = threadIdx.x, c = threadIdx.y, tid = c * SW + lane;
   const int C = lp.C;
   const int x0 = blockIdx.x * SW, oy0 = blockIdx.y * RCH;
@@ -70,8 +73,13 @@ __global__ void __launch_bounds__(SW * 3, 4) ssim_map_kernel(LossParams lp,
         for (int m = 0; m < PER; ++m) {
           const int e = tid + m * SW * 3;
           if (e < RW * C) {
-            sx[e % C][e / C] = px[m];
-            sy[e % C][e / C] = py[m];
+            const double xv = px[m], yv = py[m];
+            double* d = &sv[e % C][0][e / C];
+            d[0] = xv;
+            d[RW] = yv;
+            d[2 * RW] = xv * xv;
+            d[3 * RW] = yv * yv;
+            d[4 * RW] = xv * yv;
           }
         }
         __syncthreads();
@@ -79,17 +87,23 @@ __global__ void __launch_bounds__(SW * 3, 4) ssim_map_kernel(LossParams lp,
         for (int m = 0; m < PER; ++m) px[m] = qx[m], py[m] = qy[m];
         fetch(yi + 2, qx, qy);
         // horizontal sums of this input row at column xcol
-        double hx = 0, hy = 0, hxx = 0, hyy = 0, hxy = 0;
+        // two interleaved chains per statistic (taps 0..5 and 6..10)
+        double h[5], h2[5];
+        const double(*row)[RW] = sv[c < C ? c : 0];
 #pragma unroll
-        for (int k = 0; k < WIN; ++k) {
-          const double xv = sx[c < C ? c : 0][lane + k], yv = sy[c < C ? c : 0][lane + k];
-          const double gx = lp.g[k] * xv, gy = lp.g[k] * yv;
-          hx += gx;
-          hy += gy;
-          hxx = fma(gx, xv, hxx);
-          hxy = fma(gx, yv, hxy);
-          hyy = fma(gy, yv, hyy);
+        for (int q = 0; q < 5; ++q) {
+          h[q] = lp.g[0] * row[q][lane];
+          h2[q] = lp.g[6] * row[q][lane + 6];
         }
+#pragma unroll
+        for (int k = 1; k < 6; ++k)
+#pragma unroll
+          for (int q = 0; q < 5; ++q) {
+            h[q] = fma(lp.g[k], row[q][lane + k], h[q]);
+            if (k + 6 < WIN) h2[q] = fma(lp.g[k + 6], row[q][lane + k + 6], h2[q]);
+          }
+        const double hx = h[0] + h2[0], hy = h[1] + h2[1], hxx = h[2] + h2[2],
+                     hyy = h[3] + h2[3], hxy = h[4] + h2[4];
         // scatter into the 11 rotating vertical accumulators (tap t -> output row yi - t)
 #pragma unroll
         for (int t = 0; t < WIN; ++t) {
@@ -112,7 +126,8 @@ __global__ void __launch_bounds__(SW * 3, 4) ssim_map_kernel(LossParams lp,
           const double inv = 1.0 / (b1 * b2);
           const double sv = a1 * a2 * inv;
           ssum += sv;
-          const double ga1 = a2 * inv, ga2 = a1 * inv, gb1 = -sv / b1, gb2 = -sv / b2;
+          // one division: sv / b1 = sv b2 inv, sv / b2 = sv b1 inv
+          const double ga1 = a2 * inv, ga2 = a1 * inv, gb1 = -sv * b2 * inv, gb2 = -sv * b1 * inv;
           const double gmx = 2.0 * my * ga1 + 2.0 * mx * gb1 - 2.0 * my * ga2 - 2.0 * mx * gb2;
           const int64_t oo = (int64_t)o * lp.Wv + xcol;
           maps[(0 * C + c) * plane + oo] = (float)gmx;
@@ -170,7 +185,6 @@ __global__ void __launch_bounds__(SW * 3, 5) ssim_grad_kernel(LossParams lp,
   float a0[WIN], a1[WIN], a2[WIN];
 #pragma unroll
   for (int j = 0; j < WIN; ++j) a0[j] = a1[j] = a2[j] = 0.f;
-  const double size = (double)lp.H * lp.W * C;
   double l1 = 0.0;
   // walk map rows r = ry0 .. oy1 - 1 (rows >= Hv contribute zero); output row
   // y = r completes after map row r (tap 0): accumulator slot y mod 11
@@ -181,7 +195,7 @@ __global__ void __launch_bounds__(SW * 3, 5) ssim_grad_kernel(LossParams lp,
       l1 += fabs((double)x - (double)t);
       const double sgn = d > 0.f ? 1.0 : (d < 0.f ? -1.0 : 0.0);
       const double back = (double)b0 + (double)b1 * 2.0 * x + (double)b2 * t;
-      grad[o] = (float)((1.0 - lp.lam) * sgn / size + lp.up * back);
+      grad[o] = (float)(lp.l1w * sgn + lp.up * back);
     }
   };
   fetch(ry0, pm, pi0, pt0);
@@ -276,6 +290,7 @@ int ss_render_loss(const float* image, const float* target, int32_t height, int3
   for (int k = 0; k < WIN; ++k) lp.g[k] /= tot;
   lp.c1 = c1, lp.c2 = c2, lp.lam = lam;
   lp.up = -lam / (2.0 * (double)lp.Hv * lp.Wv * channels);
+  lp.l1w = (1.0 - lam) / ((double)height * width * channels);
   double* sums = static_cast<double*>(scratch);
   float* maps = reinterpret_cast<float*>(static_cast<char*>(scratch) + align_up(2 * sizeof(double)));
   prof_begin(PH_LOSS, st);

@@ -550,6 +550,23 @@ __device__ inline float alpha_from_log2(const BlendParams& bp, float lg, float o
   return a < bp.skip ? 0.f : a;
 }
 
+// Fast-path alpha decision on the log2 form.  rank_kernel sets the reject
+// threshold q.w = log2(skip (1 - 2e-4) / op); a live pair with
+// lg >= q.w + kNearBand (= log2(skip (1 + 1e-4) / op)) has alpha above skip
+// beyond any fp32 rounding, so only pairs inside [q.w, q.w + kNearBand) need
+// the float64 decision (taken on a rare, per-thread branch).
+constexpr float kNearBand = 4.3284e-4f;  // log2(1 + 1e-4) - log2(1 - 2e-4), rounded up
+
+__device__ __noinline__ float alpha_f64(const BlendParams& bp, const Geom& g, int rank, float px,
+                                        float py) {
+  const double2 m = g.r_mean[rank];
+  const double4 c = g.r_conop_d[rank];
+  const double ddx = (double)px - m.x, ddy = (double)py - m.y;
+  const double mh = c.x * ddx * ddx + c.y * ddx * ddy + c.z * ddy * ddy;
+  const double ad = fmin(bp.clamp_d, c.w * exp(-0.5 * mh));
+  return ad < bp.skip_d ? 0.f : fmaxf((float)ad, bp.skip);
+}
+
 template <int TS>
 struct BlendShape {
   // 16x16 tiles: 128 threads with two pixels each (rows r and r + 8), which halves
@@ -619,31 +636,29 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_fwd_kernel(
       int contrib = 0;
       if (!TOUCH) {  // fast path: reject on the log2 form before the exponential
         const float4 q = s_q[k];
+        const float qhi = q.w + kNearBand;
         float lgs[PPT];
-        bool live[PPT], any_live = false;
+        bool live[PPT], any_live = false, any_near = false;
 #pragma unroll
         for (int p = 0; p < PPT; ++p) {
           lgs[p] = log2_gauss(q, lx[p] - xy.x, ly[p] - xy.y);
           live[p] = !done[p] && !(lgs[p] < q.w);
           any_live |= live[p];
+          any_near |= live[p] && lgs[p] < qhi;
         }
         if (!__any_sync(0xffffffffu, any_live)) continue;  // warp-uniform skip
         const float4 col = s_col[k];
+        float av[PPT];
+#pragma unroll
+        for (int p = 0; p < PPT; ++p) av[p] = live[p] ? fminf(bp.clamp, col.w * ex2_approx(lgs[p])) : 0.f;
+        if (any_near) {  // rare: decide in float64
+#pragma unroll
+          for (int p = 0; p < PPT; ++p)
+            if (live[p] && lgs[p] < qhi) av[p] = alpha_f64(bp, g, s_rank[k], lx[p] + x0, ly[p] + y0);
+        }
 #pragma unroll
         for (int p = 0; p < PPT; ++p) {  // predicated: a = 0 leaves the pixel unchanged
-          const float G = ex2_approx(lgs[p]);
-          float a = fminf(bp.clamp, col.w * G);
-          if (fabsf(a - bp.skip) <= 1e-4f * bp.skip) {  // rare: decide in float64
-            const double2 m = g.r_mean[s_rank[k]];
-            const double4 c = g.r_conop_d[s_rank[k]];
-            const double ddx = (double)(lx[p] + x0) - m.x, ddy = (double)(ly[p] + y0) - m.y;
-            const double mh = c.x * ddx * ddx + c.y * ddx * ddy + c.z * ddy * ddy;
-            const double ad = fmin(bp.clamp_d, c.w * exp(-0.5 * mh));
-            a = ad < bp.skip_d ? 0.f : fmaxf((float)ad, bp.skip);
-          } else {
-            a = a < bp.skip ? 0.f : a;
-          }
-          a = live[p] ? a : 0.f;
+          const float a = av[p];
           const float wgt = a * T[p];
           C[p][0] = fmaf(wgt, col.x, C[p][0]);
           C[p][1] = fmaf(wgt, col.y, C[p][1]);
@@ -732,14 +747,17 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_bwd_kernel(
   constexpr int NT = BlendShape<TS>::NT, PPT = BlendShape<TS>::PPT;
   constexpr int NA = 9;  // colour 3, mean2d 2, conic 3, opacity
   __shared__ float2 s_xy[NT];
-  __shared__ float4 s_co[NT];
   __shared__ float4 s_q[NT];
   __shared__ float4 s_col[NT];
   __shared__ int s_rank[NT];
-  __shared__ float s_acc[NT * NA];
+  // each warp owns a slot per splat (plain stores, summed at the flush);
+  // larger tiles share one slot through shared-memory atomics
+  constexpr bool PRIV = NT / 32 <= 4;
+  constexpr int NW = PRIV ? NT / 32 : 1;
+  __shared__ float s_acc[NW * NT * NA];  // [warp][splat][term]
   __shared__ int s_any[NT];
   __shared__ int s_last;
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int tile = blockIdx.x;
   const int x0 = (tile % bp.ntx) * TS, y0 = (tile / bp.ntx) * TS;
   const int2 range = g.ranges[tile];
@@ -769,7 +787,7 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_bwd_kernel(
     max_last = max(max_last, last[p]);
   }
   if (threadIdx.x == 0) s_last = 0;
-  for (int i = threadIdx.x; i < NT * NA; i += NT) s_acc[i] = 0.f;
+  for (int i = threadIdx.x; i < NW * NT * NA; i += NT) s_acc[i] = 0.f;
   s_any[threadIdx.x] = 0;
   __syncthreads();
   atomicMax(&s_last, max_last);
@@ -783,7 +801,6 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_bwd_kernel(
       const int r = (int)vals[pos];
       const double2 m = g.r_mean[r];
       s_xy[threadIdx.x] = make_float2((float)(m.x - x0), (float)(m.y - y0));
-      s_co[threadIdx.x] = g.r_conop[r];
       s_q[threadIdx.x] = g.r_q[r];
       s_col[threadIdx.x] = g.r_color[r];
       s_rank[threadIdx.x] = r;
@@ -793,10 +810,11 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_bwd_kernel(
       const int pos_rel = end - 1 - k - range.x;
       const float2 xy = s_xy[k];
       const float4 q = s_q[k];
+      const float qhi = q.w + kNearBand;
       // cheap part for every pixel, then a warp-uniform skip; the rest is
       // predicated (a = 0 makes every update a no-op) instead of branching
       float dxs[PPT], dys[PPT], lgs[PPT];
-      bool live[PPT], any_live = false;
+      bool live[PPT], any_live = false, any_near = false;
 #pragma unroll
       for (int p = 0; p < PPT; ++p) {
         dxs[p] = lx[p] - xy.x;
@@ -804,30 +822,30 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_bwd_kernel(
         lgs[p] = log2_gauss(q, dxs[p], dys[p]);  // same decisions as the forward
         live[p] = pos_rel < last[p] && !(lgs[p] < q.w);
         any_live |= live[p];
+        any_near |= live[p] && lgs[p] < qhi;
       }
       if (!__any_sync(0xffffffffu, any_live)) continue;
       const float4 col = s_col[k];
-      const float4 co = s_co[k];
-      // d(maha)/d(mean2d) and conic coefficients: mean grads += (-2C d) dm
-      const float k1 = -2.f * co.x, k2 = -co.y, k3 = -2.f * co.z;
+      float Gs[PPT], av[PPT];
+#pragma unroll
+      for (int p = 0; p < PPT; ++p) {
+        Gs[p] = ex2_approx(lgs[p]);
+        av[p] = live[p] ? fminf(bp.clamp, col.w * Gs[p]) : 0.f;
+      }
+      if (any_near) {  // rare: decide in float64
+#pragma unroll
+        for (int p = 0; p < PPT; ++p)
+          if (live[p] && lgs[p] < qhi) av[p] = alpha_f64(bp, g, s_rank[k], lx[p] + x0, ly[p] + y0);
+      }
+      // d(maha)/d(mean2d) and conic coefficients: mean grads += (-2C d) dm,
+      // with the conic recovered from the log2 form q = -0.5 log2(e) conic
+      constexpr float kc = 2.7725887222397811f;  // 4 / log2(e)
+      const float k1 = kc * q.x, k2 = 0.5f * kc * q.y, k3 = kc * q.z;
       float v[NA] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
       bool any = false;
 #pragma unroll
       for (int p = 0; p < PPT; ++p) {
-        const float G = ex2_approx(lgs[p]);
-        const float og = col.w * G;
-        float a = fminf(bp.clamp, og);
-        if (fabsf(a - bp.skip) <= 1e-4f * bp.skip) {  // rare: decide in float64
-          const double2 m = g.r_mean[s_rank[k]];
-          const double4 c = g.r_conop_d[s_rank[k]];
-          const double ddx = (double)(lx[p] + x0) - m.x, ddy = (double)(ly[p] + y0) - m.y;
-          const double mh = c.x * ddx * ddx + c.y * ddx * ddy + c.z * ddy * ddy;
-          const double ad = fmin(bp.clamp_d, c.w * exp(-0.5 * mh));
-          a = ad < bp.skip_d ? 0.f : fmaxf((float)ad, bp.skip);
-        } else {
-          a = a < bp.skip ? 0.f : a;
-        }
-        a = live[p] ? a : 0.f;
+        const float G = Gs[p], og = col.w * G, a = av[p];
         // one approximate reciprocal serves T_before = T / (1 - a) and S / (1 - a)
         const float ioma = rcp_approx(fmaxf(1.f - a, 1e-12f));
         const float tb = T[p] * ioma;
@@ -873,10 +891,17 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_bwd_kernel(
         }
         h1 += __shfl_xor_sync(0xffffffffu, h1, 2);
         h1 += __shfl_xor_sync(0xffffffffu, h1, 1);
-        if ((lane & 3) == 0) atomicAdd(&s_acc[k * NA + (lane >> 2)], h1);
+        float* slot = s_acc + ((PRIV ? warp : 0) * NT + k) * NA;
+        if ((lane & 3) == 0) {
+          if (PRIV) slot[lane >> 2] = h1;
+          else atomicAdd(slot + (lane >> 2), h1);
+        }
         if (FULL) {
           const float o = warp_sum(v[8]);
-          if (lane == 0) atomicAdd(&s_acc[k * NA + 8], o);
+          if (lane == 0) {
+            if (PRIV) slot[8] = o;
+            else atomicAdd(slot + 8, o);
+          }
         }
         if (lane == 0) s_any[k] = 1;
       }
@@ -885,13 +910,22 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_bwd_kernel(
     // flush this batch's per-splat sums (one row per splat) and reset them
     if (threadIdx.x < cnt && s_any[threadIdx.x]) {
       float* a = g.acc + (int64_t)s_rank[threadIdx.x] * kAccStride;
-      float* sa = s_acc + threadIdx.x * NA;
-      red_add_v4(a, sa[0], sa[1], sa[2], sa[3]);
-      red_add_v4(a + 4, sa[4], sa[5], sa[6], sa[7]);
-      if (FULL) atomicAdd(a + 8, sa[8]);
-      g.touched[s_rank[threadIdx.x]] = 1;
+      float t[NA];
 #pragma unroll
-      for (int q = 0; q < NA; ++q) sa[q] = 0.f;
+      for (int q = 0; q < NA; ++q) t[q] = 0.f;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) {
+        float* sa = s_acc + (w * NT + threadIdx.x) * NA;
+#pragma unroll
+        for (int q = 0; q < NA; ++q) {
+          t[q] += sa[q];
+          sa[q] = 0.f;
+        }
+      }
+      red_add_v4(a, t[0], t[1], t[2], t[3]);
+      red_add_v4(a + 4, t[4], t[5], t[6], t[7]);
+      if (FULL) atomicAdd(a + 8, t[8]);
+      g.touched[s_rank[threadIdx.x]] = 1;
       s_any[threadIdx.x] = 0;
     }
     __syncthreads();
