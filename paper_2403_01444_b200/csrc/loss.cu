@@ -3,8 +3,7 @@
 //   L = (1-lam) mean|x-y| + lam (1 - mean_valid SSIM) / 2,
 // 11x11 Gaussian window (sigma 1.5), VALID windows only, mean over windows x
 // channels; the SSIM adjoint is a FULL convolution of three per-window maps.
-// Separable 11-tap strip walks (below); window moments in fp32 on shifted
-// data, per-window SSIM algebra in fp64.
+// Separable 11-tap strip walks (below) in fp32, window moments on shifted data.
 #include "common.cuh"
 
 namespace ss {
@@ -16,6 +15,7 @@ constexpr int RCH = 60;  // rows per chunk: 42 x 17 CTAs of 3 warps at 1352x1014
 struct LossParams {
   int H, W, Hv, Wv, C;
   double g[WIN];
+  float gf[WIN];  // fp32 copy: FFMA operands straight from the parameter bank
   double c1, c2, lam, up;  // up = -lam / (2 n_windows)
   double l1w;              // (1 - lam) / (H W C)
 };
@@ -33,10 +33,9 @@ struct LossParams {
 // a per-channel constant (the pixel at its first row, strip centre) from x and
 // y.  Variances and the covariance are shift-invariant, so the shift removes
 // the E[x^2] - mu^2 cancellation that would otherwise cost fp32 its accuracy in
-// flat regions; the means get the constant added back and the per-window
-// SSIM / adjoint algebra runs in fp64.  Against the all-fp64 statistics the
-// per-window SSIM differs by <= 3e-5 and the mean by ~1e-10 (smooth, flat and
-// noise images, 1352x1014).
+// flat regions; the means get the constant added back.  Against all-fp64
+// statistics the per-window SSIM differs by <= 3e-5 and the mean by ~1e-10
+// (smooth, flat and noise images, 1352x1014).
 //
 // The vertical pass keeps acc[j] = partial sum of output row yi - 10 + j; each
 // input row completes acc[0] and shifts the rest down inside the FMAs, so the
@@ -93,8 +92,9 @@ __global__ void __launch_bounds__(SW * 3, 5) ssim_map_kernel(LossParams lp,
   for (int j = 0; j < WIN; ++j) ax[j] = ay[j] = as[j] = axy[j] = 0.f;
   float g[WIN];
 #pragma unroll
-  for (int k = 0; k < WIN; ++k) g[k] = (float)lp.g[k];
+  for (int k = 0; k < WIN; ++k) g[k] = lp.gf[k];
   double ssum = 0.0;
+  const float c1f = (float)lp.c1, c2f = (float)lp.c2;
   const int64_t plane = (int64_t)lp.Hv * lp.Wv;
   // buffers: P holds row yi + 1 at the start of an even step, Q row yi + 2;
   // each step stages one and refills it three rows ahead
@@ -129,21 +129,22 @@ __global__ void __launch_bounds__(SW * 3, 5) ssim_map_kernel(LossParams lp,
     ax[HALO] = ay[HALO] = as[HALO] = axy[HALO] = 0.f;
     const int o = yi - HALO;
     if (o >= oy0 && col_ok) {
-      const double sx = mx0, sy = my0;  // shifted means
-      const double vsum = (double)ss - sx * sx - sy * sy, cxy = (double)sxy - sx * sy;
-      const double mx = sx + shx, my = sy + shy;
-      const double a1 = 2.0 * mx * my + lp.c1, a2 = 2.0 * cxy + lp.c2;
-      const double b1 = mx * mx + my * my + lp.c1, b2 = vsum + lp.c2;
-      const double inv = 1.0 / (b1 * b2);
-      const double sv_ = a1 * a2 * inv;
-      ssum += sv_;
+      // per-window algebra in fp32 (the maps are stored in fp32 anyway); the
+      // shifted moments carry no cancellation, the SSIM sum is kept in fp64
+      const float vsum = ss - mx0 * mx0 - my0 * my0, cxy = sxy - mx0 * my0;
+      const float mx = mx0 + shx, my = my0 + shy;
+      const float a1 = 2.f * mx * my + c1f, a2 = 2.f * cxy + c2f;
+      const float b1 = mx * mx + my * my + c1f, b2 = vsum + c2f;
+      const float inv = 1.f / (b1 * b2);
+      const float sv_ = a1 * a2 * inv;
+      ssum += (double)sv_;
       // one division: sv / b1 = sv b2 inv, sv / b2 = sv b1 inv
-      const double ga1 = a2 * inv, ga2 = a1 * inv, gb1 = -sv_ * b2 * inv, gb2 = -sv_ * b1 * inv;
-      const double gmx = 2.0 * my * ga1 + 2.0 * mx * gb1 - 2.0 * my * ga2 - 2.0 * mx * gb2;
+      const float ga1 = a2 * inv, ga2 = a1 * inv, gb1 = -sv_ * b2 * inv, gb2 = -sv_ * b1 * inv;
+      const float gmx = 2.f * (my * (ga1 - ga2) + mx * (gb1 - gb2));
       const int64_t oo = (int64_t)o * lp.Wv + xcol;
-      maps[(0 * C + c) * plane + oo] = (float)gmx;
-      maps[(1 * C + c) * plane + oo] = (float)gb2;
-      maps[(2 * C + c) * plane + oo] = (float)(2.0 * ga2);
+      maps[(0 * C + c) * plane + oo] = gmx;
+      maps[(1 * C + c) * plane + oo] = gb2;
+      maps[(2 * C + c) * plane + oo] = 2.f * ga2;
     }
     __syncwarp();
   };
@@ -176,7 +177,7 @@ __global__ void __launch_bounds__(SW * 3, 5) ssim_grad_kernel(LossParams lp,
   const int64_t plane = (int64_t)lp.Hv * lp.Wv;
   float g[WIN];
 #pragma unroll
-  for (int k = 0; k < WIN; ++k) g[k] = (float)lp.g[k];
+  for (int k = 0; k < WIN; ++k) g[k] = lp.gf[k];
   // prefetch: lane loads map q of channel c at columns x0 - 10 + lane (+32)
   constexpr int PER = 2;
   float pm[3][PER], qm[3][PER];  // map rows in flight
@@ -305,6 +306,7 @@ int ss_render_loss(const float* image, const float* target, int32_t height, int3
     tot += lp.g[k];
   }
   for (int k = 0; k < WIN; ++k) lp.g[k] /= tot;
+  for (int k = 0; k < WIN; ++k) lp.gf[k] = (float)lp.g[k];
   lp.c1 = c1, lp.c2 = c2, lp.lam = lam;
   lp.up = -lam / (2.0 * (double)lp.Hv * lp.Wv * channels);
   lp.l1w = (1.0 - lam) / ((double)height * width * channels);

@@ -273,7 +273,8 @@ def test_stage1_no_sync_matches_synchronised_path(P):
     torch.cuda.synchronize()
     assert b.check_status() == 0
     np.testing.assert_allclose(b.pairs_of_last(5), ref_pairs, rtol=1e-3)
-    np.testing.assert_allclose(b.loss_hist[1:6].cpu().numpy(), ref_losses, rtol=1e-6)
+    # later steps differ only by float-atomic accumulation order
+    np.testing.assert_allclose(b.loss_hist[1:6].cpu().numpy(), ref_losses, rtol=2e-5)
     assert close(a.tables, b.tables) and close(a.params, b.params)
     # run() with a deliberately tiny workspace: overflow -> replay with a larger one
     c, d = trainer(), trainer()
