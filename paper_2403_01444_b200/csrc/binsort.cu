@@ -25,6 +25,7 @@ constexpr int kBsStepsBig = 8;    // items per lane (2048-item tiles)
 constexpr int kBsStepsSmall = 4;  // 1024-item tiles for small sorts (more CTAs)
 constexpr uint32_t kFlagAgg = 1u << 30, kFlagInc = 2u << 30, kCntMask = (1u << 30) - 1;
 constexpr int kMaxPasses = 4;
+constexpr int kWin = 8;  // look-back window (predecessor flags read per round trip)
 
 __device__ __forceinline__ uint32_t lanemask_lt() {
   uint32_t m;
@@ -143,13 +144,26 @@ __global__ void __launch_bounds__(kBsThreads) bs_pass_kernel(
     atomicExch(my, kFlagInc | cnt);
   } else {
     atomicExch(my, kFlagAgg | cnt);
-    for (int64_t p = (int64_t)bid - 1; p >= 0; --p) {
-      uint32_t st;
-      do {
-        st = ld_volatile(status + (size_t)p * 256 + d);
-      } while ((st & ~kCntMask) == 0);
-      excl += st & kCntMask;
-      if (st & kFlagInc) break;
+    // windowed look-back: kWin predecessors' flags in flight per round trip,
+    // consumed nearest first up to the first inclusive prefix; a predecessor
+    // that has not published yet is re-polled at the start of the next window
+    int64_t p = (int64_t)bid - 1;
+    bool done = false;
+    while (!done) {
+      uint32_t st[kWin];
+#pragma unroll
+      for (int j = 0; j < kWin; ++j)
+        st[j] = p - j >= 0 ? ld_volatile(status + (size_t)(p - j) * 256 + d) : kFlagInc;
+      int used = 0;
+#pragma unroll
+      for (int j = 0; j < kWin; ++j) {
+        if (done || used < j) continue;  // stopped at an inclusive or unready flag
+        if ((st[j] & ~kCntMask) == 0) continue;  // not published: re-poll from here
+        excl += st[j] & kCntMask;
+        used = j + 1;
+        done = (st[j] & kFlagInc) != 0;
+      }
+      p -= used;
     }
     atomicExch(my, kFlagInc | (excl + cnt));
   }
