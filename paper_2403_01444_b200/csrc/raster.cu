@@ -746,6 +746,9 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_bwd_kernel(
     BlendParams bp, Geom g, const uint32_t* __restrict__ vals, const float* __restrict__ d_image) {
   constexpr int NT = BlendShape<TS>::NT, PPT = BlendShape<TS>::PPT;
   constexpr int NA = 9;  // colour 3, mean2d 2, conic 3, opacity
+  // d(maha)/d(mean2d) = -2C d, with the conic recovered from the log2 form
+  // q = -0.5 log2(e) conic: k1, k2, k3 = kc (q.x, q.y / 2, q.z)
+  constexpr float kc = 2.7725887222397811f;  // 4 / log2(e)
   __shared__ float2 s_xy[NT];
   __shared__ float4 s_q[NT];
   __shared__ float4 s_col[NT];
@@ -837,10 +840,6 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_bwd_kernel(
         for (int p = 0; p < PPT; ++p)
           if (live[p] && lgs[p] < qhi) av[p] = alpha_f64(bp, g, s_rank[k], lx[p] + x0, ly[p] + y0);
       }
-      // d(maha)/d(mean2d) and conic coefficients: mean grads += (-2C d) dm,
-      // with the conic recovered from the log2 form q = -0.5 log2(e) conic
-      constexpr float kc = 2.7725887222397811f;  // 4 / log2(e)
-      const float k1 = kc * q.x, k2 = 0.5f * kc * q.y, k3 = kc * q.z;
       float v[NA] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
       bool any = false;
 #pragma unroll
@@ -859,10 +858,12 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_bwd_kernel(
         T[p] = tb;
         // no contribution, or flat above the clamp (rasterizer.py:336-337)
         da = (a > 0.f && og < bp.clamp) ? da : 0.f;
-        const float dm = -0.5f * og * da;
+        // dm = -0.5 og da; the -0.5 and the conic factors k1..k3 are per-splat
+        // constants applied once at the flush (terms 3, 4 hold sum e, sum f)
+        const float dm = og * da;
         const float e = dm * dxs[p], f = dm * dys[p];
-        v[3] = fmaf(k1, e, fmaf(k2, f, v[3]));
-        v[4] = fmaf(k2, e, fmaf(k3, f, v[4]));
+        v[3] += e;
+        v[4] += f;
         v[5] = fmaf(e, dxs[p], v[5]);
         v[6] = fmaf(e, dys[p], v[6]);
         v[7] = fmaf(f, dys[p], v[7]);
@@ -921,6 +922,16 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_bwd_kernel(
           t[q] += sa[q];
           sa[q] = 0.f;
         }
+      }
+      {  // mean2d = -0.5 (-2C) [sum e, sum f]; conic terms times -0.5
+        const float4 q = s_q[threadIdx.x];
+        const float k1 = kc * q.x, k2 = 0.5f * kc * q.y, k3 = kc * q.z;
+        const float E = t[3], F = t[4];
+        t[3] = -0.5f * fmaf(k1, E, k2 * F);
+        t[4] = -0.5f * fmaf(k2, E, k3 * F);
+        t[5] *= -0.5f;
+        t[6] *= -0.5f;
+        t[7] *= -0.5f;
       }
       red_add_v4(a, t[0], t[1], t[2], t[3]);
       red_add_v4(a + 4, t[4], t[5], t[6], t[7]);
