@@ -352,6 +352,14 @@ int32_t ss_get_mlp_mode(void);
 // Debug: clock64 stamps of CTA 0 / thread 0 at the decoder kernels' stage
 // boundaries (out: 2 x 64 uint64, forward then backward).
 int ss_debug_mlp_trace(uint64_t* out);
+/* Decoder-forward event clocks of CTA 0 (debug): out[0..127] epilogue thread 0
+   (TMEM stores published / MMA completion seen), out[128..255] MMA lane
+   (operands ready seen / MMAs committed). */
+int ss_debug_mlp_events(uint64_t* out);
+/* Debug: cycles of `count` back-to-back M = 128 tcgen05 MMAs (kind 0 tf32, 1 bf16;
+   a_tmem: tf32 A operand from TMEM); out_dev[0] total incl. completion, [1] issue. */
+int ss_debug_umma_rate(int32_t kind, int32_t N, int32_t a_tmem, int32_t count, uint64_t* out_dev,
+                       void* stream);
 
 int ss_selftest_umma(int32_t M, int32_t N, int32_t K, int32_t flags, const float* A,
                      const float* B, float* D, void* stream);

@@ -133,6 +133,8 @@ SIGNATURES = [
     ("ss_get_mlp_mode", I32, []),
     ("ss_selftest_umma", I32, [I32, I32, I32, I32, P, P, P, P]),
     ("ss_debug_mlp_trace", I32, [P]),
+    ("ss_debug_mlp_events", I32, [P]),
+    ("ss_debug_umma_rate", I32, [I32, I32, I32, I32, P, P]),
 ]
 
 

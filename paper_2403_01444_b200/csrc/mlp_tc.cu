@@ -24,6 +24,13 @@ namespace ss {
 
 // per-stage clock64 stamps of CTA 0, thread 0, first tiles (ss_debug_mlp_trace)
 __device__ unsigned long long g_mlp_trace[2][64];
+// forward event stamps of CTA 0: [0] epilogue thread 0, [1] MMA lane (ss_debug_mlp_events)
+__device__ unsigned long long g_mlp_ev[2][128];
+#define SS_EV(k, cnt)                                                              \
+  do {                                                                           \
+    if (blockIdx.x == 0 && (cnt) < 128) g_mlp_ev[k][(cnt)] = clock64();          \
+    ++(cnt);                                                                     \
+  } while (0)
 #define SS_STAMP(k, i)                                                           \
   do {                                                                           \
     if (blockIdx.x == 0 && threadIdx.x == 0 && (i) < 64) g_mlp_trace[k][i] = clock64(); \
@@ -55,17 +62,15 @@ __device__ __forceinline__ void sync_mma(uint64_t* bar, uint32_t& phase) {
 
 // ---------------------------------------------------------------- tf32 pieces
 template <int IN, int NL, int P>
-struct TcFwdSmem {
+struct TcFwdSmem {  // the weights only: activations live in TMEM
+  static constexpr int PL = P == 3 ? 2 : 1;  // hi (+ lo) planes
   static constexpr uint32_t W0 = umma::tile_bytes(64, IN);
   static constexpr uint32_t W1 = NL == 2 ? umma::tile_bytes(64, 64) : 0;
   static constexpr uint32_t W2 = umma::tile_bytes(16, 64);
-  static constexpr uint32_t A = umma::tile_bytes(128, 64);
   static constexpr uint32_t oW0 = 0;
-  static constexpr uint32_t oW1 = oW0 + (P == 3 ? 2 : 1) * W0;
-  static constexpr uint32_t oW2 = oW1 + (P == 3 ? 2 : 1) * W1;
-  static constexpr uint32_t oA0 = oW2 + (P == 3 ? 2 : 1) * W2;
-  static constexpr uint32_t oA1 = oA0 + (P == 3 ? 2 : 1) * A;
-  static constexpr uint32_t BYTES = oA1 + (P == 3 ? 2 : 1) * A;
+  static constexpr uint32_t oW1 = oW0 + PL * W0;
+  static constexpr uint32_t oW2 = oW1 + PL * W1;
+  static constexpr uint32_t BYTES = oW2 + PL * W2;
 };
 
 // write x as (hi, lo) tf32 pair into the hi tile and (for P = 3) the lo tile
@@ -191,31 +196,42 @@ struct XSlice {
 }  // namespace
 
 // ================================================================= forward
+// Warp-specialised: 16 epilogue warps + 1 MMA warp.  Every activation operand
+// lives in TMEM (tcgen05.mma with A from tensor memory), so a layer's epilogue
+// is tcgen05.ld (accumulator) -> bias, ReLU, tf32 hi/lo split -> tcgen05.st
+// (next layer's A operand); only the weights (B operands) are in shared
+// memory.  Two 128-row tiles are in flight (slots 0 and 1): while the
+// epilogue warps work on one slot, the MMA warp runs the other's layer.
+// Handshakes are mbarriers (ready[s]: 16 warp arrivals after the TMEM
+// stores; done[s]: tcgen05.commit), never a CTA-wide barrier.
+//
+// TMEM of slot s (base 256 s): [0, 64) A hi, [64, 128) A lo (X, then h1,
+// then h2), [128, 192) acc1 / acc2, [192, 208) acc3.
+constexpr int NT_FWD = NT + 32;
+
 template <int IN, int NL, int P>
-__global__ void __launch_bounds__(NT, 1) mlp_fwd_tc_kernel(int64_t n, const float* __restrict__ X,
-                                                           int xs, const float* __restrict__ params,
-                                                           float* __restrict__ out, int os,
-                                                           uint64_t* __restrict__ relu_masks) {
+__global__ void __launch_bounds__(NT_FWD, 1) mlp_fwd_tc_kernel(int64_t n, const float* __restrict__ X,
+                                                               int xs, const float* __restrict__ params,
+                                                               float* __restrict__ out, int os,
+                                                               uint64_t* __restrict__ relu_masks) {
   using L = TcLay<IN, NL>;
   using S = TcFwdSmem<IN, NL, P>;
   extern __shared__ __align__(1024) uint8_t sm[];
-  __shared__ uint64_t bar;
+  __shared__ uint64_t ready[2], done[2];
   __shared__ uint32_t tbase;
   __shared__ float sbias[64 + 64 + 8];
-  __shared__ uint16_t smask[2][4][128];
   const int tid = threadIdx.x, warp = tid >> 5;
-  const int r = tid & 127, q = tid >> 7;
   // ---- stage the weights as K-major B tiles (rows = output unit, cols = input)
-  for (int i = tid; i < 64 * IN; i += NT) {
+  for (int i = tid; i < 64 * IN; i += NT_FWD) {
     const int nn = i / IN, k = i % IN;
     put<P>(sm + S::oW0, S::W0, umma::tile_off(nn, k, IN), params[L::W0 + k * 64 + nn]);
   }
   if (NL == 2)
-    for (int i = tid; i < 64 * 64; i += NT) {
+    for (int i = tid; i < 64 * 64; i += NT_FWD) {
       const int nn = i / 64, k = i % 64;
       put<P>(sm + S::oW1, S::W1, umma::tile_off(nn, k, 64), params[L::W1 + k * 64 + nn]);
     }
-  for (int i = tid; i < 16 * 64; i += NT) {
+  for (int i = tid; i < 16 * 64; i += NT_FWD) {
     const int nn = i / 64, k = i % 64;
     put<P>(sm + S::oW2, S::W2, umma::tile_off(nn, k, 64), nn < 8 ? params[L::W2 + k * 8 + nn] : 0.f);
   }
@@ -225,122 +241,140 @@ __global__ void __launch_bounds__(NT, 1) mlp_fwd_tc_kernel(int64_t n, const floa
   }
   if (tid < 8) sbias[128 + tid] = params[L::B2 + tid];
   if (tid == 0) {
-    umma::mbar_init(&bar, 1);
+    for (int s = 0; s < 2; ++s) {
+      umma::mbar_init(&ready[s], NT / 32);
+      umma::mbar_init(&done[s], 1);
+    }
     umma::fence_mbar_init();
   }
-  if (warp == 0) umma::tmem_alloc(&tbase, 256);
+  if (warp == 0) umma::tmem_alloc(&tbase, 512);
   to_async();
   umma::fence_after();
   const uint32_t tmem = tbase;
-  const uint32_t acc1 = tmem, acc2 = tmem + 64, acc3 = tmem + 128;
-  const uint32_t lane = (uint32_t)((warp & 3) * 32) << 16;
-  const Op32 dW0 = op32(umma::smem_u32(sm + S::oW0), S::W0, IN);
-  const Op32 dW1 = op32(umma::smem_u32(sm + S::oW1), S::W1, 64);
-  const Op32 dW2 = op32(umma::smem_u32(sm + S::oW2), S::W2, 64);
-  const Op32 dX0 = op32(umma::smem_u32(sm + S::oA0), S::A, IN);
-  const Op32 dA0 = op32(umma::smem_u32(sm + S::oA0), S::A, 64);
-  const Op32 dA1 = op32(umma::smem_u32(sm + S::oA1), S::A, 64);
-  constexpr uint32_t id64 = umma::idesc_tf32(128, 64, 0, 0);
-  constexpr uint32_t id16 = umma::idesc_tf32(128, 16, 0, 0);
-  const int c0 = 16 * q;  // this thread's accumulator columns
-  uint32_t phase = 0;
   const int64_t ntiles = (n + 127) / 128;
-  XSlice<IN> xr;
-  // X slice of the prefetched tile -> A0 and the first layer's MMAs
-  auto issue_l1 = [&]() {
+  const int64_t G = gridDim.x;
+  constexpr int NLAY = NL == 2 ? 3 : 2;  // MMA layers per tile
+
+  if (warp == NT / 32) {
+    // ================= MMA warp: one elected lane issues, in tile/slot order
+    const Op32 dW0 = op32(umma::smem_u32(sm + S::oW0), S::W0, IN);
+    const Op32 dW1 = op32(umma::smem_u32(sm + S::oW1), S::W1, 64);
+    const Op32 dW2 = op32(umma::smem_u32(sm + S::oW2), S::W2, 64);
+    constexpr uint32_t id64 = umma::idesc_tf32(128, 64, 0, 0);
+    constexpr uint32_t id16 = umma::idesc_tf32(128, 16, 0, 0);
+    uint32_t ph[2] = {0u, 0u};
+    int nev = 0;
+    for (int64_t t0 = blockIdx.x; t0 < ntiles; t0 += 2 * G) {
+      const bool two = t0 + G < ntiles;
 #pragma unroll
-    for (int b = 0; b < XSlice<IN>::NB; ++b) {
-      const int c = 8 * q + 32 * b;
-      if (c < IN) {
-        put4<P>(sm + S::oA0, S::A, umma::tile_off(r, c, IN), xr.v[b]);
-        put4<P>(sm + S::oA0, S::A, umma::tile_off(r, c + 4, IN), xr.v[b] + 4);
+      for (int l = 0; l < NLAY; ++l) {
+        const int layer = l == NLAY - 1 ? 2 : l;
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+          if (s == 1 && !two) continue;
+          umma::mbar_wait(&ready[s], ph[s]);
+          ph[s] ^= 1;
+          umma::fence_after();
+          if ((tid & 31) == 0) SS_EV(1, nev);
+          if ((tid & 31) == 0) {
+            const uint32_t base = tmem + 256u * s;
+            const Op32& B = layer == 0 ? dW0 : (layer == 1 ? dW1 : dW2);
+            const uint32_t acc = base + (layer == 2 ? 192u : 128u);
+            const uint32_t id = layer == 2 ? id16 : id64;
+            const int nk = layer == 0 ? IN / 8 : 8;
+            for (int k = 0; k < nk; ++k) {
+              const uint64_t d = 16ull * k;
+              umma::mma_tf32_ts(acc, base + 8u * k, B.hi + d, id, k > 0);
+              if (P == 3) {
+                umma::mma_tf32_ts(acc, base + 8u * k, B.lo + d, id, 1);
+                umma::mma_tf32_ts(acc, base + 64u + 8u * k, B.hi + d, id, 1);
+              }
+            }
+            umma::commit(&done[s]);
+            SS_EV(1, nev);
+          }
+          __syncwarp();
+        }
       }
     }
-    to_async();
-    if (tid == 0) {
+  } else {
+    // ================= epilogue warps: thread (r, q) = row r, columns 16q..16q+15
+    const int r = tid & 127, q = tid >> 7;
+    const int c0 = 16 * q;
+    const uint32_t lane = (uint32_t)((warp & 3) * 32) << 16;
+    uint32_t ph[2] = {0u, 0u};
+    int nev = 0;
+    XSlice<IN> xr[2];
+    auto load_x = [&](int s, int64_t t) {
+      xr[s].load(X, t * 128 + r, xs, q, t < ntiles && t * 128 + r < n);
+    };
+    auto arrive = [&](int s) {  // this warp's TMEM stores are complete
+      umma::tmem_st_wait();
+      umma::fence_before();
+      __syncwarp();
+      if ((tid & 31) == 0) umma::mbar_arrive(&ready[s]);
+      if (tid == 0) SS_EV(0, nev);
+    };
+    auto put_x = [&](int s) {  // X slice -> A hi / lo columns of slot s
+      const uint32_t base = tmem + 256u * s + lane;
+#pragma unroll
+      for (int b = 0; b < XSlice<IN>::NB; ++b) {
+        const int c = 8 * q + 32 * b;
+        if (c < IN) {
+          float h[8], l[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            h[j] = umma::to_tf32(xr[s].v[b][j]);
+            l[j] = umma::to_tf32(xr[s].v[b][j] - h[j]);
+          }
+          umma::tmem_st8(base + (uint32_t)c, h);
+          if (P == 3) umma::tmem_st8(base + 64u + (uint32_t)c, l);
+        }
+      }
+      arrive(s);
+    };
+    auto wait_done = [&](int s) {
+      umma::mbar_wait(&done[s], ph[s]);
+      ph[s] ^= 1;
       umma::fence_after();
-      mma_layer<P, IN / 8>(acc1, dX0, dW0, id64);
-      umma::commit(&bar);
-    }
-  };
-  if (blockIdx.x < ntiles) {
-    xr.load(X, (int64_t)blockIdx.x * 128 + r, xs, q, (int64_t)blockIdx.x * 128 + r < n);
-    issue_l1();
-  }
-  int it = 0;
-  SS_STAMP(0, 0);
-  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
-    const int64_t row = t * 128 + r;
-    SS_STAMP(0, 1 + 8 * it);
-    {
-      const int64_t nrow = (t + gridDim.x) * 128 + r;
-      xr.load(X, nrow, xs, q, t + gridDim.x < ntiles && nrow < n);
-    }
-    sync_mma(&bar, phase);
-    SS_STAMP(0, 2 + 8 * it);
-    // ---- h1 = relu(acc1 + b0) -> A1 (64 columns), this thread's 16
-    uint32_t m1 = 0, m2 = 0;
-    {
-      float v[16];
-      umma::tmem_ld16(acc1 + lane + c0, v);
+      if (tid == 0) SS_EV(0, nev);
+    };
+    // hidden layer: relu(acc + b) -> A hi / lo of slot s; ReLU mask quarter -> HBM
+    auto hidden = [&](int s, int layer, int64_t t) {
+      wait_done(s);
+      const uint32_t base = tmem + 256u * s + lane;
+      float v[16], l[16];
+      umma::tmem_ld16(base + 128u + (uint32_t)c0, v);
+      uint32_t m = 0;
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
-        v[j] = fmaxf(v[j] + sbias[c0 + j], 0.f);
-        m1 |= (uint32_t)(v[j] > 0.f) << j;
+        const float x = fmaxf(v[j] + sbias[64 * layer + c0 + j], 0.f);
+        m |= (uint32_t)(x > 0.f) << j;
+        v[j] = umma::to_tf32(x);
+        l[j] = umma::to_tf32(x - v[j]);
       }
-#pragma unroll
-      for (int j = 0; j < 16; j += 4) put4<P>(sm + S::oA1, S::A, umma::tile_off(r, c0 + j, 64), v + j);
-    }
-    if (NL == 2) {
-      SS_STAMP(0, 3 + 8 * it);
-      to_async();
-      if (tid == 0) {
-        umma::fence_after();
-        mma_layer<P, 8>(acc2, dA1, dW1, id64);
-        umma::commit(&bar);
+      umma::tmem_st16(base + (uint32_t)c0, v);
+      if (P == 3) umma::tmem_st16(base + 64u + (uint32_t)c0, l);
+      arrive(s);
+      // the backward reuses the forward's ReLU decisions (self-consistent
+      // gradient): 16-bit quarter q of the row's 64-bit mask of this layer
+      const int64_t row = t * 128 + r;
+      if (relu_masks && row < n) {
+        uint16_t* mk = reinterpret_cast<uint16_t*>(relu_masks + 2 * row);
+        mk[4 * layer + q] = (uint16_t)m;
+        if (NL == 1) mk[4 + q] = (uint16_t)m;
       }
-      sync_mma(&bar, phase);
-      SS_STAMP(0, 4 + 8 * it);
-      float v[16];
-      umma::tmem_ld16(acc2 + lane + c0, v);
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        v[j] = fmaxf(v[j] + sbias[64 + c0 + j], 0.f);
-        m2 |= (uint32_t)(v[j] > 0.f) << j;
-      }
-#pragma unroll
-      for (int j = 0; j < 16; j += 4) put4<P>(sm + S::oA0, S::A, umma::tile_off(r, c0 + j, 64), v + j);
-    } else {
-      m2 = m1;
-    }
-    smask[0][q][r] = (uint16_t)m1;
-    smask[1][q][r] = (uint16_t)m2;
-    SS_STAMP(0, 5 + 8 * it);
-    to_async();
-    if (tid == 0) {
-      umma::fence_after();
-      mma_layer<P, 8>(acc3, NL == 2 ? dA0 : dA1, dW2, id16);
-      umma::commit(&bar);
-    }
-    // the backward reuses the forward's ReLU decisions (self-consistent gradient)
-    if (q == 1 && relu_masks && row < n) {
-      uint64_t a = 0, b = 0;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        a |= (uint64_t)smask[0][k][r] << (16 * k);
-        b |= (uint64_t)smask[1][k][r] << (16 * k);
-      }
-      *reinterpret_cast<ulonglong2*>(relu_masks + 2 * row) = make_ulonglong2(a, b);
-    }
-    sync_mma(&bar, phase);
-    SS_STAMP(0, 6 + 8 * it);
-    // ---- the next tile's first layer runs under this tile's output epilogue
-    if (t + gridDim.x < ntiles) issue_l1();
-    SS_STAMP(0, 7 + 8 * it);
-    if (q == 0) {
+    };
+    auto finish = [&](int s, int64_t t) {
+      wait_done(s);
       float o[8];
-      umma::tmem_ld8(acc3 + lane, o);
-      if (row < n) {
+      if (q == 0) umma::tmem_ld8(tmem + 256u * s + lane + 192u, o);
+      if (t + 2 * G < ntiles) {  // the slot's next tile
+        put_x(s);
+        load_x(s, t + 4 * G);
+      }
+      const int64_t row = t * 128 + r;
+      if (q == 0 && row < n) {
         if (os == 8) {
           *reinterpret_cast<float4*>(out + row * 8) = make_float4(
               o[0] + sbias[128], o[1] + sbias[129], o[2] + sbias[130], o[3] + sbias[131]);
@@ -351,13 +385,43 @@ __global__ void __launch_bounds__(NT, 1) mlp_fwd_tc_kernel(int64_t n, const floa
           for (int k = 0; k < 7; ++k) out[row * os + k] = o[k] + sbias[128 + k];
         }
       }
+    };
+    int64_t t0 = blockIdx.x;
+    if (t0 < ntiles) {
+      load_x(0, t0);
+      load_x(1, t0 + G);
+      put_x(0);
+      if (t0 + G < ntiles) put_x(1);
+      load_x(0, t0 + 2 * G);
+      load_x(1, t0 + 3 * G);
+    }
+    SS_STAMP(0, 0);
+    int it = 0;
+    for (; t0 < ntiles; t0 += 2 * G, ++it) {
+      const int64_t t1 = t0 + G;
+      const bool two = t1 < ntiles;
+      SS_STAMP(0, 1 + 8 * it);
+      hidden(0, 0, t0);
+      SS_STAMP(0, 2 + 8 * it);
+      if (two) hidden(1, 0, t1);
+      SS_STAMP(0, 3 + 8 * it);
+      if (NL == 2) {
+        hidden(0, 1, t0);
+        SS_STAMP(0, 4 + 8 * it);
+        if (two) hidden(1, 1, t1);
+      }
+      SS_STAMP(0, 5 + 8 * it);
+      finish(0, t0);
+      SS_STAMP(0, 6 + 8 * it);
+      if (two) finish(1, t1);
+      SS_STAMP(0, 7 + 8 * it);
     }
   }
   umma::fence_before();
   __syncthreads();
   if (warp == 0) {
     umma::fence_after();
-    umma::tmem_free(tmem, 256);
+    umma::tmem_free(tmem, 512);
   }
 }
 
@@ -717,7 +781,7 @@ static int launch_tc(int64_t n, const float* X, int xs, const float* params, flo
   auto k = mlp_fwd_tc_kernel<IN, NL, P>;
   SS_CUDA(smem_attr_once(k, (int)smem));
   const unsigned grid = (unsigned)std::min<int64_t>((n + 127) / 128, (int64_t)num_sms_tc());
-  k<<<grid, NT, smem, st>>>(n, X, xs, params, out, os, masks);
+  k<<<grid, NT_FWD, smem, st>>>(n, X, xs, params, out, os, masks);
   SS_CHECK_LAUNCH("mlp_fwd_tc_kernel");
   return SS_OK;
 }
@@ -775,6 +839,11 @@ extern "C" int ss_set_mlp_mode(int32_t mode) {
 extern "C" int32_t ss_get_mlp_mode(void) { return ss::g_mlp_mode; }
 
 // debug: clock64 stamps of CTA 0 (kernel 0 = forward, 1 = backward), 64 each
+extern "C" int ss_debug_mlp_events(uint64_t* out) {
+  SS_CUDA(cudaMemcpyFromSymbol(out, ss::g_mlp_ev, sizeof(ss::g_mlp_ev)));
+  return SS_OK;
+}
+
 extern "C" int ss_debug_mlp_trace(uint64_t* out) {
   SS_CUDA(cudaMemcpyFromSymbol(out, ss::g_mlp_trace, sizeof(ss::g_mlp_trace)));
   return SS_OK;

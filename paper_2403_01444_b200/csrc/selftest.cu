@@ -18,7 +18,7 @@ __global__ void __launch_bounds__(128) umma_selftest_kernel(const float* __restr
                                                             const float* __restrict__ B,
                                                             float* __restrict__ D, int M, int N,
                                                             int K, int a_mn, int b_mn, int swap,
-                                                            int raw) {
+                                                            int raw, int a_tmem) {
   extern __shared__ __align__(128) uint8_t sm[];
   __shared__ uint64_t bar;
   __shared__ uint32_t tbase;
@@ -35,16 +35,32 @@ __global__ void __launch_bounds__(128) umma_selftest_kernel(const float* __restr
     umma::mbar_init(&bar, 1);
     umma::fence_mbar_init();
   }
-  if (warp == 0) umma::tmem_alloc(&tbase, 64);
+  if (warp == 0) umma::tmem_alloc(&tbase, a_tmem ? 256 : 64);
   umma::fence_proxy_async();
   umma::fence_before();
   __syncthreads();
   umma::fence_after();
   const uint32_t tmem = tbase;
+  if (a_tmem) {  // A (M = 128, K-major) -> TMEM columns 128.., row i in lane i
+    const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+    for (int c0 = 0; c0 < K; c0 += 8) {
+      float v[8];
+      for (int j = 0; j < 8; ++j) v[j] = umma::to_tf32(A[tid * K + c0 + j]);
+      umma::tmem_st8(tmem + lane_base + 128u + (uint32_t)c0, v);
+    }
+    umma::tmem_st_wait();
+    umma::fence_before();
+    __syncthreads();
+    umma::fence_after();
+  }
   if (tid == 0) {
     const uint32_t a0 = umma::smem_u32(sa), b0 = umma::smem_u32(sb);
     const uint32_t id = umma::idesc_tf32(M, N, a_mn, b_mn);
     for (int k = 0; k < K; k += 8) {
+      if (a_tmem) {
+        umma::mma_tf32_ts(tmem, tmem + 128u + (uint32_t)k, umma::desc_k(b0, BC, k), id, k > 0);
+        continue;
+      }
       uint64_t da, db;
       if (a_mn)
         da = swap ? umma::desc(a0 + (k >> 3) * umma::tile_sbo(AC), 128u, umma::tile_sbo(AC))
@@ -74,7 +90,7 @@ __global__ void __launch_bounds__(128) umma_selftest_kernel(const float* __restr
   }
   umma::fence_before();
   __syncthreads();
-  if (warp == 0) umma::tmem_free(tmem, 64);
+  if (warp == 0) umma::tmem_free(tmem, a_tmem ? 256 : 64);
 }
 
 // kind::f16 (bf16) variant: operands rounded to bf16, K steps of 16,
@@ -135,9 +151,54 @@ __global__ void __launch_bounds__(128) umma_selftest16_kernel(const float* __res
   if (warp == 0) umma::tmem_free(tmem, 128);
 }
 
+// Issue-rate probe: `count` back-to-back M = 128 MMAs (K = 8 tf32 / 16 bf16
+// per instruction, fixed operands) issued by one thread; out[0] = cycles from
+// the first issue to the commit's completion, out[1] = cycles spent issuing.
+__global__ void __launch_bounds__(128) umma_rate_kernel(int kind, int N, int a_tmem, int count,
+                                                        unsigned long long* out) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tbase;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  for (int i = tid; i < (128 * 64 + 64 * 64) / 4 * 4; i += 128) reinterpret_cast<float*>(sm)[i] = 0.f;
+  if (tid == 0) {
+    umma::mbar_init(&bar, 1);
+    umma::fence_mbar_init();
+  }
+  if (warp == 0) umma::tmem_alloc(&tbase, 256);
+  umma::fence_proxy_async();
+  umma::fence_before();
+  __syncthreads();
+  umma::fence_after();
+  const uint32_t tmem = tbase;
+  if (tid == 0) {
+    const uint32_t a0 = umma::smem_u32(sm), b0 = umma::smem_u32(sm + 128 * 64 * 4);
+    const uint64_t da = kind ? umma::desc16_k(a0, 64, 0) : umma::desc_k(a0, 32, 0);
+    const uint64_t db = kind ? umma::desc16_k(b0, 64, 0) : umma::desc_k(b0, 32, 0);
+    const uint32_t id = kind ? umma::idesc_bf16(128, N, 0, 0) : umma::idesc_tf32(128, N, 0, 0);
+    const unsigned long long c0 = clock64();
+#pragma unroll 1
+    for (int i = 0; i < count; ++i) {
+      if (kind) umma::mma_bf16(tmem, da, db, id, 1);
+      else if (a_tmem) umma::mma_tf32_ts(tmem, tmem + 128u, db, id, 1);
+      else umma::mma_tf32(tmem, da, db, id, 1);
+    }
+    const unsigned long long c1 = clock64();
+    umma::commit(&bar);
+    umma::mbar_wait(&bar, 0);
+    const unsigned long long c2 = clock64();
+    out[0] = c2 - c0;
+    out[1] = c1 - c0;
+  }
+  umma::fence_before();
+  __syncthreads();
+  if (warp == 0) umma::tmem_free(tmem, 256);
+}
+
 }  // namespace ss
 
-// flags: bit0 a_mn, bit1 b_mn, bit2 swap, bit3 raw, bit4 bf16 (kind::f16)
+// flags: bit0 a_mn, bit1 b_mn, bit2 swap, bit3 raw, bit4 bf16 (kind::f16),
+// bit5 A from TMEM (tf32, M = 128, K-major)
 extern "C" int ss_selftest_umma(int32_t M, int32_t N, int32_t K, int32_t flags, const float* A,
                                 const float* B, float* D, void* stream) {
   const int bf16 = (flags >> 4) & 1;
@@ -159,8 +220,22 @@ extern "C" int ss_selftest_umma(int32_t M, int32_t N, int32_t K, int32_t flags, 
                       ss::umma::tile_bytes(b_mn ? K : N, b_mn ? N : K);
   auto k = ss::umma_selftest_kernel;
   SS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int a_tmem = (flags >> 5) & 1;
+  if (a_tmem && (M != 128 || a_mn)) return SS_ERR_DATA;
   k<<<1, 128, smem, ss::as_stream(stream)>>>(A, B, D, M, N, K, a_mn, b_mn, (flags >> 2) & 1,
-                                             (flags >> 3) & 1);
+                                             (flags >> 3) & 1, a_tmem);
   SS_CHECK_LAUNCH("umma_selftest_kernel");
+  return SS_OK;
+}
+
+// kind 0 tf32 / 1 bf16, a_tmem (tf32 only): see umma_rate_kernel
+extern "C" int ss_debug_umma_rate(int32_t kind, int32_t N, int32_t a_tmem, int32_t count,
+                                  uint64_t* out_dev, void* stream) {
+  const size_t smem = 128 * 64 * 4 + 64 * 64 * 4;
+  auto k = ss::umma_rate_kernel;
+  SS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k<<<1, 128, smem, ss::as_stream(stream)>>>(kind, N, a_tmem, count,
+                                             reinterpret_cast<unsigned long long*>(out_dev));
+  SS_CHECK_LAUNCH("umma_rate_kernel");
   return SS_OK;
 }

@@ -37,6 +37,27 @@ def test_umma_tf32(test):
     np.testing.assert_allclose(out, ref, rtol=1e-5, atol=1e-4)
 
 
+def test_umma_tf32_a_from_tmem():
+    """A operand in TMEM (tcgen05.st, row i in lane i), B K-major in smem."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2403_01444_b200 import _lib
+    from paper_2403_01444_b200.device import ptr, stream
+
+    lib = _lib.load()
+    rng = np.random.default_rng(7)
+    M, N, K = 128, 64, 64
+    a, b = rng.normal(size=(M, K)), rng.normal(size=(N, K))
+    ref = _tf32(a) @ _tf32(b).T
+    da = torch.tensor(a, dtype=torch.float32, device="cuda")
+    db = torch.tensor(b, dtype=torch.float32, device="cuda")
+    dd = torch.full(ref.shape, float("nan"), dtype=torch.float32, device="cuda")
+    assert lib.ss_selftest_umma(M, N, K, 32, ptr(da), ptr(db), ptr(dd), stream()) == 0
+    out = dd.cpu().numpy().astype(np.float64)
+    np.testing.assert_allclose(out, ref, rtol=1e-5, atol=1e-4)
+
+
 @pytest.mark.parametrize("mode", [1, 2])
 def test_tensor_core_decoder_matches_fp32(mode):
     """ss_ntc_forward with the tcgen05 decoder (3xTF32 / tf32) vs the FFMA path."""

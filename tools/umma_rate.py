@@ -1,0 +1,22 @@
+"""Cycles per tcgen05.mma (M = 128) issued back to back by one thread:
+  python tools/umma_rate.py"""
+import sys
+
+import torch
+
+sys.path.insert(0, "/root/repo")
+from paper_2403_01444_b200 import _lib  # noqa: E402
+from paper_2403_01444_b200.device import ptr, stream  # noqa: E402
+
+lib = _lib.load()
+out = torch.zeros(2, dtype=torch.int64, device="cuda")
+for kind, a_tmem, name in ((0, 0, "tf32 SS"), (0, 1, "tf32 TS"), (1, 0, "bf16 SS")):
+    for N in (16, 64, 128):
+        res = []
+        for count in (16, 256):
+            lib.ss_debug_umma_rate(kind, N, a_tmem, count, ptr(out), stream())
+            torch.cuda.synchronize()
+            res.append(out.cpu().tolist())
+        (t16, i16), (t256, i256) = res
+        print(f"{name} N={N:3d}: {(t256 - t16) / 240:6.1f} cyc/MMA (issue {(i256 - i16) / 240:5.1f}), "
+              f"16 MMAs: total {t16} issue {i16}")
