@@ -276,22 +276,24 @@ __global__ void __launch_bounds__(NT_FWD, 1) mlp_fwd_tc_kernel(int64_t n, const 
           ph[s] ^= 1;
           umma::fence_after();
           if ((tid & 31) == 0) SS_EV(1, nev);
-          if ((tid & 31) == 0) {
+          {  // warp-uniform issue, one elected lane (umma::*_elect)
             const uint32_t base = tmem + 256u * s;
             const Op32& B = layer == 0 ? dW0 : (layer == 1 ? dW1 : dW2);
             const uint32_t acc = base + (layer == 2 ? 192u : 128u);
             const uint32_t id = layer == 2 ? id16 : id64;
-            const int nk = layer == 0 ? IN / 8 : 8;
-            for (int k = 0; k < nk; ++k) {
+            constexpr int nk0 = IN / 8;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              if (layer == 0 && k >= nk0) break;
               const uint64_t d = 16ull * k;
-              umma::mma_tf32_ts(acc, base + 8u * k, B.hi + d, id, k > 0);
+              umma::mma_tf32_ts_elect(acc, base + 8u * k, B.hi + d, id, k > 0);
               if (P == 3) {
-                umma::mma_tf32_ts(acc, base + 8u * k, B.lo + d, id, 1);
-                umma::mma_tf32_ts(acc, base + 64u + 8u * k, B.hi + d, id, 1);
+                umma::mma_tf32_ts_elect(acc, base + 8u * k, B.lo + d, id, 1);
+                umma::mma_tf32_ts_elect(acc, base + 64u + 8u * k, B.hi + d, id, 1);
               }
             }
-            umma::commit(&done[s]);
-            SS_EV(1, nev);
+            umma::commit_elect(&done[s]);
+            if ((tid & 31) == 0) SS_EV(1, nev);
           }
           __syncwarp();
         }

@@ -176,13 +176,20 @@ __global__ void __launch_bounds__(128) umma_rate_kernel(int kind, int N, int a_t
     const uint64_t da = kind ? umma::desc16_k(a0, 64, 0) : umma::desc_k(a0, 32, 0);
     const uint64_t db = kind ? umma::desc16_k(b0, 64, 0) : umma::desc_k(b0, 32, 0);
     const uint32_t id = kind ? umma::idesc_bf16(128, N, 0, 0) : umma::idesc_tf32(128, N, 0, 0);
-    const unsigned long long c0 = clock64();
-#pragma unroll 1
-    for (int i = 0; i < count; ++i) {
-      if (kind) umma::mma_bf16(tmem, da, db, id, 1);
-      else if (a_tmem) umma::mma_tf32_ts(tmem, tmem + 128u, db, id, 1);
-      else umma::mma_tf32(tmem, da, db, id, 1);
+    unsigned long long c0 = clock64();
+    // 16 MMAs per unrolled group, one code path per variant
+#define SS_RATE_LOOP(CALL)                       \
+  for (int i = 0; i < count; i += 16) {          \
+    _Pragma("unroll") for (int j = 0; j < 16; ++j) CALL; \
+  }
+    if (kind) {
+      SS_RATE_LOOP(umma::mma_bf16(tmem, da, db, id, 1))
+    } else if (a_tmem) {
+      SS_RATE_LOOP(umma::mma_tf32_ts(tmem, tmem + 128u, db, id, 1))
+    } else {
+      SS_RATE_LOOP(umma::mma_tf32(tmem, da, db, id, 1))
     }
+#undef SS_RATE_LOOP
     const unsigned long long c1 = clock64();
     umma::commit(&bar);
     umma::mbar_wait(&bar, 0);
