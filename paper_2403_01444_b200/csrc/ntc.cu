@@ -121,18 +121,6 @@ __device__ inline void band_vals(float x, float y, float z, float* v) {
 #pragma unroll
   for (int m = 0; m < B; ++m) v[m] = b[off + m];
 }
-template <int B>
-__device__ inline void band_vjp(float x, float y, float z, const float* gv, float g[3]) {
-  float gb[16];
-#pragma unroll
-  for (int m = 0; m < 16; ++m) gb[m] = 0.f;
-  const int off = B == 5 ? 4 : 9;
-#pragma unroll
-  for (int m = 0; m < B; ++m) gb[off + m] = gv[m];
-  // degree-1 terms are zero in gb, so the lower bands contribute nothing
-  sh_basis_vjp<float>(B == 5 ? 2 : 3, x, y, z, gb, g);
-}
-
 __device__ __constant__ int c_perm[3] = {1, 2, 0};  // (y, z, x) basis order, sh.py:30-32
 
 // One colour channel of bands l >= 2 (4 lanes per Gaussian, see
@@ -165,8 +153,33 @@ __device__ inline void rotate_band_channel(const float R[3][3], const float* in,
   }
 }
 
+// Gradient at e of the band-l function f(e) = sum_b c_b Y_{l,b}(e): the band-l
+// terms of sh_basis_vjp (the same polynomial derivatives), without the lower
+// bands' zero-weighted work.
+__device__ __forceinline__ void band_grad(const float* c, float x, float y, float z, float g[3],
+                                          int B) {
+  if (B == 5) {
+    const float a = kShC2a, b = kShC2b, cc = kShC2c;
+    g[0] = a * y * c[0] + a * z * c[3] - 2.f * b * x * c[2] + 2.f * cc * x * c[4];
+    g[1] = a * x * c[0] + a * z * c[1] - 2.f * b * y * c[2] - 2.f * cc * y * c[4];
+    g[2] = a * y * c[1] + 4.f * b * z * c[2] + a * x * c[3];
+  } else {
+    const float c3 = kShC3a, c2 = kShC3b, c1 = kShC3c, c0 = kShC3d, ch = kShC3e;
+    const float xx = x * x, yy = y * y, zz = z * z, xy = x * y, xz = x * z, yz = y * z;
+    g[0] = 6.f * c3 * xy * c[0] + c2 * yz * c[1] - 2.f * c1 * xy * c[2] - 6.f * c0 * xz * c[3] +
+           c1 * (4.f * zz - 3.f * xx - yy) * c[4] + 2.f * ch * xz * c[5] +
+           c3 * (3.f * xx - 3.f * yy) * c[6];
+    g[1] = c3 * (3.f * xx - 3.f * yy) * c[0] + c2 * xz * c[1] +
+           c1 * (4.f * zz - xx - 3.f * yy) * c[2] - 6.f * c0 * yz * c[3] - 2.f * c1 * xy * c[4] -
+           2.f * ch * yz * c[5] - 6.f * c3 * xy * c[6];
+    g[2] = c2 * xy * c[1] + 8.f * c1 * yz * c[2] + c0 * (6.f * zz - 3.f * xx - 3.f * yy) * c[3] +
+           8.f * c1 * xz * c[4] + ch * (xx - yy) * c[5];
+  }
+}
+
 // This channel's share of g_R for band l >= 2 (band_matrix_vjp is linear in
-// g_M = sum_c g_c in_c^T, so the channels' shares add up to it)
+// g_M = sum_c g_c in_c^T, so the channels' shares add up to it).  With
+// h = S^{-T} g, direction k contributes d_k (x) h_k grad f_in(R^T d_k).
 template <int B>
 __device__ inline void band_channel_vjp(const float R[3][3], const float* g, const float* in,
                                         float gR[3][3]) {
@@ -177,18 +190,16 @@ __device__ inline void band_channel_vjp(const float R[3][3], const float* g, con
     float h = 0.f;
 #pragma unroll
     for (int a = 0; a < B; ++a) h = fmaf(sinv[a * B + k], g[a], h);
-    float e[3], gE[B];
+    float e[3];
 #pragma unroll
     for (int i = 0; i < 3; ++i)
       e[i] = R[0][i] * dirs[k][0] + R[1][i] * dirs[k][1] + R[2][i] * dirs[k][2];
-#pragma unroll
-    for (int b = 0; b < B; ++b) gE[b] = h * in[b];
-    float ge[3] = {0.f, 0.f, 0.f};
-    band_vjp<B>(e[0], e[1], e[2], gE, ge);
+    float ge[3];
+    band_grad(in, e[0], e[1], e[2], ge, B);
 #pragma unroll
     for (int jj = 0; jj < 3; ++jj)
 #pragma unroll
-      for (int ii = 0; ii < 3; ++ii) gR[jj][ii] = fmaf(dirs[k][jj], ge[ii], gR[jj][ii]);
+      for (int ii = 0; ii < 3; ++ii) gR[jj][ii] = fmaf(dirs[k][jj] * h, ge[ii], gR[jj][ii]);
   }
 }
 

@@ -949,12 +949,13 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_bwd_kernel(
 // parameter reads and gradient writes; the rank accumulators are gathered).
 // The EWA / covariance / projection chain runs in fp64; the SH part (d_sh,
 // the view-direction gradient) in fp32 with the forward's clip mask.
+template <int DEG>
 __global__ void __launch_bounds__(128, 4) gaussian_bwd_kernel(CamD cam, ss_cloud cl, Geom g,
                                                               int64_t n, ss_cloud_grads out,
                                                               int full) {
   const int64_t gid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (gid >= n) return;
-  const int K = cl.sh_coeffs;
+  constexpr int K = (DEG + 1) * (DEG + 1);  // == cl.sh_coeffs
   const int r = g.rank_of[gid];
   // culled, or no pixel of this view took a weight from it (all accumulators
   // are exactly 0, so every gradient is): zero rows so callers need no memset
@@ -964,7 +965,15 @@ __global__ void __launch_bounds__(128, 4) gaussian_bwd_kernel(CamD cam, ss_cloud
     if (out.d_means) for (int j = 0; j < 3; ++j) out.d_means[3 * gid + j] = 0.f;
     if (out.d_rotations)
       *reinterpret_cast<float4*>(out.d_rotations + 4 * gid) = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (out.d_sh) for (int j = 0; j < 3 * K; ++j) out.d_sh[gid * 3 * K + j] = 0.f;
+    if (out.d_sh) {
+      if (K == 16) {
+#pragma unroll
+        for (int j = 0; j < 12; ++j)
+          reinterpret_cast<float4*>(out.d_sh + gid * 48)[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+      } else {
+        for (int j = 0; j < 3 * K; ++j) out.d_sh[gid * 3 * K + j] = 0.f;
+      }
+    }
     if (full && out.d_log_scales) for (int j = 0; j < 3; ++j) out.d_log_scales[3 * gid + j] = 0.f;
     if (full && out.d_opacity_logits) out.d_opacity_logits[gid] = 0.f;
     return;
@@ -977,32 +986,59 @@ __global__ void __launch_bounds__(128, 4) gaussian_bwd_kernel(CamD cam, ss_cloud
   const double aop = a8;
   if (out.viewspace) out.viewspace[gid] = (float)sqrt(am[0] * am[0] + am[1] * am[1]);
   if (out.contributed) out.contributed[gid] = g.touched[r];
+  // ---- colour -> SH and view direction first (sh.py:62-81), fp32 with the
+  // forward's clip mask; its registers are free before the fp64 chain below
+  double gw[3];
+  {
+    const float* m = cl.means + 3 * gid;
+    double d[3];
+    for (int q = 0; q < 3; ++q) d[q] = (double)m[q] - cam.pos[q];
+    const double dist = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
+    const double dd = fmax(dist, 1e-12);
+    double dir[3];
+    for (int q = 0; q < 3; ++q) dir[q] = d[q] / dd;
+    const int cm = (int)g.g_color[gid].w;
+    const float gc[3] = {(cm & 1) ? a0.x : 0.f, (cm & 2) ? a0.y : 0.f, (cm & 4) ? a0.z : 0.f};
+    const float fdir[3] = {(float)dir[0], (float)dir[1], (float)dir[2]};
+    float basis[K], gbasis[K];
+    sh_basis<float>(DEG, fdir[0], fdir[1], fdir[2], basis);
+    const float* sh = cl.sh + gid * 3 * K;
+    float* dsh = out.d_sh ? out.d_sh + gid * 3 * K : nullptr;
+    if (K == 16) {  // degree 3: the 48 coefficients as 12 float4 loads / stores
+#pragma unroll
+      for (int k = 0; k < K; ++k) gbasis[k] = 0.f;
+#pragma unroll
+      for (int j = 0; j < 12; ++j) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(sh) + j);
+        const float e[4] = {v.x, v.y, v.z, v.w};
+        float o[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const int k = (4 * j + t) / 3, c = (4 * j + t) % 3;
+          gbasis[k] = fmaf(e[t], gc[c], gbasis[k]);
+          o[t] = basis[k] * gc[c];
+        }
+        if (dsh) reinterpret_cast<float4*>(dsh)[j] = make_float4(o[0], o[1], o[2], o[3]);
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        gbasis[k] = sh[3 * k] * gc[0] + sh[3 * k + 1] * gc[1] + sh[3 * k + 2] * gc[2];
+        if (dsh) {
+          dsh[3 * k] = basis[k] * gc[0];
+          dsh[3 * k + 1] = basis[k] * gc[1];
+          dsh[3 * k + 2] = basis[k] * gc[2];
+        }
+      }
+    }
+    float gdirf[3] = {0.f, 0.f, 0.f};
+    sh_basis_vjp<float>(DEG, fdir[0], fdir[1], fdir[2], gbasis, gdirf);
+    const double gdir[3] = {gdirf[0], gdirf[1], gdirf[2]};
+    const double dg = dir[0] * gdir[0] + dir[1] * gdir[1] + dir[2] * gdir[2];
+    for (int i = 0; i < 3; ++i) gw[i] = (gdir[i] - dir[i] * dg) / dd;
+  }
   Projected P;
   project_geom(cam, cl, gid, P);
-  const int deg = sh_degree_of(K);
-  // colour -> SH and view direction (sh.py:62-81), fp32, forward clip mask
-  const int cm = (int)g.g_color[gid].w;
-  const float gc[3] = {(cm & 1) ? a0.x : 0.f, (cm & 2) ? a0.y : 0.f, (cm & 4) ? a0.z : 0.f};
-  const float fdir[3] = {(float)P.dir[0], (float)P.dir[1], (float)P.dir[2]};
-  float basis[16], gbasis[16];
-  sh_basis<float>(deg, fdir[0], fdir[1], fdir[2], basis);
-  const float* sh = cl.sh + gid * 3 * K;
-  float* dsh = out.d_sh ? out.d_sh + gid * 3 * K : nullptr;
-  for (int k = 0; k < K; ++k) {
-    gbasis[k] = sh[3 * k] * gc[0] + sh[3 * k + 1] * gc[1] + sh[3 * k + 2] * gc[2];
-    if (dsh) {
-      dsh[3 * k] = basis[k] * gc[0];
-      dsh[3 * k + 1] = basis[k] * gc[1];
-      dsh[3 * k + 2] = basis[k] * gc[2];
-    }
-  }
-  float gdirf[3] = {0.f, 0.f, 0.f};
-  sh_basis_vjp<float>(deg, fdir[0], fdir[1], fdir[2], gbasis, gdirf);
-  const double gdir[3] = {gdirf[0], gdirf[1], gdirf[2]};
-  const double dd = fmax(P.dist, 1e-12);
-  const double dg = P.dir[0] * gdir[0] + P.dir[1] * gdir[1] + P.dir[2] * gdir[2];
-  double gw[3];
-  for (int i = 0; i < 3; ++i) gw[i] = (gdir[i] - P.dir[i] * dg) / dd;
   // conic -> cov2d: -C A C
   double CA[2][2], gcov2[2][2];
   for (int i = 0; i < 2; ++i)
@@ -1215,8 +1251,16 @@ int raster_backward(const ss_cloud* cl, const ss_camera* cam, const ss_raster_se
   else SS_TRY(launch_blend_bwd<false>(s->tile_size, ntiles, st, bp, g, b.vals_out, d_image));
   prof_end(PH_BLEND_BWD, st);
   prof_begin(PH_GAUSS_BWD, st);
-  gaussian_bwd_kernel<<<(unsigned)cdiv(n, 128), 128, 0, st>>>(make_cam(cam), *cl, g, n, *grads,
-                                                               full);
+  {
+    const unsigned grid = (unsigned)cdiv(n, 128);
+    const CamD cd = make_cam(cam);
+    switch (cl->sh_coeffs) {
+      case 1: gaussian_bwd_kernel<0><<<grid, 128, 0, st>>>(cd, *cl, g, n, *grads, full); break;
+      case 4: gaussian_bwd_kernel<1><<<grid, 128, 0, st>>>(cd, *cl, g, n, *grads, full); break;
+      case 9: gaussian_bwd_kernel<2><<<grid, 128, 0, st>>>(cd, *cl, g, n, *grads, full); break;
+      default: gaussian_bwd_kernel<3><<<grid, 128, 0, st>>>(cd, *cl, g, n, *grads, full); break;
+    }
+  }
   SS_CHECK_LAUNCH("gaussian_bwd_kernel");
   prof_end(PH_GAUSS_BWD, st);
   return SS_OK;
