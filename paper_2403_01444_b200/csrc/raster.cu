@@ -201,19 +201,33 @@ __device__ inline void project_geom(const CamD& cam, const ss_cloud& cl, int64_t
   P.op = 1.0 / (1.0 + exp(-(double)cl.opacity_logits[i]));
 }
 
+template <int DEG>
 __device__ inline void project_one(const CamD& cam, const ss_cloud& cl, int64_t i, Projected& P) {
   project_geom(cam, cl, i, P);
-  const int K = cl.sh_coeffs;
-  double basis[16];
-  sh_basis<double>(sh_degree_of(K), P.dir[0], P.dir[1], P.dir[2], basis);
-  for (int c = 0; c < 3; ++c) {
-    double s = 0.5;
-    for (int k = 0; k < K; ++k) s += basis[k] * (double)cl.sh[(i * K + k) * 3 + c];
-    P.raw[c] = s;
+  constexpr int K = (DEG + 1) * (DEG + 1);
+  double basis[K];
+  sh_basis<double>(DEG, P.dir[0], P.dir[1], P.dir[2], basis);
+  double raw[3] = {0.5, 0.5, 0.5};
+  const float* sh = cl.sh + i * 3 * K;
+  if (K % 4 == 0 && (reinterpret_cast<uintptr_t>(cl.sh) & 15) == 0) {  // 3K floats as float4 (K = 4, 16)
+#pragma unroll
+    for (int j = 0; j < 3 * K / 4; ++j) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(sh) + j);
+      const float e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int t = 0; t < 4; ++t) raw[(4 * j + t) % 3] += basis[(4 * j + t) / 3] * (double)e[t];
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) raw[c] += basis[k] * (double)sh[3 * k + c];
   }
+  for (int c = 0; c < 3; ++c) P.raw[c] = raw[c];
 }
 
 // K4a: per-Gaussian projection; depth key (+inf when culled)
+template <int DEG>
 __global__ void __launch_bounds__(256) preprocess_kernel(CamD cam, ss_cloud cl, Geom g) {
   __shared__ uint32_t s_hist[4][256];  // the depth sort's digit histograms
   for (int k = threadIdx.x; k < 1024; k += blockDim.x) (&s_hist[0][0])[k] = 0;
@@ -235,7 +249,7 @@ __global__ void __launch_bounds__(256) preprocess_kernel(CamD cam, ss_cloud cl, 
       key = __float_as_uint((float)z);
       atomicAdd(reinterpret_cast<unsigned long long*>(&g.dev_counts[0]), 1ull);
       Projected P;
-      project_one(cam, cl, i, P);
+      project_one<DEG>(cam, cl, i, P);
       g.g_mean[i] = make_double2(P.mean[0], P.mean[1]);
       g.g_conop[i] =
           make_double4(P.conic[0][0], P.conic[0][1] + P.conic[1][0], P.conic[1][1], P.op);
@@ -966,7 +980,7 @@ __global__ void __launch_bounds__(128, 4) gaussian_bwd_kernel(CamD cam, ss_cloud
     if (out.d_rotations)
       *reinterpret_cast<float4*>(out.d_rotations + 4 * gid) = make_float4(0.f, 0.f, 0.f, 0.f);
     if (out.d_sh) {
-      if (K == 16) {
+      if (K == 16 && (reinterpret_cast<uintptr_t>(out.d_sh) & 15) == 0) {
 #pragma unroll
         for (int j = 0; j < 12; ++j)
           reinterpret_cast<float4*>(out.d_sh + gid * 48)[j] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -1004,7 +1018,8 @@ __global__ void __launch_bounds__(128, 4) gaussian_bwd_kernel(CamD cam, ss_cloud
     sh_basis<float>(DEG, fdir[0], fdir[1], fdir[2], basis);
     const float* sh = cl.sh + gid * 3 * K;
     float* dsh = out.d_sh ? out.d_sh + gid * 3 * K : nullptr;
-    if (K == 16) {  // degree 3: the 48 coefficients as 12 float4 loads / stores
+    if (K == 16 && ((reinterpret_cast<uintptr_t>(cl.sh) | reinterpret_cast<uintptr_t>(out.d_sh)) &
+                    15) == 0) {  // degree 3: the 48 coefficients as 12 float4 loads / stores
 #pragma unroll
       for (int k = 0; k < K; ++k) gbasis[k] = 0.f;
 #pragma unroll
@@ -1178,7 +1193,15 @@ int raster_begin(const ss_cloud* cl, const ss_camera* cam, const ss_raster_setti
   if (n > 0) {
     SS_TRY(binsort_clear(g.dsort, 32, st));  // preprocess_kernel builds the histograms
     prof_begin(PH_PROJECT, st);
-    preprocess_kernel<<<(unsigned)cdiv(n, 256), 256, 0, st>>>(cd, *cl, g);
+    {
+      const unsigned grid = (unsigned)cdiv(n, 256);
+      switch (cl->sh_coeffs) {
+        case 1: preprocess_kernel<0><<<grid, 256, 0, st>>>(cd, *cl, g); break;
+        case 4: preprocess_kernel<1><<<grid, 256, 0, st>>>(cd, *cl, g); break;
+        case 9: preprocess_kernel<2><<<grid, 256, 0, st>>>(cd, *cl, g); break;
+        default: preprocess_kernel<3><<<grid, 256, 0, st>>>(cd, *cl, g); break;
+      }
+    }
     SS_CHECK_LAUNCH("preprocess_kernel");
     prof_end(PH_PROJECT, st);
     prof_begin(PH_DEPTH_SORT, st);
