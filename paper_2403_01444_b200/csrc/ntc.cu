@@ -177,32 +177,6 @@ __device__ __forceinline__ void band_grad(const float* c, float x, float y, floa
   }
 }
 
-// This channel's share of g_R for band l >= 2 (band_matrix_vjp is linear in
-// g_M = sum_c g_c in_c^T, so the channels' shares add up to it).  With
-// h = S^{-T} g, direction k contributes d_k (x) h_k grad f_in(R^T d_k).
-template <int B>
-__device__ inline void band_channel_vjp(const float R[3][3], const float* g, const float* in,
-                                        float gR[3][3]) {
-  const float(*dirs)[3] = B == 5 ? c_shrot.dirs2 : c_shrot.dirs3;
-  const float* sinv = B == 5 ? &c_shrot.binvT2[0][0] : &c_shrot.binvT3[0][0];
-#pragma unroll
-  for (int k = 0; k < B; ++k) {
-    float h = 0.f;
-#pragma unroll
-    for (int a = 0; a < B; ++a) h = fmaf(sinv[a * B + k], g[a], h);
-    float e[3];
-#pragma unroll
-    for (int i = 0; i < 3; ++i)
-      e[i] = R[0][i] * dirs[k][0] + R[1][i] * dirs[k][1] + R[2][i] * dirs[k][2];
-    float ge[3];
-    band_grad(in, e[0], e[1], e[2], ge, B);
-#pragma unroll
-    for (int jj = 0; jj < 3; ++jj)
-#pragma unroll
-      for (int ii = 0; ii < 3; ++ii) gR[jj][ii] = fmaf(dirs[k][jj] * h, ge[ii], gR[jj][ii]);
-  }
-}
-
 // ------------------------------------------------------------------ kernels
 __global__ void encode_kernel(ss_grid g, int64_t n, const float* __restrict__ means,
                               int32_t* __restrict__ corner_idx, float* __restrict__ corner_w,
@@ -463,9 +437,49 @@ __global__ void __launch_bounds__(128) transform_kernel(ss_cloud src, int64_t n,
 }
 
 // K3b: dL/d[d_mu | d_q] from transformed-cloud gradients (transform.py:111-134).
-// Four lanes per inside row: lanes 0-2 form one colour channel's share of g_R,
-// the shares are summed with shuffles, lane 3 finishes (A(q_src)^T g_rot, the
-// rotation and normalisation Jacobians) and writes g7.
+// One thread per inside row.  The SH part of g_R is linear in the per-channel
+// band gradients, so each band direction k is evaluated once for the three
+// channels: with h_kc = (S^{-T} g_c)_k and w = sum_c h_kc in_c, direction k
+// contributes d_k (x) grad f_w(R^T d_k) (band_channel_vjp summed over c).
+// Then A(q_src)^T g_rot, the rotation and normalisation Jacobians -> g7.
+template <int B>
+__device__ __forceinline__ void band_vjp_rows(const float R[3][3], const float (*gc)[B],
+                                              const float (*ic)[B], float gR[3][3]) {
+  const float(*dirs)[3] = B == 5 ? c_shrot.dirs2 : c_shrot.dirs3;
+  const float* sinv = B == 5 ? &c_shrot.binvT2[0][0] : &c_shrot.binvT3[0][0];
+#pragma unroll
+  for (int k = 0; k < B; ++k) {
+    float h[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+    for (int a = 0; a < B; ++a)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) h[c] = fmaf(sinv[a * B + k], gc[c][a], h[c]);
+    float w[B];
+#pragma unroll
+    for (int b = 0; b < B; ++b) w[b] = h[0] * ic[0][b] + h[1] * ic[1][b] + h[2] * ic[2][b];
+    float e[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+      e[i] = R[0][i] * dirs[k][0] + R[1][i] * dirs[k][1] + R[2][i] * dirs[k][2];
+    float ge[3];
+    band_grad(w, e[0], e[1], e[2], ge, B);
+#pragma unroll
+    for (int jj = 0; jj < 3; ++jj)
+#pragma unroll
+      for (int ii = 0; ii < 3; ++ii) gR[jj][ii] = fmaf(dirs[k][jj], ge[ii], gR[jj][ii]);
+  }
+}
+
+// coefficients [first, first + B) of the 3 channels of one SH row (3K floats,
+// coefficient-major): out[c][b] = row[3 (first + b) + c]
+template <int B>
+__device__ __forceinline__ void load_band(const float* __restrict__ row, int first, float (*out)[B]) {
+#pragma unroll
+  for (int b = 0; b < B; ++b)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) out[c][b] = __ldg(row + 3 * (first + b) + c);
+}
+
 template <int DEG>
 __global__ void __launch_bounds__(128) transform_vjp_kernel(
     ss_cloud src, int64_t n, const int32_t* __restrict__ rows, const int32_t* __restrict__ pos,
@@ -473,65 +487,58 @@ __global__ void __launch_bounds__(128) transform_vjp_kernel(
     const float* __restrict__ d_rot, const float* __restrict__ d_sh, float* __restrict__ g7,
     int gs, const uint8_t* __restrict__ live) {
   constexpr int K = (DEG + 1) * (DEG + 1);
-  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int64_t j = t >> 2;
-  const int c = (int)(t & 3);
-  const bool in_range = j < n;  // no early exit: the 4-lane reduction below is warp-wide
-  const int64_t gid = in_range ? (rows ? rows[j] : j) : 0;
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const int64_t gid = rows ? rows[j] : j;
+  const int64_t i = pos ? pos[j] : j;
   // a Gaussian no pixel of this view used has all-zero gradients: g7 row = 0
-  const bool ok = in_range && (!live || live[gid]);
-  if (in_range && !ok && c == 3) {
-    const int64_t i0 = pos ? pos[j] : j;
-    for (int k = 0; k < gs; ++k) g7[i0 * gs + k] = 0.f;
+  if (live && !live[gid]) {
+    if (gs == 8) {
+      *reinterpret_cast<float4*>(g7 + i * 8) = make_float4(0.f, 0.f, 0.f, 0.f);
+      *reinterpret_cast<float4*>(g7 + i * 8 + 4) = make_float4(0.f, 0.f, 0.f, 0.f);
+    } else {
+      for (int k = 0; k < gs; ++k) g7[i * gs + k] = 0.f;
+    }
+    return;
   }
-  const int64_t i = ok ? (pos ? pos[j] : j) : 0;
-  float o[7] = {0.f, 0.f, 0.f, 1.f, 0.f, 0.f, 0.f};
-  if (ok) {
+  float o[7];
 #pragma unroll
-    for (int k = 0; k < 7; ++k) o[k] = out7[i * os + k];
-  }
+  for (int k = 0; k < 7; ++k) o[k] = out7[i * os + k];
   float nq = sqrtf(o[3] * o[3] + o[4] * o[4] + o[5] * o[5] + o[6] * o[6]);
   nq = nq < 1e-12f ? 1.f : nq;
   const float u[4] = {o[3] / nq, o[4] / nq, o[5] / nq, o[6] / nq};
   float gR[3][3] = {{0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}};
   const bool rot = DEG >= 1 && rotate_sh;
-  if (rot && ok && c < 3) {
+  if (rot) {
     float R[3][3];
     quat_to_rot(u[0], u[1], u[2], u[3], R);
-    const float* sh = src.sh + gid * 3 * K + c;
-    const float* gsh = d_sh + gid * 3 * K + c;
-    {  // band 1: g_R += P^T (g in^T) P
-      float in[3], g[3];
+    const float* sh = src.sh + gid * 3 * K;
+    const float* gsh = d_sh + gid * 3 * K;
+    {  // band 1: g_R += P^T (sum_c g_c in_c^T) P
+      float in[3][3], g[3][3];
+      load_band<3>(sh, 1, in);
+      load_band<3>(gsh, 1, g);
 #pragma unroll
-      for (int b = 0; b < 3; ++b) in[b] = sh[(1 + b) * 3], g[b] = gsh[(1 + b) * 3];
+      for (int c = 0; c < 3; ++c)
 #pragma unroll
-      for (int a = 0; a < 3; ++a)
+        for (int a = 0; a < 3; ++a)
 #pragma unroll
-        for (int b = 0; b < 3; ++b) gR[c_perm[a]][c_perm[b]] = fmaf(g[a], in[b], gR[c_perm[a]][c_perm[b]]);
+          for (int b = 0; b < 3; ++b)
+            gR[c_perm[a]][c_perm[b]] = fmaf(g[c][a], in[c][b], gR[c_perm[a]][c_perm[b]]);
     }
     if (DEG >= 2) {
-      float in[5], g[5];
-#pragma unroll
-      for (int b = 0; b < 5; ++b) in[b] = sh[(4 + b) * 3], g[b] = gsh[(4 + b) * 3];
-      band_channel_vjp<5>(R, g, in, gR);
+      float in[3][5], g[3][5];
+      load_band<5>(sh, 4, in);
+      load_band<5>(gsh, 4, g);
+      band_vjp_rows<5>(R, g, in, gR);
     }
     if (DEG >= 3) {
-      float in[7], g[7];
-#pragma unroll
-      for (int b = 0; b < 7; ++b) in[b] = sh[(9 + b) * 3], g[b] = gsh[(9 + b) * 3];
-      band_channel_vjp<7>(R, g, in, gR);
+      float in[3][7], g[3][7];
+      load_band<7>(sh, 9, in);
+      load_band<7>(gsh, 9, g);
+      band_vjp_rows<7>(R, g, in, gR);
     }
   }
-  if (rot) {
-#pragma unroll
-    for (int a = 0; a < 3; ++a)
-#pragma unroll
-      for (int b = 0; b < 3; ++b) {
-        gR[a][b] += __shfl_xor_sync(0xffffffffu, gR[a][b], 1);
-        gR[a][b] += __shfl_xor_sync(0xffffffffu, gR[a][b], 2);
-      }
-  }
-  if (!ok || c != 3) return;
   const float4 q = *reinterpret_cast<const float4*>(src.rotations + 4 * gid);
   const float4 gr = *reinterpret_cast<const float4*>(d_rot + 4 * gid);
   // g_u = A(q_src)^T g_rot, A rows: [w,-x,-y,-z],[x,w,z,-y],[y,-z,w,x],[z,y,-x,w]
@@ -1025,7 +1032,7 @@ int transform_vjp_run(const ss_cloud* src, int64_t n, const int32_t* rows, const
   if (n == 0) return SS_OK;
   SS_TRY(ensure_shrot_const());
   prof_begin(PH_TRANSFORM_BWD, st);
-  const unsigned grid = (unsigned)cdiv(4 * n, 128);  // 4 lanes per row
+  const unsigned grid = (unsigned)cdiv(n, 128);  // one thread per row
   switch (sh_degree_of(src->sh_coeffs)) {
     case 0: transform_vjp_kernel<0><<<grid, 128, 0, st>>>(*src, n, rows, pos, out7, os, rotate_sh, dm, dr, ds, g7, gs, live); break;
     case 1: transform_vjp_kernel<1><<<grid, 128, 0, st>>>(*src, n, rows, pos, out7, os, rotate_sh, dm, dr, ds, g7, gs, live); break;
