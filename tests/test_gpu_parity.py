@@ -281,7 +281,8 @@ def test_stage1_no_sync_matches_synchronised_path(P):
     la = c.run(6)
     d.plan_capacity(margin=0.2)
     lb = d.run(6)
-    np.testing.assert_allclose(la, lb, rtol=1e-6)
+    np.testing.assert_allclose(la[0], lb[0], rtol=1e-12)
+    np.testing.assert_allclose(la, lb, rtol=2e-5)  # float-atomic order after step 0
     assert close(c.tables, d.tables) and close(c.params, d.params)
 
 
