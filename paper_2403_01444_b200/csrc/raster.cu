@@ -397,12 +397,27 @@ __device__ inline int64_t owner_rank(const int64_t* __restrict__ off, int64_t lo
   return lo;
 }
 
+// Block-parallel form (all threads call it, block-uniform result): each round
+// the threads test blockDim.x evenly spaced ranks and the bracket shrinks by
+// that factor, so a search over 250k ranks takes 3 rounds of one load each
+// instead of 18 dependent loads on one thread.
+__device__ inline int64_t block_owner_rank(const int64_t* __restrict__ off, int64_t lo,
+                                           int64_t hi, int64_t j) {  // off[lo] <= j < off[hi]
+  while (hi - lo > 1) {
+    const int64_t step = (hi - lo + blockDim.x - 1) / blockDim.x;
+    const int64_t r = lo + (int64_t)threadIdx.x * step;
+    const int cnt = __syncthreads_count(r < hi && off[r] <= j);  // a prefix of the threads
+    lo += (int64_t)(cnt - 1) * step;
+    hi = min(lo + step, hi);
+  }
+  return lo;
+}
+
 __global__ void __launch_bounds__(256) duplicate_kernel(int ntx, int64_t n, Geom g, Bins b,
                                                         uint32_t* kdst, uint32_t* vdst,
                                                         uint32_t* status, int cull, int ts, int W,
                                                         int H, uint32_t sentinel, int key_bits) {
   constexpr int CH = 1024, SOFF = 2048;
-  __shared__ int64_t s_lo, s_hi;
   __shared__ int64_t s_off[SOFF];
   __shared__ uint32_t s_hist[2][256];  // binsort digit histograms of the emitted keys
   for (int i = threadIdx.x; i < 512; i += blockDim.x) (&s_hist[0][0])[i] = 0;
@@ -411,13 +426,9 @@ __global__ void __launch_bounds__(256) duplicate_kernel(int ntx, int64_t n, Geom
     atomicOr(status, SS_FLAG_OVERFLOW);
   const int64_t pairs = min(count, b.capacity);
   for (int64_t j0 = (int64_t)blockIdx.x * CH; j0 < pairs; j0 += (int64_t)gridDim.x * CH) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      s_lo = owner_rank(g.offsets, 0, n, j0);
-      s_hi = owner_rank(g.offsets, s_lo, n, min(j0 + CH, pairs) - 1) + 1;
-    }
-    __syncthreads();
-    const int64_t rlo = s_lo, rhi = s_hi;
+    __syncthreads();  // the previous chunk is done with s_off
+    const int64_t rlo = block_owner_rank(g.offsets, 0, n, j0);
+    const int64_t rhi = block_owner_rank(g.offsets, rlo, n, min(j0 + CH, pairs) - 1) + 1;
     // the chunk's owning ranks' offsets staged in shared memory when they fit
     const bool staged = rhi - rlo + 1 <= SOFF;
     if (staged)
