@@ -167,22 +167,27 @@ __global__ void __launch_bounds__(kBsThreads) bs_pass_kernel(
     }
     atomicExch(my, kFlagInc | (excl + cnt));
   }
-  // ---- exclusive scans over digits: global digit offsets and tile-local starts
+  // ---- exclusive scans over digits (global digit offsets, tile-local starts):
+  // warp shuffle scans, then the 8 warp totals
   const uint32_t h = hist[d];
-  s_scan[d] = h;
-  s_lstart[d] = cnt;
-  __syncthreads();
-  for (int off = 1; off < 256; off <<= 1) {
-    const uint32_t a = d >= off ? s_scan[d - off] : 0u;
-    const uint32_t b = d >= off ? s_lstart[d - off] : 0u;
-    __syncthreads();
-    s_scan[d] += a;
-    s_lstart[d] += b;
-    __syncthreads();
+  uint32_t sh = h, sl = cnt;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const uint32_t a = __shfl_up_sync(0xffffffffu, sh, off);
+    const uint32_t b = __shfl_up_sync(0xffffffffu, sl, off);
+    if (lane >= off) sh += a, sl += b;
   }
-  const uint32_t g_excl = s_scan[d] - h;
-  const uint32_t l_excl = s_lstart[d] - cnt;
+  if (lane == 31) {
+    s_scan[warp] = sh;
+    s_scan[32 + warp] = sl;
+  }
   __syncthreads();
+  uint32_t wh_ = 0, wl_ = 0;
+#pragma unroll
+  for (int w = 0; w < kBsWarps; ++w)
+    if (w < warp) wh_ += s_scan[w], wl_ += s_scan[32 + w];
+  const uint32_t g_excl = sh - h + wh_;
+  const uint32_t l_excl = sl - cnt + wl_;
   s_lstart[d] = l_excl;
   s_gbase[d] = g_excl + excl;
   __syncthreads();
