@@ -147,6 +147,19 @@ __device__ __forceinline__ void gemm3(uint32_t acc, const Op16& A, const Op16& B
   }
 }
 
+// warp-collective form: called by a whole converged warp, one lane issues
+template <int NK>
+__device__ __forceinline__ void gemm3e(uint32_t acc, const Op16& A, const Op16& B, uint32_t idesc,
+                                       uint32_t accumulate) {
+#pragma unroll
+  for (int s = 0; s < NK; ++s) {
+    const uint64_t da = (uint64_t)A.kstep * s, db = (uint64_t)B.kstep * s;
+    umma::mma_bf16_elect(acc, A.hi + da, B.hi + db, idesc, accumulate | (s > 0));
+    umma::mma_bf16_elect(acc, A.hi + da, B.lo + db, idesc, 1);
+    umma::mma_bf16_elect(acc, A.lo + da, B.hi + db, idesc, 1);
+  }
+}
+
 // store 8 consecutive columns c0..c0+7 of row r as hi/lo bf16 (two 16-byte stores)
 __device__ __forceinline__ void put8(uint8_t* tile, uint32_t lo_off, int r, int c0, int cols,
                                      const float* v) {
@@ -479,7 +492,7 @@ __global__ void __launch_bounds__(NT, 1) mlp_bwd_tc_kernel(
   using S = TcBwdSmem<IN, NL>;
   constexpr int XC = S::XC, HC = S::HC;
   extern __shared__ __align__(1024) uint8_t sm[];
-  __shared__ uint64_t bar;
+  __shared__ uint64_t bar, bar_w;  // bar: activation / delta GEMMs, bar_w: weight gradients
   __shared__ uint32_t tbase;
   __shared__ float sbias[128];
   __shared__ float sdb2[4][8];
@@ -515,6 +528,7 @@ __global__ void __launch_bounds__(NT, 1) mlp_bwd_tc_kernel(
   }
   if (tid == 0) {
     umma::mbar_init(&bar, 1);
+    umma::mbar_init(&bar_w, 1);
     umma::fence_mbar_init();
   }
   if (warp == 0) umma::tmem_alloc(&tbase, 512);
@@ -543,7 +557,14 @@ __global__ void __launch_bounds__(NT, 1) mlp_bwd_tc_kernel(
   constexpr uint32_t idW2 = umma::idesc_bf16(64, 8, 1, 1);
   constexpr uint32_t idW1 = umma::idesc_bf16(64, HC, 1, 1);
   constexpr uint32_t idW0 = umma::idesc_bf16(64, XC, 1, 1);
-  uint32_t phase = 0, acc_w = 0;
+  uint32_t phase = 0, phase_w = 0, acc_w = 0;
+  bool w_pending = false;  // weight-gradient GEMMs of the last tile still reading X, G, H, D
+  auto wait_w = [&]() {
+    if (w_pending) {
+      sync_mma(&bar_w, phase_w);
+      w_pending = false;
+    }
+  };
   float db2[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   const int64_t ntiles = (n + 127) / 128;
   // register prefetch of this thread's slices of the X, g and mask rows
@@ -575,11 +596,11 @@ __global__ void __launch_bounds__(NT, 1) mlp_bwd_tc_kernel(
   };
   auto issue_stage1 = [&]() {
     to_async();
-    if (tid == 0) {
+    if (warp == 0) {  // warp-uniform issue: descriptors stay in uniform registers
       umma::fence_after();
-      gemm3<IN / 16>(tmem + S::cH1, oX_k, oW0_k, idF, 0);
-      gemm3<1>(tmem + S::cDL, oG_k, oW2_mn, idB64, 0);
-      umma::commit(&bar);
+      gemm3e<IN / 16>(tmem + S::cH1, oX_k, oW0_k, idF, 0);
+      gemm3e<1>(tmem + S::cDL, oG_k, oW2_mn, idB64, 0);
+      umma::commit_elect(&bar);
     }
   };
   // a tile whose output gradients are all zero (Gaussians no pixel of the view
@@ -611,6 +632,7 @@ __global__ void __launch_bounds__(NT, 1) mlp_bwd_tc_kernel(
         fetch(t + gridDim.x);
         continue;
       }
+      wait_w();
       stage_in();
       issue_stage1();
     }
@@ -643,12 +665,13 @@ __global__ void __launch_bounds__(NT, 1) mlp_bwd_tc_kernel(
       // ---- stage 2: H2 = H1 W1;  D1 = D2 W1^T;  dW1^T += D2^T [H1 | 1]
       SS_STAMP(1, 3 + 8 * it);
       to_async();
-      if (tid == 0) {
+      if (warp == 0) {
         umma::fence_after();
-        gemm3<4>(tmem + S::cH2, oH1_k, oW1_k, idF, 0);
-        gemm3<4>(tmem + S::cD1, oD2_k, oW1_mn, idB64, 0);
-        gemm3<8>(tmem + S::cW1, oD2_mn, oH1_mn, idW1, acc_w);
-        umma::commit(&bar);
+        gemm3e<4>(tmem + S::cH2, oH1_k, oW1_k, idF, 0);
+        gemm3e<4>(tmem + S::cD1, oD2_k, oW1_mn, idB64, 0);
+        umma::commit_elect(&bar);
+        // dW1 reads D2 and H1 only: it runs under the H2 / D1 epilogue
+        gemm3e<8>(tmem + S::cW1, oD2_mn, oH1_mn, idW1, acc_w);
       }
       sync_mma(&bar, phase);
       SS_STAMP(1, 4 + 8 * it);
@@ -668,18 +691,23 @@ __global__ void __launch_bounds__(NT, 1) mlp_bwd_tc_kernel(
     // ---- stage 3: dX = D1 W0^T;  dW0^T += D1^T [X | 1];  dW2 += H_last^T G
     SS_STAMP(1, 5 + 8 * it);
     to_async();
-    if (tid == 0) {
+    if (warp == 0) {
       umma::fence_after();
-      gemm3<4>(tmem + S::cDX, oD1_k, oW0_mn, idBX, 0);
-      gemm3<8>(tmem + S::cW0, oD1_mn, oX_mn, idW0, acc_w);
-      gemm3<8>(tmem + S::cW2, oHl_mn, oG_mn, idW2, acc_w);
-      umma::commit(&bar);
+      gemm3e<4>(tmem + S::cDX, oD1_k, oW0_mn, idBX, 0);
+      umma::commit_elect(&bar);
+      // dW0 / dW2 (and dW1 before them) read X, G, H, D: they run under the dX
+      // epilogue; the next tile's staging waits for bar_w
+      gemm3e<8>(tmem + S::cW0, oD1_mn, oX_mn, idW0, acc_w);
+      gemm3e<8>(tmem + S::cW2, oHl_mn, oG_mn, idW2, acc_w);
+      umma::commit_elect(&bar_w);
     }
+    w_pending = true;
     sync_mma(&bar, phase);
     SS_STAMP(1, 6 + 8 * it);
     acc_w = 1;
     // ---- next tile's stage 1 runs under this tile's dX epilogue
     if (t + gridDim.x < ntiles && !tile_zero()) {
+      wait_w();
       stage_in();
       issue_stage1();
       issued = true;
@@ -700,6 +728,7 @@ __global__ void __launch_bounds__(NT, 1) mlp_bwd_tc_kernel(
   }
   // ---- flush the weight gradients: M = 64 accumulators, row j = 16 (w & 3) + lane
   //      (lanes < 16); the four warps of a lane quarter take 8-column blocks 8q + 32b
+  wait_w();
   umma::fence_before();
   __syncthreads();
   umma::fence_after();

@@ -246,6 +246,14 @@ __device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
       "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
 }
+// warp-collective form (see mma_tf32_ts_elect)
+__device__ __forceinline__ void mma_bf16_elect(uint32_t tmem_d, uint64_t a, uint64_t b,
+                                               uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
 // x = hi + lo with hi = bf16(x) (round to nearest even), lo = bf16(x - hi):
 // the 3-product split A_hi.B_hi + A_hi.B_lo + A_lo.B_hi keeps ~16 mantissa bits.
 __device__ __forceinline__ void split_bf16(float x, uint16_t& hi, uint16_t& lo) {

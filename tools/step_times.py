@@ -2,7 +2,7 @@
 (cfg1), L2 flushed between steps, to compare against the kernel-time sums of
 the ncu launch lists (gap / launch overhead inside the graph):
 
-  python tools/step_times.py [steps]
+  python tools/step_times.py [steps] [tile_size]
 """
 import sys
 
@@ -13,9 +13,13 @@ sys.path.insert(0, "/root/repo")
 import bench  # noqa: E402
 from paper_2403_01444_b200.stage1 import Stage1Config, Stage1Trainer  # noqa: E402
 
+from paper_2403_01444_b200.types import RasterSettings  # noqa: E402
+
 steps = int(sys.argv[1]) if len(sys.argv) > 1 else 150
+ts = int(sys.argv[2]) if len(sys.argv) > 2 else 16
 sc, cache, targets = bench.build_problem(1)
-tr = Stage1Trainer(sc.cloud, cache, list(zip(sc.cameras, targets)), Stage1Config())
+tr = Stage1Trainer(sc.cloud, cache, list(zip(sc.cameras, targets)),
+                   Stage1Config(raster=RasterSettings(tile_size=ts)))
 n = len(sc.cameras)
 for k in range(20):
     tr.iterate(k % n)
