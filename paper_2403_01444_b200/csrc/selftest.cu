@@ -173,16 +173,37 @@ __global__ void __launch_bounds__(128) umma_rate_kernel(int kind, int N, int a_t
   const uint32_t tmem = tbase;
   if (tid == 0) {
     const uint32_t a0 = umma::smem_u32(sm), b0 = umma::smem_u32(sm + 128 * 64 * 4);
-    const uint64_t da = kind ? umma::desc16_k(a0, 64, 0) : umma::desc_k(a0, 32, 0);
-    const uint64_t db = kind ? umma::desc16_k(b0, 64, 0) : umma::desc_k(b0, 32, 0);
-    const uint32_t id = kind ? umma::idesc_bf16(128, N, 0, 0) : umma::idesc_tf32(128, N, 0, 0);
+    // kind bits: 0 tf32 / 1 bf16; bit 1: MN-major A and B (bf16); bit 2:
+    // SWIZZLE_128B K-major descriptors (bf16; timing only, data ignored);
+    // bit 3: M = 64
+    const int bf = kind & 1, mn = (kind >> 1) & 1, swz = (kind >> 2) & 1, M = (kind & 8) ? 64 : 128;
+    uint64_t da = bf ? (mn ? umma::desc16_mn(a0, 128, 0) : umma::desc16_k(a0, 64, 0))
+                     : umma::desc_k(a0, 32, 0);
+    uint64_t db = bf ? (mn ? umma::desc16_mn(b0, 128, 0) : umma::desc16_k(b0, 64, 0))
+                     : umma::desc_k(b0, 32, 0);
+    if (swz) {
+      da = umma::desc(a0, 16u, 1024u) | (2ull << 61);
+      db = umma::desc(b0, 16u, 1024u) | (2ull << 61);
+    }
+    const uint32_t id = bf ? umma::idesc_bf16(M, N, mn, mn) : umma::idesc_tf32(M, N, 0, 0);
     unsigned long long c0 = clock64();
     // 16 MMAs per unrolled group, one code path per variant
 #define SS_RATE_LOOP(CALL)                       \
   for (int i = 0; i < count; i += 16) {          \
     _Pragma("unroll") for (int j = 0; j < 16; ++j) CALL; \
   }
-    if (kind) {
+    if (kind & 16) {  // bf16 3-product pattern over a K = 64 tile: A/B hi/lo alternate, K advances
+      const uint64_t dal = da + (uint64_t)((64 * 16 * 2) >> 4), dbl = db + (uint64_t)((64 * 16 * 2) >> 4);
+      for (int i = 0; i < count; i += 12) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint64_t o = (uint64_t)(256u >> 4) * k;
+          umma::mma_bf16(tmem, da + o, db + o, id, 1);
+          umma::mma_bf16(tmem, da + o, dbl + o, id, 1);
+          umma::mma_bf16(tmem, dal + o, db + o, id, 1);
+        }
+      }
+    } else if (kind & 1) {
       SS_RATE_LOOP(umma::mma_bf16(tmem, da, db, id, 1))
     } else if (a_tmem) {
       SS_RATE_LOOP(umma::mma_tf32_ts(tmem, tmem + 128u, db, id, 1))

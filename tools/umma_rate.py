@@ -10,13 +10,15 @@ from paper_2403_01444_b200.device import ptr, stream  # noqa: E402
 
 lib = _lib.load()
 out = torch.zeros(2, dtype=torch.int64, device="cuda")
-for kind, a_tmem, name in ((0, 0, "tf32 SS"), (0, 1, "tf32 TS"), (1, 0, "bf16 SS")):
-    for N in (16, 64, 128):
+for kind, a_tmem, name in ((0, 0, "tf32 SS"), (0, 1, "tf32 TS"), (1, 0, "bf16 SS K-major"),
+                           (3, 0, "bf16 SS MN-major"), (5, 0, "bf16 SS K-major 128B-swizzle"),
+                           (9, 0, "bf16 SS K-major M=64"), (11, 0, "bf16 SS MN-major M=64"),
+                           (17, 0, "bf16 3-product K=64 pattern")):
+    for N in ((64,) if kind & 16 else (16, 64, 128)):
         res = []
-        for count in (16, 256):
+        for count in ((24, 264) if kind & 16 else (16, 256)):
             lib.ss_debug_umma_rate(kind, N, a_tmem, count, ptr(out), stream())
             torch.cuda.synchronize()
             res.append(out.cpu().tolist())
         (t16, i16), (t256, i256) = res
-        print(f"{name} N={N:3d}: {(t256 - t16) / 240:6.1f} cyc/MMA (issue {(i256 - i16) / 240:5.1f}), "
-              f"16 MMAs: total {t16} issue {i16}")
+        print(f"{name:30s} N={N:3d}: {(t256 - t16) / 240:6.1f} cyc/MMA (issue {(i256 - i16) / 240:5.1f})")
