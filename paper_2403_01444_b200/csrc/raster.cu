@@ -614,7 +614,7 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_fwd_kernel(
     float* __restrict__ alpha_map, int32_t* __restrict__ touch) {
   constexpr int NT = BlendShape<TS>::NT, PPT = BlendShape<TS>::PPT;
   __shared__ float2 s_xy[NT];
-  __shared__ float4 s_co[NT];
+  __shared__ float4 s_co[TOUCH ? NT : 1];
   __shared__ float4 s_q[NT];
   __shared__ float4 s_col[NT];
   __shared__ int s_rank[NT];
@@ -648,7 +648,7 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_fwd_kernel(
       const int r = (int)vals[j];
       const double2 m = g.r_mean[r];
       s_xy[threadIdx.x] = make_float2((float)(m.x - x0), (float)(m.y - y0));
-      s_co[threadIdx.x] = g.r_conop[r];
+      if (TOUCH) s_co[threadIdx.x] = g.r_conop[r];  // the fast path uses the log2 form only
       s_q[threadIdx.x] = g.r_q[r];
       s_col[threadIdx.x] = g.r_color[r];
       s_rank[threadIdx.x] = r;
