@@ -260,35 +260,13 @@ __global__ void __launch_bounds__(256) gather_kernel(ss_grid g, int64_t n,
   for (int k = L * F; k < xs; ++k) xr[k] = 0.f;
 }
 
-// Warp-aggregated reduction of (vx, vy) into g[key]: lanes whose key equals
-// their left neighbour's form a run (the rows are Morton-ordered, so equal
-// corners are adjacent at the coarse levels); a segmented suffix sum gives
-// each run head the run total and only heads issue the vector reduction.
-// Non-adjacent duplicates are separate runs (still correct).  Lanes with
-// key == 0xffffffff are inactive.
-__device__ __forceinline__ void red_add_v2_agg(float* gl, uint32_t key, float vx, float vy) {
-  const int lane = threadIdx.x & 31;
-  const uint32_t prev = __shfl_up_sync(0xffffffffu, key, 1);
-  const bool head = lane == 0 || prev != key;
-  const uint32_t heads = __ballot_sync(0xffffffffu, head);
-  if (heads == 0xffffffffu) {  // no two adjacent lanes share a corner
-    if (key != 0xffffffffu) red_add_v2(gl + 2 * (size_t)key, vx, vy);
-    return;
-  }
-  const uint32_t after = heads & ~(0xffffffffu >> (31 - lane));  // heads strictly above lane
-  const int seg_end = after ? __ffs(after) - 1 : 32;
-#pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    const float ox = __shfl_down_sync(0xffffffffu, vx, off);
-    const float oy = __shfl_down_sync(0xffffffffu, vy, off);
-    if (lane + off < seg_end) vx += ox, vy += oy;
-  }
-  if (head && key != 0xffffffffu) red_add_v2(gl + 2 * (size_t)key, vx, vy);
-}
-
 // K1b: table scatter of the feature gradient (ntc.py:278-288), one thread per
 // inside row walking the levels, warp-aggregated vector reductions into the
-// L2-resident gradient tables.
+// L2-resident gradient tables: lanes whose corner equals their left
+// neighbour's form a run (rows are Morton-ordered, so equal corners are
+// adjacent at the coarse levels), a segmented suffix sum gives each run head
+// the run total and only heads issue red.global.add.v2.f32.  Non-adjacent
+// duplicates are separate runs (still correct).
 __global__ void __launch_bounds__(256) scatter_kernel(ss_grid g, int64_t n,
                                                       const float* __restrict__ means,
                                                       const int32_t* __restrict__ rows,
@@ -321,9 +299,43 @@ __global__ void __launch_bounds__(256) scatter_kernel(ss_grid g, int64_t n,
     if (F == 2) {
       const float2 d = ok ? *reinterpret_cast<const float2*>(dr + 2 * l) : make_float2(0.f, 0.f);
       const bool live = ok && (d.x != 0.f || d.y != 0.f);
+      // the 8 corners' warp aggregations side by side (independent shuffle
+      // chains overlap): runs of equal keys in adjacent lanes, segmented
+      // suffix sums over only as many steps as the longest run needs
+      const int lane = threadIdx.x & 31;
+      uint32_t key[8], seg_end[8];
+      float vx[8], vy[8];
+      bool head[8];
+      uint32_t all_heads = 0xffffffffu;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        key[k] = live ? idx[k] : 0xffffffffu;
+        vx[k] = w[k] * d.x;
+        vy[k] = w[k] * d.y;
+        const uint32_t prev = __shfl_up_sync(0xffffffffu, key[k], 1);
+        head[k] = lane == 0 || prev != key[k];
+        const uint32_t heads = __ballot_sync(0xffffffffu, head[k]);
+        all_heads &= heads;
+        const uint32_t after = heads & ~(0xffffffffu >> (31 - lane));  // heads above lane
+        seg_end[k] = after ? __ffs(after) - 1 : 32;
+      }
+      if (all_heads != 0xffffffffu) {
+        uint32_t run = 1;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) run = max(run, head[k] ? seg_end[k] - lane : 1u);
+        run = __reduce_max_sync(0xffffffffu, run);
+        for (int off = 1; off < (int)run; off <<= 1) {  // warp-uniform
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const float ox = __shfl_down_sync(0xffffffffu, vx[k], off);
+            const float oy = __shfl_down_sync(0xffffffffu, vy[k], off);
+            if (lane + off < (int)seg_end[k]) vx[k] += ox, vy[k] += oy;
+          }
+        }
+      }
 #pragma unroll
       for (int k = 0; k < 8; ++k)
-        red_add_v2_agg(gl, live ? idx[k] : 0xffffffffu, w[k] * d.x, w[k] * d.y);
+        if (head[k] && key[k] != 0xffffffffu) red_add_v2(gl + 2 * (size_t)key[k], vx[k], vy[k]);
     } else if (ok) {
       for (int f = 0; f < F; ++f) {
         const float d = dr[l * F + f];
