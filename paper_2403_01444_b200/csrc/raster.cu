@@ -592,6 +592,15 @@ __device__ __noinline__ float alpha_f64(const BlendParams& bp, const Geom& g, in
   return ad < bp.skip_d ? 0.f : fmaxf((float)ad, bp.skip);
 }
 
+// One staged splat of a blend batch: everything the inner loop reads, at one
+// base address (48 B: three vector loads, one pointer increment per splat)
+struct __align__(16) SplatRec {
+  float4 q;    // log2 form (A, B, C, reject threshold)
+  float4 col;  // rgb, opacity
+  float2 xy;   // mean relative to the tile origin
+  int rank, pad;
+};
+
 template <int TS>
 struct BlendShape {
   // 16x16 tiles: 128 threads with two pixels each (rows r and r + 8), which halves
@@ -613,11 +622,8 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_fwd_kernel(
     BlendParams bp, Geom g, const uint32_t* __restrict__ vals, float* __restrict__ image,
     float* __restrict__ alpha_map, int32_t* __restrict__ touch) {
   constexpr int NT = BlendShape<TS>::NT, PPT = BlendShape<TS>::PPT;
-  __shared__ float2 s_xy[NT];
+  __shared__ SplatRec s_sp[NT];
   __shared__ float4 s_co[TOUCH ? NT : 1];
-  __shared__ float4 s_q[NT];
-  __shared__ float4 s_col[NT];
-  __shared__ int s_rank[NT];
   __shared__ int s_touch[TOUCH ? NT : 1];
   const int tile = blockIdx.x;
   const int x0 = (tile % bp.ntx) * TS, y0 = (tile / bp.ntx) * TS;
@@ -647,20 +653,20 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_fwd_kernel(
     if (j < range.y) {
       const int r = (int)vals[j];
       const double2 m = g.r_mean[r];
-      s_xy[threadIdx.x] = make_float2((float)(m.x - x0), (float)(m.y - y0));
+      s_sp[threadIdx.x].xy = make_float2((float)(m.x - x0), (float)(m.y - y0));
       if (TOUCH) s_co[threadIdx.x] = g.r_conop[r];  // the fast path uses the log2 form only
-      s_q[threadIdx.x] = g.r_q[r];
-      s_col[threadIdx.x] = g.r_color[r];
-      s_rank[threadIdx.x] = r;
+      s_sp[threadIdx.x].q = g.r_q[r];
+      s_sp[threadIdx.x].col = g.r_color[r];
+      s_sp[threadIdx.x].rank = r;
     }
     if (TOUCH) s_touch[threadIdx.x] = 0;
     __syncthreads();
     const int cnt = min(NT, range.y - b);
     for (int k = 0; k < cnt; ++k) {
-      const float2 xy = s_xy[k];
+      const float2 xy = s_sp[k].xy;
       int contrib = 0;
       if (!TOUCH) {  // fast path: reject on the log2 form before the exponential
-        const float4 q = s_q[k];
+        const float4 q = s_sp[k].q;
         const float qhi = q.w + kNearBand;
         float lgs[PPT];
         bool live[PPT], any_live = false, any_near = false;
@@ -672,14 +678,14 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_fwd_kernel(
           any_near |= live[p] && lgs[p] < qhi;
         }
         if (!__any_sync(0xffffffffu, any_live)) continue;  // warp-uniform skip
-        const float4 col = s_col[k];
+        const float4 col = s_sp[k].col;
         float av[PPT];
 #pragma unroll
         for (int p = 0; p < PPT; ++p) av[p] = live[p] ? fminf(bp.clamp, col.w * ex2_approx(lgs[p])) : 0.f;
         if (any_near) {  // rare: decide in float64
 #pragma unroll
           for (int p = 0; p < PPT; ++p)
-            if (live[p] && lgs[p] < qhi) av[p] = alpha_f64(bp, g, s_rank[k], lx[p] + x0, ly[p] + y0);
+            if (live[p] && lgs[p] < qhi) av[p] = alpha_f64(bp, g, s_sp[k].rank, lx[p] + x0, ly[p] + y0);
         }
 #pragma unroll
         for (int p = 0; p < PPT; ++p) {  // predicated: a = 0 leaves the pixel unchanged
@@ -700,7 +706,7 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_fwd_kernel(
         if (done[p]) continue;
         const float dx = lx[p] - xy.x, dy = ly[p] - xy.y;
         float G, og;
-        const float a = pair_alpha(bp, dx, dy, co, s_rank[k], lx[p] + x0, ly[p] + y0, g.r_mean,
+        const float a = pair_alpha(bp, dx, dy, co, s_sp[k].rank, lx[p] + x0, ly[p] + y0, g.r_mean,
                                    g.r_conop_d, G, og);
         // Touch counts (rasterizer.py:279) count weight = alpha T_before > 0 in
         // float64.  With skip_alpha = 0 that includes alphas and transmittances far
@@ -720,7 +726,7 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_fwd_kernel(
           if (log((double)a) + logT[p] > lim) ++contrib;
           logT[p] += log1p(-(double)a);
         }
-        const float4 col = s_col[k];
+        const float4 col = s_sp[k].col;
         const float w = a * T[p];
         C[p][0] = fmaf(w, col.x, C[p][0]);
         C[p][1] = fmaf(w, col.y, C[p][1]);
@@ -741,7 +747,7 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_fwd_kernel(
     if (TOUCH) {
       __syncthreads();
       if (threadIdx.x < cnt && s_touch[threadIdx.x] > 0)
-        atomicAdd(&touch[g.order[s_rank[threadIdx.x]]], s_touch[threadIdx.x]);
+        atomicAdd(&touch[g.order[s_sp[threadIdx.x].rank]], s_touch[threadIdx.x]);
     }
   }
 #pragma unroll
@@ -774,10 +780,7 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_bwd_kernel(
   // d(maha)/d(mean2d) = -2C d, with the conic recovered from the log2 form
   // q = -0.5 log2(e) conic: k1, k2, k3 = kc (q.x, q.y / 2, q.z)
   constexpr float kc = 2.7725887222397811f;  // 4 / log2(e)
-  __shared__ float2 s_xy[NT];
-  __shared__ float4 s_q[NT];
-  __shared__ float4 s_col[NT];
-  __shared__ int s_rank[NT];
+  __shared__ SplatRec s_sp[NT];
   // each warp owns a slot per splat (plain stores, summed at the flush);
   // larger tiles share one slot through shared-memory atomics
   constexpr bool PRIV = NT / 32 <= 4;
@@ -828,16 +831,16 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_bwd_kernel(
       const int pos = end - 1 - threadIdx.x;
       const int r = (int)vals[pos];
       const double2 m = g.r_mean[r];
-      s_xy[threadIdx.x] = make_float2((float)(m.x - x0), (float)(m.y - y0));
-      s_q[threadIdx.x] = g.r_q[r];
-      s_col[threadIdx.x] = g.r_color[r];
-      s_rank[threadIdx.x] = r;
+      s_sp[threadIdx.x].xy = make_float2((float)(m.x - x0), (float)(m.y - y0));
+      s_sp[threadIdx.x].q = g.r_q[r];
+      s_sp[threadIdx.x].col = g.r_color[r];
+      s_sp[threadIdx.x].rank = r;
     }
     __syncthreads();
     for (int k = 0; k < cnt; ++k) {
       const int pos_rel = end - 1 - k - range.x;
-      const float2 xy = s_xy[k];
-      const float4 q = s_q[k];
+      const float2 xy = s_sp[k].xy;
+      const float4 q = s_sp[k].q;
       const float qhi = q.w + kNearBand;
       // cheap part for every pixel, then a warp-uniform skip; the rest is
       // predicated (a = 0 makes every update a no-op) instead of branching
@@ -853,7 +856,7 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_bwd_kernel(
         any_near |= live[p] && lgs[p] < qhi;
       }
       if (!__any_sync(0xffffffffu, any_live)) continue;
-      const float4 col = s_col[k];
+      const float4 col = s_sp[k].col;
       float Gs[PPT], av[PPT];
 #pragma unroll
       for (int p = 0; p < PPT; ++p) {
@@ -863,7 +866,7 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_bwd_kernel(
       if (any_near) {  // rare: decide in float64
 #pragma unroll
         for (int p = 0; p < PPT; ++p)
-          if (live[p] && lgs[p] < qhi) av[p] = alpha_f64(bp, g, s_rank[k], lx[p] + x0, ly[p] + y0);
+          if (live[p] && lgs[p] < qhi) av[p] = alpha_f64(bp, g, s_sp[k].rank, lx[p] + x0, ly[p] + y0);
       }
       float v[NA] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
       bool any = false;
@@ -935,7 +938,7 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_bwd_kernel(
     __syncthreads();
     // flush this batch's per-splat sums (one row per splat) and reset them
     if (threadIdx.x < cnt && s_any[threadIdx.x]) {
-      float* a = g.acc + (int64_t)s_rank[threadIdx.x] * kAccStride;
+      float* a = g.acc + (int64_t)s_sp[threadIdx.x].rank * kAccStride;
       float t[NA];
 #pragma unroll
       for (int q = 0; q < NA; ++q) t[q] = 0.f;
@@ -949,7 +952,7 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_bwd_kernel(
         }
       }
       {  // mean2d = -0.5 (-2C) [sum e, sum f]; conic terms times -0.5
-        const float4 q = s_q[threadIdx.x];
+        const float4 q = s_sp[threadIdx.x].q;
         const float k1 = kc * q.x, k2 = 0.5f * kc * q.y, k3 = kc * q.z;
         const float E = t[3], F = t[4];
         t[3] = -0.5f * fmaf(k1, E, k2 * F);
@@ -961,7 +964,7 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_bwd_kernel(
       red_add_v4(a, t[0], t[1], t[2], t[3]);
       red_add_v4(a + 4, t[4], t[5], t[6], t[7]);
       if (FULL) atomicAdd(a + 8, t[8]);
-      g.touched[s_rank[threadIdx.x]] = 1;
+      g.touched[s_sp[threadIdx.x].rank] = 1;
       s_any[threadIdx.x] = 0;
     }
     __syncthreads();
