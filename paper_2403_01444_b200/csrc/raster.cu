@@ -874,7 +874,7 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_bwd_kernel(
       for (int p = 0; p < PPT; ++p) {
         const float G = Gs[p], og = col.w * G, a = av[p];
         // one approximate reciprocal serves T_before = T / (1 - a) and S / (1 - a)
-        const float ioma = rcp_approx(fmaxf(1.f - a, 1e-12f));
+        const float ioma = rcp_approx(1.f - a);  // a <= alpha_clamp < 1
         const float tb = T[p] * ioma;
         const float w = a * tb;
         v[0] = fmaf(w, gp[p][0], v[0]);
