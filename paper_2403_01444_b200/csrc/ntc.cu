@@ -844,13 +844,13 @@ __global__ void __launch_bounds__(256) adam_kernel(
     double* __restrict__ m_p, double* __restrict__ v_p, const int32_t* __restrict__ step_dev,
     double lr, double b1, double b2, double eps, int zero_grads) {
   __shared__ double s_bc[2];
-  if (threadIdx.x == 0) {  // bias corrections once per block (optim.py:52-53)
+  if (threadIdx.x == 0) {  // bias corrections once per block (optim.py:52-53), as reciprocals
     const int step = *step_dev + 1;
-    s_bc[0] = 1.0 - pow(b1, (double)step);
-    s_bc[1] = 1.0 - pow(b2, (double)step);
+    s_bc[0] = 1.0 / (1.0 - pow(b1, (double)step));
+    s_bc[1] = 1.0 / (1.0 - pow(b2, (double)step));
   }
   __syncthreads();
-  const double bc1 = s_bc[0], bc2 = s_bc[1];
+  const double ibc1 = s_bc[0], ibc2 = s_bc[1];
   const int shift = (row_width & (row_width - 1)) == 0 ? __ffs(row_width) - 1 : -1;
   const int64_t total = n_table + n_params;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
@@ -872,7 +872,7 @@ __global__ void __launch_bounds__(256) adam_kernel(
     const double vv = b2 * v[j] + (1.0 - b2) * (g * g);
     m[j] = mm;
     v[j] = vv;
-    p[j] = (float)((double)p[j] - lr * (mm / bc1) / (sqrt(vv / bc2) + eps));
+    p[j] = (float)((double)p[j] - lr * (mm * ibc1) / (sqrt(vv * ibc2) + eps));
     if (zero_grads) gp[j] = 0.f;
   }
 }
