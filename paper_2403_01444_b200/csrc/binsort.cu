@@ -142,7 +142,10 @@ __global__ void __launch_bounds__(kBsThreads) bs_pass_kernel(
   // ---- decoupled look-back over the predecessors' per-digit counts
   uint32_t* my = status + (size_t)bid * 256 + d;
   uint32_t excl = 0;
-  if (bid == 0) {
+  if (d >> bits) {
+    // digit unused by a narrow pass (e.g. the 5-bit top pass of the tile key):
+    // nothing to publish or look back for
+  } else if (bid == 0) {
     atomicExch(my, kFlagInc | cnt);
   } else {
     atomicExch(my, kFlagAgg | cnt);
