@@ -58,9 +58,12 @@ def test_umma_tf32_a_from_tmem():
     np.testing.assert_allclose(out, ref, rtol=1e-5, atol=1e-4)
 
 
-@pytest.mark.parametrize("mode", [1, 2])
-def test_tensor_core_decoder_matches_fp32(mode):
-    """ss_ntc_forward with the tcgen05 decoder (3xTF32 / tf32) vs the FFMA path."""
+@pytest.mark.parametrize("mode,rows,hidden", [(1, 5000, 2), (2, 5000, 2), (1, 250000, 2),
+                                              (1, 200003, 1)])
+def test_tensor_core_decoder_matches_fp32(mode, rows, hidden):
+    """ss_ntc_forward with the tcgen05 decoder (3xTF32 / tf32) vs the FFMA path.
+    The large cases give every CTA many tiles (both pipeline slots, odd tile
+    counts, a ragged last tile)."""
     torch = pytest.importorskip("torch")
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
@@ -70,9 +73,10 @@ def test_tensor_core_decoder_matches_fp32(mode):
 
     lib = _lib.load()
     sc = scenes.config(1)
-    cache = NeuralTransformationCache(HashGridConfig.from_any(sc.grid), output_init="random")
+    cache = NeuralTransformationCache(HashGridConfig.from_any(sc.grid), hidden_layers=hidden,
+                                      output_init="random")
     cache.tables[:] = np.random.default_rng(0).uniform(-0.5, 0.5, size=cache.tables.shape)
-    x = sc.cloud["means"][:5000]
+    x = sc.cloud["means"][:rows]
     lib.ss_set_mlp_mode(0)
     ref, _, _ = cache.forward(x)
     ref = np.concatenate([ref, cache.forward(x)[1]], 1)
@@ -117,8 +121,9 @@ def test_umma_bf16_layouts(M, N, flags):
     np.testing.assert_allclose(dd.cpu().numpy().astype(np.float64), ref, rtol=1e-5, atol=1e-4)
 
 
-@pytest.mark.parametrize("cfg,hidden", [(1, 2), (0, 2), (0, 1)])
-def test_tensor_core_decoder_backward_matches_fp32(cfg, hidden):
+@pytest.mark.parametrize("cfg,hidden,rows", [(1, 2, 3001), (0, 2, 3001), (0, 1, 3001),
+                                             (1, 2, 150001)])
+def test_tensor_core_decoder_backward_matches_fp32(cfg, hidden, rows):
     """ss_ntc_backward with the tcgen05 decoder backward (bf16 hi/lo split) vs
     the FFMA fp32 path: every weight, bias and table gradient, norm-relative."""
     torch = pytest.importorskip("torch")
@@ -134,7 +139,7 @@ def test_tensor_core_decoder_backward_matches_fp32(cfg, hidden):
                                       output_init="random")
     rng = np.random.default_rng(1)
     cache.tables[:] = rng.uniform(-0.5, 0.5, size=cache.tables.shape)
-    x = sc.cloud["means"][:3001]  # ragged last tile
+    x = sc.cloud["means"][:rows]  # ragged last tile; 150001 rows: many tiles per CTA
     g_mu, g_q = rng.normal(size=(len(x), 3)), rng.normal(size=(len(x), 4))
     out = {}
     for mode in (0, 1):
