@@ -63,15 +63,27 @@ __global__ void __launch_bounds__(SW * 3, 5) ssim_map_kernel(LossParams lp,
   const int64_t cs = ((int64_t)oy0 * lp.W + min(x0 + SW / 2, lp.W - 1)) * C + c;
   const float shx = __ldg(img + cs), shy = __ldg(tgt + cs);
   float px[PER], py[PER], qx[PER], qy[PER];  // two rows in flight (no register moves)
+  // rows are fetched strictly in order, so the addresses advance by one image
+  // row per call (no per-load 64-bit index arithmetic)
+  bool col_in[PER];
+#pragma unroll
+  for (int m = 0; m < PER; ++m) col_in[m] = lane + m * SW < RW && x0 + lane + m * SW < lp.W;
+  const int64_t row_stride = (int64_t)lp.W * C;
+  const float* fimg = img + ((int64_t)oy0 * lp.W + x0 + lane) * C + c;
+  const float* ftgt = tgt + ((int64_t)oy0 * lp.W + x0 + lane) * C + c;
+  int fy_next = oy0;
   auto fetch = [&](int y, float (&fx)[PER], float (&fy)[PER]) {
+    (void)y;  // == fy_next
+    const bool row_ok = fy_next < lp.H;
 #pragma unroll
     for (int m = 0; m < PER; ++m) {
-      const int e = lane + m * SW;
-      const bool ok = e < RW && y < lp.H && x0 + e < lp.W;
-      const int64_t o = ((int64_t)y * lp.W + x0 + e) * C + c;
-      fx[m] = ok ? __ldg(img + o) : 0.f;
-      fy[m] = ok ? __ldg(tgt + o) : 0.f;
+      const bool ok = row_ok && col_in[m];
+      fx[m] = ok ? __ldg(fimg + m * SW * C) : 0.f;
+      fy[m] = ok ? __ldg(ftgt + m * SW * C) : 0.f;
     }
+    fimg += row_stride;
+    ftgt += row_stride;
+    ++fy_next;
   };
   auto stage = [&](int buf, const float (&fx)[PER], const float (&fy)[PER]) {
 #pragma unroll
