@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(128) umma_rate_kernel(int kind, int N, int a_t
   __shared__ uint64_t bar;
   __shared__ uint32_t tbase;
   const int tid = threadIdx.x, warp = tid >> 5;
-  for (int i = tid; i < (128 * 64 + 64 * 64) / 4 * 4; i += 128) reinterpret_cast<float*>(sm)[i] = 0.f;
+  for (int i = tid; i < (128 * 64 * 4 + 128 * 128 * 2) / 4; i += 128) reinterpret_cast<float*>(sm)[i] = 0.f;
   if (tid == 0) {
     umma::mbar_init(&bar, 1);
     umma::fence_mbar_init();
@@ -192,7 +192,17 @@ __global__ void __launch_bounds__(128) umma_rate_kernel(int kind, int N, int a_t
   for (int i = 0; i < count; i += 16) {          \
     _Pragma("unroll") for (int j = 0; j < 16; ++j) CALL; \
   }
-    if (kind & 16) {  // bf16 3-product pattern over a K = 64 tile: A/B hi/lo alternate, K advances
+    if (kind & 32) {  // the decoder backward's weight-gradient GEMM: M = 64, A = D^T (MN-major,
+                      // tile cols 64), B = [H | 1] (MN-major, tile cols N), K = 128 rows
+      const uint64_t A0 = umma::desc16_mn(a0, 64, 0), B0 = umma::desc16_mn(b0, N, 0);
+      const uint32_t ks_a = (2u * umma::sbo16(64)) >> 4, ks_b = (2u * umma::sbo16(N)) >> 4;
+      const uint32_t idw = umma::idesc_bf16(64, N, 1, 1);
+      for (int i = 0; i < count; i += 8) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          umma::mma_bf16(tmem, A0 + (uint64_t)ks_a * k, B0 + (uint64_t)ks_b * k, idw, 1);
+      }
+    } else if (kind & 16) {  // bf16 3-product pattern over a K = 64 tile: A/B hi/lo alternate, K advances
       const uint64_t dal = da + (uint64_t)((64 * 16 * 2) >> 4), dbl = db + (uint64_t)((64 * 16 * 2) >> 4);
       for (int i = 0; i < count; i += 12) {
 #pragma unroll
@@ -259,7 +269,7 @@ extern "C" int ss_selftest_umma(int32_t M, int32_t N, int32_t K, int32_t flags, 
 // kind 0 tf32 / 1 bf16, a_tmem (tf32 only): see umma_rate_kernel
 extern "C" int ss_debug_umma_rate(int32_t kind, int32_t N, int32_t a_tmem, int32_t count,
                                   uint64_t* out_dev, void* stream) {
-  const size_t smem = 128 * 64 * 4 + 64 * 64 * 4;
+  const size_t smem = 128 * 64 * 4 + 128 * 128 * 2;
   auto k = ss::umma_rate_kernel;
   SS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   k<<<1, 128, smem, ss::as_stream(stream)>>>(kind, N, a_tmem, count,
