@@ -372,9 +372,9 @@ __global__ void __launch_bounds__(128) mlp_fwd_kernel(int64_t n, const float* __
 }
 
 // K3f: transform (transform.py:70-84): mu' = mu + d_mu, q' = norm(d_q) (x) q_src,
-// SH bands >= 1 rotated by R(norm(d_q)).  Four lanes per inside row (rows in
-// index order, so the 4-lane groups of a warp read 8 consecutive cloud rows):
-// lanes 0-2 rotate one colour channel each, lane 3 writes mean and rotation.
+// SH bands >= 1 rotated by R(norm(d_q)).  Three lanes per inside row (rows in
+// index order, so a warp reads ~11 consecutive cloud rows): lane c rotates
+// colour channel c; lane 0 also writes the mean and the rotation.
 template <int DEG>
 __global__ void __launch_bounds__(128) transform_kernel(ss_cloud src, int64_t n,
                                                         const int32_t* __restrict__ rows,
@@ -385,9 +385,11 @@ __global__ void __launch_bounds__(128) transform_kernel(ss_cloud src, int64_t n,
                                                         float* __restrict__ t_sh,
                                                         uint32_t* status) {
   constexpr int K = (DEG + 1) * (DEG + 1);
+  // three lanes per row (no idle fourth lane): lane c rotates colour channel c,
+  // lane 0 also writes the mean and the rotation
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int64_t j = t >> 2;
-  const int c = (int)(t & 3);
+  const int64_t j = t / 3;
+  const int c = (int)(t - 3 * j);
   if (j >= n) return;
   // rows in index order (coalesced cloud rows); pos = the row's slot in out7
   const int64_t gid = rows ? rows[j] : j;
@@ -397,11 +399,11 @@ __global__ void __launch_bounds__(128) transform_kernel(ss_cloud src, int64_t n,
   for (int k = 0; k < 7; ++k) o[k] = out7[i * os + k];
   float nq = sqrtf(o[3] * o[3] + o[4] * o[4] + o[5] * o[5] + o[6] * o[6]);
   if (nq < 1e-12f) {  // gaussians.py:46-47
-    if (status && c == 3) atomicOr(status, SS_FLAG_ZERO_QUAT);
+    if (status && c == 0) atomicOr(status, SS_FLAG_ZERO_QUAT);
     nq = 1.f;
   }
   const float u[4] = {o[3] / nq, o[4] / nq, o[5] / nq, o[6] / nq};
-  if (c == 3) {
+  if (c == 0) {
     const float* m = src.means + 3 * gid;
     t_means[3 * gid + 0] = m[0] + o[0];
     t_means[3 * gid + 1] = m[1] + o[1];
@@ -411,7 +413,6 @@ __global__ void __launch_bounds__(128) transform_kernel(ss_cloud src, int64_t n,
     float qo[4];
     quat_mul(u, qs, qo);
     *reinterpret_cast<float4*>(t_rot + 4 * gid) = make_float4(qo[0], qo[1], qo[2], qo[3]);
-    return;
   }
   if (DEG < 1 || !rotate_sh) return;
   float R[3][3];
@@ -1022,7 +1023,7 @@ int transform_run(const ss_cloud* src, int64_t n, const int32_t* rows, const int
   if (n == 0) return SS_OK;
   SS_TRY(ensure_shrot_const());
   prof_begin(PH_TRANSFORM, st);
-  const unsigned grid = (unsigned)cdiv(4 * n, 128);  // 4 lanes per row
+  const unsigned grid = (unsigned)cdiv(3 * n, 128);  // 3 lanes per row
   switch (sh_degree_of(src->sh_coeffs)) {
     case 0: transform_kernel<0><<<grid, 128, 0, st>>>(*src, n, rows, pos, out7, os, rotate_sh, tm, tr, ts, status); break;
     case 1: transform_kernel<1><<<grid, 128, 0, st>>>(*src, n, rows, pos, out7, os, rotate_sh, tm, tr, ts, status); break;
