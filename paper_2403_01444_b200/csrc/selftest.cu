@@ -160,7 +160,12 @@ __global__ void __launch_bounds__(128) umma_rate_kernel(int kind, int N, int a_t
   __shared__ uint64_t bar;
   __shared__ uint32_t tbase;
   const int tid = threadIdx.x, warp = tid >> 5;
-  for (int i = tid; i < (128 * 64 * 4 + 128 * 128 * 2) / 4; i += 128) reinterpret_cast<float*>(sm)[i] = 0.f;
+  // operands: zeros, or (kind bit 6) pseudo-random values (data-dependent MMA rate)
+  for (int i = tid; i < (128 * 64 * 4 + 128 * 128 * 2) / 4; i += 128) {
+    uint32_t h = (uint32_t)i * 2654435761u;
+    h ^= h >> 15;
+    reinterpret_cast<uint32_t*>(sm)[i] = (kind & 64) ? (h & 0x3fff3fffu) | 0x3c003c00u : 0u;
+  }
   if (tid == 0) {
     umma::mbar_init(&bar, 1);
     umma::fence_mbar_init();

@@ -14,8 +14,11 @@ for kind, a_tmem, name in ((0, 0, "tf32 SS"), (0, 1, "tf32 TS"), (1, 0, "bf16 SS
                            (3, 0, "bf16 SS MN-major"), (5, 0, "bf16 SS K-major 128B-swizzle"),
                            (9, 0, "bf16 SS K-major M=64"), (11, 0, "bf16 SS MN-major M=64"),
                            (17, 0, "bf16 3-product K=64 pattern"),
-                           (33, 0, "bf16 dW GEMM M=64 MN/MN K=128")):
-    for N in ((64,) if kind & 16 else ((8, 40, 64, 72, 80) if kind & 32 else (16, 64, 128))):
+                           (33, 0, "bf16 dW GEMM M=64 MN/MN K=128"),
+                           (1 | 64, 0, "bf16 SS K-major random data"),
+                           (33 | 64, 0, "bf16 dW GEMM random data"),
+                           (0 | 64, 0, "tf32 SS random data"), (0 | 64, 1, "tf32 TS random data")):
+    for N in ((64,) if kind & 16 else ((8, 40, 64, 72, 80) if kind & 32 else ((64,) if kind & 64 else (16, 64, 128)))):
         res = []
         for count in ((24, 264) if kind & 16 else ((16, 256) if not kind & 32 else (16, 256))):
             lib.ss_debug_umma_rate(kind, N, a_tmem, count, ptr(out), stream())
