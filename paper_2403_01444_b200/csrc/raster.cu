@@ -228,7 +228,7 @@ __device__ inline void project_one(const CamD& cam, const ss_cloud& cl, int64_t 
 
 // K4a: per-Gaussian projection; depth key (+inf when culled)
 template <int DEG>
-__global__ void __launch_bounds__(256) preprocess_kernel(CamD cam, ss_cloud cl, Geom g) {
+__global__ void __launch_bounds__(256, 3) preprocess_kernel(CamD cam, ss_cloud cl, Geom g) {
   __shared__ uint32_t s_hist[4][256];  // the depth sort's digit histograms
   for (int k = threadIdx.x; k < 1024; k += blockDim.x) (&s_hist[0][0])[k] = 0;
   __syncthreads();
