@@ -189,6 +189,42 @@ def test_raster_random_scenes_vs_oracle(P, deg):
         assert G.norm_rel(getattr(g, k), rg[rk]) <= GRAD_TOL, k
 
 
+@pytest.mark.parametrize("case", ["mostly_offscreen", "huge_splats"])
+def test_raster_adversarial_scenes_vs_oracle(P, case):
+    """Pair-generation corner cases against the oracle: most Gaussians in front
+    of the camera but off-screen, with zero tile pairs interleaved in depth
+    order (a 1024-pair duplicate chunk then spans more ranks than its staged
+    offsets hold), and a few near-camera splats covering every tile next to
+    many small ones (long per-rank pair runs)."""
+    from paper_2403_01444_b200 import scenes
+
+    sc = scenes.small_scene(seed=77, n=6000, width=96, height=72, sh_degree=1)
+    cloud = {k: np.array(v, copy=True) for k, v in sc.cloud.items()}
+    rng = np.random.default_rng(5)
+    if case == "mostly_offscreen":
+        far = rng.random(len(cloud["means"])) < 0.9
+        cloud["means"][far, 0] += 60.0
+    else:
+        big = rng.choice(len(cloud["means"]), 8, replace=False)
+        cloud["log_scales"][big] = np.log(3.0)
+    # both sides see the same fp32-lattice values (SURVEY.md §8 c6)
+    cloud = {k: v.astype(np.float32).astype(np.float64) for k, v in cloud.items()}
+    R, T = P["rasterizer"], P["types"]
+    cam = sc.cameras[0]
+    bg = np.array([0.1, 0.2, 0.3])
+    ref, rctx = O.render(cloud, cam, bg)
+    out, ctx = R.rasterize_forward(T.GaussianCloud(**cloud), T.Camera.from_any(cam), bg)
+    assert np.abs(out.image - ref["image"]).max() <= IMG_TOL
+    np.testing.assert_array_equal(ctx.indices, rctx["proj"]["indices"])
+    mem = np.concatenate([t[4] for t in ctx.tiles])
+    np.testing.assert_array_equal(mem, np.concatenate([t[4] for t in rctx["tiles"]]))
+    d_img = np.random.default_rng(1).normal(size=out.image.shape)
+    g = R.rasterize_backward(ctx, d_img)
+    rg = O.render_backward(rctx, d_img)
+    for k in ("d_means", "d_rotations", "d_log_scales", "d_opacity_logits", "d_sh"):
+        assert G.norm_rel(getattr(g, k), rg[k]) <= GRAD_TOL, k
+
+
 def test_stage1_cfg0_single_step_vs_oracle(P):
     """The parity config (BASELINE configs[0]): one full Stage-1 step, fp32."""
     from paper_2403_01444_b200 import scenes
