@@ -58,9 +58,10 @@ def test_umma_tf32_a_from_tmem():
     np.testing.assert_allclose(out, ref, rtol=1e-5, atol=1e-4)
 
 
-@pytest.mark.parametrize("mode,rows,hidden", [(1, 5000, 2), (2, 5000, 2), (1, 250000, 2),
-                                              (1, 200003, 1)])
-def test_tensor_core_decoder_matches_fp32(mode, rows, hidden):
+@pytest.mark.parametrize("mode,rows,hidden,cfg", [(1, 5000, 2, 1), (2, 5000, 2, 1),
+                                                  (1, 250000, 2, 1), (1, 200003, 1, 1),
+                                                  (1, 20000, 1, 0)])
+def test_tensor_core_decoder_matches_fp32(mode, rows, hidden, cfg):
     """ss_ntc_forward with the tcgen05 decoder (3xTF32 / tf32) vs the FFMA path.
     The large cases give every CTA many tiles (both pipeline slots, odd tile
     counts, a ragged last tile)."""
@@ -72,7 +73,7 @@ def test_tensor_core_decoder_matches_fp32(mode, rows, hidden):
     from paper_2403_01444_b200.types import HashGridConfig
 
     lib = _lib.load()
-    sc = scenes.config(1)
+    sc = scenes.config(cfg)  # cfg 0: 16 input features; cfg 1: 32
     cache = NeuralTransformationCache(HashGridConfig.from_any(sc.grid), hidden_layers=hidden,
                                       output_init="random")
     cache.tables[:] = np.random.default_rng(0).uniform(-0.5, 0.5, size=cache.tables.shape)
