@@ -878,6 +878,55 @@ __global__ void __launch_bounds__(256) adam_kernel(
   }
 }
 
+// Two-feature tables (the common F = 2): one row per thread iteration with
+// 8/16-byte vector accesses and one mask read per row; the MLP part is scalar.
+__global__ void __launch_bounds__(256) adam_rows2_kernel(
+    int64_t n_rows, float2* __restrict__ tables, float2* __restrict__ g_tables,
+    double2* __restrict__ m_t, double2* __restrict__ v_t, const uint8_t* __restrict__ row_mask,
+    int64_t n_params, float* __restrict__ params, float* __restrict__ g_params,
+    double* __restrict__ m_p, double* __restrict__ v_p, const int32_t* __restrict__ step_dev,
+    double lr, double b1, double b2, double eps, int zero_grads) {
+  __shared__ double s_bc[2];
+  if (threadIdx.x == 0) {  // bias corrections once per block (optim.py:52-53), as reciprocals
+    const int step = *step_dev + 1;
+    s_bc[0] = 1.0 / (1.0 - pow(b1, (double)step));
+    s_bc[1] = 1.0 / (1.0 - pow(b2, (double)step));
+  }
+  __syncthreads();
+  const double ibc1 = s_bc[0], ibc2 = s_bc[1];
+  auto upd = [&](double g, double& m, double& v, float& p) {
+    m = b1 * m + (1.0 - b1) * g;
+    v = b2 * v + (1.0 - b2) * (g * g);
+    p = (float)((double)p - lr * (m * ibc1) / (sqrt(v * ibc2) + eps));
+  };
+  const int64_t total = n_rows + n_params;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (i < n_rows) {
+      // untouched rows: no Adam update, and their gradient is never written
+      if (row_mask && !row_mask[i]) continue;
+      const float2 g = g_tables[i];
+      double2 m = m_t[i], v = v_t[i];
+      float2 p = tables[i];
+      upd(g.x, m.x, v.x, p.x);
+      upd(g.y, m.y, v.y, p.y);
+      m_t[i] = m;
+      v_t[i] = v;
+      tables[i] = p;
+      if (zero_grads) g_tables[i] = make_float2(0.f, 0.f);
+    } else {
+      const int64_t j = i - n_rows;
+      double m = m_p[j], v = v_p[j];
+      float p = params[j];
+      upd(g_params[j], m, v, p);
+      m_p[j] = m;
+      v_p[j] = v;
+      params[j] = p;
+      if (zero_grads) g_params[j] = 0.f;
+    }
+  }
+}
+
 __global__ void increment_kernel(int32_t* step) { *step += 1; }
 
 // ------------------------------------------------------------------ dispatch
@@ -1269,10 +1318,24 @@ int ss_adam_step(int64_t n_table, float* tables, float* g_tables, double* m_tabl
   if (total > 0) {
     const unsigned blocks = (unsigned)std::min<int64_t>(cdiv(total, 256), 148 * 8);
     prof_begin(PH_ADAM, st);
-    adam_kernel<<<blocks, 256, 0, st>>>(n_table, tables, g_tables, m_tables, v_tables, row_mask,
-                                        row_width, n_params, params, g_params, m_params,
-                                        v_params, step_dev, lr, beta1, beta2, eps, zero_grads);
-    SS_CHECK_LAUNCH("adam_kernel");
+    const bool rows2 = row_width == 2 && n_table % 2 == 0 &&
+                       ((reinterpret_cast<uintptr_t>(tables) | reinterpret_cast<uintptr_t>(g_tables) |
+                         reinterpret_cast<uintptr_t>(m_tables) | reinterpret_cast<uintptr_t>(v_tables)) &
+                        15) == 0;
+    if (rows2) {
+      const unsigned b2 = (unsigned)std::min<int64_t>(cdiv(n_table / 2 + n_params, 256), 148 * 8);
+      adam_rows2_kernel<<<b2, 256, 0, st>>>(
+          n_table / 2, reinterpret_cast<float2*>(tables), reinterpret_cast<float2*>(g_tables),
+          reinterpret_cast<double2*>(m_tables), reinterpret_cast<double2*>(v_tables), row_mask,
+          n_params, params, g_params, m_params, v_params, step_dev, lr, beta1, beta2, eps,
+          zero_grads);
+      SS_CHECK_LAUNCH("adam_rows2_kernel");
+    } else {
+      adam_kernel<<<blocks, 256, 0, st>>>(n_table, tables, g_tables, m_tables, v_tables, row_mask,
+                                          row_width, n_params, params, g_params, m_params,
+                                          v_params, step_dev, lr, beta1, beta2, eps, zero_grads);
+      SS_CHECK_LAUNCH("adam_kernel");
+    }
     prof_end(PH_ADAM, st);
   }
   increment_kernel<<<1, 1, 0, st>>>(step_dev);
