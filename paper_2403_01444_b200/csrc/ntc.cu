@@ -232,6 +232,34 @@ __global__ void __launch_bounds__(256) gather_kernel(ss_grid g, int64_t n,
   if (!normalise(g, means + 3 * gid, xn) && status) atomicOr(status, SS_FLAG_OUTSIDE);
   const size_t T = (size_t)1 << g.log2_table;
   float* xr = X + i * xs;
+  if (F == 2 && (L & 1) == 0) {
+    // two levels per step: 16 corner gathers in flight, one 16-byte store
+    for (int l = 0; l < L; l += 2) {
+      uint32_t ia[8], ib[8];
+      float wa[8], wb[8];
+      level_corners(g, l, xn, ia, wa);
+      level_corners(g, l + 1, xn, ib, wb);
+      const float2* ta = reinterpret_cast<const float2*>(tables + (size_t)l * T * 2);
+      const float2* tb = reinterpret_cast<const float2*>(tables + (size_t)(l + 1) * T * 2);
+      float2 va[8], vb[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        va[k] = __ldg(ta + ia[k]);
+        vb[k] = __ldg(tb + ib[k]);
+      }
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        acc.x = fmaf(wa[k], va[k].x, acc.x);
+        acc.y = fmaf(wa[k], va[k].y, acc.y);
+        acc.z = fmaf(wb[k], vb[k].x, acc.z);
+        acc.w = fmaf(wb[k], vb[k].y, acc.w);
+      }
+      *reinterpret_cast<float4*>(xr + 2 * l) = acc;
+    }
+    for (int k = L * F; k < xs; ++k) xr[k] = 0.f;
+    return;
+  }
   for (int l = 0; l < L; ++l) {
     uint32_t idx[8];
     float w[8];
