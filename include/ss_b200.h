@@ -314,6 +314,15 @@ typedef struct ss_stage1 {
   void *geom, *bins, *loss_scratch, *ntc_scratch;
   int64_t bin_capacity; /* n_pairs the `bins` workspace holds; more raises
                            SS_FLAG_OVERFLOW in *status (the pairs beyond are dropped) */
+  double ssim_c1, ssim_c2; /* LossConfig.ssim_c1 / ssim_c2 (losses.py:21-33); the window is
+                              the reference default 11x11, sigma 1.5 */
+  float* loss_accum;       /* nullable: every iteration adds its (unscaled) loss here, the
+                              batch-loss sum of view-sharded training */
+  int32_t defer_scatter;   /* != 0: ss_stage1_iter_grads stops after the decoder backward
+                              (g_params final, dX in ntc_scratch); ss_stage1_table_scatter
+                              then adds the table gradient (lets the caller start the
+                              g_params all-reduce while the scatter runs) */
+  int32_t reserved2;
 } ss_stage1;
 
 /* Start of a frame: touched-row mask, transformed <- source copy, zero Adam
@@ -332,6 +341,9 @@ int ss_stage1_iter_finish(ss_stage1* st, const ss_camera* cam, const float* targ
 int ss_stage1_iter_grads(ss_stage1* st, const ss_camera* cam, const float* target,
                          int64_t n_pairs, float grad_scale, void* stream);
 int ss_stage1_apply_adam(ss_stage1* st, void* stream);
+/* The hash-table scatter (ntc.py:278-288) of the last ss_stage1_iter_grads call
+ * made with defer_scatter != 0: g_tables += the corner-weighted feature gradient. */
+int ss_stage1_table_scatter(ss_stage1* st, void* stream);
 /* One whole iteration (parts A and B, plus Adam when apply_adam != 0) with no
  * host synchronisation: the pair count stays on the device and the binning
  * is bounded by bin_capacity (overflow -> SS_FLAG_OVERFLOW).  Stream-ordered,

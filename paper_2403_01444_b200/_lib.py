@@ -79,7 +79,9 @@ class Stage1(C.Structure):
                 ("loss_dev", P), ("loss_history", P), ("pair_history", P),
                 ("history_len", C.c_int64), ("iteration", C.c_int32), ("iter_dev", P),
                 ("status", P), ("geom", P), ("bins", P), ("loss_scratch", P),
-                ("ntc_scratch", P), ("bin_capacity", C.c_int64)]
+                ("ntc_scratch", P), ("bin_capacity", C.c_int64),
+                ("ssim_c1", C.c_double), ("ssim_c2", C.c_double), ("loss_accum", P),
+                ("defer_scatter", C.c_int32), ("reserved2", C.c_int32)]
 
 
 STRUCTS = [Grid, Mlp, MlpLayout, Camera, RasterSettings, Cloud, CloudGrads, Stage1]
@@ -127,6 +129,7 @@ SIGNATURES = [
     ("ss_stage1_iter_finish", I32, [C.POINTER(Stage1), PCam, P, I64, P]),
     ("ss_stage1_iter_grads", I32, [C.POINTER(Stage1), PCam, P, I64, C.c_float, P]),
     ("ss_stage1_apply_adam", I32, [C.POINTER(Stage1), P]),
+    ("ss_stage1_table_scatter", I32, [C.POINTER(Stage1), P]),
     ("ss_stage1_iter", I32, [C.POINTER(Stage1), PCam, P, C.c_float, I32, P]),
     ("ss_stage1_render", I32, [C.POINTER(Stage1), PCam, P]),
     ("ss_set_mlp_mode", I32, [I32]),

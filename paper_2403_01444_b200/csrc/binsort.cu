@@ -94,9 +94,9 @@ __global__ void __launch_bounds__(kBsThreads) bs_pass_kernel(
   constexpr int kBsSteps = STEPS, kBsTile = kBsThreads * STEPS;
   __shared__ uint32_t s_keys[kBsTile], s_vals[kBsTile];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  // ticket == nullptr: the whole grid is co-resident (host-checked), so the
-  // block index itself orders the look-back without the ticket round trip
-  if (tid == 0) s_bid = ticket ? atomicAdd(ticket, 1u) : blockIdx.x;
+  // logical tile id from the ticket: every predecessor of a running CTA has
+  // already been scheduled, whatever order the hardware dispatches blocks in
+  if (tid == 0) s_bid = atomicAdd(ticket, 1u);
   for (int i = tid; i < kBsWarps * 256; i += kBsThreads) (&wh[0][0])[i] = 0;
   __syncthreads();
   const int64_t n = min(*d_n, cap);
@@ -258,21 +258,11 @@ int binsort_run(const BinSortWS& w, uint32_t* keys_tmp, uint32_t* vals_tmp, uint
   }
   uint32_t* tickets = w.hist + kMaxPasses * 256;
   const unsigned grid = (unsigned)w.max_blocks;
-  static int resident = 0;  // CTAs of either pass kernel that fit on the device at once
-  if (!resident) {
-    int dev = 0, sms = 0, a = 0, b = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, bs_pass_kernel<kBsStepsSmall>, kBsThreads, 0);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, bs_pass_kernel<kBsStepsBig>, kBsThreads, 0);
-    resident = std::max(1, sms * std::min(a, b));
-  }
-  const bool co_resident = (int64_t)grid <= resident;
   for (int p = 0; p < passes; ++p) {
     const int bits = std::min(8, key_bits - 8 * p);
     auto k = w.steps == kBsStepsSmall ? bs_pass_kernel<kBsStepsSmall> : bs_pass_kernel<kBsStepsBig>;
     k<<<grid, kBsThreads, 0, st>>>(ka, va, kb, vb, d_n, cap, 8 * p, bits, w.hist + 256 * p,
-                                   co_resident ? nullptr : tickets + p,
+                                   tickets + p,
                                    w.status + (size_t)p * w.max_blocks * 256);
     SS_CHECK_LAUNCH("bs_pass_kernel");
     std::swap(ka, kb);

@@ -229,10 +229,13 @@ int raster_backward(const ss_cloud* cl, const ss_camera* cam, const ss_raster_se
 // CUDA events recorded on the launching stream around each hot-path phase when
 // enabled with ss_profile_enable(1); read back with ss_profile_read().
 namespace ss {
+// One phase per kernel, except depth_sort / tile_sort (radix passes + tie fix-up)
+// and rank_scan (rank kernel + scan).
 enum Phase {
-  PH_NTC_FWD = 0, PH_PROJECT, PH_DEPTH_SORT, PH_RANK_SCAN, PH_DUPLICATE, PH_TILE_SORT,
-  PH_RANGES, PH_BLEND_FWD, PH_LOSS, PH_BLEND_BWD, PH_GAUSS_BWD, PH_NTC_BWD, PH_ADAM,
-  PH_TRANSFORM, PH_TRANSFORM_BWD, PH_COUNT
+  PH_GATHER = 0, PH_DECODER_FWD, PH_TRANSFORM, PH_PROJECT, PH_DEPTH_SORT, PH_RANK_SCAN,
+  PH_DUPLICATE, PH_TILE_SORT, PH_RANGES, PH_BLEND_FWD, PH_SSIM_MAP, PH_SSIM_GRAD,
+  PH_BLEND_BWD, PH_GAUSS_BWD, PH_TRANSFORM_BWD, PH_DECODER_BWD, PH_SCATTER, PH_ADAM,
+  PH_COUNT
 };
 void prof_begin(int phase, cudaStream_t s);
 void prof_end(int phase, cudaStream_t s);
@@ -289,6 +292,9 @@ int ntc_backward_run(const ss_grid* g, const ss_mlp* mlp, int64_t n, const float
                      const int32_t* rows, const float* params, const float* X, int xs,
                      const float* g_out, int gs, const uint64_t* relu, float* dX,
                      float* g_tables, float* g_params, cudaStream_t st);
+// K1b alone: g_tables += corner-weighted dX (ntc.py:278-288)
+int ntc_scatter_run(const ss_grid* g, int64_t n, const float* means, const int32_t* rows,
+                    const float* dX, int xs, float* g_tables, cudaStream_t st);
 // rows: cloud row of thread j; pos (nullable = identity): its slot in out7 / g7
 int transform_run(const ss_cloud* src, int64_t n, const int32_t* rows, const int32_t* pos,
                   const float* out7, int os, int rotate_sh, float* tm, float* tr, float* ts,

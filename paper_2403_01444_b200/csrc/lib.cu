@@ -167,9 +167,10 @@ static bool g_prof = false;
 static cudaEvent_t g_ev[2 * PH_COUNT];
 static bool g_ev_ready = false, g_used[PH_COUNT];
 static const char* kPhaseNames[PH_COUNT] = {
-    "ntc_forward_transform", "project", "depth_sort", "rank_scan", "duplicate", "tile_sort",
-    "ranges", "blend_forward", "loss", "blend_backward", "gaussian_backward",
-    "ntc_backward", "adam", "transform", "transform_vjp"};
+    "gather", "decoder_forward", "transform", "project", "depth_sort", "rank_scan",
+    "duplicate", "tile_sort", "ranges", "blend_forward", "ssim_map", "ssim_grad",
+    "blend_backward", "gaussian_backward", "transform_vjp", "decoder_backward", "scatter",
+    "adam"};
 
 void prof_begin(int phase, cudaStream_t s) {
   if (!g_prof) return;

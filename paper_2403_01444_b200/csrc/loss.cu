@@ -324,18 +324,20 @@ int ss_render_loss(const float* image, const float* target, int32_t height, int3
   lp.l1w = (1.0 - lam) / ((double)height * width * channels);
   double* sums = static_cast<double*>(scratch);
   float* maps = reinterpret_cast<float*>(static_cast<char*>(scratch) + align_up(2 * sizeof(double)));
-  prof_begin(PH_LOSS, st);
   SS_CUDA(cudaMemsetAsync(sums, 0, 2 * sizeof(double), st));
   dim3 blk(SW, 3);
   dim3 g1((unsigned)cdiv(lp.Wv, SW), (unsigned)cdiv(lp.Hv, RCH));
+  prof_begin(PH_SSIM_MAP, st);
   ssim_map_kernel<<<g1, blk, 0, st>>>(lp, image, target, maps, sums);
   SS_CHECK_LAUNCH("ssim_map_kernel");
+  prof_end(PH_SSIM_MAP, st);
   dim3 g2((unsigned)cdiv(lp.W, SW), (unsigned)cdiv(lp.H, RCH));
+  prof_begin(PH_SSIM_GRAD, st);
   ssim_grad_kernel<<<g2, blk, 0, st>>>(lp, image, target, maps, d_image, sums);
   SS_CHECK_LAUNCH("ssim_grad_kernel");
+  prof_end(PH_SSIM_GRAD, st);
   loss_finalize_kernel<<<1, 1, 0, st>>>(lp, sums, loss_dev, status);
   SS_CHECK_LAUNCH("loss_finalize_kernel");
-  prof_end(PH_LOSS, st);
   return SS_OK;
 }
 

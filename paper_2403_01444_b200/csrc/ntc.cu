@@ -973,9 +973,14 @@ static int check_grid(const ss_grid* g, const ss_mlp* mlp) {
     set_error("invalid hash-grid configuration");
     return SS_ERR_DATA;
   }
-  if (mlp && g->n_levels * g->n_features != mlp->in_dim) {
-    set_error("decoder in_dim must equal n_levels * n_features");
-    return SS_ERR_DATA;
+  if (mlp) {
+    // the decoder shape decides the scratch layout: reject it before any carving
+    ss_mlp_layout L{};
+    if (ss_mlp_get_layout(mlp, &L) != SS_OK) return SS_ERR_DATA;
+    if (g->n_levels * g->n_features != mlp->in_dim) {
+      set_error("decoder in_dim must equal n_levels * n_features");
+      return SS_ERR_DATA;
+    }
   }
   return SS_OK;
 }
@@ -1062,14 +1067,16 @@ int ntc_forward_run(const ss_grid* g, const ss_mlp* mlp, int64_t n, const float*
                     float* out, int os, uint64_t* relu, uint32_t* status, cudaStream_t st) {
   SS_TRY(check_grid(g, mlp));
   if (n == 0) return SS_OK;
-  prof_begin(PH_NTC_FWD, st);
+  prof_begin(PH_GATHER, st);
   gather_kernel<<<(unsigned)cdiv(n, 256), 256, 0, st>>>(*g, n, means, rows, tables, X, xs, status);
   SS_CHECK_LAUNCH("gather_kernel");
+  prof_end(PH_GATHER, st);
+  prof_begin(PH_DECODER_FWD, st);
   if (mlp_mode() != 0)
     SS_TRY(mlp_fwd_tc(xs, mlp->n_hidden, n, X, xs, params, out, os, relu, st));  // tcgen05
   else
     SS_TRY(dispatch_mlp(mlp, MlpFwd{n, X, xs, params, out, os, st}));
-  prof_end(PH_NTC_FWD, st);
+  prof_end(PH_DECODER_FWD, st);
   return SS_OK;
 }
 
@@ -1079,14 +1086,24 @@ int ntc_backward_run(const ss_grid* g, const ss_mlp* mlp, int64_t n, const float
                      float* g_tables, float* g_params, cudaStream_t st) {
   SS_TRY(check_grid(g, mlp));
   if (n == 0) return SS_OK;
-  prof_begin(PH_NTC_BWD, st);
+  prof_begin(PH_DECODER_BWD, st);
   if (mlp_mode() != 0)
     SS_TRY(mlp_bwd_tc(xs, mlp->n_hidden, n, X, xs, g_out, gs, relu, params, dX, g_params, st));
   else
     SS_TRY(dispatch_mlp(mlp, MlpBwd{n, X, xs, g_out, gs, params, dX, g_params, st}));
+  prof_end(PH_DECODER_BWD, st);
+  // g_tables == nullptr: the caller runs the scatter later (ntc_scatter_run)
+  return g_tables ? ntc_scatter_run(g, n, means, rows, dX, xs, g_tables, st) : SS_OK;
+}
+
+int ntc_scatter_run(const ss_grid* g, int64_t n, const float* means, const int32_t* rows,
+                    const float* dX, int xs, float* g_tables, cudaStream_t st) {
+  SS_TRY(check_grid(g, nullptr));
+  if (n == 0) return SS_OK;
+  prof_begin(PH_SCATTER, st);
   scatter_kernel<<<(unsigned)cdiv(n, 256), 256, 0, st>>>(*g, n, means, rows, dX, xs, g_tables);
   SS_CHECK_LAUNCH("scatter_kernel");
-  prof_end(PH_NTC_BWD, st);
+  prof_end(PH_SCATTER, st);
   return SS_OK;
 }
 

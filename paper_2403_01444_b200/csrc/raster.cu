@@ -237,8 +237,14 @@ __global__ void __launch_bounds__(256, 3) preprocess_kernel(CamD cam, ss_cloud c
     if (i == 0) g.dev_counts[2] = cl.n;
     g.order[i] = (int32_t)i;  // sort input (4 passes: the input sits in the output buffers)
     const float* m = cl.means + 3 * i;
-    const double z = cam.R[2][0] * (double)m[0] + cam.R[2][1] * (double)m[1] +
-                     cam.R[2][2] * (double)m[2] + cam.t[2];
+    // depth key, every operation rounded (no FMA contraction) in a fixed order,
+    // ((R20 m0 + R21 m1) + R22 m2) + t2, so it is reproducible on the host; the
+    // reference's own depth is a BLAS DGEMM (cameras.py:80) whose FMA use
+    // depends on the CPU, which only matters for ties at the last ulp
+    const double z = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(cam.R[2][0], (double)m[0]),
+                                                   __dmul_rn(cam.R[2][1], (double)m[1])),
+                                         __dmul_rn(cam.R[2][2], (double)m[2])),
+                               cam.t[2]);
     uint32_t key = 0x7f800000u;  // +inf: culled (rasterizer.py:228)
     if (!(z > cam.near_clip)) {
       g.key_in[i] = __longlong_as_double(0x7ff0000000000000ll);
@@ -282,27 +288,151 @@ __device__ inline int tile_of(double v, int ts, int nt) {
 // K4b tie-break: survivors are sorted by their fp32 depth bits (stable, so
 // index order within equal keys); runs of equal fp32 keys are re-sorted by
 // (fp64 depth, index) so the order equals the stable fp64 sort
-// (rasterizer.py:228-230).  Runs are rare and short.
-__global__ void depth_tie_kernel(Geom g) {
+// (rasterizer.py:228-230).  Runs of up to kTieShort ranks (the common case) are
+// insertion-sorted by the thread at their head; a longer run (a plane facing
+// the camera puts every splat in one) is queued in shared memory and sorted by
+// the whole CTA with a stable LSD radix sort over the fp64 depth's offset from
+// the run minimum, so the cost stays linear in the run length.
+constexpr int kTieShort = 32;
+constexpr int kTieThreads = 256, kTieSteps = 4, kTieChunk = kTieThreads * kTieSteps;
+
+// stable 4 x 8-bit LSD sort of order[r, e) by (fp64 depth bits - minimum bits);
+// the run is in index order on entry, so equal depths keep index order
+__device__ void tie_sort_run_cta(const Geom& g, int64_t r, int64_t e, uint64_t minb,
+                                 uint32_t (*wh)[256], uint32_t* s_base, uint32_t* s_scan) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  uint32_t lt;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
+  int32_t* src = g.order + r;
+  int32_t* dst = g.idx_in + r;  // the depth sort's ping-pong buffer, free after it
+  const int64_t k = e - r;
+  for (int pass = 0; pass < 4; ++pass) {
+    const int sh = 8 * pass;
+    s_base[tid] = 0;
+    __syncthreads();
+    for (int64_t i = tid; i < k; i += kTieThreads) {
+      const uint64_t b = (uint64_t)__double_as_longlong(g.key_in[src[i]]) - minb;
+      atomicAdd(&s_base[(b >> sh) & 255], 1u);
+    }
+    __syncthreads();
+    {  // exclusive scan over the 256 digits (thread = digit)
+      const uint32_t h = s_base[tid];
+      uint32_t x = h;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      if (lane == 31) s_scan[warp] = x;
+      __syncthreads();
+      uint32_t w = 0;
+      for (int j = 0; j < warp; ++j) w += s_scan[j];
+      __syncthreads();
+      s_base[tid] = x - h + w;
+    }
+    for (int64_t c = 0; c < k; c += kTieChunk) {
+      for (int j = 0; j < kTieThreads / 32; ++j) wh[j][tid] = 0;
+      __syncthreads();
+      int32_t v[kTieSteps];
+      uint32_t d[kTieSteps], rk[kTieSteps];
+#pragma unroll
+      for (int s2 = 0; s2 < kTieSteps; ++s2) {  // warp w owns [w*128, w*128+128) of the chunk
+        const int64_t i = c + warp * (kTieSteps * 32) + s2 * 32 + lane;
+        v[s2] = i < k ? src[i] : 0;
+        d[s2] = i < k ? (uint32_t)((((uint64_t)__double_as_longlong(g.key_in[v[s2]]) - minb) >> sh) & 255)
+                      : 256u;
+        const uint32_t peers = __match_any_sync(0xffffffffu, d[s2]);
+        const int leader = __ffs(peers) - 1;
+        uint32_t old = 0;
+        if (i < k && lane == leader) {
+          old = wh[warp][d[s2]];
+          wh[warp][d[s2]] = old + __popc(peers);
+        }
+        rk[s2] = __shfl_sync(0xffffffffu, old, leader) + __popc(peers & lt);
+        __syncwarp();
+      }
+      __syncthreads();
+      {  // per digit: exclusive prefix over warps, chunk total into the base
+        uint32_t cnt = 0;
+#pragma unroll
+        for (int j = 0; j < kTieThreads / 32; ++j) {
+          const uint32_t t = wh[j][tid];
+          wh[j][tid] = cnt;
+          cnt += t;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int s2 = 0; s2 < kTieSteps; ++s2)
+          if (d[s2] < 256u) dst[s_base[d[s2]] + wh[warp][d[s2]] + rk[s2]] = v[s2];
+        __syncthreads();
+        s_base[tid] += cnt;
+      }
+      __syncthreads();
+    }
+    int32_t* t = src;
+    src = dst;
+    dst = t;
+  }
+}
+
+__global__ void __launch_bounds__(kTieThreads) depth_tie_kernel(Geom g) {
+  __shared__ uint32_t wh[kTieThreads / 32][256];
+  __shared__ uint32_t s_base[256], s_scan[64];
+  __shared__ int64_t s_long[kTieThreads];
+  __shared__ int s_nlong;
+  __shared__ unsigned long long s_min;
+  __shared__ long long s_end;
   const int64_t V = g.dev_counts[0];
   const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (r >= V) return;
-  const uint32_t k = g.key32[r];
-  if ((r > 0 && g.key32[r - 1] == k) || r + 1 >= V || g.key32[r + 1] != k) return;
-  int64_t e = r + 1;
-  while (e < V && g.key32[e] == k) ++e;
-  for (int64_t a = r + 1; a < e; ++a) {  // insertion sort by (fp64 depth, index)
-    const int32_t v = g.order[a];
-    const double dv = g.key_in[v];
-    int64_t b = a - 1;
-    while (b >= r) {
-      const int32_t u = g.order[b];
-      const double du = g.key_in[u];
-      if (du < dv || (du == dv && u < v)) break;
-      g.order[b + 1] = u;
-      --b;
+  if (threadIdx.x == 0) s_nlong = 0;
+  __syncthreads();
+  if (r < V) {
+    const uint32_t k = g.key32[r];
+    if (!(r > 0 && g.key32[r - 1] == k) && r + 1 < V && g.key32[r + 1] == k) {
+      int64_t e = r + 1;
+      while (e < V && e - r <= kTieShort && g.key32[e] == k) ++e;
+      if (e < V && g.key32[e] == k) {
+        s_long[atomicAdd(&s_nlong, 1)] = r;  // longer than kTieShort: the CTA sorts it
+      } else {
+        for (int64_t a = r + 1; a < e; ++a) {  // insertion sort by (fp64 depth, index)
+          const int32_t v = g.order[a];
+          const double dv = g.key_in[v];
+          int64_t b = a - 1;
+          while (b >= r) {
+            const int32_t u = g.order[b];
+            const double du = g.key_in[u];
+            if (du < dv || (du == dv && u < v)) break;
+            g.order[b + 1] = u;
+            --b;
+          }
+          g.order[b + 1] = v;
+        }
+      }
     }
-    g.order[b + 1] = v;
+  }
+  __syncthreads();
+  const int nlong = s_nlong;
+  for (int j = 0; j < nlong; ++j) {  // block-uniform
+    const int64_t h = s_long[j];
+    const uint32_t k = g.key32[h];
+    if (threadIdx.x == 0) {
+      s_end = V;
+      s_min = ~0ull;
+    }
+    __syncthreads();
+    // run end: the first mismatching rank, found a CTA-width window at a time
+    for (int64_t base = h + 1;; base += kTieThreads) {
+      const int64_t i = base + threadIdx.x;
+      if (i < V && g.key32[i] != k) atomicMin(&s_end, (long long)i);
+      __syncthreads();
+      if (s_end < base + kTieThreads || base + kTieThreads >= V) break;
+    }
+    const int64_t e = s_end;
+    for (int64_t i = h + threadIdx.x; i < e; i += kTieThreads)
+      atomicMin(&s_min, (unsigned long long)__double_as_longlong(g.key_in[g.order[i]]));
+    __syncthreads();
+    tie_sort_run_cta(g, h, e, s_min, wh, s_base, s_scan);
+    __syncthreads();
   }
 }
 
@@ -513,31 +643,9 @@ static int bin_pairs(const ss_camera* cam, const ss_raster_settings* s, int64_t 
 struct BlendParams {
   int W, H, ntx;
   float clamp, skip, stop;
-  double clamp_d, skip_d;
+  double clamp_d, skip_d, stop_d;
   float bg[3];
 };
-
-// alpha of one pixel/splat pair (rasterizer.py:187-199).  Pairs whose fp32
-// alpha lies within 1e-4 (relative) of the skip threshold are recomputed in
-// float64 from the float64 records so the include/skip decision matches the
-// float64 reference (SURVEY.md "Hard parts").
-__device__ inline float pair_alpha(const BlendParams& bp, float dx, float dy, float4 co,
-                                   int rank, float px, float py, const double2* __restrict__ mean_d,
-                                   const double4* __restrict__ conop_d, float& G, float& og) {
-  const float maha = co.x * dx * dx + co.y * dx * dy + co.z * dy * dy;
-  G = expf(-0.5f * maha);
-  og = co.w * G;
-  float a = fminf(bp.clamp, og);
-  if (fabsf(a - bp.skip) <= 1e-4f * bp.skip) {
-    const double2 m = mean_d[rank];
-    const double4 c = conop_d[rank];
-    const double ddx = (double)px - m.x, ddy = (double)py - m.y;
-    const double mh = c.x * ddx * ddx + c.y * ddx * ddy + c.z * ddy * ddy;
-    const double ad = fmin(bp.clamp_d, c.w * exp(-0.5 * mh));
-    return ad < bp.skip_d ? 0.f : fmaxf((float)ad, bp.skip);
-  }
-  return a < bp.skip ? 0.f : a;
-}
 
 __device__ __forceinline__ float ex2_approx(float x) {
   float y;
@@ -556,31 +664,28 @@ __device__ __forceinline__ float log2_gauss(float4 q, float dx, float dy) {
   return fmaf(fmaf(q.x, dx, q.y * dy), dx, q.z * dy * dy);
 }
 
-// alpha from the log2 form (caller has already rejected lg < qthr); near the
-// skip threshold it is recomputed in float64 exactly as pair_alpha does
-__device__ inline float alpha_from_log2(const BlendParams& bp, float lg, float op, int rank,
-                                        float px, float py, const double2* __restrict__ mean_d,
-                                        const double4* __restrict__ conop_d, float& G, float& og) {
-  G = ex2_approx(lg);
-  og = op * G;
-  const float a = fminf(bp.clamp, og);
-  if (fabsf(a - bp.skip) <= 1e-4f * bp.skip) {
-    const double2 m = mean_d[rank];
-    const double4 c = conop_d[rank];
-    const double ddx = (double)px - m.x, ddy = (double)py - m.y;
-    const double mh = c.x * ddx * ddx + c.y * ddx * ddy + c.z * ddy * ddy;
-    const double ad = fmin(bp.clamp_d, c.w * exp(-0.5 * mh));
-    return ad < bp.skip_d ? 0.f : fmaxf((float)ad, bp.skip);
-  }
-  return a < bp.skip ? 0.f : a;
-}
-
 // Fast-path alpha decision on the log2 form.  rank_kernel sets the reject
-// threshold q.w = log2(skip (1 - 2e-4) / op); a live pair with
-// lg >= q.w + kNearBand (= log2(skip (1 + 1e-4) / op)) has alpha above skip
-// beyond any fp32 rounding, so only pairs inside [q.w, q.w + kNearBand) need
-// the float64 decision (taken on a rare, per-thread branch).
+// threshold q.w = log2(skip (1 - 2e-4) / op); with the exact log2 form lg, a
+// pair with lg < q.w has alpha below skip and a pair with lg >= q.w + kNearBand
+// (= log2(skip (1 + 1e-4) / op)) alpha above it, beyond the ex2.approx error.
+// The fp32 evaluation of lg is off by at most splat_band() (below), so pairs
+// with lg in [q.w - band, q.w + kNearBand + band) take the float64 decision
+// (a rare, per-thread branch) and every include/skip decision equals the
+// float64 reference's (rasterizer.py:198-199).
 constexpr float kNearBand = 4.3284e-4f;  // log2(1 + 1e-4) - log2(1 - 2e-4), rounded up
+
+// Bound of |lg_fp32 - lg| over one tile for a staged splat: the quadratic form
+// with absolute coefficients at the tile's farthest pixel, |A| dx^2 + |B| |dx dy|
+// + |C| dy^2, times 16 fp32 epsilons (coefficient rounding 1, mean-offset
+// rounding <= 4 since |xy| <= the reach, 4 rounded operations, headroom).
+// Cancellation in the form (a thin splat at 45 degrees) makes this far larger
+// than |lg|, which is what a fixed band would miss.
+template <int TS>
+__device__ __forceinline__ float splat_band(float4 q, float2 xy) {
+  const float rx = fmaxf(fabsf(xy.x), fabsf((float)(TS - 1) - xy.x));
+  const float ry = fmaxf(fabsf(xy.y), fabsf((float)(TS - 1) - xy.y));
+  return 9.6e-7f * (fabsf(q.x) * rx * rx + fabsf(q.y) * rx * ry + fabsf(q.z) * ry * ry);
+}
 
 __device__ __noinline__ float alpha_f64(const BlendParams& bp, const Geom& g, int rank, float px,
                                         float py) {
@@ -598,7 +703,8 @@ struct __align__(16) SplatRec {
   float4 q;    // log2 form (A, B, C, reject threshold)
   float4 col;  // rgb, opacity
   float2 xy;   // mean relative to the tile origin
-  int rank, pad;
+  int rank;
+  float band;  // splat_band(q, xy) over this tile
 };
 
 template <int TS>
@@ -617,19 +723,26 @@ __device__ __forceinline__ int tile_pixel(int t, int p) {
   return (t >> 5) * (32 * BlendShape<TS>::PPT) + p * 32 + (t & 31);
 }
 
+// TOUCH = false: the Stage-1 path, fp32 with the float64 decision band above.
+// TOUCH = true (the public rasterize_forward, which also returns the per-
+// Gaussian touch counts, rasterizer.py:279): every pair in float64 exactly as
+// the reference evaluates it (maha, exp, alpha, T_before and the stop test), so
+// the counts of weight = alpha T_before > 0 are the reference's, including the
+// denormal weights skip_alpha = 0 admits.
 template <int TS, bool TOUCH>
 __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_fwd_kernel(
     BlendParams bp, Geom g, const uint32_t* __restrict__ vals, float* __restrict__ image,
     float* __restrict__ alpha_map, int32_t* __restrict__ touch) {
   constexpr int NT = BlendShape<TS>::NT, PPT = BlendShape<TS>::PPT;
   __shared__ SplatRec s_sp[NT];
-  __shared__ float4 s_co[TOUCH ? NT : 1];
+  __shared__ double2 s_md[TOUCH ? NT : 1];  // float64 mean (TOUCH)
+  __shared__ double4 s_cd[TOUCH ? NT : 1];  // float64 conic (c00, c01 + c10, c11) + opacity
   __shared__ int s_touch[TOUCH ? NT : 1];
   const int tile = blockIdx.x;
   const int x0 = (tile % bp.ntx) * TS, y0 = (tile / bp.ntx) * TS;
   const int2 range = g.ranges[tile];
   float T[PPT], C[PPT][3];
-  double logT[PPT];  // float64 log-transmittance, touch counting with skip_alpha = 0 only
+  double Td[TOUCH ? PPT : 1], Cd[TOUCH ? PPT : 1][3];
   int last[PPT];
   bool done[PPT];
   float lx[PPT], ly[PPT];
@@ -639,8 +752,11 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_fwd_kernel(
     lx[p] = (float)(li % TS);
     ly[p] = (float)(li / TS);
     T[p] = 1.f;
-    logT[p] = 0.0;
     C[p][0] = C[p][1] = C[p][2] = 0.f;
+    if (TOUCH) {
+      Td[p] = 1.0;
+      Cd[p][0] = Cd[p][1] = Cd[p][2] = 0.0;
+    }
     last[p] = 0;
     done[p] = (x0 + li % TS >= bp.W) || (y0 + li / TS >= bp.H);
   }
@@ -653,27 +769,33 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_fwd_kernel(
     if (j < range.y) {
       const int r = (int)vals[j];
       const double2 m = g.r_mean[r];
-      s_sp[threadIdx.x].xy = make_float2((float)(m.x - x0), (float)(m.y - y0));
-      if (TOUCH) s_co[threadIdx.x] = g.r_conop[r];  // the fast path uses the log2 form only
-      s_sp[threadIdx.x].q = g.r_q[r];
+      const float2 xy = make_float2((float)(m.x - x0), (float)(m.y - y0));
+      const float4 q = g.r_q[r];
+      s_sp[threadIdx.x].xy = xy;
+      s_sp[threadIdx.x].q = q;
+      s_sp[threadIdx.x].band = splat_band<TS>(q, xy);
       s_sp[threadIdx.x].col = g.r_color[r];
       s_sp[threadIdx.x].rank = r;
+      if (TOUCH) {
+        s_md[threadIdx.x] = m;
+        s_cd[threadIdx.x] = g.r_conop_d[r];
+      }
     }
     if (TOUCH) s_touch[threadIdx.x] = 0;
     __syncthreads();
     const int cnt = min(NT, range.y - b);
     for (int k = 0; k < cnt; ++k) {
-      const float2 xy = s_sp[k].xy;
-      int contrib = 0;
       if (!TOUCH) {  // fast path: reject on the log2 form before the exponential
+        const float2 xy = s_sp[k].xy;
         const float4 q = s_sp[k].q;
-        const float qhi = q.w + kNearBand;
+        const float band = s_sp[k].band;
+        const float qlo = q.w - band, qhi = q.w + (kNearBand + band);
         float lgs[PPT];
         bool live[PPT], any_live = false, any_near = false;
 #pragma unroll
         for (int p = 0; p < PPT; ++p) {
           lgs[p] = log2_gauss(q, lx[p] - xy.x, ly[p] - xy.y);
-          live[p] = !done[p] && !(lgs[p] < q.w);
+          live[p] = !done[p] && !(lgs[p] < qlo);
           any_live |= live[p];
           any_near |= live[p] && lgs[p] < qhi;
         }
@@ -700,49 +822,33 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_fwd_kernel(
         }
         continue;
       }
-      const float4 co = s_co[k];
+      // ---- TOUCH: float64 per pair (rasterizer.py:187-211, :279)
+      const double2 md = s_md[k];
+      const double4 cd = s_cd[k];
+      const float4 col = s_sp[k].col;
+      int contrib = 0;
 #pragma unroll
       for (int p = 0; p < PPT; ++p) {
         if (done[p]) continue;
-        const float dx = lx[p] - xy.x, dy = ly[p] - xy.y;
-        float G, og;
-        const float a = pair_alpha(bp, dx, dy, co, s_sp[k].rank, lx[p] + x0, ly[p] + y0, g.r_mean,
-                                   g.r_conop_d, G, og);
-        // Touch counts (rasterizer.py:279) count weight = alpha T_before > 0 in
-        // float64.  With skip_alpha = 0 that includes alphas and transmittances far
-        // below the float32 range (glibc keeps denormals down to 2^-1075), so that
-        // mode tracks log(alpha) + log(T) in float64; the colour is unaffected.
-        const bool exact_touch = TOUCH && bp.skip_d == 0.0;
-        const double lim = -745.1332191019412;  // ln(2^-1075)
-        if (a == 0.f) {
-          if (exact_touch) {
-            const double mh = (double)co.x * dx * dx + (double)co.y * dx * dy + (double)co.z * dy * dy;
-            const double la = -0.5 * mh + log((double)co.w);
-            if (-0.5 * mh > lim && la > lim && la + logT[p] > lim) ++contrib;
-          }
-          continue;
-        }
-        if (exact_touch) {
-          if (log((double)a) + logT[p] > lim) ++contrib;
-          logT[p] += log1p(-(double)a);
-        }
-        const float4 col = s_sp[k].col;
-        const float w = a * T[p];
-        C[p][0] = fmaf(w, col.x, C[p][0]);
-        C[p][1] = fmaf(w, col.y, C[p][1]);
-        C[p][2] = fmaf(w, col.z, C[p][2]);
-        T[p] *= 1.f - a;
+        const double ddx = (double)(lx[p] + x0) - md.x, ddy = (double)(ly[p] + y0) - md.y;
+        const double mh = cd.x * ddx * ddx + cd.y * ddx * ddy + cd.z * ddy * ddy;
+        double a = fmin(bp.clamp_d, cd.w * exp(-0.5 * mh));
+        if (a < bp.skip_d) a = 0.0;
+        const double w = a * Td[p];
+        if (w > 0.0) ++contrib;
+        if (a == 0.0) continue;
+        Cd[p][0] += w * (double)col.x;
+        Cd[p][1] += w * (double)col.y;
+        Cd[p][2] += w * (double)col.z;
+        Td[p] *= 1.0 - a;
         last[p] = b - range.x + k + 1;
-        if (!exact_touch) ++contrib;
-        if (T[p] < bp.stop) done[p] = true;  // later splats fail T_before >= stop
+        if (Td[p] < bp.stop_d) done[p] = true;  // later splats fail T_before >= stop
       }
-      if (TOUCH) {
-        const unsigned bal = __ballot_sync(0xffffffffu, contrib > 0);
-        int tot = contrib;
+      const unsigned bal = __ballot_sync(0xffffffffu, contrib > 0);
+      int tot = contrib;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
-        if (bal && (threadIdx.x & 31) == 0) atomicAdd(&s_touch[k], tot);
-      }
+      for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+      if (bal && (threadIdx.x & 31) == 0) atomicAdd(&s_touch[k], tot);
     }
     if (TOUCH) {
       __syncthreads();
@@ -756,10 +862,21 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_fwd_kernel(
     const int px = x0 + li % TS, py = y0 + li / TS;
     if (px >= bp.W || py >= bp.H) continue;
     const int64_t pix = (int64_t)py * bp.W + px;
-    image[3 * pix + 0] = C[p][0] + T[p] * bp.bg[0];
-    image[3 * pix + 1] = C[p][1] + T[p] * bp.bg[1];
-    image[3 * pix + 2] = C[p][2] + T[p] * bp.bg[2];
-    if (alpha_map) alpha_map[pix] = 1.f - T[p];
+    if (TOUCH) {
+      T[p] = (float)Td[p];
+      C[p][0] = (float)(Cd[p][0] + Td[p] * (double)bp.bg[0]);
+      C[p][1] = (float)(Cd[p][1] + Td[p] * (double)bp.bg[1]);
+      C[p][2] = (float)(Cd[p][2] + Td[p] * (double)bp.bg[2]);
+      image[3 * pix + 0] = C[p][0];
+      image[3 * pix + 1] = C[p][1];
+      image[3 * pix + 2] = C[p][2];
+      if (alpha_map) alpha_map[pix] = (float)(1.0 - Td[p]);
+    } else {
+      image[3 * pix + 0] = C[p][0] + T[p] * bp.bg[0];
+      image[3 * pix + 1] = C[p][1] + T[p] * bp.bg[1];
+      image[3 * pix + 2] = C[p][2] + T[p] * bp.bg[2];
+      if (alpha_map) alpha_map[pix] = 1.f - T[p];
+    }
     g.t_final[pix] = T[p];
     g.n_contrib[pix] = last[p];
   }
@@ -831,8 +948,11 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_bwd_kernel(
       const int pos = end - 1 - threadIdx.x;
       const int r = (int)vals[pos];
       const double2 m = g.r_mean[r];
-      s_sp[threadIdx.x].xy = make_float2((float)(m.x - x0), (float)(m.y - y0));
-      s_sp[threadIdx.x].q = g.r_q[r];
+      const float2 xy = make_float2((float)(m.x - x0), (float)(m.y - y0));
+      const float4 q = g.r_q[r];
+      s_sp[threadIdx.x].xy = xy;
+      s_sp[threadIdx.x].q = q;
+      s_sp[threadIdx.x].band = splat_band<TS>(q, xy);
       s_sp[threadIdx.x].col = g.r_color[r];
       s_sp[threadIdx.x].rank = r;
     }
@@ -841,7 +961,8 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_bwd_kernel(
       const int pos_rel = end - 1 - k - range.x;
       const float2 xy = s_sp[k].xy;
       const float4 q = s_sp[k].q;
-      const float qhi = q.w + kNearBand;
+      const float band = s_sp[k].band;
+      const float qlo = q.w - band, qhi = q.w + (kNearBand + band);
       // cheap part for every pixel, then a warp-uniform skip; the rest is
       // predicated (a = 0 makes every update a no-op) instead of branching
       float dxs[PPT], dys[PPT], lgs[PPT];
@@ -851,7 +972,7 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_bwd_kernel(
         dxs[p] = lx[p] - xy.x;
         dys[p] = ly[p] - xy.y;
         lgs[p] = log2_gauss(q, dxs[p], dys[p]);  // same decisions as the forward
-        live[p] = pos_rel < last[p] && !(lgs[p] < q.w);
+        live[p] = pos_rel < last[p] && !(lgs[p] < qlo);
         any_live |= live[p];
         any_near |= live[p] && lgs[p] < qhi;
       }
@@ -1147,6 +1268,7 @@ static BlendParams blend_params(const ss_camera* cam, const ss_raster_settings* 
   bp.stop = (float)s->stop_transmittance;
   bp.clamp_d = s->alpha_clamp;
   bp.skip_d = s->skip_alpha;
+  bp.stop_d = s->stop_transmittance;
   for (int i = 0; i < 3; ++i) bp.bg[i] = (float)s->background[i];
   return bp;
 }
@@ -1280,9 +1402,9 @@ int raster_backward(const ss_cloud* cl, const ss_camera* cam, const ss_raster_se
   Geom g = plan_geom(geom, n, cam, s);
   Bins b = plan_bins(bins, pairs);
   const int64_t ntiles = (int64_t)ntiles_x(cam, s) * ntiles_y(cam, s);
-  prof_begin(PH_BLEND_BWD, st);
   SS_CUDA(cudaMemsetAsync(g.acc, 0, n * kAccStride * sizeof(float), st));
   SS_CUDA(cudaMemsetAsync(g.touched, 0, n, st));
+  prof_begin(PH_BLEND_BWD, st);
   const BlendParams bp = blend_params(cam, s);
   if (full) SS_TRY(launch_blend_bwd<true>(s->tile_size, ntiles, st, bp, g, b.vals_out, d_image));
   else SS_TRY(launch_blend_bwd<false>(s->tile_size, ntiles, st, bp, g, b.vals_out, d_image));

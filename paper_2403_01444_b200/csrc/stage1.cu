@@ -14,23 +14,30 @@ static ss_cloud transformed(const ss_stage1* st) {
   return c;
 }
 
+// ViewspaceStats.add (adaptive.py:92-94).  The view's image gradient was scaled
+// by grad_scale (1/B in a batch); the statistic is of the per-view gradient, so
+// the norm is scaled back by inv_scale = 1/grad_scale.
 __global__ void stats_kernel(int64_t n, const float* __restrict__ vs,
                              const uint8_t* __restrict__ contrib, float* __restrict__ norm,
-                             int32_t* __restrict__ count) {
+                             int32_t* __restrict__ count, float inv_scale) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
-  norm[i] += vs[i];  // ViewspaceStats.add (adaptive.py:92-94)
+  norm[i] += vs[i] * inv_scale;
   count[i] += contrib[i];
 }
 
 // loss / pair-count histories at the device-side iteration index
+// (+ the batch-loss sum of view-sharded training)
 __global__ void history_kernel(const double* __restrict__ loss, const int64_t* __restrict__ pairs,
                                double* loss_hist, int64_t* pair_hist, int64_t len,
-                               int32_t* __restrict__ iter_dev) {
-  const int64_t slot = len > 0 ? *iter_dev % len : 0;
-  if (loss_hist) loss_hist[slot] = *loss;
-  if (pair_hist) pair_hist[slot] = *pairs;
-  *iter_dev += 1;
+                               int32_t* __restrict__ iter_dev, float* loss_accum) {
+  if (iter_dev) {
+    const int64_t slot = len > 0 ? *iter_dev % len : 0;
+    if (loss_hist) loss_hist[slot] = *loss;
+    if (pair_hist) pair_hist[slot] = *pairs;
+    *iter_dev += 1;
+  }
+  if (loss_accum) *loss_accum += (float)*loss;
 }
 
 __global__ void scale_kernel(int64_t n, float* __restrict__ v, float s) {
@@ -112,13 +119,18 @@ int ss_stage1_iter_grads(ss_stage1* st, const ss_camera* cam, const float* targe
   SS_TRY(raster_finish(&tc, cam, &st->settings, st->geom, st->bins, cap, st->image,
                        st->alpha_map, nullptr, st->status, 1, s));
   SS_TRY(ss_render_loss(st->image, target, cam->height, cam->width, 3, st->lambda_dssim,
-                        0.01 * 0.01, 0.03 * 0.03, st->loss_scratch, st->loss_dev, st->d_image,
+                        st->ssim_c1, st->ssim_c2, st->loss_scratch, st->loss_dev, st->d_image,
                         st->status, stream));
-  if (st->iter_dev && st->history_len > 0) {
+  const bool hist = st->iter_dev && st->history_len > 0;
+  if (hist || st->loss_accum) {
     history_kernel<<<1, 1, 0, s>>>(st->loss_dev, raster_counts(st->geom, tc.n, cam, &st->settings) + 1,
                                    st->loss_history, st->pair_history, st->history_len,
-                                   st->iter_dev);
+                                   hist ? st->iter_dev : nullptr, st->loss_accum);
     SS_CHECK_LAUNCH("history_kernel");
+  }
+  if (!(grad_scale > 0.0f)) {
+    set_error("grad_scale must be positive");
+    return SS_ERR_DATA;
   }
   if (grad_scale != 1.0f) {
     const int64_t m = (int64_t)cam->width * cam->height * 3;
@@ -136,7 +148,8 @@ int ss_stage1_iter_grads(ss_stage1* st, const ss_camera* cam, const float* targe
   if (st->accumulate_stats && st->stats_norm && st->stats_count) {
     const int64_t n = st->src.n;
     stats_kernel<<<(unsigned)cdiv(n, 256), 256, 0, s>>>(n, st->viewspace, st->contributed,
-                                                         st->stats_norm, st->stats_count);
+                                                         st->stats_norm, st->stats_count,
+                                                         1.0f / grad_scale);
     SS_CHECK_LAUNCH("stats_kernel");
   }
   const NtcScratch ns = scratch_of(st);
@@ -145,9 +158,16 @@ int ss_stage1_iter_grads(ss_stage1* st, const ss_camera* cam, const float* targe
                            perm ? st->rows_pos : nullptr, ns.out7, 8, st->rotate_sh, st->d_means,
                            st->d_rotations, st->d_sh, ns.g7, 8, s, st->contributed));
   SS_TRY(ntc_backward_run(&st->grid, &st->mlp, st->n_in, st->src.means, st->rows, st->params,
-                          ns.X, ns.xs, ns.g7, 8, ns.relu, ns.dX, st->g_tables, st->g_params, s));
+                          ns.X, ns.xs, ns.g7, 8, ns.relu, ns.dX,
+                          st->defer_scatter ? nullptr : st->g_tables, st->g_params, s));
   st->iteration += 1;
   return SS_OK;
+}
+
+int ss_stage1_table_scatter(ss_stage1* st, void* stream) {
+  const NtcScratch ns = scratch_of(st);
+  return ntc_scatter_run(&st->grid, st->n_in, st->src.means, st->rows, ns.dX, ns.xs,
+                         st->g_tables, as_stream(stream));
 }
 
 int ss_stage1_apply_adam(ss_stage1* st, void* stream) {

@@ -1,19 +1,41 @@
 """View-sharded data-parallel Stage-1 (BASELINE configs 3-4).
 
 Gaussians and NTC parameters are replicated; the B views of an iteration are
-split across the W ranks (one process per GPU).  Each rank runs the whole
-Stage-1 chain on its views with the image gradient scaled by 1/B, so the sum
-all-reduce of the packed NTC gradient [tables | MLP] over NCCL yields the
-gradient of the mean batch loss.  Every rank then applies the identical lazy
-Adam step, which keeps the replicas bit-identical with no parameter broadcast.
-The only collective is that one all-reduce per iteration.
+split contiguously across the W ranks (one process per GPU).  Each rank runs
+the whole Stage-1 chain on its views with the image gradient scaled by 1/B, so
+the sum all-reduce of the packed NTC gradient [tables | MLP | loss] yields the
+gradient of the mean batch loss, and the batch-loss sum rides in the same
+buffer.  Every rank then applies the identical lazy Adam step, which keeps the
+replicas bit-identical with no parameter broadcast.
 
-Batch semantics (no reference equivalent, D6): loss = mean over views; the
-oracle is the mean of per-view reference gradients followed by one Adam step.
+Per iteration the exchange is split in two so it overlaps the last kernel of
+the backward: the decoder gradient (plus the loss slot) is all-reduced while
+the hash-table scatter (ntc.py:278-288) still runs, then the table gradient.
+View-space statistics (adaptive.py:79-97) are accumulated per view over the
+last epoch's views and all-reduced once, at the end of the frame.
+
+Batch semantics (no reference equivalent, D6): loss = mean over the views of
+an iteration; the oracle is the mean of per-view reference gradients
+(transform.py:99-135 -> ntc.py:250-288) followed by one Adam step
+(optim.py:33-66).  The view sequence is the reference's per-epoch permutation
+(pipeline.py:251-256, :263) read B views at a time.
+
+The trainer is duck-typed (a `stage1.Stage1Trainer` on the GPU; the CPU tests
+drive the same code with an oracle-backed stand-in):
+  g_flat            packed fp32 gradient [tables | MLP | loss slot]
+  n_table           length of the tables part
+  n_views           number of training views
+  iterate(view, grad_scale=, adam=False, defer_scatter=, accumulate_stats=, staged=)
+  stage_target(view, host_tensor)   H2D copy of a view's target into the staging buffer
+  table_scatter()   the deferred hash-table scatter of the last iterate
+  apply_adam()      lazy Adam on g_flat (zeroes the table/MLP gradient)
+  stats_norm, stats_count   per-Gaussian view-space statistics
+  enable_loss_accum()       every iterate adds its loss to the loss slot
 """
 
 from __future__ import annotations
 
+import numpy as np
 import torch
 import torch.distributed as dist
 
@@ -33,43 +55,96 @@ def allreduce_sum_(flat: torch.Tensor, world: int, group=None) -> torch.Tensor:
     return flat
 
 
+def batched_view_order(seed: int, frame_index: int, n_views: int, iterations: int,
+                       views_per_iteration: int) -> list[list[int]]:
+    """The reference view sequence (pipeline.py:251-256, :263, :278-279) read B
+    views per iteration: iteration t trains positions [tB, tB + B)."""
+    from .stage1 import view_order
+
+    b = views_per_iteration
+    seq = view_order(seed, frame_index, n_views, iterations * b)
+    return [seq[t * b:(t + 1) * b] for t in range(iterations)]
+
+
 class ViewShardedStage1:
-    def __init__(self, prev_cloud, cache, views, cfg=None, rank: int = 0, world: int = 1,
-                 group=None, views_per_iteration: int | None = None):
-        from .stage1 import Stage1Trainer
-
+    def __init__(self, prev_cloud=None, cache=None, views=None, cfg=None, rank: int = 0,
+                 world: int = 1, group=None, views_per_iteration: int | None = None,
+                 trainer=None):
         self.rank, self.world, self.group = rank, world, group
-        self.trainer = Stage1Trainer(prev_cloud, cache, views, cfg)
-        self.views_per_iteration = views_per_iteration
+        if trainer is None:
+            from .stage1 import Stage1Trainer
 
-    def _grads_for(self, views: list[int], total: int) -> None:
-        tr = self.trainer
-        for v in views:
-            tr.iterate(v, grad_scale=1.0 / total, adam=False)
+            trainer = Stage1Trainer(prev_cloud, cache, views, cfg)
+        self.trainer = trainer
+        self.views_per_iteration = views_per_iteration or world
+        self.cfg = getattr(trainer, "cfg", cfg)
+        trainer.enable_loss_accum()
+        self.loss_slot = trainer.g_flat[trainer.n_table + trainer.n_params:][:1]
+        self._losses: list[torch.Tensor] = []
 
-    def step(self, batch: list[int]) -> None:
+    # ------------------------------------------------------------------
+    def step(self, batch: list[int], accumulate_stats=False, host_targets=None) -> None:
         """One iteration over `batch` (global view ids), stream-ordered with no
-        host synchronisation (the all-reduce is an NCCL kernel on the stream)."""
+        host synchronisation.  `accumulate_stats`: one flag for the batch or
+        one per view (the last-epoch window of pipeline.py:259, :276-277).
+        `host_targets` (pinned host tensors by view id): each of this rank's
+        targets is copied host -> device just before its view's iteration."""
         tr = self.trainer
-        if self.world == 1 and len(batch) == 1:
-            tr.iterate(batch[0])
-            return
+        b = len(batch)
+        flags = (list(accumulate_stats) if isinstance(accumulate_stats, (list, tuple))
+                 else [bool(accumulate_stats)] * b)
+        lo = (b * self.rank) // self.world
         mine = shard_views(batch, self.rank, self.world)
-        self._grads_for(mine, len(batch))
-        allreduce_sum_(tr.g_flat, self.world, self.group)
+        last = len(mine) - 1
+        split = self.world > 1
+        for j, v in enumerate(mine):
+            if host_targets is not None:
+                tr.stage_target(v, host_targets[v])
+            tr.iterate(v, grad_scale=1.0 / b, adam=False, defer_scatter=split and j == last,
+                       accumulate_stats=flags[lo + j], staged=host_targets is not None)
+        if split:  # (a rank without views contributes zeros: the collectives stay matched)
+            nt = tr.n_table
+            w1 = dist.all_reduce(tr.g_flat[nt:], op=dist.ReduceOp.SUM, group=self.group,
+                                 async_op=True)  # decoder grads + loss, under the scatter
+            if last >= 0:
+                tr.table_scatter()
+            w2 = dist.all_reduce(tr.g_flat[:nt], op=dist.ReduceOp.SUM, group=self.group,
+                                 async_op=True)
+            w1.wait()
+            w2.wait()
+        self._losses.append(self.loss_slot.clone())
+        self.loss_slot.zero_()
         tr.apply_adam()
 
-    def step_from_host(self, batch: list[int], host_targets) -> float:
-        """End-to-end iteration through host buffers (pinned target H2D, loss D2H)."""
-        tr = self.trainer
-        mine = shard_views(batch, self.rank, self.world)
-        if self.world == 1 and len(batch) == 1:
-            return tr.step_from_host(mine[0], host_targets[mine[0]])
-        loss = 0.0
-        for v in mine:
-            tr.stage_target(v, host_targets[v])
-            tr.iterate(v, grad_scale=1.0 / len(batch), adam=False, staged=True)
-            loss += tr.last_loss()
-        allreduce_sum_(tr.g_flat, self.world, self.group)
-        tr.apply_adam()
-        return loss
+    def step_from_host(self, batch: list[int], host_targets, accumulate_stats=False) -> float:
+        """End-to-end iteration through host buffers: each view's target is
+        copied from pinned host memory, the iteration runs, and the batch loss
+        is read back (device -> host)."""
+        self.step(batch, accumulate_stats, host_targets)
+        return float(self._losses[-1].item()) / len(batch)
+
+    def run(self, iterations: int | None = None, frame_index: int = 1) -> np.ndarray:
+        """The batched Stage-1 loop: reference view sequence B views at a time,
+        statistics over the last epoch's views, then the statistics all-reduce.
+        Returns the batch loss per iteration (mean over the batch's views)."""
+        it = iterations if iterations is not None else self.cfg.stage1_iterations
+        b = self.views_per_iteration
+        n_views = self.trainer.n_views
+        seed = getattr(self.cfg, "seed", 0)
+        stats_from = it * b - n_views
+        self._losses = []
+        for t, batch in enumerate(batched_view_order(seed, frame_index, n_views, it, b)):
+            self.step(batch, [t * b + j >= stats_from for j in range(b)])
+        self.reduce_stats()
+        return torch.cat(self._losses).double().cpu().numpy() / b
+
+    def reduce_stats(self) -> None:
+        """Sum the per-rank view-space statistics (once per frame)."""
+        if self.world > 1:
+            tr = self.trainer
+            dist.all_reduce(tr.stats_norm, op=dist.ReduceOp.SUM, group=self.group)
+            dist.all_reduce(tr.stats_count, op=dist.ReduceOp.SUM, group=self.group)
+
+    def batch_losses(self) -> np.ndarray:
+        b = self.views_per_iteration
+        return torch.cat(self._losses).double().cpu().numpy() / b if self._losses else np.zeros(0)

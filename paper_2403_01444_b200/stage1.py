@@ -104,6 +104,7 @@ class Stage1Trainer:
             raise DataError("no training views")
         # ---- views: cameras on the host, targets resident in HBM
         self.cameras = [Camera.from_any(c) for c, _ in views]
+        self.n_views = len(self.cameras)
         self.cam_structs = [camera_struct(c) for c in self.cameras]
         self.targets = [to_dev(t, dev=dev) for _, t in views]
         self.settings = settings_struct(self.cfg.raster, background)
@@ -119,9 +120,11 @@ class Stage1Trainer:
         f32, f64 = dict(dtype=torch.float32, device=dev), dict(dtype=torch.float64, device=dev)
         # one packed gradient buffer [tables | MLP] so data parallelism needs a
         # single all-reduce (nt is a multiple of 4: the MLP part stays 16B-aligned)
-        self.g_flat = torch.zeros(nt + npar, **f32)
+        # (+ 4 floats: the batch-loss slot of view-sharded training, reduced with it)
+        self.g_flat = torch.zeros(nt + npar + 4, **f32)
         self.g_tables = self.g_flat[:nt]
-        self.g_params = self.g_flat[nt:]
+        self.g_params = self.g_flat[nt:nt + npar]
+        self.n_table, self.n_params = nt, npar
         self.m_tables = torch.zeros(nt, **f64)
         self.v_tables = torch.zeros(nt, **f64)
         self.m_params = torch.zeros(npar, **f64)
@@ -172,7 +175,11 @@ class Stage1Trainer:
         s.mlp = self.mlp
         s.settings = self.settings
         s.lr, s.beta1, s.beta2, s.eps = self.cfg.ntc_lr, 0.9, 0.999, 1e-15  # optim.py:22-24
-        s.lambda_dssim = self.cfg.loss.lambda_dssim
+        loss = self.cfg.loss  # may be the reference's LossConfig: re-validated here
+        loss = LossConfig(lambda_dssim=loss.lambda_dssim, ssim_window=loss.ssim_window,
+                          ssim_sigma=loss.ssim_sigma, ssim_c1=loss.ssim_c1, ssim_c2=loss.ssim_c2)
+        s.lambda_dssim = loss.lambda_dssim
+        s.ssim_c1, s.ssim_c2 = loss.ssim_c1, loss.ssim_c2
         s.rotate_sh = int(self.cfg.rotate_sh)
         s.accumulate_stats = int(accumulate_stats)
         s.src = self.cloud.struct()
@@ -269,6 +276,15 @@ class Stage1Trainer:
     def apply_adam(self):
         self._call(self.lib.ss_stage1_apply_adam, C.byref(self.s), stream())
 
+    def table_scatter(self):
+        """The hash-table scatter deferred by iterate(..., defer_scatter=True)."""
+        self._call(self.lib.ss_stage1_table_scatter, C.byref(self.s), stream())
+
+    def enable_loss_accum(self):
+        """Every iteration adds its loss to g_flat's loss slot (batch-loss sum)."""
+        self.s.loss_accum = ptr(self.g_flat[self.n_table + self.n_params:])
+        self._graphs = {}
+
     def render_async(self, view: int) -> None:
         """Forward only with no host synchronisation (ss_stage1_render), one
         CUDA-graph replay per call when graphs are on."""
@@ -316,7 +332,8 @@ class Stage1Trainer:
 
     def iterate(self, view: int, grad_scale: float = 1.0, adam: bool = True,
                 staged: bool = False, target: torch.Tensor | None = None,
-                graph: bool | None = None) -> None:
+                graph: bool | None = None, defer_scatter: bool = False,
+                accumulate_stats: bool | None = None) -> None:
         """One Stage-1 iteration with no host synchronisation (ss_stage1_iter):
         the pair count stays on the device, bounded by the planned capacity.
         `target` overrides the view's resident target (a device buffer).
@@ -328,13 +345,16 @@ class Stage1Trainer:
         device, so replays are exact."""
         if self.bins is None:
             self.plan_capacity()
+        if accumulate_stats is not None:
+            self.s.accumulate_stats = int(accumulate_stats)
+        self.s.defer_scatter = int(defer_scatter)
         use = self.use_graphs if graph is None else graph
         if not use:
             self._iterate_eager(view, grad_scale, adam, staged, target)
             return
         buf = target if target is not None else (self._staging if staged else None)
         key = (view, None if buf is None else buf.data_ptr(), int(self.s.accumulate_stats),
-               bool(adam), float(grad_scale))
+               bool(adam), float(grad_scale), bool(defer_scatter))
         self._replay(key, lambda: self._iterate_eager(view, grad_scale, adam, staged, target))
 
     def _replay(self, key, launch) -> None:

@@ -19,15 +19,11 @@ import struct
 
 import numpy as np
 
-from .errors import DataError
+from .errors import FormatError
 from .ntc import NeuralTransformationCache
 from .types import HashGridConfig
 
 NTC_HEADER = struct.Struct("<IIIId6dIII")
-
-
-class FormatError(DataError):
-    """Malformed blob (the reference's FormatError, errors.py)."""
 
 
 def _header(grid: HashGridConfig, hidden_layers: int, hidden_dim: int, n_out: int) -> bytes:
@@ -75,22 +71,16 @@ def deserialize_ntc(data: bytes) -> NeuralTransformationCache:
     cache = NeuralTransformationCache(grid, hidden_layers=hidden_layers, hidden_dim=hidden_dim)
     if cache.weights[-1].shape[1] != n_out:
         raise FormatError(f"cache output width {n_out} unsupported")
-    off = NTC_HEADER.size
-
-    def take(shape):
-        nonlocal off
-        n = int(np.prod(shape))
-        if off + 4 * n > len(data):
-            raise FormatError("truncated cache payload")
-        a = np.frombuffer(data, dtype="<f4", count=n, offset=off)
-        off += 4 * n
-        return a.astype(np.float64).reshape(shape)
-
-    cache.tables[:] = take(cache.tables.shape)
-    for w, b in zip(cache.weights, cache.biases):
-        w[:] = take(w.shape)
-        b[:] = take(b.shape)
-    if off != len(data):
-        raise FormatError(f"cache payload has {len(data) - off} trailing bytes")
+    # every parameter array in wire order, as float32 runs after the header
+    dests = [cache.tables] + [a for wb in zip(cache.weights, cache.biases) for a in wb]
+    sizes = np.array([a.size for a in dests], dtype=np.int64)
+    need = NTC_HEADER.size + 4 * int(sizes.sum())
+    if len(data) < need:
+        raise FormatError("truncated cache payload")
+    if len(data) > need:
+        raise FormatError(f"cache payload has {len(data) - need} trailing bytes")
+    flat = np.frombuffer(data, dtype="<f4", offset=NTC_HEADER.size).astype(np.float64)
+    for a, lo, hi in zip(dests, np.cumsum(sizes) - sizes, np.cumsum(sizes)):
+        a[...] = flat[lo:hi].reshape(a.shape)
     cache.reset_adam()
     return cache
