@@ -12,7 +12,7 @@ the result against `stage1.stage1_iteration`.
 Partition (pipeline.py:263-277):
   NTC forward + transform      inside rows       ntc.py:205-248, transform.py:53-96
   projection                   Gaussian rows     rasterizer.py:227-240 (+ global lexsort)
-  blend forward / backward     bands of tile rows rasterizer.py:107-211, :264-349
+  blend forward / backward     tile rows (interleaved) rasterizer.py:107-211, :264-349
   loss                         colour channels   losses.py:84-148
   per-Gaussian backward        survivor chunks   rasterizer.py:351-402
   transform/MLP bwd + scatter  inside rows       transform.py:99-135, ntc.py:250-288
@@ -186,7 +186,11 @@ class ParallelStage1:
         rect, vis = O.tile_rects(pj["mean2d"], pj["cov2d"], pj["opacity"], wd, h, ts,
                                  s["skip_alpha"])
         ntx, nty = (wd + ts - 1) // ts, (h + ts - 1) // ts
-        bands = _chunks(nty, min(P, nty))
+        # tile rows interleaved over the workers (the centre rows carry most pairs)
+        bands = [[(r, r + 1) for r in range(wk, nty, P)] for wk in range(min(P, nty))]
+
+        def band_tiles(wid):
+            return [t for band in bands[wid] for t in _band_tiles(rect, vis, *band, ntx, ts, wd, h)]
         # ---- blend forward (bands of tile rows)
         image = shared((h, wd, 3))
         alpha_map = shared((h, wd))
@@ -194,7 +198,7 @@ class ParallelStage1:
         def blend(wid):
             if wid >= len(bands):
                 return
-            for tile in _band_tiles(rect, vis, *bands[wid], ntx, ts, wd, h):
+            for tile in band_tiles(wid):
                 y0, y1, x0, x1, mem = tile
                 _, _, _, _, al, tb, alive, tf = O._tile_pairs(pj, tile, s)
                 wgt = al * tb * alive
@@ -227,7 +231,7 @@ class ParallelStage1:
             if wid >= len(bands):
                 return
             ac = acc[wid]
-            for tile in _band_tiles(rect, vis, *bands[wid], ntx, ts, wd, h):
+            for tile in band_tiles(wid):
                 y0, y1, x0, x1, mem = tile
                 dx, dy, g, og, al, tb, alive, tf = O._tile_pairs(pj, tile, s)
                 gp = d_img[y0:y1, x0:x1].reshape(-1, 3)

@@ -31,7 +31,7 @@ struct Geom {
   int4* r_rect;     // per rank (tx0, tx1, ty0, ty1)
   double4* r_cull;  // per rank: 2 ln(opacity / skip_alpha) (tile-cull threshold), -c01/c11, -c01/c00
   int64_t* offsets;  // per rank, exclusive prefix of tile counts (n+1)
-  float* acc;        // per rank x kAccStride: colour 3, mean2d 2, conic 00/01/11, opacity
+  float* acc;        // per rank x kAccStride: colour 3, M0 | M1 2, M2 3 (anchor moments, K5a)
   uint8_t* touched;  // per rank
   float* t_final;    // per pixel
   int32_t* n_contrib;
@@ -659,33 +659,65 @@ __device__ __forceinline__ float rcp_approx(float x) {
   return y;
 }
 
-// log2 of the Gaussian at (dx, dy) from the per-rank form
-__device__ __forceinline__ float log2_gauss(float4 q, float dx, float dy) {
-  return fmaf(fmaf(q.x, dx, q.y * dy), dx, q.z * dy * dy);
-}
-
-// Fast-path alpha decision on the log2 form.  rank_kernel sets the reject
-// threshold q.w = log2(skip (1 - 2e-4) / op); with the exact log2 form lg, a
-// pair with lg < q.w has alpha below skip and a pair with lg >= q.w + kNearBand
-// (= log2(skip (1 + 1e-4) / op)) alpha above it, beyond the ex2.approx error.
-// The fp32 evaluation of lg is off by at most splat_band() (below), so pairs
-// with lg in [q.w - band, q.w + kNearBand + band) take the float64 decision
-// (a rare, per-thread branch) and every include/skip decision equals the
-// float64 reference's (rasterizer.py:198-199).
+// ---- the tile-centred log2 form
+// For a splat staged in a tile, with D = (tile centre) - mean (float64) and a
+// pixel at offset d from the tile centre, the log2 Gaussian is exactly
+//   lg(d) = lg0 + gx dx + gy dy + A dx^2 + B dx dy + C dy^2,
+// lg0 = k D^T Q D, (gx, gy) = 2 k Q D, (A, B, C) = k (c00, c01 + c10, c11),
+// k = -0.5 log2(e): the large mean offset lives in lg0 and g, evaluated in
+// float64 once per (splat, tile) at staging, so the per-pixel fp32 evaluation
+// (five FMAs on per-thread constants d, d^2) carries no cancellation even for
+// splats whose mean lies 1e5 pixels away (a Gaussian at the near plane).
+//
+// Alpha decisions: rank_kernel sets the reject threshold
+// thr = log2(skip (1 - 2e-4) / op); with the exact lg, a pair with lg < thr has
+// alpha below skip and a pair with lg >= thr + kNearBand (= log2(skip (1 + 1e-4)
+// / op)) alpha above it, beyond the ex2.approx error.  The fp32 lg is off by at
+// most `band` (below), so pairs with lg in [thr - band, thr + kNearBand + band)
+// take the float64 decision (a rare, per-thread branch) and every include /
+// skip decision equals the float64 reference's (rasterizer.py:198-199).
 constexpr float kNearBand = 4.3284e-4f;  // log2(1 + 1e-4) - log2(1 - 2e-4), rounded up
 
-// Bound of |lg_fp32 - lg| over one tile for a staged splat: the quadratic form
-// with absolute coefficients at the tile's farthest pixel, |A| dx^2 + |B| |dx dy|
-// + |C| dy^2, times 16 fp32 epsilons (coefficient rounding 1, mean-offset
-// rounding <= 4 since |xy| <= the reach, 4 rounded operations, headroom).
-// Cancellation in the form (a thin splat at 45 degrees) makes this far larger
-// than |lg|, which is what a fixed band would miss.
+// One staged splat of a blend batch: everything the inner loop reads (64 B:
+// three vector loads per splat, the rank only on rare paths)
+struct __align__(16) SplatRec {
+  float4 L;    // lg0, gx, gy, reject threshold
+  float4 Q;    // A, B, C, band: bound of |lg_fp32 - lg| over the tile
+  float4 col;  // rgb, opacity
+  int rank, pad0, pad1, pad2;
+};
+
 template <int TS>
-__device__ __forceinline__ float splat_band(float4 q, float2 xy) {
-  const float rx = fmaxf(fabsf(xy.x), fabsf((float)(TS - 1) - xy.x));
-  const float ry = fmaxf(fabsf(xy.y), fabsf((float)(TS - 1) - xy.y));
-  return 9.6e-7f * (fabsf(q.x) * rx * rx + fabsf(q.y) * rx * ry + fabsf(q.z) * ry * ry);
+__device__ __forceinline__ void stage_splat(const Geom& g, int r, int x0, int y0, SplatRec& rec) {
+  constexpr double c0 = 0.5 * (TS - 1);
+  constexpr double kq = -0.72134752044448170368;  // -0.5 log2(e)
+  const double2 m = g.r_mean[r];
+  const double4 c = g.r_conop_d[r];  // c00, c01 + c10, c11, opacity
+  const float4 q = g.r_q[r];         // (float) k (c00, c01 + c10, c11), thr
+  const double dx = ((double)x0 + c0) - m.x, dy = ((double)y0 + c0) - m.y;
+  const float lg0 = (float)(kq * (c.x * dx * dx + c.y * dx * dy + c.z * dy * dy));
+  const float gx = (float)(kq * (2.0 * c.x * dx + c.y * dy));
+  const float gy = (float)(kq * (c.y * dx + 2.0 * c.z * dy));
+  // coefficient rounding (1 eps) + five rounded FMAs whose partial sums are all
+  // bounded by S (5 eps), with headroom: 8 eps
+  constexpr float h = (float)c0;
+  const float S = fabsf(lg0) + (fabsf(gx) + fabsf(gy)) * h +
+                  (fabsf(q.x) + fabsf(q.y) + fabsf(q.z)) * h * h;
+  rec.L = make_float4(lg0, gx, gy, q.w);
+  rec.Q = make_float4(q.x, q.y, q.z, 4.8e-7f * S + 1e-30f);
+  rec.col = g.r_color[r];
+  rec.rank = r;
 }
+
+// per-thread pixel constants: offsets from the tile centre and their products
+template <int TS, int PPT>
+struct PixelOffsets {
+  float dx[PPT], dy[PPT], xx[PPT], xy[PPT], yy[PPT];
+  __device__ __forceinline__ void init(int t);
+  __device__ __forceinline__ float lg(const float4& L, const float4& Q, int p) const {
+    return fmaf(Q.x, xx[p], fmaf(Q.y, xy[p], fmaf(Q.z, yy[p], fmaf(L.y, dx[p], fmaf(L.z, dy[p], L.x)))));
+  }
+};
 
 __device__ __noinline__ float alpha_f64(const BlendParams& bp, const Geom& g, int rank, float px,
                                         float py) {
@@ -696,16 +728,6 @@ __device__ __noinline__ float alpha_f64(const BlendParams& bp, const Geom& g, in
   const double ad = fmin(bp.clamp_d, c.w * exp(-0.5 * mh));
   return ad < bp.skip_d ? 0.f : fmaxf((float)ad, bp.skip);
 }
-
-// One staged splat of a blend batch: everything the inner loop reads, at one
-// base address (48 B: three vector loads, one pointer increment per splat)
-struct __align__(16) SplatRec {
-  float4 q;    // log2 form (A, B, C, reject threshold)
-  float4 col;  // rgb, opacity
-  float2 xy;   // mean relative to the tile origin
-  int rank;
-  float band;  // splat_band(q, xy) over this tile
-};
 
 template <int TS>
 struct BlendShape {
@@ -723,12 +745,25 @@ __device__ __forceinline__ int tile_pixel(int t, int p) {
   return (t >> 5) * (32 * BlendShape<TS>::PPT) + p * 32 + (t & 31);
 }
 
+template <int TS, int PPT>
+__device__ __forceinline__ void PixelOffsets<TS, PPT>::init(int t) {
+  constexpr float c0 = 0.5f * (TS - 1);
+#pragma unroll
+  for (int p = 0; p < PPT; ++p) {
+    const int li = tile_pixel<TS>(t, p);
+    dx[p] = (float)(li % TS) - c0;  // k + 1/2: the products below are exact
+    dy[p] = (float)(li / TS) - c0;
+    xx[p] = dx[p] * dx[p];
+    xy[p] = dx[p] * dy[p];
+    yy[p] = dy[p] * dy[p];
+  }
+}
+
 // TOUCH = false: the Stage-1 path, fp32 with the float64 decision band above.
 // TOUCH = true (the public rasterize_forward, which also returns the per-
 // Gaussian touch counts, rasterizer.py:279): every pair in float64 exactly as
 // the reference evaluates it (maha, exp, alpha, T_before and the stop test), so
-// the counts of weight = alpha T_before > 0 are the reference's, including the
-// denormal weights skip_alpha = 0 admits.
+// the counts of weight = alpha T_before > 0 are the reference's.
 template <int TS, bool TOUCH>
 __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_fwd_kernel(
     BlendParams bp, Geom g, const uint32_t* __restrict__ vals, float* __restrict__ image,
@@ -741,16 +776,18 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_fwd_kernel(
   const int tile = blockIdx.x;
   const int x0 = (tile % bp.ntx) * TS, y0 = (tile / bp.ntx) * TS;
   const int2 range = g.ranges[tile];
+  PixelOffsets<TS, PPT> po;
+  po.init(threadIdx.x);
   float T[PPT], C[PPT][3];
   double Td[TOUCH ? PPT : 1], Cd[TOUCH ? PPT : 1][3];
   int last[PPT];
   bool done[PPT];
-  float lx[PPT], ly[PPT];
+  float px[PPT], py[PPT];
 #pragma unroll
   for (int p = 0; p < PPT; ++p) {
     const int li = tile_pixel<TS>(threadIdx.x, p);
-    lx[p] = (float)(li % TS);
-    ly[p] = (float)(li / TS);
+    px[p] = (float)(x0 + li % TS);
+    py[p] = (float)(y0 + li / TS);
     T[p] = 1.f;
     C[p][0] = C[p][1] = C[p][2] = 0.f;
     if (TOUCH) {
@@ -768,16 +805,9 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_fwd_kernel(
     const int j = b + threadIdx.x;
     if (j < range.y) {
       const int r = (int)vals[j];
-      const double2 m = g.r_mean[r];
-      const float2 xy = make_float2((float)(m.x - x0), (float)(m.y - y0));
-      const float4 q = g.r_q[r];
-      s_sp[threadIdx.x].xy = xy;
-      s_sp[threadIdx.x].q = q;
-      s_sp[threadIdx.x].band = splat_band<TS>(q, xy);
-      s_sp[threadIdx.x].col = g.r_color[r];
-      s_sp[threadIdx.x].rank = r;
+      stage_splat<TS>(g, r, x0, y0, s_sp[threadIdx.x]);
       if (TOUCH) {
-        s_md[threadIdx.x] = m;
+        s_md[threadIdx.x] = g.r_mean[r];
         s_cd[threadIdx.x] = g.r_conop_d[r];
       }
     }
@@ -786,15 +816,13 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_fwd_kernel(
     const int cnt = min(NT, range.y - b);
     for (int k = 0; k < cnt; ++k) {
       if (!TOUCH) {  // fast path: reject on the log2 form before the exponential
-        const float2 xy = s_sp[k].xy;
-        const float4 q = s_sp[k].q;
-        const float band = s_sp[k].band;
-        const float qlo = q.w - band, qhi = q.w + (kNearBand + band);
+        const float4 L = s_sp[k].L, Q = s_sp[k].Q;
+        const float qlo = L.w - Q.w, qhi = L.w + (kNearBand + Q.w);
         float lgs[PPT];
         bool live[PPT], any_live = false, any_near = false;
 #pragma unroll
         for (int p = 0; p < PPT; ++p) {
-          lgs[p] = log2_gauss(q, lx[p] - xy.x, ly[p] - xy.y);
+          lgs[p] = po.lg(L, Q, p);
           live[p] = !done[p] && !(lgs[p] < qlo);
           any_live |= live[p];
           any_near |= live[p] && lgs[p] < qhi;
@@ -807,7 +835,7 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_fwd_kernel(
         if (any_near) {  // rare: decide in float64
 #pragma unroll
           for (int p = 0; p < PPT; ++p)
-            if (live[p] && lgs[p] < qhi) av[p] = alpha_f64(bp, g, s_sp[k].rank, lx[p] + x0, ly[p] + y0);
+            if (live[p] && lgs[p] < qhi) av[p] = alpha_f64(bp, g, s_sp[k].rank, px[p], py[p]);
         }
 #pragma unroll
         for (int p = 0; p < PPT; ++p) {  // predicated: a = 0 leaves the pixel unchanged
@@ -830,7 +858,7 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_fwd_kernel(
 #pragma unroll
       for (int p = 0; p < PPT; ++p) {
         if (done[p]) continue;
-        const double ddx = (double)(lx[p] + x0) - md.x, ddy = (double)(ly[p] + y0) - md.y;
+        const double ddx = (double)px[p] - md.x, ddy = (double)py[p] - md.y;
         const double mh = cd.x * ddx * ddx + cd.y * ddx * ddy + cd.z * ddy * ddy;
         double a = fmin(bp.clamp_d, cd.w * exp(-0.5 * mh));
         if (a < bp.skip_d) a = 0.0;
@@ -858,18 +886,14 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_fwd_kernel(
   }
 #pragma unroll
   for (int p = 0; p < PPT; ++p) {
-    const int li = tile_pixel<TS>(threadIdx.x, p);
-    const int px = x0 + li % TS, py = y0 + li / TS;
-    if (px >= bp.W || py >= bp.H) continue;
-    const int64_t pix = (int64_t)py * bp.W + px;
+    const int pxi = (int)px[p], pyi = (int)py[p];
+    if (pxi >= bp.W || pyi >= bp.H) continue;
+    const int64_t pix = (int64_t)pyi * bp.W + pxi;
     if (TOUCH) {
       T[p] = (float)Td[p];
-      C[p][0] = (float)(Cd[p][0] + Td[p] * (double)bp.bg[0]);
-      C[p][1] = (float)(Cd[p][1] + Td[p] * (double)bp.bg[1]);
-      C[p][2] = (float)(Cd[p][2] + Td[p] * (double)bp.bg[2]);
-      image[3 * pix + 0] = C[p][0];
-      image[3 * pix + 1] = C[p][1];
-      image[3 * pix + 2] = C[p][2];
+      image[3 * pix + 0] = (float)(Cd[p][0] + Td[p] * (double)bp.bg[0]);
+      image[3 * pix + 1] = (float)(Cd[p][1] + Td[p] * (double)bp.bg[1]);
+      image[3 * pix + 2] = (float)(Cd[p][2] + Td[p] * (double)bp.bg[2]);
       if (alpha_map) alpha_map[pix] = (float)(1.0 - Td[p]);
     } else {
       image[3 * pix + 0] = C[p][0] + T[p] * bp.bg[0];
@@ -884,19 +908,24 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_fwd_kernel(
 
 // K5a: reverse blend (rasterizer.py:306-349).  Per pixel, walk the tile list
 // back to front from the last contributor reconstructing T_before by
-// division, keeping the suffix sum incl. the background term.  Per splat, the
-// 8 pixel-gradient terms are reduced across the warp with a reduce-scatter
-// butterfly (9 shuffles instead of 8x5) so lane 4i ends up holding term i;
-// those lanes add into shared-memory per-splat accumulators (8 warps -> one
-// row), which are flushed to the per-rank global accumulators once per batch.
-template <int TS, bool FULL>
+// division, keeping the suffix sum incl. the background term.  Per splat the
+// geometric gradient is kept as moments about the tile centre d:
+//   M0 = sum dm, M1 = sum dm d, M2 = sum dm d d^T   (dm = op G dalpha),
+// which carry no large offsets; the flush shifts them to the splat's anchor
+// (the centre of its rectangle's first tile, integer multiples of the tile
+// size away) and K5b applies the anchor-to-mean offset in float64:
+//   sum dm (x - mu) = Delta M0 + M1, sum dm (x - mu)(x - mu)^T = ... .
+// Without that, fp32 sums of dm (x - mu)^2 over a splat near the camera plane
+// (|x - mu| ~ 1e5 px) lose the gradient entirely.  Per splat the 8 terms
+// colour 3, M1 2, M2 3 are reduced across the warp with a reduce-scatter
+// butterfly (9 shuffles) so lane 4i ends up holding term i, M0 with a warp
+// sum; those lanes add into shared-memory per-splat accumulators, flushed to
+// the per-rank global accumulators once per batch.
+template <int TS>
 __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_bwd_kernel(
     BlendParams bp, Geom g, const uint32_t* __restrict__ vals, const float* __restrict__ d_image) {
   constexpr int NT = BlendShape<TS>::NT, PPT = BlendShape<TS>::PPT;
-  constexpr int NA = 9;  // colour 3, mean2d 2, conic 3, opacity
-  // d(maha)/d(mean2d) = -2C d, with the conic recovered from the log2 form
-  // q = -0.5 log2(e) conic: k1, k2, k3 = kc (q.x, q.y / 2, q.z)
-  constexpr float kc = 2.7725887222397811f;  // 4 / log2(e)
+  constexpr int NA = 9;  // colour 3, M1 2, M2 3, M0
   __shared__ SplatRec s_sp[NT];
   // each warp owns a slot per splat (plain stores, summed at the flush);
   // larger tiles share one slot through shared-memory atomics
@@ -907,19 +936,22 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_bwd_kernel(
   __shared__ int s_last;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int tile = blockIdx.x;
-  const int x0 = (tile % bp.ntx) * TS, y0 = (tile / bp.ntx) * TS;
+  const int tx = tile % bp.ntx, ty = tile / bp.ntx;
+  const int x0 = tx * TS, y0 = ty * TS;
   const int2 range = g.ranges[tile];
-  float T[PPT], S[PPT], gp[PPT][3], lx[PPT], ly[PPT];
+  PixelOffsets<TS, PPT> po;
+  po.init(threadIdx.x);
+  float T[PPT], S[PPT], gp[PPT][3], px[PPT], py[PPT];
   int last[PPT];
   int max_last = 0;
 #pragma unroll
   for (int p = 0; p < PPT; ++p) {
     const int li = tile_pixel<TS>(threadIdx.x, p);
-    const int px = x0 + li % TS, py = y0 + li / TS;
-    lx[p] = (float)(li % TS);
-    ly[p] = (float)(li / TS);
-    if (px < bp.W && py < bp.H) {
-      const int64_t pix = (int64_t)py * bp.W + px;
+    const int pxi = x0 + li % TS, pyi = y0 + li / TS;
+    px[p] = (float)pxi;
+    py[p] = (float)pyi;
+    if (pxi < bp.W && pyi < bp.H) {
+      const int64_t pix = (int64_t)pyi * bp.W + pxi;
       T[p] = g.t_final[pix];
       last[p] = g.n_contrib[pix];
       gp[p][0] = d_image[3 * pix];
@@ -944,34 +976,20 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_bwd_kernel(
   for (int end = end0; end > range.x; end -= NT) {
     const int start = max(range.x, end - NT);
     const int cnt = end - start;
-    if (threadIdx.x < cnt) {
-      const int pos = end - 1 - threadIdx.x;
-      const int r = (int)vals[pos];
-      const double2 m = g.r_mean[r];
-      const float2 xy = make_float2((float)(m.x - x0), (float)(m.y - y0));
-      const float4 q = g.r_q[r];
-      s_sp[threadIdx.x].xy = xy;
-      s_sp[threadIdx.x].q = q;
-      s_sp[threadIdx.x].band = splat_band<TS>(q, xy);
-      s_sp[threadIdx.x].col = g.r_color[r];
-      s_sp[threadIdx.x].rank = r;
-    }
+    if (threadIdx.x < cnt) stage_splat<TS>(g, (int)vals[end - 1 - threadIdx.x], x0, y0,
+                                           s_sp[threadIdx.x]);
     __syncthreads();
     for (int k = 0; k < cnt; ++k) {
       const int pos_rel = end - 1 - k - range.x;
-      const float2 xy = s_sp[k].xy;
-      const float4 q = s_sp[k].q;
-      const float band = s_sp[k].band;
-      const float qlo = q.w - band, qhi = q.w + (kNearBand + band);
+      const float4 L = s_sp[k].L, Q = s_sp[k].Q;
+      const float qlo = L.w - Q.w, qhi = L.w + (kNearBand + Q.w);
       // cheap part for every pixel, then a warp-uniform skip; the rest is
       // predicated (a = 0 makes every update a no-op) instead of branching
-      float dxs[PPT], dys[PPT], lgs[PPT];
+      float lgs[PPT];
       bool live[PPT], any_live = false, any_near = false;
 #pragma unroll
       for (int p = 0; p < PPT; ++p) {
-        dxs[p] = lx[p] - xy.x;
-        dys[p] = ly[p] - xy.y;
-        lgs[p] = log2_gauss(q, dxs[p], dys[p]);  // same decisions as the forward
+        lgs[p] = po.lg(L, Q, p);  // same decisions as the forward
         live[p] = pos_rel < last[p] && !(lgs[p] < qlo);
         any_live |= live[p];
         any_near |= live[p] && lgs[p] < qhi;
@@ -987,7 +1005,7 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_bwd_kernel(
       if (any_near) {  // rare: decide in float64
 #pragma unroll
         for (int p = 0; p < PPT; ++p)
-          if (live[p] && lgs[p] < qhi) av[p] = alpha_f64(bp, g, s_sp[k].rank, lx[p] + x0, ly[p] + y0);
+          if (live[p] && lgs[p] < qhi) av[p] = alpha_f64(bp, g, s_sp[k].rank, px[p], py[p]);
       }
       float v[NA] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
       bool any = false;
@@ -1007,16 +1025,15 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_bwd_kernel(
         T[p] = tb;
         // no contribution, or flat above the clamp (rasterizer.py:336-337)
         da = (a > 0.f && og < bp.clamp) ? da : 0.f;
-        // dm = -0.5 og da; the -0.5 and the conic factors k1..k3 are per-splat
-        // constants applied once at the flush (terms 3, 4 hold sum e, sum f)
+        // dm = og da (the reference's -0.5 is applied in K5b); moments about the tile centre
         const float dm = og * da;
-        const float e = dm * dxs[p], f = dm * dys[p];
+        const float e = dm * po.dx[p], f = dm * po.dy[p];
         v[3] += e;
         v[4] += f;
-        v[5] = fmaf(e, dxs[p], v[5]);
-        v[6] = fmaf(e, dys[p], v[6]);
-        v[7] = fmaf(f, dys[p], v[7]);
-        if (FULL) v[8] = fmaf(da, G, v[8]);
+        v[5] = fmaf(e, po.dx[p], v[5]);
+        v[6] = fmaf(e, po.dy[p], v[6]);
+        v[7] = fmaf(f, po.dy[p], v[7]);
+        v[8] += dm;
         any |= a > 0.f;
       }
       const unsigned bal = __ballot_sync(0xffffffffu, any);
@@ -1041,25 +1058,24 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_bwd_kernel(
         }
         h1 += __shfl_xor_sync(0xffffffffu, h1, 2);
         h1 += __shfl_xor_sync(0xffffffffu, h1, 1);
+        const float m0 = warp_sum(v[8]);
         float* slot = s_acc + ((PRIV ? warp : 0) * NT + k) * NA;
         if ((lane & 3) == 0) {
           if (PRIV) slot[lane >> 2] = h1;
           else atomicAdd(slot + (lane >> 2), h1);
         }
-        if (FULL) {
-          const float o = warp_sum(v[8]);
-          if (lane == 0) {
-            if (PRIV) slot[8] = o;
-            else atomicAdd(slot + 8, o);
-          }
+        if (lane == 0) {
+          if (PRIV) slot[8] = m0;
+          else atomicAdd(slot + 8, m0);
+          s_any[k] = 1;
         }
-        if (lane == 0) s_any[k] = 1;
       }
     }
     __syncthreads();
     // flush this batch's per-splat sums (one row per splat) and reset them
     if (threadIdx.x < cnt && s_any[threadIdx.x]) {
-      float* a = g.acc + (int64_t)s_sp[threadIdx.x].rank * kAccStride;
+      const int r = s_sp[threadIdx.x].rank;
+      float* a = g.acc + (int64_t)r * kAccStride;
       float t[NA];
 #pragma unroll
       for (int q = 0; q < NA; ++q) t[q] = 0.f;
@@ -1072,27 +1088,23 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_bwd_kernel(
           sa[q] = 0.f;
         }
       }
-      {  // mean2d = -0.5 (-2C) [sum e, sum f]; conic terms times -0.5
-        const float4 q = s_sp[threadIdx.x].q;
-        const float k1 = kc * q.x, k2 = 0.5f * kc * q.y, k3 = kc * q.z;
-        const float E = t[3], F = t[4];
-        t[3] = -0.5f * fmaf(k1, E, k2 * F);
-        t[4] = -0.5f * fmaf(k2, E, k3 * F);
-        t[5] *= -0.5f;
-        t[6] *= -0.5f;
-        t[7] *= -0.5f;
-      }
-      red_add_v4(a, t[0], t[1], t[2], t[3]);
-      red_add_v4(a + 4, t[4], t[5], t[6], t[7]);
-      if (FULL) atomicAdd(a + 8, t[8]);
-      g.touched[s_sp[threadIdx.x].rank] = 1;
+      // shift the moments from this tile's centre to the anchor (the centre
+      // of the rectangle's first tile): d_anchor = d_tile + s, s multiples of TS
+      const int4 rc = g.r_rect[r];
+      const float sx = (float)((tx - rc.x) * TS), sy = (float)((ty - rc.z) * TS);
+      const float M0 = t[8], M1x = t[3], M1y = t[4];
+      red_add_v4(a, t[0], t[1], t[2], M0);
+      red_add_v4(a + 4, fmaf(sx, M0, M1x), fmaf(sy, M0, M1y),
+                 fmaf(sx * sx, M0, fmaf(2.f * sx, M1x, t[5])),
+                 fmaf(sx * sy, M0, fmaf(sx, M1y, fmaf(sy, M1x, t[6]))));
+      atomicAdd(a + 8, fmaf(sy * sy, M0, fmaf(2.f * sy, M1y, t[7])));
+      g.touched[r] = 1;
       s_any[threadIdx.x] = 0;
     }
     __syncthreads();
   }
 }
 
-// K5b: per-survivor chain to raw parameters (rasterizer.py:351-402), float64
 // K5b: per-Gaussian chain from the rank accumulators back to the raw parameters
 // (rasterizer.py:351-402).  One thread per Gaussian in index order (coalesced
 // parameter reads and gradient writes; the rank accumulators are gathered).
@@ -1101,7 +1113,7 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_bwd_kernel(
 template <int DEG>
 __global__ void __launch_bounds__(128, 4) gaussian_bwd_kernel(CamD cam, ss_cloud cl, Geom g,
                                                               int64_t n, ss_cloud_grads out,
-                                                              int full) {
+                                                              int full, int ts) {
   const int64_t gid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (gid >= n) return;
   constexpr int K = (DEG + 1) * (DEG + 1);  // == cl.sh_coeffs
@@ -1130,9 +1142,29 @@ __global__ void __launch_bounds__(128, 4) gaussian_bwd_kernel(CamD cam, ss_cloud
   const float4 a0 = *reinterpret_cast<const float4*>(g.acc + (int64_t)r * kAccStride);
   const float4 a1 = *reinterpret_cast<const float4*>(g.acc + (int64_t)r * kAccStride + 4);
   const float a8 = g.acc[(int64_t)r * kAccStride + 8];
-  const double am[2] = {a0.w, a1.x};
-  const double A[2][2] = {{a1.y, a1.z}, {a1.z, a1.w}};
-  const double aop = a8;
+  // moments about the anchor (K5a) -> sums over (x - mu): Delta = anchor - mu
+  double am[2], A[2][2], aop;
+  {
+    const int4 rc = g.r_rect[r];
+    const double2 m = g.r_mean[r];
+    const double4 cd = g.r_conop_d[r];
+    const double c0 = 0.5 * (ts - 1);
+    const double Dx = ((double)rc.x * ts + c0) - m.x, Dy = ((double)rc.z * ts + c0) - m.y;
+    const double M0 = a0.w, M1x = a1.x, M1y = a1.y, M2xx = a1.z, M2xy = a1.w, M2yy = a8;
+    const double E = Dx * M0 + M1x, F = Dy * M0 + M1y;
+    const double Exx = Dx * Dx * M0 + 2.0 * Dx * M1x + M2xx;
+    const double Exy = Dx * Dy * M0 + Dx * M1y + Dy * M1x + M2xy;
+    const double Fyy = Dy * Dy * M0 + 2.0 * Dy * M1y + M2yy;
+    // acc_mean2d = C [E, F] (rasterizer.py:342-343 with dm_ref = -dm / 2),
+    // acc_conic = -1/2 [E_xx E_xy; E_xy F_yy], acc_opacity = sum G da = M0 / op
+    const double c01 = 0.5 * cd.y;
+    am[0] = cd.x * E + c01 * F;
+    am[1] = c01 * E + cd.z * F;
+    A[0][0] = -0.5 * Exx;
+    A[0][1] = A[1][0] = -0.5 * Exy;
+    A[1][1] = -0.5 * Fyy;
+    aop = M0 / cd.w;
+  }
   if (out.viewspace) out.viewspace[gid] = (float)sqrt(am[0] * am[0] + am[1] * am[1]);
   if (out.contributed) out.contributed[gid] = g.touched[r];
   // ---- colour -> SH and view direction first (sh.py:62-81), fp32 with the
@@ -1305,15 +1337,14 @@ static int launch_blend_fwd(int ts, int64_t ntiles, cudaStream_t st, const Blend
   return SS_OK;
 }
 
-template <bool FULL>
 static int launch_blend_bwd(int ts, int64_t ntiles, cudaStream_t st, const BlendParams& bp,
                             const Geom& g, const uint32_t* vals, const float* d_image) {
   const unsigned grid = (unsigned)ntiles;
   switch (ts) {
-    case 8: blend_bwd_kernel<8, FULL><<<grid, BlendShape<8>::NT, 0, st>>>(bp, g, vals, d_image); break;
-    case 16: blend_bwd_kernel<16, FULL><<<grid, BlendShape<16>::NT, 0, st>>>(bp, g, vals, d_image); break;
-    case 32: blend_bwd_kernel<32, FULL><<<grid, BlendShape<32>::NT, 0, st>>>(bp, g, vals, d_image); break;
-    default: blend_bwd_kernel<64, FULL><<<grid, BlendShape<64>::NT, 0, st>>>(bp, g, vals, d_image); break;
+    case 8: blend_bwd_kernel<8><<<grid, BlendShape<8>::NT, 0, st>>>(bp, g, vals, d_image); break;
+    case 16: blend_bwd_kernel<16><<<grid, BlendShape<16>::NT, 0, st>>>(bp, g, vals, d_image); break;
+    case 32: blend_bwd_kernel<32><<<grid, BlendShape<32>::NT, 0, st>>>(bp, g, vals, d_image); break;
+    default: blend_bwd_kernel<64><<<grid, BlendShape<64>::NT, 0, st>>>(bp, g, vals, d_image); break;
   }
   SS_CHECK_LAUNCH("blend_bwd_kernel");
   return SS_OK;
@@ -1406,18 +1437,17 @@ int raster_backward(const ss_cloud* cl, const ss_camera* cam, const ss_raster_se
   SS_CUDA(cudaMemsetAsync(g.touched, 0, n, st));
   prof_begin(PH_BLEND_BWD, st);
   const BlendParams bp = blend_params(cam, s);
-  if (full) SS_TRY(launch_blend_bwd<true>(s->tile_size, ntiles, st, bp, g, b.vals_out, d_image));
-  else SS_TRY(launch_blend_bwd<false>(s->tile_size, ntiles, st, bp, g, b.vals_out, d_image));
+  SS_TRY(launch_blend_bwd(s->tile_size, ntiles, st, bp, g, b.vals_out, d_image));
   prof_end(PH_BLEND_BWD, st);
   prof_begin(PH_GAUSS_BWD, st);
   {
     const unsigned grid = (unsigned)cdiv(n, 128);
     const CamD cd = make_cam(cam);
     switch (cl->sh_coeffs) {
-      case 1: gaussian_bwd_kernel<0><<<grid, 128, 0, st>>>(cd, *cl, g, n, *grads, full); break;
-      case 4: gaussian_bwd_kernel<1><<<grid, 128, 0, st>>>(cd, *cl, g, n, *grads, full); break;
-      case 9: gaussian_bwd_kernel<2><<<grid, 128, 0, st>>>(cd, *cl, g, n, *grads, full); break;
-      default: gaussian_bwd_kernel<3><<<grid, 128, 0, st>>>(cd, *cl, g, n, *grads, full); break;
+      case 1: gaussian_bwd_kernel<0><<<grid, 128, 0, st>>>(cd, *cl, g, n, *grads, full, s->tile_size); break;
+      case 4: gaussian_bwd_kernel<1><<<grid, 128, 0, st>>>(cd, *cl, g, n, *grads, full, s->tile_size); break;
+      case 9: gaussian_bwd_kernel<2><<<grid, 128, 0, st>>>(cd, *cl, g, n, *grads, full, s->tile_size); break;
+      default: gaussian_bwd_kernel<3><<<grid, 128, 0, st>>>(cd, *cl, g, n, *grads, full, s->tile_size); break;
     }
   }
   SS_CHECK_LAUNCH("gaussian_bwd_kernel");

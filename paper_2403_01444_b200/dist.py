@@ -78,7 +78,11 @@ class ViewShardedStage1:
         self.trainer = trainer
         self.views_per_iteration = views_per_iteration or world
         self.cfg = getattr(trainer, "cfg", cfg)
-        trainer.enable_loss_accum()
+        # one view per iteration on one rank is the reference loop itself: the
+        # iteration (Adam included) replays as one graph, losses in its history
+        self.single = world == 1 and self.views_per_iteration == 1
+        if not self.single:
+            trainer.enable_loss_accum()
         self.loss_slot = trainer.g_flat[trainer.n_table + trainer.n_params:][:1]
         self._losses: list[torch.Tensor] = []
 
@@ -93,6 +97,12 @@ class ViewShardedStage1:
         b = len(batch)
         flags = (list(accumulate_stats) if isinstance(accumulate_stats, (list, tuple))
                  else [bool(accumulate_stats)] * b)
+        if self.single and b == 1:
+            if host_targets is not None:
+                tr.stage_target(batch[0], host_targets[batch[0]])
+            tr.iterate(batch[0], accumulate_stats=flags[0], staged=host_targets is not None)
+            self._losses.append(tr.loss_dev)
+            return
         lo = (b * self.rank) // self.world
         mine = shard_views(batch, self.rank, self.world)
         last = len(mine) - 1
@@ -121,7 +131,7 @@ class ViewShardedStage1:
         copied from pinned host memory, the iteration runs, and the batch loss
         is read back (device -> host)."""
         self.step(batch, accumulate_stats, host_targets)
-        return float(self._losses[-1].item()) / len(batch)
+        return float(self._losses[-1].item()) / (1 if self.single else len(batch))
 
     def run(self, iterations: int | None = None, frame_index: int = 1) -> np.ndarray:
         """The batched Stage-1 loop: reference view sequence B views at a time,
@@ -135,8 +145,10 @@ class ViewShardedStage1:
         self._losses = []
         for t, batch in enumerate(batched_view_order(seed, frame_index, n_views, it, b)):
             self.step(batch, [t * b + j >= stats_from for j in range(b)])
+            if self.single:
+                self._losses[-1] = self._losses[-1].clone()
         self.reduce_stats()
-        return torch.cat(self._losses).double().cpu().numpy() / b
+        return self.batch_losses()
 
     def reduce_stats(self) -> None:
         """Sum the per-rank view-space statistics (once per frame)."""
@@ -146,5 +158,8 @@ class ViewShardedStage1:
             dist.all_reduce(tr.stats_count, op=dist.ReduceOp.SUM, group=self.group)
 
     def batch_losses(self) -> np.ndarray:
-        b = self.views_per_iteration
-        return torch.cat(self._losses).double().cpu().numpy() / b if self._losses else np.zeros(0)
+        """Mean loss over the views of each iteration stepped so far."""
+        if not self._losses:
+            return np.zeros(0)
+        b = 1 if self.single else self.views_per_iteration
+        return torch.cat([x.reshape(1) for x in self._losses]).double().cpu().numpy() / b

@@ -384,12 +384,19 @@ class Stage1Trainer:
     def step(self, view: int) -> None:
         self.iterate(view)
 
-    def run_from_host(self, order: list[int], host_targets) -> np.ndarray:
+    def run_from_host(self, order: list[int], host_targets, before_step=None,
+                      after_step=None) -> np.ndarray:
         """Stage-1 iterations whose targets live in pinned HOST memory: each
         iteration's target is copied host->device on a copy stream while the
-        previous iteration computes (two staging buffers, event-ordered), and
-        each iteration's loss is read device->host into pinned memory.  One
-        synchronisation at the end; returns the per-iteration losses."""
+        previous iteration computes (two staging buffers), and each
+        iteration's loss is read device->host into pinned memory.  One
+        synchronisation at the end; returns the per-iteration losses.
+
+        before_step(k) / after_step(k) run on the host around step k's work;
+        everything step k puts on the device -- its own target copy if not
+        already prefetched, the prefetch of step k+1's target, the iteration,
+        the loss read-back -- is stream-ordered between them (a timer can
+        record CUDA events there)."""
         dev = self.dev
         main = torch.cuda.current_stream(dev)
         copy = getattr(self, "_copy_stream", None) or torch.cuda.Stream(dev)
@@ -397,27 +404,30 @@ class Stage1Trainer:
         if getattr(self, "_stage2", None) is None:
             self._stage2 = [torch.empty_like(self.targets[0]) for _ in range(2)]
         ready = [torch.cuda.Event() for _ in range(2)]
-        free = [torch.cuda.Event() for _ in range(2)]
         losses = torch.empty(len(order), dtype=torch.float64, pin_memory=True)
 
         def h2d(k):
             b = k & 1
+            copy.wait_stream(main)  # buffer b is free, and the copy starts inside step k-1
             with torch.cuda.stream(copy):
-                if k >= 2:
-                    copy.wait_event(free[b])
                 t = host_targets[order[k]]
                 self._stage2[b].view(-1)[: t.numel()].copy_(t.view(-1), non_blocking=True)
                 ready[b].record(copy)
 
-        if order:
-            h2d(0)
         for k, v in enumerate(order):
+            if before_step is not None:
+                before_step(k)
+            if k == 0:
+                h2d(0)
             if k + 1 < len(order):
                 h2d(k + 1)
             main.wait_event(ready[k & 1])
             self.iterate(v, target=self._stage2[k & 1])
-            free[k & 1].record(main)
             losses[k:k + 1].copy_(self.loss_dev, non_blocking=True)
+            if k + 1 < len(order):
+                main.wait_event(ready[(k + 1) & 1])  # the prefetch counts in this step
+            if after_step is not None:
+                after_step(k)
         main.synchronize()
         return losses.numpy().copy()
 
