@@ -117,6 +117,73 @@ class ParallelStage1:
         self.nproc = int(nproc or os.cpu_count() or 1)
 
     # ------------------------------------------------------------------
+    def render(self, cloud, cam) -> np.ndarray:
+        """rasterize_forward's image (rasterizer.py:214-281), black background."""
+        return np.array(self._render(cloud, cam)[4])
+
+    def _render(self, cloud, cam):
+        """Projection over Gaussian rows, the global stable depth order, then the
+        forward blend over interleaved tile rows.  Returns the projected
+        survivors, tile rectangles, a per-worker tile-list function and the image."""
+        P = self.nproc
+        n = len(cloud["means"])
+        ncol = sum(c for _, c in _PROJ_COLS)
+        pbuf = shared((n, ncol))
+        pcount = shared(P, np.int64)
+        gch = _chunks(n, P)
+
+        def proj(wid):
+            a, b = gch[wid]
+            if a == b:
+                return
+            pj = O.project({k: v[a:b] for k, v in cloud.items()}, cam)
+            m = len(pj["indices"])
+            col = 0
+            for name, c in _PROJ_COLS:
+                v = pj[name] + (a if name == "indices" else 0)
+                pbuf[a:a + m, col:col + c] = v.reshape(m, c)
+                col += c
+            pcount[wid] = m
+
+        fork_map(P, proj)
+        parts = np.concatenate([pbuf[a:a + int(pcount[i])] for i, (a, _) in enumerate(gch)])
+        keep = parts[:, 0].astype(np.int64)
+        order = np.lexsort((keep, parts[:, 3]))  # (depth, index): rasterizer.py:228-230
+        parts = parts[order]
+        pj, col = {}, 0
+        for name, c in _PROJ_COLS:
+            v = parts[:, col:col + c]
+            shape = {"cov3d": (3, 3), "cov2d": (2, 2), "conic": (2, 2)}.get(name)
+            pj[name] = v.reshape(-1, *shape) if shape else (v[:, 0] if c == 1 else v)
+            col += c
+        pj["indices"] = pj["indices"].astype(np.int64)
+        s = dict(O.DEFAULT_SETTINGS)
+        h, wd, ts = cam["height"], cam["width"], s["tile_size"]
+        rect, vis = O.tile_rects(pj["mean2d"], pj["cov2d"], pj["opacity"], wd, h, ts,
+                                 s["skip_alpha"])
+        ntx, nty = (wd + ts - 1) // ts, (h + ts - 1) // ts
+        # tile rows interleaved over the workers (the centre rows carry most pairs)
+        bands = [[(r, r + 1) for r in range(wk, nty, P)] for wk in range(min(P, nty))]
+        self._bands = bands
+
+        def band_tiles(wid):
+            return [t for band in bands[wid] for t in _band_tiles(rect, vis, *band, ntx, ts, wd, h)]
+
+        image = shared((h, wd, 3))
+
+        def blend(wid):
+            if wid >= len(bands):
+                return
+            for tile in band_tiles(wid):
+                y0, y1, x0, x1, mem = tile
+                _, _, _, _, al, tb, alive, tf = O._tile_pairs(pj, tile, s)
+                wgt = al * tb * alive
+                image[y0:y1, x0:x1] = (wgt @ pj["colors"][mem]).reshape(y1 - y0, x1 - x0, 3)
+
+        fork_map(P, blend)
+        return pj, rect, vis, band_tiles, image
+
+    # ------------------------------------------------------------------
     def iteration(self, state, cloud, cam, target, lam=0.2, lr=0.002, apply_adam=True,
                   rotate_sh=True):
         """Same contract as oracle.stage1.stage1_iteration with its defaults
@@ -149,63 +216,11 @@ class ParallelStage1:
                 moved[k][inside[a:b]] = mv[k]
 
         fork_map(P, fwd)
-        # ---- projection (Gaussian rows), then the global stable depth order
-        ncol = sum(c for _, c in _PROJ_COLS)
-        pbuf = shared((n, ncol))
-        pcount = shared(P, np.int64)
-        gch = _chunks(n, P)
-
-        def proj(wid):
-            a, b = gch[wid]
-            if a == b:
-                return
-            pj = O.project({k: v[a:b] for k, v in moved.items()}, cam)
-            m = len(pj["indices"])
-            col = 0
-            for name, c in _PROJ_COLS:
-                v = pj[name] + (a if name == "indices" else 0)
-                pbuf[a:a + m, col:col + c] = v.reshape(m, c)
-                col += c
-            pcount[wid] = m
-
-        fork_map(P, proj)
-        parts = np.concatenate([pbuf[a:a + int(pcount[i])] for i, (a, _) in enumerate(gch)])
-        keep = parts[:, 0].astype(np.int64)
-        order = np.lexsort((keep, parts[:, 3]))  # (depth, index): rasterizer.py:228-230
-        parts = parts[order]
-        pj, col = {}, 0
-        for name, c in _PROJ_COLS:
-            v = parts[:, col:col + c]
-            shape = {"cov3d": (3, 3), "cov2d": (2, 2), "conic": (2, 2)}.get(name)
-            pj[name] = v.reshape(-1, *shape) if shape else (v[:, 0] if c == 1 else v)
-            col += c
-        pj["indices"] = pj["indices"].astype(np.int64)
+        pj, rect, vis, band_tiles, image = self._render(moved, cam)
         m = len(pj["indices"])
         s = dict(O.DEFAULT_SETTINGS)
-        h, wd, ts = cam["height"], cam["width"], s["tile_size"]
-        rect, vis = O.tile_rects(pj["mean2d"], pj["cov2d"], pj["opacity"], wd, h, ts,
-                                 s["skip_alpha"])
-        ntx, nty = (wd + ts - 1) // ts, (h + ts - 1) // ts
-        # tile rows interleaved over the workers (the centre rows carry most pairs)
-        bands = [[(r, r + 1) for r in range(wk, nty, P)] for wk in range(min(P, nty))]
-
-        def band_tiles(wid):
-            return [t for band in bands[wid] for t in _band_tiles(rect, vis, *band, ntx, ts, wd, h)]
-        # ---- blend forward (bands of tile rows)
-        image = shared((h, wd, 3))
-        alpha_map = shared((h, wd))
-
-        def blend(wid):
-            if wid >= len(bands):
-                return
-            for tile in band_tiles(wid):
-                y0, y1, x0, x1, mem = tile
-                _, _, _, _, al, tb, alive, tf = O._tile_pairs(pj, tile, s)
-                wgt = al * tb * alive
-                image[y0:y1, x0:x1] = (wgt @ pj["colors"][mem]).reshape(y1 - y0, x1 - x0, 3)
-                alpha_map[y0:y1, x0:x1] = (1.0 - tf).reshape(y1 - y0, x1 - x0)
-
-        fork_map(P, blend)
+        h, wd = cam["height"], cam["width"]
+        bands = self._bands
         # ---- loss (colour channels): the 3-channel loss is the mean of the
         # per-channel losses and its gradient a third of theirs (losses.py:84-148)
         lbuf = shared(3)

@@ -385,7 +385,7 @@ class Stage1Trainer:
         self.iterate(view)
 
     def run_from_host(self, order: list[int], host_targets, before_step=None,
-                      after_step=None) -> np.ndarray:
+                      after_step=None, flags=None) -> np.ndarray:
         """Stage-1 iterations whose targets live in pinned HOST memory: each
         iteration's target is copied host->device on a copy stream while the
         previous iteration computes (two staging buffers), and each
@@ -396,7 +396,7 @@ class Stage1Trainer:
         everything step k puts on the device -- its own target copy if not
         already prefetched, the prefetch of step k+1's target, the iteration,
         the loss read-back -- is stream-ordered between them (a timer can
-        record CUDA events there)."""
+        record CUDA events there).  flags: per-step accumulate_stats."""
         dev = self.dev
         main = torch.cuda.current_stream(dev)
         copy = getattr(self, "_copy_stream", None) or torch.cuda.Stream(dev)
@@ -422,7 +422,8 @@ class Stage1Trainer:
             if k + 1 < len(order):
                 h2d(k + 1)
             main.wait_event(ready[k & 1])
-            self.iterate(v, target=self._stage2[k & 1])
+            self.iterate(v, target=self._stage2[k & 1],
+                         accumulate_stats=None if flags is None else flags[k])
             losses[k:k + 1].copy_(self.loss_dev, non_blocking=True)
             if k + 1 < len(order):
                 main.wait_event(ready[(k + 1) & 1])  # the prefetch counts in this step

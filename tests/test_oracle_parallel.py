@@ -33,3 +33,12 @@ def test_parallel_iteration_equals_serial():
         np.testing.assert_allclose(got["render_grads"][k], ref["render_grads"][k], rtol=1e-9,
                                    atol=1e-18)
     np.testing.assert_allclose(sb["tables"], sa["tables"], rtol=1e-9, atol=1e-15)
+
+
+def test_parallel_render_equals_serial():
+    from paper_2403_01444_b200 import scenes
+
+    sc = scenes.small_scene(seed=9, n=900, width=64, height=48, sh_degree=1, n_views=1)
+    ref = O.render(sc.cloud, sc.cameras[0])[0]["image"]
+    got = parallel.ParallelStage1(4).render(sc.cloud, sc.cameras[0])
+    np.testing.assert_allclose(got, ref, rtol=0, atol=1e-14)
