@@ -392,12 +392,16 @@ def main():
         raise RuntimeError("tile-pair capacity overflow in the timed region")
     ms = max_over_ranks(torch, dist, world, float(np.mean(step_ms)))
     value = world * 1000.0 / ms  # view-iterations per second over the whole job
-    # ---- per-kernel breakdown: the same timed positions again, eager launches
-    # with phase events and a synchronisation per step
-    tr.use_graphs = False
+    # ---- per-kernel breakdown: the same timed positions replayed again from
+    # the frame start, from graphs captured with event-record nodes around every
+    # phase (ss_profile_enable), the L2 flushed before each timed iteration
     tr.reset_frame()
-    tl.cur = 0
     lib.ss_profile_enable(1)
+    tl.cur = 0
+    tl.advance_to(FRAME)  # capture the profiled graphs
+    tr.reset_frame()
+    torch.cuda.synchronize()
+    tl.cur = 0
     nph = lib.ss_profile_count()
     names = [lib.ss_profile_name(i).decode() for i in range(nph)]
     phase_ms = {n: [] for n in names}
@@ -405,7 +409,6 @@ def main():
     buf = (np.ctypeslib.ctypes.c_double * nph)()
     for k, p in enumerate(positions):
         tl.advance_to(p)
-        lib.ss_profile_read(buf, nph)  # drop the untimed iterations' events
         flush.fill_(k & 0xFF)
         tl.run(p)
         tl.cur = p + 1
@@ -416,7 +419,6 @@ def main():
                 phase_ms[n].append(buf[i])
         pairs.append(int(tr.pairs_of_last(1)[0]))
     lib.ss_profile_enable(0)
-    tr.use_graphs = True
     hbm, tc, peak_src = peaks()
     surv = survivors(sc)
     units = dict(n=len(sc.cloud["means"]), n_in=int(tr.rows.numel()),
@@ -466,6 +468,8 @@ def main():
                                  f"iterations between them run untimed",
                            graph_capture="every (view, statistics flag) iteration graph captured "
                                          "in one untimed pass over the frame after the warm-up",
+                           kernel_times="CUDA events recorded inside the replayed iteration "
+                                        "graphs (a second pass over the same positions)",
                            mean_tile_pairs=units["D"],
                            decoder=["fp32 FFMA", "tcgen05 3xTF32",
                                     "tcgen05 tf32"][lib.ss_get_mlp_mode()]),

@@ -115,9 +115,12 @@ size_t ss_struct_size(int32_t which);
 /* number of kernel launches issued by this library since load (telemetry) */
 int64_t ss_launch_count(void);
 /* Phase timing: when enabled, CUDA events are recorded on the launching
- * stream around each hot-path phase; ss_profile_read returns the ms of the
- * last instance of each phase (-1 when not run since the previous read). */
+ * stream around each hot-path phase (as event-record nodes when the stream is
+ * being captured into a CUDA graph, so replays re-record them);
+ * ss_profile_read returns the ms of the last instance of each phase (-1 when
+ * never recorded since ss_profile_enable). */
 int ss_profile_enable(int32_t on);
+int32_t ss_profile_enabled(void);
 int32_t ss_profile_count(void);
 const char* ss_profile_name(int32_t phase);
 int ss_profile_read(double* ms, int32_t n);

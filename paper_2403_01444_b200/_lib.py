@@ -95,6 +95,7 @@ SIGNATURES = [
     ("ss_struct_size", SZ, [I32]),
     ("ss_launch_count", I64, []),
     ("ss_profile_enable", I32, [I32]),
+    ("ss_profile_enabled", I32, []),
     ("ss_profile_name", C.c_char_p, [I32]),
     ("ss_profile_count", I32, []),
     ("ss_profile_read", I32, [C.POINTER(D), I32]),

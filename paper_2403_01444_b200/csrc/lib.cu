@@ -172,17 +172,25 @@ static const char* kPhaseNames[PH_COUNT] = {
     "blend_backward", "gaussian_backward", "transform_vjp", "decoder_backward", "scatter",
     "adam"};
 
+// Inside a CUDA-graph capture the events become external event-record nodes,
+// so a replayed graph re-records them and the phases can be timed in replay.
+static void prof_record(cudaEvent_t e, cudaStream_t s) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(s, &cs);
+  if (cs == cudaStreamCaptureStatusActive) cudaEventRecordWithFlags(e, s, cudaEventRecordExternal);
+  else cudaEventRecord(e, s);
+}
 void prof_begin(int phase, cudaStream_t s) {
   if (!g_prof) return;
   if (!g_ev_ready) {
     for (auto& e : g_ev) cudaEventCreate(&e);
     g_ev_ready = true;
   }
-  cudaEventRecord(g_ev[2 * phase], s);
+  prof_record(g_ev[2 * phase], s);
 }
 void prof_end(int phase, cudaStream_t s) {
   if (!g_prof || !g_ev_ready) return;
-  cudaEventRecord(g_ev[2 * phase + 1], s);
+  prof_record(g_ev[2 * phase + 1], s);
   g_used[phase] = true;
 }
 }  // namespace ss
@@ -191,24 +199,28 @@ extern "C" {
 int ss_profile_enable(int32_t on) {
   ss::g_prof = on != 0;
   for (bool& u : ss::g_used) u = false;
+  if (on && !ss::g_ev_ready) {  // created outside any capture
+    for (auto& e : ss::g_ev) cudaEventCreate(&e);
+    ss::g_ev_ready = true;
+  }
   return SS_OK;
 }
+int32_t ss_profile_enabled(void) { return ss::g_prof ? 1 : 0; }
 const char* ss_profile_name(int32_t phase) {
   return phase >= 0 && phase < ss::PH_COUNT ? ss::kPhaseNames[phase] : "";
 }
-/* ms of the last recorded instance of each phase (-1 if not recorded since the
- * previous read); synchronises on the recorded events. */
+/* ms of the last recorded instance of each phase (-1 if never recorded since
+ * ss_profile_enable); synchronises on the recorded events. */
 int32_t ss_profile_count(void) { return ss::PH_COUNT; }
 
 int ss_profile_read(double* ms, int32_t n) {
   for (int p = 0; p < n && p < ss::PH_COUNT; ++p) {
     ms[p] = -1.0;
-    if (!ss::g_used[p]) continue;
+    if (!ss::g_used[p] || !ss::g_prof) continue;
     float t = 0.f;
     SS_CUDA(cudaEventSynchronize(ss::g_ev[2 * p + 1]));
     SS_CUDA(cudaEventElapsedTime(&t, ss::g_ev[2 * p], ss::g_ev[2 * p + 1]));
-    ms[p] = t;
-    ss::g_used[p] = false;
+    ms[p] = t;  // (g_used stays set: graph replays re-record the same events)
   }
   return SS_OK;
 }

@@ -354,7 +354,8 @@ class Stage1Trainer:
             return
         buf = target if target is not None else (self._staging if staged else None)
         key = (view, None if buf is None else buf.data_ptr(), int(self.s.accumulate_stats),
-               bool(adam), float(grad_scale), bool(defer_scatter))
+               bool(adam), float(grad_scale), bool(defer_scatter),
+               int(self.lib.ss_profile_enabled()))  # profiled graphs hold event nodes
         self._replay(key, lambda: self._iterate_eager(view, grad_scale, adam, staged, target))
 
     def _replay(self, key, launch) -> None:
