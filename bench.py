@@ -352,9 +352,11 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    backend = os.environ.get("SS_DIST_BACKEND", "nccl")  # gloo: functional tests only
+    if backend == "gloo":  # (ranks may then share a GPU; never a measurement)
+        local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if world > 1:
-        backend = os.environ.get("SS_DIST_BACKEND", "nccl")  # gloo: functional tests only
         dist.init_process_group(backend, device_id=torch.device("cuda", local)
                                 if backend == "nccl" else None)
     from paper_2403_01444_b200 import _lib

@@ -326,9 +326,69 @@ def gen_stage2(R):
                         rng_seed=11)
 
 
+def gen_stage1_loop(R):
+    """The reference's own Stage-1 loop: process_frame (pipeline.py:238-283)
+    with stage2_iterations = 0, run unmodified; observers on ViewspaceStats.add
+    and on the rasterize_forward it calls record the view order and the
+    last-epoch statistics window (pipeline.py:251-279, adaptive.py:79-97)."""
+    import sys
+
+    if rb.REF_SRC not in sys.path:
+        sys.path.insert(0, rb.REF_SRC)
+    from splatstream import adaptive, pipeline
+
+    from oracle import stage1 as O
+
+    sc = scenes.small_scene(seed=31, n=1200, width=64, height=48, sh_degree=1, n_views=4)
+    cloud, grid = sc.cloud, sc.grid
+    tables, mlp = O.init_ntc(grid, hidden_dim=64, output_init="random", seed=6)
+    tables = scenes.f32(np.random.default_rng(707).uniform(-0.05, 0.05, size=tables.shape))
+    cache = rb.ref_cache(R, grid, tables, mlp)
+    cams = [rb.ref_camera(R, c) for c in sc.cameras]
+    moved = scenes.moved_cloud(cloud, np.random.default_rng(98), deg=2.5, shift=(0.02, 0.0, -0.01))
+    targets = [R["rasterizer"].rasterize_forward(rb.ref_cloud(R, moved), c)[0].image for c in cams]
+    views = list(zip(cams, targets))
+    cfg = pipeline.PipelineConfig(stage1_iterations=10, stage2_iterations=0, seed=5,
+                                  grid=rb.ref_grid(R, grid))
+    frame_index = 3
+    seen, stats_obj = [], []
+    orig_raster, orig_add = pipeline.rasterize_forward, adaptive.ViewspaceStats.add
+
+    def raster_observer(cloud_, camera, *a, **k):
+        seen.append(next(i for i, c in enumerate(cams) if c is camera))
+        return orig_raster(cloud_, camera, *a, **k)
+
+    def add_observer(self, norms, contributed):
+        stats_obj[:] = [self]
+        return orig_add(self, norms, contributed)
+
+    pipeline.rasterize_forward = raster_observer
+    adaptive.ViewspaceStats.add = add_observer
+    try:
+        record, transformed, summary = pipeline.process_frame(rb.ref_cloud(R, cloud), cache, views,
+                                                              cfg, frame_index)
+    finally:
+        pipeline.rasterize_forward = orig_raster
+        adaptive.ViewspaceStats.add = orig_add
+    it = cfg.stage1_iterations
+    order = np.array(seen[:it])  # then the train-PSNR renders of every view
+    st = stats_obj[0]
+    np.savez_compressed(os.path.join(OUT, "stage1_loop.npz"), **_cloud_arr(cloud), **_grid_arr(grid),
+                        tables=tables, **{f"mlp_w{i}": w for i, w in enumerate(mlp["weights"])},
+                        **{f"mlp_b{i}": b for i, b in enumerate(mlp["biases"])},
+                        **{k: v for i, c in enumerate(sc.cameras) for k, v in _cam_arr(c, f"cam{i}_").items()},
+                        **{f"target{i}": t for i, t in enumerate(targets)},
+                        n_views=len(cams), iterations=it, seed=cfg.seed, frame_index=frame_index,
+                        view_order=order, losses=np.array(summary.stage1_losses),
+                        stats_norm=st.norm_accum, stats_count=st.view_count,
+                        ntc_blob=np.frombuffer(record.ntc_blob, dtype=np.uint8),
+                        out_means=transformed.means, out_rotations=transformed.rotations,
+                        out_sh=transformed.sh)
+
+
 GENERATORS = dict(encode=gen_encode, ntc=gen_ntc, transform=gen_transform, raster=gen_raster,
                   loss=gen_loss, stage1=gen_stage1, ntc_blob=gen_ntc_blob, warmup=gen_warmup, playback=gen_playback,
-                  stage2=gen_stage2)
+                  stage2=gen_stage2, stage1_loop=gen_stage1_loop)
 
 
 def main():
