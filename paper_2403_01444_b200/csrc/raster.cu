@@ -681,8 +681,8 @@ constexpr float kNearBand = 4.3284e-4f;  // log2(1 + 1e-4) - log2(1 - 2e-4), rou
 // One staged splat of a blend batch: everything the inner loop reads (64 B:
 // three vector loads per splat, the rank only on rare paths)
 struct __align__(16) SplatRec {
-  float4 L;    // lg0, gx, gy, reject threshold
-  float4 Q;    // A, B, C, band: bound of |lg_fp32 - lg| over the tile
+  float4 L;    // lg0, gx, gy, lo: reject below lo = thr - band
+  float4 Q;    // A, B, C, hi: float64 decision below hi = thr + kNearBand + band
   float4 col;  // rgb, opacity
   int rank, pad0, pad1, pad2;
 };
@@ -698,24 +698,29 @@ __device__ __forceinline__ void stage_splat(const Geom& g, int r, int x0, int y0
   const float lg0 = (float)(kq * (c.x * dx * dx + c.y * dx * dy + c.z * dy * dy));
   const float gx = (float)(kq * (2.0 * c.x * dx + c.y * dy));
   const float gy = (float)(kq * (c.y * dx + 2.0 * c.z * dy));
-  // coefficient rounding (1 eps) + five rounded FMAs whose partial sums are all
-  // bounded by S (5 eps), with headroom: 8 eps
+  // band = bound of |lg_fp32 - lg| over the tile: coefficient rounding (1 eps)
+  // + five rounded FMAs whose partial sums are all bounded by S (5 eps), with
+  // headroom: 8 eps
   constexpr float h = (float)c0;
   const float S = fabsf(lg0) + (fabsf(gx) + fabsf(gy)) * h +
                   (fabsf(q.x) + fabsf(q.y) + fabsf(q.z)) * h * h;
-  rec.L = make_float4(lg0, gx, gy, q.w);
-  rec.Q = make_float4(q.x, q.y, q.z, 4.8e-7f * S + 1e-30f);
+  const float band = 4.8e-7f * S + 1e-30f;
+  rec.L = make_float4(lg0, gx, gy, q.w - band);
+  rec.Q = make_float4(q.x, q.y, q.z, q.w + (kNearBand + band));
   rec.col = g.r_color[r];
   rec.rank = r;
 }
 
-// per-thread pixel constants: offsets from the tile centre and their products
+// per-thread pixel constants: offsets from the tile centre (k + 1/2, exact)
 template <int TS, int PPT>
 struct PixelOffsets {
-  float dx[PPT], dy[PPT], xx[PPT], xy[PPT], yy[PPT];
+  float dx[PPT], dy[PPT];
   __device__ __forceinline__ void init(int t);
+  // lg = (A dx + B dy + gx) dx + (C dy + gy) dy + lg0: five FMAs
   __device__ __forceinline__ float lg(const float4& L, const float4& Q, int p) const {
-    return fmaf(Q.x, xx[p], fmaf(Q.y, xy[p], fmaf(Q.z, yy[p], fmaf(L.y, dx[p], fmaf(L.z, dy[p], L.x)))));
+    const float t1 = fmaf(Q.y, dy[p], fmaf(Q.x, dx[p], L.y));
+    const float t2 = fmaf(Q.z, dy[p], L.z);
+    return fmaf(t2, dy[p], fmaf(t1, dx[p], L.x));
   }
 };
 
@@ -751,11 +756,8 @@ __device__ __forceinline__ void PixelOffsets<TS, PPT>::init(int t) {
 #pragma unroll
   for (int p = 0; p < PPT; ++p) {
     const int li = tile_pixel<TS>(t, p);
-    dx[p] = (float)(li % TS) - c0;  // k + 1/2: the products below are exact
+    dx[p] = (float)(li % TS) - c0;
     dy[p] = (float)(li / TS) - c0;
-    xx[p] = dx[p] * dx[p];
-    xy[p] = dx[p] * dy[p];
-    yy[p] = dy[p] * dy[p];
   }
 }
 
@@ -817,7 +819,7 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_fwd_kernel(
     for (int k = 0; k < cnt; ++k) {
       if (!TOUCH) {  // fast path: reject on the log2 form before the exponential
         const float4 L = s_sp[k].L, Q = s_sp[k].Q;
-        const float qlo = L.w - Q.w, qhi = L.w + (kNearBand + Q.w);
+        const float qlo = L.w, qhi = Q.w;
         float lgs[PPT];
         bool live[PPT], any_live = false, any_near = false;
 #pragma unroll
@@ -982,7 +984,7 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_bwd_kernel(
     for (int k = 0; k < cnt; ++k) {
       const int pos_rel = end - 1 - k - range.x;
       const float4 L = s_sp[k].L, Q = s_sp[k].Q;
-      const float qlo = L.w - Q.w, qhi = L.w + (kNearBand + Q.w);
+      const float qlo = L.w, qhi = Q.w;
       // cheap part for every pixel, then a warp-uniform skip; the rest is
       // predicated (a = 0 makes every update a no-op) instead of branching
       float lgs[PPT];
