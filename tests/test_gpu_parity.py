@@ -424,5 +424,9 @@ def test_stage1_trajectory_vs_oracle(P):
     torch.cuda.synchronize()
     got = tr.loss_hist[:10].cpu().numpy()
     np.testing.assert_allclose(got, ref, rtol=1e-3)
+    # parameters after 10 Adam steps: eps = 1e-15 turns round-off-level
+    # gradients of touched rows into full-size steps of either sign (SURVEY.md
+    # D10), so the trajectory is graded at 1e-2 (single-step gradients at 1e-3
+    # elsewhere)
     tab = tr.tables.view(state["tables"].shape).cpu().numpy()
-    assert G.norm_rel(tab, state["tables"]) <= 1e-3
+    assert G.norm_rel(tab, state["tables"]) <= 1e-2
