@@ -515,6 +515,7 @@ def main():
     if not a.no_extras:
         line["cfg3"] = cfg3_rate(a, torch, dist, rank, world, flush)
     if rank == 0 and world == 1 and not a.no_extras:
+        line["cfg4"] = cfg4_rate(a)
         line["render"] = render_fps(a)
         line["ntc_warmup"] = warmup_rate(sc, cache)
         line["stage2"] = stage2_rate(sc, targets)
@@ -587,6 +588,45 @@ def cfg3_rate(a, torch, dist, rank, world, flush):
                        f"{world} rank(s), NTC gradient all-reduced per iteration "
                        f"(iterations 0..{k - 1} of the frame, L2 flushed between them)"}
     del vs
+    torch.cuda.empty_cache()
+    return out
+
+
+def cfg4_rate(a):
+    """BASELINE config 4: 3M SH-3 Gaussians at 3840x2160 (T = 2^19 NTC), one
+    Stage-1 iteration per view (forward, loss, backward, NTC gradients, Adam)
+    through the banded path: the view's pair count is read on the host and the
+    view is binned and blended in bands of tile rows (bin workspace of
+    rasterizer.BIN_PAIR_LIMIT pairs)."""
+    import torch
+
+    from paper_2403_01444_b200 import rasterizer
+    from paper_2403_01444_b200.stage1 import Stage1Config, Stage1Trainer
+
+    sc, cache, targets = build_problem(4)
+    tr = Stage1Trainer(sc.cloud, cache, list(zip(sc.cameras, targets)), Stage1Config())
+    pairs = tr.begin(0)
+    tr.finish(0, pairs)  # warm-up (workspace, first launches)
+    torch.cuda.synchronize()
+    ms, counts = [], []
+    for v in range(min(len(sc.cameras), max(2, a.steps // 10))):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        p = tr.begin(v)  # (reads the pair count: a host synchronisation inside the window)
+        tr.finish(v, p)
+        e1.record()
+        torch.cuda.synchronize()
+        ms.append(e0.elapsed_time(e1))
+        counts.append(p)
+    m = float(np.mean(ms))
+    out = {"metric": "cfg4_stage1_iters_per_s", "value": 1000.0 / m, "unit": "iter/s",
+           "ms_per_iteration": m, "tile_pairs_per_view": [int(c) for c in counts],
+           "bin_workspace_pairs": int(tr.bin_capacity),
+           "bands": [int(-(-c // rasterizer.BIN_PAIR_LIMIT)) for c in counts],
+           "workload": f"cfg4: {len(sc.cloud['means'])} SH-3 Gaussians (16 clusters, "
+                       f"anisotropy <= 10:1), 3840x2160, NTC 2^19 rows; one view per iteration "
+                       f"on 1 GPU (the 8-views-over-8-GPUs batch is the view-sharded path)"}
+    del tr
     torch.cuda.empty_cache()
     return out
 

@@ -227,6 +227,21 @@ int ss_raster_forward_finish(const ss_cloud* cloud, const ss_camera* cam,
                              int64_t n_pairs, float* image, float* alpha_map, int32_t* touch,
                              void* stream);
 
+/* The same two calls for views whose pairs exceed the bin workspace (configs
+ * with billions of tile pairs): the bins hold bin_capacity pairs
+ * (ss_raster_bin_bytes(bin_capacity, ...)) and n_pairs is the view's count from
+ * ss_raster_forward_begin; above the capacity the view is binned and blended
+ * in bands of tile rows, each at most bin_capacity pairs (synchronises the
+ * stream once per call to plan the bands; the backward bins each band again). */
+int ss_raster_forward_finish_banded(const ss_cloud* cloud, const ss_camera* cam,
+                                    const ss_raster_settings* s, void* geom, void* bins,
+                                    int64_t bin_capacity, int64_t n_pairs, float* image,
+                                    float* alpha_map, int32_t* touch, void* stream);
+int ss_raster_backward_banded(const ss_cloud* cloud, const ss_camera* cam,
+                              const ss_raster_settings* s, void* geom, void* bins,
+                              int64_t bin_capacity, int64_t n_pairs, const float* d_image,
+                              const ss_cloud_grads* grads, void* stream);
+
 /* rasterize_backward (rasterizer.py:284-402).  Output arrays are written for
  * survivors only: caller zeroes them.  opacity_and_scales=0 skips
  * d_opacity_logits / d_log_scales work (Stage 1 consumes neither). */
@@ -340,7 +355,8 @@ int ss_stage1_iter_begin(ss_stage1* st, const ss_camera* cam, int64_t* counts_ho
 int ss_stage1_iter_finish(ss_stage1* st, const ss_camera* cam, const float* target,
                           int64_t n_pairs, void* stream);
 /* Part B up to (and including) the NTC gradients but without the Adam step
- * (view-sharded data parallelism all-reduces g_tables/g_params in between). */
+ * (view-sharded data parallelism all-reduces g_tables/g_params in between).
+ * n_pairs > bin_capacity (the count from part A): binned in bands of tile rows. */
 int ss_stage1_iter_grads(ss_stage1* st, const ss_camera* cam, const float* target,
                          int64_t n_pairs, float grad_scale, void* stream);
 int ss_stage1_apply_adam(ss_stage1* st, void* stream);

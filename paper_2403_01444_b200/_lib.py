@@ -117,6 +117,9 @@ SIGNATURES = [
     ("ss_raster_forward_begin", I32, [PCloud, PCam, PSet, P, P, P]),
     ("ss_raster_forward_finish", I32, [PCloud, PCam, PSet, P, P, I64, P, P, P, P]),
     ("ss_raster_backward", I32, [PCloud, PCam, PSet, P, P, I64, P, C.POINTER(CloudGrads), P]),
+    ("ss_raster_forward_finish_banded", I32, [PCloud, PCam, PSet, P, P, I64, I64, P, P, P, P]),
+    ("ss_raster_backward_banded", I32, [PCloud, PCam, PSet, P, P, I64, I64, P,
+                                        C.POINTER(CloudGrads), P]),
     ("ss_raster_tile_lists", I32, [PCam, PSet, P, P, I64, I64, P, P, P, P]),
     ("ss_tile_bin_begin", I32, [I64, P, P, P, PCam, PSet, P, P, P]),
     ("ss_tile_bin_finish", I32, [I64, PCam, PSet, P, P, I64, P, P, P]),

@@ -214,15 +214,18 @@ inline cudaError_t smem_attr_once(K* kernel, int bytes) {
 namespace ss {
 int raster_begin(const ss_cloud* cl, const ss_camera* cam, const ss_raster_settings* s,
                  void* geom, int64_t* counts_host, cudaStream_t st);
+// cap: pairs the bins workspace holds; total: the view's pairs if known on the
+// host (above cap: binned and blended in bands of tile rows), else <= cap
 int raster_finish(const ss_cloud* cl, const ss_camera* cam, const ss_raster_settings* s,
-                  void* geom, void* bins, int64_t pairs, float* image, float* alpha,
-                  int32_t* touch, uint32_t* status, int cull, cudaStream_t st);
+                  void* geom, void* bins, int64_t cap, float* image, float* alpha,
+                  int32_t* touch, uint32_t* status, int cull, cudaStream_t st, int64_t total);
 // device pointer to [survivors, pairs] of the last raster_begin on `geom`
 const int64_t* raster_counts(void* geom, int64_t n, const ss_camera* cam,
                              const ss_raster_settings* s);
 int raster_backward(const ss_cloud* cl, const ss_camera* cam, const ss_raster_settings* s,
-                    void* geom, void* bins, int64_t pairs, const float* d_image,
-                    const ss_cloud_grads* grads, int full, cudaStream_t st);
+                    void* geom, void* bins, int64_t cap, const float* d_image,
+                    const ss_cloud_grads* grads, int full, cudaStream_t st, int64_t total,
+                    int cull, uint32_t* status);
 }  // namespace ss
 
 // ---------------------------------------------------------------- phase timing

@@ -6,6 +6,7 @@
 // Reference: rasterizer.py:107-402, cameras.py:132-178, sh.py:51-81,
 // gaussians.py:120-154 (/root/reference/pkg/src/splatstream/).
 #include <cub/cub.cuh>
+#include <vector>
 
 #include "common.cuh"
 
@@ -36,7 +37,9 @@ struct Geom {
   float* t_final;    // per pixel
   int32_t* n_contrib;
   int2* ranges;      // per tile
-  int64_t* dev_counts;  // [survivors, pairs, n]
+  int64_t* dev_counts;  // [survivors, pairs, n, band pairs]
+  int64_t* band_off;    // per rank, prefix of the pairs inside the current band of tile rows
+  unsigned long long* row_pairs;  // per tile row: pairs of every visible rectangle
   BinSortWS dsort;      // depth sort workspace
   void* cub_scan;
   size_t cub_scan_bytes;
@@ -91,7 +94,9 @@ static Geom plan_geom(void* base, int64_t n, const ss_camera* cam, const ss_rast
   g.t_final = c.take<float>(P);
   g.n_contrib = c.take<int32_t>(P);
   g.ranges = c.take<int2>(NT);
-  g.dev_counts = c.take<int64_t>(3);
+  g.dev_counts = c.take<int64_t>(4);
+  g.band_off = c.take<int64_t>(nn + 1);
+  g.row_pairs = c.take<unsigned long long>((size_t)ntiles_y(cam, s));
   g.dsort = binsort_plan(c, nn, 4);
   size_t qb = 0;
   cub::DeviceScan::InclusiveSum(nullptr, qb, (const int64_t*)nullptr, (int64_t*)nullptr,
@@ -490,6 +495,43 @@ __global__ void finish_counts_kernel(Geom g, int64_t n) {
   g.dev_counts[1] = n > 0 ? g.offsets[n] : 0;
 }
 
+// ---- tile-row bands: a view whose pairs exceed the bin workspace is binned
+// and blended one band of tile rows at a time (host-driven, synchronous)
+__global__ void row_pairs_kernel(int64_t n, Geom g, int nty) {
+  extern __shared__ unsigned long long s_rows[];
+  for (int i = threadIdx.x; i < nty; i += blockDim.x) s_rows[i] = 0;
+  __syncthreads();
+  const int64_t V = g.dev_counts[0];
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < min(n, V);
+       r += (int64_t)gridDim.x * blockDim.x) {
+    if (g.offsets[r + 1] == g.offsets[r]) continue;  // not visible
+    const int4 rc = g.r_rect[r];
+    const unsigned long long wx = (unsigned long long)(rc.y - rc.x + 1);
+    for (int ty = rc.z; ty <= rc.w; ++ty) atomicAdd(&s_rows[ty], wx);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < nty; i += blockDim.x)
+    if (s_rows[i]) atomicAdd(&g.row_pairs[i], s_rows[i]);
+}
+
+// pairs of each rank inside tile rows [ty_lo, ty_hi) (band_off[r], scanned later)
+__global__ void band_counts_kernel(int64_t n, Geom g, int ty_lo, int ty_hi) {
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  int64_t c = 0;
+  if (r < g.dev_counts[0] && g.offsets[r + 1] > g.offsets[r]) {
+    const int4 rc = g.r_rect[r];
+    const int rows = min(rc.w, ty_hi - 1) - max(rc.z, ty_lo) + 1;
+    c = rows > 0 ? (int64_t)(rc.y - rc.x + 1) * rows : 0;
+  }
+  g.band_off[r] = c;
+}
+
+__global__ void band_finish_kernel(Geom g, int64_t n) {
+  g.band_off[0] = 0;
+  g.dev_counts[3] = n > 0 ? g.band_off[n] : 0;
+}
+
 // K4c (render path) tile cull:
 // near-camera splats can cover thousands of tiles).  The owning rank is the last
 // r with offsets[r] <= j (zero-count ranks are skipped by construction).
@@ -546,23 +588,26 @@ __device__ inline int64_t block_owner_rank(const int64_t* __restrict__ off, int6
 __global__ void __launch_bounds__(256) duplicate_kernel(int ntx, int64_t n, Geom g, Bins b,
                                                         uint32_t* kdst, uint32_t* vdst,
                                                         uint32_t* status, int cull, int ts, int W,
-                                                        int H, uint32_t sentinel, int key_bits) {
+                                                        int H, uint32_t sentinel, int key_bits,
+                                                        const int64_t* __restrict__ offs,
+                                                        const int64_t* __restrict__ d_count,
+                                                        int ty_lo) {
   constexpr int CH = 1024, SOFF = 2048;
   __shared__ int64_t s_off[SOFF];
   __shared__ uint32_t s_hist[2][256];  // binsort digit histograms of the emitted keys
   for (int i = threadIdx.x; i < 512; i += blockDim.x) (&s_hist[0][0])[i] = 0;
-  const int64_t count = g.dev_counts[1];
+  const int64_t count = *d_count;
   if (count > b.capacity && blockIdx.x == 0 && threadIdx.x == 0 && status)
     atomicOr(status, SS_FLAG_OVERFLOW);
   const int64_t pairs = min(count, b.capacity);
   for (int64_t j0 = (int64_t)blockIdx.x * CH; j0 < pairs; j0 += (int64_t)gridDim.x * CH) {
     __syncthreads();  // the previous chunk is done with s_off
-    const int64_t rlo = block_owner_rank(g.offsets, 0, n, j0);
-    const int64_t rhi = block_owner_rank(g.offsets, rlo, n, min(j0 + CH, pairs) - 1) + 1;
+    const int64_t rlo = block_owner_rank(offs, 0, n, j0);
+    const int64_t rhi = block_owner_rank(offs, rlo, n, min(j0 + CH, pairs) - 1) + 1;
     // the chunk's owning ranks' offsets staged in shared memory when they fit
     const bool staged = rhi - rlo + 1 <= SOFF;
     if (staged)
-      for (int64_t r = rlo + threadIdx.x; r <= rhi; r += blockDim.x) s_off[r - rlo] = g.offsets[r];
+      for (int64_t r = rlo + threadIdx.x; r <= rhi; r += blockDim.x) s_off[r - rlo] = offs[r];
     __syncthreads();
     for (int64_t j = j0 + threadIdx.x; j < min(j0 + CH, pairs); j += blockDim.x) {
       int64_t lo;
@@ -574,12 +619,12 @@ __global__ void __launch_bounds__(256) duplicate_kernel(int ntx, int64_t n, Geom
         }
         lo = rlo + a;
       } else {
-        lo = owner_rank(g.offsets, rlo, rhi, j);
+        lo = owner_rank(offs, rlo, rhi, j);
       }
       const int4 rc = g.r_rect[lo];
       const int wx = rc.y - rc.x + 1;
-      const int local = (int)(j - (staged ? s_off[lo - rlo] : g.offsets[lo]));
-      const int ty = rc.z + local / wx, tx = rc.x + local % wx;
+      const int64_t local = j - (staged ? s_off[lo - rlo] : offs[lo]);
+      const int ty = max(rc.z, ty_lo) + (int)(local / wx), tx = rc.x + (int)(local % wx);
       uint32_t key = (uint32_t)(ty * ntx + tx);
       if (cull) {
         const double xa = tx * ts, xb = min(tx * ts + ts, W) - 1, ya = ty * ts,
@@ -608,11 +653,16 @@ __global__ void ranges_kernel(const int64_t* __restrict__ d_pairs, int64_t cap,
   }
 }
 
-// duplicate -> stable tile sort -> per-tile ranges, all driven by the device count
+// duplicate -> stable tile sort -> per-tile ranges, all driven by the device
+// count *d_count of the pairs listed by `offs` (the whole view, or one band of
+// tile rows starting at ty_lo)
 static int bin_pairs(const ss_camera* cam, const ss_raster_settings* s, int64_t n, Geom& g,
-                     Bins& b, uint32_t* status, int cull, cudaStream_t st) {
+                     Bins& b, uint32_t* status, int cull, cudaStream_t st,
+                     const int64_t* offs = nullptr, const int64_t* d_count = nullptr,
+                     int ty_lo = 0) {
   const int ntx = ntiles_x(cam, s), nty = ntiles_y(cam, s);
   const int64_t ntiles = (int64_t)ntx * nty;
+  if (!offs) offs = g.offsets, d_count = g.dev_counts + 1;
   cull = cull && s->skip_alpha > 0.0;
   const int kb = key_bits(cull ? ntiles + 1 : ntiles);
   const bool two = binsort_passes(kb) == 2;
@@ -623,20 +673,65 @@ static int bin_pairs(const ss_camera* cam, const ss_raster_settings* s, int64_t 
                                                                          148 * 8));
   duplicate_kernel<<<dgrid, 256, 0, st>>>(ntx, n, g, b, two ? b.keys_out : b.keys_in,
                                           two ? b.vals_out : b.vals_in, status, cull, s->tile_size,
-                                          cam->width, cam->height, (uint32_t)ntiles, kb);
+                                          cam->width, cam->height, (uint32_t)ntiles, kb, offs,
+                                          d_count, ty_lo);
   SS_CHECK_LAUNCH("duplicate_kernel");
   prof_end(PH_DUPLICATE, st);
   prof_begin(PH_TILE_SORT, st);
-  SS_TRY(binsort_run(b.sort, b.keys_in, b.vals_in, b.keys_out, b.vals_out, g.dev_counts + 1,
-                     b.capacity, kb, st, /*hist_ready=*/true));
+  SS_TRY(binsort_run(b.sort, b.keys_in, b.vals_in, b.keys_out, b.vals_out, d_count, b.capacity, kb,
+                     st, /*hist_ready=*/true));
   g_launches.fetch_add(two ? 2 : 1);
   prof_end(PH_TILE_SORT, st);
   prof_begin(PH_RANGES, st);
-  ranges_kernel<<<stride_grid(b.capacity), 256, 0, st>>>(g.dev_counts + 1, b.capacity, b.keys_out,
+  ranges_kernel<<<stride_grid(b.capacity), 256, 0, st>>>(d_count, b.capacity, b.keys_out,
                                                          g.ranges, (uint32_t)ntiles);
   SS_CHECK_LAUNCH("ranges_kernel");
   prof_end(PH_RANGES, st);
   return SS_OK;
+}
+
+// Bands of tile rows whose pairs fit `cap` (host side, after raster_begin):
+// per-row pair totals, then a greedy split.  Synchronises the stream.
+static int plan_bands(const ss_camera* cam, const ss_raster_settings* s, int64_t n, Geom& g,
+                      int64_t cap, std::vector<int2>& bands, cudaStream_t st) {
+  const int nty = ntiles_y(cam, s);
+  SS_CUDA(cudaMemsetAsync(g.row_pairs, 0, nty * sizeof(unsigned long long), st));
+  row_pairs_kernel<<<stride_grid(n), 256, nty * sizeof(unsigned long long), st>>>(n, g, nty);
+  SS_CHECK_LAUNCH("row_pairs_kernel");
+  std::vector<unsigned long long> rows(nty);
+  SS_CUDA(cudaMemcpyAsync(rows.data(), g.row_pairs, nty * sizeof(unsigned long long),
+                          cudaMemcpyDeviceToHost, st));
+  SS_CUDA(cudaStreamSynchronize(st));
+  bands.clear();
+  int lo = 0;
+  unsigned long long acc = 0;
+  for (int ty = 0; ty < nty; ++ty) {
+    if (rows[ty] > (unsigned long long)cap) {
+      set_error("one tile row holds more pairs than the bin workspace");
+      return SS_ERR_CAPACITY;
+    }
+    if (acc + rows[ty] > (unsigned long long)cap) {
+      bands.push_back(make_int2(lo, ty));
+      lo = ty;
+      acc = 0;
+    }
+    acc += rows[ty];
+  }
+  bands.push_back(make_int2(lo, nty));
+  return SS_OK;
+}
+
+// list the pairs of band [ty_lo, ty_hi) (band_off, dev_counts[3]) and bin them
+static int bin_band(const ss_camera* cam, const ss_raster_settings* s, int64_t n, Geom& g, Bins& b,
+                    uint32_t* status, int cull, int2 band, cudaStream_t st) {
+  band_counts_kernel<<<(unsigned)cdiv(n, 256), 256, 0, st>>>(n, g, band.x, band.y);
+  SS_CHECK_LAUNCH("band_counts_kernel");
+  size_t qb = g.cub_scan_bytes;
+  SS_CUDA(cub::DeviceScan::InclusiveSum(g.cub_scan, qb, g.band_off, g.band_off + 1, (int)n, st));
+  g_launches.fetch_add(2);
+  band_finish_kernel<<<1, 1, 0, st>>>(g, n);
+  SS_CHECK_LAUNCH("band_finish_kernel");
+  return bin_pairs(cam, s, n, g, b, status, cull, st, g.band_off, g.dev_counts + 3, band.x);
 }
 
 // ------------------------------------------------------------------ blend
@@ -769,13 +864,13 @@ __device__ __forceinline__ void PixelOffsets<TS, PPT>::init(int t) {
 template <int TS, bool TOUCH>
 __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_fwd_kernel(
     BlendParams bp, Geom g, const uint32_t* __restrict__ vals, float* __restrict__ image,
-    float* __restrict__ alpha_map, int32_t* __restrict__ touch) {
+    float* __restrict__ alpha_map, int32_t* __restrict__ touch, int tile0) {
   constexpr int NT = BlendShape<TS>::NT, PPT = BlendShape<TS>::PPT;
   __shared__ SplatRec s_sp[NT];
   __shared__ double2 s_md[TOUCH ? NT : 1];  // float64 mean (TOUCH)
   __shared__ double4 s_cd[TOUCH ? NT : 1];  // float64 conic (c00, c01 + c10, c11) + opacity
   __shared__ int s_touch[TOUCH ? NT : 1];
-  const int tile = blockIdx.x;
+  const int tile = tile0 + blockIdx.x;
   const int x0 = (tile % bp.ntx) * TS, y0 = (tile / bp.ntx) * TS;
   const int2 range = g.ranges[tile];
   PixelOffsets<TS, PPT> po;
@@ -925,7 +1020,8 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_fwd_kernel(
 // the per-rank global accumulators once per batch.
 template <int TS>
 __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_bwd_kernel(
-    BlendParams bp, Geom g, const uint32_t* __restrict__ vals, const float* __restrict__ d_image) {
+    BlendParams bp, Geom g, const uint32_t* __restrict__ vals, const float* __restrict__ d_image,
+    int tile0) {
   constexpr int NT = BlendShape<TS>::NT, PPT = BlendShape<TS>::PPT;
   constexpr int NA = 9;  // colour 3, M1 2, M2 3, M0
   __shared__ SplatRec s_sp[NT];
@@ -937,7 +1033,7 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_bwd_kernel(
   __shared__ int s_any[NT];
   __shared__ int s_last;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int tile = blockIdx.x;
+  const int tile = tile0 + blockIdx.x;
   const int tx = tile % bp.ntx, ty = tile / bp.ntx;
   const int x0 = tx * TS, y0 = ty * TS;
   const int2 range = g.ranges[tile];
@@ -1327,26 +1423,27 @@ static int check_raster(const ss_cloud* cl, const ss_camera* cam, const ss_raste
 template <bool TOUCH>
 static int launch_blend_fwd(int ts, int64_t ntiles, cudaStream_t st, const BlendParams& bp,
                             const Geom& g, const uint32_t* vals, float* image, float* alpha,
-                            int32_t* touch) {
+                            int32_t* touch, int tile0 = 0) {
   const unsigned grid = (unsigned)ntiles;
   switch (ts) {
-    case 8: blend_fwd_kernel<8, TOUCH><<<grid, BlendShape<8>::NT, 0, st>>>(bp, g, vals, image, alpha, touch); break;
-    case 16: blend_fwd_kernel<16, TOUCH><<<grid, BlendShape<16>::NT, 0, st>>>(bp, g, vals, image, alpha, touch); break;
-    case 32: blend_fwd_kernel<32, TOUCH><<<grid, BlendShape<32>::NT, 0, st>>>(bp, g, vals, image, alpha, touch); break;
-    default: blend_fwd_kernel<64, TOUCH><<<grid, BlendShape<64>::NT, 0, st>>>(bp, g, vals, image, alpha, touch); break;
+    case 8: blend_fwd_kernel<8, TOUCH><<<grid, BlendShape<8>::NT, 0, st>>>(bp, g, vals, image, alpha, touch, tile0); break;
+    case 16: blend_fwd_kernel<16, TOUCH><<<grid, BlendShape<16>::NT, 0, st>>>(bp, g, vals, image, alpha, touch, tile0); break;
+    case 32: blend_fwd_kernel<32, TOUCH><<<grid, BlendShape<32>::NT, 0, st>>>(bp, g, vals, image, alpha, touch, tile0); break;
+    default: blend_fwd_kernel<64, TOUCH><<<grid, BlendShape<64>::NT, 0, st>>>(bp, g, vals, image, alpha, touch, tile0); break;
   }
   SS_CHECK_LAUNCH("blend_fwd_kernel");
   return SS_OK;
 }
 
 static int launch_blend_bwd(int ts, int64_t ntiles, cudaStream_t st, const BlendParams& bp,
-                            const Geom& g, const uint32_t* vals, const float* d_image) {
+                            const Geom& g, const uint32_t* vals, const float* d_image,
+                            int tile0 = 0) {
   const unsigned grid = (unsigned)ntiles;
   switch (ts) {
-    case 8: blend_bwd_kernel<8><<<grid, BlendShape<8>::NT, 0, st>>>(bp, g, vals, d_image); break;
-    case 16: blend_bwd_kernel<16><<<grid, BlendShape<16>::NT, 0, st>>>(bp, g, vals, d_image); break;
-    case 32: blend_bwd_kernel<32><<<grid, BlendShape<32>::NT, 0, st>>>(bp, g, vals, d_image); break;
-    default: blend_bwd_kernel<64><<<grid, BlendShape<64>::NT, 0, st>>>(bp, g, vals, d_image); break;
+    case 8: blend_bwd_kernel<8><<<grid, BlendShape<8>::NT, 0, st>>>(bp, g, vals, d_image, tile0); break;
+    case 16: blend_bwd_kernel<16><<<grid, BlendShape<16>::NT, 0, st>>>(bp, g, vals, d_image, tile0); break;
+    case 32: blend_bwd_kernel<32><<<grid, BlendShape<32>::NT, 0, st>>>(bp, g, vals, d_image, tile0); break;
+    default: blend_bwd_kernel<64><<<grid, BlendShape<64>::NT, 0, st>>>(bp, g, vals, d_image, tile0); break;
   }
   SS_CHECK_LAUNCH("blend_bwd_kernel");
   return SS_OK;
@@ -1397,28 +1494,44 @@ int raster_begin(const ss_cloud* cl, const ss_camera* cam, const ss_raster_setti
   return SS_OK;
 }
 
+// cap: pairs the `bins` workspace holds; total: the view's pair count when the
+// host knows it (-1: only on the device, single band, overflow flagged).  A
+// known total above cap is binned and blended in bands of tile rows.
 int raster_finish(const ss_cloud* cl, const ss_camera* cam, const ss_raster_settings* s,
-                  void* geom, void* bins, int64_t pairs, float* image, float* alpha,
-                  int32_t* touch, uint32_t* status, int cull, cudaStream_t st) {
+                  void* geom, void* bins, int64_t cap, float* image, float* alpha,
+                  int32_t* touch, uint32_t* status, int cull, cudaStream_t st, int64_t total) {
   SS_TRY(check_raster(cl, cam, s));
   const int64_t n = cl->n;
   Geom g = plan_geom(geom, n, cam, s);
-  Bins b = plan_bins(bins, pairs);
+  Bins b = plan_bins(bins, cap);
   const int ntx = ntiles_x(cam, s), nty = ntiles_y(cam, s);
   const int64_t ntiles = (int64_t)ntx * nty;
-  if (pairs > (int64_t)0x7fffffff) {
-    set_error("more than 2^31 tile pairs in one view");
+  if (cap > (int64_t)0x7fffffff) {
+    set_error("bin workspace above 2^31 pairs: bin in bands of tile rows instead");
     return SS_ERR_CAPACITY;
   }
-  SS_TRY(bin_pairs(cam, s, n, g, b, status, cull, st));
   const BlendParams bp = blend_params(cam, s);
-  prof_begin(PH_BLEND_FWD, st);
-  const int rc = touch ? launch_blend_fwd<true>(s->tile_size, ntiles, st, bp, g, b.vals_out, image,
-                                                alpha, touch)
-                       : launch_blend_fwd<false>(s->tile_size, ntiles, st, bp, g, b.vals_out,
-                                                 image, alpha, nullptr);
-  prof_end(PH_BLEND_FWD, st);
-  return rc;
+  if (total <= cap) {
+    SS_TRY(bin_pairs(cam, s, n, g, b, status, cull, st));
+    prof_begin(PH_BLEND_FWD, st);
+    const int rc = touch ? launch_blend_fwd<true>(s->tile_size, ntiles, st, bp, g, b.vals_out,
+                                                  image, alpha, touch)
+                         : launch_blend_fwd<false>(s->tile_size, ntiles, st, bp, g, b.vals_out,
+                                                   image, alpha, nullptr);
+    prof_end(PH_BLEND_FWD, st);
+    return rc;
+  }
+  std::vector<int2> bands;
+  SS_TRY(plan_bands(cam, s, n, g, cap, bands, st));
+  for (const int2 band : bands) {
+    SS_TRY(bin_band(cam, s, n, g, b, status, cull, band, st));
+    const int64_t nt = (int64_t)(band.y - band.x) * ntx;
+    if (touch) SS_TRY(launch_blend_fwd<true>(s->tile_size, nt, st, bp, g, b.vals_out, image, alpha,
+                                             touch, band.x * ntx));
+    else SS_TRY(launch_blend_fwd<false>(s->tile_size, nt, st, bp, g, b.vals_out, image, alpha,
+                                        nullptr, band.x * ntx));
+  }
+  return SS_OK;
 }
 
 const int64_t* raster_counts(void* geom, int64_t n, const ss_camera* cam,
@@ -1427,20 +1540,32 @@ const int64_t* raster_counts(void* geom, int64_t n, const ss_camera* cam,
 }
 
 int raster_backward(const ss_cloud* cl, const ss_camera* cam, const ss_raster_settings* s,
-                    void* geom, void* bins, int64_t pairs, const float* d_image,
-                    const ss_cloud_grads* grads, int full, cudaStream_t st) {
+                    void* geom, void* bins, int64_t cap, const float* d_image,
+                    const ss_cloud_grads* grads, int full, cudaStream_t st, int64_t total,
+                    int cull, uint32_t* status) {
   SS_TRY(check_raster(cl, cam, s));
   const int64_t n = cl->n;
   if (n == 0) return SS_OK;
   Geom g = plan_geom(geom, n, cam, s);
-  Bins b = plan_bins(bins, pairs);
-  const int64_t ntiles = (int64_t)ntiles_x(cam, s) * ntiles_y(cam, s);
+  Bins b = plan_bins(bins, cap);
+  const int ntx = ntiles_x(cam, s);
+  const int64_t ntiles = (int64_t)ntx * ntiles_y(cam, s);
   SS_CUDA(cudaMemsetAsync(g.acc, 0, n * kAccStride * sizeof(float), st));
   SS_CUDA(cudaMemsetAsync(g.touched, 0, n, st));
-  prof_begin(PH_BLEND_BWD, st);
   const BlendParams bp = blend_params(cam, s);
-  SS_TRY(launch_blend_bwd(s->tile_size, ntiles, st, bp, g, b.vals_out, d_image));
-  prof_end(PH_BLEND_BWD, st);
+  if (total <= cap) {  // the forward's bins are still in the workspace
+    prof_begin(PH_BLEND_BWD, st);
+    SS_TRY(launch_blend_bwd(s->tile_size, ntiles, st, bp, g, b.vals_out, d_image));
+    prof_end(PH_BLEND_BWD, st);
+  } else {  // bin every band again (the workspace holds one band)
+    std::vector<int2> bands;
+    SS_TRY(plan_bands(cam, s, n, g, cap, bands, st));
+    for (const int2 band : bands) {
+      SS_TRY(bin_band(cam, s, n, g, b, status, cull, band, st));
+      SS_TRY(launch_blend_bwd(s->tile_size, (int64_t)(band.y - band.x) * ntx, st, bp, g,
+                              b.vals_out, d_image, band.x * ntx));
+    }
+  }
   prof_begin(PH_GAUSS_BWD, st);
   {
     const unsigned grid = (unsigned)cdiv(n, 128);
@@ -1538,14 +1663,30 @@ int ss_raster_forward_finish(const ss_cloud* cloud, const ss_camera* cam,
                              int64_t n_pairs, float* image, float* alpha_map, int32_t* touch,
                              void* stream) {
   return raster_finish(cloud, cam, s, geom, bins, n_pairs, image, alpha_map, touch, nullptr, 0,
-                       as_stream(stream));
+                       as_stream(stream), n_pairs);
 }
 
 int ss_raster_backward(const ss_cloud* cloud, const ss_camera* cam, const ss_raster_settings* s,
                        void* geom, void* bins, int64_t n_pairs, const float* d_image,
                        const ss_cloud_grads* grads, void* stream) {
   return raster_backward(cloud, cam, s, geom, bins, n_pairs, d_image, grads, 1,
-                         as_stream(stream));
+                         as_stream(stream), n_pairs, 0, nullptr);
+}
+
+int ss_raster_forward_finish_banded(const ss_cloud* cloud, const ss_camera* cam,
+                                    const ss_raster_settings* s, void* geom, void* bins,
+                                    int64_t bin_capacity, int64_t n_pairs, float* image,
+                                    float* alpha_map, int32_t* touch, void* stream) {
+  return raster_finish(cloud, cam, s, geom, bins, bin_capacity, image, alpha_map, touch, nullptr,
+                       0, as_stream(stream), n_pairs);
+}
+
+int ss_raster_backward_banded(const ss_cloud* cloud, const ss_camera* cam,
+                              const ss_raster_settings* s, void* geom, void* bins,
+                              int64_t bin_capacity, int64_t n_pairs, const float* d_image,
+                              const ss_cloud_grads* grads, void* stream) {
+  return raster_backward(cloud, cam, s, geom, bins, bin_capacity, d_image, grads, 1,
+                         as_stream(stream), n_pairs, 0, nullptr);
 }
 
 int ss_tile_bin_begin(int64_t n, const double* mean2d, const double* cov2d, const double* opacity,

@@ -110,14 +110,12 @@ int ss_stage1_iter_begin(ss_stage1* st, const ss_camera* cam, int64_t* counts_ho
 int ss_stage1_iter_grads(ss_stage1* st, const ss_camera* cam, const float* target,
                          int64_t n_pairs, float grad_scale, void* stream) {
   cudaStream_t s = as_stream(stream);
-  if (n_pairs > st->bin_capacity) {
-    set_error("tile-pair workspace too small");
-    return SS_ERR_CAPACITY;
-  }
+  // n_pairs above the workspace: the host-known count selects binning in bands
+  // of tile rows (synchronous); otherwise the device count drives one band
   const int64_t cap = st->bin_capacity;
   const ss_cloud tc = transformed(st);
   SS_TRY(raster_finish(&tc, cam, &st->settings, st->geom, st->bins, cap, st->image,
-                       st->alpha_map, nullptr, st->status, 1, s));
+                       st->alpha_map, nullptr, st->status, 1, s, n_pairs));
   SS_TRY(ss_render_loss(st->image, target, cam->height, cam->width, 3, st->lambda_dssim,
                         st->ssim_c1, st->ssim_c2, st->loss_scratch, st->loss_dev, st->d_image,
                         st->status, stream));
@@ -144,7 +142,7 @@ int ss_stage1_iter_grads(ss_stage1* st, const ss_camera* cam, const float* targe
   gr.viewspace = st->viewspace;
   gr.contributed = st->contributed;
   SS_TRY(raster_backward(&tc, cam, &st->settings, st->geom, st->bins, cap, st->d_image, &gr, 0,
-                         s));
+                         s, n_pairs, 1, st->status));
   if (st->accumulate_stats && st->stats_norm && st->stats_count) {
     const int64_t n = st->src.n;
     stats_kernel<<<(unsigned)cdiv(n, 256), 256, 0, s>>>(n, st->viewspace, st->contributed,
@@ -187,7 +185,7 @@ int ss_stage1_render(ss_stage1* st, const ss_camera* cam, void* stream) {
   SS_TRY(ss_stage1_iter_begin(st, cam, nullptr, stream));
   const ss_cloud tc = transformed(st);
   return raster_finish(&tc, cam, &st->settings, st->geom, st->bins, st->bin_capacity, st->image,
-                       st->alpha_map, nullptr, st->status, 1, as_stream(stream));
+                       st->alpha_map, nullptr, st->status, 1, as_stream(stream), 0);
 }
 
 int ss_stage1_iter(ss_stage1* st, const ss_camera* cam, const float* target, float grad_scale,

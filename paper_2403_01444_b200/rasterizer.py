@@ -9,6 +9,7 @@ lazily on attribute access.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -22,6 +23,11 @@ from .types import Camera, GaussianCloud, RasterSettings
 
 __all__ = ["RasterSettings", "RenderOutput", "GradientBuffer", "RenderContext", "tile_bin",
            "rasterize_forward", "rasterize_backward"]
+
+# Tile pairs one bin workspace holds.  A view with more pairs (config 4: 3M
+# Gaussians at 3840x2160, billions of pairs) is binned and blended in bands of
+# tile rows of at most this many pairs (ss_raster_*_banded).
+BIN_PAIR_LIMIT = int(os.environ.get("SS_BIN_PAIR_LIMIT", str(1 << 29)))
 
 
 @dataclass
@@ -55,7 +61,7 @@ class RenderContext:
     (rasterizer.py:71-90): projected records, sort order, tile lists."""
 
     def __init__(self, cloud, camera, settings, background, dcloud, geom, bins, n_pairs,
-                 n_survivors):
+                 n_survivors, bin_capacity=None):
         self.cloud = cloud
         self.camera = camera
         self.settings = settings
@@ -65,11 +71,16 @@ class RenderContext:
         self._bins = bins
         self.n_pairs = n_pairs
         self.n_survivors = n_survivors
+        self.bin_capacity = n_pairs if bin_capacity is None else bin_capacity
         self._tiles = None
         self._indices = None
 
     def _lists(self):
         lib = _lib.load()
+        if self.n_pairs > self.bin_capacity:
+            raise DataError("tile lists of a view rendered in bands are not retained "
+                            f"({self.n_pairs} pairs > {self.bin_capacity}); raise "
+                            "SS_BIN_PAIR_LIMIT to keep them")
         cam, s = camera_struct(self.camera), settings_struct(self.settings, self.background)
         ts = self.settings.tile_size
         ntx = (self.camera.width + ts - 1) // ts
@@ -134,15 +145,17 @@ def render_device(dcloud: DeviceCloud, camera, background=None,
                                            ptr(counts), stream()), "rasterize_forward")
     torch.cuda.current_stream().synchronize()
     survivors, pairs = int(counts[0]), int(counts[1])
-    bins = empty_bytes(lib.ss_raster_bin_bytes(pairs, dcloud.n, C.byref(cam), C.byref(s)), dev)
+    cap = min(pairs, BIN_PAIR_LIMIT)
+    bins = empty_bytes(lib.ss_raster_bin_bytes(cap, dcloud.n, C.byref(cam), C.byref(s)), dev)
     h, w = camera.height, camera.width
     image = torch.empty(h, w, 3, dtype=torch.float32, device=dev)
     alpha = torch.empty(h, w, dtype=torch.float32, device=dev)
     touch = torch.zeros(max(dcloud.n, 1), dtype=torch.int32, device=dev) if want_touch else None
-    _lib.check(lib.ss_raster_forward_finish(C.byref(cl), C.byref(cam), C.byref(s), ptr(geom),
-                                            ptr(bins), pairs, ptr(image), ptr(alpha), ptr(touch),
-                                            stream()), "rasterize_forward")
-    return image, alpha, touch, geom, bins, pairs, survivors
+    _lib.check(lib.ss_raster_forward_finish_banded(C.byref(cl), C.byref(cam), C.byref(s),
+                                                   ptr(geom), ptr(bins), cap, pairs, ptr(image),
+                                                   ptr(alpha), ptr(touch), stream()),
+               "rasterize_forward")
+    return image, alpha, touch, geom, bins, pairs, survivors, cap
 
 
 def rasterize_forward(cloud, camera, background=None,
@@ -153,12 +166,12 @@ def rasterize_forward(cloud, camera, background=None,
     background = np.asarray(background, dtype=np.float64)
     camera = Camera.from_any(camera)
     dcloud = _device_cloud(cloud)
-    image, alpha, touch, geom, bins, pairs, surv = render_device(dcloud, camera, background,
-                                                                 settings)
+    image, alpha, touch, geom, bins, pairs, surv, cap = render_device(dcloud, camera, background,
+                                                                      settings)
     out = RenderOutput(image=image.cpu().numpy().astype(np.float64),
                        alpha_map=alpha.cpu().numpy().astype(np.float64),
                        per_gaussian_touch_count=touch[: dcloud.n].cpu().numpy().astype(np.int64))
-    ctx = RenderContext(cloud, camera, settings, background, dcloud, geom, bins, pairs, surv)
+    ctx = RenderContext(cloud, camera, settings, background, dcloud, geom, bins, pairs, surv, cap)
     return out, ctx
 
 
@@ -186,9 +199,10 @@ def rasterize_backward(ctx: RenderContext, d_image) -> GradientBuffer:
     for k, t in bufs.items():
         setattr(g, k, ptr(t))
     cam, s = camera_struct(cam_o), settings_struct(ctx.settings, ctx.background)
-    _lib.check(lib.ss_raster_backward(C.byref(dc.struct()), C.byref(cam), C.byref(s),
-                                      ptr(ctx._geom), ptr(ctx._bins), ctx.n_pairs, ptr(dimg),
-                                      C.byref(g), stream()), "rasterize_backward")
+    _lib.check(lib.ss_raster_backward_banded(C.byref(dc.struct()), C.byref(cam), C.byref(s),
+                                             ptr(ctx._geom), ptr(ctx._bins), ctx.bin_capacity,
+                                             ctx.n_pairs, ptr(dimg), C.byref(g), stream()),
+               "rasterize_backward")
     h = {k: v.cpu().numpy() for k, v in bufs.items()}
     return GradientBuffer(h["d_means"].astype(np.float64), h["d_rotations"].astype(np.float64),
                           h["d_log_scales"].astype(np.float64),

@@ -208,6 +208,7 @@ class Stage1Trainer:
         s.ntc_scratch = ptr(self.ntc_scratch)
         self.s = s
         self.capacity_margin = 1.3
+        self.banded = False
         self.use_graphs = True
         self._graphs = {}
         self._frame_start = (self.tables.clone(), self.params.clone())
@@ -231,9 +232,13 @@ class Stage1Trainer:
         self._call(self.lib.ss_stage1_frame_begin, C.byref(self.s), stream())
 
     def _ensure_bins(self, pairs: int, cam, exact: bool = False):
-        if pairs <= self.bin_capacity and self.bins is not None:
+        from .rasterizer import BIN_PAIR_LIMIT
+
+        if self.bins is not None and (pairs <= self.bin_capacity or
+                                      self.bin_capacity >= BIN_PAIR_LIMIT):
             return
         cap = max(pairs if exact else int(pairs * 1.25) + 1024, 1 << 16)
+        cap = min(cap, BIN_PAIR_LIMIT)  # more pairs: binned in bands of tile rows
         self._graphs = {}  # captured iterations point at the old workspace
         nbytes = self.lib.ss_raster_bin_bytes(cap, self.cloud.n, C.byref(cam),
                                               C.byref(self.settings))
@@ -260,10 +265,12 @@ class Stage1Trainer:
                                                             non_blocking=True)
 
     def finish(self, view: int, pairs: int, adam: bool = True, grad_scale: float = 1.0,
-               staged: bool = False):
+               staged: bool = False, target: torch.Tensor | None = None):
+        """Iteration part B with the host-known pair count (views above the bin
+        workspace are binned in bands of tile rows)."""
         cam = self.cam_structs[view]
         self._ensure_bins(pairs, cam)
-        tgt = ptr(self._staging if staged else self.targets[view])
+        tgt = ptr(target if target is not None else (self._staging if staged else self.targets[view]))
         if adam and grad_scale == 1.0:
             self._call(self.lib.ss_stage1_iter_finish, C.byref(self.s), C.byref(cam), tgt, pairs,
                        stream())
@@ -307,18 +314,24 @@ class Stage1Trainer:
         cam = self.cam_structs[view]
         self._ensure_bins(pairs, cam)
         tc = self.cloud.struct(self.t_means, self.t_rot, self.t_sh)
-        self._call(self.lib.ss_raster_forward_finish, C.byref(tc), C.byref(cam),
-                   C.byref(self.settings), ptr(self.geom), ptr(self.bins), pairs, ptr(self.image),
-                   ptr(self.alpha), None, stream())
+        self._call(self.lib.ss_raster_forward_finish_banded, C.byref(tc), C.byref(cam),
+                   C.byref(self.settings), ptr(self.geom), ptr(self.bins), self.bin_capacity,
+                   pairs, ptr(self.image), ptr(self.alpha), None, stream())
         return pairs
 
     def plan_capacity(self, margin: float | None = None) -> int:
         """Size the tile-pair workspace for the no-sync iteration: the pair
         count of every view under the current parameters (one host read per
         view, once), times a margin for the motion Stage 1 applies."""
+        from .rasterizer import BIN_PAIR_LIMIT
+
         m = self.capacity_margin if margin is None else margin
         peak = max(self.begin(v) for v in range(len(self.cameras)))
         cap = int(peak * m) + 65536
+        # views beyond one bin workspace: every iteration reads its pair count
+        # and bins in bands of tile rows (synchronous, no graphs)
+        self.banded = cap > BIN_PAIR_LIMIT
+        cap = min(cap, BIN_PAIR_LIMIT)
         if cap > self.bin_capacity:
             self._ensure_bins(cap, self.cam_structs[0], exact=True)
         return self.bin_capacity
@@ -348,6 +361,11 @@ class Stage1Trainer:
         if accumulate_stats is not None:
             self.s.accumulate_stats = int(accumulate_stats)
         self.s.defer_scatter = int(defer_scatter)
+        if self.banded:
+            pairs = self.begin(view)
+            self.finish(view, pairs, adam=adam, grad_scale=grad_scale, staged=staged,
+                        target=target)
+            return
         use = self.use_graphs if graph is None else graph
         if not use:
             self._iterate_eager(view, grad_scale, adam, staged, target)
