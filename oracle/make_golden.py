@@ -386,9 +386,55 @@ def gen_stage1_loop(R):
                         out_sh=transformed.sh)
 
 
+def gen_stream(R):
+    """A .splv container written by the reference's StreamWriter
+    (streamio.py:185-226): HEAD, INIT, WARM and two FREC blocks."""
+    import sys
+    import tempfile
+
+    if rb.REF_SRC not in sys.path:
+        sys.path.insert(0, rb.REF_SRC)
+    from splatstream import streamio
+
+    from oracle import stage1 as O
+
+    sc = scenes.small_scene(seed=41, n=50, width=32, height=24, sh_degree=1, n_views=1)
+    grid = dict(sc.grid, levels=2, log2_table=6)
+    tables, mlp = O.init_ntc(grid, hidden_dim=8, hidden_layers=1, output_init="random", seed=3)
+    warm = rb.ref_cache(R, grid, scenes.f32(tables), mlp, hidden_dim=8)
+    warm.quantize_float32()
+    adds = [scenes.make_cloud(np.random.default_rng(60 + k), 3 + 4 * k, 2, 1.0, 0.3, 1)
+            for k in range(2)]
+    blobs = []
+    for k in range(2):
+        c = rb.ref_cache(R, grid, scenes.f32(tables + 0.01 * (k + 1)), mlp, hidden_dim=8)
+        c.quantize_float32()
+        blobs.append(streamio.serialize_ntc(c))
+    header = {"format": "splv", "cameras": [{"width": 32, "height": 24}], "fps": 30}
+    with tempfile.TemporaryDirectory() as d:
+        path = os.path.join(d, "s.splv")
+        with streamio.StreamWriter(path, header) as w:
+            w.write_initial(rb.ref_cloud(R, sc.cloud))
+            w.write_warmup(warm)
+            for k in range(2):
+                w.write_frame(streamio.FrameRecord(k + 1, blobs[k], rb.ref_cloud(R, adds[k])))
+        data = open(path, "rb").read()
+    np.savez_compressed(os.path.join(OUT, "stream.npz"), container=np.frombuffer(data, np.uint8),
+                        header=json_bytes(header), **_cloud_arr(sc.cloud, "init_"),
+                        warm_blob=np.frombuffer(streamio.serialize_ntc(warm), np.uint8),
+                        **{f"blob{k}": np.frombuffer(b, np.uint8) for k, b in enumerate(blobs)},
+                        **{k2: v for k, a in enumerate(adds) for k2, v in _cloud_arr(a, f"add{k}_").items()})
+
+
+def json_bytes(obj):
+    import json
+
+    return np.frombuffer(json.dumps(obj).encode(), np.uint8)
+
+
 GENERATORS = dict(encode=gen_encode, ntc=gen_ntc, transform=gen_transform, raster=gen_raster,
                   loss=gen_loss, stage1=gen_stage1, ntc_blob=gen_ntc_blob, warmup=gen_warmup, playback=gen_playback,
-                  stage2=gen_stage2, stage1_loop=gen_stage1_loop)
+                  stage2=gen_stage2, stage1_loop=gen_stage1_loop, stream=gen_stream)
 
 
 def main():
