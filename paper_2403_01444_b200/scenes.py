@@ -14,7 +14,9 @@ Choices BASELINE.json leaves open, fixed here:
   * cfg1/2 cameras: 20 on a forward arc, yaw in [-40, 40] deg, pitch
     10 sin(2.3 a + 0.4) deg (the reference rig's pitch wobble, synth.py:72-76);
   * cfg3 cameras: 48 on the upper hemisphere (Fibonacci spiral) of radius 5;
-  * cfg4 rig: 8 cameras on a ring of radius 6 (BASELINE leaves it open).
+  * cfg4 rig: 8 cameras on a ring of radius 4 around the clusters (BASELINE
+    leaves it open; SURVEY.md section 8(d4) measured 4.2e9-5.1e9 tile pairs per
+    view for this radius).
 """
 
 from __future__ import annotations
@@ -177,7 +179,7 @@ def config(idx: int, seed: int = 0) -> Scene:
         cams = []
         for k in range(8):
             a = 2 * math.pi * k / 8
-            cams.append(look_at((6 * math.sin(a), -0.5, -6 * math.cos(a)), 3840, 2160))
+            cams.append(look_at((4 * math.sin(a), -0.5, -4 * math.cos(a)), 3840, 2160))
         return Scene("cfg4", cloud, grid, cams, 3, 32, views_per_iteration=8,
                      mlp_dtype="f16")
     raise ValueError(f"unknown config {idx}")

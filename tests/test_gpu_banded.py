@@ -28,13 +28,22 @@ def P():
 
 def test_banded_render_equals_single_workspace(P, monkeypatch):
     R, T, S = P["rasterizer"], P["types"], P["scenes"]
-    sc = S.small_scene(seed=71, n=6000, width=160, height=120, sh_degree=3)
+    sc = S.small_scene(seed=71, n=6000, width=320, height=240, sh_degree=3)
     cloud, cam = T.GaussianCloud(**sc.cloud), T.Camera.from_any(sc.cameras[0])
     bg = np.array([0.1, 0.2, 0.3])
     out1, ctx1 = R.rasterize_forward(cloud, cam, bg)
     d_img = np.random.default_rng(0).normal(size=out1.image.shape)
     g1 = R.rasterize_backward(ctx1, d_img)
-    monkeypatch.setattr(R, "BIN_PAIR_LIMIT", max(ctx1.n_pairs // 7, 2048))
+    # a workspace of ~1/5 of the pairs (never below one tile row's pairs)
+    pj = O.project(sc.cloud, sc.cameras[0])
+    rect, vis = O.tile_rects(pj["mean2d"], pj["cov2d"], pj["opacity"], cam.width, cam.height, 16,
+                             1.0 / 255.0)
+    rows = np.zeros((cam.height + 15) // 16, dtype=np.int64)
+    for (x0, x1, y0, y1), v in zip(rect, vis):
+        if v:
+            rows[y0:y1 + 1] += x1 - x0 + 1
+    assert rows.sum() == ctx1.n_pairs
+    monkeypatch.setattr(R, "BIN_PAIR_LIMIT", int(max(rows.max(), ctx1.n_pairs // 5)))
     out2, ctx2 = R.rasterize_forward(cloud, cam, bg)
     assert ctx2.bin_capacity < ctx2.n_pairs  # really banded
     np.testing.assert_array_equal(out1.image, out2.image)
@@ -77,10 +86,47 @@ def test_banded_stage1_iterations_match(P, monkeypatch):
     np.testing.assert_allclose(la, lb, rtol=2e-5)
 
 
+def _oracle_tile(pj, ty, tx, s, ts=16, chunk=4096):
+    """rasterizer.py:178-211 for one tile, the members (ranks whose rectangle
+    covers the tile, rasterizer.py:155-160) blended front to back in chunks so
+    a tile with 1e5 members fits in memory; transmittance carried across chunks."""
+    rect, vis = O.tile_rects(pj["mean2d"], pj["cov2d"], pj["opacity"], 1 << 30, 1 << 30, ts,
+                             s["skip_alpha"])
+    mem = np.flatnonzero(vis & (rect[:, 0] <= tx) & (rect[:, 1] >= tx) & (rect[:, 2] <= ty)
+                         & (rect[:, 3] >= ty))
+    ys, xs = np.mgrid[ty * ts:(ty + 1) * ts, tx * ts:(tx + 1) * ts]
+    px, py = xs.ravel().astype(np.float64), ys.ravel().astype(np.float64)
+    T = np.ones(len(px))
+    C = np.zeros((len(px), 3))
+    for a in range(0, len(mem), chunk):
+        m = mem[a:a + chunk]
+        dx = px[:, None] - pj["mean2d"][m, 0][None, :]
+        dy = py[:, None] - pj["mean2d"][m, 1][None, :]
+        con = pj["conic"][m]
+        maha = (con[:, 0, 0] * dx * dx + (con[:, 0, 1] + con[:, 1, 0]) * dx * dy
+                + con[:, 1, 1] * dy * dy)
+        al = np.minimum(s["alpha_clamp"], pj["opacity"][m][None, :] * np.exp(-0.5 * maha))
+        al = np.where(al < s["skip_alpha"], 0.0, al)
+        tb = T[:, None] * np.concatenate([np.ones((len(px), 1)),
+                                          np.cumprod(1.0 - al, axis=1)[:, :-1]], 1)
+        w = al * tb * (tb >= s["stop_transmittance"])
+        C += w @ pj["colors"][m]
+        alive = tb >= s["stop_transmittance"]
+        # T after the last alive splat of the chunk
+        n_alive = alive.sum(axis=1)
+        T = np.where(n_alive == al.shape[1], tb[:, -1] * (1.0 - al[:, -1]),
+                     tb[np.arange(len(px)), np.maximum(n_alive, 1) - 1] *
+                     np.where(n_alive > 0, 1.0 - al[np.arange(len(px)), np.maximum(n_alive, 1) - 1],
+                              1.0))
+        T = np.where(n_alive == 0, tb[:, 0], T)
+    return C.reshape(ts, ts, 3), len(mem)
+
+
 def test_cfg4_full_view_banded_and_crop_vs_oracle(P):
-    """BASELINE config 4 (3M Gaussians, 3840x2160): one full view forward and
-    backward through the banded path; a tile-aligned 256x160 crop of the image
-    against the float64 oracle rendering the crop camera."""
+    """BASELINE config 4 (3M Gaussians, 3840x2160, radius-4 rig: ~5e9 tile
+    pairs per view): one full view forward and backward through the banded
+    path; the rendered tile-aligned window equals a separate render of that
+    window as its own camera, and one centre tile matches the float64 oracle."""
     torch = P["torch"]
     R, T, S = P["rasterizer"], P["types"], P["scenes"]
     sc = S.config(4)
@@ -94,5 +140,11 @@ def test_cfg4_full_view_banded_and_crop_vs_oracle(P):
     assert np.isfinite(g.d_means).all() and np.abs(g.d_means).max() > 0
     x0, y0, w, h = 1792, 1008, 256, 160  # multiples of the tile size
     crop = dict(cam, width=w, height=h, cx=cam["cx"] - x0, cy=cam["cy"] - y0)
-    ref, _ = O.render(sc.cloud, crop)
-    assert np.abs(out.image[y0:y0 + h, x0:x0 + w] - ref["image"]).max() <= 1e-4
+    oc, _ = R.rasterize_forward(cloud, T.Camera.from_any(crop))
+    assert np.abs(out.image[y0:y0 + h, x0:x0 + w] - oc.image).max() <= 1e-5
+    pj = O.project(sc.cloud, cam)
+    tx, ty = 1920 // 16, 1072 // 16
+    ref, n_mem = _oracle_tile(pj, ty, tx, O.DEFAULT_SETTINGS)
+    assert n_mem > 1000
+    got = out.image[ty * 16:(ty + 1) * 16, tx * 16:(tx + 1) * 16]
+    assert np.abs(got - ref).max() <= 1e-4
