@@ -107,18 +107,11 @@ def _oracle_tile(pj, ty, tx, s, ts=16, chunk=4096):
                 + con[:, 1, 1] * dy * dy)
         al = np.minimum(s["alpha_clamp"], pj["opacity"][m][None, :] * np.exp(-0.5 * maha))
         al = np.where(al < s["skip_alpha"], 0.0, al)
-        tb = T[:, None] * np.concatenate([np.ones((len(px), 1)),
-                                          np.cumprod(1.0 - al, axis=1)[:, :-1]], 1)
-        w = al * tb * (tb >= s["stop_transmittance"])
-        C += w @ pj["colors"][m]
-        alive = tb >= s["stop_transmittance"]
-        # T after the last alive splat of the chunk
-        n_alive = alive.sum(axis=1)
-        T = np.where(n_alive == al.shape[1], tb[:, -1] * (1.0 - al[:, -1]),
-                     tb[np.arange(len(px)), np.maximum(n_alive, 1) - 1] *
-                     np.where(n_alive > 0, 1.0 - al[np.arange(len(px)), np.maximum(n_alive, 1) - 1],
-                              1.0))
-        T = np.where(n_alive == 0, tb[:, 0], T)
+        t_all = np.concatenate([T[:, None], T[:, None] * np.cumprod(1.0 - al, axis=1)], 1)
+        tb = t_all[:, :-1]
+        alive = tb >= s["stop_transmittance"]  # a prefix: T only decreases
+        C += (al * tb * alive) @ pj["colors"][m]
+        T = t_all[np.arange(len(px)), alive.sum(axis=1)]  # T after the last alive splat
     return C.reshape(ts, ts, 3), len(mem)
 
 
