@@ -364,6 +364,8 @@ def main():
     from paper_2403_01444_b200.stage1 import Stage1Config
 
     lib = _lib.load()
+    if "SS_MLP_MODE" in os.environ:  # decoder arithmetic (0 FFMA, 1 3xTF32, 2 tf32)
+        lib.ss_set_mlp_mode(int(os.environ["SS_MLP_MODE"]))
     sc, cache, targets = build_problem(a.config)
     views = list(zip(sc.cameras, targets))
     n_views = len(views)

@@ -894,6 +894,7 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_fwd_kernel(
   const int2 range = g.ranges[tile];
   PixelOffsets<TS, PPT> po;
   po.init(threadIdx.x);
+  const unsigned wbit = 1u << (threadIdx.x >> 5);
   float T[PPT], C[PPT][3];
   double Td[TOUCH ? PPT : 1], Cd[TOUCH ? PPT : 1][3];
   int last[PPT];
@@ -932,7 +933,9 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_fwd_kernel(
     const int cnt = min(NT, range.y - b);
     for (int k = 0; k < cnt; ++k) {
       if (!TOUCH) {  // fast path: reject on the log2 form before the exponential
-        if (!((s_sp[k].rows >> (threadIdx.x >> 5)) & 1u)) continue;  // warp-uniform
+        // (the vote makes the branch provably warp-uniform: the loop keeps its
+        // uniform-register addressing)
+        if (!__any_sync(0xffffffffu, s_sp[k].rows & wbit)) continue;
         const float4 L = s_sp[k].L, Q = s_sp[k].Q;
         const float qlo = L.w, qhi = Q.w;
         float lgs[PPT];
@@ -1059,6 +1062,7 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_bwd_kernel(
   const int2 range = g.ranges[tile];
   PixelOffsets<TS, PPT> po;
   po.init(threadIdx.x);
+  const unsigned wbit = 1u << warp;
   float T[PPT], S[PPT], gp[PPT][3], px[PPT], py[PPT];
   int last[PPT];
   int max_last = 0;
@@ -1098,7 +1102,7 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_bwd_kernel(
                                            s_sp[threadIdx.x]);
     __syncthreads();
     for (int k = 0; k < cnt; ++k) {
-      if (!((s_sp[k].rows >> warp) & 1u)) continue;  // warp-uniform: no live row
+      if (!__any_sync(0xffffffffu, s_sp[k].rows & wbit)) continue;  // no live row
       const int pos_rel = end - 1 - k - range.x;
       const float4 L = s_sp[k].L, Q = s_sp[k].Q;
       const float qlo = L.w, qhi = Q.w;
