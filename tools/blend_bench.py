@@ -1,0 +1,46 @@
+"""Deterministic A/B timing of the raster kernels (no training trajectory):
+the cfg1 cloud with its means displaced by a fixed seeded field (|d| ~ the
+late-frame drift of bench.py's frame), four views, forward + backward through
+the Stage-1 trainer's device path, per-phase CUDA events (graph replay).
+
+python tools/blend_bench.py [sigma]   -> one JSON line"""
+import json
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, "/root/repo")
+import bench  # noqa: E402
+from paper_2403_01444_b200 import _lib, scenes  # noqa: E402
+from paper_2403_01444_b200.stage1 import Stage1Config, Stage1Trainer  # noqa: E402
+
+sigma = float(sys.argv[1]) if len(sys.argv) > 1 else 0.5
+lib = _lib.load()
+sc, cache, targets = bench.build_problem(1)
+cloud = dict(sc.cloud)
+cloud["means"] = scenes.f32(cloud["means"] + np.random.default_rng(3).normal(scale=sigma,
+                                                                              size=cloud["means"].shape))
+tr = Stage1Trainer(cloud, cache, list(zip(sc.cameras, targets)), Stage1Config())
+views = [0, 5, 10, 15]
+lib.ss_profile_enable(1)
+for v in views:  # capture
+    tr.iterate(v, adam=False)
+torch.cuda.synchronize()
+flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+nph = lib.ss_profile_count()
+names = [lib.ss_profile_name(i).decode() for i in range(nph)]
+acc = {n: [] for n in names}
+buf = (np.ctypeslib.ctypes.c_double * nph)()
+for rep in range(3):
+    for v in views:
+        flush.fill_(rep)
+        tr.iterate(v, adam=False)
+        torch.cuda.synchronize()
+        lib.ss_profile_read(buf, nph)
+        for i, n in enumerate(names):
+            acc[n].append(buf[i])
+out = {n: round(1000 * float(np.mean(x)), 1) for n, x in acc.items() if x}
+out["pairs"] = int(np.mean(tr.pairs_of_last(len(views))))
+out["sigma"] = sigma
+print(json.dumps(out))
