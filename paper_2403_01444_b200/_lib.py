@@ -13,7 +13,8 @@ import os
 
 from .errors import DataError, NumericalError, SplatstreamError
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libss_b200.so")
+LIB_PATH = os.environ.get("SS_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                                                     "libss_b200.so")
 
 MAX_LEVELS = 32
 SS_OK, SS_ERR_DATA, SS_ERR_NUMERICAL, SS_ERR_CUDA, SS_ERR_CAPACITY = 0, 1, 2, 3, 4

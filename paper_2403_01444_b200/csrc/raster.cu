@@ -30,8 +30,7 @@ struct Geom {
   double4* r_conop_d;
   float4* r_color;
   int4* r_rect;     // per rank (tx0, tx1, ty0, ty1)
-  double4* r_cull;  // per rank: 2 ln(opacity / skip_alpha) (tile-cull threshold), -c01/c11, -c01/c00,
-                    // half height (px) of the alpha >= skip ellipse (< 0: empty)
+  double4* r_cull;  // per rank: 2 ln(opacity / skip_alpha) (tile-cull threshold), -c01/c11, -c01/c00
   int64_t* offsets;  // per rank, exclusive prefix of tile counts (n+1)
   float* acc;        // per rank x kAccStride: colour 3, M0 | M1 2, M2 3 (anchor moments, K5a)
   uint8_t* touched;  // per rank
@@ -480,15 +479,11 @@ __global__ void rank_kernel(CamD cam, ss_raster_settings s, int64_t n, Geom g) {
                      tile_of(yh, ts, nty));
     vis = !((xh < 0) || (xl > cam.W - 1) || (yh < 0) || (yl > cam.H - 1));
     // co.y = c01 + c10: the minimiser of the form along x = const is dy = -co.y dx / (2 c11)
-    // alpha >= skip <=> maha <= R2 = 2 ln(op / skip): the ellipse's half height is
-    // sqrt(R2 cov11), widened for rounding (the blends' per-warp row mask)
-    const double R2 = 2.0 * log(co.w / s.skip_alpha);
-    const double hh = R2 > -1e-9 ? sqrt(fmax(R2, 0.0) * fmax(cv.y, 0.0)) * (1.0 + 1e-6) + 1e-3 : -1.0;
-    g.r_cull[r] = make_double4(R2, -co.y / (2.0 * co.z), -co.y / (2.0 * co.x), hh);
+    g.r_cull[r] = make_double4(2.0 * log(co.w / s.skip_alpha), -co.y / (2.0 * co.z),
+                               -co.y / (2.0 * co.x), 0.0);
   } else {  // skip = 0: every tile (rasterizer.py:149-154)
     rect = make_int4(0, ntx - 1, 0, nty - 1);
     vis = true;
-    g.r_cull[r] = make_double4(1e300, 0.0, 0.0, 1e300);  // every row live
   }
   g.r_rect[r] = rect;
   g.offsets[r] = vis ? (int64_t)(rect.y - rect.x + 1) * (rect.w - rect.z + 1) : 0;
@@ -784,9 +779,7 @@ struct __align__(16) SplatRec {
   float4 L;    // lg0, gx, gy, lo: reject below lo = thr - band
   float4 Q;    // A, B, C, hi: float64 decision below hi = thr + kNearBand + band
   float4 col;  // rgb, opacity
-  int rank;
-  unsigned rows;  // bit w: warp w's pixel rows meet the alpha >= skip ellipse
-  int pad1, pad2;
+  int rank, pad0, pad1, pad2;
 };
 
 template <int TS>
@@ -820,17 +813,6 @@ __device__ __forceinline__ void stage_splat(const Geom& g, int r, int x0, int y0
   rec.Q = make_float4(q.x, q.y, q.z, q.w + (kNearBand + band));
   rec.col = g.r_color[r];
   rec.rank = r;
-  // warps own whole pixel rows (tile_pixel): RW rows each; a warp none of whose
-  // rows meets [mu_y - h, mu_y + h] has alpha < skip at all its pixels
-  constexpr int NW = BlendShape<TS>::NT / 32, RW = TS / NW;
-  const double hh = g.r_cull[r].w;
-  const double ylo = m.y - hh - (double)y0, yhi = m.y + hh - (double)y0;
-  unsigned rows = 0;
-  if (hh >= 0.0)
-#pragma unroll
-    for (int w = 0; w < NW; ++w)
-      rows |= (ylo <= (double)(RW * w + RW - 1) && yhi >= (double)(RW * w)) ? (1u << w) : 0u;
-  rec.rows = rows;
 }
 
 // per-thread pixel constants: offsets from the tile centre (k + 1/2, exact)
@@ -894,7 +876,6 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_fwd_kernel(
   const int2 range = g.ranges[tile];
   PixelOffsets<TS, PPT> po;
   po.init(threadIdx.x);
-  const unsigned wbit = 1u << (threadIdx.x >> 5);
   float T[PPT], C[PPT][3];
   double Td[TOUCH ? PPT : 1], Cd[TOUCH ? PPT : 1][3];
   int last[PPT];
@@ -935,7 +916,6 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_fwd_kernel(
       if (!TOUCH) {  // fast path: reject on the log2 form before the exponential
         // (the vote makes the branch provably warp-uniform: the loop keeps its
         // uniform-register addressing)
-        if (!__any_sync(0xffffffffu, s_sp[k].rows & wbit)) continue;
         const float4 L = s_sp[k].L, Q = s_sp[k].Q;
         const float qlo = L.w, qhi = Q.w;
         float lgs[PPT];
@@ -1062,7 +1042,6 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_bwd_kernel(
   const int2 range = g.ranges[tile];
   PixelOffsets<TS, PPT> po;
   po.init(threadIdx.x);
-  const unsigned wbit = 1u << warp;
   float T[PPT], S[PPT], gp[PPT][3], px[PPT], py[PPT];
   int last[PPT];
   int max_last = 0;
@@ -1102,7 +1081,6 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_bwd_kernel(
                                            s_sp[threadIdx.x]);
     __syncthreads();
     for (int k = 0; k < cnt; ++k) {
-      if (!__any_sync(0xffffffffu, s_sp[k].rows & wbit)) continue;  // no live row
       const int pos_rel = end - 1 - k - range.x;
       const float4 L = s_sp[k].L, Q = s_sp[k].Q;
       const float qlo = L.w, qhi = Q.w;
