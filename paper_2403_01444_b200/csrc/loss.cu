@@ -61,16 +61,27 @@ __global__ void __launch_bounds__(32 * WPB) ssim_map_kernel(LossParams lp,
   float g[WIN];
 #pragma unroll
   for (int k = 0; k < WIN; ++k) g[k] = lp.gf[k];
-  // staging: lane covers input columns lane, lane + 32, lane + 64 (< RW)
-  auto stage = [&](int b, int yi) {
+  // staging: lane covers input columns lane, lane + 32, lane + 64 (< RW); the
+  // raw values of the row after next are fetched into registers one step
+  // ahead, so their global latency overlaps the current row's filtering
+  float rx[3], ry[3];
+  auto fetch = [&](int yi) {
     const bool row_ok = yi < lp.H;
 #pragma unroll
     for (int m = 0; m < 3; ++m) {
       const int e = lane + 32 * m;
+      const bool ok = e < RW && row_ok && x0 + e < lp.W;
+      const int64_t o = ((int64_t)yi * lp.W + x0 + e) * C + c;
+      rx[m] = ok ? __ldg(img + o) : shx;
+      ry[m] = ok ? __ldg(tgt + o) : shy;
+    }
+  };
+  auto stage = [&](int b) {
+#pragma unroll
+    for (int m = 0; m < 3; ++m) {
+      const int e = lane + 32 * m;
       if (e < RW) {
-        const bool ok = row_ok && x0 + e < lp.W;
-        const int64_t o = ((int64_t)yi * lp.W + x0 + e) * C + c;
-        const float xv = ok ? __ldg(img + o) - shx : 0.f, yv = ok ? __ldg(tgt + o) - shy : 0.f;
+        const float xv = rx[m] - shx, yv = ry[m] - shy;
         buf[b][0][e] = xv;
         buf[b][1][e] = yv;
         buf[b][2][e] = fmaf(xv, xv, yv * yv);
@@ -89,11 +100,16 @@ __global__ void __launch_bounds__(32 * WPB) ssim_map_kernel(LossParams lp,
   const float c1f = (float)lp.c1, c2f = (float)lp.c2;
   const int64_t plane = (int64_t)lp.Hv * lp.Wp;
   const int col = x0 + 2 * lane;  // this lane's first output column
-  stage(0, oy0);
+  fetch(oy0);
+  stage(0);
+  fetch(oy0 + 1);
   __syncwarp();
   for (int yi = oy0; yi < iy1; ++yi) {
     const int cur = (yi - oy0) & 1;
-    if (yi + 1 < iy1) stage(cur ^ 1, yi + 1);  // next row into the other buffer
+    if (yi + 1 < iy1) {  // next row into the other buffer, then fetch the one after
+      stage(cur ^ 1);
+      fetch(yi + 2);
+    }
     // horizontal sums of row yi at columns col, col + 1
     float h[2][NQ];
 #pragma unroll
@@ -183,17 +199,26 @@ __global__ void __launch_bounds__(32 * WPB) ssim_grad_kernel(LossParams lp,
   float g[WIN];
 #pragma unroll
   for (int k = 0; k < WIN; ++k) g[k] = lp.gf[k];
-  // staging: lane covers map columns x0 - 10 + e, e = lane, lane + 32, lane + 64
-  auto stage = [&](int b, int r) {
+  // staging: lane covers map columns x0 - 10 + e, e = lane, lane + 32, lane + 64;
+  // one row fetched into registers ahead of its staging
+  float rm[3][NQ];
+  auto fetch = [&](int r) {
 #pragma unroll
     for (int m = 0; m < 3; ++m) {
       const int e = lane + 32 * m, vx = x0 - HALO + e;
-      if (e < RW) {
-        const bool ok = r < ry1 && vx >= 0 && vx < lp.Wv;
+      const bool ok = e < RW && r < ry1 && vx >= 0 && vx < lp.Wv;
 #pragma unroll
-        for (int q = 0; q < NQ; ++q)
-          buf[b][q][e] = ok ? __ldg(maps + (q * C + c) * plane + (int64_t)r * lp.Wp + vx) : 0.f;
-      }
+      for (int q = 0; q < NQ; ++q)
+        rm[m][q] = ok ? __ldg(maps + (q * C + c) * plane + (int64_t)r * lp.Wp + vx) : 0.f;
+    }
+  };
+  auto stage = [&](int b) {
+#pragma unroll
+    for (int m = 0; m < 3; ++m) {
+      const int e = lane + 32 * m;
+      if (e < RW)
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) buf[b][q][e] = rm[m][q];
     }
   };
   float acc[2][NQ][WIN];
@@ -208,11 +233,25 @@ __global__ void __launch_bounds__(32 * WPB) ssim_grad_kernel(LossParams lp,
   // output row r needs map rows r - 10 .. r; walk map rows from ry0 and emit
   // output row r once map row r (or the last map row) has been folded in
   const int rend = oy1;  // walk rows [ry0, rend): rows >= ry1 contribute zeros
-  stage(0, ry0);
+  float xn[2] = {0.f, 0.f}, tn[2] = {0.f, 0.f};
+  if (ry0 >= oy0)  // (ry0 == oy0 == 0): the first output row's pixels
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const bool ok = px + u < lp.W;
+      const int64_t o = ((int64_t)ry0 * lp.W + px + u) * C + c;
+      xn[u] = ok ? __ldg(img + o) : 0.f;
+      tn[u] = ok ? __ldg(tgt + o) : 0.f;
+    }
+  fetch(ry0);
+  stage(0);
+  fetch(ry0 + 1);
   __syncwarp();
   for (int r = ry0; r < rend; ++r) {
     const int cur = (r - ry0) & 1;
-    if (r + 1 < rend) stage(cur ^ 1, r + 1);
+    if (r + 1 < rend) {
+      stage(cur ^ 1);
+      fetch(r + 2);
+    }
     // horizontal full convolution at output columns px, px + 1: map cols px - j
     float h[2][NQ];
 #pragma unroll
@@ -246,12 +285,23 @@ __global__ void __launch_bounds__(32 * WPB) ssim_grad_kernel(LossParams lp,
         for (int i = 0; i < HALO; ++i) acc[u][q][i] = fmaf(g[i + 1], h[u][q], acc[u][q][i + 1]);
         acc[u][q][HALO] = 0.f;
       }
+    float xc[2], tc[2];  // this row's image / target (fetched a row ahead)
+#pragma unroll
+    for (int u = 0; u < 2; ++u) xc[u] = xn[u], tc[u] = tn[u];
+    if (r + 1 >= oy0 && r + 1 < oy1)
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const bool ok = px + u < lp.W;
+        const int64_t o = ((int64_t)(r + 1) * lp.W + px + u) * C + c;
+        xn[u] = ok ? __ldg(img + o) : 0.f;
+        tn[u] = ok ? __ldg(tgt + o) : 0.f;
+      }
     if (r >= oy0) {
 #pragma unroll
       for (int u = 0; u < 2; ++u) {
         if (px + u >= lp.W) continue;
         const int64_t o = ((int64_t)r * lp.W + px + u) * C + c;
-        const float xr = __ldg(img + o), tr = __ldg(tgt + o);
+        const float xr = xc[u], tr = tc[u];
         const float d = xr - tr;
         l1 += fabs((double)xr - (double)tr);
         const double sgn = d > 0.f ? 1.0 : (d < 0.f ? -1.0 : 0.0);
