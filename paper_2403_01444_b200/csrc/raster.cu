@@ -585,6 +585,12 @@ __device__ inline int64_t block_owner_rank(const int64_t* __restrict__ off, int6
   return lo;
 }
 
+// One thread per pair, chunks of 1024 pairs per CTA pass.  The owner of every
+// pair of a chunk comes from a block max-scan instead of a per-pair binary
+// search: each rank starting inside the chunk marks its first pair, the chunk's
+// first pair is owned by the rank found once per chunk (block_owner_rank), and
+// the inclusive max-scan carries the owners forward (zero-count ranks share
+// their successor's start and lose the max).
 __global__ void __launch_bounds__(256) duplicate_kernel(int ntx, int64_t n, Geom g, Bins b,
                                                         uint32_t* kdst, uint32_t* vdst,
                                                         uint32_t* status, int cull, int ts, int W,
@@ -592,41 +598,63 @@ __global__ void __launch_bounds__(256) duplicate_kernel(int ntx, int64_t n, Geom
                                                         const int64_t* __restrict__ offs,
                                                         const int64_t* __restrict__ d_count,
                                                         int ty_lo) {
-  constexpr int CH = 1024, SOFF = 2048;
-  __shared__ int64_t s_off[SOFF];
+  constexpr int CH = 1024, NTH = 256, PER = CH / NTH;
+  __shared__ int s_owner[CH];
+  __shared__ int s_wmax[NTH / 32];
   __shared__ uint32_t s_hist[2][256];  // binsort digit histograms of the emitted keys
   for (int i = threadIdx.x; i < 512; i += blockDim.x) (&s_hist[0][0])[i] = 0;
   const int64_t count = *d_count;
   if (count > b.capacity && blockIdx.x == 0 && threadIdx.x == 0 && status)
     atomicOr(status, SS_FLAG_OVERFLOW);
   const int64_t pairs = min(count, b.capacity);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int64_t j0 = (int64_t)blockIdx.x * CH; j0 < pairs; j0 += (int64_t)gridDim.x * CH) {
-    __syncthreads();  // the previous chunk is done with s_off
+    __syncthreads();  // the previous chunk is done with s_owner
+    const int cn = (int)min((int64_t)CH, pairs - j0);
     const int64_t rlo = block_owner_rank(offs, 0, n, j0);
-    const int64_t rhi = block_owner_rank(offs, rlo, n, min(j0 + CH, pairs) - 1) + 1;
-    // the chunk's owning ranks' offsets staged in shared memory when they fit
-    const bool staged = rhi - rlo + 1 <= SOFF;
-    if (staged)
-      for (int64_t r = rlo + threadIdx.x; r <= rhi; r += blockDim.x) s_off[r - rlo] = offs[r];
+    const int64_t rhi = block_owner_rank(offs, rlo, n, j0 + cn - 1);
+    for (int i = threadIdx.x; i < CH; i += NTH) s_owner[i] = i == 0 ? (int)rlo : -1;
     __syncthreads();
-    for (int64_t j = j0 + threadIdx.x; j < min(j0 + CH, pairs); j += blockDim.x) {
-      int64_t lo;
-      if (staged) {
-        int64_t a = 0, c = rhi - rlo;  // s_off[a] <= j < s_off[c]
-        while (c - a > 1) {
-          const int64_t mid = (a + c) >> 1;
-          if (s_off[mid] <= j) a = mid; else c = mid;
-        }
-        lo = rlo + a;
-      } else {
-        lo = owner_rank(offs, rlo, rhi, j);
-      }
+    for (int64_t r = rlo + 1 + threadIdx.x; r <= rhi; r += NTH)
+      atomicMax(&s_owner[(int)(offs[r] - j0)], (int)r);
+    __syncthreads();
+    // inclusive max-scan: PER consecutive entries per thread, then the warps
+    int v[PER], m = -1;
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      m = max(m, s_owner[threadIdx.x * PER + q]);
+      v[q] = m;
+    }
+    int x = m;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x = max(x, y);
+    }
+    if (lane == 31) s_wmax[warp] = x;
+    const int prev_lane = __shfl_up_sync(0xffffffffu, x, 1);
+    __syncthreads();
+    int carry = lane == 0 ? -1 : prev_lane;
+    for (int w = 0; w < warp; ++w) carry = max(carry, s_wmax[w]);
+#pragma unroll
+    for (int q = 0; q < PER; ++q) s_owner[threadIdx.x * PER + q] = max(carry, v[q]);
+    __syncthreads();
+    for (int i = threadIdx.x; i < cn; i += NTH) {
+      const int64_t j = j0 + i;
+      const int lo = s_owner[i];
       const int4 rc = g.r_rect[lo];
       const int wx = rc.y - rc.x + 1;
-      const int64_t local = j - (staged ? s_off[lo - rlo] : offs[lo]);
-      const int ty = max(rc.z, ty_lo) + (int)(local / wx), tx = rc.x + (int)(local % wx);
+      const int local = (int)(j - offs[lo]);  // < tiles per view
+      // local / wx and local % wx (local < 2^22: one float estimate, one fix-up)
+      int qy = (int)__fdividef((float)local, (float)wx);
+      int qx = local - qy * wx;
+      if (qx < 0) qx += wx, --qy;
+      else if (qx >= wx) qx -= wx, ++qy;
+      const int ty = max(rc.z, ty_lo) + qy, tx = rc.x + qx;
       uint32_t key = (uint32_t)(ty * ntx + tx);
-      if (cull) {
+      // the cull test pays off for splats spanning several tiles; it never
+      // changes a result (culled pairs have alpha < skip at every pixel)
+      if (cull && wx * (rc.w - rc.z + 1) > 2) {
         const double xa = tx * ts, xb = min(tx * ts + ts, W) - 1, ya = ty * ts,
                      yb = min(ty * ts + ts, H) - 1;
         if (splat_misses_tile(g.r_mean[lo], g.r_conop_d[lo], g.r_cull[lo], xa, xb, ya, yb))
