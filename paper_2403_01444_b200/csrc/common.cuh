@@ -263,20 +263,10 @@ int binsort_run(const BinSortWS& w, uint32_t* keys_tmp, uint32_t* vals_tmp, uint
 // Producer-side histogram for binsort (8-bit digits, up to 4 passes): add a
 // key into the block's shared histogram sh[pass][digit]; bs_hist_flush adds
 // the block's counts to the global ones after a __syncthreads().
-// Lanes of a warp that share a digit are aggregated first (match + popc), so a
-// run of equal digits -- the high byte of tile keys emitted by one splat, the
-// exponent byte of depths -- costs one shared-memory atomic, not 32 serialised
-// ones.  Must be called by all lanes of the warp (pass valid = false for lanes
-// without a key).
-__device__ __forceinline__ void bs_hist_add(uint32_t (*sh)[256], uint32_t key, int key_bits,
-                                            bool valid = true) {
-  const unsigned act = __ballot_sync(0xffffffffu, valid);
+__device__ __forceinline__ void bs_hist_add(uint32_t (*sh)[256], uint32_t key, int key_bits) {
   for (int p = 0; 8 * p < key_bits; ++p) {
     const int bits = key_bits - 8 * p < 8 ? key_bits - 8 * p : 8;
-    const uint32_t d = valid ? (key >> (8 * p)) & ((1u << bits) - 1) : 0x100u;
-    const unsigned peers = __match_any_sync(0xffffffffu, d) & act;
-    if (valid && (__ffs(peers) - 1) == (int)(threadIdx.x & 31))
-      atomicAdd(&sh[p][d], (uint32_t)__popc(peers));
+    atomicAdd(&sh[p][(key >> (8 * p)) & ((1u << bits) - 1)], 1u);
   }
 }
 __device__ __forceinline__ void bs_hist_flush(const uint32_t (*sh)[256], uint32_t* hist,

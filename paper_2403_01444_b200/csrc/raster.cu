@@ -238,7 +238,6 @@ __global__ void __launch_bounds__(256, 3) preprocess_kernel(CamD cam, ss_cloud c
   for (int k = threadIdx.x; k < 1024; k += blockDim.x) (&s_hist[0][0])[k] = 0;
   __syncthreads();
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  uint32_t key = 0x7f800000u;  // +inf: culled (rasterizer.py:228)
   if (i < cl.n) {
     if (i == 0) g.dev_counts[2] = cl.n;
     g.order[i] = (int32_t)i;  // sort input (4 passes: the input sits in the output buffers)
@@ -251,6 +250,7 @@ __global__ void __launch_bounds__(256, 3) preprocess_kernel(CamD cam, ss_cloud c
                                                    __dmul_rn(cam.R[2][1], (double)m[1])),
                                          __dmul_rn(cam.R[2][2], (double)m[2])),
                                cam.t[2]);
+    uint32_t key = 0x7f800000u;  // +inf: culled (rasterizer.py:228)
     if (!(z > cam.near_clip)) {
       g.key_in[i] = __longlong_as_double(0x7ff0000000000000ll);
     } else {
@@ -274,8 +274,8 @@ __global__ void __launch_bounds__(256, 3) preprocess_kernel(CamD cam, ss_cloud c
       g.g_cov[i] = make_double2(P.cov2d[0][0], P.cov2d[1][1]);
     }
     g.key32[i] = key;
+    bs_hist_add(s_hist, key, 32);
   }
-  bs_hist_add(s_hist, key, 32, i < cl.n);  // every lane (warp-aggregated)
   __syncthreads();
   bs_hist_flush(s_hist, g.dsort.hist, 32);
 }
@@ -639,11 +639,9 @@ __global__ void __launch_bounds__(256) duplicate_kernel(int ntx, int64_t n, Geom
 #pragma unroll
     for (int q = 0; q < PER; ++q) s_owner[threadIdx.x * PER + q] = max(carry, v[q]);
     __syncthreads();
-    for (int i0 = 0; i0 < cn; i0 += NTH) {  // whole warps (the histogram votes)
-      const int i = i0 + threadIdx.x;
-      const bool ok = i < cn;
+    for (int i = threadIdx.x; i < cn; i += NTH) {
       const int64_t j = j0 + i;
-      const int lo = s_owner[ok ? i : 0];
+      const int lo = s_owner[i];
       const int4 rc = g.r_rect[lo];
       const int wx = rc.y - rc.x + 1;
       const int local = (int)(j - offs[lo]);  // < tiles per view
@@ -662,11 +660,9 @@ __global__ void __launch_bounds__(256) duplicate_kernel(int ntx, int64_t n, Geom
         if (splat_misses_tile(g.r_mean[lo], g.r_conop_d[lo], g.r_cull[lo], xa, xb, ya, yb))
           key = sentinel;
       }
-      if (ok) {
-        kdst[j] = key;
-        vdst[j] = (uint32_t)lo;
-      }
-      bs_hist_add(s_hist, key, key_bits, ok);
+      kdst[j] = key;
+      vdst[j] = (uint32_t)lo;
+      bs_hist_add(s_hist, key, key_bits);
     }
   }
   __syncthreads();
