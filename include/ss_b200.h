@@ -360,6 +360,17 @@ int ss_stage1_iter_finish(ss_stage1* st, const ss_camera* cam, const float* targ
 int ss_stage1_iter_grads(ss_stage1* st, const ss_camera* cam, const float* target,
                          int64_t n_pairs, float grad_scale, void* stream);
 int ss_stage1_apply_adam(ss_stage1* st, void* stream);
+/* A batch of views sharing one parameter state (view-sharded training, the
+ * mean of per-view gradients before one Adam step, transform.py:99-135 is
+ * linear in the transformed-cloud gradients): ss_stage1_batch_view renders one
+ * view and adds its transformed-cloud gradient (first != 0: also the NTC
+ * forward + transform, and the gradients are overwritten instead of added);
+ * ss_stage1_batch_ntc_grads then runs the transform VJP, decoder backward and
+ * table scatter (unless defer_scatter) once for the whole batch.  Device pair
+ * count (graph capturable). */
+int ss_stage1_batch_view(ss_stage1* st, const ss_camera* cam, const float* target,
+                         float grad_scale, int32_t first, void* stream);
+int ss_stage1_batch_ntc_grads(ss_stage1* st, void* stream);
 /* The hash-table scatter (ntc.py:278-288) of the last ss_stage1_iter_grads call
  * made with defer_scatter != 0: g_tables += the corner-weighted feature gradient. */
 int ss_stage1_table_scatter(ss_stage1* st, void* stream);

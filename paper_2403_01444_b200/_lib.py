@@ -135,6 +135,8 @@ SIGNATURES = [
     ("ss_stage1_iter_grads", I32, [C.POINTER(Stage1), PCam, P, I64, C.c_float, P]),
     ("ss_stage1_apply_adam", I32, [C.POINTER(Stage1), P]),
     ("ss_stage1_table_scatter", I32, [C.POINTER(Stage1), P]),
+    ("ss_stage1_batch_view", I32, [C.POINTER(Stage1), PCam, P, C.c_float, I32, P]),
+    ("ss_stage1_batch_ntc_grads", I32, [C.POINTER(Stage1), P]),
     ("ss_stage1_iter", I32, [C.POINTER(Stage1), PCam, P, C.c_float, I32, P]),
     ("ss_stage1_render", I32, [C.POINTER(Stage1), PCam, P]),
     ("ss_set_mlp_mode", I32, [I32]),

@@ -21,11 +21,17 @@ namespace ss {
 namespace {
 constexpr int kBsThreads = 256;
 constexpr int kBsWarps = kBsThreads / 32;
-constexpr int kBsStepsBig = 8;    // items per lane (2048-item tiles)
+#ifndef SS_BS_STEPS_BIG
+#define SS_BS_STEPS_BIG 8
+#endif
+#ifndef SS_BS_WIN
+#define SS_BS_WIN 8
+#endif
+constexpr int kBsStepsBig = SS_BS_STEPS_BIG;  // items per lane (2048-item tiles)
 constexpr int kBsStepsSmall = 4;  // 1024-item tiles for small sorts (more CTAs)
 constexpr uint32_t kFlagAgg = 1u << 30, kFlagInc = 2u << 30, kCntMask = (1u << 30) - 1;
 constexpr int kMaxPasses = 4;
-constexpr int kWin = 8;  // look-back window (predecessor flags read per round trip)
+constexpr int kWin = SS_BS_WIN;  // look-back window (predecessor flags read per round trip)
 
 __device__ __forceinline__ uint32_t lanemask_lt() {
   uint32_t m;

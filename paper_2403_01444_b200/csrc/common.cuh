@@ -225,7 +225,7 @@ const int64_t* raster_counts(void* geom, int64_t n, const ss_camera* cam,
 int raster_backward(const ss_cloud* cl, const ss_camera* cam, const ss_raster_settings* s,
                     void* geom, void* bins, int64_t cap, const float* d_image,
                     const ss_cloud_grads* grads, int full, cudaStream_t st, int64_t total,
-                    int cull, uint32_t* status);
+                    int cull, uint32_t* status, int accumulate = 0);
 }  // namespace ss
 
 // ---------------------------------------------------------------- phase timing

@@ -1242,16 +1242,18 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_bwd_kernel(
 template <int DEG>
 __global__ void __launch_bounds__(128, 4) gaussian_bwd_kernel(CamD cam, ss_cloud cl, Geom g,
                                                               int64_t n, ss_cloud_grads out,
-                                                              int full, int ts) {
+                                                              int full, int ts, int acc) {
   const int64_t gid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (gid >= n) return;
   constexpr int K = (DEG + 1) * (DEG + 1);  // == cl.sh_coeffs
   const int r = g.rank_of[gid];
   // culled, or no pixel of this view took a weight from it (all accumulators
   // are exactly 0, so every gradient is): zero rows so callers need no memset
+  // (acc != 0: the parameter gradients are sums over views, leave them)
   if (r >= g.dev_counts[0] || !g.touched[r]) {
     if (out.viewspace) out.viewspace[gid] = 0.f;
     if (out.contributed) out.contributed[gid] = 0;
+    if (acc) return;
     if (out.d_means) for (int j = 0; j < 3; ++j) out.d_means[3 * gid + j] = 0.f;
     if (out.d_rotations)
       *reinterpret_cast<float4*>(out.d_rotations + 4 * gid) = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -1329,16 +1331,23 @@ __global__ void __launch_bounds__(128, 4) gaussian_bwd_kernel(CamD cam, ss_cloud
           gbasis[k] = fmaf(e[t], gc[c], gbasis[k]);
           o[t] = basis[k] * gc[c];
         }
-        if (dsh) reinterpret_cast<float4*>(dsh)[j] = make_float4(o[0], o[1], o[2], o[3]);
+        if (dsh) {
+          float4 w4 = make_float4(o[0], o[1], o[2], o[3]);
+          if (acc) {
+            const float4 p4 = reinterpret_cast<const float4*>(dsh)[j];
+            w4.x += p4.x, w4.y += p4.y, w4.z += p4.z, w4.w += p4.w;
+          }
+          reinterpret_cast<float4*>(dsh)[j] = w4;
+        }
       }
     } else {
 #pragma unroll
       for (int k = 0; k < K; ++k) {
         gbasis[k] = sh[3 * k] * gc[0] + sh[3 * k + 1] * gc[1] + sh[3 * k + 2] * gc[2];
         if (dsh) {
-          dsh[3 * k] = basis[k] * gc[0];
-          dsh[3 * k + 1] = basis[k] * gc[1];
-          dsh[3 * k + 2] = basis[k] * gc[2];
+          dsh[3 * k] = basis[k] * gc[0] + (acc ? dsh[3 * k] : 0.f);
+          dsh[3 * k + 1] = basis[k] * gc[1] + (acc ? dsh[3 * k + 1] : 0.f);
+          dsh[3 * k + 2] = basis[k] * gc[2] + (acc ? dsh[3 * k + 2] : 0.f);
         }
       }
     }
@@ -1389,7 +1398,8 @@ __global__ void __launch_bounds__(128, 4) gaussian_bwd_kernel(CamD cam, ss_cloud
   for (int j = 0; j < 3; ++j)
     gw[j] += gp[0] * cam.R[0][j] + gp[1] * cam.R[1][j] + gp[2] * cam.R[2][j];
   if (out.d_means)
-    for (int j = 0; j < 3; ++j) out.d_means[3 * gid + j] = (float)gw[j];
+    for (int j = 0; j < 3; ++j)
+      out.d_means[3 * gid + j] = (float)gw[j] + (acc ? out.d_means[3 * gid + j] : 0.f);
   // covariance -> quaternion / log scales (gaussians.py:127-154)
   double gsym[3][3], gR[3][3];
   for (int i = 0; i < 3; ++i)
@@ -1402,9 +1412,15 @@ __global__ void __launch_bounds__(128, 4) gaussian_bwd_kernel(CamD cam, ss_cloud
     double gu[4];
     quat_to_rot_vjp(P.u[0], P.u[1], P.u[2], P.u[3], gR, gu);
     const double dot = P.u[0] * gu[0] + P.u[1] * gu[1] + P.u[2] * gu[2] + P.u[3] * gu[3];
-    *reinterpret_cast<float4*>(out.d_rotations + 4 * gid) =
-        make_float4((float)((gu[0] - P.u[0] * dot) / P.qn), (float)((gu[1] - P.u[1] * dot) / P.qn),
-                    (float)((gu[2] - P.u[2] * dot) / P.qn), (float)((gu[3] - P.u[3] * dot) / P.qn));
+    float4 q4 = make_float4((float)((gu[0] - P.u[0] * dot) / P.qn),
+                            (float)((gu[1] - P.u[1] * dot) / P.qn),
+                            (float)((gu[2] - P.u[2] * dot) / P.qn),
+                            (float)((gu[3] - P.u[3] * dot) / P.qn));
+    if (acc) {
+      const float4 p4 = *reinterpret_cast<const float4*>(out.d_rotations + 4 * gid);
+      q4.x += p4.x, q4.y += p4.y, q4.z += p4.z, q4.w += p4.w;
+    }
+    *reinterpret_cast<float4*>(out.d_rotations + 4 * gid) = q4;
   }
   if (full) {
     if (out.d_log_scales)
@@ -1412,9 +1428,12 @@ __global__ void __launch_bounds__(128, 4) gaussian_bwd_kernel(CamD cam, ss_cloud
         double s = 0;
         for (int j = 0; j < 3; ++j)
           for (int k = 0; k < 3; ++k) s += P.Rq[j][i] * gS[j][k] * P.Rq[k][i];
-        out.d_log_scales[3 * gid + i] = (float)(s * 2.0 * P.var[i]);
+        out.d_log_scales[3 * gid + i] =
+            (float)(s * 2.0 * P.var[i]) + (acc ? out.d_log_scales[3 * gid + i] : 0.f);
       }
-    if (out.d_opacity_logits) out.d_opacity_logits[gid] = (float)(aop * P.op * (1.0 - P.op));
+    if (out.d_opacity_logits)
+      out.d_opacity_logits[gid] =
+          (float)(aop * P.op * (1.0 - P.op)) + (acc ? out.d_opacity_logits[gid] : 0.f);
   }
 }
 
@@ -1573,7 +1592,7 @@ const int64_t* raster_counts(void* geom, int64_t n, const ss_camera* cam,
 int raster_backward(const ss_cloud* cl, const ss_camera* cam, const ss_raster_settings* s,
                     void* geom, void* bins, int64_t cap, const float* d_image,
                     const ss_cloud_grads* grads, int full, cudaStream_t st, int64_t total,
-                    int cull, uint32_t* status) {
+                    int cull, uint32_t* status, int accumulate) {
   SS_TRY(check_raster(cl, cam, s));
   const int64_t n = cl->n;
   if (n == 0) return SS_OK;
@@ -1602,10 +1621,10 @@ int raster_backward(const ss_cloud* cl, const ss_camera* cam, const ss_raster_se
     const unsigned grid = (unsigned)cdiv(n, 128);
     const CamD cd = make_cam(cam);
     switch (cl->sh_coeffs) {
-      case 1: gaussian_bwd_kernel<0><<<grid, 128, 0, st>>>(cd, *cl, g, n, *grads, full, s->tile_size); break;
-      case 4: gaussian_bwd_kernel<1><<<grid, 128, 0, st>>>(cd, *cl, g, n, *grads, full, s->tile_size); break;
-      case 9: gaussian_bwd_kernel<2><<<grid, 128, 0, st>>>(cd, *cl, g, n, *grads, full, s->tile_size); break;
-      default: gaussian_bwd_kernel<3><<<grid, 128, 0, st>>>(cd, *cl, g, n, *grads, full, s->tile_size); break;
+      case 1: gaussian_bwd_kernel<0><<<grid, 128, 0, st>>>(cd, *cl, g, n, *grads, full, s->tile_size, accumulate); break;
+      case 4: gaussian_bwd_kernel<1><<<grid, 128, 0, st>>>(cd, *cl, g, n, *grads, full, s->tile_size, accumulate); break;
+      case 9: gaussian_bwd_kernel<2><<<grid, 128, 0, st>>>(cd, *cl, g, n, *grads, full, s->tile_size, accumulate); break;
+      default: gaussian_bwd_kernel<3><<<grid, 128, 0, st>>>(cd, *cl, g, n, *grads, full, s->tile_size, accumulate); break;
     }
   }
   SS_CHECK_LAUNCH("gaussian_bwd_kernel");
@@ -1701,7 +1720,7 @@ int ss_raster_backward(const ss_cloud* cloud, const ss_camera* cam, const ss_ras
                        void* geom, void* bins, int64_t n_pairs, const float* d_image,
                        const ss_cloud_grads* grads, void* stream) {
   return raster_backward(cloud, cam, s, geom, bins, n_pairs, d_image, grads, 1,
-                         as_stream(stream), n_pairs, 0, nullptr);
+                         as_stream(stream), n_pairs, 0, nullptr, 0);
 }
 
 int ss_raster_forward_finish_banded(const ss_cloud* cloud, const ss_camera* cam,
@@ -1717,7 +1736,7 @@ int ss_raster_backward_banded(const ss_cloud* cloud, const ss_camera* cam,
                               int64_t bin_capacity, int64_t n_pairs, const float* d_image,
                               const ss_cloud_grads* grads, void* stream) {
   return raster_backward(cloud, cam, s, geom, bins, bin_capacity, d_image, grads, 1,
-                         as_stream(stream), n_pairs, 0, nullptr);
+                         as_stream(stream), n_pairs, 0, nullptr, 0);
 }
 
 int ss_tile_bin_begin(int64_t n, const double* mean2d, const double* cov2d, const double* opacity,

@@ -107,9 +107,14 @@ int ss_stage1_iter_begin(ss_stage1* st, const ss_camera* cam, int64_t* counts_ho
   return raster_begin(&tc, cam, &st->settings, st->geom, counts_host, as_stream(stream));
 }
 
-int ss_stage1_iter_grads(ss_stage1* st, const ss_camera* cam, const float* target,
-                         int64_t n_pairs, float grad_scale, void* stream) {
-  cudaStream_t s = as_stream(stream);
+}  // extern "C"
+
+namespace ss {
+// One view's render, loss and raster backward into the transformed-cloud
+// gradients d_means / d_rotations / d_sh (accumulate: added to them, the
+// views of a batch), plus the loss history and the view-space statistics.
+static int stage1_view(ss_stage1* st, const ss_camera* cam, const float* target, int64_t n_pairs,
+                       float grad_scale, int accumulate, cudaStream_t s) {
   // n_pairs above the workspace: the host-known count selects binning in bands
   // of tile rows (synchronous); otherwise the device count drives one band
   const int64_t cap = st->bin_capacity;
@@ -118,7 +123,7 @@ int ss_stage1_iter_grads(ss_stage1* st, const ss_camera* cam, const float* targe
                        st->alpha_map, nullptr, st->status, 1, s, n_pairs));
   SS_TRY(ss_render_loss(st->image, target, cam->height, cam->width, 3, st->lambda_dssim,
                         st->ssim_c1, st->ssim_c2, st->loss_scratch, st->loss_dev, st->d_image,
-                        st->status, stream));
+                        st->status, s));
   const bool hist = st->iter_dev && st->history_len > 0;
   if (hist || st->loss_accum) {
     history_kernel<<<1, 1, 0, s>>>(st->loss_dev, raster_counts(st->geom, tc.n, cam, &st->settings) + 1,
@@ -142,7 +147,7 @@ int ss_stage1_iter_grads(ss_stage1* st, const ss_camera* cam, const float* targe
   gr.viewspace = st->viewspace;
   gr.contributed = st->contributed;
   SS_TRY(raster_backward(&tc, cam, &st->settings, st->geom, st->bins, cap, st->d_image, &gr, 0,
-                         s, n_pairs, 1, st->status));
+                         s, n_pairs, 1, st->status, accumulate));
   if (st->accumulate_stats && st->stats_norm && st->stats_count) {
     const int64_t n = st->src.n;
     stats_kernel<<<(unsigned)cdiv(n, 256), 256, 0, s>>>(n, st->viewspace, st->contributed,
@@ -150,16 +155,50 @@ int ss_stage1_iter_grads(ss_stage1* st, const ss_camera* cam, const float* targe
                                                          1.0f / grad_scale);
     SS_CHECK_LAUNCH("stats_kernel");
   }
+  return SS_OK;
+}
+
+// transform VJP, decoder backward and (unless deferred) the table scatter of
+// the transformed-cloud gradients; live: skip rows no pixel saw (one view)
+static int stage1_ntc_grads(ss_stage1* st, const uint8_t* live, cudaStream_t s) {
   const NtcScratch ns = scratch_of(st);
   const bool perm = st->rows_index && st->rows_pos;
   SS_TRY(transform_vjp_run(&st->src, st->n_in, perm ? st->rows_index : st->rows,
                            perm ? st->rows_pos : nullptr, ns.out7, 8, st->rotate_sh, st->d_means,
-                           st->d_rotations, st->d_sh, ns.g7, 8, s, st->contributed));
-  SS_TRY(ntc_backward_run(&st->grid, &st->mlp, st->n_in, st->src.means, st->rows, st->params,
+                           st->d_rotations, st->d_sh, ns.g7, 8, s, live));
+  return ntc_backward_run(&st->grid, &st->mlp, st->n_in, st->src.means, st->rows, st->params,
                           ns.X, ns.xs, ns.g7, 8, ns.relu, ns.dX,
-                          st->defer_scatter ? nullptr : st->g_tables, st->g_params, s));
+                          st->defer_scatter ? nullptr : st->g_tables, st->g_params, s);
+}
+}  // namespace ss
+
+extern "C" {
+
+int ss_stage1_iter_grads(ss_stage1* st, const ss_camera* cam, const float* target,
+                         int64_t n_pairs, float grad_scale, void* stream) {
+  cudaStream_t s = as_stream(stream);
+  SS_TRY(stage1_view(st, cam, target, n_pairs, grad_scale, 0, s));
+  SS_TRY(stage1_ntc_grads(st, st->contributed, s));
   st->iteration += 1;
   return SS_OK;
+}
+
+int ss_stage1_batch_view(ss_stage1* st, const ss_camera* cam, const float* target,
+                         float grad_scale, int32_t first, void* stream) {
+  cudaStream_t s = as_stream(stream);
+  if (first) {
+    SS_TRY(ss_stage1_iter_begin(st, cam, nullptr, stream));
+  } else {  // the parameters have not moved: same transformed cloud
+    const ss_cloud tc = transformed(st);
+    SS_TRY(raster_begin(&tc, cam, &st->settings, st->geom, nullptr, s));
+  }
+  SS_TRY(stage1_view(st, cam, target, 0, grad_scale, first ? 0 : 1, s));
+  st->iteration += 1;
+  return SS_OK;
+}
+
+int ss_stage1_batch_ntc_grads(ss_stage1* st, void* stream) {
+  return stage1_ntc_grads(st, nullptr, as_stream(stream));
 }
 
 int ss_stage1_table_scatter(ss_stage1* st, void* stream) {

@@ -25,9 +25,13 @@ drive the same code with an oracle-backed stand-in):
   g_flat            packed fp32 gradient [tables | MLP | loss slot]
   n_table           length of the tables part
   n_views           number of training views
-  iterate(view, grad_scale=, adam=False, defer_scatter=, accumulate_stats=, staged=)
+  batch_view(view, grad_scale=, first=, accumulate_stats=, staged=)   one view's render,
+                    loss and raster backward, its transformed-cloud gradient added
+                    to the batch's (first: NTC forward, gradient overwritten)
+  batch_ntc_grads(defer_scatter=)   transform VJP + decoder backward + table scatter
+                    (deferred: table_scatter()) of the batch gradient, once
   stage_target(view, host_tensor)   H2D copy of a view's target into the staging buffer
-  table_scatter()   the deferred hash-table scatter of the last iterate
+  table_scatter()   the deferred hash-table scatter
   apply_adam()      lazy Adam on g_flat (zeroes the table/MLP gradient)
   stats_norm, stats_count   per-Gaussian view-space statistics
   enable_loss_accum()       every iterate adds its loss to the loss slot
@@ -105,18 +109,22 @@ class ViewShardedStage1:
             return
         lo = (b * self.rank) // self.world
         mine = shard_views(batch, self.rank, self.world)
-        last = len(mine) - 1
         split = self.world > 1
+        # the views share the parameters: each adds its transformed-cloud
+        # gradient, and the NTC backward (transform VJP, decoder, scatter) runs
+        # once for the rank's views -- it is linear in that gradient
         for j, v in enumerate(mine):
             if host_targets is not None:
                 tr.stage_target(v, host_targets[v])
-            tr.iterate(v, grad_scale=1.0 / b, adam=False, defer_scatter=split and j == last,
-                       accumulate_stats=flags[lo + j], staged=host_targets is not None)
+            tr.batch_view(v, grad_scale=1.0 / b, first=j == 0, accumulate_stats=flags[lo + j],
+                          staged=host_targets is not None)
+        if mine:
+            tr.batch_ntc_grads(defer_scatter=split)
         if split:  # (a rank without views contributes zeros: the collectives stay matched)
             nt = tr.n_table
             w1 = dist.all_reduce(tr.g_flat[nt:], op=dist.ReduceOp.SUM, group=self.group,
                                  async_op=True)  # decoder grads + loss, under the scatter
-            if last >= 0:
+            if mine:
                 tr.table_scatter()
             w2 = dist.all_reduce(tr.g_flat[:nt], op=dist.ReduceOp.SUM, group=self.group,
                                  async_op=True)

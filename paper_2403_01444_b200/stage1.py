@@ -376,6 +376,46 @@ class Stage1Trainer:
                int(self.lib.ss_profile_enabled()))  # profiled graphs hold event nodes
         self._replay(key, lambda: self._iterate_eager(view, grad_scale, adam, staged, target))
 
+    def batch_view(self, view: int, grad_scale: float, first: bool, staged: bool = False,
+                   accumulate_stats: bool | None = None) -> None:
+        """One view of a batch that shares the parameter state (ss_stage1_batch_view):
+        render, loss and raster backward, its transformed-cloud gradient added
+        to the batch's (first: NTC forward + transform, gradient overwritten).
+        The NTC backward runs once per batch in batch_ntc_grads()."""
+        if self.bins is None:
+            self.plan_capacity()
+        if self.banded:
+            raise DataError("views above the bin workspace train one view per iteration")
+        if accumulate_stats is not None:
+            self.s.accumulate_stats = int(accumulate_stats)
+        cam = self.cam_structs[view]
+
+        def launch():
+            tgt = ptr(self._staging if staged else self.targets[view])
+            self._call(self.lib.ss_stage1_batch_view, C.byref(self.s), C.byref(cam), tgt,
+                       C.c_float(grad_scale), int(bool(first)), stream())
+
+        if not self.use_graphs:
+            launch()
+            return
+        key = ("batch", view, bool(first), float(grad_scale), int(self.s.accumulate_stats),
+               self._staging.data_ptr() if staged else None,
+               int(self.lib.ss_profile_enabled()))
+        self._replay(key, launch)
+
+    def batch_ntc_grads(self, defer_scatter: bool = False) -> None:
+        """Transform VJP + decoder backward (+ table scatter unless deferred) of
+        the accumulated batch gradient (ss_stage1_batch_ntc_grads)."""
+        self.s.defer_scatter = int(defer_scatter)
+
+        def launch():
+            self._call(self.lib.ss_stage1_batch_ntc_grads, C.byref(self.s), stream())
+
+        if not self.use_graphs:
+            launch()
+            return
+        self._replay(("batch_ntc", bool(defer_scatter), int(self.lib.ss_profile_enabled())), launch)
+
     def _replay(self, key, launch) -> None:
         """Capture `launch` into a CUDA graph on first use of `key`, then replay.
         Kernel nodes per graph are counted (graph_launches) for telemetry."""

@@ -100,6 +100,30 @@ class OracleTrainer:
             self.stats_norm += torch.from_numpy(r["render_grads"]["viewspace"])
             self.stats_count += torch.from_numpy(r["render_grads"]["contributed"].astype(np.int64))
 
+    def batch_view(self, view, grad_scale=1.0, first=False, accumulate_stats=False,
+                   staged=False):
+        """One view of a batch: the oracle's gradient of this view, pending
+        until batch_ntc_grads (the device runs the NTC backward once)."""
+        if first:
+            self._batch = None
+        r = self.O.stage1_iteration(self.state, self.sc.cloud, self.sc.cameras[view],
+                                    self.targets[view], apply_adam=False)
+        g = grad_scale * _flat(r["g_tables"], r["g_w"], r["g_b"])
+        self._batch = g if self._batch is None else self._batch + g
+        if self.loss_accum:
+            self.g_flat[self.n_table + self.n_params] += r["loss"]
+        if accumulate_stats:
+            self.stats_norm += torch.from_numpy(r["render_grads"]["viewspace"])
+            self.stats_count += torch.from_numpy(r["render_grads"]["contributed"].astype(np.int64))
+
+    def batch_ntc_grads(self, defer_scatter=False):
+        g, nt = self._batch, self.n_table
+        self.g_flat[nt:nt + self.n_params] += torch.from_numpy(g[nt:])
+        if defer_scatter:
+            self._pending = g[:nt]
+        else:
+            self.g_flat[:nt] += torch.from_numpy(g[:nt])
+
     def table_scatter(self):
         self.g_flat[:self.n_table] += torch.from_numpy(self._pending)
         self._pending = None

@@ -41,6 +41,23 @@ for rep in range(3):
         for i, n in enumerate(names):
             acc[n].append(buf[i])
 out = {n: round(1000 * float(np.mean(x)), 1) for n, x in acc.items() if x}
+# the same iterations from graphs without event nodes, timed whole
+lib.ss_profile_enable(0)
+for v in views:
+    tr.iterate(v, adam=False)
+torch.cuda.synchronize()
+tot = []
+for rep in range(3):
+    for v in views:
+        flush.fill_(rep)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        tr.iterate(v, adam=False)
+        e1.record()
+        torch.cuda.synchronize()
+        tot.append(e0.elapsed_time(e1))
+out["iteration_us"] = round(1000 * float(np.mean(tot)), 1)
+out["sum_of_kernels_us"] = round(sum(v for k, v in out.items() if k != "iteration_us" and v > 0), 1)
 out["pairs"] = int(np.mean(tr.pairs_of_last(len(views))))
 out["sigma"] = sigma
 print(json.dumps(out))
