@@ -922,11 +922,14 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_fwd_kernel(
     }
     last[p] = 0;
     done[p] = (x0 + li % TS >= bp.W) || (y0 + li / TS >= bp.H);
+    // fast path: "done" is T < stop itself (later splats fail T_before >= stop);
+    // pixels outside the image start at T = 0 and are never written
+    if (!TOUCH && done[p]) T[p] = 0.f;
   }
   for (int b = range.x; b < range.y; b += NT) {
     bool all_done = true;
 #pragma unroll
-    for (int p = 0; p < PPT; ++p) all_done &= done[p];
+    for (int p = 0; p < PPT; ++p) all_done &= TOUCH ? done[p] : !(T[p] >= bp.stop);
     if (__syncthreads_count(all_done) == NT) break;
     const int j = b + threadIdx.x;
     if (j < range.y) {
@@ -951,7 +954,7 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_fwd_kernel(
 #pragma unroll
         for (int p = 0; p < PPT; ++p) {
           lgs[p] = po.lg(L, Q, p);
-          live[p] = !done[p] && !(lgs[p] < qlo);
+          live[p] = T[p] >= bp.stop && !(lgs[p] < qlo);
           any_live |= live[p];
           any_near |= live[p] && lgs[p] < qhi;
         }
@@ -974,7 +977,6 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_fwd_kernel(
           C[p][2] = fmaf(wgt, col.z, C[p][2]);
           T[p] *= 1.f - a;
           last[p] = a > 0.f ? b - range.x + k + 1 : last[p];
-          done[p] = done[p] || T[p] < bp.stop;  // later splats fail T_before >= stop
         }
         continue;
       }
