@@ -28,14 +28,14 @@ def sources():
     return sorted(f for f in os.listdir(CSRC) if f.endswith(".cu"))
 
 
-def _compile(src: str) -> tuple[str, str]:
-    out = os.path.join(OBJ, src[:-3] + ".o")
+def _compile(src: str, obj: str = OBJ, defs: tuple = ()) -> tuple[str, str]:
+    out = os.path.join(obj, src[:-3] + ".o")
     inp = os.path.join(CSRC, src)
     deps = [inp] + [os.path.join(CSRC, h) for h in os.listdir(CSRC) if h.endswith(".cuh")]
     deps.append(os.path.join(INCLUDE, "ss_b200.h"))
     if os.path.exists(out) and os.path.getmtime(out) >= max(os.path.getmtime(d) for d in deps):
         return out, ""
-    cmd = [NVCC, *ARCH, *FLAGS, "-c", inp, "-o", out]
+    cmd = [NVCC, *ARCH, *FLAGS, *defs, "-c", inp, "-o", out]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")
@@ -44,24 +44,34 @@ def _compile(src: str) -> tuple[str, str]:
     return out, r.stderr
 
 
-def build(verbose: bool = False) -> str:
-    os.makedirs(OBJ, exist_ok=True)
+def build(verbose: bool = False, defs: tuple = (), lib: str = LIB, obj: str = OBJ) -> str:
+    """defs / lib / obj: a tuning variant (-D flags) built beside the product
+    library, e.g. for tools/ A/B runs with SS_LIB pointing at it."""
+    os.makedirs(obj, exist_ok=True)
     srcs = sources()
     with cf.ThreadPoolExecutor(max_workers=min(8, len(srcs))) as ex:
-        results = list(ex.map(_compile, srcs))
+        results = list(ex.map(lambda f: _compile(f, obj, tuple(defs)), srcs))
     objs = [o for o, _ in results]
     if verbose:
         for o, log in results:
             if log:
                 print(log, file=sys.stderr)
     newest = max(os.path.getmtime(o) for o in objs)
-    if not os.path.exists(LIB) or os.path.getmtime(LIB) < newest:
-        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart"]
+    if not os.path.exists(lib) or os.path.getmtime(lib) < newest:
+        cmd = [NVCC, *ARCH, "-shared", "-o", lib, *objs, "-lcudart"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(verbose="-v" in sys.argv))
+    # python -m paper_2403_01444_b200.build [-v] [--variant NAME -DX=1 ...]
+    args = sys.argv[1:]
+    if "--variant" in args:
+        name = args[args.index("--variant") + 1]
+        defs = tuple(a for a in args if a.startswith("-D"))
+        print(build("-v" in args, defs, os.path.join(ROOT, "build", f"libss_b200_{name}.so"),
+                    os.path.join(ROOT, "build", f"obj_{name}")))
+    else:
+        print(build(verbose="-v" in args))

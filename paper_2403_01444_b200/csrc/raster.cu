@@ -810,12 +810,19 @@ struct __align__(16) SplatRec {
   int rank, pad0, pad1, pad2;
 };
 
-template <int TS>
+#ifndef SS_FWD_PPT16
+#define SS_FWD_PPT16 2
+#endif
+#ifndef SS_BWD_PPT16
+#define SS_BWD_PPT16 4
+#endif
+template <int TS, bool BWD = false>
 struct BlendShape {
-  // 16x16 tiles: 128 threads with two pixels each (rows r and r + 8), which halves
+  // 16x16 tiles: several pixels per thread (whole rows per warp), which divides
   // the per-splat shared-memory loads, loop overhead and (backward) warp
   // reductions per pixel
-  static constexpr int NT = TS == 16 ? 128 : (TS * TS <= 256 ? TS * TS : 256);
+  static constexpr int P16 = BWD ? SS_BWD_PPT16 : SS_FWD_PPT16;
+  static constexpr int NT = TS == 16 ? 256 / P16 : (TS * TS <= 256 ? TS * TS : 256);
   static constexpr int PPT = TS * TS / NT;
 };
 
@@ -868,10 +875,19 @@ __device__ __noinline__ float alpha_f64(const BlendParams& bp, const Geom& g, in
 
 
 // Pixel p of thread t: each warp owns a contiguous run of 32 * PPT pixels of
-// the tile (whole rows).
-template <int TS>
+// the tile (whole rows), or with two pixels per thread on 16x16 tiles an 8x8
+// quadrant (fewer splats touch a quadrant than a 16x4 strip, so more
+// warp-uniform skips; SS_QUAD=0 restores the strips).
+#ifndef SS_QUAD
+#define SS_QUAD 1
+#endif
+template <int TS, int PPT>
 __device__ __forceinline__ int tile_pixel(int t, int p) {
-  return (t >> 5) * (32 * BlendShape<TS>::PPT) + p * 32 + (t & 31);
+  if (SS_QUAD && TS == 16 && PPT == 2) {  // warp w: the 8x8 quadrant w
+    const int w = t >> 5, l = t & 31;
+    return ((w >> 1) * 8 + p * 4 + (l >> 3)) * 16 + (w & 1) * 8 + (l & 7);
+  }
+  return (t >> 5) * (32 * PPT) + p * 32 + (t & 31);
 }
 
 template <int TS, int PPT>
@@ -879,7 +895,7 @@ __device__ __forceinline__ void PixelOffsets<TS, PPT>::init(int t) {
   constexpr float c0 = 0.5f * (TS - 1);
 #pragma unroll
   for (int p = 0; p < PPT; ++p) {
-    const int li = tile_pixel<TS>(t, p);
+    const int li = tile_pixel<TS, PPT>(t, p);
     dx[p] = (float)(li % TS) - c0;
     dy[p] = (float)(li / TS) - c0;
   }
@@ -911,7 +927,7 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_fwd_kernel(
   float px[PPT], py[PPT];
 #pragma unroll
   for (int p = 0; p < PPT; ++p) {
-    const int li = tile_pixel<TS>(threadIdx.x, p);
+    const int li = tile_pixel<TS, PPT>(threadIdx.x, p);
     px[p] = (float)(x0 + li % TS);
     py[p] = (float)(y0 + li / TS);
     T[p] = 1.f;
@@ -958,7 +974,13 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_fwd_kernel(
           any_live |= live[p];
           any_near |= live[p] && lgs[p] < qhi;
         }
-        if (!__any_sync(0xffffffffu, any_live)) continue;  // warp-uniform skip
+        if (!__any_sync(0xffffffffu, any_live)) {  // warp-uniform skip
+          bool alive = false;
+#pragma unroll
+          for (int p = 0; p < PPT; ++p) alive |= T[p] >= bp.stop;
+          if (!__any_sync(0xffffffffu, alive)) break;  // this warp's pixels are all finished
+          continue;
+        }
         const float4 col = s_sp[k].col;
         float av[PPT];
 #pragma unroll
@@ -1052,10 +1074,10 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_fwd_kernel(
 // sum; those lanes add into shared-memory per-splat accumulators, flushed to
 // the per-rank global accumulators once per batch.
 template <int TS>
-__global__ void __launch_bounds__(BlendShape<TS>::NT) blend_bwd_kernel(
+__global__ void __launch_bounds__(BlendShape<TS, true>::NT) blend_bwd_kernel(
     BlendParams bp, Geom g, const uint32_t* __restrict__ vals, const float* __restrict__ d_image,
     int tile0) {
-  constexpr int NT = BlendShape<TS>::NT, PPT = BlendShape<TS>::PPT;
+  constexpr int NT = BlendShape<TS, true>::NT, PPT = BlendShape<TS, true>::PPT;
   constexpr int NA = 9;  // colour 3, M1 2, M2 3, M0
   __shared__ SplatRec s_sp[NT];
   // each warp owns a slot per splat (plain stores, summed at the flush);
@@ -1077,7 +1099,7 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_bwd_kernel(
   int max_last = 0;
 #pragma unroll
   for (int p = 0; p < PPT; ++p) {
-    const int li = tile_pixel<TS>(threadIdx.x, p);
+    const int li = tile_pixel<TS, PPT>(threadIdx.x, p);
     const int pxi = x0 + li % TS, pyi = y0 + li / TS;
     px[p] = (float)pxi;
     py[p] = (float)pyi;
@@ -1492,10 +1514,10 @@ static int launch_blend_bwd(int ts, int64_t ntiles, cudaStream_t st, const Blend
                             int tile0 = 0) {
   const unsigned grid = (unsigned)ntiles;
   switch (ts) {
-    case 8: blend_bwd_kernel<8><<<grid, BlendShape<8>::NT, 0, st>>>(bp, g, vals, d_image, tile0); break;
-    case 16: blend_bwd_kernel<16><<<grid, BlendShape<16>::NT, 0, st>>>(bp, g, vals, d_image, tile0); break;
-    case 32: blend_bwd_kernel<32><<<grid, BlendShape<32>::NT, 0, st>>>(bp, g, vals, d_image, tile0); break;
-    default: blend_bwd_kernel<64><<<grid, BlendShape<64>::NT, 0, st>>>(bp, g, vals, d_image, tile0); break;
+    case 8: blend_bwd_kernel<8><<<grid, BlendShape<8, true>::NT, 0, st>>>(bp, g, vals, d_image, tile0); break;
+    case 16: blend_bwd_kernel<16><<<grid, BlendShape<16, true>::NT, 0, st>>>(bp, g, vals, d_image, tile0); break;
+    case 32: blend_bwd_kernel<32><<<grid, BlendShape<32, true>::NT, 0, st>>>(bp, g, vals, d_image, tile0); break;
+    default: blend_bwd_kernel<64><<<grid, BlendShape<64, true>::NT, 0, st>>>(bp, g, vals, d_image, tile0); break;
   }
   SS_CHECK_LAUNCH("blend_bwd_kernel");
   return SS_OK;
