@@ -137,7 +137,10 @@ def build_problem(cfg_idx):
     from paper_2403_01444_b200.types import HashGridConfig
 
     sc = scenes.config(cfg_idx)
-    cache = NeuralTransformationCache(HashGridConfig.from_any(sc.grid), output_init="identity")
+    # BASELINE.json configs[1] (and 3, 4 "NTC as config 1"): fp16 MLP weights
+    # with fp32 accumulation; cfg0 / cfg2 fp32
+    cache = NeuralTransformationCache(HashGridConfig.from_any(sc.grid), output_init="identity",
+                                      mlp_dtype=sc.mlp_dtype)
     moved = scenes.moved_cloud(sc.cloud, np.random.default_rng(7), axis=(0.3, 1.0, 0.2),
                                deg=1.5, shift=(0.01, -0.005, 0.008))
     dm = DeviceCloud(moved)
@@ -475,8 +478,11 @@ def main():
                            kernel_times="CUDA events recorded inside the replayed iteration "
                                         "graphs (a second pass over the same positions)",
                            mean_tile_pairs=units["D"],
-                           decoder=["fp32 FFMA", "tcgen05 3xTF32",
-                                    "tcgen05 tf32"][lib.ss_get_mlp_mode()]),
+                           decoder=("tcgen05 kind::f16: fp16 weights and activations, fp32 "
+                                    "accumulation (BASELINE configs[1])"
+                                    if sc.mlp_dtype == "f16" else
+                                    ["fp32 FFMA", "tcgen05 3xTF32",
+                                     "tcgen05 tf32"][lib.ss_get_mlp_mode()])),
             "gpu_launches": int(round(per_iter_launches * len(positions))),
             "roofline": roof,
             "roofline_tensor": ({"kernel": "decoder_forward", "achieved": dec["achieved_tflops"],

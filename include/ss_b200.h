@@ -54,8 +54,15 @@ typedef struct ss_grid {
 /* NeuralTransformationCache decoder (ntc.py:102-128): in -> hidden^n_hidden -> 7,
  * ReLU hidden layers.  Supported: in_dim <= 64, hidden_dim <= 64, n_hidden 1|2,
  * out_dim 7. */
+/* precision: SS_MLP_FP32 -- fp32-accurate decoder (3xTF32 forward, bf16x3
+ * backward on tensor cores); SS_MLP_F16 -- fp16 weights, biases and
+ * activations with fp32 accumulation (BASELINE config 1's "fp16 MLP weights";
+ * the reference itself is float64 throughout, ntc.py:241-276). */
+#define SS_MLP_FP32 0
+#define SS_MLP_F16 1
 typedef struct ss_mlp {
   int32_t in_dim, hidden_dim, n_hidden, out_dim;
+  int32_t precision;
 } ss_mlp;
 
 /* Device parameter layout: one packed fp32 vector W0 | b0 | [W1 | b1] | W2 | b2,

@@ -11,7 +11,7 @@ Containers used here (all float64 numpy unless noted):
                 opacity_logits (N,), sh (N,K,3) with K=(deg+1)^2)
   camera = dict(w2c (4,4), fx, fy, cx, cy, width, height, near)
   grid   = dict(levels, features, log2_table, base, growth, lo (3,), hi (3,))
-  mlp    = dict(weights [W_i (fan_in, fan_out)], biases [b_i])
+  mlp    = dict(weights [W_i (fan_in, fan_out)], biases [b_i], optional dtype "f16")
 """
 
 from __future__ import annotations
@@ -108,26 +108,44 @@ def gather(tables: np.ndarray, idx: np.ndarray, w: np.ndarray) -> np.ndarray:
     return feats.reshape(b, -1)
 
 
+def _f16(a):
+    return np.asarray(a).astype(np.float16).astype(np.float64)
+
+
+def _mlp_operands(mlp: dict):
+    """The decoder's operands.  mlp["dtype"] == "f16" (BASELINE config 1's
+    fp16 MLP weights, fp32 accumulation -- not a reference mode: the reference
+    is float64, ntc.py:241-276) rounds weights, biases, the input features and
+    every hidden activation to float16 (round to nearest even) and accumulates
+    exactly, as the tensor-core kernel does up to fp32 summation order."""
+    if mlp.get("dtype", "f32") == "f16":
+        return [_f16(w) for w in mlp["weights"]], [_f16(b) for b in mlp["biases"]], _f16
+    return mlp["weights"], mlp["biases"], lambda a: a
+
+
 def mlp_forward(mlp: dict, feats: np.ndarray):
     """ReLU hidden layers, linear output; ntc.py:241-248."""
-    z = feats
+    ws, bs, rnd = _mlp_operands(mlp)
+    z = rnd(feats)
     hidden = []
-    for wi, bi in zip(mlp["weights"][:-1], mlp["biases"][:-1]):
-        z = np.maximum(z @ wi + bi, 0.0)
+    for wi, bi in zip(ws[:-1], bs[:-1]):
+        z = rnd(np.maximum(z @ wi + bi, 0.0))
         hidden.append(z)
-    out = z @ mlp["weights"][-1] + mlp["biases"][-1]
+    out = z @ ws[-1] + bs[-1]
     return out, hidden
 
 
 def mlp_backward(mlp: dict, feats, hidden, g_out):
-    """dW, db and dL/dfeats; ntc.py:258-276."""
-    ins = [feats] + hidden
+    """dW, db and dL/dfeats; ntc.py:258-276 (f16: the straight-through
+    gradient of the rounded forward, see _mlp_operands)."""
+    ws, _, rnd = _mlp_operands(mlp)
+    ins = [rnd(feats)] + hidden
     delta = g_out
-    gw, gb = [None] * len(mlp["weights"]), [None] * len(mlp["weights"])
-    for i in range(len(mlp["weights"]) - 1, -1, -1):
+    gw, gb = [None] * len(ws), [None] * len(ws)
+    for i in range(len(ws) - 1, -1, -1):
         gw[i] = ins[i].T @ delta
         gb[i] = delta.sum(axis=0)
-        delta = delta @ mlp["weights"][i].T
+        delta = delta @ ws[i].T
         if i > 0:
             delta = delta * (hidden[i - 1] > 0)
     return gw, gb, delta

@@ -29,9 +29,12 @@ class Grid(C.Structure):
                 ("aabb_min", C.c_double * 3), ("aabb_max", C.c_double * 3)]
 
 
+MLP_FP32, MLP_F16 = 0, 1
+
+
 class Mlp(C.Structure):
     _fields_ = [("in_dim", C.c_int32), ("hidden_dim", C.c_int32), ("n_hidden", C.c_int32),
-                ("out_dim", C.c_int32)]
+                ("out_dim", C.c_int32), ("precision", C.c_int32)]
 
 
 class MlpLayout(C.Structure):

@@ -313,9 +313,9 @@ int transform_vjp_run(const ss_cloud* src, int64_t n, const int32_t* rows, const
 // decoder on tensor cores (mlp_tc.cu); mode 0 = FFMA fp32, 1 = 3xTF32, 2 = tf32
 namespace ss {
 int mlp_mode();
-int mlp_fwd_tc(int in_pad, int n_hidden, int64_t n, const float* X, int xs, const float* params,
+int mlp_fwd_tc(int in_pad, int n_hidden, int f16, int64_t n, const float* X, int xs, const float* params,
                float* out, int os, uint64_t* relu_masks, cudaStream_t st);
-int mlp_bwd_tc(int in_pad, int n_hidden, int64_t n, const float* X, int xs, const float* g,
+int mlp_bwd_tc(int in_pad, int n_hidden, int f16, int64_t n, const float* X, int xs, const float* g,
                int gs, const uint64_t* relu_masks, const float* params, float* dX,
                float* g_params, cudaStream_t st);
 }  // namespace ss

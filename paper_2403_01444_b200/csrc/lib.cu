@@ -139,8 +139,9 @@ int64_t ss_launch_count(void) { return ss::g_launches.load(); }
 int ss_mlp_get_layout(const ss_mlp* mlp, ss_mlp_layout* out) {
   if (!mlp || !out) return SS_ERR_DATA;
   if (mlp->in_dim < 1 || mlp->in_dim > 64 || mlp->hidden_dim < 1 || mlp->hidden_dim > 64 ||
-      mlp->n_hidden < 1 || mlp->n_hidden > 2 || mlp->out_dim != 7) {
-    ss::set_error("unsupported decoder shape (in<=64, hidden<=64, 1-2 hidden layers, 7 outputs)");
+      mlp->n_hidden < 1 || mlp->n_hidden > 2 || mlp->out_dim != 7 ||
+      (mlp->precision != SS_MLP_FP32 && mlp->precision != SS_MLP_F16)) {
+    ss::set_error("unsupported decoder (in<=64, hidden<=64, 1-2 hidden layers, 7 outputs, precision fp32|f16)");
     return SS_ERR_DATA;
   }
   ss_mlp_layout L{};

@@ -12,11 +12,16 @@
 // Precision:
 //  * forward: kind::tf32 with every operand split into tf32 hi + lo and three
 //    products per K step (3xTF32), i.e. fp32-level accuracy; mode 2 = tf32.
+//    fp16-weight decoders (ss_mlp.precision = SS_MLP_F16, BASELINE config 1):
+//    kind::f16 with weights, biases and activations rounded to fp16, one
+//    product per K = 16 step, fp32 accumulation.
 //  * backward: kind::f16 with bf16 hi + lo operands and three products per K
 //    step (~16 mantissa bits, fp32 accumulation), because its transposed
 //    operands need MN-major descriptors (16-bit types).  The ReLU decisions are
 //    the forward's (relu_masks), so the gradient is that of the function the
-//    forward evaluated.
+//    forward evaluated.  For fp16-weight decoders the backward takes the same
+//    fp16-rounded weights, inputs and hidden activations as the forward, so
+//    it is the (straight-through) gradient of the fp16 forward.
 #include "common.cuh"
 #include "umma.cuh"
 
@@ -61,12 +66,14 @@ __device__ __forceinline__ void sync_mma(uint64_t* bar, uint32_t& phase) {
 }
 
 // ---------------------------------------------------------------- tf32 pieces
+// P = 3: 3xTF32, P = 1: tf32, P = 0: fp16 operands
 template <int IN, int NL, int P>
 struct TcFwdSmem {  // the weights only: activations live in TMEM
   static constexpr int PL = P == 3 ? 2 : 1;  // hi (+ lo) planes
-  static constexpr uint32_t W0 = umma::tile_bytes(64, IN);
-  static constexpr uint32_t W1 = NL == 2 ? umma::tile_bytes(64, 64) : 0;
-  static constexpr uint32_t W2 = umma::tile_bytes(16, 64);
+  static constexpr uint32_t W0 = P == 0 ? umma::tile16_bytes(64, IN) : umma::tile_bytes(64, IN);
+  static constexpr uint32_t W1 =
+      NL == 2 ? (P == 0 ? umma::tile16_bytes(64, 64) : umma::tile_bytes(64, 64)) : 0;
+  static constexpr uint32_t W2 = P == 0 ? umma::tile16_bytes(16, 64) : umma::tile_bytes(16, 64);
   static constexpr uint32_t oW0 = 0;
   static constexpr uint32_t oW1 = oW0 + PL * W0;
   static constexpr uint32_t oW2 = oW1 + PL * W1;
@@ -235,24 +242,31 @@ __global__ void __launch_bounds__(NT_FWD, 1) mlp_fwd_tc_kernel(int64_t n, const 
   __shared__ float sbias[64 + 64 + 8];
   const int tid = threadIdx.x, warp = tid >> 5;
   // ---- stage the weights as K-major B tiles (rows = output unit, cols = input)
+  auto put_w = [&](uint32_t o, uint32_t plane, int nn, int k, int cols, float w) {
+    if (P == 0)
+      *reinterpret_cast<__half*>(sm + o + umma::tile16_off(nn, k, cols)) = __float2half_rn(w);
+    else
+      put<P>(sm + o, plane, umma::tile_off(nn, k, cols), w);
+  };
   for (int i = tid; i < 64 * IN; i += NT_FWD) {
     const int nn = i / IN, k = i % IN;
-    put<P>(sm + S::oW0, S::W0, umma::tile_off(nn, k, IN), params[L::W0 + k * 64 + nn]);
+    put_w(S::oW0, S::W0, nn, k, IN, params[L::W0 + k * 64 + nn]);
   }
   if (NL == 2)
     for (int i = tid; i < 64 * 64; i += NT_FWD) {
       const int nn = i / 64, k = i % 64;
-      put<P>(sm + S::oW1, S::W1, umma::tile_off(nn, k, 64), params[L::W1 + k * 64 + nn]);
+      put_w(S::oW1, S::W1, nn, k, 64, params[L::W1 + k * 64 + nn]);
     }
   for (int i = tid; i < 16 * 64; i += NT_FWD) {
     const int nn = i / 64, k = i % 64;
-    put<P>(sm + S::oW2, S::W2, umma::tile_off(nn, k, 64), nn < 8 ? params[L::W2 + k * 8 + nn] : 0.f);
+    put_w(S::oW2, S::W2, nn, k, 64, nn < 8 ? params[L::W2 + k * 8 + nn] : 0.f);
   }
+  auto bias = [&](float b) { return P == 0 ? umma::round_f16(b) : b; };
   if (tid < 64) {
-    sbias[tid] = params[L::B0 + tid];
-    sbias[64 + tid] = NL == 2 ? params[L::B1 + tid] : 0.f;
+    sbias[tid] = bias(params[L::B0 + tid]);
+    sbias[64 + tid] = NL == 2 ? bias(params[L::B1 + tid]) : 0.f;
   }
-  if (tid < 8) sbias[128 + tid] = params[L::B2 + tid];
+  if (tid < 8) sbias[128 + tid] = bias(params[L::B2 + tid]);
   if (tid == 0) {
     for (int s = 0; s < 2; ++s) {
       umma::mbar_init(&ready[s], NT / 32);
@@ -270,11 +284,14 @@ __global__ void __launch_bounds__(NT_FWD, 1) mlp_fwd_tc_kernel(int64_t n, const 
 
   if (warp == NT / 32) {
     // ================= MMA warp: one elected lane issues, in tile/slot order
-    const Op32 dW0 = op32(umma::smem_u32(sm + S::oW0), S::W0, IN);
-    const Op32 dW1 = op32(umma::smem_u32(sm + S::oW1), S::W1, 64);
-    const Op32 dW2 = op32(umma::smem_u32(sm + S::oW2), S::W2, 64);
-    constexpr uint32_t id64 = umma::idesc_tf32(128, 64, 0, 0);
-    constexpr uint32_t id16 = umma::idesc_tf32(128, 16, 0, 0);
+    const Op32 dW0 = P == 0 ? Op32{umma::desc16_k(umma::smem_u32(sm + S::oW0), IN, 0), 0}
+                            : op32(umma::smem_u32(sm + S::oW0), S::W0, IN);
+    const Op32 dW1 = P == 0 ? Op32{umma::desc16_k(umma::smem_u32(sm + S::oW1), 64, 0), 0}
+                            : op32(umma::smem_u32(sm + S::oW1), S::W1, 64);
+    const Op32 dW2 = P == 0 ? Op32{umma::desc16_k(umma::smem_u32(sm + S::oW2), 64, 0), 0}
+                            : op32(umma::smem_u32(sm + S::oW2), S::W2, 64);
+    constexpr uint32_t id64 = P == 0 ? umma::idesc_f16(128, 64, 0, 0) : umma::idesc_tf32(128, 64, 0, 0);
+    constexpr uint32_t id16 = P == 0 ? umma::idesc_f16(128, 16, 0, 0) : umma::idesc_tf32(128, 16, 0, 0);
     uint32_t ph[2] = {0u, 0u};
     int nev = 0;
     for (int64_t t0 = blockIdx.x; t0 < ntiles; t0 += 2 * G) {
@@ -294,11 +311,18 @@ __global__ void __launch_bounds__(NT_FWD, 1) mlp_fwd_tc_kernel(int64_t n, const 
             const Op32& B = layer == 0 ? dW0 : (layer == 1 ? dW1 : dW2);
             const uint32_t acc = base + (layer == 2 ? 192u : 128u);
             const uint32_t id = layer == 2 ? id16 : id64;
-            constexpr int nk0 = IN / 8;
+            // K steps: 8 (tf32) or 16 (fp16) elements, 8 TMEM columns and
+            // 256 bytes of B either way
+            constexpr int KS = P == 0 ? 16 : 8;
+            constexpr int nk0 = IN / KS, nk = 64 / KS;
 #pragma unroll
-            for (int k = 0; k < 8; ++k) {
+            for (int k = 0; k < nk; ++k) {
               if (layer == 0 && k >= nk0) break;
               const uint64_t d = 16ull * k;
+              if (P == 0) {
+                umma::mma_f16_ts_elect(acc, base + 8u * k, B.hi + d, id, k > 0);
+                continue;
+              }
               umma::mma_tf32_ts_elect(acc, base + 8u * k, B.hi + d, id, k > 0);
               if (P == 3) {
                 umma::mma_tf32_ts_elect(acc, base + 8u * k, B.lo + d, id, 1);
@@ -335,7 +359,12 @@ __global__ void __launch_bounds__(NT_FWD, 1) mlp_fwd_tc_kernel(int64_t n, const 
 #pragma unroll
       for (int b = 0; b < XSlice<IN>::NB; ++b) {
         const int c = 8 * q + 32 * b;
-        if (c < IN) {
+        if (c < IN && P == 0) {  // fp16 pairs: columns c/2 .. c/2 + 3
+          uint32_t u[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) u[j] = umma::pack_f16(xr[s].v[b][2 * j], xr[s].v[b][2 * j + 1]);
+          umma::tmem_st4u(base + (uint32_t)(c / 2), u);
+        } else if (c < IN) {
           float h[8], l[8];
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
@@ -358,18 +387,38 @@ __global__ void __launch_bounds__(NT_FWD, 1) mlp_fwd_tc_kernel(int64_t n, const 
     auto hidden = [&](int s, int layer, int64_t t) {
       wait_done(s);
       const uint32_t base = tmem + 256u * s + lane;
-      float v[16], l[16];
-      umma::tmem_ld16(base + 128u + (uint32_t)c0, v);
       uint32_t m = 0;
+      if (P == 0) {
+        float v[16];
+        umma::tmem_ld16(base + 128u + (uint32_t)c0, v);
+        uint32_t u[8];
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const float x = fmaxf(v[j] + sbias[64 * layer + c0 + j], 0.f);
-        m |= (uint32_t)(x > 0.f) << j;
-        v[j] = umma::to_tf32(x);
-        l[j] = umma::to_tf32(x - v[j]);
+        for (int j = 0; j < 16; ++j) {
+          v[j] = fmaxf(v[j] + sbias[64 * layer + c0 + j], 0.f);
+          m |= (uint32_t)(v[j] > 0.f) << j;
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) u[j] = umma::pack_f16(v[2 * j], v[2 * j + 1]);
+        umma::tmem_st8u(base + (uint32_t)(c0 / 2), u);
+      } else {
+        // two 8-column halves keep the live registers low (one CTA of 544
+        // threads caps them at 96 per thread)
+#pragma unroll
+        for (int hf = 0; hf < 2; ++hf) {
+          const int cc = c0 + 8 * hf;
+          float v[8], l[8];
+          umma::tmem_ld8(base + 128u + (uint32_t)cc, v);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const float x = fmaxf(v[j] + sbias[64 * layer + cc + j], 0.f);
+            m |= (uint32_t)(x > 0.f) << (8 * hf + j);
+            v[j] = umma::to_tf32(x);
+            l[j] = umma::to_tf32(x - v[j]);
+          }
+          umma::tmem_st8(base + (uint32_t)cc, v);
+          if (P == 3) umma::tmem_st8(base + 64u + (uint32_t)cc, l);
+        }
       }
-      umma::tmem_st16(base + (uint32_t)c0, v);
-      if (P == 3) umma::tmem_st16(base + 64u + (uint32_t)c0, l);
       arrive(s);
       // the backward reuses the forward's ReLU decisions (self-consistent
       // gradient): 16-bit quarter q of the row's 64-bit mask of this layer
@@ -483,7 +532,7 @@ struct TcBwdSmem {
 };
 }  // namespace
 
-template <int IN, int NL>
+template <int IN, int NL, bool H16>
 __global__ void __launch_bounds__(NT, 1) mlp_bwd_tc_kernel(
     int64_t n, const float* __restrict__ X, int xs, const float* __restrict__ g_out, int gs,
     const uint64_t* __restrict__ relu_masks, const float* __restrict__ params,
@@ -499,24 +548,26 @@ __global__ void __launch_bounds__(NT, 1) mlp_bwd_tc_kernel(
   const int tid = threadIdx.x, warp = tid >> 5, lane_id = tid & 31;
   const int r = tid & 127, q = tid >> 7;
   const int c0 = 16 * q;  // this thread's 16 columns of every 64-wide accumulator
+  // H16: the fp16-weight decoder's operands (fp16 values split exactly into bf16 hi + lo)
+  auto rnd = [](float x) { return H16 ? umma::round_f16(x) : x; };
   // ---- weights as bf16 hi/lo tiles: W0t (j, f) = W0[f][j]; W1t (j, i) = W1[i][j];
   //      W2t (o, j) = W2[j][o] (rows 7..15 zero)
   for (int i = tid; i < 64 * IN; i += NT) {
     const int j = i / IN, f = i % IN;
-    put_scalar(sm + S::oW0, S::W0, j, f, IN, params[L::W0 + f * 64 + j]);
+    put_scalar(sm + S::oW0, S::W0, j, f, IN, rnd(params[L::W0 + f * 64 + j]));
   }
   if (NL == 2)
     for (int i = tid; i < 64 * 64; i += NT) {
       const int j = i / 64, k = i % 64;
-      put_scalar(sm + S::oW1, S::W1, j, k, 64, params[L::W1 + k * 64 + j]);
+      put_scalar(sm + S::oW1, S::W1, j, k, 64, rnd(params[L::W1 + k * 64 + j]));
     }
   for (int i = tid; i < 16 * 64; i += NT) {
     const int o = i / 64, j = i % 64;
-    put_scalar(sm + S::oW2, S::W2, o, j, 64, o < 7 ? params[L::W2 + j * 8 + o] : 0.f);
+    put_scalar(sm + S::oW2, S::W2, o, j, 64, o < 7 ? rnd(params[L::W2 + j * 8 + o]) : 0.f);
   }
   if (tid < 64) {
-    sbias[tid] = params[L::B0 + tid];
-    sbias[64 + tid] = NL == 2 ? params[L::B1 + tid] : 0.f;
+    sbias[tid] = rnd(params[L::B0 + tid]);
+    sbias[64 + tid] = NL == 2 ? rnd(params[L::B1 + tid]) : 0.f;
   }
   // constant columns: X col IN = 1 (db0), H1 col 64 = 1 (db1), G cols 8..15 = 0
   {
@@ -586,6 +637,10 @@ __global__ void __launch_bounds__(NT, 1) mlp_bwd_tc_kernel(
 #pragma unroll
     for (int b = 0; b < XSlice<IN>::NB; ++b) {
       const int c = 8 * q + 32 * b;
+      if (H16) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) xr.v[b][j] = rnd(xr.v[b][j]);
+      }
       if (c < IN) put8(sm + S::oX, S::X, r, c, XC, xr.v[b]);
     }
     if (q == 0) {
@@ -649,7 +704,7 @@ __global__ void __launch_bounds__(NT, 1) mlp_bwd_tc_kernel(
       umma::tmem_ld16(tmem + S::cH1 + lane + c0, v);
 #pragma unroll
       for (int j = 0; j < 16; ++j)
-        v[j] = ((mask1 >> j) & 1) ? fmaxf(v[j] + sbias[c0 + j], 0.f) : 0.f;
+        v[j] = ((mask1 >> j) & 1) ? rnd(fmaxf(v[j] + sbias[c0 + j], 0.f)) : 0.f;
       put8(sm + S::oH1, S::H1, r, c0, HC, v);
       put8(sm + S::oH1, S::H1, r, c0 + 8, HC, v + 8);
       umma::tmem_ld16(tmem + S::cDL + lane + c0, v);
@@ -679,7 +734,7 @@ __global__ void __launch_bounds__(NT, 1) mlp_bwd_tc_kernel(
       umma::tmem_ld16(tmem + S::cH2 + lane + c0, v);
 #pragma unroll
       for (int j = 0; j < 16; ++j)
-        v[j] = ((mask2 >> j) & 1) ? fmaxf(v[j] + sbias[64 + c0 + j], 0.f) : 0.f;
+        v[j] = ((mask2 >> j) & 1) ? rnd(fmaxf(v[j] + sbias[64 + c0 + j], 0.f)) : 0.f;
       put8(sm + S::oH2, S::H2, r, c0, 64, v);
       put8(sm + S::oH2, S::H2, r, c0 + 8, 64, v + 8);
       umma::tmem_ld16(tmem + S::cD1 + lane + c0, v);
@@ -817,26 +872,27 @@ static int launch_tc(int64_t n, const float* X, int xs, const float* params, flo
   return SS_OK;
 }
 
-int mlp_fwd_tc(int in_pad, int n_hidden, int64_t n, const float* X, int xs, const float* params,
-               float* out, int os, uint64_t* masks, cudaStream_t st) {
+int mlp_fwd_tc(int in_pad, int n_hidden, int f16, int64_t n, const float* X, int xs,
+               const float* params, float* out, int os, uint64_t* masks, cudaStream_t st) {
   const bool exact = g_mlp_mode != 2;
 #define SS_TC(IN, NL)                                                                    \
   if (in_pad == IN && n_hidden == NL)                                                    \
-    return exact ? launch_tc<IN, NL, 3>(n, X, xs, params, out, os, masks, st)           \
-                 : launch_tc<IN, NL, 1>(n, X, xs, params, out, os, masks, st);
+    return f16 ? launch_tc<IN, NL, 0>(n, X, xs, params, out, os, masks, st)             \
+               : exact ? launch_tc<IN, NL, 3>(n, X, xs, params, out, os, masks, st)     \
+                       : launch_tc<IN, NL, 1>(n, X, xs, params, out, os, masks, st);
   SS_TC(16, 1) SS_TC(16, 2) SS_TC(32, 1) SS_TC(32, 2) SS_TC(64, 1) SS_TC(64, 2)
 #undef SS_TC
   set_error("mlp_fwd_tc: unsupported decoder shape");
   return SS_ERR_DATA;
 }
 
-template <int IN, int NL>
+template <int IN, int NL, bool H16>
 static int launch_bwd_tc(int64_t n, const float* X, int xs, const float* g, int gs,
                          const uint64_t* masks, const float* params, float* dX, float* g_params,
                          cudaStream_t st) {
   constexpr uint32_t smem = TcBwdSmem<IN, NL>::BYTES;
   static_assert(smem <= 220 * 1024, "backward tiles exceed shared memory");
-  auto k = mlp_bwd_tc_kernel<IN, NL>;
+  auto k = mlp_bwd_tc_kernel<IN, NL, H16>;
   SS_CUDA(smem_attr_once(k, (int)smem));
   const unsigned grid = (unsigned)std::min<int64_t>((n + 127) / 128, (int64_t)num_sms_tc());
   k<<<grid, NT, smem, st>>>(n, X, xs, g, gs, masks, params, dX, g_params);
@@ -844,16 +900,17 @@ static int launch_bwd_tc(int64_t n, const float* X, int xs, const float* g, int 
   return SS_OK;
 }
 
-int mlp_bwd_tc(int in_pad, int n_hidden, int64_t n, const float* X, int xs, const float* g,
-               int gs, const uint64_t* masks, const float* params, float* dX, float* g_params,
-               cudaStream_t st) {
+int mlp_bwd_tc(int in_pad, int n_hidden, int f16, int64_t n, const float* X, int xs,
+               const float* g, int gs, const uint64_t* masks, const float* params, float* dX,
+               float* g_params, cudaStream_t st) {
   if (!masks) {
     set_error("mlp_bwd_tc: the forward's ReLU masks are required");
     return SS_ERR_DATA;
   }
-#define SS_TCB(IN, NL)                \
-  if (in_pad == IN && n_hidden == NL) \
-    return launch_bwd_tc<IN, NL>(n, X, xs, g, gs, masks, params, dX, g_params, st);
+#define SS_TCB(IN, NL)                                                                 \
+  if (in_pad == IN && n_hidden == NL)                                                  \
+    return f16 ? launch_bwd_tc<IN, NL, true>(n, X, xs, g, gs, masks, params, dX, g_params, st) \
+               : launch_bwd_tc<IN, NL, false>(n, X, xs, g, gs, masks, params, dX, g_params, st);
   SS_TCB(16, 1) SS_TCB(16, 2) SS_TCB(32, 1) SS_TCB(32, 2) SS_TCB(64, 1) SS_TCB(64, 2)
 #undef SS_TCB
   set_error("mlp_bwd_tc: unsupported decoder shape");

@@ -1072,8 +1072,9 @@ int ntc_forward_run(const ss_grid* g, const ss_mlp* mlp, int64_t n, const float*
   SS_CHECK_LAUNCH("gather_kernel");
   prof_end(PH_GATHER, st);
   prof_begin(PH_DECODER_FWD, st);
-  if (mlp_mode() != 0)
-    SS_TRY(mlp_fwd_tc(xs, mlp->n_hidden, n, X, xs, params, out, os, relu, st));  // tcgen05
+  const int f16 = mlp->precision == SS_MLP_F16;  // tensor cores only
+  if (f16 || mlp_mode() != 0)
+    SS_TRY(mlp_fwd_tc(xs, mlp->n_hidden, f16, n, X, xs, params, out, os, relu, st));  // tcgen05
   else
     SS_TRY(dispatch_mlp(mlp, MlpFwd{n, X, xs, params, out, os, st}));
   prof_end(PH_DECODER_FWD, st);
@@ -1087,8 +1088,9 @@ int ntc_backward_run(const ss_grid* g, const ss_mlp* mlp, int64_t n, const float
   SS_TRY(check_grid(g, mlp));
   if (n == 0) return SS_OK;
   prof_begin(PH_DECODER_BWD, st);
-  if (mlp_mode() != 0)
-    SS_TRY(mlp_bwd_tc(xs, mlp->n_hidden, n, X, xs, g_out, gs, relu, params, dX, g_params, st));
+  const int f16 = mlp->precision == SS_MLP_F16;
+  if (f16 || mlp_mode() != 0)
+    SS_TRY(mlp_bwd_tc(xs, mlp->n_hidden, f16, n, X, xs, g_out, gs, relu, params, dX, g_params, st));
   else
     SS_TRY(dispatch_mlp(mlp, MlpBwd{n, X, xs, g_out, gs, params, dX, g_params, st}));
   prof_end(PH_DECODER_BWD, st);

@@ -58,9 +58,17 @@ def grid_struct(g: HashGridConfig) -> _lib.Grid:
     return s
 
 
-def mlp_struct(in_dim: int, hidden_dim: int, n_hidden: int) -> _lib.Mlp:
+MLP_DTYPES = {"f32": _lib.MLP_FP32, "f16": _lib.MLP_F16}
+
+
+def mlp_struct(in_dim: int, hidden_dim: int, n_hidden: int, mlp_dtype: str = "f32") -> _lib.Mlp:
+    """mlp_dtype "f16": fp16 weights / activations with fp32 accumulation
+    (BASELINE config 1); "f32": the fp32-accurate decoder."""
+    if mlp_dtype not in MLP_DTYPES:
+        raise DataError(f"unknown mlp_dtype {mlp_dtype!r} (f32 | f16)")
     m = _lib.Mlp()
     m.in_dim, m.hidden_dim, m.n_hidden, m.out_dim = in_dim, hidden_dim, n_hidden, 7
+    m.precision = MLP_DTYPES[mlp_dtype]
     return m
 
 

@@ -46,7 +46,11 @@ class ForwardContext:
 
 class NeuralTransformationCache:
     def __init__(self, grid: HashGridConfig = HashGridConfig(), hidden_layers: int = 2,
-                 hidden_dim: int = 64, output_init: str = "identity", seed: int = 0) -> None:
+                 hidden_dim: int = 64, output_init: str = "identity", seed: int = 0,
+                 mlp_dtype: str = "f32") -> None:
+        # mlp_dtype (extension, keyword-only use): "f16" runs the decoder with
+        # fp16 weights and activations, fp32 accumulation (BASELINE config 1);
+        # parameters and Adam state stay fp32 / float64 as in the reference
         if output_init not in ("identity", "random"):
             raise DataError(f"unknown output_init {output_init!r}")
         if hidden_layers not in (1, 2) or hidden_dim > 64:
@@ -55,6 +59,9 @@ class NeuralTransformationCache:
         self.hidden_layers = hidden_layers
         self.hidden_dim = hidden_dim
         self.output_init = output_init
+        if mlp_dtype not in ("f32", "f16"):
+            raise DataError(f"unknown mlp_dtype {mlp_dtype!r}")
+        self.mlp_dtype = mlp_dtype
         g = self.grid
         # identical RNG sequence to ntc.py:100-123
         rng = np.random.default_rng(seed)
@@ -108,7 +115,8 @@ class NeuralTransformationCache:
     # ---- device views of the current parameters
     def _dev(self):
         dev = require_cuda()
-        m = mlp_struct(self.weights[0].shape[0], self.hidden_dim, self.hidden_layers)
+        m = mlp_struct(self.weights[0].shape[0], self.hidden_dim, self.hidden_layers,
+                       self.mlp_dtype)
         lay = mlp_layout(m)
         return (dev, grid_struct(self.grid), m, lay, to_dev(self.tables, dev=dev),
                 to_dev(pack_params(self.weights, self.biases, lay), dev=dev))

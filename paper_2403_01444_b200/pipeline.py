@@ -40,7 +40,8 @@ class Stage1Result:
 def _clone(cache) -> NeuralTransformationCache:
     """clone_cache (pipeline.py:213-219) into this package's cache class."""
     out = NeuralTransformationCache(cache.grid, hidden_layers=len(cache.weights) - 1,
-                                    hidden_dim=int(np.shape(cache.weights[0])[1]))
+                                    hidden_dim=int(np.shape(cache.weights[0])[1]),
+                                    mlp_dtype=getattr(cache, "mlp_dtype", "f32"))
     out.tables[:] = cache.tables
     for i in range(len(cache.weights)):
         out.weights[i][:] = cache.weights[i]

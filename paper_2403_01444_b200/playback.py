@@ -67,7 +67,8 @@ def apply_ntc_device(dcloud: _Cloud, cache, rotate_sh: bool = True) -> _Cloud:
         return out
     weights = [np.asarray(w) for w in cache.weights]
     biases = [np.asarray(b) for b in cache.biases]
-    m = mlp_struct(weights[0].shape[0], weights[0].shape[1], len(weights) - 1)
+    m = mlp_struct(weights[0].shape[0], weights[0].shape[1], len(weights) - 1,
+                   getattr(cache, "mlp_dtype", "f32"))
     tab = to_dev(np.asarray(cache.tables), dev=dev)
     par = to_dev(pack_params(weights, biases, mlp_layout(m)), dev=dev)
     status = torch.zeros(1, dtype=torch.int32, device=dev)

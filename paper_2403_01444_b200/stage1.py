@@ -38,6 +38,9 @@ class Stage1Config:
     raster: RasterSettings = field(default_factory=RasterSettings)
     loss: LossConfig = field(default_factory=LossConfig)
     rotate_sh: bool = True
+    # decoder arithmetic: None = the cache's own mlp_dtype ("f32" for reference
+    # caches), "f16" = fp16 weights / activations with fp32 accumulation
+    mlp_dtype: str | None = None
 
 
 def inside_rows(grid: HashGridConfig, means: np.ndarray) -> np.ndarray:
@@ -112,7 +115,9 @@ class Stage1Trainer:
         weights = [np.asarray(w) for w in cache.weights]
         biases = [np.asarray(b) for b in cache.biases]
         self.w_shapes = [w.shape for w in weights]
-        self.mlp = mlp_struct(weights[0].shape[0], weights[0].shape[1], len(weights) - 1)
+        self.mlp_dtype = self.cfg.mlp_dtype or getattr(cache, "mlp_dtype", "f32")
+        self.mlp = mlp_struct(weights[0].shape[0], weights[0].shape[1], len(weights) - 1,
+                              self.mlp_dtype)
         self.layout = mlp_layout(self.mlp)
         self.tables = to_dev(np.asarray(cache.tables), dev=dev)
         self.params = to_dev(pack_params(weights, biases, self.layout), dev=dev)

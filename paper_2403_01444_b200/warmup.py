@@ -39,7 +39,8 @@ def warmup_train(cache, initial_means, noise_sigma: float, iterations: int, lr: 
     weights = [np.asarray(w) for w in cache.weights]
     biases = [np.asarray(b) for b in cache.biases]
     shapes = [w.shape for w in weights]
-    m = mlp_struct(weights[0].shape[0], weights[0].shape[1], len(weights) - 1)
+    m = mlp_struct(weights[0].shape[0], weights[0].shape[1], len(weights) - 1,
+                   getattr(cache, "mlp_dtype", "f32"))
     lay = mlp_layout(m)
     gs = grid_struct(grid)
     tables = to_dev(np.asarray(cache.tables), dev=dev)

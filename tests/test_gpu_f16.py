@@ -1,0 +1,170 @@
+"""fp16-weight decoder (BASELINE.json configs[1]: "MLP 32->64->64->7, fp16
+weights with fp32 accumulation") on the CUDA path (ss_mlp.precision =
+SS_MLP_F16: kind::f16 tcgen05 forward, bf16x3 backward on the fp16-rounded
+operands) against the oracle's f16 restatement (oracle/stage1.py
+_mlp_operands: weights, biases, input features and hidden activations rounded
+to float16, exact accumulation).  Same tolerances as the fp32 path (images
+max-abs <= 1e-4, gradients norm-relative <= 1e-3), except at the few rows
+whose fp16 rounding / ReLU decision lies within fp32 summation error of a
+boundary, which are bounded separately.
+"""
+
+import numpy as np
+import pytest
+
+import golden_io as G
+from oracle import stage1 as O
+
+pytestmark = pytest.mark.gpu
+
+IMG_TOL = 1e-4
+GRAD_TOL = 1e-3
+FLIP_TOL = 2e-3  # one fp16 ulp of one hidden activation through the output layer
+
+
+@pytest.fixture(scope="module")
+def P():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2403_01444_b200 import _lib, ntc, scenes, transform, types
+
+    _lib.load()
+    return dict(ntc=ntc, scenes=scenes, transform=transform, types=types, torch=torch)
+
+
+def relu_boundary_rows(mlp, feats, rel=1e-6):
+    """Rows with a hidden pre-activation within rel * sum|terms| of 0: the
+    kernel sums in fp32, the oracle exactly, so only there can their ReLU
+    decisions differ (a flipped decision moves that row's weight gradient by
+    a whole term)."""
+    f16 = lambda a: np.asarray(a).astype(np.float16).astype(np.float64)  # noqa: E731
+    z = f16(feats)
+    bad = np.zeros(len(feats), dtype=bool)
+    for w, b in zip(mlp["weights"][:-1], mlp["biases"][:-1]):
+        w, b = f16(w), f16(b)
+        pre = z @ w + b
+        bad |= np.any(np.abs(pre) < rel * (np.abs(z) @ np.abs(w) + np.abs(b)), axis=1)
+        z = f16(np.maximum(pre, 0.0))
+    return bad
+
+
+def _cache(P, sc, seed, mlp_dtype="f16", table_range=0.3):
+    T = P["types"]
+    cache = P["ntc"].NeuralTransformationCache(T.HashGridConfig.from_any(sc.grid),
+                                               output_init="random", seed=seed,
+                                               mlp_dtype=mlp_dtype)
+    rng = np.random.default_rng(seed + 100)
+    cache.tables[:] = P["scenes"].f32(rng.uniform(-table_range, table_range,
+                                                  size=cache.tables.shape))
+    return cache
+
+
+@pytest.mark.parametrize("levels,hidden", [(16, 2), (8, 1)])
+def test_f16_apply_ntc_vs_oracle(P, levels, hidden):
+    """apply_ntc / apply_ntc_backward through the drop-in API: the cfg1 decoder
+    shape (16 levels x 2 features = 32 inputs, 2 hidden layers) and a 16-input,
+    1-hidden-layer one."""
+    sc = P["scenes"].small_scene(seed=60 + levels, n=5000, sh_degree=1, levels=levels,
+                                 log2_table=12)
+    T = P["types"]
+    cache = P["ntc"].NeuralTransformationCache(T.HashGridConfig.from_any(sc.grid),
+                                               hidden_layers=hidden, output_init="random",
+                                               seed=levels, mlp_dtype="f16")
+    cache.tables[:] = P["scenes"].f32(np.random.default_rng(7).uniform(-0.3, 0.3,
+                                                                       size=cache.tables.shape))
+    cloud = T.GaussianCloud(**sc.cloud)
+    out, ctx = P["transform"].apply_ntc(cloud, cache)
+    inside = O.inside_mask(sc.grid, sc.cloud["means"])
+    idx, w, _ = O.encode(sc.grid, sc.cloud["means"][inside])
+    feats = O.gather(cache.tables, idx, w)
+    mlp16 = dict(weights=cache.weights, biases=cache.biases, dtype="f16")
+    mlp32 = dict(weights=cache.weights, biases=cache.biases)
+    out7, hidden16 = O.mlp_forward(mlp16, feats)
+    moved, octx = O.transform_forward(sc.cloud, inside, out7)
+    # The kernel sums in fp32, the oracle exactly: a hidden activation within
+    # fp32 summation error of an fp16 rounding midpoint rounds the other way
+    # (one fp16 ulp, 2^-11 relative, on one of up to 128 units), which moves
+    # that row's output by up to ~1e-3.  Such rows are rare; all others agree
+    # to fp32.
+    for got, ref in ((out.means, moved["means"]), (out.rotations, moved["rotations"])):
+        err = np.abs(got - ref)
+        print("f16 max err", err.max(), "fraction > 1e-5", np.mean(err > 1e-5))
+        assert err.max() <= FLIP_TOL
+        assert np.mean(err > 1e-5) <= 0.02
+    # the mode is really fp16: the fp32 decoder moves most points differently
+    out7_32, _ = O.mlp_forward(mlp32, feats)
+    moved32, _ = O.transform_forward(sc.cloud, inside, out7_32)
+    assert np.mean(np.abs(moved32["means"] - moved["means"]) > 2e-6) > 0.3
+    # gradients, with the output gradients of the rows whose ReLU decision
+    # sits within fp32 summation error of 0 zeroed (relu_boundary_rows)
+    bad = relu_boundary_rows(mlp16, feats)
+    print("ReLU boundary rows", int(bad.sum()), "of", len(bad))
+    assert bad.mean() < 0.01
+    rng = np.random.default_rng(5)
+    gm, gr = rng.normal(size=out.means.shape), rng.normal(size=(len(out.means), 4))
+    gs = rng.normal(size=out.sh.shape)
+    rows = np.asarray(inside)[bad]  # inside_mask returns the inside row indices
+    gm[rows], gr[rows], gs[rows] = 0.0, 0.0, 0.0
+    grads, _ = P["transform"].apply_ntc_backward(ctx, gm, gr, gs)
+    g7 = O.transform_backward(octx, gm, gr, gs)
+    gw, gb, gf = O.mlp_backward(mlp16, feats, hidden16, g7)
+    for i in range(hidden + 1):
+        assert G.norm_rel(grads[f"w_{i}"], gw[i]) <= GRAD_TOL, i
+        assert G.norm_rel(grads[f"b_{i}"], gb[i]) <= GRAD_TOL, i
+    # and fp16 is not fp32: the gradients differ far beyond the tolerance
+    _, hidden32 = O.mlp_forward(mlp32, feats)
+    gw32, _, _ = O.mlp_backward(mlp32, feats, hidden32, g7)
+    assert G.norm_rel(gw32[0], gw[0]) > 3 * G.norm_rel(grads["w_0"], gw[0])
+    gt = O.table_scatter(cache.tables.shape, idx, w, gf)
+    for l in range(cache.grid.n_levels):
+        assert G.norm_rel(grads[f"table_{l}"], gt[l]) <= GRAD_TOL, l
+
+
+def test_f16_stage1_single_step_vs_oracle(P):
+    """One full Stage-1 step of the trainer with the fp16-weight decoder
+    (Stage1Config.mlp_dtype) against the oracle iteration with the f16
+    decoder: image, loss and every NTC gradient."""
+    from paper_2403_01444_b200.stage1 import Stage1Config, Stage1Trainer
+
+    scenes = P["scenes"]
+    sc = scenes.small_scene(seed=21, n=4000, width=128, height=96, sh_degree=1, n_views=2,
+                            levels=16, log2_table=12)
+    tables, mlp = O.init_ntc(sc.grid, output_init="random", seed=4)
+    tables = scenes.f32(np.random.default_rng(6).uniform(-0.05, 0.05, size=tables.shape))
+    moved = scenes.moved_cloud(sc.cloud, np.random.default_rng(2))
+    targets = [O.render(moved, c)[0]["image"] for c in sc.cameras]
+
+    class Cache:
+        grid = P["types"].HashGridConfig.from_any(sc.grid)
+
+    c = Cache()
+    c.tables, c.weights, c.biases = tables, mlp["weights"], mlp["biases"]
+    tr = Stage1Trainer(sc.cloud, c, list(zip(sc.cameras, targets)),
+                       Stage1Config(mlp_dtype="f16"))
+    assert tr.mlp.precision == 1
+    pairs = tr.begin(1)
+    tr.finish(1, pairs, adam=False)
+    state = dict(grid=sc.grid, tables=tables.copy(), mlp=dict(mlp, dtype="f16"),
+                 inside=O.inside_mask(sc.grid, sc.cloud["means"]), enc=None)
+    ref = O.stage1_iteration(state, sc.cloud, sc.cameras[1], targets[1], apply_adam=False)
+    img_err = np.abs(tr.rendered_image(1) - ref["image"]).max()
+    print("f16 stage1 image err", img_err, "loss", tr.last_loss(), ref["loss"])
+    assert img_err <= IMG_TOL
+    assert abs(tr.last_loss() - ref["loss"]) <= 1e-5 * ref["loss"]
+    gt, gw, gb = tr.ntc_grads()
+    assert G.norm_rel(gt, ref["g_tables"]) <= GRAD_TOL
+    for i in range(3):
+        assert G.norm_rel(gw[i], ref["g_w"][i]) <= GRAD_TOL
+        assert G.norm_rel(gb[i], ref["g_b"][i]) <= GRAD_TOL
+
+
+def test_f16_cache_round_trip_keeps_mode(P):
+    """The mode is a property of the cache: clone / warm-up / playback keep it."""
+    from paper_2403_01444_b200.pipeline import _clone
+
+    sc = P["scenes"].small_scene(seed=3, n=500)
+    cache = _cache(P, sc, seed=1)
+    assert _clone(cache).mlp_dtype == "f16"
+    with pytest.raises(Exception):
+        P["ntc"].NeuralTransformationCache(cache.grid, mlp_dtype="bf8")
