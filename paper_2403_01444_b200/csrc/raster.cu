@@ -1079,6 +1079,9 @@ __global__ void __launch_bounds__(BlendShape<TS, true>::NT) blend_bwd_kernel(
     int tile0) {
   constexpr int NT = BlendShape<TS, true>::NT, PPT = BlendShape<TS, true>::PPT;
   constexpr int NA = 9;  // colour 3, M1 2, M2 3, M0
+  // a thread's pixels share their column when the tile width divides the
+  // warp's 32-pixel rows (tile_pixel): the dx moments then follow from M0, M1y
+  constexpr bool DXC = TS <= 32;
   __shared__ SplatRec s_sp[NT];
   // each warp owns a slot per splat (plain stores, summed at the flush);
   // larger tiles share one slot through shared-memory atomics
@@ -1180,14 +1183,26 @@ __global__ void __launch_bounds__(BlendShape<TS, true>::NT) blend_bwd_kernel(
         da = (a > 0.f && og < bp.clamp) ? da : 0.f;
         // dm = og da (the reference's -0.5 is applied in K5b); moments about the tile centre
         const float dm = og * da;
-        const float e = dm * po.dx[p], f = dm * po.dy[p];
-        v[3] += e;
-        v[4] += f;
-        v[5] = fmaf(e, po.dx[p], v[5]);
-        v[6] = fmaf(e, po.dy[p], v[6]);
-        v[7] = fmaf(f, po.dy[p], v[7]);
+        if (DXC) {  // this thread's pixels share dx: sum dm, dm dy, dm dy^2 only
+          const float f = dm * po.dy[p];
+          v[4] += f;
+          v[7] = fmaf(f, po.dy[p], v[7]);
+        } else {
+          const float e = dm * po.dx[p], f = dm * po.dy[p];
+          v[3] += e;
+          v[4] += f;
+          v[5] = fmaf(e, po.dx[p], v[5]);
+          v[6] = fmaf(e, po.dy[p], v[6]);
+          v[7] = fmaf(f, po.dy[p], v[7]);
+        }
         v[8] += dm;
         any |= a > 0.f;
+      }
+      if (DXC) {  // M1x = dx M0, M2xx = dx M1x, M2xy = dx M1y
+        const float dx = po.dx[0];
+        v[3] = dx * v[8];
+        v[5] = dx * v[3];
+        v[6] = dx * v[4];
       }
       const unsigned bal = __ballot_sync(0xffffffffu, any);
       if (bal) {
