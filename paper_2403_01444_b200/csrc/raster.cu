@@ -1152,23 +1152,29 @@ __global__ void __launch_bounds__(BlendShape<TS, true>::NT) blend_bwd_kernel(
       }
       if (!__any_sync(0xffffffffu, any_live)) continue;
       const float4 col = s_sp[k].col;
-      float Gs[PPT], av[PPT];
+      // og = opacity G for live pixels, 0 otherwise: a = min(clamp, og) is then
+      // 0 for dead pixels without a separate select
+      float og[PPT], av[PPT];
 #pragma unroll
       for (int p = 0; p < PPT; ++p) {
-        Gs[p] = ex2_approx(lgs[p]);
-        av[p] = live[p] ? fminf(bp.clamp, col.w * Gs[p]) : 0.f;
+        og[p] = live[p] ? col.w * ex2_approx(lgs[p]) : 0.f;
+        av[p] = fminf(bp.clamp, og[p]);
       }
       if (any_near) {  // rare: decide in float64
 #pragma unroll
         for (int p = 0; p < PPT; ++p)
-          if (live[p] && lgs[p] < qhi) av[p] = alpha_f64(bp, g, s_sp[k].rank, px[p], py[p]);
+          if (live[p] && lgs[p] < qhi) {
+            av[p] = alpha_f64(bp, g, s_sp[k].rank, px[p], py[p]);
+            if (!(av[p] > 0.f)) og[p] = 0.f;
+          }
       }
       float v[NA] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
       bool any = false;
 #pragma unroll
       for (int p = 0; p < PPT; ++p) {
-        const float G = Gs[p], og = col.w * G, a = av[p];
-        // one approximate reciprocal serves T_before = T / (1 - a) and S / (1 - a)
+        const float a = av[p];
+        // one approximate reciprocal serves T_before = T / (1 - a) and
+        // dL/dalpha = (u T - S) / (1 - a)  (T after this splat, S the suffix)
         const float ioma = rcp_approx(1.f - a);  // a <= alpha_clamp < 1
         const float tb = T[p] * ioma;
         const float w = a * tb;
@@ -1176,13 +1182,13 @@ __global__ void __launch_bounds__(BlendShape<TS, true>::NT) blend_bwd_kernel(
         v[1] = fmaf(w, gp[p][1], v[1]);
         v[2] = fmaf(w, gp[p][2], v[2]);
         const float u = gp[p][0] * col.x + gp[p][1] * col.y + gp[p][2] * col.z;
-        float da = u * tb - S[p] * ioma;
-        S[p] = fmaf(u * a, tb, S[p]);
+        const float da = fmaf(u, T[p], -S[p]) * ioma;
+        S[p] = fmaf(u, w, S[p]);
         T[p] = tb;
-        // no contribution, or flat above the clamp (rasterizer.py:336-337)
-        da = (a > 0.f && og < bp.clamp) ? da : 0.f;
-        // dm = og da (the reference's -0.5 is applied in K5b); moments about the tile centre
-        const float dm = og * da;
+        // dm = og da (the reference's -0.5 is applied in K5b), zero for dead
+        // pixels (og = 0) and flat above the clamp (rasterizer.py:336-337);
+        // moments about the tile centre
+        const float dm = og[p] < bp.clamp ? og[p] * da : 0.f;
         if (DXC) {  // this thread's pixels share dx: sum dm, dm dy, dm dy^2 only
           const float f = dm * po.dy[p];
           v[4] += f;
