@@ -28,7 +28,10 @@ constexpr int kBsWarps = kBsThreads / 32;
 #define SS_BS_WIN 8
 #endif
 constexpr int kBsStepsBig = SS_BS_STEPS_BIG;  // items per lane (2048-item tiles)
-constexpr int kBsStepsSmall = 4;  // 1024-item tiles for small sorts (more CTAs)
+#ifndef SS_BS_STEPS_SMALL
+#define SS_BS_STEPS_SMALL 8
+#endif
+constexpr int kBsStepsSmall = SS_BS_STEPS_SMALL;  // small sorts (e.g. the depth keys): 2048-item tiles measured best
 constexpr uint32_t kFlagAgg = 1u << 30, kFlagInc = 2u << 30, kCntMask = (1u << 30) - 1;
 constexpr int kMaxPasses = 4;
 constexpr int kWin = SS_BS_WIN;  // look-back window (predecessor flags read per round trip)
