@@ -708,9 +708,34 @@ def render_fps(a):
         raise RuntimeError("tile-pair capacity overflow while rendering")
     times = [e0.elapsed_time(e1) for e0, e1 in ev]
     ms = float(np.mean(times))
-    return {"metric": "render_fps", "value": 1000.0 / ms, "unit": "frames/s", "ms_per_frame": ms,
-            "workload": "cfg2: 300k SH-3 Gaussians, 1352x1014, NTC transform + forward, "
-                        "20 views x 2, L2 flushed between frames"}
+    out = {"metric": "render_fps", "value": 1000.0 / ms, "unit": "frames/s", "ms_per_frame": ms,
+           "workload": "cfg2: 300k SH-3 Gaussians, 1352x1014, NTC transform + forward, "
+                       "20 views x 2, L2 flushed between frames"}
+    if not a.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_render_sample()
+    return out
+
+
+def cpu_render_sample():
+    """SURVEY 8(d8) cfg2 CPU baseline: one full frame (apply_ntc +
+    rasterize_forward of view 0) of the float64 oracle port on every host core
+    (oracle/parallel.py; the views are independent, so frames/s per core set)."""
+    from threadpoolctl import threadpool_limits
+
+    from oracle import parallel
+
+    sc, state, _ = _cpu_problem(2)
+    cam = sc.cameras[0]
+    cores = os.cpu_count() or 1
+    ps = parallel.ParallelStage1(cores)
+    with threadpool_limits(1):
+        t0 = time.perf_counter()
+        ps.transform_render(state, sc.cloud, cam)
+        dt = time.perf_counter() - t0
+    return {"value": 1.0 / dt, "unit": "frames/s", "cores": cores, "kind": "port",
+            "sample": f"one cfg2 frame (NTC transform + forward of {len(sc.cloud['means'])} SH-3 "
+                      f"Gaussians at {cam['width']}x{cam['height']}), float64 oracle port on "
+                      f"{cores} forked workers: {dt:.1f} s"}
 
 
 if __name__ == "__main__":

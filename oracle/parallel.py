@@ -184,20 +184,16 @@ class ParallelStage1:
         return pj, rect, vis, band_tiles, image
 
     # ------------------------------------------------------------------
-    def iteration(self, state, cloud, cam, target, lam=0.2, lr=0.002, apply_adam=True,
-                  rotate_sh=True):
-        """Same contract as oracle.stage1.stage1_iteration with its defaults
-        (RasterSettings(), black background, as Stage 1 renders); returns
-        dict(loss, image, d_image, render_grads, g_tables, g_w, g_b)."""
+    def _ntc_transform(self, state, cloud, rotate_sh=True):
+        """NTC forward + transform of the inside rows (ntc.py:205-248,
+        transform.py:53-96): the moved cloud (shared arrays) and out7."""
         P = self.nproc
         grid, mlp, tables = state["grid"], state["mlp"], state["tables"]
         inside = state["inside"]
         if state.get("enc") is None:
             state["enc"] = O.encode(grid, cloud["means"][inside])
         idx, w, _ = state["enc"]
-        n_in, n = len(inside), len(cloud["means"])
-        K = cloud["sh"].shape[1]
-        # ---- NTC forward + transform (inside rows)
+        n_in = len(inside)
         out7 = shared((n_in, 7))
         moved = {k: shared(v.shape) for k, v in cloud.items()}
         for k in cloud:
@@ -216,6 +212,28 @@ class ParallelStage1:
                 moved[k][inside[a:b]] = mv[k]
 
         fork_map(P, fwd)
+        return moved, out7
+
+    def transform_render(self, state, cloud, cam, rotate_sh=True) -> np.ndarray:
+        """apply_ntc + rasterize_forward (pipeline.py:471-480, render-only: the
+        config-2 frame), black background: the image."""
+        moved, _ = self._ntc_transform(state, cloud, rotate_sh)
+        return np.array(self._render(moved, cam)[4])
+
+    # ------------------------------------------------------------------
+    def iteration(self, state, cloud, cam, target, lam=0.2, lr=0.002, apply_adam=True,
+                  rotate_sh=True):
+        """Same contract as oracle.stage1.stage1_iteration with its defaults
+        (RasterSettings(), black background, as Stage 1 renders); returns
+        dict(loss, image, d_image, render_grads, g_tables, g_w, g_b)."""
+        P = self.nproc
+        grid, mlp, tables = state["grid"], state["mlp"], state["tables"]
+        inside = state["inside"]
+        n_in, n = len(inside), len(cloud["means"])
+        K = cloud["sh"].shape[1]
+        moved, out7 = self._ntc_transform(state, cloud, rotate_sh)
+        idx, w, _ = state["enc"]
+        rows = _chunks(n_in, P)
         pj, rect, vis, band_tiles, image = self._render(moved, cam)
         m = len(pj["indices"])
         s = dict(O.DEFAULT_SETTINGS)

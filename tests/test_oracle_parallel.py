@@ -42,3 +42,21 @@ def test_parallel_render_equals_serial():
     ref = O.render(sc.cloud, sc.cameras[0])[0]["image"]
     got = parallel.ParallelStage1(4).render(sc.cloud, sc.cameras[0])
     np.testing.assert_allclose(got, ref, rtol=0, atol=1e-14)
+
+
+def test_parallel_transform_render_equals_serial():
+    """The config-2 CPU frame (apply_ntc + rasterize_forward) of bench.py's
+    render line: equal to the serial oracle's transform then render."""
+    from paper_2403_01444_b200 import scenes
+
+    sc = scenes.small_scene(seed=10, n=900, width=64, height=48, sh_degree=3, n_views=1)
+    tables, mlp = O.init_ntc(sc.grid, output_init="random", seed=4)
+    tables = scenes.f32(np.random.default_rng(5).uniform(-0.05, 0.05, size=tables.shape))
+    inside = O.inside_mask(sc.grid, sc.cloud["means"])
+    idx, w, _ = O.encode(sc.grid, sc.cloud["means"][inside])
+    o7, _ = O.mlp_forward(mlp, O.gather(tables, idx, w))
+    moved, _ = O.transform_forward(sc.cloud, inside, o7)
+    ref = O.render(moved, sc.cameras[0])[0]["image"]
+    state = dict(grid=sc.grid, tables=tables, mlp=mlp, inside=inside, enc=None)
+    got = parallel.ParallelStage1(3).transform_render(state, sc.cloud, sc.cameras[0])
+    np.testing.assert_allclose(got, ref, rtol=0, atol=1e-13)
