@@ -37,6 +37,7 @@ struct Geom {
   float* t_final;    // per pixel
   int32_t* n_contrib;
   int2* ranges;      // per tile
+  int32_t* tile_order;  // tiles by descending pair count: the blends' block -> tile map
   int64_t* dev_counts;  // [survivors, pairs, n, band pairs]
   int64_t* band_off;    // per rank, prefix of the pairs inside the current band of tile rows
   unsigned long long* row_pairs;  // per tile row: pairs of every visible rectangle
@@ -94,6 +95,7 @@ static Geom plan_geom(void* base, int64_t n, const ss_camera* cam, const ss_rast
   g.t_final = c.take<float>(P);
   g.n_contrib = c.take<int32_t>(P);
   g.ranges = c.take<int2>(NT);
+  g.tile_order = c.take<int32_t>(NT);
   g.dev_counts = c.take<int64_t>(4);
   g.band_off = c.take<int64_t>(nn + 1);
   g.row_pairs = c.take<unsigned long long>((size_t)ntiles_y(cam, s));
@@ -681,6 +683,65 @@ __global__ void ranges_kernel(const int64_t* __restrict__ d_pairs, int64_t cap,
   }
 }
 
+// Block -> tile map of the blends, heaviest tiles first (longest-processing-
+// time order): the per-tile work ranges over orders of magnitude, and in
+// index order the last wave's heavy tiles leave most SMs idle.  Tiles are
+// bucketed by 4 log2(pairs) (one CTA: histogram, descending scan, scatter);
+// the order inside a bucket is free (it changes no result).
+__global__ void __launch_bounds__(1024) tile_order_kernel(int ntiles, const int2* __restrict__ ranges,
+                                                          int32_t* __restrict__ order) {
+  constexpr int NB = 64, PER = 8;  // up to 8192 tiles from registers, beyond that re-read
+  __shared__ uint32_t s_hist[NB];
+  auto bucket = [](int c) { return c <= 0 ? 0 : min(NB - 1, 1 + (int)(4.f * __log2f((float)c))); };
+  if (threadIdx.x < NB) s_hist[threadIdx.x] = 0;
+  int b[PER];
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    const int t = threadIdx.x + k * 1024;
+    b[k] = -1;
+    if (t < ntiles) {
+      const int2 r = ranges[t];
+      b[k] = bucket(r.y - r.x);
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < PER; ++k)
+    if (b[k] >= 0) atomicAdd(&s_hist[b[k]], 1u);
+  for (int t = threadIdx.x + PER * 1024; t < ntiles; t += blockDim.x) {
+    const int2 r = ranges[t];
+    atomicAdd(&s_hist[bucket(r.y - r.x)], 1u);
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {  // descending exclusive scan of the 64 buckets
+    const int l = threadIdx.x;
+    const uint32_t hi = s_hist[NB - 1 - l], lo = s_hist[NB / 2 - 1 - l];  // bucket 63 - l, 31 - l
+    uint32_t x = hi;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (l >= o) x += y;
+    }
+    const uint32_t tot_hi = __shfl_sync(0xffffffffu, x, 31);
+    uint32_t z = lo;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, z, o);
+      if (l >= o) z += y;
+    }
+    s_hist[NB - 1 - l] = x - hi;
+    s_hist[NB / 2 - 1 - l] = tot_hi + z - lo;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < PER; ++k)
+    if (b[k] >= 0) order[atomicAdd(&s_hist[b[k]], 1u)] = threadIdx.x + k * 1024;
+  for (int t = threadIdx.x + PER * 1024; t < ntiles; t += blockDim.x) {
+    const int2 r = ranges[t];
+    order[atomicAdd(&s_hist[bucket(r.y - r.x)], 1u)] = t;
+  }
+}
+
 // duplicate -> stable tile sort -> per-tile ranges, all driven by the device
 // count *d_count of the pairs listed by `offs` (the whole view, or one band of
 // tile rows starting at ty_lo)
@@ -690,6 +751,7 @@ static int bin_pairs(const ss_camera* cam, const ss_raster_settings* s, int64_t 
                      int ty_lo = 0) {
   const int ntx = ntiles_x(cam, s), nty = ntiles_y(cam, s);
   const int64_t ntiles = (int64_t)ntx * nty;
+  const bool whole = !offs;  // the whole view (not one band of tile rows)
   if (!offs) offs = g.offsets, d_count = g.dev_counts + 1;
   cull = cull && s->skip_alpha > 0.0;
   const int kb = key_bits(cull ? ntiles + 1 : ntiles);
@@ -714,6 +776,10 @@ static int bin_pairs(const ss_camera* cam, const ss_raster_settings* s, int64_t 
   ranges_kernel<<<stride_grid(b.capacity), 256, 0, st>>>(d_count, b.capacity, b.keys_out,
                                                          g.ranges, (uint32_t)ntiles);
   SS_CHECK_LAUNCH("ranges_kernel");
+  if (whole) {
+    tile_order_kernel<<<1, 1024, 0, st>>>((int)ntiles, g.ranges, g.tile_order);
+    SS_CHECK_LAUNCH("tile_order_kernel");
+  }
   prof_end(PH_RANGES, st);
   return SS_OK;
 }
@@ -915,7 +981,8 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_fwd_kernel(
   __shared__ double2 s_md[TOUCH ? NT : 1];  // float64 mean (TOUCH)
   __shared__ double4 s_cd[TOUCH ? NT : 1];  // float64 conic (c00, c01 + c10, c11) + opacity
   __shared__ int s_touch[TOUCH ? NT : 1];
-  const int tile = tile0 + blockIdx.x;
+  // tile0 < 0: the whole view in tile_order (heaviest first); else a band
+  const int tile = tile0 >= 0 ? tile0 + (int)blockIdx.x : g.tile_order[blockIdx.x];
   const int x0 = (tile % bp.ntx) * TS, y0 = (tile / bp.ntx) * TS;
   const int2 range = g.ranges[tile];
   PixelOffsets<TS, PPT> po;
@@ -1091,7 +1158,7 @@ __global__ void __launch_bounds__(BlendShape<TS, true>::NT) blend_bwd_kernel(
   __shared__ int s_any[NT];
   __shared__ int s_last;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int tile = tile0 + blockIdx.x;
+  const int tile = tile0 >= 0 ? tile0 + (int)blockIdx.x : g.tile_order[blockIdx.x];
   const int tx = tile % bp.ntx, ty = tile / bp.ntx;
   const int x0 = tx * TS, y0 = ty * TS;
   const int2 range = g.ranges[tile];
@@ -1610,9 +1677,9 @@ int raster_finish(const ss_cloud* cl, const ss_camera* cam, const ss_raster_sett
     SS_TRY(bin_pairs(cam, s, n, g, b, status, cull, st));
     prof_begin(PH_BLEND_FWD, st);
     const int rc = touch ? launch_blend_fwd<true>(s->tile_size, ntiles, st, bp, g, b.vals_out,
-                                                  image, alpha, touch)
+                                                  image, alpha, touch, -1)
                          : launch_blend_fwd<false>(s->tile_size, ntiles, st, bp, g, b.vals_out,
-                                                   image, alpha, nullptr);
+                                                   image, alpha, nullptr, -1);
     prof_end(PH_BLEND_FWD, st);
     return rc;
   }
@@ -1650,7 +1717,7 @@ int raster_backward(const ss_cloud* cl, const ss_camera* cam, const ss_raster_se
   const BlendParams bp = blend_params(cam, s);
   if (total <= cap) {  // the forward's bins are still in the workspace
     prof_begin(PH_BLEND_BWD, st);
-    SS_TRY(launch_blend_bwd(s->tile_size, ntiles, st, bp, g, b.vals_out, d_image));
+    SS_TRY(launch_blend_bwd(s->tile_size, ntiles, st, bp, g, b.vals_out, d_image, -1));
     prof_end(PH_BLEND_BWD, st);
   } else {  // bin every band again (the workspace holds one band)
     std::vector<int2> bands;
