@@ -193,6 +193,54 @@ __device__ __forceinline__ void put_scalar(uint8_t* tile, uint32_t lo_off, int r
   *reinterpret_cast<uint16_t*>(tile + lo_off + off) = l;
 }
 
+// ---- fp16 operands of the fp16-weight decoder's backward (kind::f16, f16 A/B):
+// weights, inputs and hidden activations are exact fp16 values (one plane);
+// gradients and deltas are scaled into the fp16 range and split hi + lo
+__device__ __forceinline__ void put8h(uint8_t* tile, int r, int c0, int cols, const float* v) {
+  uint32_t h[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) h[j] = umma::pack_f16(v[2 * j], v[2 * j + 1]);
+  *reinterpret_cast<uint4*>(tile + umma::tile16_off(r, c0, cols)) = make_uint4(h[0], h[1], h[2], h[3]);
+}
+__device__ __forceinline__ void put8s(uint8_t* tile, uint32_t lo_off, int r, int c0, int cols,
+                                      const float* v, float scale) {
+  uint32_t h[4], l[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const float a = v[2 * j] * scale, b = v[2 * j + 1] * scale;
+    const float ha = umma::round_f16(a), hb = umma::round_f16(b);
+    h[j] = umma::pack_f16(ha, hb);
+    l[j] = umma::pack_f16(a - ha, b - hb);
+  }
+  const uint32_t off = umma::tile16_off(r, c0, cols);
+  *reinterpret_cast<uint4*>(tile + off) = make_uint4(h[0], h[1], h[2], h[3]);
+  *reinterpret_cast<uint4*>(tile + lo_off + off) = make_uint4(l[0], l[1], l[2], l[3]);
+}
+__device__ __forceinline__ void put_scalar_h(uint8_t* tile, int r, int c, int cols, float x) {
+  *reinterpret_cast<__half*>(tile + umma::tile16_off(r, c, cols)) = __float2half_rn(x);
+}
+// one product per K step (both operands exact), or two with the A or the B
+// operand split hi + lo (the A_lo B_lo term is below fp32 resolution)
+template <int NK>
+__device__ __forceinline__ void gemm1e(uint32_t acc, const Op16& A, const Op16& B, uint32_t idesc,
+                                       uint32_t accumulate) {
+#pragma unroll
+  for (int s = 0; s < NK; ++s)
+    umma::mma_bf16_elect(acc, A.hi + (uint64_t)A.kstep * s, B.hi + (uint64_t)B.kstep * s, idesc,
+                         accumulate | (s > 0));
+}
+template <int NK, bool SPLIT_A>
+__device__ __forceinline__ void gemm2e(uint32_t acc, const Op16& A, const Op16& B, uint32_t idesc,
+                                       uint32_t accumulate) {
+#pragma unroll
+  for (int s = 0; s < NK; ++s) {
+    const uint64_t da = (uint64_t)A.kstep * s, db = (uint64_t)B.kstep * s;
+    umma::mma_bf16_elect(acc, A.hi + da, B.hi + db, idesc, accumulate | (s > 0));
+    if (SPLIT_A) umma::mma_bf16_elect(acc, A.lo + da, B.hi + db, idesc, 1);
+    else umma::mma_bf16_elect(acc, A.hi + da, B.lo + db, idesc, 1);
+  }
+}
+
 // X row slices: thread quarter q owns column blocks 8q + 32b < IN
 template <int IN>
 struct XSlice {
@@ -548,22 +596,29 @@ __global__ void __launch_bounds__(NT, 1) mlp_bwd_tc_kernel(
   const int tid = threadIdx.x, warp = tid >> 5, lane_id = tid & 31;
   const int r = tid & 127, q = tid >> 7;
   const int c0 = 16 * q;  // this thread's 16 columns of every 64-wide accumulator
-  // H16: the fp16-weight decoder's operands (fp16 values split exactly into bf16 hi + lo)
+  // H16: the fp16-weight decoder: fp16 operands (kind::f16 with f16 A/B); the
+  // weights, inputs and activations are exact in one plane, the gradient chain
+  // (G, D) is scaled by gsc into the fp16 range and split hi + lo, so every
+  // GEMM takes one or two products instead of three
   auto rnd = [](float x) { return H16 ? umma::round_f16(x) : x; };
   // ---- weights as bf16 hi/lo tiles: W0t (j, f) = W0[f][j]; W1t (j, i) = W1[i][j];
   //      W2t (o, j) = W2[j][o] (rows 7..15 zero)
+  auto putw = [&](uint32_t o, uint32_t lo, int r_, int c_, int cols, float x) {
+    if (H16) put_scalar_h(sm + o, r_, c_, cols, x);
+    else put_scalar(sm + o, lo, r_, c_, cols, x);
+  };
   for (int i = tid; i < 64 * IN; i += NT) {
     const int j = i / IN, f = i % IN;
-    put_scalar(sm + S::oW0, S::W0, j, f, IN, rnd(params[L::W0 + f * 64 + j]));
+    putw(S::oW0, S::W0, j, f, IN, rnd(params[L::W0 + f * 64 + j]));
   }
   if (NL == 2)
     for (int i = tid; i < 64 * 64; i += NT) {
       const int j = i / 64, k = i % 64;
-      put_scalar(sm + S::oW1, S::W1, j, k, 64, rnd(params[L::W1 + k * 64 + j]));
+      putw(S::oW1, S::W1, j, k, 64, rnd(params[L::W1 + k * 64 + j]));
     }
   for (int i = tid; i < 16 * 64; i += NT) {
     const int o = i / 64, j = i % 64;
-    put_scalar(sm + S::oW2, S::W2, o, j, 64, o < 7 ? rnd(params[L::W2 + j * 8 + o]) : 0.f);
+    putw(S::oW2, S::W2, o, j, 64, o < 7 ? rnd(params[L::W2 + j * 8 + o]) : 0.f);
   }
   if (tid < 64) {
     sbias[tid] = rnd(params[L::B0 + tid]);
@@ -573,9 +628,64 @@ __global__ void __launch_bounds__(NT, 1) mlp_bwd_tc_kernel(
   {
     const float pad[8] = {1.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     const float z[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    if (q == 0) put8(sm + S::oX, S::X, r, IN, XC, pad);
-    if (q == 1) put8(sm + S::oH1, S::H1, r, 64, HC, pad);
-    if (q == 2) put8(sm + S::oG, S::G, r, 8, 16, z);
+    if (q == 0) {
+      if (H16) put8h(sm + S::oX, r, IN, XC, pad);
+      else put8(sm + S::oX, S::X, r, IN, XC, pad);
+    }
+    if (q == 1) {
+      if (H16) put8h(sm + S::oH1, r, 64, HC, pad);
+      else put8(sm + S::oH1, S::H1, r, 64, HC, pad);
+    }
+    if (q == 2) put8(sm + S::oG, S::G, r, 8, 16, z);  // zero in both planes either way
+  }
+  // H16: the gradient scale of this CTA, a power of two that keeps G and the
+  // deltas D_last = G W2^T (masked) and D1 = D2 W1^T within fp16:
+  // |D_last| <= max|G| max_j sum_o |W2_jo|, |D1| <= |D2| max_k sum_n |W1_kn|
+  float gsc = 1.f, igsc = 1.f;
+  if (H16) {
+    __shared__ float s_max[NT / 32][3];
+    float gm = 0.f, r2 = 0.f, r1 = 0.f;
+    const int64_t nt_ = (n + 127) / 128;
+    const int64_t mine = nt_ > blockIdx.x ? (nt_ - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    if (gs == 8 && (reinterpret_cast<uintptr_t>(g_out) & 15) == 0) {
+      // rows of 8 floats (the 8th is zero padding): two float4 per row, all in flight
+#pragma unroll 4
+      for (int64_t k = tid; k < mine * 256; k += NT) {
+        const int64_t row = (blockIdx.x + (k >> 8) * gridDim.x) * 128 + ((k & 255) >> 1);
+        if (row < n) {
+          const float4 v = __ldg(reinterpret_cast<const float4*>(g_out + row * 8) + (k & 1));
+          gm = fmaxf(gm, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+        }
+      }
+    } else {
+      for (int64_t k = tid; k < mine * 128 * 7; k += NT) {
+        const int64_t e = k % (128 * 7);
+        const int64_t row = (blockIdx.x + (k / (128 * 7)) * gridDim.x) * 128 + e / 7;
+        if (row < n) gm = fmaxf(gm, fabsf(__ldg(g_out + row * gs + e % 7)));
+      }
+    }
+    if (tid < 64) {
+      for (int o = 0; o < 7; ++o) r2 += fabsf(rnd(params[L::W2 + tid * 8 + o]));
+      if (NL == 2)
+        for (int k = 0; k < 64; ++k) r1 += fabsf(rnd(params[L::W1 + tid * 64 + k]));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      gm = fmaxf(gm, __shfl_xor_sync(0xffffffffu, gm, o));
+      r2 = fmaxf(r2, __shfl_xor_sync(0xffffffffu, r2, o));
+      r1 = fmaxf(r1, __shfl_xor_sync(0xffffffffu, r1, o));
+    }
+    if ((tid & 31) == 0) s_max[warp][0] = gm, s_max[warp][1] = r2, s_max[warp][2] = r1;
+    __syncthreads();
+    gm = r2 = r1 = 0.f;
+#pragma unroll
+    for (int w = 0; w < NT / 32; ++w)
+      gm = fmaxf(gm, s_max[w][0]), r2 = fmaxf(r2, s_max[w][1]), r1 = fmaxf(r1, s_max[w][2]);
+    const float bound = gm * fmaxf(1.f, fmaxf(r2, NL == 2 ? r2 * r1 : 0.f));
+    const int e = bound > 0.f ? (int)ceilf(log2f(bound)) : 0;
+    const int sh = min(100, max(-100, 14 - e));
+    gsc = exp2f((float)sh);
+    igsc = exp2f((float)-sh);
   }
   if (tid == 0) {
     umma::mbar_init(&bar, 1);
@@ -602,12 +712,12 @@ __global__ void __launch_bounds__(NT, 1) mlp_bwd_tc_kernel(
   const Op16 oD2_k = op16(aD2, S::D2, 64, 0), oD2_mn = op16(aD2, S::D2, 64, 1);
   const Op16 oD1_k = op16(aD1, S::D1, 64, 0), oD1_mn = op16(aD1, S::D1, 64, 1);
   const Op16 oHl_mn = NL == 2 ? oH2_mn : oH1_mn;
-  constexpr uint32_t idF = umma::idesc_bf16(128, 64, 0, 0);
-  constexpr uint32_t idB64 = umma::idesc_bf16(128, 64, 0, 1);
-  constexpr uint32_t idBX = umma::idesc_bf16(128, IN, 0, 1);
-  constexpr uint32_t idW2 = umma::idesc_bf16(64, 8, 1, 1);
-  constexpr uint32_t idW1 = umma::idesc_bf16(64, HC, 1, 1);
-  constexpr uint32_t idW0 = umma::idesc_bf16(64, XC, 1, 1);
+  constexpr uint32_t idF = H16 ? umma::idesc_f16(128, 64, 0, 0) : umma::idesc_bf16(128, 64, 0, 0);
+  constexpr uint32_t idB64 = H16 ? umma::idesc_f16(128, 64, 0, 1) : umma::idesc_bf16(128, 64, 0, 1);
+  constexpr uint32_t idBX = H16 ? umma::idesc_f16(128, IN, 0, 1) : umma::idesc_bf16(128, IN, 0, 1);
+  constexpr uint32_t idW2 = H16 ? umma::idesc_f16(64, 8, 1, 1) : umma::idesc_bf16(64, 8, 1, 1);
+  constexpr uint32_t idW1 = H16 ? umma::idesc_f16(64, HC, 1, 1) : umma::idesc_bf16(64, HC, 1, 1);
+  constexpr uint32_t idW0 = H16 ? umma::idesc_f16(64, XC, 1, 1) : umma::idesc_bf16(64, XC, 1, 1);
   uint32_t phase = 0, phase_w = 0, acc_w = 0;
   bool w_pending = false;  // weight-gradient GEMMs of the last tile still reading X, G, H, D
   auto wait_w = [&]() {
@@ -637,24 +747,29 @@ __global__ void __launch_bounds__(NT, 1) mlp_bwd_tc_kernel(
 #pragma unroll
     for (int b = 0; b < XSlice<IN>::NB; ++b) {
       const int c = 8 * q + 32 * b;
-      if (H16) {
-#pragma unroll
-        for (int j = 0; j < 8; ++j) xr.v[b][j] = rnd(xr.v[b][j]);
+      if (c < IN) {
+        if (H16) put8h(sm + S::oX, r, c, XC, xr.v[b]);  // rounds to fp16
+        else put8(sm + S::oX, S::X, r, c, XC, xr.v[b]);
       }
-      if (c < IN) put8(sm + S::oX, S::X, r, c, XC, xr.v[b]);
     }
     if (q == 0) {
 #pragma unroll
       for (int k = 0; k < 8; ++k) db2[k] += gr[k];
-      put8(sm + S::oG, S::G, r, 0, 16, gr);
+      if (H16) put8s(sm + S::oG, S::G, r, 0, 16, gr, gsc);
+      else put8(sm + S::oG, S::G, r, 0, 16, gr);
     }
   };
   auto issue_stage1 = [&]() {
     to_async();
     if (warp == 0) {  // warp-uniform issue: descriptors stay in uniform registers
       umma::fence_after();
-      gemm3e<IN / 16>(tmem + S::cH1, oX_k, oW0_k, idF, 0);
-      gemm3e<1>(tmem + S::cDL, oG_k, oW2_mn, idB64, 0);
+      if (H16) {
+        gemm1e<IN / 16>(tmem + S::cH1, oX_k, oW0_k, idF, 0);
+        gemm2e<1, true>(tmem + S::cDL, oG_k, oW2_mn, idB64, 0);
+      } else {
+        gemm3e<IN / 16>(tmem + S::cH1, oX_k, oW0_k, idF, 0);
+        gemm3e<1>(tmem + S::cDL, oG_k, oW2_mn, idB64, 0);
+      }
       umma::commit_elect(&bar);
     }
   };
@@ -705,16 +820,26 @@ __global__ void __launch_bounds__(NT, 1) mlp_bwd_tc_kernel(
 #pragma unroll
       for (int j = 0; j < 16; ++j)
         v[j] = ((mask1 >> j) & 1) ? rnd(fmaxf(v[j] + sbias[c0 + j], 0.f)) : 0.f;
-      put8(sm + S::oH1, S::H1, r, c0, HC, v);
-      put8(sm + S::oH1, S::H1, r, c0 + 8, HC, v + 8);
+      if (H16) {
+        put8h(sm + S::oH1, r, c0, HC, v);
+        put8h(sm + S::oH1, r, c0 + 8, HC, v + 8);
+      } else {
+        put8(sm + S::oH1, S::H1, r, c0, HC, v);
+        put8(sm + S::oH1, S::H1, r, c0 + 8, HC, v + 8);
+      }
       umma::tmem_ld16(tmem + S::cDL + lane + c0, v);
       const uint32_t ml = NL == 2 ? mask2 : mask1;
 #pragma unroll
       for (int j = 0; j < 16; ++j) v[j] = ((ml >> j) & 1) ? v[j] : 0.f;
       uint8_t* dst = sm + (NL == 2 ? S::oD2 : S::oD1);
       const uint32_t dlo = NL == 2 ? S::D2 : S::D1;
-      put8(dst, dlo, r, c0, 64, v);
-      put8(dst, dlo, r, c0 + 8, 64, v + 8);
+      if (H16) {  // already scaled (G was)
+        put8s(dst, dlo, r, c0, 64, v, 1.f);
+        put8s(dst, dlo, r, c0 + 8, 64, v + 8, 1.f);
+      } else {
+        put8(dst, dlo, r, c0, 64, v);
+        put8(dst, dlo, r, c0 + 8, 64, v + 8);
+      }
     }
     if (NL == 2) {
       // ---- stage 2: H2 = H1 W1;  D1 = D2 W1^T;  dW1^T += D2^T [H1 | 1]
@@ -722,11 +847,17 @@ __global__ void __launch_bounds__(NT, 1) mlp_bwd_tc_kernel(
       to_async();
       if (warp == 0) {
         umma::fence_after();
-        gemm3e<4>(tmem + S::cH2, oH1_k, oW1_k, idF, 0);
-        gemm3e<4>(tmem + S::cD1, oD2_k, oW1_mn, idB64, 0);
+        if (H16) {
+          gemm1e<4>(tmem + S::cH2, oH1_k, oW1_k, idF, 0);
+          gemm2e<4, true>(tmem + S::cD1, oD2_k, oW1_mn, idB64, 0);
+        } else {
+          gemm3e<4>(tmem + S::cH2, oH1_k, oW1_k, idF, 0);
+          gemm3e<4>(tmem + S::cD1, oD2_k, oW1_mn, idB64, 0);
+        }
         umma::commit_elect(&bar);
         // dW1 reads D2 and H1 only: it runs under the H2 / D1 epilogue
-        gemm3e<8>(tmem + S::cW1, oD2_mn, oH1_mn, idW1, acc_w);
+        if (H16) gemm2e<8, true>(tmem + S::cW1, oD2_mn, oH1_mn, idW1, acc_w);
+        else gemm3e<8>(tmem + S::cW1, oD2_mn, oH1_mn, idW1, acc_w);
       }
       sync_mma(&bar, phase);
       SS_STAMP(1, 4 + 8 * it);
@@ -735,25 +866,41 @@ __global__ void __launch_bounds__(NT, 1) mlp_bwd_tc_kernel(
 #pragma unroll
       for (int j = 0; j < 16; ++j)
         v[j] = ((mask2 >> j) & 1) ? rnd(fmaxf(v[j] + sbias[64 + c0 + j], 0.f)) : 0.f;
-      put8(sm + S::oH2, S::H2, r, c0, 64, v);
-      put8(sm + S::oH2, S::H2, r, c0 + 8, 64, v + 8);
+      if (H16) {
+        put8h(sm + S::oH2, r, c0, 64, v);
+        put8h(sm + S::oH2, r, c0 + 8, 64, v + 8);
+      } else {
+        put8(sm + S::oH2, S::H2, r, c0, 64, v);
+        put8(sm + S::oH2, S::H2, r, c0 + 8, 64, v + 8);
+      }
       umma::tmem_ld16(tmem + S::cD1 + lane + c0, v);
 #pragma unroll
       for (int j = 0; j < 16; ++j) v[j] = ((mask1 >> j) & 1) ? v[j] : 0.f;
-      put8(sm + S::oD1, S::D1, r, c0, 64, v);
-      put8(sm + S::oD1, S::D1, r, c0 + 8, 64, v + 8);
+      if (H16) {
+        put8s(sm + S::oD1, S::D1, r, c0, 64, v, 1.f);
+        put8s(sm + S::oD1, S::D1, r, c0 + 8, 64, v + 8, 1.f);
+      } else {
+        put8(sm + S::oD1, S::D1, r, c0, 64, v);
+        put8(sm + S::oD1, S::D1, r, c0 + 8, 64, v + 8);
+      }
     }
     // ---- stage 3: dX = D1 W0^T;  dW0^T += D1^T [X | 1];  dW2 += H_last^T G
     SS_STAMP(1, 5 + 8 * it);
     to_async();
     if (warp == 0) {
       umma::fence_after();
-      gemm3e<4>(tmem + S::cDX, oD1_k, oW0_mn, idBX, 0);
+      if (H16) gemm2e<4, true>(tmem + S::cDX, oD1_k, oW0_mn, idBX, 0);
+      else gemm3e<4>(tmem + S::cDX, oD1_k, oW0_mn, idBX, 0);
       umma::commit_elect(&bar);
       // dW0 / dW2 (and dW1 before them) read X, G, H, D: they run under the dX
       // epilogue; the next tile's staging waits for bar_w
-      gemm3e<8>(tmem + S::cW0, oD1_mn, oX_mn, idW0, acc_w);
-      gemm3e<8>(tmem + S::cW2, oHl_mn, oG_mn, idW2, acc_w);
+      if (H16) {
+        gemm2e<8, true>(tmem + S::cW0, oD1_mn, oX_mn, idW0, acc_w);
+        gemm2e<8, false>(tmem + S::cW2, oHl_mn, oG_mn, idW2, acc_w);
+      } else {
+        gemm3e<8>(tmem + S::cW0, oD1_mn, oX_mn, idW0, acc_w);
+        gemm3e<8>(tmem + S::cW2, oHl_mn, oG_mn, idW2, acc_w);
+      }
       umma::commit_elect(&bar_w);
     }
     w_pending = true;
@@ -774,6 +921,10 @@ __global__ void __launch_bounds__(NT, 1) mlp_bwd_tc_kernel(
       if (c < IN) {  // warp-uniform
         float v[8];
         umma::tmem_ld8(tmem + S::cDX + lane + c, v);
+        if (H16) {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) v[k] *= igsc;
+        }
         if (row < n) {
           *reinterpret_cast<float4*>(dX + row * xs + c) = make_float4(v[0], v[1], v[2], v[3]);
           *reinterpret_cast<float4*>(dX + row * xs + c + 4) = make_float4(v[4], v[5], v[6], v[7]);
@@ -793,6 +944,8 @@ __global__ void __launch_bounds__(NT, 1) mlp_bwd_tc_kernel(
     if (q == 0) {
       float v[8];
       umma::tmem_ld8(tmem + S::cW2 + lane, v);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] *= igsc;
       if (own) {
         red_add_v4(g_params + L::W2 + j * 8, v[0], v[1], v[2], v[3]);
         red_add_v4(g_params + L::W2 + j * 8 + 4, v[4], v[5], v[6], 0.f);
@@ -802,6 +955,8 @@ __global__ void __launch_bounds__(NT, 1) mlp_bwd_tc_kernel(
       for (int c = 8 * q; c < HC; c += 32) {
         float v[8];
         umma::tmem_ld8(tmem + S::cW1 + lane + c, v);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] *= igsc;
         if (own) {
 #pragma unroll
           for (int k = 0; k < 8; ++k) {
@@ -814,6 +969,8 @@ __global__ void __launch_bounds__(NT, 1) mlp_bwd_tc_kernel(
     for (int c = 8 * q; c < XC; c += 32) {
       float v[8];
       umma::tmem_ld8(tmem + S::cW0 + lane + c, v);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] *= igsc;
       if (own) {
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
