@@ -243,11 +243,6 @@ __global__ void __launch_bounds__(256, 3) preprocess_kernel(CamD cam, ss_cloud c
   if (i < cl.n) {
     if (i == 0) g.dev_counts[2] = cl.n;
     g.order[i] = (int32_t)i;  // sort input (4 passes: the input sits in the output buffers)
-    // the reverse blend's per-rank accumulators start at zero (rank slot i;
-    // gaussian_bwd_kernel re-zeroes the slots it consumes)
-    float4* ac = reinterpret_cast<float4*>(g.acc + i * kAccStride);
-    ac[0] = ac[1] = ac[2] = make_float4(0.f, 0.f, 0.f, 0.f);
-    g.touched[i] = 0;
     const float* m = cl.means + 3 * i;
     // depth key, every operation rounded (no FMA contraction) in a fixed order,
     // ((R20 m0 + R21 m1) + R22 m2) + t2, so it is reproducible on the host; the
@@ -1387,12 +1382,9 @@ __global__ void __launch_bounds__(128, 4) gaussian_bwd_kernel(CamD cam, ss_cloud
     if (full && out.d_opacity_logits) out.d_opacity_logits[gid] = 0.f;
     return;
   }
-  float4* acr = reinterpret_cast<float4*>(g.acc + (int64_t)r * kAccStride);
-  const float4 a0 = acr[0], a1 = acr[1];
+  const float4 a0 = *reinterpret_cast<const float4*>(g.acc + (int64_t)r * kAccStride);
+  const float4 a1 = *reinterpret_cast<const float4*>(g.acc + (int64_t)r * kAccStride + 4);
   const float a8 = g.acc[(int64_t)r * kAccStride + 8];
-  // consumed: zero for a further backward pass over the same forward
-  acr[0] = acr[1] = acr[2] = make_float4(0.f, 0.f, 0.f, 0.f);
-  g.touched[r] = 0;
   // moments about the anchor (K5a) -> sums over (x - mu): Delta = anchor - mu
   double am[2], A[2][2], aop;
   {
@@ -1417,7 +1409,7 @@ __global__ void __launch_bounds__(128, 4) gaussian_bwd_kernel(CamD cam, ss_cloud
     aop = M0 / cd.w;
   }
   if (out.viewspace) out.viewspace[gid] = (float)sqrt(am[0] * am[0] + am[1] * am[1]);
-  if (out.contributed) out.contributed[gid] = 1;  // touched (the early return above)
+  if (out.contributed) out.contributed[gid] = g.touched[r];
   // ---- colour -> SH and view direction first (sh.py:62-81), fp32 with the
   // forward's clip mask; its registers are free before the fp64 chain below
   double gw[3];
@@ -1720,7 +1712,8 @@ int raster_backward(const ss_cloud* cl, const ss_camera* cam, const ss_raster_se
   Bins b = plan_bins(bins, cap);
   const int ntx = ntiles_x(cam, s);
   const int64_t ntiles = (int64_t)ntx * ntiles_y(cam, s);
-  // g.acc / g.touched: zeroed by preprocess_kernel and after use by gaussian_bwd_kernel
+  SS_CUDA(cudaMemsetAsync(g.acc, 0, n * kAccStride * sizeof(float), st));
+  SS_CUDA(cudaMemsetAsync(g.touched, 0, n, st));
   const BlendParams bp = blend_params(cam, s);
   if (total <= cap) {  // the forward's bins are still in the workspace
     prof_begin(PH_BLEND_BWD, st);
