@@ -296,18 +296,23 @@ __global__ void __launch_bounds__(NT_FWD, 1) mlp_fwd_tc_kernel(int64_t n, const 
     else
       put<P>(sm + o, plane, umma::tile_off(nn, k, cols), w);
   };
+  // params are (fan_in, fan_out) row-major: consecutive threads read
+  // consecutive weights (coalesced, several loads in flight per thread)
+#pragma unroll 4
   for (int i = tid; i < 64 * IN; i += NT_FWD) {
-    const int nn = i / IN, k = i % IN;
-    put_w(S::oW0, S::W0, nn, k, IN, params[L::W0 + k * 64 + nn]);
+    const int k = i / 64, nn = i % 64;
+    put_w(S::oW0, S::W0, nn, k, IN, __ldg(params + L::W0 + i));
   }
   if (NL == 2)
+#pragma unroll 4
     for (int i = tid; i < 64 * 64; i += NT_FWD) {
-      const int nn = i / 64, k = i % 64;
-      put_w(S::oW1, S::W1, nn, k, 64, params[L::W1 + k * 64 + nn]);
+      const int k = i / 64, nn = i % 64;
+      put_w(S::oW1, S::W1, nn, k, 64, __ldg(params + L::W1 + i));
     }
+#pragma unroll 2
   for (int i = tid; i < 16 * 64; i += NT_FWD) {
-    const int nn = i / 64, k = i % 64;
-    put_w(S::oW2, S::W2, nn, k, 64, nn < 8 ? params[L::W2 + k * 8 + nn] : 0.f);
+    const int k = i / 16, nn = i % 16;
+    put_w(S::oW2, S::W2, nn, k, 64, nn < 8 ? __ldg(params + L::W2 + k * 8 + nn) : 0.f);
   }
   auto bias = [&](float b) { return P == 0 ? umma::round_f16(b) : b; };
   if (tid < 64) {
@@ -607,18 +612,22 @@ __global__ void __launch_bounds__(NT, 1) mlp_bwd_tc_kernel(
     if (H16) put_scalar_h(sm + o, r_, c_, cols, x);
     else put_scalar(sm + o, lo, r_, c_, cols, x);
   };
+  // (fan_in, fan_out) row-major params read in order: coalesced, several in flight
+#pragma unroll 4
   for (int i = tid; i < 64 * IN; i += NT) {
-    const int j = i / IN, f = i % IN;
-    putw(S::oW0, S::W0, j, f, IN, rnd(params[L::W0 + f * 64 + j]));
+    const int f = i / 64, j = i % 64;
+    putw(S::oW0, S::W0, j, f, IN, rnd(__ldg(params + L::W0 + i)));
   }
   if (NL == 2)
+#pragma unroll 4
     for (int i = tid; i < 64 * 64; i += NT) {
-      const int j = i / 64, k = i % 64;
-      putw(S::oW1, S::W1, j, k, 64, rnd(params[L::W1 + k * 64 + j]));
+      const int k = i / 64, j = i % 64;
+      putw(S::oW1, S::W1, j, k, 64, rnd(__ldg(params + L::W1 + i)));
     }
+#pragma unroll 2
   for (int i = tid; i < 16 * 64; i += NT) {
-    const int o = i / 64, j = i % 64;
-    putw(S::oW2, S::W2, o, j, 64, o < 7 ? rnd(params[L::W2 + j * 8 + o]) : 0.f);
+    const int j = i / 16, o = i % 16;
+    putw(S::oW2, S::W2, o, j, 64, o < 7 ? rnd(__ldg(params + L::W2 + j * 8 + o)) : 0.f);
   }
   if (tid < 64) {
     sbias[tid] = rnd(params[L::B0 + tid]);
