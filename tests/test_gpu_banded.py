@@ -26,9 +26,13 @@ def P():
     return dict(rasterizer=rasterizer, types=types, scenes=scenes, torch=torch)
 
 
-def test_banded_render_equals_single_workspace(P, monkeypatch):
+@pytest.mark.parametrize("width,height,n", [(320, 240, 6000), (3840, 2160, 3000)])
+def test_banded_render_equals_single_workspace(P, monkeypatch, width, height, n):
+    """Banded binning (tile rows, index order) equals the single-workspace
+    render (tiles launched heaviest first); at 3840x2160 the 32400 tiles also
+    take the tile-order kernel's path beyond 8192 tiles."""
     R, T, S = P["rasterizer"], P["types"], P["scenes"]
-    sc = S.small_scene(seed=71, n=6000, width=320, height=240, sh_degree=3)
+    sc = S.small_scene(seed=71, n=n, width=width, height=height, sh_degree=3)
     cloud, cam = T.GaussianCloud(**sc.cloud), T.Camera.from_any(sc.cameras[0])
     bg = np.array([0.1, 0.2, 0.3])
     out1, ctx1 = R.rasterize_forward(cloud, cam, bg)
@@ -50,8 +54,10 @@ def test_banded_render_equals_single_workspace(P, monkeypatch):
     np.testing.assert_array_equal(out1.alpha_map, out2.alpha_map)
     np.testing.assert_array_equal(out1.per_gaussian_touch_count, out2.per_gaussian_touch_count)
     g2 = R.rasterize_backward(ctx2, d_img)
+    # the per-splat sums arrive in a different float-atomic order (bands vs
+    # heaviest-tile-first): equal up to fp32 accumulation order
     for k in ("d_means", "d_rotations", "d_log_scales", "d_opacity_logits", "d_sh"):
-        assert G.norm_rel(getattr(g2, k), getattr(g1, k)) <= 1e-5, k
+        assert G.norm_rel(getattr(g2, k), getattr(g1, k)) <= 1e-4, k
     np.testing.assert_array_equal(g1.contributed, g2.contributed)
 
 
