@@ -233,7 +233,10 @@ int binsort_passes(int key_bits) { return (key_bits + 7) / 8; }
 // into keys_out/vals_out, in ceil(key_bits / 8) passes ping-ponging with the
 // tmp buffers.  The input must be in keys_out/vals_out for an even number of
 // passes and in keys_tmp/vals_tmp for an odd one: see binsort_passes().
+thread_local bool t_prezeroed = false;
+
 int binsort_clear(const BinSortWS& w, int key_bits, cudaStream_t st) {
+  if (t_prezeroed) return SS_OK;  // raster_zero_iteration did it
   const int passes = binsort_passes(key_bits);
   SS_CUDA(cudaMemsetAsync(w.hist, 0, binsort_clear_bytes(w), st));
   SS_CUDA(cudaMemsetAsync(w.status, 0, (size_t)passes * w.max_blocks * 256 * sizeof(uint32_t),

@@ -252,6 +252,20 @@ struct BinSortWS {
   int steps;  // items per thread of a pass tile
 };
 BinSortWS binsort_plan(Carve& c, int64_t capacity, int max_passes);
+// Stage-1 iterations zero the per-iteration scratch of the geometry workspace
+// and the loss (depth-sort look-back words and histograms, counters, reverse-
+// blend accumulators, loss sums) with ONE kernel (a memset node costs ~1.5 us
+// in a replayed graph); inside such a scope those memsets are skipped.  The
+// bin workspace keeps its own clears (the host may replace it mid-iteration).
+extern thread_local bool t_prezeroed;
+struct PrezeroScope {
+  bool prev;
+  explicit PrezeroScope(bool on) : prev(t_prezeroed) { t_prezeroed = on; }
+  ~PrezeroScope() { t_prezeroed = prev; }
+};
+int raster_zero_iteration(void* geom, int64_t n, const ss_camera* cam, const ss_raster_settings* s,
+                          void* bins, int64_t cap, void* extra, size_t extra_bytes,
+                          cudaStream_t st);
 int binsort_passes(int key_bits);
 // zero the histograms, tickets and look-back words (before a producer that
 // accumulates the histograms itself with bs_hist_add, then hist_ready = true)

@@ -324,7 +324,7 @@ int ss_render_loss(const float* image, const float* target, int32_t height, int3
   lp.l1w = (1.0 - lam) / ((double)height * width * channels);
   double* sums = static_cast<double*>(scratch);
   float* maps = reinterpret_cast<float*>(static_cast<char*>(scratch) + align_up(2 * sizeof(double)));
-  SS_CUDA(cudaMemsetAsync(sums, 0, 2 * sizeof(double), st));
+  if (!t_prezeroed) SS_CUDA(cudaMemsetAsync(sums, 0, 2 * sizeof(double), st));
   dim3 blk(SW, 3);
   dim3 g1((unsigned)cdiv(lp.Wv, SW), (unsigned)cdiv(lp.Hv, RCH));
   prof_begin(PH_SSIM_MAP, st);

@@ -762,6 +762,9 @@ static int bin_pairs(const ss_camera* cam, const ss_raster_settings* s, int64_t 
   cull = cull && s->skip_alpha > 0.0;
   const int kb = key_bits(cull ? ntiles + 1 : ntiles);
   const bool two = binsort_passes(kb) == 2;
+  // the bin workspace can be replaced between raster_begin and here (the host
+  // sizes it from the pair count), and bands reuse it: its clears always run
+  PrezeroScope scope(false);
   SS_CUDA(cudaMemsetAsync(g.ranges, 0, ntiles * sizeof(int2), st));
   SS_TRY(binsort_clear(b.sort, kb, st));  // duplicate_kernel builds the sort's histograms
   prof_begin(PH_DUPLICATE, st);
@@ -1617,13 +1620,54 @@ static int launch_blend_bwd(int ts, int64_t ntiles, cudaStream_t st, const Blend
   return SS_OK;
 }
 
+struct ZeroRegions {
+  static constexpr int kMax = 10;
+  uint8_t* p[kMax];
+  int64_t bytes[kMax];
+  int n;
+};
+__global__ void __launch_bounds__(256) zero_regions_kernel(ZeroRegions z) {
+  for (int r = 0; r < z.n; ++r) {
+    uint8_t* p = z.p[r];
+    const int64_t b = z.bytes[r];
+    const int64_t n16 = (reinterpret_cast<uintptr_t>(p) & 15) == 0 ? b >> 4 : 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n16;
+         i += (int64_t)gridDim.x * blockDim.x)
+      reinterpret_cast<uint4*>(p)[i] = make_uint4(0u, 0u, 0u, 0u);
+    for (int64_t i = n16 * 16 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < b;
+         i += (int64_t)gridDim.x * blockDim.x)
+      p[i] = 0;
+  }
+}
+
+int raster_zero_iteration(void* geom, int64_t n, const ss_camera* cam, const ss_raster_settings* s,
+                          void* bins, int64_t cap, void* extra, size_t extra_bytes,
+                          cudaStream_t st) {
+  const Geom g = plan_geom(geom, n, cam, s);
+  (void)bins, (void)cap;  // the bins are cleared by bin_pairs (see there)
+  ZeroRegions z{};
+  auto add = [&](void* p, int64_t bytes) {
+    if (p && bytes > 0) z.p[z.n] = static_cast<uint8_t*>(p), z.bytes[z.n++] = bytes;
+  };
+  const int64_t hist_bytes = (4 * 256 + 64) * sizeof(uint32_t);  // binsort_clear_bytes
+  add(g.dev_counts, 3 * sizeof(int64_t));
+  add(g.dsort.hist, hist_bytes);
+  add(g.dsort.status, (int64_t)g.dsort.max_passes * g.dsort.max_blocks * 256 * sizeof(uint32_t));
+  add(g.acc, n * kAccStride * (int64_t)sizeof(float));
+  add(g.touched, n);
+  add(extra, (int64_t)extra_bytes);
+  zero_regions_kernel<<<148 * 4, 256, 0, st>>>(z);
+  SS_CHECK_LAUNCH("zero_regions_kernel");
+  return SS_OK;
+}
+
 int raster_begin(const ss_cloud* cl, const ss_camera* cam, const ss_raster_settings* s,
                  void* geom, int64_t* counts_host, cudaStream_t st) {
   SS_TRY(check_raster(cl, cam, s));
   const int64_t n = cl->n;
   Geom g = plan_geom(geom, n, cam, s);
   const CamD cd = make_cam(cam);
-  SS_CUDA(cudaMemsetAsync(g.dev_counts, 0, 3 * sizeof(int64_t), st));
+  if (!t_prezeroed) SS_CUDA(cudaMemsetAsync(g.dev_counts, 0, 3 * sizeof(int64_t), st));
   if (n > 0) {
     SS_TRY(binsort_clear(g.dsort, 32, st));  // preprocess_kernel builds the histograms
     prof_begin(PH_PROJECT, st);
@@ -1718,8 +1762,10 @@ int raster_backward(const ss_cloud* cl, const ss_camera* cam, const ss_raster_se
   Bins b = plan_bins(bins, cap);
   const int ntx = ntiles_x(cam, s);
   const int64_t ntiles = (int64_t)ntx * ntiles_y(cam, s);
-  SS_CUDA(cudaMemsetAsync(g.acc, 0, n * kAccStride * sizeof(float), st));
-  SS_CUDA(cudaMemsetAsync(g.touched, 0, n, st));
+  if (!t_prezeroed) {
+    SS_CUDA(cudaMemsetAsync(g.acc, 0, n * kAccStride * sizeof(float), st));
+    SS_CUDA(cudaMemsetAsync(g.touched, 0, n, st));
+  }
   const BlendParams bp = blend_params(cam, s);
   if (total <= cap) {  // the forward's bins are still in the workspace
     prof_begin(PH_BLEND_BWD, st);

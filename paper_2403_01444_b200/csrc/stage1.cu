@@ -97,6 +97,10 @@ int ss_stage1_iter_begin(ss_stage1* st, const ss_camera* cam, int64_t* counts_ho
                          void* stream) {
   const NtcScratch ns = scratch_of(st);
   cudaStream_t s = as_stream(stream);
+  // every per-iteration scratch region zeroed by one kernel (common.cuh)
+  SS_TRY(raster_zero_iteration(st->geom, st->src.n, cam, &st->settings, st->bins,
+                               st->bin_capacity, st->loss_scratch, 2 * sizeof(double), s));
+  PrezeroScope scope(true);
   SS_TRY(ntc_forward_run(&st->grid, &st->mlp, st->n_in, st->src.means, st->rows, st->tables,
                          st->params, ns.X, ns.xs, ns.out7, 8, ns.relu, st->status, s));
   const bool perm = st->rows_index && st->rows_pos;
@@ -115,6 +119,9 @@ namespace ss {
 // views of a batch), plus the loss history and the view-space statistics.
 static int stage1_view(ss_stage1* st, const ss_camera* cam, const float* target, int64_t n_pairs,
                        float grad_scale, int accumulate, cudaStream_t s) {
+  // the view's scratch was zeroed with its raster_begin (ss_stage1_iter_begin,
+  // ss_stage1_batch_view)
+  PrezeroScope scope(true);
   // n_pairs above the workspace: the host-known count selects binning in bands
   // of tile rows (synchronous); otherwise the device count drives one band
   const int64_t cap = st->bin_capacity;
@@ -190,6 +197,9 @@ int ss_stage1_batch_view(ss_stage1* st, const ss_camera* cam, const float* targe
     SS_TRY(ss_stage1_iter_begin(st, cam, nullptr, stream));
   } else {  // the parameters have not moved: same transformed cloud
     const ss_cloud tc = transformed(st);
+    SS_TRY(raster_zero_iteration(st->geom, st->src.n, cam, &st->settings, st->bins,
+                                 st->bin_capacity, st->loss_scratch, 2 * sizeof(double), s));
+    PrezeroScope scope(true);
     SS_TRY(raster_begin(&tc, cam, &st->settings, st->geom, nullptr, s));
   }
   SS_TRY(stage1_view(st, cam, target, 0, grad_scale, first ? 0 : 1, s));
