@@ -689,6 +689,26 @@ __global__ void ranges_kernel(const int64_t* __restrict__ d_pairs, int64_t cap,
   }
 }
 
+struct ZeroRegions {
+  static constexpr int kMax = 10;
+  uint8_t* p[kMax];
+  int64_t bytes[kMax];
+  int n;
+};
+__global__ void __launch_bounds__(256) zero_regions_kernel(ZeroRegions z) {
+  for (int r = 0; r < z.n; ++r) {
+    uint8_t* p = z.p[r];
+    const int64_t b = z.bytes[r];
+    const int64_t n16 = (reinterpret_cast<uintptr_t>(p) & 15) == 0 ? b >> 4 : 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n16;
+         i += (int64_t)gridDim.x * blockDim.x)
+      reinterpret_cast<uint4*>(p)[i] = make_uint4(0u, 0u, 0u, 0u);
+    for (int64_t i = n16 * 16 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < b;
+         i += (int64_t)gridDim.x * blockDim.x)
+      p[i] = 0;
+  }
+}
+
 // Block -> tile map of the blends, heaviest tiles first (longest-processing-
 // time order): the per-tile work ranges over orders of magnitude, and in
 // index order the last wave's heavy tiles leave most SMs idle.  Tiles are
@@ -765,8 +785,17 @@ static int bin_pairs(const ss_camera* cam, const ss_raster_settings* s, int64_t 
   // the bin workspace can be replaced between raster_begin and here (the host
   // sizes it from the pair count), and bands reuse it: its clears always run
   PrezeroScope scope(false);
-  SS_CUDA(cudaMemsetAsync(g.ranges, 0, ntiles * sizeof(int2), st));
-  SS_TRY(binsort_clear(b.sort, kb, st));  // duplicate_kernel builds the sort's histograms
+  {  // ranges, the sort's histograms (duplicate_kernel fills them) and look-back
+     // words: one kernel instead of three memset nodes
+    ZeroRegions z{};
+    z.p[0] = reinterpret_cast<uint8_t*>(g.ranges), z.bytes[0] = ntiles * (int64_t)sizeof(int2);
+    z.p[1] = reinterpret_cast<uint8_t*>(b.sort.hist), z.bytes[1] = (4 * 256 + 64) * sizeof(uint32_t);
+    z.p[2] = reinterpret_cast<uint8_t*>(b.sort.status);
+    z.bytes[2] = (int64_t)binsort_passes(kb) * b.sort.max_blocks * 256 * sizeof(uint32_t);
+    z.n = 3;
+    zero_regions_kernel<<<148 * 4, 256, 0, st>>>(z);
+    SS_CHECK_LAUNCH("zero_regions_kernel");
+  }
   prof_begin(PH_DUPLICATE, st);
   const unsigned dgrid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(b.capacity, 1024),
                                                                          148 * 8));
@@ -1618,26 +1647,6 @@ static int launch_blend_bwd(int ts, int64_t ntiles, cudaStream_t st, const Blend
   }
   SS_CHECK_LAUNCH("blend_bwd_kernel");
   return SS_OK;
-}
-
-struct ZeroRegions {
-  static constexpr int kMax = 10;
-  uint8_t* p[kMax];
-  int64_t bytes[kMax];
-  int n;
-};
-__global__ void __launch_bounds__(256) zero_regions_kernel(ZeroRegions z) {
-  for (int r = 0; r < z.n; ++r) {
-    uint8_t* p = z.p[r];
-    const int64_t b = z.bytes[r];
-    const int64_t n16 = (reinterpret_cast<uintptr_t>(p) & 15) == 0 ? b >> 4 : 0;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n16;
-         i += (int64_t)gridDim.x * blockDim.x)
-      reinterpret_cast<uint4*>(p)[i] = make_uint4(0u, 0u, 0u, 0u);
-    for (int64_t i = n16 * 16 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < b;
-         i += (int64_t)gridDim.x * blockDim.x)
-      p[i] = 0;
-  }
 }
 
 int raster_zero_iteration(void* geom, int64_t n, const ss_camera* cam, const ss_raster_settings* s,
