@@ -5,7 +5,6 @@
 //
 // Reference: rasterizer.py:107-402, cameras.py:132-178, sh.py:51-81,
 // gaussians.py:120-154 (/root/reference/pkg/src/splatstream/).
-#include <cub/cub.cuh>
 #include <vector>
 
 #include "common.cuh"
@@ -42,8 +41,8 @@ struct Geom {
   int64_t* band_off;    // per rank, prefix of the pairs inside the current band of tile rows
   unsigned long long* row_pairs;  // per tile row: pairs of every visible rectangle
   BinSortWS dsort;      // depth sort workspace
-  void* cub_scan;
-  size_t cub_scan_bytes;
+  unsigned long long* scan_lb;  // single-pass offsets scan: look-back words per 256 ranks, then the ticket
+  int64_t scan_blocks;
   size_t total;
 };
 
@@ -65,6 +64,9 @@ static inline int key_bits(int64_t ntiles) {
   while ((int64_t(1) << b) < ntiles) ++b;
   return b;
 }
+
+constexpr int kScanThreads = 256;  // threads per block of the fused offsets scans
+constexpr int kScanRanks = 4;      // ranks per thread in rank_kernel
 
 static Geom plan_geom(void* base, int64_t n, const ss_camera* cam, const ss_raster_settings* s) {
   Geom g{};
@@ -100,11 +102,8 @@ static Geom plan_geom(void* base, int64_t n, const ss_camera* cam, const ss_rast
   g.band_off = c.take<int64_t>(nn + 1);
   g.row_pairs = c.take<unsigned long long>((size_t)ntiles_y(cam, s));
   g.dsort = binsort_plan(c, nn, 4);
-  size_t qb = 0;
-  cub::DeviceScan::InclusiveSum(nullptr, qb, (const int64_t*)nullptr, (int64_t*)nullptr,
-                                (int)nn);
-  g.cub_scan_bytes = qb;
-  g.cub_scan = c.take<char>(qb);
+  g.scan_blocks = (nn + kScanThreads - 1) / kScanThreads;  // band_counts: one rank per thread
+  g.scan_lb = c.take<unsigned long long>(g.scan_blocks + 1);
   g.total = c.bytes();
   return g;
 }
@@ -449,16 +448,84 @@ __global__ void __launch_bounds__(kTieThreads) depth_tie_kernel(Geom g) {
   }
 }
 
-// K4b/K4c: gather per-rank records, tile rectangle and its count
-__global__ void rank_kernel(CamD cam, ss_raster_settings s, int64_t n, Geom g) {
-  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (r >= n) return;
-  const int64_t V = g.dev_counts[0];
-  g.rank_of[g.order[r]] = (int32_t)r;
-  if (r >= V) {
-    g.offsets[r] = 0;
-    return;
+// ---- single-pass inclusive scan of per-rank int64 counts (offsets, band
+// offsets): the producer kernel's block takes a logical id from a ticket (its
+// predecessors are then running or done), scans its 256 counts, publishes the
+// aggregate and resolves its exclusive prefix by a warp-wide decoupled
+// look-back (32 predecessors per round trip).  Replaces a library scan (two
+// launches) after each producer.
+constexpr unsigned long long kLbAgg = 1ull << 62, kLbInc = 2ull << 62, kLbVal = (1ull << 62) - 1;
+
+__device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(v) : "l"(p));
+  return v;
+}
+
+__device__ __forceinline__ int64_t scan_logical_block(unsigned long long* lb, int64_t nb) {
+  __shared__ int64_t s_bid;
+  if (threadIdx.x == 0) s_bid = (int64_t)atomicAdd(lb + nb, 1ull);
+  __syncthreads();
+  return s_bid;
+}
+
+// inclusive prefix of v over all ranks before and including this thread's
+__device__ int64_t scan_inclusive(int64_t v, int64_t bid, unsigned long long* lb) {
+  __shared__ int64_t s_w[kScanThreads / 32];
+  __shared__ int64_t s_excl;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int64_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
   }
+  if (lane == 31) s_w[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    int64_t t = lane < kScanThreads / 32 ? s_w[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t y = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t += y;
+    }
+    if (lane < kScanThreads / 32) s_w[lane] = t;  // inclusive warp totals
+    const int64_t total = __shfl_sync(0xffffffffu, t, kScanThreads / 32 - 1);
+    int64_t excl = 0;
+    if (bid == 0) {
+      if (lane == 0) atomicExch(lb, kLbInc | (unsigned long long)total);
+    } else {
+      if (lane == 0) atomicExch(lb + bid, kLbAgg | (unsigned long long)total);
+      int64_t p = bid - 1;
+      while (true) {
+        const int64_t j = p - lane;
+        const unsigned long long w = j >= 0 ? ld_volatile_u64(lb + j) : kLbInc;
+        const uint32_t not_ready = __ballot_sync(0xffffffffu, (w & ~kLbVal) == 0);
+        const uint32_t inc = __ballot_sync(0xffffffffu, (w & kLbInc) != 0);
+        const int nr = not_ready ? __ffs(not_ready) - 1 : 32;
+        const int fi = inc ? __ffs(inc) - 1 : 32;
+        const int upto = fi < nr ? fi + 1 : nr;  // lanes [0, upto) are summed
+        int64_t val = lane < upto ? (int64_t)(w & kLbVal) : 0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) val += __shfl_xor_sync(0xffffffffu, val, o);
+        excl += val;
+        if (fi < nr) break;
+        p -= nr;  // re-poll from the first predecessor that has not published
+      }
+      if (lane == 0) atomicExch(lb + bid, kLbInc | (unsigned long long)(excl + total));
+    }
+    if (lane == 0) s_excl = excl;
+  }
+  __syncthreads();
+  return s_excl + (warp > 0 ? s_w[warp - 1] : 0) + x;
+}
+
+// K4b/K4c: gather per-rank records, tile rectangle and its count
+// (rank_count), then the inclusive scan of the counts into offsets[1..n]
+__device__ __forceinline__ int64_t rank_count(const CamD& cam, const ss_raster_settings& s,
+                                              int64_t r, int64_t V, Geom& g) {
+  g.rank_of[g.order[r]] = (int32_t)r;
+  if (r >= V) return 0;
   const int gid = g.order[r];
   const double2 m = g.g_mean[gid];
   const double4 co = g.g_conop[gid];
@@ -494,7 +561,34 @@ __global__ void rank_kernel(CamD cam, ss_raster_settings s, int64_t n, Geom g) {
     vis = true;
   }
   g.r_rect[r] = rect;
-  g.offsets[r] = vis ? (int64_t)(rect.y - rect.x + 1) * (rect.w - rect.z + 1) : 0;
+  return vis ? (int64_t)(rect.y - rect.x + 1) * (rect.w - rect.z + 1) : 0;
+}
+
+__global__ void __launch_bounds__(kScanThreads) rank_kernel(CamD cam, ss_raster_settings s,
+                                                             int64_t n, Geom g) {
+  // kScanRanks ranks per thread for the gathers (coalesced: rank base + k * 256 + tid),
+  // then each thread scans kScanRanks consecutive counts from shared memory
+  __shared__ int64_t s_cnt[kScanThreads * kScanRanks];
+  const int64_t bid = scan_logical_block(g.scan_lb, g.scan_blocks);
+  const int64_t base = bid * (kScanThreads * kScanRanks);
+  const int64_t V = g.dev_counts[0];
+#pragma unroll
+  for (int k = 0; k < kScanRanks; ++k) {
+    const int64_t r = base + k * kScanThreads + threadIdx.x;
+    s_cnt[k * kScanThreads + threadIdx.x] = r < n ? rank_count(cam, s, r, V, g) : 0;
+  }
+  __syncthreads();
+  int64_t c[kScanRanks], sum = 0;
+#pragma unroll
+  for (int k = 0; k < kScanRanks; ++k) c[k] = (sum += s_cnt[threadIdx.x * kScanRanks + k]);
+  const int64_t excl = scan_inclusive(sum, bid, g.scan_lb) - sum;
+  const int64_t r0 = base + threadIdx.x * kScanRanks;
+#pragma unroll
+  for (int k = 0; k < kScanRanks; ++k) {
+    if (r0 + k < n) g.offsets[r0 + k + 1] = excl + c[k];
+    if (r0 + k == n - 1) g.dev_counts[1] = excl + c[k];
+  }
+  if (bid == 0 && threadIdx.x == 0) g.offsets[0] = 0;
 }
 
 __global__ void finish_counts_kernel(Geom g, int64_t n) {
@@ -523,21 +617,21 @@ __global__ void row_pairs_kernel(int64_t n, Geom g, int nty) {
 }
 
 // pairs of each rank inside tile rows [ty_lo, ty_hi) (band_off[r], scanned later)
-__global__ void band_counts_kernel(int64_t n, Geom g, int ty_lo, int ty_hi) {
-  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (r >= n) return;
+// and their inclusive scan into band_off[1..n], the band's total in dev_counts[3]
+__global__ void __launch_bounds__(kScanThreads) band_counts_kernel(int64_t n, Geom g, int ty_lo,
+                                                                   int ty_hi) {
+  const int64_t bid = scan_logical_block(g.scan_lb, g.scan_blocks);
+  const int64_t r = bid * kScanThreads + threadIdx.x;
   int64_t c = 0;
-  if (r < g.dev_counts[0] && g.offsets[r + 1] > g.offsets[r]) {
+  if (r < n && r < g.dev_counts[0] && g.offsets[r + 1] > g.offsets[r]) {
     const int4 rc = g.r_rect[r];
     const int rows = min(rc.w, ty_hi - 1) - max(rc.z, ty_lo) + 1;
     c = rows > 0 ? (int64_t)(rc.y - rc.x + 1) * rows : 0;
   }
-  g.band_off[r] = c;
-}
-
-__global__ void band_finish_kernel(Geom g, int64_t n) {
-  g.band_off[0] = 0;
-  g.dev_counts[3] = n > 0 ? g.band_off[n] : 0;
+  const int64_t incl = scan_inclusive(c, bid, g.scan_lb);
+  if (r < n) g.band_off[r + 1] = incl;
+  if (r == 0) g.band_off[0] = 0;
+  if (r == n - 1) g.dev_counts[3] = incl;
 }
 
 // K4c (render path) tile cull:
@@ -856,13 +950,12 @@ static int plan_bands(const ss_camera* cam, const ss_raster_settings* s, int64_t
 // list the pairs of band [ty_lo, ty_hi) (band_off, dev_counts[3]) and bin them
 static int bin_band(const ss_camera* cam, const ss_raster_settings* s, int64_t n, Geom& g, Bins& b,
                     uint32_t* status, int cull, int2 band, cudaStream_t st) {
-  band_counts_kernel<<<(unsigned)cdiv(n, 256), 256, 0, st>>>(n, g, band.x, band.y);
-  SS_CHECK_LAUNCH("band_counts_kernel");
-  size_t qb = g.cub_scan_bytes;
-  SS_CUDA(cub::DeviceScan::InclusiveSum(g.cub_scan, qb, g.band_off, g.band_off + 1, (int)n, st));
-  g_launches.fetch_add(2);
-  band_finish_kernel<<<1, 1, 0, st>>>(g, n);
-  SS_CHECK_LAUNCH("band_finish_kernel");
+  SS_CUDA(cudaMemsetAsync(g.scan_lb, 0, (g.scan_blocks + 1) * sizeof(unsigned long long), st));
+  SS_CUDA(cudaMemsetAsync(g.dev_counts + 3, 0, sizeof(int64_t), st));
+  if (n > 0) {
+    band_counts_kernel<<<(unsigned)g.scan_blocks, kScanThreads, 0, st>>>(n, g, band.x, band.y);
+    SS_CHECK_LAUNCH("band_counts_kernel");
+  }
   return bin_pairs(cam, s, n, g, b, status, cull, st, g.band_off, g.dev_counts + 3, band.x);
 }
 
@@ -1662,6 +1755,7 @@ int raster_zero_iteration(void* geom, int64_t n, const ss_camera* cam, const ss_
   add(g.dev_counts, 3 * sizeof(int64_t));
   add(g.dsort.hist, hist_bytes);
   add(g.dsort.status, (int64_t)g.dsort.max_passes * g.dsort.max_blocks * 256 * sizeof(uint32_t));
+  add(g.scan_lb, (g.scan_blocks + 1) * (int64_t)sizeof(unsigned long long));
   add(g.acc, n * kAccStride * (int64_t)sizeof(float));
   add(g.touched, n);
   add(extra, (int64_t)extra_bytes);
@@ -1700,15 +1794,15 @@ int raster_begin(const ss_cloud* cl, const ss_camera* cam, const ss_raster_setti
     SS_CHECK_LAUNCH("depth_tie_kernel");
     prof_end(PH_DEPTH_SORT, st);
     prof_begin(PH_RANK_SCAN, st);
-    rank_kernel<<<(unsigned)cdiv(n, 256), 256, 0, st>>>(cd, *s, n, g);
+    if (!t_prezeroed)
+      SS_CUDA(cudaMemsetAsync(g.scan_lb, 0, (g.scan_blocks + 1) * sizeof(unsigned long long), st));
+    rank_kernel<<<(unsigned)cdiv(n, kScanThreads * kScanRanks), kScanThreads, 0, st>>>(cd, *s, n, g);
     SS_CHECK_LAUNCH("rank_kernel");
-    size_t qb = g.cub_scan_bytes;
-    SS_CUDA(cub::DeviceScan::InclusiveSum(g.cub_scan, qb, g.offsets, g.offsets + 1, (int)n, st));
-    g_launches.fetch_add(2);
+    prof_end(PH_RANK_SCAN, st);
+  } else {
+    finish_counts_kernel<<<1, 1, 0, st>>>(g, n);
+    SS_CHECK_LAUNCH("finish_counts_kernel");
   }
-  finish_counts_kernel<<<1, 1, 0, st>>>(g, n);
-  SS_CHECK_LAUNCH("finish_counts_kernel");
-  if (n > 0) prof_end(PH_RANK_SCAN, st);
   if (counts_host)
     SS_CUDA(cudaMemcpyAsync(counts_host, g.dev_counts, 2 * sizeof(int64_t),
                             cudaMemcpyDeviceToHost, st));
@@ -1835,13 +1929,14 @@ int tile_bin_begin(int64_t n, const double* mean2d, const double* cov2d, const d
   if (n > 0) {
     tile_bin_setup_kernel<<<(unsigned)cdiv(n, 256), 256, 0, st>>>(n, mean2d, cov2d, opacity, g);
     SS_CHECK_LAUNCH("tile_bin_setup_kernel");
-    rank_kernel<<<(unsigned)cdiv(n, 256), 256, 0, st>>>(make_cam(cam), *s, n, g);
+    SS_CUDA(cudaMemsetAsync(g.scan_lb, 0, (g.scan_blocks + 1) * sizeof(unsigned long long), st));
+    rank_kernel<<<(unsigned)cdiv(n, kScanThreads * kScanRanks), kScanThreads, 0, st>>>(make_cam(cam),
+                                                                                   *s, n, g);
     SS_CHECK_LAUNCH("rank_kernel");
-    size_t qb = g.cub_scan_bytes;
-    SS_CUDA(cub::DeviceScan::InclusiveSum(g.cub_scan, qb, g.offsets, g.offsets + 1, (int)n, st));
+  } else {
+    finish_counts_kernel<<<1, 1, 0, st>>>(g, n);
+    SS_CHECK_LAUNCH("finish_counts_kernel");
   }
-  finish_counts_kernel<<<1, 1, 0, st>>>(g, n);
-  SS_CHECK_LAUNCH("finish_counts_kernel");
   if (counts_host)
     SS_CUDA(cudaMemcpyAsync(counts_host, g.dev_counts, 2 * sizeof(int64_t),
                             cudaMemcpyDeviceToHost, st));

