@@ -7,8 +7,8 @@
 //
 // Per 8-bit digit pass ("onesweep"): a CTA of 256 threads takes a logical
 // tile id from an atomic ticket (so every predecessor is already running),
-// ranks its 4096 keys stably with warp match + per-warp digit counters (warp
-// w owns items [512 w, 512 w + 512) of the tile, in index order), publishes
+// ranks its tile of 256 x STEPS keys stably with warp match + per-warp digit
+// counters (warp w owns the w-th eighth of the tile, in index order), publishes
 // its per-digit counts and resolves its global offsets by decoupled look-back
 // over the predecessors, stages the tile in shared memory in sorted order and
 // writes it out in coalesced runs.  One histogram kernel serves all passes.
@@ -22,12 +22,12 @@ namespace {
 constexpr int kBsThreads = 256;
 constexpr int kBsWarps = kBsThreads / 32;
 #ifndef SS_BS_STEPS_BIG
-#define SS_BS_STEPS_BIG 8
+#define SS_BS_STEPS_BIG 12
 #endif
 #ifndef SS_BS_WIN
 #define SS_BS_WIN 8
 #endif
-constexpr int kBsStepsBig = SS_BS_STEPS_BIG;  // items per lane (2048-item tiles)
+constexpr int kBsStepsBig = SS_BS_STEPS_BIG;  // items per lane (3072-item tiles: 8 / 12 / 16 measured 96 / 90 / 95 us on 3.3M tile pairs)
 #ifndef SS_BS_STEPS_SMALL
 #define SS_BS_STEPS_SMALL 8
 #endif
