@@ -121,7 +121,10 @@ __device__ inline void band_vals(float x, float y, float z, float* v) {
 #pragma unroll
   for (int m = 0; m < B; ++m) v[m] = b[off + m];
 }
-__device__ __constant__ int c_perm[3] = {1, 2, 0};  // (y, z, x) basis order, sh.py:30-32
+// (y, z, x) basis order of band 1, sh.py:30-32; constexpr so the unrolled
+// loops index R / g_R with constants (a __constant__ table made every access
+// a select chain over the nine registers)
+__device__ __forceinline__ constexpr int c_perm(int a) { return a == 0 ? 1 : (a == 1 ? 2 : 0); }
 
 // One colour channel of bands l >= 2 (4 lanes per Gaussian, see
 // transform_kernel): out = S^{-1} y with y_k = f(R^T d_k), f the band-l SH
@@ -455,7 +458,7 @@ __global__ void __launch_bounds__(128) transform_kernel(ss_cloud src, int64_t n,
     for (int a = 0; a < 3; ++a) {
       float sum = 0.f;
 #pragma unroll
-      for (int b = 0; b < 3; ++b) sum = fmaf(R[c_perm[a]][c_perm[b]], in[b], sum);
+      for (int b = 0; b < 3; ++b) sum = fmaf(R[c_perm(a)][c_perm(b)], in[b], sum);
       tsh[(1 + a) * 3] = sum;
     }
   }
@@ -565,7 +568,7 @@ __global__ void __launch_bounds__(128) transform_vjp_kernel(
         for (int a = 0; a < 3; ++a)
 #pragma unroll
           for (int b = 0; b < 3; ++b)
-            gR[c_perm[a]][c_perm[b]] = fmaf(g[c][a], in[c][b], gR[c_perm[a]][c_perm[b]]);
+            gR[c_perm(a)][c_perm(b)] = fmaf(g[c][a], in[c][b], gR[c_perm(a)][c_perm(b)]);
     }
     if (DEG >= 2) {
       float in[3][5], g[3][5];
