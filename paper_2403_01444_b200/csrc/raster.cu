@@ -522,13 +522,30 @@ __device__ int64_t scan_inclusive(int64_t v, int64_t bid, unsigned long long* lb
 
 // K4b/K4c: gather per-rank records, tile rectangle and its count
 // (rank_count), then the inclusive scan of the counts into offsets[1..n]
+// The per-Gaussian inputs of a rank (gathered by id in depth order)
+struct RankIn {
+  int gid;
+  double2 m, cv;
+  double4 co;
+  float4 gc;
+};
+__device__ __forceinline__ void rank_load(const Geom& g, int64_t r, int64_t n, int64_t V,
+                                          RankIn& in) {
+  in.gid = r < n ? g.order[r] : 0;
+  if (r < V) {
+    in.m = g.g_mean[in.gid];
+    in.co = g.g_conop[in.gid];
+    in.gc = g.g_color[in.gid];
+    in.cv = g.g_cov[in.gid];
+  }
+}
 __device__ __forceinline__ int64_t rank_count(const CamD& cam, const ss_raster_settings& s,
-                                              int64_t r, int64_t V, Geom& g) {
-  g.rank_of[g.order[r]] = (int32_t)r;
+                                              int64_t r, int64_t V, Geom& g, const RankIn& in) {
+  g.rank_of[in.gid] = (int32_t)r;
   if (r >= V) return 0;
-  const int gid = g.order[r];
-  const double2 m = g.g_mean[gid];
-  const double4 co = g.g_conop[gid];
+  const int gid = in.gid;
+  const double2 m = in.m;
+  const double4 co = in.co;
   g.r_mean[r] = m;
   g.r_conop_d[r] = co;
   g.r_conop[r] = make_float4((float)co.x, (float)co.y, (float)co.z, (float)co.w);
@@ -537,7 +554,7 @@ __device__ __forceinline__ int64_t rank_count(const CamD& cam, const ss_raster_s
   constexpr double kq = -0.72134752044448170368;  // -0.5 log2(e)
   const double qthr = s.skip_alpha > 0.0 ? log2(s.skip_alpha * (1.0 - 2e-4) / co.w) : -1e30;
   g.r_q[r] = make_float4((float)(kq * co.x), (float)(kq * co.y), (float)(kq * co.z), (float)qthr);
-  const float4 gc = g.g_color[gid];
+  const float4 gc = in.gc;
   g.r_color[r] = make_float4(gc.x, gc.y, gc.z, (float)co.w);  // w: opacity
   const int ts = s.tile_size;
   const int ntx = (cam.W + ts - 1) / ts, nty = (cam.H + ts - 1) / ts;
@@ -546,7 +563,7 @@ __device__ __forceinline__ int64_t rank_count(const CamD& cam, const ss_raster_s
   if (s.skip_alpha > 0.0) {  // rasterizer.py:132-148
     const double ratio = fmax(co.w / s.skip_alpha, 1.0);
     const double r2 = sqrt(fmax(9.0, 2.0 * log(ratio)));
-    const double2 cv = g.g_cov[gid];
+    const double2 cv = in.cv;
     const double hx = r2 * sqrt(fmax(cv.x, 0.0));
     const double hy = r2 * sqrt(fmax(cv.y, 0.0));
     const double xl = m.x - hx, xh = m.x + hx, yl = m.y - hy, yh = m.y + hy;
@@ -572,10 +589,15 @@ __global__ void __launch_bounds__(kScanThreads) rank_kernel(CamD cam, ss_raster_
   const int64_t bid = scan_logical_block(g.scan_lb, g.scan_blocks);
   const int64_t base = bid * (kScanThreads * kScanRanks);
   const int64_t V = g.dev_counts[0];
+  // every rank's gathers in flight before any store (the Geom pointers may alias)
+  RankIn in[kScanRanks];
+#pragma unroll
+  for (int k = 0; k < kScanRanks; ++k)
+    rank_load(g, base + k * kScanThreads + threadIdx.x, n, V, in[k]);
 #pragma unroll
   for (int k = 0; k < kScanRanks; ++k) {
     const int64_t r = base + k * kScanThreads + threadIdx.x;
-    s_cnt[k * kScanThreads + threadIdx.x] = r < n ? rank_count(cam, s, r, V, g) : 0;
+    s_cnt[k * kScanThreads + threadIdx.x] = r < n ? rank_count(cam, s, r, V, g, in[k]) : 0;
   }
   __syncthreads();
   int64_t c[kScanRanks], sum = 0;
