@@ -233,18 +233,42 @@ __device__ inline void project_one(const CamD& cam, const ss_cloud& cl, int64_t 
 }
 
 // K4a: per-Gaussian projection; depth key (+inf when culled)
-template <int DEG>
 #ifndef SS_PP_BLOCKS
 #define SS_PP_BLOCKS 4  // 64 registers: 4 CTAs per SM (measured 36 -> 34 us)
 #endif
 #ifndef SS_GB_BLOCKS
 #define SS_GB_BLOCKS 4
 #endif
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                   (uint32_t)__cvta_generic_to_shared(smem)),
+               "l"(gmem)
+               : "memory");
+}
+
+// Degree 3: the block's 256 SH rows (48 KB, contiguous) are copied into shared
+// memory with cp.async at the start, so their latency hides under the fp64
+// projection instead of stalling the colour evaluation after it.
+constexpr int kPpPrefetchBytes = 256 * 48 * 4;
+template <int DEG>
 __global__ void __launch_bounds__(256, SS_PP_BLOCKS) preprocess_kernel(CamD cam, ss_cloud cl, Geom g) {
+  constexpr int K = (DEG + 1) * (DEG + 1), RW = 3 * K;
+  constexpr bool PF = DEG == 3;
+  extern __shared__ __align__(16) float s_pf[];  // PF: [256][RW]
   __shared__ uint32_t s_hist[4][256];  // the depth sort's digit histograms
+  const int64_t row0 = blockIdx.x * (int64_t)blockDim.x;
+  const bool pf = PF && (reinterpret_cast<uintptr_t>(cl.sh) & 15) == 0;  // grid-uniform
+  if (pf) {
+    const int nv = (int)(min((int64_t)blockDim.x, cl.n - row0) * RW / 4);
+    const float4* src = reinterpret_cast<const float4*>(cl.sh + row0 * RW);
+    for (int v = threadIdx.x; v < nv; v += blockDim.x) cp_async16(s_pf + 4 * v, src + v);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
   for (int k = threadIdx.x; k < 1024; k += blockDim.x) (&s_hist[0][0])[k] = 0;
   __syncthreads();
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t i = row0 + threadIdx.x;
+  bool vis = false;
+  Projected P;
   if (i < cl.n) {
     if (i == 0) g.dev_counts[2] = cl.n;
     g.order[i] = (int32_t)i;  // sort input (4 passes: the input sits in the output buffers)
@@ -266,22 +290,43 @@ __global__ void __launch_bounds__(256, SS_PP_BLOCKS) preprocess_kernel(CamD cam,
       // depths up to ties, which depth_tie_kernel resolves
       key = __float_as_uint((float)z);
       atomicAdd(reinterpret_cast<unsigned long long*>(&g.dev_counts[0]), 1ull);
-      Projected P;
-      project_one<DEG>(cam, cl, i, P);
-      g.g_mean[i] = make_double2(P.mean[0], P.mean[1]);
-      g.g_conop[i] =
-          make_double4(P.conic[0][0], P.conic[0][1] + P.conic[1][0], P.conic[1][1], P.op);
-      // w: the unclipped-channel mask of clip(0.5 + SH, 0, 1) (sh.py:51-59) for the backward
-      const int clip_mask = (P.raw[0] > 0.0 && P.raw[0] < 1.0) |
-                            (P.raw[1] > 0.0 && P.raw[1] < 1.0) << 1 |
-                            (P.raw[2] > 0.0 && P.raw[2] < 1.0) << 2;
-      g.g_color[i] = make_float4((float)fmin(fmax(P.raw[0], 0.0), 1.0),
-                                 (float)fmin(fmax(P.raw[1], 0.0), 1.0),
-                                 (float)fmin(fmax(P.raw[2], 0.0), 1.0), (float)clip_mask);
-      g.g_cov[i] = make_double2(P.cov2d[0][0], P.cov2d[1][1]);
+      if (pf) project_geom(cam, cl, i, P);
+      else project_one<DEG>(cam, cl, i, P);
+      vis = true;
     }
     g.key32[i] = key;
     bs_hist_add(s_hist, key, 32);
+  }
+  if (pf) {
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+    if (vis) {  // the colour from the staged row, the same operation order as project_one
+      double basis[K];
+      sh_basis<double>(DEG, P.dir[0], P.dir[1], P.dir[2], basis);
+      double raw[3] = {0.5, 0.5, 0.5};
+      const float4* row = reinterpret_cast<const float4*>(s_pf + threadIdx.x * RW);
+#pragma unroll
+      for (int j = 0; j < RW / 4; ++j) {
+        const float4 v = row[j];
+        const float e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int t = 0; t < 4; ++t) raw[(4 * j + t) % 3] += basis[(4 * j + t) / 3] * (double)e[t];
+      }
+      for (int c = 0; c < 3; ++c) P.raw[c] = raw[c];
+    }
+  }
+  if (vis) {
+    g.g_mean[i] = make_double2(P.mean[0], P.mean[1]);
+    g.g_conop[i] =
+        make_double4(P.conic[0][0], P.conic[0][1] + P.conic[1][0], P.conic[1][1], P.op);
+    // w: the unclipped-channel mask of clip(0.5 + SH, 0, 1) (sh.py:51-59) for the backward
+    const int clip_mask = (P.raw[0] > 0.0 && P.raw[0] < 1.0) |
+                          (P.raw[1] > 0.0 && P.raw[1] < 1.0) << 1 |
+                          (P.raw[2] > 0.0 && P.raw[2] < 1.0) << 2;
+    g.g_color[i] = make_float4((float)fmin(fmax(P.raw[0], 0.0), 1.0),
+                               (float)fmin(fmax(P.raw[1], 0.0), 1.0),
+                               (float)fmin(fmax(P.raw[2], 0.0), 1.0), (float)clip_mask);
+    g.g_cov[i] = make_double2(P.cov2d[0][0], P.cov2d[1][1]);
   }
   __syncthreads();
   bs_hist_flush(s_hist, g.dsort.hist, 32);
@@ -1535,6 +1580,20 @@ __global__ void __launch_bounds__(128, SS_GB_BLOCKS) gaussian_bwd_kernel(CamD ca
     if (full && out.d_opacity_logits) out.d_opacity_logits[gid] = 0.f;
     return;
   }
+  // degree 3: this Gaussian's 48 SH coefficients copied into shared memory
+  // now (cp.async, no registers), consumed after the accumulator loads and
+  // the anchor algebra instead of stalling the colour backward
+  __shared__ __align__(16) float s_sh[K == 16 ? 128 * 48 : 1];
+  const bool pf = K == 16 && blockDim.x <= 128 &&
+                  ((reinterpret_cast<uintptr_t>(cl.sh) | reinterpret_cast<uintptr_t>(out.d_sh)) &
+                   15) == 0;
+  float* my_sh = s_sh + (K == 16 ? threadIdx.x * 48 : 0);
+  if (pf) {
+#pragma unroll
+    for (int j = 0; j < 12; ++j)
+      cp_async16(my_sh + 4 * j, reinterpret_cast<const float4*>(cl.sh + gid * 48) + j);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
   const float4 a0 = *reinterpret_cast<const float4*>(g.acc + (int64_t)r * kAccStride);
   const float4 a1 = *reinterpret_cast<const float4*>(g.acc + (int64_t)r * kAccStride + 4);
   const float a8 = g.acc[(int64_t)r * kAccStride + 8];
@@ -1581,13 +1640,13 @@ __global__ void __launch_bounds__(128, SS_GB_BLOCKS) gaussian_bwd_kernel(CamD ca
     sh_basis<float>(DEG, fdir[0], fdir[1], fdir[2], basis);
     const float* sh = cl.sh + gid * 3 * K;
     float* dsh = out.d_sh ? out.d_sh + gid * 3 * K : nullptr;
-    if (K == 16 && ((reinterpret_cast<uintptr_t>(cl.sh) | reinterpret_cast<uintptr_t>(out.d_sh)) &
-                    15) == 0) {  // degree 3: the 48 coefficients as 12 float4 loads / stores
+    if (pf) {  // degree 3: the 48 staged coefficients as 12 float4 / 12 float4 stores
+      asm volatile("cp.async.wait_all;" ::: "memory");
 #pragma unroll
       for (int k = 0; k < K; ++k) gbasis[k] = 0.f;
 #pragma unroll
       for (int j = 0; j < 12; ++j) {
-        const float4 v = __ldg(reinterpret_cast<const float4*>(sh) + j);
+        const float4 v = reinterpret_cast<const float4*>(my_sh)[j];
         const float e[4] = {v.x, v.y, v.z, v.w};
         float o[4];
 #pragma unroll
@@ -1802,7 +1861,17 @@ int raster_begin(const ss_cloud* cl, const ss_camera* cam, const ss_raster_setti
         case 1: preprocess_kernel<0><<<grid, 256, 0, st>>>(cd, *cl, g); break;
         case 4: preprocess_kernel<1><<<grid, 256, 0, st>>>(cd, *cl, g); break;
         case 9: preprocess_kernel<2><<<grid, 256, 0, st>>>(cd, *cl, g); break;
-        default: preprocess_kernel<3><<<grid, 256, 0, st>>>(cd, *cl, g); break;
+        default: {
+          static bool attr = false;  // 48 KB dynamic + the static histograms
+          if (!attr) {
+            SS_CUDA(cudaFuncSetAttribute(preprocess_kernel<3>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         kPpPrefetchBytes));
+            attr = true;
+          }
+          preprocess_kernel<3><<<grid, 256, kPpPrefetchBytes, st>>>(cd, *cl, g);
+          break;
+        }
       }
     }
     SS_CHECK_LAUNCH("preprocess_kernel");
