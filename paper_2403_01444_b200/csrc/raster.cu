@@ -838,15 +838,40 @@ __global__ void __launch_bounds__(256) duplicate_kernel(int ntx, int64_t n, Geom
   bs_hist_flush(s_hist, b.sort.hist, key_bits);
 }
 
+// Per-tile [start, end) of the sorted keys: four keys per thread (one 16-byte
+// load), the neighbours across threads by warp shuffles (only the warp's end
+// lanes read past their own keys)
 __global__ void ranges_kernel(const int64_t* __restrict__ d_pairs, int64_t cap,
                               const uint32_t* __restrict__ keys, int2* ranges, uint32_t ntiles) {
   const int64_t pairs = min(*d_pairs, cap);
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < pairs;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t k = keys[i];
-    if (k >= ntiles) continue;  // culled pairs (sentinel key) sort past the last tile
-    if (i == 0 || keys[i - 1] != k) ranges[k].x = (int)i;
-    if (i == pairs - 1 || keys[i + 1] != k) ranges[k].y = (int)(i + 1);
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x * 4;
+  for (int64_t i0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x - lane) * 4; i0 < pairs;
+       i0 += stride) {  // warp-uniform: i0 = the warp's first key
+    const int64_t i = i0 + 4 * lane;
+    uint32_t k[4];
+    if (i + 3 < pairs) {  // keys is 16-byte aligned (Carve), i a multiple of 4
+      const uint4 v = *reinterpret_cast<const uint4*>(keys + i);
+      k[0] = v.x, k[1] = v.y, k[2] = v.z, k[3] = v.w;
+    } else {
+#pragma unroll
+      for (int t = 0; t < 4; ++t) k[t] = i + t < pairs ? keys[i + t] : 0xffffffffu;
+    }
+    uint32_t prev = __shfl_up_sync(0xffffffffu, k[3], 1);
+    uint32_t next = __shfl_down_sync(0xffffffffu, k[0], 1);
+    if (lane == 0) prev = i > 0 && i - 1 < pairs ? keys[i - 1] : 0xffffffffu;
+    if (lane == 31) next = i + 4 < pairs ? keys[i + 4] : 0xffffffffu;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int64_t e = i + t;
+      if (e >= pairs) break;
+      const uint32_t kk = k[t];
+      if (kk >= ntiles) continue;  // culled pairs (sentinel key) sort past the last tile
+      const uint32_t kp = t == 0 ? prev : k[t - 1];
+      const uint32_t kn = t == 3 ? next : k[t + 1];
+      if (e == 0 || kp != kk) ranges[kk].x = (int)e;
+      if (e == pairs - 1 || kn != kk) ranges[kk].y = (int)(e + 1);
+    }
   }
 }
 
