@@ -135,6 +135,33 @@ def test_tile_bin_matches_reference_lists(P):
     np.testing.assert_array_equal(np.array([t[:4] for t in tiles]).reshape(-1, 4), d["tile_rects"])
 
 
+@pytest.mark.parametrize("n,ts", [(120_001, 16), (50_003, 8)])
+def test_tile_bin_large_random_vs_oracle(P, n, ts):
+    """Tile binning of many projected splats against the oracle, bit-exact:
+    the rank kernel's single-pass scan across hundreds of look-back blocks,
+    runs of zero-pair (off-screen) ranks, a few screen-filling splats, pair
+    counts that are not multiples of the ranges kernel's four keys per thread
+    (rasterizer.py:107-175)."""
+    rng = np.random.default_rng(n)
+    W, H = 333, 250
+    mean2d = np.stack([rng.uniform(-80, W + 80, n), rng.uniform(-80, H + 80, n)], 1)
+    sx, sy = rng.uniform(0.3, 12.0, n), rng.uniform(0.3, 12.0, n)
+    sx[:5] = sy[:5] = 400.0  # screen-filling
+    rho = rng.uniform(-0.6, 0.6, n) * sx * sy
+    cov2d = np.zeros((n, 2, 2))
+    cov2d[:, 0, 0], cov2d[:, 1, 1] = sx * sx, sy * sy
+    cov2d[:, 0, 1] = cov2d[:, 1, 0] = rho
+    opacity = rng.uniform(0.01, 0.99, n)
+    skip = 1.0 / 255.0
+    tiles = P["rasterizer"].tile_bin(mean2d, cov2d, opacity, W, H, ts, skip)
+    ref = O.tile_lists(mean2d, cov2d, opacity, W, H, ts, skip)
+    assert len(tiles) == len(ref)
+    np.testing.assert_array_equal(np.array([t[:4] for t in tiles]),
+                                  np.array([t[:4] for t in ref]))
+    np.testing.assert_array_equal(np.concatenate([t[4] for t in tiles]),
+                                  np.concatenate([t[4] for t in ref]))
+
+
 def test_render_loss_golden(P):
     d = G.load("loss")
     loss, grad = P["losses"].render_loss(d["x"], d["y"])
