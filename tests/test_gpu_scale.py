@@ -13,7 +13,8 @@ the power to catch that class of bug:
   * image (max-abs <= 1e-4) and every render gradient (norm-relative <= 1e-3)
     on two 32-row bands, the camera's principal point shifted as bench.py's
     CPU sample does (rasterizer.py:214-402);
-  * one full Stage-1 step at cfg1 on a band (pipeline.py:263-277).
+  * one full Stage-1 step at cfg1 on a band, and one on the full 1352x1014
+    view against the all-core oracle port (pipeline.py:263-277).
 """
 
 import numpy as np
@@ -153,6 +154,55 @@ def test_stage1_step_cfg1_band(P):
     state = dict(grid=sc.grid, tables=tables.copy(), mlp=mlp,
                  inside=O.inside_mask(sc.grid, sc.cloud["means"]), enc=None)
     ref = O.stage1_iteration(state, sc.cloud, cam, target, apply_adam=False)
+    assert np.abs(tr.rendered_image(0) - ref["image"]).max() <= IMG_TOL
+    assert abs(tr.last_loss() - ref["loss"]) <= 1e-5 * ref["loss"]
+    gt, gw, gb = tr.ntc_grads()
+    assert G.norm_rel(gt, ref["g_tables"]) <= GRAD_TOL
+    for i in range(3):
+        assert G.norm_rel(gw[i], ref["g_w"][i]) <= GRAD_TOL, i
+        assert G.norm_rel(gb[i], ref["g_b"][i]) <= GRAD_TOL, i
+
+
+def test_stage1_step_cfg1_full_height(P):
+    """One FULL-HEIGHT Stage-1 iteration of the cfg1 workload (250k SH-3
+    Gaussians, 1352x1014, the view bench.py's CPU sample times) against the
+    float64 oracle port on every host core (oracle/parallel.py, itself pinned
+    to the serial oracle by test_oracle_parallel.py): image, loss and the NTC
+    gradients after the whole chain apply_ntc -> render -> loss -> backward ->
+    apply_ntc_backward (pipeline.py:263-277).  fp32 cache (the reference's
+    arithmetic); random-initialised NTC so every gradient is live."""
+    import os
+
+    from threadpoolctl import threadpool_limits
+
+    from oracle import parallel
+    from paper_2403_01444_b200.stage1 import Stage1Config, Stage1Trainer
+
+    sc = scene(P, 1)
+    scenes = P["scenes"]
+    cam = sc.cameras[0]
+    tables, mlp = O.init_ntc(sc.grid, output_init="random", seed=4)
+    tables = scenes.f32(np.random.default_rng(6).uniform(-0.02, 0.02, size=tables.shape))
+    moved = scenes.moved_cloud(sc.cloud, np.random.default_rng(7), axis=(0.3, 1.0, 0.2),
+                               deg=1.5, shift=(0.01, -0.005, 0.008))
+    state = dict(grid=sc.grid, tables=tables.copy(), mlp=mlp,
+                 inside=O.inside_mask(sc.grid, sc.cloud["means"]), enc=None)
+    state["enc"] = O.encode(sc.grid, sc.cloud["means"][state["inside"]])
+    ps = parallel.ParallelStage1(os.cpu_count() or 1)
+    with threadpool_limits(1):
+        target = ps.render(moved, cam)
+        ref = ps.iteration(state, sc.cloud, cam, target, apply_adam=False)
+
+    class Cache:
+        grid = P["types"].HashGridConfig.from_any(sc.grid)
+
+    c = Cache()
+    c.tables, c.weights, c.biases = tables, mlp["weights"], mlp["biases"]
+    tr = Stage1Trainer(sc.cloud, c, [(cam, target.astype(np.float32))],
+                       Stage1Config(stage1_iterations=1))
+    pairs = tr.begin(0)
+    tr.finish(0, pairs, adam=False)
+    assert tr.check_status() == 0
     assert np.abs(tr.rendered_image(0) - ref["image"]).max() <= IMG_TOL
     assert abs(tr.last_loss() - ref["loss"]) <= 1e-5 * ref["loss"]
     gt, gw, gb = tr.ntc_grads()
