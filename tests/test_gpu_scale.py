@@ -163,14 +163,16 @@ def test_stage1_step_cfg1_band(P):
         assert G.norm_rel(gb[i], ref["g_b"][i]) <= GRAD_TOL, i
 
 
-def test_stage1_step_cfg1_full_height(P):
+@pytest.mark.parametrize("mlp_dtype", ["f32", "f16"])
+def test_stage1_step_cfg1_full_height(P, mlp_dtype):
     """One FULL-HEIGHT Stage-1 iteration of the cfg1 workload (250k SH-3
     Gaussians, 1352x1014, the view bench.py's CPU sample times) against the
     float64 oracle port on every host core (oracle/parallel.py, itself pinned
     to the serial oracle by test_oracle_parallel.py): image, loss and the NTC
     gradients after the whole chain apply_ntc -> render -> loss -> backward ->
     apply_ntc_backward (pipeline.py:263-277).  fp32 cache (the reference's
-    arithmetic); random-initialised NTC so every gradient is live."""
+    arithmetic) and the fp16-weight decoder BASELINE configs[1] specifies (the
+    oracle's f16 restatement); random-initialised NTC so every gradient is live."""
     import os
 
     from threadpoolctl import threadpool_limits
@@ -185,7 +187,7 @@ def test_stage1_step_cfg1_full_height(P):
     tables = scenes.f32(np.random.default_rng(6).uniform(-0.02, 0.02, size=tables.shape))
     moved = scenes.moved_cloud(sc.cloud, np.random.default_rng(7), axis=(0.3, 1.0, 0.2),
                                deg=1.5, shift=(0.01, -0.005, 0.008))
-    state = dict(grid=sc.grid, tables=tables.copy(), mlp=mlp,
+    state = dict(grid=sc.grid, tables=tables.copy(), mlp=dict(mlp, dtype=mlp_dtype),
                  inside=O.inside_mask(sc.grid, sc.cloud["means"]), enc=None)
     state["enc"] = O.encode(sc.grid, sc.cloud["means"][state["inside"]])
     ps = parallel.ParallelStage1(os.cpu_count() or 1)
@@ -199,7 +201,8 @@ def test_stage1_step_cfg1_full_height(P):
     c = Cache()
     c.tables, c.weights, c.biases = tables, mlp["weights"], mlp["biases"]
     tr = Stage1Trainer(sc.cloud, c, [(cam, target.astype(np.float32))],
-                       Stage1Config(stage1_iterations=1))
+                       Stage1Config(stage1_iterations=1, mlp_dtype=mlp_dtype))
+    assert tr.mlp.precision == (1 if mlp_dtype == "f16" else 0)
     pairs = tr.begin(0)
     tr.finish(0, pairs, adam=False)
     assert tr.check_status() == 0
