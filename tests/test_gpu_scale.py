@@ -14,7 +14,8 @@ the power to catch that class of bug:
     on two 32-row bands, the camera's principal point shifted as bench.py's
     CPU sample does (rasterizer.py:214-402);
   * one full Stage-1 step at cfg1 on a band, and one on the full 1352x1014
-    view against the all-core oracle port (pipeline.py:263-277).
+    view against the all-core oracle port (pipeline.py:263-277);
+  * a full cfg2 frame through the benchmarked render path.
 """
 
 import numpy as np
@@ -213,3 +214,42 @@ def test_stage1_step_cfg1_full_height(P, mlp_dtype):
     for i in range(3):
         assert G.norm_rel(gw[i], ref["g_w"][i]) <= GRAD_TOL, i
         assert G.norm_rel(gb[i], ref["g_b"][i]) <= GRAD_TOL, i
+
+
+@pytest.mark.parametrize("mlp_dtype", ["f32", "f16"])
+def test_render_cfg2_full_frame(P, mlp_dtype):
+    """The render FPS workload (config 2: NTC transform + rasterize_forward of
+    300k SH-3 Gaussians at 1352x1014, the graph-replayed ss_stage1_render path
+    bench.py times) on a full frame against the all-core float64 oracle port
+    (transform.py:53-96 -> rasterizer.py:214-281); random-initialised NTC."""
+    import os
+
+    from threadpoolctl import threadpool_limits
+
+    from oracle import parallel
+    from paper_2403_01444_b200.stage1 import Stage1Config, Stage1Trainer
+
+    sc = scene(P, 2)
+    scenes = P["scenes"]
+    cam = sc.cameras[3]
+    tables, mlp = O.init_ntc(sc.grid, output_init="random", seed=9)
+    tables = scenes.f32(np.random.default_rng(10).uniform(-0.02, 0.02, size=tables.shape))
+    state = dict(grid=sc.grid, tables=tables.copy(), mlp=dict(mlp, dtype=mlp_dtype),
+                 inside=O.inside_mask(sc.grid, sc.cloud["means"]), enc=None)
+    state["enc"] = O.encode(sc.grid, sc.cloud["means"][state["inside"]])
+    ps = parallel.ParallelStage1(os.cpu_count() or 1)
+    with threadpool_limits(1):
+        ref = ps.transform_render(state, sc.cloud, cam)
+
+    class Cache:
+        grid = P["types"].HashGridConfig.from_any(sc.grid)
+
+    c = Cache()
+    c.tables, c.weights, c.biases = tables, mlp["weights"], mlp["biases"]
+    tr = Stage1Trainer(sc.cloud, c, [(cam, np.zeros_like(ref, dtype=np.float32))],
+                       Stage1Config(mlp_dtype=mlp_dtype))
+    tr.render_async(0)  # captured
+    tr.render_async(0)  # replayed
+    P["torch"].cuda.synchronize()
+    assert tr.check_status() == 0
+    assert np.abs(tr.rendered_image(0) - ref).max() <= IMG_TOL
