@@ -15,7 +15,8 @@ the power to catch that class of bug:
     CPU sample does (rasterizer.py:214-402);
   * one full Stage-1 step at cfg1 on a band, and one on the full 1352x1014
     view against the all-core oracle port (pipeline.py:263-277);
-  * a full cfg2 frame through the benchmarked render path.
+  * a full cfg2 frame through the benchmarked render path;
+  * config 3's batched 4-view step at 1M Gaussians (view bands).
 """
 
 import numpy as np
@@ -253,3 +254,63 @@ def test_render_cfg2_full_frame(P, mlp_dtype):
     P["torch"].cuda.synchronize()
     assert tr.check_status() == 0
     assert np.abs(tr.rendered_image(0) - ref).max() <= IMG_TOL
+
+
+def test_batched_step_cfg3_bands(P):
+    """Config 3's batched step at its own scale (1M SH-3 Gaussians, four of its
+    hemisphere cameras, each on a 32-row band): ViewShardedStage1 accumulates
+    the 1/B-scaled gradients of the four views and takes one lazy Adam step;
+    the oracle takes the mean of the per-view reference gradients
+    (transform.py:99-135 -> ntc.py:250-288) and one Adam step (optim.py:33-66),
+    on every host core (oracle/parallel.py)."""
+    import os
+
+    from threadpoolctl import threadpool_limits
+
+    from oracle import parallel
+    from paper_2403_01444_b200.device import unpack_params
+    from paper_2403_01444_b200.dist import ViewShardedStage1
+    from paper_2403_01444_b200.stage1 import Stage1Config
+
+    torch = P["torch"]
+    sc = scene(P, 3)
+    scenes = P["scenes"]
+    cams = [band(sc.cameras[v], y0) for v, y0 in ((0, 500), (11, 300), (23, 700), (40, 100))]
+    tables, mlp = O.init_ntc(sc.grid, output_init="random", seed=12)
+    tables = scenes.f32(np.random.default_rng(13).uniform(-0.02, 0.02, size=tables.shape))
+    moved = scenes.moved_cloud(sc.cloud, np.random.default_rng(7), axis=(0.3, 1.0, 0.2),
+                               deg=1.5, shift=(0.01, -0.005, 0.008))
+    st = dict(grid=sc.grid, tables=tables.copy(),
+              mlp=dict(weights=[w.copy() for w in mlp["weights"]],
+                       biases=[b.copy() for b in mlp["biases"]]),
+              inside=O.inside_mask(sc.grid, sc.cloud["means"]), enc=None)
+    st["enc"] = O.encode(sc.grid, sc.cloud["means"][st["inside"]])
+    ps = parallel.ParallelStage1(os.cpu_count() or 1)
+    with threadpool_limits(1):
+        targets = [ps.render(moved, c) for c in cams]
+        rs = [ps.iteration(st, sc.cloud, c, t, apply_adam=False) for c, t in zip(cams, targets)]
+
+    class Cache:
+        grid = P["types"].HashGridConfig.from_any(sc.grid)
+
+    c = Cache()
+    c.tables, c.weights, c.biases = tables.copy(), mlp["weights"], mlp["biases"]
+    vs = ViewShardedStage1(sc.cloud, c, [(cm, t.astype(np.float32)) for cm, t in zip(cams, targets)],
+                           Stage1Config(stage1_iterations=1), views_per_iteration=4)
+    vs.step([0, 1, 2, 3])
+    torch.cuda.synchronize()
+    assert vs.trainer.check_status() == 0
+    b = len(rs)
+    O.adam_apply(st, sum(r["g_tables"] for r in rs) / b,
+                 [sum(r["g_w"][i] for r in rs) / b for i in range(3)],
+                 [sum(r["g_b"][i] for r in rs) / b for i in range(3)], 0.002)
+    tab = vs.trainer.tables.view(st["tables"].shape).cpu().numpy()
+    assert G.norm_rel(tab - tables, st["tables"] - tables) <= 1e-3
+    ws, bs = unpack_params(vs.trainer.params.cpu().numpy(), vs.trainer.w_shapes,
+                           vs.trainer.layout)
+    for i in range(3):
+        assert G.norm_rel(ws[i] - mlp["weights"][i],
+                          st["mlp"]["weights"][i] - mlp["weights"][i]) <= 1e-3, i
+        assert G.norm_rel(bs[i] - mlp["biases"][i],
+                          st["mlp"]["biases"][i] - mlp["biases"][i]) <= 1e-3, i
+    np.testing.assert_allclose(vs.batch_losses()[0], np.mean([r["loss"] for r in rs]), rtol=1e-5)
