@@ -10,10 +10,10 @@ from launch_table import table  # noqa: E402
 
 PHASE = [("gather_kernel", "gather"), ("mlp_fwd_tc_kernel", "decoder_forward"),
          ("transform_kernel", "transform"), ("preprocess_kernel", "project"),
-         ("bs_pass_kernel<4>", "depth_sort"), ("depth_tie_kernel", "depth_sort"),
-         ("rank_kernel", "rank_scan"), ("DeviceScan", "rank_scan"), ("finish_counts", "rank_scan"),
-         ("duplicate_kernel", "duplicate"), ("bs_pass_kernel<8>", "tile_sort"),
-         ("ranges_kernel", "ranges"), ("blend_fwd_kernel", "blend_forward"),
+         ("bs_pass_kernel<8>", "depth_sort"), ("depth_tie_kernel", "depth_sort"),
+         ("rank_kernel", "rank_scan"),
+         ("duplicate_kernel", "duplicate"), ("bs_pass_kernel<12>", "tile_sort"),
+         ("ranges_kernel", "ranges"), ("tile_order_kernel", "ranges"), ("blend_fwd_kernel", "blend_forward"),
          ("ssim_map_kernel", "ssim_map"), ("ssim_grad_kernel", "ssim_grad"),
          ("blend_bwd_kernel", "blend_backward"), ("gaussian_bwd_kernel", "gaussian_backward"),
          ("transform_vjp_kernel", "transform_vjp"), ("mlp_bwd_tc_kernel", "decoder_backward"),
