@@ -1287,7 +1287,7 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_fwd_kernel(
           C[p][0] = fmaf(wgt, col.x, C[p][0]);
           C[p][1] = fmaf(wgt, col.y, C[p][1]);
           C[p][2] = fmaf(wgt, col.z, C[p][2]);
-          T[p] *= 1.f - a;
+          T[p] = fmaf(-a, T[p], T[p]);  // T (1 - a) in one rounding
           last[p] = a > 0.f ? b - range.x + k + 1 : last[p];
         }
         continue;
