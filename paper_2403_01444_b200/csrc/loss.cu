@@ -51,8 +51,9 @@ __global__ void __launch_bounds__(SW * 3, 5) ssim_map_kernel(LossParams lp,
   // per input column of a row: x, y, x^2 + y^2, xy (shifted; SSIM needs only
   // the sum of the two variances), formed once per element instead of once per
   // tap; two row buffers per channel
-  constexpr int NS = 4;
-  __shared__ float sv[3][2][NS][RW];
+  // one float4 per column (x, y, x^2 + y^2, xy): a tap is one 16-byte shared
+  // load feeding two packed FMAs (FFMA2, sm_100), bit-identical to four FFMAs
+  __shared__ float4 sv[3][2][RW];
   const int lane = threadIdx.x, c = threadIdx.y;
   const int C = lp.C;
   if (c >= C) return;  // warp-uniform; no block-level synchronisation below
@@ -91,20 +92,17 @@ __global__ void __launch_bounds__(SW * 3, 5) ssim_map_kernel(LossParams lp,
       const int e = lane + m * SW;
       if (e < RW) {
         const float xv = fx[m] - shx, yv = fy[m] - shy;
-        float* d = &sv[c][buf][0][e];
-        d[0] = xv;
-        d[RW] = yv;
-        d[2 * RW] = fmaf(xv, xv, yv * yv);
-        d[3 * RW] = xv * yv;
+        sv[c][buf][e] = make_float4(xv, yv, fmaf(xv, xv, yv * yv), xv * yv);
       }
     }
   };
-  float ax[WIN], ay[WIN], as[WIN], axy[WIN];
+  // vertical accumulators as packed pairs: (x, y) and (x^2 + y^2, xy)
+  float2 axy2[WIN], asx[WIN];
 #pragma unroll
-  for (int j = 0; j < WIN; ++j) ax[j] = ay[j] = as[j] = axy[j] = 0.f;
-  float g[WIN];
+  for (int j = 0; j < WIN; ++j) axy2[j] = asx[j] = make_float2(0.f, 0.f);
+  float2 g[WIN];
 #pragma unroll
-  for (int k = 0; k < WIN; ++k) g[k] = lp.gf[k];
+  for (int k = 0; k < WIN; ++k) g[k] = make_float2(lp.gf[k], lp.gf[k]);
   double ssum = 0.0;
   const float c1f = (float)lp.c1, c2f = (float)lp.c2;
   const int64_t plane = (int64_t)lp.Hv * lp.Wv;
@@ -122,23 +120,23 @@ __global__ void __launch_bounds__(SW * 3, 5) ssim_map_kernel(LossParams lp,
       fetch(yi + 3, fx, fy);
     }
     // horizontal sums of row yi at column xcol
-    float h[NS] = {0.f, 0.f, 0.f, 0.f};
-    const float(*row)[RW] = sv[c][cur];
+    float2 h01 = make_float2(0.f, 0.f), h23 = make_float2(0.f, 0.f);
+    const float4* row = sv[c][cur];
 #pragma unroll
-    for (int k = 0; k < WIN; ++k)
-#pragma unroll
-      for (int q = 0; q < NS; ++q) h[q] = fmaf(g[k], row[q][lane + k], h[q]);
+    for (int k = 0; k < WIN; ++k) {
+      const float4 v = row[lane + k];
+      h01 = __ffma2_rn(g[k], make_float2(v.x, v.y), h01);
+      h23 = __ffma2_rn(g[k], make_float2(v.z, v.w), h23);
+    }
     // output row yi - 10 completes with tap 10; the others shift down one row
-    const float mx0 = fmaf(g[HALO], h[0], ax[0]), my0 = fmaf(g[HALO], h[1], ay[0]);
-    const float ss = fmaf(g[HALO], h[2], as[0]), sxy = fmaf(g[HALO], h[3], axy[0]);
+    const float2 m01 = __ffma2_rn(g[HALO], h01, axy2[0]), s01 = __ffma2_rn(g[HALO], h23, asx[0]);
+    const float mx0 = m01.x, my0 = m01.y, ss = s01.x, sxy = s01.y;
 #pragma unroll
     for (int j = 0; j < HALO; ++j) {
-      ax[j] = fmaf(g[HALO - 1 - j], h[0], ax[j + 1]);
-      ay[j] = fmaf(g[HALO - 1 - j], h[1], ay[j + 1]);
-      as[j] = fmaf(g[HALO - 1 - j], h[2], as[j + 1]);
-      axy[j] = fmaf(g[HALO - 1 - j], h[3], axy[j + 1]);
+      axy2[j] = __ffma2_rn(g[HALO - 1 - j], h01, axy2[j + 1]);
+      asx[j] = __ffma2_rn(g[HALO - 1 - j], h23, asx[j + 1]);
     }
-    ax[HALO] = ay[HALO] = as[HALO] = axy[HALO] = 0.f;
+    axy2[HALO] = asx[HALO] = make_float2(0.f, 0.f);
     const int o = yi - HALO;
     if (o >= oy0 && col_ok) {
       // per-window algebra in fp32 (the maps are stored in fp32 anyway); the
@@ -179,7 +177,7 @@ __global__ void __launch_bounds__(SW * 3, 5) ssim_grad_kernel(LossParams lp,
                                                            float* __restrict__ grad,
                                                            double* __restrict__ sums) {
   constexpr int RW = SW + HALO;
-  __shared__ float sm[3][2][3][RW + 1];  // [channel][buffer][map][column]
+  __shared__ float4 sm[3][2][RW];  // [channel][buffer][column] = (map 0, map 1, map 2, -)
   const int lane = threadIdx.x, c = threadIdx.y;
   const int C = lp.C;
   if (c >= C) return;  // warp-uniform; warp-level synchronisation only
@@ -188,8 +186,9 @@ __global__ void __launch_bounds__(SW * 3, 5) ssim_grad_kernel(LossParams lp,
   const int ry0 = max(oy0 - HALO, 0), ry1 = min(oy1, lp.Hv);  // map rows that contribute
   const int64_t plane = (int64_t)lp.Hv * lp.Wv;
   float g[WIN];
+  float2 g2[WIN];  // packed copies for FFMA2 (maps 0 and 1 as one pair)
 #pragma unroll
-  for (int k = 0; k < WIN; ++k) g[k] = lp.gf[k];
+  for (int k = 0; k < WIN; ++k) g[k] = lp.gf[k], g2[k] = make_float2(g[k], g[k]);
   // prefetch: lane loads map q of channel c at columns x0 - 10 + lane (+32)
   constexpr int PER = 2;
   float pm[3][PER], qm[3][PER];  // map rows in flight
@@ -212,14 +211,13 @@ __global__ void __launch_bounds__(SW * 3, 5) ssim_grad_kernel(LossParams lp,
   };
   auto stage = [&](int buf, const float (&fm)[3][PER]) {
 #pragma unroll
-    for (int q = 0; q < 3; ++q)
-#pragma unroll
-      for (int m = 0; m < PER; ++m)
-        if (lane + m * SW < RW) sm[c][buf][q][lane + m * SW] = fm[q][m];
+    for (int m = 0; m < PER; ++m)
+      if (lane + m * SW < RW) sm[c][buf][lane + m * SW] = make_float4(fm[0][m], fm[1][m], fm[2][m], 0.f);
   };
-  float a0[WIN], a1[WIN], a2[WIN];
+  float2 a01[WIN];  // maps 0 and 1, packed
+  float a2[WIN];
 #pragma unroll
-  for (int j = 0; j < WIN; ++j) a0[j] = a1[j] = a2[j] = 0.f;
+  for (int j = 0; j < WIN; ++j) a01[j] = make_float2(0.f, 0.f), a2[j] = 0.f;
   double l1 = 0.0;
   // register buffers P / Q alternate (no moves): at step r the one passed in
   // holds map row r + 1 and the image / target of output row r + 1; it is
@@ -240,24 +238,24 @@ __global__ void __launch_bounds__(SW * 3, 5) ssim_grad_kernel(LossParams lp,
       fetch(r + 3, fm, fi, ft);
     }
     // horizontal full convolution at output column px_: map cols px_ - j
-    float h0 = 0.f, h1 = 0.f, h2 = 0.f;
+    float2 h01 = make_float2(0.f, 0.f);
+    float h2 = 0.f;
 #pragma unroll
     for (int j = 0; j < WIN; ++j) {
-      const int e = lane + HALO - j;
-      h0 = fmaf(g[j], sm[c][cur][0][e], h0);
-      h1 = fmaf(g[j], sm[c][cur][1][e], h1);
-      h2 = fmaf(g[j], sm[c][cur][2][e], h2);
+      const float4 v = sm[c][cur][lane + HALO - j];
+      h01 = __ffma2_rn(g2[j], make_float2(v.x, v.y), h01);
+      h2 = fmaf(g[j], v.z, h2);
     }
     // output row r completes with tap 0; rows r + 1 .. r + 10 shift down
-    const float b0 = fmaf(g[0], h0, a0[0]), b1 = fmaf(g[0], h1, a1[0]),
-                b2 = fmaf(g[0], h2, a2[0]);
+    const float2 b01 = __ffma2_rn(g2[0], h01, a01[0]);
+    const float b0 = b01.x, b1 = b01.y, b2 = fmaf(g[0], h2, a2[0]);
 #pragma unroll
     for (int i = 0; i < HALO; ++i) {
-      a0[i] = fmaf(g[i + 1], h0, a0[i + 1]);
-      a1[i] = fmaf(g[i + 1], h1, a1[i + 1]);
+      a01[i] = __ffma2_rn(g2[i + 1], h01, a01[i + 1]);
       a2[i] = fmaf(g[i + 1], h2, a2[i + 1]);
     }
-    a0[HALO] = a1[HALO] = a2[HALO] = 0.f;
+    a01[HALO] = make_float2(0.f, 0.f);
+    a2[HALO] = 0.f;
     if (r >= oy0 && col_ok) {
       const int64_t o = ((int64_t)r * lp.W + px_) * C + c;
       const float d = xr - tr;
