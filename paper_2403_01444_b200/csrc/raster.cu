@@ -1150,6 +1150,26 @@ struct PixelOffsets {
     const float t2 = fmaf(Q.z, dy[p], L.z);
     return fmaf(t2, dy[p], fmaf(t1, dx[p], L.x));
   }
+  // every pixel's lg, two pixels per packed FMA (FFMA2 with the splat's
+  // coefficients as broadcast scalars): the same five roundings per pixel
+  __device__ __forceinline__ void lg_all(const float4& L, const float4& Q, float (&out)[PPT]) const {
+    if constexpr (PPT % 2 == 0) {
+      const float2 qx = make_float2(Q.x, Q.x), qy = make_float2(Q.y, Q.y), qz = make_float2(Q.z, Q.z);
+      const float2 lx = make_float2(L.x, L.x), ly = make_float2(L.y, L.y), lz = make_float2(L.z, L.z);
+#pragma unroll
+      for (int p = 0; p < PPT; p += 2) {
+        const float2 ddx = make_float2(dx[p], dx[p + 1]), ddy = make_float2(dy[p], dy[p + 1]);
+        const float2 t1 = __ffma2_rn(qy, ddy, __ffma2_rn(qx, ddx, ly));
+        const float2 t2 = __ffma2_rn(qz, ddy, lz);
+        const float2 r = __ffma2_rn(t2, ddy, __ffma2_rn(t1, ddx, lx));
+        out[p] = r.x;
+        out[p + 1] = r.y;
+      }
+    } else {
+#pragma unroll
+      for (int p = 0; p < PPT; ++p) out[p] = lg(L, Q, p);
+    }
+  }
 };
 
 __device__ __noinline__ float alpha_f64(const BlendParams& bp, const Geom& g, int rank, float px,
@@ -1257,9 +1277,9 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_fwd_kernel(
         const float qlo = L.w, qhi = Q.w;
         float lgs[PPT];
         bool live[PPT], any_live = false, any_near = false;
+        po.lg_all(L, Q, lgs);
 #pragma unroll
         for (int p = 0; p < PPT; ++p) {
-          lgs[p] = po.lg(L, Q, p);
           live[p] = T[p] >= bp.stop && !(lgs[p] < qlo);
           any_live |= live[p];
           any_near |= live[p] && lgs[p] < qhi;
@@ -1372,6 +1392,10 @@ __global__ void __launch_bounds__(BlendShape<TS, true>::NT) blend_bwd_kernel(
   // a thread's pixels share their column when the tile width divides the
   // warp's 32-pixel rows (tile_pixel): the dx moments then follow from M0, M1y
   constexpr bool DXC = TS <= 32;
+#ifndef SS_BWD_PAIRS
+#define SS_BWD_PAIRS 1
+#endif
+  constexpr bool PAIRS = SS_BWD_PAIRS && DXC && PPT % 2 == 0;
   __shared__ SplatRec s_sp[NT];
   // each warp owns a slot per splat (plain stores, summed at the flush);
   // larger tiles share one slot through shared-memory atomics
@@ -1419,6 +1443,20 @@ __global__ void __launch_bounds__(BlendShape<TS, true>::NT) blend_bwd_kernel(
   atomicMax(&s_last, max_last);
   __syncthreads();
   const int end0 = range.x + s_last;  // positions past every pixel's last contributor are dead
+  // pixel pairs as packed registers for the FFMA2 path
+  float2 T2[PAIRS ? PPT / 2 : 1], S2[PAIRS ? PPT / 2 : 1], G0[PAIRS ? PPT / 2 : 1],
+      G1[PAIRS ? PPT / 2 : 1], G2[PAIRS ? PPT / 2 : 1], DY[PAIRS ? PPT / 2 : 1];
+  if constexpr (PAIRS) {
+#pragma unroll
+    for (int q = 0; q < PPT / 2; ++q) {
+      T2[q] = make_float2(T[2 * q], T[2 * q + 1]);
+      S2[q] = make_float2(S[2 * q], S[2 * q + 1]);
+      G0[q] = make_float2(gp[2 * q][0], gp[2 * q + 1][0]);
+      G1[q] = make_float2(gp[2 * q][1], gp[2 * q + 1][1]);
+      G2[q] = make_float2(gp[2 * q][2], gp[2 * q + 1][2]);
+      DY[q] = make_float2(po.dy[2 * q], po.dy[2 * q + 1]);
+    }
+  }
   for (int end = end0; end > range.x; end -= NT) {
     const int start = max(range.x, end - NT);
     const int cnt = end - start;
@@ -1433,9 +1471,9 @@ __global__ void __launch_bounds__(BlendShape<TS, true>::NT) blend_bwd_kernel(
       // predicated (a = 0 makes every update a no-op) instead of branching
       float lgs[PPT];
       bool live[PPT], any_live = false, any_near = false;
+      po.lg_all(L, Q, lgs);  // same decisions as the forward
 #pragma unroll
       for (int p = 0; p < PPT; ++p) {
-        lgs[p] = po.lg(L, Q, p);  // same decisions as the forward
         live[p] = pos_rel < last[p] && !(lgs[p] < qlo);
         any_live |= live[p];
         any_near |= live[p] && lgs[p] < qhi;
@@ -1460,6 +1498,44 @@ __global__ void __launch_bounds__(BlendShape<TS, true>::NT) blend_bwd_kernel(
       }
       float v[NA] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
       bool any = false;
+      if constexpr (PAIRS) {
+        // the same per-pixel roundings, two pixels per packed instruction
+        // (FFMA2 / FMUL2, the splat's values as broadcast scalars); the
+        // accumulators keep one partial per pixel of a pair
+        const float2 cx = make_float2(col.x, col.x), cy = make_float2(col.y, col.y),
+                     cz = make_float2(col.z, col.z);
+        const float2 one = make_float2(1.f, 1.f), mone = make_float2(-1.f, -1.f);
+        float2 c0 = make_float2(0.f, 0.f), c1 = c0, c2 = c0, m1 = c0, m2 = c0, m0 = c0;
+#pragma unroll
+        for (int q = 0; q < PPT / 2; ++q) {
+          const float2 a = make_float2(av[2 * q], av[2 * q + 1]);
+          const float2 om = __ffma2_rn(a, mone, one);  // 1 - a, one rounding
+          const float2 ioma = make_float2(rcp_approx(om.x), rcp_approx(om.y));
+          const float2 tb = __fmul2_rn(T2[q], ioma);
+          const float2 w = __fmul2_rn(a, tb);
+          c0 = __ffma2_rn(w, G0[q], c0);
+          c1 = __ffma2_rn(w, G1[q], c1);
+          c2 = __ffma2_rn(w, G2[q], c2);
+          const float2 u = __ffma2_rn(G2[q], cz, __ffma2_rn(G1[q], cy, __fmul2_rn(G0[q], cx)));
+          const float2 da = __fmul2_rn(__ffma2_rn(u, T2[q], make_float2(-S2[q].x, -S2[q].y)), ioma);
+          S2[q] = __ffma2_rn(u, w, S2[q]);
+          T2[q] = tb;
+          const float2 dmr = __fmul2_rn(make_float2(og[2 * q], og[2 * q + 1]), da);
+          const float2 dm = make_float2(og[2 * q] < bp.clamp ? dmr.x : 0.f,
+                                        og[2 * q + 1] < bp.clamp ? dmr.y : 0.f);
+          const float2 f = __fmul2_rn(dm, DY[q]);
+          m1 = __fadd2_rn(m1, f);
+          m2 = __ffma2_rn(f, DY[q], m2);
+          m0 = __fadd2_rn(m0, dm);
+          any |= a.x > 0.f || a.y > 0.f;
+        }
+        v[0] = c0.x + c0.y;
+        v[1] = c1.x + c1.y;
+        v[2] = c2.x + c2.y;
+        v[4] = m1.x + m1.y;
+        v[7] = m2.x + m2.y;
+        v[8] = m0.x + m0.y;
+      } else {
 #pragma unroll
       for (int p = 0; p < PPT; ++p) {
         const float a = av[p];
@@ -1493,6 +1569,7 @@ __global__ void __launch_bounds__(BlendShape<TS, true>::NT) blend_bwd_kernel(
         }
         v[8] += dm;
         any |= a > 0.f;
+      }
       }
       if (DXC) {  // M1x = dx M0, M2xx = dx M1x, M2xy = dx M1y
         const float dx = po.dx[0];
