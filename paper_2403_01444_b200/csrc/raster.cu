@@ -1230,7 +1230,11 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_fwd_kernel(
   const int2 range = g.ranges[tile];
   PixelOffsets<TS, PPT> po;
   po.init(threadIdx.x);
-  float T[PPT], C[PPT][3];
+  // per-pixel transmittance and colour as register pairs (pixels 2q, 2q + 1),
+  // so the update below runs two pixels per packed FMA
+  float2 TT[(PPT + 1) / 2], CC[3][(PPT + 1) / 2];
+  auto Tr = [&](int p) -> float& { return (p & 1) ? TT[p >> 1].y : TT[p >> 1].x; };
+  auto Cr = [&](int p, int c) -> float& { return (p & 1) ? CC[c][p >> 1].y : CC[c][p >> 1].x; };
   double Td[TOUCH ? PPT : 1], Cd[TOUCH ? PPT : 1][3];
   int last[PPT];
   bool done[PPT];
@@ -1240,8 +1244,10 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_fwd_kernel(
     const int li = tile_pixel<TS, PPT>(threadIdx.x, p);
     px[p] = (float)(x0 + li % TS);
     py[p] = (float)(y0 + li / TS);
-    T[p] = 1.f;
-    C[p][0] = C[p][1] = C[p][2] = 0.f;
+    Tr(p) = 1.f;
+    Cr(p, 0) = 0.f;
+    Cr(p, 1) = 0.f;
+    Cr(p, 2) = 0.f;
     if (TOUCH) {
       Td[p] = 1.0;
       Cd[p][0] = Cd[p][1] = Cd[p][2] = 0.0;
@@ -1250,12 +1256,12 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_fwd_kernel(
     done[p] = (x0 + li % TS >= bp.W) || (y0 + li / TS >= bp.H);
     // fast path: "done" is T < stop itself (later splats fail T_before >= stop);
     // pixels outside the image start at T = 0 and are never written
-    if (!TOUCH && done[p]) T[p] = 0.f;
+    if (!TOUCH && done[p]) Tr(p) = 0.f;
   }
   for (int b = range.x; b < range.y; b += NT) {
     bool all_done = true;
 #pragma unroll
-    for (int p = 0; p < PPT; ++p) all_done &= TOUCH ? done[p] : !(T[p] >= bp.stop);
+    for (int p = 0; p < PPT; ++p) all_done &= TOUCH ? done[p] : !(Tr(p) >= bp.stop);
     if (__syncthreads_count(all_done) == NT) break;
     const int j = b + threadIdx.x;
     if (j < range.y) {
@@ -1280,14 +1286,14 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_fwd_kernel(
         po.lg_all(L, Q, lgs);
 #pragma unroll
         for (int p = 0; p < PPT; ++p) {
-          live[p] = T[p] >= bp.stop && !(lgs[p] < qlo);
+          live[p] = Tr(p) >= bp.stop && !(lgs[p] < qlo);
           any_live |= live[p];
           any_near |= live[p] && lgs[p] < qhi;
         }
         if (!__any_sync(0xffffffffu, any_live)) {  // warp-uniform skip
           bool alive = false;
 #pragma unroll
-          for (int p = 0; p < PPT; ++p) alive |= T[p] >= bp.stop;
+          for (int p = 0; p < PPT; ++p) alive |= Tr(p) >= bp.stop;
           if (!__any_sync(0xffffffffu, alive)) break;  // this warp's pixels are all finished
           continue;
         }
@@ -1300,15 +1306,29 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_fwd_kernel(
           for (int p = 0; p < PPT; ++p)
             if (live[p] && lgs[p] < qhi) av[p] = alpha_f64(bp, g, s_sp[k].rank, px[p], py[p]);
         }
+        if constexpr (PPT % 2 == 0) {  // two pixels per packed FMA, the same roundings
+#pragma unroll
+          for (int q = 0; q < PPT / 2; ++q) {
+            const float2 a = make_float2(av[2 * q], av[2 * q + 1]);
+            const float2 wgt = __fmul2_rn(a, TT[q]);
+            CC[0][q] = __ffma2_rn(wgt, make_float2(col.x, col.x), CC[0][q]);
+            CC[1][q] = __ffma2_rn(wgt, make_float2(col.y, col.y), CC[1][q]);
+            CC[2][q] = __ffma2_rn(wgt, make_float2(col.z, col.z), CC[2][q]);
+            TT[q] = __ffma2_rn(make_float2(-a.x, -a.y), TT[q], TT[q]);  // T (1 - a) in one rounding
+            last[2 * q] = a.x > 0.f ? b - range.x + k + 1 : last[2 * q];
+            last[2 * q + 1] = a.y > 0.f ? b - range.x + k + 1 : last[2 * q + 1];
+          }
+        } else {
 #pragma unroll
         for (int p = 0; p < PPT; ++p) {  // predicated: a = 0 leaves the pixel unchanged
           const float a = av[p];
-          const float wgt = a * T[p];
-          C[p][0] = fmaf(wgt, col.x, C[p][0]);
-          C[p][1] = fmaf(wgt, col.y, C[p][1]);
-          C[p][2] = fmaf(wgt, col.z, C[p][2]);
-          T[p] = fmaf(-a, T[p], T[p]);  // T (1 - a) in one rounding
+          const float wgt = a * Tr(p);
+          Cr(p, 0) = fmaf(wgt, col.x, Cr(p, 0));
+          Cr(p, 1) = fmaf(wgt, col.y, Cr(p, 1));
+          Cr(p, 2) = fmaf(wgt, col.z, Cr(p, 2));
+          Tr(p) = fmaf(-a, Tr(p), Tr(p));  // T (1 - a) in one rounding
           last[p] = a > 0.f ? b - range.x + k + 1 : last[p];
+        }
         }
         continue;
       }
@@ -1352,18 +1372,18 @@ __global__ void __launch_bounds__(BlendShape<TS>::NT) blend_fwd_kernel(
     if (pxi >= bp.W || pyi >= bp.H) continue;
     const int64_t pix = (int64_t)pyi * bp.W + pxi;
     if (TOUCH) {
-      T[p] = (float)Td[p];
+      Tr(p) = (float)Td[p];
       image[3 * pix + 0] = (float)(Cd[p][0] + Td[p] * (double)bp.bg[0]);
       image[3 * pix + 1] = (float)(Cd[p][1] + Td[p] * (double)bp.bg[1]);
       image[3 * pix + 2] = (float)(Cd[p][2] + Td[p] * (double)bp.bg[2]);
       if (alpha_map) alpha_map[pix] = (float)(1.0 - Td[p]);
     } else {
-      image[3 * pix + 0] = C[p][0] + T[p] * bp.bg[0];
-      image[3 * pix + 1] = C[p][1] + T[p] * bp.bg[1];
-      image[3 * pix + 2] = C[p][2] + T[p] * bp.bg[2];
-      if (alpha_map) alpha_map[pix] = 1.f - T[p];
+      image[3 * pix + 0] = Cr(p, 0) + Tr(p) * bp.bg[0];
+      image[3 * pix + 1] = Cr(p, 1) + Tr(p) * bp.bg[1];
+      image[3 * pix + 2] = Cr(p, 2) + Tr(p) * bp.bg[2];
+      if (alpha_map) alpha_map[pix] = 1.f - Tr(p);
     }
-    g.t_final[pix] = T[p];
+    g.t_final[pix] = Tr(p);
     g.n_contrib[pix] = last[p];
   }
 }
